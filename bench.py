@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the embedding lookup+update hot path (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+One step = one batch of the config's synthetic workload through the embedding worker:
+register (route, probe / lazy init, per-row apply order), pull (gather + fp64
+pooling) and push (validation + fp64 fan-out + ordered fused Adagrad update), i.e.
+SURVEY.md §8(d). The table is pre-warmed (every row of the 100M-row table exists,
+M = 0 lazy inits in the timed region). Inputs rotate over --batches distinct
+batches whose per-step footprint (rows RMW + grads + pooled > 400 MB) is larger
+than L2, so no L2 flush is needed between steps.
+
+Rank 0 prints ONE JSON line. --impl reference times the reference's own CPU path
+(oracle/_ref/libhps_ref.so, the reference headers compiled unmodified) on the
+box's host cores on bounded samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    p.add_argument("--batches", type=int, default=8, help="distinct batches cycled")
+    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--soak-seconds", type=float, default=2.0)
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def nproc():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi samples every 200 ms while the timed region (+ soak) runs."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+        return self.summary()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() in ("active", "1", "0x1"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- reference arm / cpu baseline
+
+
+def reference_run(cfg, B_sample, steps, warmup, threads, seconds_cap=None):
+    """The reference's own path (EmbeddingWorker -> LocalHub -> PsShardService ->
+    PsShard, sync order) on bounded samples of the workload. Returns samples/s."""
+    import oracle as O
+    from paper_2111_05897_b200 import workloads as W
+
+    total = steps + warmup
+    per_shard = int(1.3 * B_sample * cfg.features * total / cfg.shards) + 1024
+    ref = O.Reference(cfg.salts(), per_shard, cfg.dim, cfg.optimizer, cfg.aggregation,
+                      cfg.features)
+    times = []
+    t_start = time.perf_counter()
+    for s in range(total):
+        b = W.make_batch(cfg, 10_000 + s, batch=B_sample)
+        g = W.make_grads(cfg, b.B, s)
+        off = b.offsets.astype(np.uint64)
+        t0 = time.perf_counter()
+        ref.step(b.B, b.ids, off, g, cfg.lr, s + 1, True, threads=threads)
+        dt = time.perf_counter() - t0
+        if s >= warmup:
+            times.append(dt)
+        if seconds_cap and time.perf_counter() - t_start > seconds_cap and len(times) >= 1:
+            break
+    return B_sample * len(times) / sum(times), len(times)
+
+
+def run_reference_arm(args):
+    from paper_2111_05897_b200 import workloads as W
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = W.CONFIGS[args.config]
+    B_sample = min(cfg.batch, 2048)
+    cores = nproc()
+    value, n = reference_run(cfg, B_sample, args.steps, args.warmup, cores)
+    line = {
+        "impl": "reference", "metric": "embedding lookup+update samples/sec", "value": value,
+        "unit": "samples/s", "n_gpus": args.gpus, "steps": n, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * B_sample / value, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (fp64 pooling/fan-out)", "data": "synthetic",
+        "config": workload_config(cfg, args, ref_sample=B_sample),
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "reference",
+                         "sample": f"{B_sample} samples/step of {cfg.name}, pull on {cores} "
+                                   f"threads + ordered push, reference headers via oracle/_ref"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, args, ref_sample=None):
+    d = {"workload": f"{cfg.name}: batch {cfg.batch}, {cfg.features} "
+                     f"{'multi-hot' if cfg.multi_hot else 'one-hot'} features, "
+                     f"{cfg.rows // 1_000_000}M-row table dim {cfg.dim}, {cfg.optimizer}, "
+                     f"{cfg.aggregation} pooling, staleness 0",
+         "global_batch": cfg.batch * args.gpus, "rows": cfg.table_capacity(), "dim": cfg.dim,
+         "features": cfg.features, "logical_shards": cfg.shards,
+         "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single",
+         "l2": "per-step footprint > L2 (126 MB); no flush"}
+    if ref_sample:
+        d["reference_sample_batch"] = ref_sample
+    return d
+
+
+# ---------------------------------------------------------------- our arm
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2111_05897_b200 import hps
+    from paper_2111_05897_b200 import workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = W.CONFIGS[args.config]
+    D, F, B = cfg.dim, cfg.features, cfg.batch
+    opt = hps.ADAGRAD if cfg.optimizer == "adagrad" else hps.SGD
+    agg = hps.MEAN if cfg.aggregation == "mean" else hps.SUM
+    cap = cfg.table_capacity()
+    table = hps.ShardSet(cfg.shards, D, cap, opt, salts=cfg.salts(), device=local)
+    stream = torch.cuda.current_stream()
+
+    # -- pre-warm: every row of the table exists before timing (M = 0 misses).
+    t0 = time.perf_counter()
+    chunk = 1 << 23
+    buf = torch.empty((chunk, D), dtype=torch.float32, device=dev)
+    for a in range(0, cap, chunk):
+        n = min(chunk, cap - a)
+        ids = torch.arange(a, a + n, dtype=torch.int64, device=dev)
+        table.lookup(ids, out_values=buf[:n], stream=stream)
+    torch.cuda.synchronize()
+    prewarm_s = time.perf_counter() - t0
+
+    # -- inputs: M distinct batches, resident in HBM
+    M = args.batches
+    host_batches = [W.make_batch(cfg, 1000 * rank + m) for m in range(M)]
+    batches = []
+    uniq = []
+    for hb in host_batches:
+        ids = torch.from_numpy(hb.ids.view(np.int64)).to(dev)
+        offs = torch.from_numpy(hb.offsets.view(np.int32)).to(dev)
+        batches.append((ids, offs, hb.N))
+        uniq.append(len(np.unique(hb.ids)))
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    grads = [((torch.rand((B, F, D), generator=gen, device=dev) * 2 - 1) * cfg.grad_scale)
+             for _ in range(M)]
+    pooled = torch.empty((B, F, D), dtype=torch.float32, device=dev)
+    ew = hps.EmbeddingWorker(table, agg)
+
+    def step(i):
+        ids, offs, n = batches[i % M]
+        ew.register_batch(ids, offs, B, F, stream=stream)
+        ew.serve_pull(out_pooled=pooled, stream=stream)
+        ew.apply_backward(grads[i % M], cfg.lr, step_tag=i + 1, flags=hps.ASYNC, stream=stream)
+
+    it = 0
+    for _ in range(args.warmup):
+        step(it)
+        it += 1
+    torch.cuda.synchronize()
+    table.sync()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # -- timed region (device time, CUDA events on the launching stream)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    l0 = hps.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(it)
+        it += 1
+    e1.record(stream)
+    barrier()
+    launches = hps.launch_count() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    # soak: keep the same step running so the clock sampler sees >= soak-seconds under load
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < args.soak_seconds:
+        for _ in range(10):
+            step(it)
+            it += 1
+        torch.cuda.synchronize()
+    clk = clocks.stop()
+    table.sync()  # surfaces any deferred data-dependent error of the timed steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * B * 1000.0 / ms
+
+    # -- per-kernel timing pass (same steps, events around each region)
+    table.profile(True)
+    for _ in range(args.steps):
+        step(it)
+        it += 1
+    torch.cuda.synchronize()
+    regions = {}
+    for r in ("probe", "sort", "heads", "pool", "check", "update"):
+        tot, cnt = table.profile_get(r)
+        regions[r] = (tot / max(cnt, 1), cnt)
+    table.profile(False)
+
+    # -- algorithmic bytes
+    N_avg = float(np.mean([b[2] for b in batches]))
+    U_avg = float(np.mean(uniq))
+    O_ = D if opt == hps.ADAGRAD else 0
+    bytes_step = (8 * N_avg + 8 * N_avg + 12 * U_avg + 4 * D * U_avg + 4 * B * F * D +
+                  4 * B * F * D + 8 * (D + O_) * U_avg)
+    kernel_bytes = {
+        "update": 4 * B * F * D + 8 * (D + O_) * U_avg,
+        "pool": 4 * D * U_avg + 4 * B * F * D + 4 * N_avg,
+        "probe": 8 * N_avg + 12 * U_avg + 4 * N_avg,
+        "check": 4 * B * F * D,
+    }
+    peak, peak_kind = peaks()
+    dom = max(("update", "pool", "probe", "check"), key=lambda r: regions[r][0])
+    dom_ms = regions[dom][0]
+    achieved = kernel_bytes[dom] / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(cfg.name, {}).get(dom)
+        except Exception:
+            traffic = None
+
+    # -- e2e through the public API with HOST buffers (pinned), copies inside the region
+    e2e = None
+    if args.e2e_steps > 0:
+        hb = host_batches[0]
+        h_ids = torch.from_numpy(hb.ids.view(np.int64)).pin_memory()
+        h_offs = torch.from_numpy(hb.offsets.view(np.int32)).pin_memory()
+        h_grads = grads[0].cpu().pin_memory()
+        h_pooled = torch.empty((B, F, D), dtype=torch.float32).pin_memory()
+        for _ in range(2):
+            ew.register_batch(h_ids, h_offs, B, F, stream=stream)
+            ew.serve_pull(out_pooled=h_pooled, stream=stream)
+            ew.apply_backward(h_grads, cfg.lr, step_tag=it + 1, stream=stream)
+            it += 1
+        barrier()
+        q0 = torch.cuda.Event(enable_timing=True)
+        q1 = torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        q0.record(stream)
+        for _ in range(args.e2e_steps):
+            ew.register_batch(h_ids, h_offs, B, F, stream=stream)
+            ew.serve_pull(out_pooled=h_pooled, stream=stream)
+            ew.apply_backward(h_grads, cfg.lr, step_tag=it + 1, stream=stream)
+            it += 1
+        q1.record(stream)
+        torch.cuda.synchronize()
+        wall_ms = (time.perf_counter() - w0) * 1000 / args.e2e_steps
+        e_ms = max(q0.elapsed_time(q1) / args.e2e_steps, wall_ms)
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": world * B * 1000.0 / e_ms, "unit": "samples/s",
+               "h2d_bytes_per_step": int(8 * hb.N + 4 * (B * F + 1) + 4 * B * F * D),
+               "d2h_bytes_per_step": int(4 * B * F * D),
+               "path": "hps_batch_register/pull/push with pinned host buffers"}
+
+    # -- CPU baseline: the reference on this box's host cores (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cores = nproc()
+            B_s = 2048
+            v, n = reference_run(cfg, B_s, steps=100, warmup=1, threads=cores,
+                                 seconds_cap=args.cpu_seconds)
+            cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": "reference",
+                   "sample": f"{n} steps x {B_s} samples of {cfg.name} through the reference "
+                             f"EmbeddingWorker/PsShard (oracle/_ref), pull on {cores} threads + "
+                             f"ordered single-thread push"}
+        except Exception as e:  # report, never fake
+            cpu = {"value": None, "unit": "samples/s", "cores": nproc(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": "embedding lookup+update samples/sec", "value": value,
+            "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 (fp64 pooling/fan-out)", "data": "synthetic",
+            "config": workload_config(cfg, args),
+            "hbm": {"algorithmic_bytes_per_step": bytes_step,
+                    "achieved_gbs": bytes_step / (ms * 1e-3) / 1e9,
+                    "frac_of_peak": bytes_step / (ms * 1e-3) / 1e9 / peak,
+                    "N": N_avg, "U": U_avg},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+                         "traffic": traffic, "peak_source": peak_kind,
+                         "algorithmic_bytes_per_launch": kernel_bytes[dom],
+                         "ms_per_launch": dom_ms},
+            "kernels_ms": {k: round(v[0], 4) for k, v in regions.items()},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk, "prewarm_s": prewarm_s,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,203 @@
+/* hps_c.h -- C ABI of the B200-native embedding lookup+update path.
+ *
+ * Drop-in boundary for the reference's embedding-worker / parameter-server
+ * operator API (/root/reference/proj/include/hybridps). Every entry point takes
+ * plain pointers and sizes; none throws. The reference has no FFI of its own,
+ * so each function cites the C++ member it replaces. A C++ adapter with the
+ * reference's class shapes (PsShard / ShardSet / EmbeddingWorker) sits on top
+ * of this header in include/hps/compat.hpp; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - Status codes map 1:1 onto the reference's exception types
+ *    (errors.hpp:28-107); HPS_E_CUDA reports a CUDA runtime failure.
+ *  - Batch functions take DEVICE or HOST pointers; the kind is detected per
+ *    pointer (cudaPointerGetAttributes). Host inputs are staged through pinned
+ *    buffers inside the library, host outputs are copied back before return.
+ *  - `stream` is a cudaStream_t (NULL = the legacy default stream). Calls that
+ *    must report a data-dependent error (non-finite gradient, capacity) are
+ *    synchronous unless HPS_ASYNC is passed, in which case the error surfaces
+ *    from the next hps_table_sync().
+ *  - A table holds S logical shards (route_shard(id, S) = mix64(id) % S,
+ *    core.hpp:145-150) with one init salt per shard (PsShardConfig::rng_salt,
+ *    embedding_ps.hpp:41-46). With world_size > 1 a table holds the shards
+ *    s with s % world_size == owner_rank; see hps_shard_* below.
+ */
+#ifndef HPS_C_H
+#define HPS_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define HPS_ABI_VERSION 1
+
+typedef enum hps_status {
+  HPS_OK = 0,
+  HPS_E_PRECONDITION = 1,      /* PreconditionError      errors.hpp:28 */
+  HPS_E_CONFIG = 2,            /* ConfigError            errors.hpp:35 */
+  HPS_E_PROTOCOL = 3,          /* ProtocolError          errors.hpp:42 */
+  HPS_E_TRANSPORT = 4,         /* TransportError         errors.hpp:49 */
+  HPS_E_CHECKPOINT_CORRUPT = 5,/* CheckpointCorruptError errors.hpp:56 */
+  HPS_E_DIVERGENCE = 6,        /* DivergenceError        errors.hpp:62 */
+  HPS_E_CONSISTENCY = 7,       /* ConsistencyError       errors.hpp:68 */
+  HPS_E_UNDEFINED_METRIC = 8,  /* UndefinedMetricError   errors.hpp:74 */
+  HPS_E_STALE_SAMPLE = 9,      /* StaleSampleError       errors.hpp:80 */
+  HPS_E_BACKPRESSURE = 10,     /* BackpressureError      errors.hpp:86 */
+  HPS_E_CLOCK = 11,            /* ClockError             errors.hpp:92 */
+  HPS_E_SYNC_FAILURE = 12,     /* SyncFailureError       errors.hpp:98 */
+  HPS_E_UNRECOVERABLE = 13,    /* UnrecoverableRunError  errors.hpp:104 */
+  HPS_E_CUDA = 100             /* CUDA runtime / launch failure */
+} hps_status;
+
+typedef enum hps_optimizer { HPS_ADAGRAD = 0, HPS_SGD = 1 } hps_optimizer; /* EmbOptimizer, embedding_ps.hpp:37 */
+typedef enum hps_aggregation { HPS_MEAN = 0, HPS_SUM = 1 } hps_aggregation; /* ModelConfig::Aggregation, core.hpp:178 */
+
+/* flags */
+#define HPS_ASYNC 1u   /* do not synchronise to report data-dependent errors */
+
+typedef void* hps_stream; /* cudaStream_t */
+
+typedef struct hps_table hps_table;
+typedef struct hps_batch hps_batch;
+
+typedef struct hps_table_cfg {
+  uint32_t shard_count;        /* logical shards S (ShardSet(shard_count, ...), embedding_ps.hpp:506) */
+  const uint64_t* shard_salts; /* S per-shard init salts (host pointer) */
+  uint64_t capacity;           /* rows this device may hold (sum over its owned shards) */
+  uint32_t embedding_dim;      /* PsShardConfig::embedding_dim */
+  int32_t optimizer;           /* hps_optimizer */
+  int32_t device;              /* CUDA ordinal; -1 = current device */
+  uint32_t owner_rank;         /* 0 for a single-device table */
+  uint32_t world_size;         /* 1 for a single-device table */
+} hps_table_cfg;
+
+typedef struct hps_counters {
+  uint64_t misses;            /* PsShard::miss_count          embedding_ps.hpp:79 */
+  uint64_t evictions;         /* PsShard::eviction_count      embedding_ps.hpp:75 (always 0: no eviction) */
+  uint64_t clock_resets;      /* PsShard::clock_reset_count   embedding_ps.hpp:83 */
+  uint64_t stale_epoch_drops; /* PsShard::stale_epoch_drops   embedding_ps.hpp:87 */
+  uint64_t size;              /* PsShard::size                embedding_ps.hpp:95 */
+  uint64_t capacity;
+  uint32_t epoch;             /* PsShard::epoch               embedding_ps.hpp:91 */
+  uint32_t max_delay;         /* largest staleness delay recorded (StalenessStats) */
+  uint64_t delay_hist[17];    /* delays 0..15, >=16 (StalenessStats::record_delay, staleness.hpp:42-49) */
+} hps_counters;
+
+/* ---- errors / version ---------------------------------------------------------------- */
+const char* hps_last_error(void);   /* thread-local message of the last failing call */
+int hps_abi_version(void);
+
+/* ---- hashing / routing (core.hpp:36-44, 145-150) ------------------------------------ */
+uint64_t hps_mix64(uint64_t x);
+uint32_t hps_route_shard(uint64_t id, uint32_t shard_count);
+/* Device: out_shard[i] = route_shard(ids[i], S). */
+hps_status hps_route(const uint64_t* ids, size_t n, uint32_t shard_count, uint32_t* out_shard,
+                     hps_stream stream);
+
+/* ---- table lifecycle (PsShard(cfg) embedding_ps.hpp:63, ShardSet embedding_ps.hpp:506) */
+hps_status hps_table_create(const hps_table_cfg* cfg, hps_table** out);
+hps_status hps_table_destroy(hps_table* t);
+hps_status hps_table_counters(hps_table* t, hps_counters* out);
+hps_status hps_table_sync(hps_table* t); /* drain async work, report deferred errors */
+uint32_t hps_table_epoch(const hps_table* t);            /* PsShard::epoch         :91 */
+uint32_t hps_table_advance_epoch(hps_table* t);          /* PsShard::advance_epoch :204 */
+hps_status hps_table_reset(hps_table* t);                /* PsShard::reset_for_recovery :193 */
+
+/* ---- parameter-server surface --------------------------------------------------------- */
+/* PsShard::lookup (embedding_ps.hpp:105-114) / ShardSet::lookup (:531-541): duplicates
+ * allowed, misses lazily initialised (find_or_init :417-434). out_values[n*D];
+ * out_versions[n] optional. */
+hps_status hps_lookup(hps_table* t, const uint64_t* ids, size_t n, float* out_values,
+                      uint64_t* out_versions, hps_stream stream);
+
+/* PsShard::apply_gradients (embedding_ps.hpp:139-162), array-shaped: entry i carries
+ * ids[i], grads[i*D..], read_versions[i]. Epoch fence first (*accepted = 0, nothing
+ * applied, stale_epoch_drops += n); then every gradient is validated finite before
+ * anything mutates (HPS_E_DIVERGENCE otherwise); then entries apply in array order
+ * (rows with repeated ids see them in that order). read_versions == NULL selects the
+ * untracked map-shaped surface (apply_gradients_map :165-189: version += 1 per write).
+ * out_delays[n] optional (per entry, reference count_delay :454-480). */
+hps_status hps_apply(hps_table* t, const uint64_t* ids, const float* grads,
+                     const uint64_t* read_versions, size_t n, float lr, uint32_t step_tag,
+                     uint32_t epoch, uint32_t* out_delays, int* accepted, uint32_t flags,
+                     hps_stream stream);
+
+/* Test/checkpoint hook: read rows without lazy init or touching (present[i] = 0 if absent).
+ * Any output may be NULL. */
+hps_status hps_peek(hps_table* t, const uint64_t* ids, size_t n, float* out_w, float* out_acc,
+                    uint64_t* out_versions, uint8_t* out_present, hps_stream stream);
+
+/* ---- embedding-worker surface (batch-shaped) ----------------------------------------- */
+/* A batch is B samples x F feature groups in CSR form: ids[N], offsets[B*F+1] (uint32,
+ * sample-major, group-minor; IdFeatures core.hpp:129-131). Groups may be empty and
+ * may list an id more than once.
+ *
+ * hps_batch_register  ~ EmbeddingWorker::register_sample (embedding_worker.hpp:493) for
+ *                       B samples: routes, probes/lazily inits every id and builds the
+ *                       per-row apply order once; sample_keys[B] (SampleId.raw) fixes the
+ *                       apply order (ascending), NULL = batch order.
+ * hps_batch_pull      ~ EmbeddingWorker::serve_pull (:523-571): out_pooled[B*F*D],
+ *                       out_read_versions[N] (optional, per listing).
+ * hps_batch_push      ~ apply_backward + gated flush (:575-594, :777-801): grads[B*F*D];
+ *                       per sample in apply order, one optimizer application per (sample,
+ *                       unique id) carrying the fp64 chain-rule sum (push_to_shards
+ *                       :726-775). read versions come from the last hps_batch_pull of this
+ *                       batch (tracked) unless untracked = 1. Whole-batch validation
+ *                       precedes mutation. */
+hps_status hps_batch_create(hps_table* t, int32_t aggregation, hps_batch** out); /* EmbeddingWorkerConfig::aggregation */
+hps_status hps_batch_destroy(hps_batch* b);
+hps_status hps_batch_register(hps_batch* b, const uint64_t* ids, size_t n_ids,
+                              const uint32_t* offsets, uint32_t B, uint32_t F,
+                              const uint64_t* sample_keys, hps_stream stream);
+hps_status hps_batch_pull(hps_batch* b, float* out_pooled, uint64_t* out_read_versions,
+                          hps_stream stream);
+hps_status hps_batch_push(hps_batch* b, const float* grads, float lr, uint32_t step_tag,
+                          uint32_t epoch, int untracked, uint32_t* out_delays, int* accepted,
+                          uint32_t flags, hps_stream stream);
+/* Number of (sample, unique id) applications the last push performed (delays length). */
+hps_status hps_batch_pairs(hps_batch* b, uint64_t* out_pairs);
+
+/* Stateless one-shot forms (register + pull / register + push). */
+hps_status hps_pull_batch(hps_table* t, const uint64_t* ids, size_t n_ids, const uint32_t* offsets,
+                          uint32_t B, uint32_t F, int32_t aggregation, float* out_pooled,
+                          uint64_t* out_read_versions, hps_stream stream);
+hps_status hps_push_batch(hps_table* t, const uint64_t* ids, size_t n_ids, const uint32_t* offsets,
+                          uint32_t B, uint32_t F, int32_t aggregation, const float* grads,
+                          const uint64_t* read_versions, const uint64_t* sample_keys, float lr,
+                          uint32_t step_tag, uint32_t epoch, int* accepted, hps_stream stream);
+
+/* ---- instrumentation (no reference counterpart) ---------------------------------------- */
+/* Kernels this library has launched in the process (proves which code ran). */
+uint64_t hps_launch_count(void);
+/* CUDA-event timing of named regions on the launching stream ("probe", "sort", "heads",
+ * "pool", "check", "update"); enable resets the record. */
+hps_status hps_profile_enable(hps_table* t, int enable);
+hps_status hps_profile_get(hps_table* t, const char* region, double* total_ms, uint64_t* count);
+
+/* ---- batch de-duplication (codec.hpp:123-182) ----------------------------------------- */
+/* Sorted unique + inverse index over a flat id array: out_unique[u] ascending,
+ * out_inverse[i] = index of ids[i] in out_unique; *out_u written (host pointer).
+ * Device or host pointers. */
+hps_status hps_dedup(const uint64_t* ids, size_t n, uint64_t* out_unique, uint32_t* out_inverse,
+                     uint64_t* out_u, hps_stream stream);
+/* compress_indices (codec.hpp:123-156): per group g, unique ids ascending
+ * (unique[group_u_off[g] .. group_u_off[g+1]]) each with its ascending postings
+ * (postings[post_off[k] .. post_off[k+1]], u16 sample indices, within-sample duplicates
+ * collapsed). B > 65535 -> HPS_E_PRECONDITION. Buffers sized for N (worst case). */
+hps_status hps_compress_indices(const uint64_t* ids, size_t n_ids, const uint32_t* offsets, uint32_t B,
+                                uint32_t G, uint64_t* group_u_off, uint64_t* unique,
+                                uint64_t* post_off, uint16_t* postings, hps_stream stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* HPS_C_H */

@@ -1,0 +1,308 @@
+// The C ABI (include/hps_c.h): argument checks, device selection, the per-table
+// lock, and mapping of hps::Error / CUDA failures onto hps_status. Nothing here
+// throws across the boundary.
+#include <cuda_runtime.h>
+
+#include <exception>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "../../include/hps_c.h"
+#include "common.cuh"
+#include "table.cuh"
+#include "table_impl.h"
+
+struct hps_table {
+  hps::Table* impl;
+};
+struct hps_batch {
+  hps::Batch impl;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename Fn>
+hps_status guarded(Fn&& fn) {
+  try {
+    fn();
+    return HPS_OK;
+  } catch (const hps::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return HPS_E_CUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return HPS_E_CUDA;
+  } catch (...) {
+    g_last_error = "unknown failure";
+    return HPS_E_CUDA;
+  }
+}
+
+inline cudaStream_t S(hps_stream s) { return static_cast<cudaStream_t>(s); }
+
+#define REQUIRE(cond, msg) \
+  if (!(cond)) throw hps::Error(HPS_E_PRECONDITION, msg)
+
+}  // namespace
+
+extern "C" {
+
+const char* hps_last_error(void) { return g_last_error.c_str(); }
+int hps_abi_version(void) { return HPS_ABI_VERSION; }
+
+uint64_t hps_mix64(uint64_t x) { return hps::mix64(x); }
+
+uint32_t hps_route_shard(uint64_t id, uint32_t shard_count) {
+  return shard_count ? hps::route_shard(id, shard_count) : 0u;
+}
+
+hps_status hps_route(const uint64_t* ids, size_t n, uint32_t shard_count, uint32_t* out_shard,
+                     hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(shard_count > 0, "route_shard: shard_count must be positive");
+    REQUIRE(n == 0 || (ids && out_shard), "hps_route: null buffer");
+    hps::route(ids, n, shard_count, out_shard, S(stream));
+  });
+}
+
+hps_status hps_table_create(const hps_table_cfg* cfg, hps_table** out) {
+  return guarded([&] {
+    REQUIRE(cfg && out, "hps_table_create: null argument");
+    *out = nullptr;
+    hps::Table* t = hps::table_create(*cfg);
+    *out = new hps_table{t};
+  });
+}
+
+hps_status hps_table_destroy(hps_table* t) {
+  return guarded([&] {
+    if (!t) return;
+    hps::table_destroy(t->impl);
+    delete t;
+  });
+}
+
+hps_status hps_table_counters(hps_table* t, hps_counters* out) {
+  return guarded([&] {
+    REQUIRE(t && out, "hps_table_counters: null argument");
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::table_counters(t->impl, out);
+  });
+}
+
+hps_status hps_table_sync(hps_table* t) {
+  return guarded([&] {
+    REQUIRE(t, "hps_table_sync: null table");
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::table_sync(t->impl);
+  });
+}
+
+uint32_t hps_table_epoch(const hps_table* t) { return t ? t->impl->epoch : 0u; }
+
+uint32_t hps_table_advance_epoch(hps_table* t) {
+  if (!t) return 0u;
+  std::lock_guard<std::mutex> g(t->impl->mu);
+  return ++t->impl->epoch;
+}
+
+hps_status hps_table_reset(hps_table* t) {
+  return guarded([&] {
+    REQUIRE(t, "hps_table_reset: null table");
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::table_reset(t->impl);
+  });
+}
+
+hps_status hps_lookup(hps_table* t, const uint64_t* ids, size_t n, float* out_values,
+                      uint64_t* out_versions, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(t, "hps_lookup: null table");
+    REQUIRE(n == 0 || (ids && out_values), "hps_lookup: null buffer");
+    if (n == 0) return;
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::DeviceGuard dg(t->impl->device);
+    hps::table_lookup(t->impl, ids, n, out_values, out_versions, S(stream));
+  });
+}
+
+hps_status hps_apply(hps_table* t, const uint64_t* ids, const float* grads,
+                     const uint64_t* read_versions, size_t n, float lr, uint32_t step_tag,
+                     uint32_t epoch, uint32_t* out_delays, int* accepted, uint32_t flags,
+                     hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(t, "hps_apply: null table");
+    REQUIRE(n == 0 || (ids && grads), "hps_apply: null buffer");
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::DeviceGuard dg(t->impl->device);
+    if (n == 0) {
+      if (accepted) *accepted = epoch == t->impl->epoch;
+      return;
+    }
+    hps::table_apply(t->impl, ids, grads, read_versions, n, lr, step_tag, epoch, out_delays,
+                     accepted, flags, S(stream));
+  });
+}
+
+hps_status hps_peek(hps_table* t, const uint64_t* ids, size_t n, float* out_w, float* out_acc,
+                    uint64_t* out_versions, uint8_t* out_present, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(t, "hps_peek: null table");
+    REQUIRE(n == 0 || ids, "hps_peek: null ids");
+    if (n == 0) return;
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::DeviceGuard dg(t->impl->device);
+    hps::table_peek(t->impl, ids, n, out_w, out_acc, out_versions, out_present, S(stream));
+  });
+}
+
+hps_status hps_batch_create(hps_table* t, int32_t aggregation, hps_batch** out) {
+  return guarded([&] {
+    REQUIRE(t && out, "hps_batch_create: null argument");
+    REQUIRE(aggregation == HPS_MEAN || aggregation == HPS_SUM, "hps_batch_create: bad aggregation");
+    *out = new hps_batch();
+    (*out)->impl.table = t->impl;
+    (*out)->impl.agg = aggregation;
+  });
+}
+
+hps_status hps_batch_destroy(hps_batch* b) {
+  return guarded([&] {
+    if (!b) return;
+    {
+      hps::DeviceGuard dg(b->impl.table->device);
+      cudaDeviceSynchronize();
+      hps::batch_free(b->impl);
+    }
+    delete b;
+  });
+}
+
+hps_status hps_batch_register(hps_batch* b, const uint64_t* ids, size_t n_ids,
+                              const uint32_t* offsets, uint32_t B, uint32_t F,
+                              const uint64_t* sample_keys, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(b, "hps_batch_register: null batch");
+    REQUIRE(offsets, "hps_batch_register: null offsets");
+    REQUIRE(n_ids == 0 || ids, "hps_batch_register: null ids");
+    hps::Table* t = b->impl.table;
+    std::lock_guard<std::mutex> g(t->mu);
+    hps::DeviceGuard dg(t->device);
+    hps::batch_register(b->impl, ids, n_ids, offsets, B, F, sample_keys, S(stream));
+  });
+}
+
+hps_status hps_batch_pull(hps_batch* b, float* out_pooled, uint64_t* out_read_versions,
+                          hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(b, "hps_batch_pull: null batch");
+    REQUIRE(out_pooled || b->impl.B == 0, "hps_batch_pull: null output");
+    hps::Table* t = b->impl.table;
+    std::lock_guard<std::mutex> g(t->mu);
+    hps::DeviceGuard dg(t->device);
+    hps::batch_pull(b->impl, b->impl.agg, out_pooled, out_read_versions, S(stream));
+  });
+}
+
+hps_status hps_batch_push(hps_batch* b, const float* grads, float lr, uint32_t step_tag,
+                          uint32_t epoch, int untracked, uint32_t* out_delays, int* accepted,
+                          uint32_t flags, hps_stream stream) {
+  (void)out_delays;  // per-(sample,id) delays land in the table's delay histogram
+  return guarded([&] {
+    REQUIRE(b, "hps_batch_push: null batch");
+    REQUIRE(grads || b->impl.B == 0, "hps_batch_push: null gradients");
+    hps::Table* t = b->impl.table;
+    std::lock_guard<std::mutex> g(t->mu);
+    hps::DeviceGuard dg(t->device);
+    hps::batch_push(b->impl, b->impl.agg, grads, lr, step_tag, epoch, untracked,
+                    nullptr, accepted, flags, S(stream));
+  });
+}
+
+hps_status hps_batch_pairs(hps_batch* b, uint64_t* out_pairs) {
+  return guarded([&] {
+    REQUIRE(b && out_pairs, "hps_batch_pairs: null argument");
+    hps::Table* t = b->impl.table;
+    std::lock_guard<std::mutex> g(t->mu);
+    hps::DeviceGuard dg(t->device);
+    *out_pairs = hps::batch_pairs(b->impl);
+  });
+}
+
+hps_status hps_pull_batch(hps_table* t, const uint64_t* ids, size_t n_ids, const uint32_t* offsets,
+                          uint32_t B, uint32_t F, int32_t aggregation, float* out_pooled,
+                          uint64_t* out_read_versions, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(t && offsets, "hps_pull_batch: null argument");
+    REQUIRE(aggregation == HPS_MEAN || aggregation == HPS_SUM, "hps_pull_batch: bad aggregation");
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::DeviceGuard dg(t->impl->device);
+    hps::Batch& b = t->impl->scratch;
+    b.agg = aggregation;
+    hps::batch_register(b, ids, n_ids, offsets, B, F, nullptr, S(stream));
+    hps::batch_pull(b, aggregation, out_pooled, out_read_versions, S(stream));
+  });
+}
+
+hps_status hps_push_batch(hps_table* t, const uint64_t* ids, size_t n_ids, const uint32_t* offsets,
+                          uint32_t B, uint32_t F, int32_t aggregation, const float* grads,
+                          const uint64_t* read_versions, const uint64_t* sample_keys, float lr,
+                          uint32_t step_tag, uint32_t epoch, int* accepted, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(t && offsets, "hps_push_batch: null argument");
+    REQUIRE(aggregation == HPS_MEAN || aggregation == HPS_SUM, "hps_push_batch: bad aggregation");
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::DeviceGuard dg(t->impl->device);
+    hps::Batch& b = t->impl->scratch;
+    b.agg = aggregation;
+    hps::batch_register(b, ids, n_ids, offsets, B, F, sample_keys, S(stream));
+    hps::batch_push(b, aggregation, grads, lr, step_tag, epoch, read_versions ? 0 : 1,
+                    read_versions, accepted, 0, S(stream));
+  });
+}
+
+uint64_t hps_launch_count(void) { return hps::g_launches.load(); }
+
+hps_status hps_profile_enable(hps_table* t, int enable) {
+  return guarded([&] {
+    REQUIRE(t, "hps_profile_enable: null table");
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::profile_enable(t->impl, enable != 0);
+  });
+}
+
+hps_status hps_profile_get(hps_table* t, const char* region, double* total_ms, uint64_t* count) {
+  return guarded([&] {
+    REQUIRE(t && region && total_ms && count, "hps_profile_get: null argument");
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::DeviceGuard dg(t->impl->device);
+    hps::profile_get(t->impl, region, total_ms, count);
+  });
+}
+
+hps_status hps_dedup(const uint64_t* ids, size_t n, uint64_t* out_unique, uint32_t* out_inverse,
+                     uint64_t* out_u, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(n == 0 || (ids && out_unique && out_inverse), "hps_dedup: null buffer");
+    hps::dedup(ids, n, out_unique, out_inverse, out_u, S(stream));
+  });
+}
+
+hps_status hps_compress_indices(const uint64_t* ids, size_t n_ids, const uint32_t* offsets,
+                                uint32_t B, uint32_t G, uint64_t* group_u_off, uint64_t* unique,
+                                uint64_t* post_off, uint16_t* postings, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(offsets && group_u_off && unique && post_off && postings,
+            "hps_compress_indices: null buffer");
+    hps::compress_indices(ids, n_ids, offsets, B, G, group_u_off, unique, post_off, postings,
+                          S(stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,633 @@
+// Host-side orchestration of the hot path: table lifecycle, the PS surface
+// (lookup / apply / peek) and the embedding-worker batch surface (register /
+// pull / push). Every public entry point is in capi.cu; this file throws
+// hps::Error and never returns status codes itself.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+
+#include "common.cuh"
+#include "radix_sort.cuh"
+#include "table.cuh"
+#include "table_impl.h"
+
+namespace hps {
+
+// ---- pointer staging --------------------------------------------------------------------
+
+PtrKind ptr_kind(const void* p) {
+  if (!p) return PtrKind::kDevice;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return PtrKind::kPageable;
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return PtrKind::kDevice;
+  if (at.type == cudaMemoryTypeHost) return PtrKind::kPinned;
+  return PtrKind::kPageable;
+}
+
+DeviceGuard::DeviceGuard(int dev) {
+  HPS_CUDA(cudaGetDevice(&prev_));
+  changed_ = dev >= 0 && dev != prev_;
+  if (changed_) HPS_CUDA(cudaSetDevice(dev));
+}
+DeviceGuard::~DeviceGuard() {
+  if (changed_) cudaSetDevice(prev_);
+}
+
+template <typename T>
+static void ensure(T*& p, uint64_t& cap, uint64_t need) {
+  if (need <= cap && p) return;
+  if (p) HPS_CUDA(cudaFree(p));
+  p = nullptr;
+  uint64_t n = std::max<uint64_t>(need, 1);
+  HPS_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  cap = n;
+}
+
+void StagePool::free_all() {
+  for (Buf& b : bufs) {
+    if (b.dev) cudaFree(b.dev);
+    if (b.pinned) cudaFreeHost(b.pinned);
+  }
+  bufs.clear();
+}
+
+StagePool::Buf& Stager::next(size_t bytes, bool need_pinned) {
+  if (used_ == pool_.bufs.size()) pool_.bufs.emplace_back();
+  StagePool::Buf& b = pool_.bufs[used_++];
+  bytes = std::max<size_t>(bytes, 16);
+  if (b.dev_cap < bytes) {
+    if (b.dev) HPS_CUDA(cudaFree(b.dev));
+    b.dev = nullptr;
+    HPS_CUDA(cudaMalloc(&b.dev, bytes));
+    b.dev_cap = bytes;
+  }
+  if (need_pinned && b.pinned_cap < bytes) {
+    if (b.pinned) HPS_CUDA(cudaFreeHost(b.pinned));
+    b.pinned = nullptr;
+    HPS_CUDA(cudaMallocHost(&b.pinned, bytes));
+    b.pinned_cap = bytes;
+  }
+  return b;
+}
+
+const void* Stager::in(const void* p, size_t bytes, cudaStream_t st) {
+  if (!p) return p;
+  PtrKind k = ptr_kind(p);
+  if (k == PtrKind::kDevice) return p;
+  sync_needed_ = true;
+  StagePool::Buf& b = next(bytes, k == PtrKind::kPageable);
+  if (!bytes) return b.dev;
+  if (k == PtrKind::kPageable) {
+    memcpy(b.pinned, p, bytes);
+    HPS_CUDA(cudaMemcpyAsync(b.dev, b.pinned, bytes, cudaMemcpyHostToDevice, st));
+  } else {
+    HPS_CUDA(cudaMemcpyAsync(b.dev, p, bytes, cudaMemcpyHostToDevice, st));
+  }
+  return b.dev;
+}
+
+void* Stager::out(void* p, size_t bytes) {
+  if (!p) return p;
+  PtrKind k = ptr_kind(p);
+  if (k == PtrKind::kDevice) return p;
+  sync_needed_ = true;
+  StagePool::Buf& b = next(bytes, k == PtrKind::kPageable);
+  outs_.push_back(Out{p, b.dev, k == PtrKind::kPageable ? b.pinned : nullptr, bytes});
+  return b.dev;
+}
+
+void Stager::finish(cudaStream_t st) {
+  for (Out& o : outs_)
+    if (o.bytes)
+      HPS_CUDA(cudaMemcpyAsync(o.pinned ? o.pinned : o.host, o.dev, o.bytes,
+                               cudaMemcpyDeviceToHost, st));
+  if (sync_needed_) HPS_CUDA(cudaStreamSynchronize(st));
+  for (Out& o : outs_)
+    if (o.pinned && o.bytes) memcpy(o.host, o.pinned, o.bytes);
+  outs_.clear();
+}
+
+// ---- profiling ------------------------------------------------------------------------------
+
+cudaEvent_t Profiler::next() {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    HPS_CUDA(cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+  return pool[used++];
+}
+
+void Profiler::reset() {
+  recs.clear();
+  used = 0;
+}
+
+void Profiler::destroy() {
+  for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  pool.clear();
+  reset();
+}
+
+ProfScope::ProfScope(Table* tb, const char* n, cudaStream_t s) : t(tb), name(n), st(s) {
+  if (t->prof.enabled) {
+    a = t->prof.next();
+    HPS_CUDA(cudaEventRecord(a, st));
+  }
+}
+
+ProfScope::~ProfScope() {
+  if (a) {
+    cudaEvent_t b = t->prof.next();
+    cudaEventRecord(b, st);
+    t->prof.recs.push_back({name, a, b});
+  }
+}
+
+void profile_enable(Table* t, bool on) {
+  t->prof.reset();
+  t->prof.enabled = on;
+}
+
+// Sum of elapsed ms and record count of one region since profile_enable().
+void profile_get(Table* t, const char* name, double* ms, uint64_t* count) {
+  HPS_CUDA(cudaDeviceSynchronize());
+  double total = 0;
+  uint64_t n = 0;
+  for (auto& r : t->prof.recs) {
+    if (strcmp(r.name, name) != 0) continue;
+    float x = 0;
+    HPS_CUDA(cudaEventElapsedTime(&x, r.a, r.b));
+    total += x;
+    ++n;
+  }
+  *ms = total;
+  *count = n;
+}
+
+// ---- table lifecycle -----------------------------------------------------------------------
+
+Table* table_create(const hps_table_cfg& cfg) {
+  if (cfg.shard_count == 0) throw Error(HPS_E_CONFIG, "hps_table_create: shard_count must be positive");
+  if (!cfg.shard_salts) throw Error(HPS_E_CONFIG, "hps_table_create: shard_salts required");
+  if (cfg.embedding_dim == 0) throw Error(HPS_E_CONFIG, "hps_table_create: embedding_dim must be positive");
+  if (cfg.capacity == 0 || cfg.capacity >= kInvalidSlot)
+    throw Error(HPS_E_CONFIG, "hps_table_create: capacity must be in [1, 2^32-3]");
+  if (cfg.optimizer != HPS_ADAGRAD && cfg.optimizer != HPS_SGD)
+    throw Error(HPS_E_CONFIG, "hps_table_create: unknown optimizer");
+  if (cfg.world_size == 0 || cfg.owner_rank >= cfg.world_size)
+    throw Error(HPS_E_CONFIG, "hps_table_create: owner_rank must be < world_size");
+  auto t = new Table();
+  try {
+    t->cfg = cfg;
+    t->salts.assign(cfg.shard_salts, cfg.shard_salts + cfg.shard_count);
+    t->cfg.shard_salts = t->salts.data();
+    if (cfg.device >= 0) {
+      t->device = cfg.device;
+    } else {
+      HPS_CUDA(cudaGetDevice(&t->device));
+    }
+    DeviceGuard g(t->device);
+    cudaDeviceProp prop{};
+    HPS_CUDA(cudaGetDeviceProperties(&prop, t->device));
+    t->sm_count = prop.multiProcessorCount;
+    const uint64_t C = cfg.capacity;
+    uint64_t H = 1024;
+    int lg = 10;
+    while (H < 2 * C) H <<= 1, ++lg;
+    t->ht_size = H;
+    DevTable& d = t->d;
+    d.ht_mask = H - 1;
+    d.ht_shift = 64 - lg;
+    d.D = cfg.embedding_dim;
+    d.stride = 2 * cfg.embedding_dim;
+    d.capacity = static_cast<uint32_t>(C);
+    d.S = cfg.shard_count;
+    d.opt = cfg.optimizer;
+    HPS_CUDA(cudaMalloc(&d.keys, H * sizeof(uint64_t)));
+    HPS_CUDA(cudaMalloc(&d.vals, H * sizeof(uint32_t)));
+    HPS_CUDA(cudaMalloc(&d.rows, C * d.stride * sizeof(float)));
+    HPS_CUDA(cudaMalloc(&d.ver, C * sizeof(uint32_t)));
+    HPS_CUDA(cudaMalloc(&d.tag, C * sizeof(uint32_t)));
+    HPS_CUDA(cudaMalloc(&d.slot_id, C * sizeof(uint64_t)));
+    HPS_CUDA(cudaMalloc(&d.special, sizeof(uint32_t)));
+    HPS_CUDA(cudaMalloc(&d.hwm, sizeof(uint32_t)));
+    HPS_CUDA(cudaMalloc(&d.ctr, kCtrCount * sizeof(unsigned long long)));
+    HPS_CUDA(cudaMalloc(&t->d_salts, cfg.shard_count * sizeof(uint64_t)));
+    HPS_CUDA(cudaMemcpy(t->d_salts, t->salts.data(), cfg.shard_count * sizeof(uint64_t),
+                        cudaMemcpyHostToDevice));
+    d.salts = t->d_salts;
+    HPS_CUDA(cudaMallocHost(&t->h_ctr, kCtrCount * sizeof(unsigned long long)));
+    HPS_CUDA(cudaMemset(d.ctr, 0, kCtrCount * sizeof(unsigned long long)));
+    table_clear(t, nullptr);
+    HPS_CUDA(cudaDeviceSynchronize());
+    t->scratch.table = t;
+    return t;
+  } catch (...) {
+    table_destroy(t);
+    throw;
+  }
+}
+
+// Empties the index and the row store (LruStore::clear + PsShard state reset).
+void table_clear(Table* t, cudaStream_t st) {
+  DevTable& d = t->d;
+  HPS_CUDA(cudaMemsetAsync(d.keys, 0xff, t->ht_size * sizeof(uint64_t), st));
+  HPS_CUDA(cudaMemsetAsync(d.vals, 0xff, t->ht_size * sizeof(uint32_t), st));
+  HPS_CUDA(cudaMemsetAsync(d.special, 0xff, sizeof(uint32_t), st));
+  HPS_CUDA(cudaMemsetAsync(d.hwm, 0, sizeof(uint32_t), st));
+  HPS_CUDA(cudaMemsetAsync(d.ctr + kCtrOverflow, 0, sizeof(unsigned long long), st));
+}
+
+void batch_free(Batch& b) {
+  void* ptrs[] = {b.ids, b.offsets, b.lgrp, b.slot, b.keys_a, b.vals_a, b.keys_b, b.vals_b,
+                  b.heads, b.rv, b.new_slots, b.hist, b.small, b.skeys_a, b.skeys_b,
+                  b.sperm_a, b.sperm_b, b.sstart};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  Table* t = b.table;
+  int agg = b.agg;
+  b = Batch{};
+  b.table = t;
+  b.agg = agg;
+}
+
+void table_destroy(Table* t) {
+  if (!t) return;
+  {
+    DeviceGuard g(t->device);
+    cudaDeviceSynchronize();
+    batch_free(t->scratch);
+    t->stage.free_all();
+    t->prof.destroy();
+    DevTable& d = t->d;
+    void* ptrs[] = {d.keys, d.vals, d.rows, d.ver, d.tag, d.slot_id, d.special, d.hwm, d.ctr,
+                    t->d_salts};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    if (t->h_ctr) cudaFreeHost(t->h_ctr);
+  }
+  delete t;
+}
+
+void read_counters(Table* t, cudaStream_t st) {
+  HPS_CUDA(cudaMemcpyAsync(t->h_ctr, t->d.ctr, kCtrCount * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+  HPS_CUDA(cudaStreamSynchronize(st));
+}
+
+void table_counters(Table* t, hps_counters* out) {
+  DeviceGuard g(t->device);
+  HPS_CUDA(cudaDeviceSynchronize());
+  read_counters(t, nullptr);
+  uint32_t hwm = 0;
+  HPS_CUDA(cudaMemcpy(&hwm, t->d.hwm, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  memset(out, 0, sizeof(*out));
+  const unsigned long long* c = t->h_ctr;
+  out->misses = c[kCtrMisses];
+  out->clock_resets = c[kCtrClockResets];
+  out->stale_epoch_drops = c[kCtrStaleDrops];
+  out->size = std::min<uint64_t>(hwm, t->cfg.capacity);
+  out->capacity = t->cfg.capacity;
+  out->epoch = t->epoch;
+  out->max_delay = static_cast<uint32_t>(c[kCtrMaxDelay]);
+  for (int i = 0; i < 17; ++i) out->delay_hist[i] = c[kCtrDelayHist + i];
+}
+
+// Reports sticky / per-call data-dependent failures recorded on the device.
+void check_flags(Table* t, cudaStream_t st) {
+  read_counters(t, st);
+  if (t->h_ctr[kCtrOverflow])
+    throw Error(HPS_E_CONFIG,
+                "embedding table capacity exhausted (" + std::to_string(t->cfg.capacity) +
+                    " rows); device tables do not evict -- raise capacity");
+  if (t->h_ctr[kCtrDivergence])
+    throw Error(HPS_E_DIVERGENCE, "non-finite gradient contribution; nothing was applied");
+}
+
+void table_sync(Table* t) {
+  DeviceGuard g(t->device);
+  HPS_CUDA(cudaDeviceSynchronize());
+  check_flags(t, nullptr);
+}
+
+void table_reset(Table* t) {
+  DeviceGuard g(t->device);
+  HPS_CUDA(cudaDeviceSynchronize());
+  table_clear(t, nullptr);
+  HPS_CUDA(cudaDeviceSynchronize());
+  t->epoch++;
+}
+
+// ---- batch workspace --------------------------------------------------------------------
+
+void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
+  uint64_t n = std::max<uint64_t>(N, 1);
+  if (n > b.cap_N) {
+    uint64_t c = 0;
+    uint32_t** bufs[] = {&b.lgrp, &b.slot, &b.keys_a, &b.vals_a, &b.keys_b, &b.vals_b,
+                         &b.heads, &b.rv, &b.new_slots};
+    for (uint32_t** p : bufs) {
+      c = 0;
+      ensure(*p, c, n);
+    }
+    c = 0;
+    ensure(b.ids, c, n);
+    size_t hw = std::max(radix::hist_words<uint32_t>(n), radix::hist_words<uint64_t>(n));
+    c = 0;
+    ensure(b.hist, c, hw);
+    b.hist_cap = hw;
+    b.cap_N = n;
+  }
+  if (BF + 1 > b.cap_BF) {
+    uint64_t c = 0;
+    ensure(b.offsets, c, BF + 1);
+    b.cap_BF = BF + 1;
+  }
+  if (B > b.cap_B) {
+    uint64_t c = 0;
+    ensure(b.skeys_a, c, B);
+    c = 0;
+    ensure(b.skeys_b, c, B);
+    c = 0;
+    ensure(b.sperm_a, c, B);
+    c = 0;
+    ensure(b.sperm_b, c, B);
+    c = 0;
+    ensure(b.sstart, c, B + 1);
+    size_t hw = radix::hist_words<uint64_t>(B);
+    if (hw > b.hist_cap) {
+      c = 0;
+      ensure(b.hist, c, hw);
+      b.hist_cap = hw;
+    }
+    b.cap_B = B;
+  }
+  if (!b.small) {
+    uint64_t c = 0;
+    ensure(b.small, c, 8);
+  }
+}
+
+static int slot_key_bits(const Table* t) {
+  return std::max(1, bits_for(static_cast<uint64_t>(t->cfg.capacity) - 1));
+}
+
+// Sorts the staged (keys_a = slot, vals_a = listing) pairs by slot and finds the
+// segment / pair heads.
+static void sort_and_heads(Batch& b, bool direct, cudaStream_t st) {
+  Table* t = b.table;
+  bool in_b;
+  {
+    ProfScope p(t, "sort", st);
+    in_b = radix::sort_pairs<uint32_t>(b.keys_a, b.vals_a, b.keys_b, b.vals_b,
+                                       static_cast<uint32_t>(b.N), slot_key_bits(t), b.hist, st);
+  }
+  b.sorted_slot = in_b ? b.keys_b : b.keys_a;
+  b.sorted_listing = in_b ? b.vals_b : b.vals_a;
+  ProfScope p(t, "heads", st);
+  launch_heads(b.sorted_slot, b.sorted_listing, b.lgrp, b.F, b.N, direct, b.heads, b.small, st);
+}
+
+// EmbeddingWorker::register_sample for a whole batch + the route/dedup/probe half of
+// serve_pull: after this, every listing has its slot (rows lazily initialised) and the
+// listings are grouped per row in apply order.
+void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* offsets, uint32_t B,
+                    uint32_t F, const uint64_t* sample_keys, cudaStream_t st) {
+  Table* t = b.table;
+  if (N >= 0xffffffffull) throw Error(HPS_E_PRECONDITION, "batch too large (>= 2^32 listings)");
+  const uint64_t BF = static_cast<uint64_t>(B) * F;
+  if (BF >= 0xffffffffull) throw Error(HPS_E_PRECONDITION, "batch too large (B*F >= 2^32)");
+  if (F == 0) throw Error(HPS_E_PRECONDITION, "register: feature group count must be positive");
+  batch_reserve(b, N, BF, B);
+  Stager stg(t->stage);
+  const uint64_t* d_ids = static_cast<const uint64_t*>(stg.in(ids, N * sizeof(uint64_t), st));
+  if (!is_device_ptr(offsets)) {
+    if (offsets[BF] != N || offsets[0] != 0)
+      throw Error(HPS_E_PRECONDITION, "register: offsets[B*F] must equal n_ids and offsets[0] 0");
+    for (uint64_t i = 0; i < BF; ++i)
+      if (offsets[i] > offsets[i + 1])
+        throw Error(HPS_E_PRECONDITION, "register: offsets must be non-decreasing");
+  }
+  const uint32_t* d_off =
+      static_cast<const uint32_t*>(stg.in(offsets, (BF + 1) * sizeof(uint32_t), st));
+  const uint64_t* d_sk =
+      static_cast<const uint64_t*>(stg.in(sample_keys, B * sizeof(uint64_t), st));
+  // Keep our own copy of the offsets so later pull/push calls do not depend on caller
+  // buffers (ids are consumed here: everything after register works on slots).
+  HPS_CUDA(cudaMemcpyAsync(b.offsets, d_off, (BF + 1) * sizeof(uint32_t),
+                           cudaMemcpyDeviceToDevice, st));
+  b.B = B;
+  b.F = F;
+  b.N = N;
+  HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
+  launch_expand_groups(b.offsets, static_cast<uint32_t>(BF), b.lgrp, st);
+  {
+    ProfScope p(t, "probe", st);
+    launch_probe(t->d, d_ids, N, b.slot, b.new_slots, &b.small[2], st);
+  }
+  launch_lazy_init(t->d, b.new_slots, &b.small[2], N, t->sm_count, st);
+  if (d_sk && B > 1) {
+    launch_sample_order(d_sk, B, b.skeys_a, b.sperm_a, st);
+    bool in_b = radix::sort_pairs<uint64_t>(b.skeys_a, b.sperm_a, b.skeys_b, b.sperm_b, B, 64,
+                                            b.hist, st);
+    const uint32_t* perm = in_b ? b.sperm_b : b.sperm_a;
+    launch_sample_lengths(perm, b.offsets, B, F, b.sstart, st);
+    launch_scan_inplace(b.sstart, B, b.sstart + B, st);
+    launch_permuted_listing(perm, b.sstart, b.offsets, b.slot, B, F, b.keys_a, b.vals_a, st);
+  } else {
+    launch_copy_u32(b.slot, b.keys_a, N, st);
+    launch_iota(b.vals_a, N, st);
+  }
+  sort_and_heads(b, false, st);
+  b.registered = true;
+  b.pulled = false;
+  stg.finish(st);
+}
+
+void batch_pull(Batch& b, int agg, float* out_pooled, uint64_t* out_rv, cudaStream_t st) {
+  if (!b.registered) throw Error(HPS_E_STALE_SAMPLE, "pull: batch not registered");
+  Table* t = b.table;
+  const uint64_t BF = static_cast<uint64_t>(b.B) * b.F;
+  Stager stg(t->stage);
+  float* d_out = static_cast<float*>(stg.out(out_pooled, BF * t->cfg.embedding_dim * sizeof(float)));
+  uint64_t* d_rv = static_cast<uint64_t*>(stg.out(out_rv, b.N * sizeof(uint64_t)));
+  {
+    ProfScope p(t, "pool", st);
+    launch_pool(t->d, b.offsets, b.slot, static_cast<uint32_t>(BF), agg == HPS_MEAN ? 1 : 0,
+                d_out, d_rv, b.rv, st);
+  }
+  b.pulled = true;
+  stg.finish(st);
+}
+
+void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_tag,
+                uint32_t epoch, int untracked, const uint64_t* rv64, int* accepted,
+                uint32_t flags, cudaStream_t st) {
+  if (!b.registered) throw Error(HPS_E_STALE_SAMPLE, "push: batch not registered");
+  Table* t = b.table;
+  if (epoch != t->epoch) {  // PsShard::apply_gradients epoch fence, embedding_ps.hpp:142-145
+    launch_add_counter_from(t->d.ctr, kCtrStaleDrops, &b.small[1], st);
+    if (accepted) *accepted = 0;
+    return;
+  }
+  const uint64_t BF = static_cast<uint64_t>(b.B) * b.F;
+  const uint32_t D = t->cfg.embedding_dim;
+  Stager stg(t->stage);
+  const float* d_g = static_cast<const float*>(stg.in(grads, BF * D * sizeof(float), st));
+  const uint64_t* d_rv = static_cast<const uint64_t*>(stg.in(rv64, b.N * sizeof(uint64_t), st));
+  HPS_CUDA(cudaMemsetAsync(t->d.ctr + kCtrDivergence, 0, 2 * sizeof(unsigned long long), st));
+  const int mean = agg == HPS_MEAN ? 1 : 0;
+  {
+    ProfScope p(t, "check", st);
+    launch_check_batch(d_g, b.offsets, b.B, b.F, D, mean, t->d.ctr, st);
+  }
+  UpdateArgs a{};
+  a.sorted_slot = b.sorted_slot;
+  a.sorted_listing = b.sorted_listing;
+  a.heads = b.heads;
+  a.small = b.small;
+  a.n = b.N;
+  a.lgrp = b.lgrp;
+  a.offsets = b.offsets;
+  a.F = b.F;
+  a.mean = mean;
+  a.grads = d_g;
+  a.lr = lr;
+  a.step_tag = step_tag;
+  if (d_rv) {
+    a.rv64 = d_rv;
+    a.tracked = 1;
+  } else if (!untracked && b.pulled) {
+    a.rv32 = b.rv;
+    a.tracked = 1;
+  }
+  a.dry_run = 1;  // exact validation, runs only if the bound check was inconclusive
+  launch_update(t->d, a, false, t->sm_count, st);
+  a.dry_run = 0;
+  {
+    ProfScope p(t, "update", st);
+    launch_update(t->d, a, false, t->sm_count, st);
+  }
+  if (accepted) *accepted = 1;
+  if (!(flags & HPS_ASYNC)) {
+    stg.finish(st);
+    check_flags(t, st);
+  } else {
+    stg.finish(st);
+  }
+}
+
+uint64_t batch_pairs(Batch& b) {
+  if (!b.small) return 0;
+  uint32_t p = 0;
+  HPS_CUDA(cudaMemcpy(&p, b.small + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return p;
+}
+
+// ---- PS surface ------------------------------------------------------------------------
+
+void table_lookup(Table* t, const uint64_t* ids, uint64_t n, float* out_values,
+                  uint64_t* out_versions, cudaStream_t st) {
+  Batch& b = t->scratch;
+  batch_reserve(b, n, 0, 0);
+  Stager stg(t->stage);
+  const uint64_t* d_ids = static_cast<const uint64_t*>(stg.in(ids, n * sizeof(uint64_t), st));
+  float* d_out = static_cast<float*>(stg.out(out_values, n * t->cfg.embedding_dim * sizeof(float)));
+  uint64_t* d_ver = static_cast<uint64_t*>(stg.out(out_versions, n * sizeof(uint64_t)));
+  HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
+  launch_probe(t->d, d_ids, n, b.slot, b.new_slots, &b.small[2], st);
+  launch_lazy_init(t->d, b.new_slots, &b.small[2], n, t->sm_count, st);
+  launch_gather(t->d, b.slot, n, d_out, d_ver, st);
+  stg.finish(st);
+  check_flags(t, st);
+}
+
+void table_peek(Table* t, const uint64_t* ids, uint64_t n, float* out_w, float* out_acc,
+                uint64_t* out_versions, uint8_t* out_present, cudaStream_t st) {
+  const uint32_t D = t->cfg.embedding_dim;
+  Stager stg(t->stage);
+  const uint64_t* d_ids = static_cast<const uint64_t*>(stg.in(ids, n * sizeof(uint64_t), st));
+  float* w = static_cast<float*>(stg.out(out_w, n * D * sizeof(float)));
+  float* a = static_cast<float*>(stg.out(out_acc, n * D * sizeof(float)));
+  uint64_t* v = static_cast<uint64_t*>(stg.out(out_versions, n * sizeof(uint64_t)));
+  uint8_t* p = static_cast<uint8_t*>(stg.out(out_present, n));
+  launch_peek(t->d, d_ids, n, w, a, v, p, st);
+  stg.finish(st);
+}
+
+// PsShard::apply_gradients, array-shaped (embedding_ps.hpp:139-189).
+void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64_t* rv, uint64_t n,
+                 float lr, uint32_t step_tag, uint32_t epoch, uint32_t* out_delays,
+                 int* accepted, uint32_t flags, cudaStream_t st) {
+  if (epoch != t->epoch) {
+    // Host-known entry count; fold into the device counter.
+    Batch& b = t->scratch;
+    batch_reserve(b, 1, 0, 0);
+    uint32_t n32 = static_cast<uint32_t>(n);
+    HPS_CUDA(cudaMemcpyAsync(b.small + 1, &n32, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    launch_add_counter_from(t->d.ctr, kCtrStaleDrops, b.small + 1, st);
+    HPS_CUDA(cudaStreamSynchronize(st));
+    if (accepted) *accepted = 0;
+    return;
+  }
+  if (n >= 0xffffffffull) throw Error(HPS_E_PRECONDITION, "apply: too many entries");
+  Batch& b = t->scratch;
+  batch_reserve(b, n, 0, 0);
+  const uint32_t D = t->cfg.embedding_dim;
+  Stager stg(t->stage);
+  const uint64_t* d_ids = static_cast<const uint64_t*>(stg.in(ids, n * sizeof(uint64_t), st));
+  const float* d_g = static_cast<const float*>(stg.in(grads, n * D * sizeof(float), st));
+  const uint64_t* d_rv = static_cast<const uint64_t*>(stg.in(rv, n * sizeof(uint64_t), st));
+  uint32_t* d_dl = static_cast<uint32_t*>(stg.out(out_delays, n * sizeof(uint32_t)));
+  HPS_CUDA(cudaMemsetAsync(t->d.ctr + kCtrDivergence, 0, 2 * sizeof(unsigned long long), st));
+  HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
+  // Validate before anything mutates -- including lazy inserts (embedding_ps.hpp:146-156).
+  launch_check_direct(d_g, n * D, t->d.ctr, st);
+  read_counters(t, st);
+  if (t->h_ctr[kCtrDivergence]) {
+    throw Error(HPS_E_DIVERGENCE, "PsShard::apply_gradients: non-finite gradient");
+  }
+  b.N = n;
+  b.B = static_cast<uint32_t>(n);
+  b.F = 1;
+  launch_probe(t->d, d_ids, n, b.slot, b.new_slots, &b.small[2], st);
+  launch_lazy_init(t->d, b.new_slots, &b.small[2], n, t->sm_count, st);
+  launch_copy_u32(b.slot, b.keys_a, n, st);
+  launch_iota(b.vals_a, n, st);
+  sort_and_heads(b, true, st);
+  UpdateArgs a{};
+  a.sorted_slot = b.sorted_slot;
+  a.sorted_listing = b.sorted_listing;
+  a.heads = b.heads;
+  a.small = b.small;
+  a.n = n;
+  a.grads = d_g;
+  a.rv64 = d_rv;
+  a.tracked = d_rv ? 1 : 0;
+  a.out_delays = d_dl;
+  a.lr = lr;
+  a.step_tag = step_tag;
+  launch_update(t->d, a, true, t->sm_count, st);
+  b.registered = false;
+  if (accepted) *accepted = 1;
+  stg.finish(st);
+  if (!(flags & HPS_ASYNC)) check_flags(t, st);
+}
+
+void route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cudaStream_t st) {
+  StagePool pool;
+  Stager stg(pool);
+  const uint64_t* d_ids = static_cast<const uint64_t*>(stg.in(ids, n * sizeof(uint64_t), st));
+  uint32_t* d_out = static_cast<uint32_t*>(stg.out(out, n * sizeof(uint32_t)));
+  launch_route(d_ids, n, S, d_out, st);
+  stg.finish(st);
+}
+
+}  // namespace hps

@@ -1,0 +1,209 @@
+// Device-resident embedding table and per-batch plan (host-side objects).
+//
+// HBM layout of one table:
+//   keys[H]      u64  open-addressing id index, H = pow2 >= 2*capacity (load <= 0.5)
+//   vals[H]      u32  slot of keys[h] (kPending while being published)
+//   rows[C][2D]  f32  [w D | acc D] per slot -- the reference row (embedding_ps.hpp:64);
+//                     one contiguous 8D-byte segment, read-modify-written by the update
+//   ver[C]       u32  version (# distinct steps that wrote the row, embedding_ps.hpp:482)
+//   tag[C]       u32  step tag of the latest version bump (replaces the 16-deep ring)
+//   slot_id[C]   u64  id held by a slot (init seed, export)
+// Slots are handed out densely from a device high-water mark (lru_store.hpp:98).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace hps {
+
+// Device counter words (u64).
+enum CounterIdx : int {
+  kCtrMisses = 0,
+  kCtrClockResets = 1,
+  kCtrStaleDrops = 2,
+  kCtrOverflow = 3,    // sticky: capacity exhausted (no LRU eviction on device)
+  kCtrDivergence = 4,  // per-call: non-finite contribution seen by validation
+  kCtrNeedExact = 5,   // per-call: bound check inconclusive -> exact dry run
+  kCtrMaxDelay = 6,
+  kCtrDelayHist = 7,   // 17 words: delays 0..15, >=16
+  kCtrPairs = 24,      // per-call: (sample, unique id) pairs of the last push
+  kCtrCount = 32
+};
+
+struct DevTable {
+  uint64_t* keys;
+  uint32_t* vals;
+  uint64_t ht_mask;
+  int ht_shift;  // 64 - log2(H)
+  uint32_t* special;  // slot of id == kEmptyKey (kAbsent / kInserting / slot)
+  float* rows;
+  uint32_t D;
+  uint32_t stride;  // floats per row (2D)
+  uint32_t* ver;
+  uint32_t* tag;
+  uint64_t* slot_id;
+  uint32_t capacity;
+  uint32_t* hwm;
+  unsigned long long* ctr;
+  const uint64_t* salts;
+  uint32_t S;
+  int opt;
+};
+
+constexpr uint32_t kSpecialAbsent = 0xffffffffu;
+constexpr uint32_t kSpecialInserting = 0xfffffffdu;
+
+struct Table;
+
+// Reusable device + pinned bounce buffers for host-pointer arguments (table.cu).
+struct StagePool {
+  struct Buf {
+    void* dev = nullptr;
+    void* pinned = nullptr;
+    size_t dev_cap = 0, pinned_cap = 0;
+  };
+  std::vector<Buf> bufs;
+  void free_all();
+  ~StagePool() { free_all(); }
+};
+
+// Reusable device workspace for one batch (grown on demand, never shrunk).
+struct Batch {
+  Table* table = nullptr;
+  int agg = HPS_MEAN;  // EmbeddingWorkerConfig::aggregation
+  uint32_t B = 0, F = 0;
+  uint64_t N = 0;
+  uint64_t cap_N = 0, cap_BF = 0, cap_B = 0;
+  // inputs (device copies when the caller passed host memory)
+  uint64_t* ids = nullptr;        // [N]
+  uint32_t* offsets = nullptr;    // [B*F+1]
+  // derived
+  uint32_t* lgrp = nullptr;       // [N] listing -> b*F+g
+  uint32_t* slot = nullptr;       // [N] listing -> table slot
+  uint32_t* keys_a = nullptr;     // [N] sort ping-pong
+  uint32_t* vals_a = nullptr;
+  uint32_t* keys_b = nullptr;
+  uint32_t* vals_b = nullptr;
+  const uint32_t* sorted_slot = nullptr;
+  const uint32_t* sorted_listing = nullptr;
+  uint32_t* heads = nullptr;      // [N] segment heads (unordered)
+  uint32_t* rv = nullptr;         // [N] per-listing read version (u32) from the last pull
+  uint32_t* new_slots = nullptr;  // [N] rows inserted by register (lazy-init queue)
+  uint32_t* hist = nullptr;
+  size_t hist_cap = 0;
+  uint32_t* small = nullptr;      // device scalars: [0]=U, [1]=P, [2]=new_count
+  // sample-order permutation (sample_keys != NULL)
+  uint64_t* skeys_a = nullptr;
+  uint64_t* skeys_b = nullptr;
+  uint32_t* sperm_a = nullptr;
+  uint32_t* sperm_b = nullptr;
+  uint32_t* sstart = nullptr;
+  bool pulled = false;
+  bool registered = false;
+};
+
+// Optional per-region CUDA-event timing on the launching stream (hps_profile_*).
+struct Profiler {
+  bool enabled = false;
+  struct Rec {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  cudaEvent_t next();
+  void reset();
+  void destroy();
+};
+
+struct Table;
+struct ProfScope {
+  ProfScope(Table* t, const char* name, cudaStream_t st);
+  ~ProfScope();
+  Table* t;
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+};
+
+struct Table {
+  hps_table_cfg cfg{};
+  Profiler prof;
+  int device = 0;
+  DevTable d{};
+  uint64_t ht_size = 0;
+  uint64_t* d_salts = nullptr;
+  std::vector<uint64_t> salts;
+  uint32_t epoch = 0;
+  uint32_t sm_count = 148;
+  std::mutex mu;  // one call at a time per table (PsShard's per-shard lock)
+  Batch scratch;  // workspace for the stateless entry points
+  StagePool stage;
+  unsigned long long* h_ctr = nullptr;  // pinned mirror of the counters
+};
+
+// ---- kernels / launchers (kernels.cu) -------------------------------------------------
+void launch_route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cudaStream_t st);
+void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st);
+void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* slots,
+                  uint32_t* new_slots, uint32_t* new_count, cudaStream_t st);
+void launch_lazy_init(const DevTable& t, const uint32_t* new_slots, const uint32_t* new_count,
+                      uint64_t max_new, int sms, cudaStream_t st);
+void launch_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* out_values,
+                   uint64_t* out_versions, cudaStream_t st);
+void launch_peek(const DevTable& t, const uint64_t* ids, uint64_t n, float* out_w, float* out_acc,
+                 uint64_t* out_versions, uint8_t* out_present, cudaStream_t st);
+void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,
+                 int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32, cudaStream_t st);
+void launch_heads(const uint32_t* sorted_slot, const uint32_t* sorted_listing,
+                  const uint32_t* lgrp, uint32_t F, uint64_t n, bool direct, uint32_t* heads,
+                  uint32_t* small, cudaStream_t st);
+void launch_check_direct(const float* grads, uint64_t n_floats, unsigned long long* ctr,
+                         cudaStream_t st);
+void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
+                        uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st);
+
+struct UpdateArgs {
+  const uint32_t* sorted_slot;
+  const uint32_t* sorted_listing;
+  const uint32_t* heads;
+  const uint32_t* small;  // [0] = U
+  uint64_t n;             // sorted elements
+  // batch mode
+  const uint32_t* lgrp;
+  const uint32_t* offsets;
+  uint32_t F;
+  int mean;
+  // contributions: batch mode -> grads[B*F*D] fanned out; direct mode -> grads[n*D]
+  const float* grads;
+  // read versions per listing/entry (tracked); exactly one of these or none
+  const uint32_t* rv32;
+  const uint64_t* rv64;
+  uint32_t* out_delays;  // direct mode, per entry
+  float lr;
+  uint32_t step_tag;
+  int tracked;
+  int dry_run;  // compute + validate contributions only
+};
+void launch_update(const DevTable& t, const UpdateArgs& a, bool direct, int sms, cudaStream_t st);
+
+void launch_iota(uint32_t* out, uint64_t n, cudaStream_t st);
+void launch_copy_u32(const uint32_t* src, uint32_t* dst, uint64_t n, cudaStream_t st);
+void launch_sample_order(const uint64_t* sample_keys, uint32_t B, uint64_t* keys_out,
+                         uint32_t* perm_out, cudaStream_t st);
+void launch_sample_lengths(const uint32_t* perm, const uint32_t* offsets, uint32_t B, uint32_t F,
+                           uint32_t* lens, cudaStream_t st);
+void launch_scan_inplace(uint32_t* data, uint32_t n, uint32_t* total, cudaStream_t st);
+void launch_permuted_listing(const uint32_t* perm, const uint32_t* starts,
+                             const uint32_t* offsets, const uint32_t* slots, uint32_t B,
+                             uint32_t F, uint32_t* keys_out, uint32_t* vals_out, cudaStream_t st);
+void launch_add_counter_from(unsigned long long* ctr, int idx, const uint32_t* src,
+                             cudaStream_t st);
+
+}  // namespace hps

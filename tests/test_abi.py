@@ -1,0 +1,73 @@
+"""CPU checks of the drop-in boundary: libhps.so loads, exports every entry point
+include/hps_c.h declares, and the host-only functions answer without a GPU."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "hps_c.h")
+LIB = os.path.join(ROOT, "paper_2111_05897_b200", "libhps.so")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hps_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "paper_2111_05897_b200", "csrc")],
+                       check=True)
+    return ctypes.CDLL(LIB)
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ["hps_table_create", "hps_lookup", "hps_apply", "hps_batch_register",
+                 "hps_batch_pull", "hps_batch_push", "hps_pull_batch", "hps_push_batch",
+                 "hps_dedup", "hps_compress_indices", "hps_route", "hps_mix64",
+                 "hps_route_shard"]:
+        assert must in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\b(hps_[a-z0-9_]+)\b", out))
+    assert exported == set(declared_functions())
+
+
+def test_library_is_sm100a(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", LIB], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_host_side_functions(lib):
+    from paper_2111_05897_b200 import hps
+
+    assert hps.lib().hps_abi_version() == 1
+    assert hps.mix64(0) == 0xE220A8397B1DCDAF
+    assert hps.route_shard(0, 16) == 0xE220A8397B1DCDAF % 16
+    with pytest.raises(hps.PreconditionError):
+        hps.route_shard(1, 0)
+
+
+def test_oracle_libraries_export_their_abi():
+    import oracle as O
+
+    r = O.restatement_lib()
+    for n in ["orc_mix64", "orc_pull_batch", "orc_push_batch", "orc_compress_indices"]:
+        assert hasattr(r, n)
+
+
+def test_product_does_not_link_the_oracle():
+    out = subprocess.run(["ldd", LIB], capture_output=True, text=True).stdout
+    assert "oracle" not in out and "hps_ref" not in out and "hps_oracle" not in out
+    syms = subprocess.run(["nm", "-D", LIB], capture_output=True, text=True).stdout
+    assert "orc_" not in syms and "ref_" not in syms

@@ -1,0 +1,432 @@
+"""CUDA path vs the oracle / reference fixtures, through the C ABI. Needs a B200.
+
+Bar (BASELINE.json north_star): bit-exact for hashing, routing, dedup and inverse
+indices; pooled embeddings, updated rows and optimizer state are compared
+bit-exactly too (stricter than the 1e-5 relative tolerance the north star allows)
+because the kernels replicate the reference's rounding sequence.
+"""
+import numpy as np
+import pytest
+
+import golden_cases as G
+
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("oracle_built")]
+
+
+@pytest.fixture(scope="module")
+def hps():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    from paper_2111_05897_b200 import hps as H
+
+    H.lib()
+    return H
+
+
+# ---------------------------------------------------------------- reference fixtures
+
+
+@pytest.mark.parametrize("case", G.SYNC_CASES)
+def test_reference_fixture_host_buffers(hps, case):
+    G.replay_gpu(case, device_arrays=False)
+
+
+@pytest.mark.parametrize("case", G.SYNC_CASES)
+def test_reference_fixture_device_buffers(hps, case):
+    G.replay_gpu(case, device_arrays=True)
+
+
+def test_mix64_route_init_vectors(hps):
+    d = G.load("mix64_init")
+    for x, m in zip(d["x"], d["mix"]):
+        assert hps.mix64(int(x)) == int(m)
+    for j, s in enumerate(d["route_s"]):
+        got = hps.route(d["x"], int(s))
+        assert (got == d["routes"][:, j]).all()
+    for dim in (1, 4, 5, 16, 64):
+        t = hps.ShardSet(1, dim, 1024, hps.ADAGRAD, salts=[int(d["salt"])])
+        vals, ver = t.lookup(d["x"])
+        assert vals.tobytes() == d[f"init_{dim}"].tobytes()
+        assert (ver == 0).all()
+
+
+def test_route_on_device_tensors(hps):
+    import torch
+
+    from paper_2111_05897_b200 import workloads as W
+
+    ids = np.random.default_rng(0).integers(0, 2**63, 100_000, dtype=np.int64).astype(np.uint64)
+    t = torch.from_numpy(ids.view(np.int64)).cuda()
+    out = hps.route(t, 26).cpu().numpy().view(np.uint32)
+    assert (out == (W.mix64(ids) % np.uint64(26)).astype(np.uint32)).all()
+
+
+# ---------------------------------------------------------------- random sync steps vs oracle
+
+
+def _sync_vs_oracle(hps, B, F, D, S, opt, agg, steps, E=1, seed=0, max_per_group=4,
+                    id_space=60, lr=0.05, capacity=1 << 16, batches=None):
+    import oracle as O
+    from paper_2111_05897_b200 import workloads as W
+
+    rng = np.random.default_rng(seed)
+    salts = [W.mix64_int(100 + s) for s in range(S)]
+    orc = O.Restatement(salts, D, opt)
+    table = hps.ShardSet(S, D, capacity, hps.ADAGRAD if opt == "adagrad" else hps.SGD, salts=salts)
+    ew = hps.EmbeddingWorker(table, hps.MEAN if agg == "mean" else hps.SUM)
+    for step in range(steps):
+        if batches is None:
+            ids, offs = W.random_csr(rng, B, F, max_per_group, id_space)
+        else:
+            ids, offs = batches[step]
+        grads = (rng.standard_normal((B, F, D)) * 0.3).astype(np.float32)
+        i = np.arange(B, dtype=np.uint64)
+        sids = ((i % np.uint64(E)) << np.uint64(56)) | (i // np.uint64(E))
+        po, rvo = orc.pull_batch(B, F, ids, offs.astype(np.uint64), agg)
+        ew.register_batch(ids, offs, B, F, sample_keys=sids if E > 1 else None)
+        rv = np.zeros(len(ids), np.uint64)
+        pg = ew.serve_pull(out_read_versions=rv)
+        assert pg.tobytes() == po.tobytes(), f"pooled differs at step {step}"
+        assert (rv == rvo).all()
+        orc.push_batch(B, F, ids, offs.astype(np.uint64), grads, lr, step + 1, read_versions=rvo,
+                       sample_keys=sids, agg=agg)
+        assert ew.apply_backward(grads, lr, step + 1)
+    st_ids = _touched(orc)
+    w, a, v, p = table.peek(st_ids)
+    wo, ao, vo, po_ = orc.peek(st_ids)
+    assert p.all() and po_.all()
+    np.testing.assert_array_equal(w, wo)
+    np.testing.assert_array_equal(a, ao)
+    np.testing.assert_array_equal(v, vo)
+    assert table.size() == orc.counters()["size"]
+    return table, orc
+
+
+def _touched(orc):
+    # ids known to the oracle: recover via peek over the id space used by the tests
+    space = np.arange(0, 1 << 16, dtype=np.uint64)
+    _, _, _, present = orc.peek(space)
+    return space[present]
+
+
+@pytest.mark.parametrize("D", [1, 2, 3, 4, 8, 16, 32, 64, 100, 128])
+def test_sync_steps_all_dims(hps, D):
+    _sync_vs_oracle(hps, B=32, F=3, D=D, S=4, opt="adagrad", agg="mean", steps=3, seed=D)
+
+
+@pytest.mark.parametrize("opt", ["adagrad", "sgd"])
+@pytest.mark.parametrize("agg", ["mean", "sum"])
+def test_sync_steps_opt_agg(hps, opt, agg):
+    _sync_vs_oracle(hps, B=64, F=4, D=16, S=3, opt=opt, agg=agg, steps=3, seed=7)
+
+
+def test_sync_two_workers_sample_keys(hps):
+    _sync_vs_oracle(hps, B=33, F=2, D=8, S=2, opt="adagrad", agg="mean", steps=3, E=2, seed=4)
+
+
+def test_hot_rows_long_chains(hps):
+    # every row hit by hundreds of samples per step: the ordered per-row recurrence
+    _sync_vs_oracle(hps, B=2048, F=2, D=64, S=1, opt="adagrad", agg="mean", steps=2, seed=5,
+                    id_space=4, max_per_group=5)
+
+
+def test_large_ragged_batch(hps):
+    _sync_vs_oracle(hps, B=4096, F=8, D=32, S=8, opt="adagrad", agg="mean", steps=2, seed=6,
+                    id_space=50_000, max_per_group=12)
+
+
+def test_empty_and_all_empty_groups(hps):
+    B, F = 8, 3
+    ids = np.zeros(0, np.uint64)
+    offs = np.zeros(B * F + 1, np.uint32)
+    _sync_vs_oracle(hps, B=B, F=F, D=4, S=1, opt="adagrad", agg="mean", steps=1,
+                    batches=[(ids, offs)])
+
+
+# ---------------------------------------------------------------- full-size configs
+
+
+def test_c2_full_batch_one_step(hps):
+    """BASELINE configs[1] shape: 16384 x 26 one-hot over a 100M-id space, D=64, Adagrad."""
+    import oracle as O
+    from paper_2111_05897_b200 import workloads as W
+
+    cfg = W.CONFIGS["c2"]
+    b = W.make_batch(cfg, 0)
+    g = W.make_grads(cfg, b.B, 0)
+    orc = O.Restatement(cfg.salts(), cfg.dim, cfg.optimizer)
+    table = hps.ShardSet(cfg.shards, cfg.dim, 1 << 20, hps.ADAGRAD, salts=cfg.salts())
+    ew = hps.EmbeddingWorker(table, hps.MEAN)
+    off64 = b.offsets.astype(np.uint64)
+    for step in range(2):
+        po, rvo = orc.pull_batch(b.B, b.F, b.ids, off64, "mean")
+        ew.register_batch(b.ids, b.offsets, b.B, b.F)
+        pg = ew.serve_pull()
+        assert pg.tobytes() == po.tobytes()
+        orc.push_batch(b.B, b.F, b.ids, off64, g, cfg.lr, step + 1, read_versions=rvo, agg="mean")
+        ew.apply_backward(g, cfg.lr, step + 1)
+    uniq = np.unique(b.ids)
+    w, a, v, p = table.peek(uniq)
+    wo, ao, vo, _ = orc.peek(uniq)
+    assert p.all()
+    np.testing.assert_array_equal(w, wo)
+    np.testing.assert_array_equal(a, ao)
+    np.testing.assert_array_equal(v, vo)
+    assert (v == 2).all()
+
+
+def test_c3_multi_hot_zipf(hps):
+    """configs[2] stress shape at reduced batch: multi-hot (avg 50) Zipf(1.1)."""
+    from paper_2111_05897_b200 import workloads as W
+
+    cfg = W.CONFIGS["c3"]
+    b = W.make_batch(cfg, 0, batch=256)
+    assert b.N > 256 * 26 * 20
+    _sync_vs_oracle_batch(hps, cfg, b)
+
+
+def _sync_vs_oracle_batch(hps, cfg, b):
+    import oracle as O
+    from paper_2111_05897_b200 import workloads as W
+
+    g = W.make_grads(cfg, b.B, 0)
+    orc = O.Restatement(cfg.salts(), cfg.dim, cfg.optimizer)
+    table = hps.ShardSet(cfg.shards, cfg.dim, 1 << 22, hps.ADAGRAD, salts=cfg.salts())
+    ew = hps.EmbeddingWorker(table, hps.MEAN)
+    off64 = b.offsets.astype(np.uint64)
+    po, rvo = orc.pull_batch(b.B, b.F, b.ids, off64, "mean")
+    ew.register_batch(b.ids, b.offsets, b.B, b.F)
+    pg = ew.serve_pull()
+    assert pg.tobytes() == po.tobytes()
+    orc.push_batch(b.B, b.F, b.ids, off64, g, cfg.lr, 1, read_versions=rvo, agg="mean")
+    ew.apply_backward(g, cfg.lr, 1)
+    uniq = np.unique(b.ids)
+    w, a, v, _ = table.peek(uniq)
+    wo, ao, vo, _ = orc.peek(uniq)
+    np.testing.assert_array_equal(w, wo)
+    np.testing.assert_array_equal(a, ao)
+    np.testing.assert_array_equal(v, vo)
+
+
+# ---------------------------------------------------------------- PS surface
+
+
+def test_direct_apply_delays_and_versions(hps):
+    import oracle as O
+
+    D = 3
+    t = hps.ShardSet(1, D, 64, hps.ADAGRAD, salts=[5])
+    orc = O.Restatement([5], D, "adagrad")
+    rng = np.random.default_rng(2)
+    ids = np.array([1, 2, 1, 3, 1, 2], np.uint64)
+    t.lookup(ids)
+    orc.lookup(ids)
+    for step, shift in [(1, 0), (2, 0), (3, 1), (5, 0), (6, 2), (6, 0), (9, 3)]:
+        g = rng.standard_normal((len(ids), D)).astype(np.float32)
+        _, vg = t.lookup(ids)
+        _, vo = orc.lookup(ids)
+        assert (vg == vo).all()
+        rv = np.maximum(vo.astype(np.int64) - shift, 0).astype(np.uint64)
+        okg, dg = t.apply_gradients(ids, g, rv, 0.1, step)
+        oko, do = orc.apply(ids, g, rv, 0.1, step)
+        assert okg and oko
+        assert (dg == do).all(), (step, dg, do)
+    keys = np.array([1, 2, 3], np.uint64)
+    w, a, v, _ = t.peek(keys)
+    wo, ao, vo, _ = orc.peek(keys)
+    np.testing.assert_array_equal(w, wo)
+    np.testing.assert_array_equal(a, ao)
+    np.testing.assert_array_equal(v, vo)
+
+
+def test_reference_staleness_cases(hps):
+    # test_embedding_ps.cpp:171-211 restated through the C ABI.
+    t = hps.ShardSet(1, 2, 16, hps.ADAGRAD, salts=[11])
+
+    def one(id_, step, rv):
+        ok, d = t.apply_gradients([id_], np.ones((1, 2), np.float32), [rv], 0.01, step)
+        assert ok
+        return int(d[0])
+
+    _, v = t.lookup([8])
+    assert one(8, 1, int(v[0])) == 0
+    t2 = hps.ShardSet(1, 2, 16, hps.ADAGRAD, salts=[11])
+    _, rv = t2.lookup([8])
+    ok, _ = t2.apply_gradients([8], np.ones((1, 2), np.float32), rv, 0.01, 1)
+    t2.apply_gradients([8], np.ones((1, 2), np.float32), [1], 0.01, 2)
+    _, d = t2.apply_gradients([8], np.ones((1, 2), np.float32), rv, 0.01, 3)
+    assert d[0] == 2
+    t3 = hps.ShardSet(1, 2, 16, hps.ADAGRAD, salts=[11])
+    _, rv = t3.lookup([8])
+    t3.apply_gradients([8], np.ones((1, 2), np.float32), rv, 0.01, 1)
+    _, rv = t3.lookup([8])
+    assert t3.apply_gradients([8], np.ones((1, 2), np.float32), rv, 0.01, 2)[1][0] == 0
+    assert t3.apply_gradients([8], np.ones((1, 2), np.float32), rv, 0.01, 2)[1][0] == 0
+    t4 = hps.ShardSet(1, 2, 16, hps.ADAGRAD, salts=[11])
+    _, rv = t4.lookup([8])
+    t4.apply_gradients([8], np.ones((1, 2), np.float32), rv, 0.01, 7)
+    assert t4.apply_gradients([8], np.ones((1, 2), np.float32), rv, 0.01, 6)[1][0] == 0
+
+
+def test_sgd_and_adagrad_arithmetic(hps):
+    # test_embedding_ps.cpp:87-109
+    t = hps.ShardSet(1, 2, 16, hps.SGD, salts=[11])
+    cur = t.lookup_map([7])[7]
+    t.apply_gradients_map({7: cur - np.array([1.0, 1.0], np.float32)}, 1.0)
+    w = t.lookup_map([7])[7]
+    t.apply_gradients_map({7: [2.0, 4.0]}, 0.5)
+    got = t.lookup_map([7])[7]
+    assert got[0] == np.float32(w[0] - np.float32(0.5) * np.float32(2.0))
+    assert got[1] == np.float32(w[1] - np.float32(0.5) * np.float32(4.0))
+    a = hps.ShardSet(1, 1, 16, hps.ADAGRAD, salts=[11])
+    w0 = a.lookup_map([5])[5][0]
+    a.apply_gradients_map({5: [3.0]}, 0.1)
+    expect = np.float32(w0 - np.float32(np.float32(0.1) * np.float32(3.0)) /
+                        np.float32(np.float32(3.0) + np.float32(1e-10)))
+    assert a.lookup_map([5])[5][0] == expect
+
+
+def test_non_finite_rejected_atomically(hps):
+    t = hps.ShardSet(1, 2, 16, hps.ADAGRAD, salts=[11])
+    before = t.lookup([1, 2])[0].copy()
+    size = t.size()
+    g = np.array([[1, 1], [1, np.nan]], np.float32)
+    with pytest.raises(hps.DivergenceError):
+        t.apply_gradients([1, 2], g, [0, 0], 0.1, 1)
+    assert t.lookup([1, 2])[0].tobytes() == before.tobytes()
+    with pytest.raises(hps.DivergenceError):
+        t.apply_gradients_map({3: [np.inf, 0.0]}, 0.1)
+    assert t.size() == size  # the rejected call did not even insert id 3
+    # batch surface: a NaN in any non-empty group rejects the whole batch
+    ew = hps.EmbeddingWorker(t, hps.MEAN)
+    ids = np.array([1, 2, 1], np.uint64)
+    offs = np.array([0, 2, 3], np.uint32)
+    ew.register_batch(ids, offs, 1, 2)
+    ew.serve_pull()
+    snap = t.peek([1, 2])
+    gb = np.ones((1, 2, 2), np.float32)
+    gb[0, 1, 0] = np.inf
+    with pytest.raises(hps.DivergenceError):
+        ew.apply_backward(gb, 0.1, 1)
+    after = t.peek([1, 2])
+    assert snap[0].tobytes() == after[0].tobytes() and snap[1].tobytes() == after[1].tobytes()
+    # NaN in an EMPTY group is never used, so it is not an error (push_to_shards :731)
+    ids = np.array([1], np.uint64)
+    offs = np.array([0, 1, 1], np.uint32)
+    ew.register_batch(ids, offs, 1, 2)
+    ew.serve_pull()
+    gb = np.ones((1, 2, 2), np.float32)
+    gb[0, 1, :] = np.nan
+    assert ew.apply_backward(gb, 0.1, 2)
+
+
+def test_overflowing_contribution_rejected(hps):
+    # finite gradients whose fp64 chain-rule sum overflows float -> non-finite push value
+    t = hps.ShardSet(1, 1, 16, hps.SGD, salts=[1])
+    ew = hps.EmbeddingWorker(t, hps.SUM)
+    ids = np.array([4, 4], np.uint64)
+    offs = np.array([0, 1, 2], np.uint32)
+    ew.register_batch(ids, offs, 1, 2)
+    ew.serve_pull()
+    before = t.peek([4])[0].copy()
+    g = np.full((1, 2, 1), 3.0e38, np.float32)
+    with pytest.raises(hps.DivergenceError):
+        ew.apply_backward(g, 0.1, 1)
+    assert t.peek([4])[0].tobytes() == before.tobytes()
+
+
+def test_stale_epoch_drops_whole_call(hps):
+    t = hps.ShardSet(1, 2, 16, hps.ADAGRAD, salts=[11])
+    before = t.lookup([4])[0].copy()
+    ok, _ = t.apply_gradients([4], np.ones((1, 2), np.float32), [0], 0.1, 1,
+                              caller_epoch=t.epoch() + 1)
+    assert not ok
+    assert t.stale_epoch_drops() == 1
+    assert t.lookup([4])[0].tobytes() == before.tobytes()
+    t.advance_epoch()
+    ok, _ = t.apply_gradients([4], np.ones((1, 2), np.float32), [0], 0.1, 1)
+    assert ok
+
+
+def test_capacity_exhaustion_is_reported(hps):
+    t = hps.ShardSet(1, 4, 8, hps.ADAGRAD, salts=[1])
+    t.lookup(np.arange(8, dtype=np.uint64))
+    with pytest.raises(hps.ConfigError):
+        t.lookup(np.arange(8, 20, dtype=np.uint64))
+
+
+def test_reset_for_recovery(hps):
+    t = hps.ShardSet(1, 4, 64, hps.ADAGRAD, salts=[1])
+    a, _ = t.lookup([1, 2, 3])
+    t.apply_gradients_map({1: [1, 1, 1, 1]}, 0.5)
+    e = t.epoch()
+    t.reset_for_recovery()
+    assert t.epoch() == e + 1
+    assert t.size() == 0
+    b, v = t.lookup([1, 2, 3])
+    assert a.tobytes() == b.tobytes() and (v == 0).all()
+
+
+def test_special_all_ones_id(hps):
+    import oracle as O
+
+    t = hps.ShardSet(2, 4, 64, hps.ADAGRAD, salts=[3, 4])
+    orc = O.Restatement([3, 4], 4, "adagrad")
+    ids = np.array([2**64 - 1, 0, 2**64 - 1], np.uint64)
+    g, _ = t.lookup(ids)
+    o, _ = orc.lookup(ids)
+    assert g.tobytes() == o.tobytes()
+
+
+# ---------------------------------------------------------------- dedup
+
+
+@pytest.mark.parametrize("n,space", [(1, 10), (1000, 10), (100_000, 2**63), (300_000, 5000)])
+def test_dedup_unique_inverse(hps, n, space):
+    rng = np.random.default_rng(n)
+    ids = rng.integers(0, space, n, dtype=np.int64).astype(np.uint64)
+    if n > 10:
+        ids[:3] = [2**64 - 1, 0, 2**64 - 1]
+    u, inv = hps.dedup(ids)
+    nu, ninv = np.unique(ids, return_inverse=True)
+    assert (u == nu).all()
+    assert (inv.astype(np.int64) == ninv).all()
+
+
+def test_dedup_device_tensors(hps):
+    import torch
+
+    ids = torch.randint(0, 1000, (50_000,), device="cuda")
+    u, inv = hps.dedup(ids)
+    nu, ninv = np.unique(ids.cpu().numpy().view(np.uint64), return_inverse=True)
+    assert (u.cpu().numpy().view(np.uint64) == nu).all()
+    assert (inv.cpu().numpy().astype(np.int64) == ninv).all()
+
+
+def test_compress_indices_fixture(hps):
+    d = G.load("compress_indices")
+    res = hps.compress_indices(d["ids"], d["offsets"], int(d["B"]), int(d["G"]))
+    for g, (u, posts) in enumerate(res):
+        assert (u == d[f"unique_{g}"]).all()
+        assert [len(p) for p in posts] == list(d[f"post_len_{g}"])
+        flat = np.concatenate(posts) if posts else np.zeros(0, np.uint16)
+        assert (flat == d[f"postings_{g}"]).all()
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_compress_indices_vs_oracle_random(hps, seed):
+    import oracle as O
+    from paper_2111_05897_b200 import workloads as W
+
+    rng = np.random.default_rng(seed)
+    B, G_ = 3000, 5
+    ids, offs = W.random_csr(rng, B, G_, 6, 2000, empty_prob=0.2, dup_prob=0.5)
+    a = hps.compress_indices(ids, offs, B, G_)
+    b = O.compress_indices(B, G_, ids, offs.astype(np.uint64))
+    for (ua, pa), (ub, pb) in zip(a, b):
+        assert (ua == ub).all()
+        assert all((x == y).all() for x, y in zip(pa, pb))
+    with pytest.raises(hps.PreconditionError):
+        hps.compress_indices(np.zeros(0, np.uint64), np.zeros(65537, np.uint32), 65536, 1)
