@@ -304,7 +304,7 @@ def main():
         it += 1
     torch.cuda.synchronize()
     regions = {}
-    for r in ("probe", "sort", "heads", "pool", "check", "update"):
+    for r in ("probe", "sort", "pool", "check", "update"):
         tot, cnt = table.profile_get(r)
         regions[r] = (tot / max(cnt, 1), cnt)
     table.profile(False)

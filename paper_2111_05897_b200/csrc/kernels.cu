@@ -1,9 +1,10 @@
-// Hot-path kernels for the embedding lookup+update path (sm_100a).
+// Hot-path kernels except the ordered update (update.cu) and the radix sort
+// (radix_sort.cuh): routing, CSR expansion, id-index probe with lazy insert, lazy
+// init, gather / peek, fp64 pooling and the pre-mutation validation.
 //
-// Every kernel is HBM-bound integer/byte or fp32/fp64 streaming work; nothing is a
-// dense contraction, so there are no tensor cores here. Rows are
-// moved with 128-bit vector loads by "row groups" of L lanes x V floats (L*V = D),
-// grids are sized in multiples of the SM count and loop grid-stride.
+// Everything here is HBM-bound integer/byte or fp32/fp64 streaming work; nothing is a
+// dense contraction, so there are no tensor cores. Rows move as
+// 128-bit vectors by "row groups" of L lanes x V floats (vec.cuh).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -14,17 +15,13 @@
 #include "common.cuh"
 #include "radix_sort.cuh"
 #include "table.cuh"
+#include "vec.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace hps {
 
 namespace {
-
-template <typename T>
-__device__ __forceinline__ T ld_volatile(const T* p) {
-  return *const_cast<const volatile T*>(p);
-}
 
 // Warp-aggregated atomicAdd on a u32 counter (one atomic per coalesced group).
 __device__ __forceinline__ uint32_t agg_inc(uint32_t* ctr) {
@@ -51,9 +48,9 @@ __device__ uint32_t alloc_slot(const DevTable& t, uint64_t id, uint32_t* new_slo
 }
 
 // id -> slot with lazy insert (PsShard::find_or_init embedding_ps.hpp:417-434; the
-// LruStore index lru_store.hpp:62-113). Linear probing on an open-addressing table
-// of u64 keys; the inserting thread publishes the slot, racing readers of the same
-// id spin on the (at most one in flight) publication.
+// LruStore index lru_store.hpp:62-113). Linear probing over 16-byte {key, slot}
+// entries; the inserting thread publishes the slot, racing readers of the same id
+// spin on that (single, in-flight) publication.
 __device__ uint32_t find_or_insert(const DevTable& t, uint64_t id, uint32_t* new_slots,
                                    uint32_t* new_count, bool insert) {
   if (id == kEmptyKey) {
@@ -73,24 +70,26 @@ __device__ uint32_t find_or_insert(const DevTable& t, uint64_t id, uint32_t* new
   }
   uint64_t h = mix64(id ^ kTableHashSalt) >> t.ht_shift;
   for (uint64_t probes = 0; probes <= t.ht_mask; ++probes) {
-    uint64_t k = ld_volatile(&t.keys[h]);
+    HashEntry* e = &t.ht[h];
+    // one 16-byte load brings key and slot together
+    unsigned long long k, sv;
+    asm volatile("ld.volatile.v2.u64 {%0, %1}, [%2];" : "=l"(k), "=l"(sv) : "l"(e));
     if (k == kEmptyKey) {
       if (!insert) return kPending;
-      unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long*>(&t.keys[h]),
-                                         static_cast<unsigned long long>(kEmptyKey),
+      unsigned long long old = atomicCAS(&e->key, static_cast<unsigned long long>(kEmptyKey),
                                          static_cast<unsigned long long>(id));
       if (old == kEmptyKey) {
         uint32_t slot = alloc_slot(t, id, new_slots, new_count);
         __threadfence();
-        atomicExch(&t.vals[h], slot);
+        atomicExch(&e->slot, slot);
         return slot;
       }
       k = old;
+      sv = kPending;
     }
     if (k == id) {
-      uint32_t v;
-      while ((v = ld_volatile(&t.vals[h])) == kPending) {
-      }
+      uint32_t v = static_cast<uint32_t>(sv);
+      while (v == kPending) v = ld_volatile(&e->slot);
       return v;
     }
     h = (h + 1) & t.ht_mask;
@@ -98,86 +97,6 @@ __device__ uint32_t find_or_insert(const DevTable& t, uint64_t id, uint32_t* new
   atomicExch(&t.ctr[kCtrOverflow], 1ull);
   return kInvalidSlot;
 }
-
-__device__ __forceinline__ bool slot_ok(const DevTable& t, uint32_t s) { return s < t.capacity; }
-
-// ---- vector helpers for row groups -----------------------------------------------------
-
-template <int V>
-struct VecT;
-template <>
-struct VecT<1> {
-  using T = float;
-};
-template <>
-struct VecT<2> {
-  using T = float2;
-};
-template <>
-struct VecT<4> {
-  using T = float4;
-};
-
-template <int V>
-__device__ __forceinline__ void load_vec(const float* p, float (&v)[V]) {
-  if constexpr (V == 4) {
-    float4 x = *reinterpret_cast<const float4*>(p);
-    v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
-  } else if constexpr (V == 2) {
-    float2 x = *reinterpret_cast<const float2*>(p);
-    v[0] = x.x, v[1] = x.y;
-  } else {
-    v[0] = *p;
-  }
-}
-
-template <int V>
-__device__ __forceinline__ void load_vec_stream(const float* p, float (&v)[V]) {
-  if constexpr (V == 4) {
-    float4 x = __ldcs(reinterpret_cast<const float4*>(p));
-    v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
-  } else if constexpr (V == 2) {
-    float2 x = __ldcs(reinterpret_cast<const float2*>(p));
-    v[0] = x.x, v[1] = x.y;
-  } else {
-    v[0] = __ldcs(p);
-  }
-}
-
-template <int V>
-__device__ __forceinline__ void store_vec(float* p, const float (&v)[V]) {
-  if constexpr (V == 4) {
-    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-  } else if constexpr (V == 2) {
-    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
-  } else {
-    *p = v[0];
-  }
-}
-
-template <int V>
-__device__ __forceinline__ void store_vec_stream(float* p, const float (&v)[V]) {
-  if constexpr (V == 4) {
-    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
-  } else if constexpr (V == 2) {
-    __stcs(reinterpret_cast<float2*>(p), make_float2(v[0], v[1]));
-  } else {
-    __stcs(p, v[0]);
-  }
-}
-
-// Row-group geometry: L lanes x V floats cover kSpan = L*V dims per chunk; a row of D
-// dims takes ceil(D / kSpan) chunks (1 on the specialised paths). kGuard enables the
-// d < D bounds check of the generic path.
-template <int V, int L, bool kGuard>
-struct Geo {
-  static constexpr int kSpan = V * L;
-  __device__ static int lane() { return threadIdx.x % L; }
-  __device__ static uint64_t group() {
-    return (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
-  }
-  __device__ static uint64_t groups() { return static_cast<uint64_t>(gridDim.x) * blockDim.x / L; }
-};
 
 }  // namespace
 
@@ -209,26 +128,36 @@ __global__ void expand_groups_kernel(const uint32_t* __restrict__ offsets, uint3
 
 void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st) {
   if (!BF) return;
-  expand_groups_kernel<<<std::min<uint64_t>(ceil_div(BF, 256), 148 * 16), 256, 0, st>>>(offsets, BF,
-                                                                                    lgrp);
+  expand_groups_kernel<<<std::min<uint64_t>(ceil_div(BF, 256), 148 * 16), 256, 0, st>>>(
+      offsets, BF, lgrp);
   HPS_LAUNCH_CHECK();
 }
 
 // ---- probe / lazy insert ------------------------------------------------------------------
 
-__global__ void probe_kernel(DevTable t, const uint64_t* __restrict__ ids, uint64_t n,
-                             uint32_t* __restrict__ slots, uint32_t* __restrict__ new_slots,
-                             uint32_t* __restrict__ new_count) {
+__global__ void __launch_bounds__(256)
+    probe_kernel(DevTable t, const uint64_t* __restrict__ ids, uint64_t n,
+                 uint32_t* __restrict__ slots, uint32_t* __restrict__ sort_keys,
+                 uint32_t* __restrict__ sort_vals, uint32_t* __restrict__ new_slots,
+                 uint32_t* __restrict__ new_count, const unsigned long long* gate) {
+  if (gate && ld_volatile(gate)) return;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    slots[i] = find_or_insert(t, ids[i], new_slots, new_count, true);
+    uint32_t s = find_or_insert(t, ids[i], new_slots, new_count, true);
+    slots[i] = s;
+    if (sort_keys) {
+      sort_keys[i] = s;
+      sort_vals[i] = static_cast<uint32_t>(i);
+    }
   }
 }
 
 void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* slots,
-                  uint32_t* new_slots, uint32_t* new_count, cudaStream_t st) {
+                  uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
+                  uint32_t* new_count, const unsigned long long* gate, cudaStream_t st) {
   if (!n) return;
-  probe_kernel<<<ceil_div(n, 256), 256, 0, st>>>(t, ids, n, slots, new_slots, new_count);
+  probe_kernel<<<ceil_div(n, 256), 256, 0, st>>>(t, ids, n, slots, sort_keys, sort_vals,
+                                                 new_slots, new_count, gate);
   HPS_LAUNCH_CHECK();
 }
 
@@ -287,7 +216,7 @@ void launch_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* 
                    uint64_t* out_ver, cudaStream_t st) {
   if (!n) return;
   gather_kernel<<<std::min<uint64_t>(ceil_div(n, 8), 148 * 32), 256, 0, st>>>(t, slots, n, out,
-                                                                          out_ver);
+                                                                               out_ver);
   HPS_LAUNCH_CHECK();
 }
 
@@ -316,8 +245,8 @@ __global__ void peek_kernel(DevTable t, const uint64_t* __restrict__ ids, uint64
 void launch_peek(const DevTable& t, const uint64_t* ids, uint64_t n, float* out_w, float* out_acc,
                  uint64_t* out_ver, uint8_t* out_present, cudaStream_t st) {
   if (!n) return;
-  peek_kernel<<<std::min<uint64_t>(ceil_div(n, 8), 148 * 32), 256, 0, st>>>(t, ids, n, out_w, out_acc,
-                                                                        out_ver, out_present);
+  peek_kernel<<<std::min<uint64_t>(ceil_div(n, 8), 148 * 32), 256, 0, st>>>(
+      t, ids, n, out_w, out_acc, out_ver, out_present);
   HPS_LAUNCH_CHECK();
 }
 
@@ -339,7 +268,8 @@ __global__ void __launch_bounds__(256)
   const int chunks = kGuard ? (D + G::kSpan - 1) / G::kSpan : 1;
   for (uint64_t sg = G::group(); sg < BF; sg += G::groups()) {
     const uint32_t a = offsets[sg], e = offsets[sg + 1];
-    const double scale = mean ? __drcp_rn(static_cast<double>(e - a)) : 1.0;
+    // Empty groups pool to zeros (embedding_worker.hpp:543): keep scale finite there.
+    const double scale = (mean && e > a) ? __drcp_rn(static_cast<double>(e - a)) : 1.0;
     for (int c = 0; c < chunks; ++c) {
       const uint32_t d0 = c * G::kSpan + ln * V;
       if (kGuard && d0 >= D) break;
@@ -387,65 +317,21 @@ __global__ void __launch_bounds__(256)
         for (int k = 0; k < V; ++k)
           if (d0 + k < D) dst[k] = o[k];
       } else {
-        store_vec_stream<V>(dst, o);
+        store_vec_cs<V>(dst, o);
       }
     }
   }
 }
-
-// Dispatch on embedding dim: 128-bit row groups where D allows, else the generic
-// one-float-per-lane path.
-#define HPS_DISPATCH_DIM(D, ...)                      \
-  do {                                                        \
-    switch (D) {                                              \
-      case 1: { constexpr int V = 1, L = 1; constexpr bool G = false; __VA_ARGS__; } break;   \
-      case 2: { constexpr int V = 2, L = 1; constexpr bool G = false; __VA_ARGS__; } break;   \
-      case 4: { constexpr int V = 4, L = 1; constexpr bool G = false; __VA_ARGS__; } break;   \
-      case 8: { constexpr int V = 4, L = 2; constexpr bool G = false; __VA_ARGS__; } break;   \
-      case 16: { constexpr int V = 4, L = 4; constexpr bool G = false; __VA_ARGS__; } break;  \
-      case 32: { constexpr int V = 4, L = 8; constexpr bool G = false; __VA_ARGS__; } break;  \
-      case 64: { constexpr int V = 4, L = 16; constexpr bool G = false; __VA_ARGS__; } break; \
-      case 128: { constexpr int V = 4, L = 32; constexpr bool G = false; __VA_ARGS__; } break; \
-      default: { constexpr int V = 1, L = 32; constexpr bool G = true; __VA_ARGS__; } break;  \
-    }                                                         \
-  } while (0)
 
 void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,
                  int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32, cudaStream_t st) {
   if (!BF) return;
   HPS_DISPATCH_DIM(t.D, {
     uint64_t groups_per_block = 256 / L;
-    uint32_t blocks = std::min<uint64_t>(ceil_div(BF, groups_per_block), 148ull * 16);
+    uint32_t blocks = std::min<uint64_t>(ceil_div(BF, groups_per_block), 148ull * 32);
     pool_kernel<V, L, G><<<blocks, 256, 0, st>>>(t, offsets, slots, BF, mean, out, out_rv64,
                                                  out_rv32);
   });
-  HPS_LAUNCH_CHECK();
-}
-
-// ---- segment heads over the slot-sorted listings -----------------------------------------
-// head: first element of a slot's run (one unique row); pair head: first element of
-// a (slot, sample) run -- one optimizer application per (sample, unique id).
-
-__global__ void heads_kernel(const uint32_t* __restrict__ ss, const uint32_t* __restrict__ sl,
-                             const uint32_t* __restrict__ lgrp, uint32_t F, uint64_t n,
-                             bool direct, uint32_t* __restrict__ heads,
-                             uint32_t* __restrict__ small) {
-  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
-       p += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t s = ss[p];
-    bool head = p == 0 || ss[p - 1] != s;
-    bool pair = head || direct;
-    if (!pair) pair = lgrp[sl[p]] / F != lgrp[sl[p - 1]] / F;
-    if (head) heads[agg_inc(&small[0])] = static_cast<uint32_t>(p);
-    if (pair) agg_inc(&small[1]);
-  }
-}
-
-void launch_heads(const uint32_t* ss, const uint32_t* sl, const uint32_t* lgrp, uint32_t F,
-                  uint64_t n, bool direct, uint32_t* heads, uint32_t* small, cudaStream_t st) {
-  if (!n) return;
-  heads_kernel<<<std::min<uint64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st>>>(ss, sl, lgrp, F, n,
-                                                                          direct, heads, small);
   HPS_LAUNCH_CHECK();
 }
 
@@ -463,217 +349,65 @@ __global__ void check_direct_kernel(const float* __restrict__ g, uint64_t n,
 void launch_check_direct(const float* grads, uint64_t n, unsigned long long* ctr,
                          cudaStream_t st) {
   if (!n) return;
-  check_direct_kernel<<<std::min<uint64_t>(ceil_div(n, 256), 148 * 8), 256, 0, st>>>(grads, n, ctr);
+  check_direct_kernel<<<std::min<uint64_t>(ceil_div(n, 256), 148 * 8), 256, 0, st>>>(grads, n,
+                                                                                      ctr);
   HPS_LAUNCH_CHECK();
 }
 
-// Batch validation: every gradient of a non-empty group feeds some contribution, so
-// a non-finite one is a certain rejection. Finite gradients can still overflow a
-// contribution in the float narrowing; per sample, |c| <= sum_g |grad_g|_inf * (n_g
-// for sum, 1 for mean), and only when that bound reaches 2^127 is the exact dry run
-// of the update kernel requested.
-__global__ void check_batch_kernel(const float* __restrict__ grads,
-                                   const uint32_t* __restrict__ offsets, uint32_t B, uint32_t F,
-                                   uint32_t D, int mean, unsigned long long* ctr) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  bool bad = false, exact = false;
-  for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; b < B; b += warps) {
-    double bound = 0.0;
-    for (uint32_t g = 0; g < F; ++g) {
-      uint32_t n = offsets[b * F + g + 1] - offsets[b * F + g];
-      if (!n) continue;
-      const float* gr = grads + (b * F + g) * (uint64_t)D;
-      float m = 0.0f;
-      for (uint32_t d = lane; d < D; d += 32) {
-        float x = __ldcs(gr + d);
-        bad |= !isfinite(x);
-        m = fmaxf(m, fabsf(x));
-      }
+// Batch validation. Every gradient of a non-empty group feeds some contribution, so a
+// non-finite one is a certain rejection. Finite gradients can still overflow in the
+// float narrowing of a contribution: |c| <= sum_g n_g*scale_g*|grad_g|_inf
+// <= F * max_g(n_g*scale_g*|grad_g|_inf); only when that bound reaches 2^127 is the
+// exact dry run of the update kernel requested. One flat, 128-bit-vectorised pass.
+template <int V>
+__global__ void __launch_bounds__(256)
+    check_batch_kernel(const float* __restrict__ grads, const uint32_t* __restrict__ offsets,
+                       uint64_t n_vec, uint32_t D, uint32_t F, int mean,
+                       unsigned long long* ctr) {
+  bool bad = false;
+  float m = 0.0f;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n_vec;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = k * V;
+    const uint64_t bg = e / D;
+    const uint32_t n = __ldg(offsets + bg + 1) - __ldg(offsets + bg);
+    float x[V];
+    load_vec_cs<V>(grads + e, x);
+    if (n) {
+      float mm = 0.0f;
 #pragma unroll
-      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      bound += static_cast<double>(m) * (mean ? 1.0 : static_cast<double>(n));
+      for (int j = 0; j < V; ++j) {
+        bad |= !isfinite(x[j]);
+        mm = fmaxf(mm, fabsf(x[j]));
+      }
+      m = fmaxf(m, mean ? mm : mm * static_cast<float>(n));
     }
-    exact |= bound >= 0x1.0p127;
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   bad = __syncthreads_or(bad);
-  exact = __syncthreads_or(exact);
+  __shared__ float s_m[8];
+  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
+  __syncthreads();
   if (threadIdx.x == 0) {
+    float bm = 0.0f;
+    for (int w = 0; w < 8; ++w) bm = fmaxf(bm, s_m[w]);
     if (bad) atomicExch(&ctr[kCtrDivergence], 1ull);
-    if (exact) atomicExch(&ctr[kCtrNeedExact], 1ull);
+    if (static_cast<double>(bm) * F >= 0x1.0p127) atomicExch(&ctr[kCtrNeedExact], 1ull);
   }
 }
 
 void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
                         uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st) {
-  if (!B) return;
-  check_batch_kernel<<<std::min<uint64_t>(ceil_div(B, 8), 148 * 8), 256, 0, st>>>(grads, offsets, B,
-                                                                             F, D, mean, ctr);
-  HPS_LAUNCH_CHECK();
-}
-
-// ---- ordered fused optimizer update ------------------------------------------------------
-// One row group per unique row (a slot run of the slot-sorted listings). The group
-// walks the run in apply order; consecutive listings of one sample form one pair
-// whose contribution is the fp64 chain-rule sum (push_to_shards :728-743, product
-// rounded then added), narrowed to float and applied once (apply_one
-// embedding_ps.hpp:436-449, each op individually rounded). The row [w | acc] stays in
-// registers across the whole run and is written back once. Versions / delays follow
-// count_delay + bump_version (embedding_ps.hpp:454-488) with the latest bump tag
-// standing in for the 16-deep ring (exact when steps apply in order, which the
-// stream-ordered pipeline guarantees).
-template <int V, int L, bool kGuard, bool kDirect>
-__global__ void __launch_bounds__(256)
-    update_kernel(DevTable t, UpdateArgs a) {
-  using G = Geo<V, L, kGuard>;
-  __shared__ unsigned long long s_hist[17];
-  __shared__ unsigned int s_resets, s_max;
-  if (threadIdx.x < 17) s_hist[threadIdx.x] = 0;
-  if (threadIdx.x == 0) s_resets = 0, s_max = 0;
-  __syncthreads();
-  const bool gated = ld_volatile(&t.ctr[kCtrDivergence]) | ld_volatile(&t.ctr[kCtrOverflow]) |
-                     (a.dry_run ? !ld_volatile(&t.ctr[kCtrNeedExact]) : 0ull);
-  const int ln = G::lane();
-  const uint32_t D = t.D;
-  const int chunks = kGuard ? (D + G::kSpan - 1) / G::kSpan : 1;
-  const uint32_t U = gated ? 0u : a.small[0];
-  const bool adagrad = t.opt == HPS_ADAGRAD;
-  bool bad = false;
-  for (uint64_t u = G::group(); u < U; u += G::groups()) {
-    const uint32_t p0 = a.heads[u];
-    const uint32_t slot = a.sorted_slot[p0];
-    if (!slot_ok(t, slot)) continue;
-    float* row = t.rows + static_cast<uint64_t>(slot) * t.stride;
-    for (int c = 0; c < chunks; ++c) {
-      const uint32_t d0 = c * G::kSpan + ln * V;
-      const bool dims_ok = !kGuard || d0 < D;
-      float w[V], acc[V];
-      if (dims_ok && !a.dry_run) {
-        load_vec<V>(row + d0, w);
-        if (adagrad) load_vec<V>(row + D + d0, acc);
-      }
-      uint32_t ver = t.ver[slot], tag = t.tag[slot];
-      uint64_t p = p0;
-      while (p < a.n && a.sorted_slot[p] == slot) {
-        float cval[V];
-        uint64_t rv = 0;
-        uint32_t entry = a.sorted_listing[p];
-        if constexpr (kDirect) {
-          if (dims_ok) {
-            if (kGuard) cval[0] = a.grads[(uint64_t)entry * D + d0];
-            else load_vec<V>(a.grads + (uint64_t)entry * D + d0, cval);
-          }
-          if (a.tracked) rv = a.rv64 ? a.rv64[entry] : a.rv32[entry];
-          ++p;
-        } else {
-          if (a.tracked) rv = a.rv32 ? a.rv32[entry] : a.rv64[entry];
-          uint32_t lg = a.lgrp[entry];
-          const uint32_t b = lg / a.F;
-          double sum[V];
-#pragma unroll
-          for (int k = 0; k < V; ++k) sum[k] = 0.0;
-          while (true) {
-            const double scale =
-                a.mean ? __drcp_rn(static_cast<double>(a.offsets[lg + 1] - a.offsets[lg])) : 1.0;
-            if (dims_ok) {
-              float gv[V];
-              if (kGuard) gv[0] = a.grads[(uint64_t)lg * D + d0];
-              else load_vec<V>(a.grads + (uint64_t)lg * D + d0, gv);
-#pragma unroll
-              for (int k = 0; k < V; ++k)
-                sum[k] = __dadd_rn(sum[k], __dmul_rn(static_cast<double>(gv[k]), scale));
-            }
-            ++p;
-            if (p >= a.n || a.sorted_slot[p] != slot) break;
-            uint32_t lg2 = a.lgrp[a.sorted_listing[p]];
-            if (lg2 / a.F != b) break;
-            lg = lg2;
-          }
-#pragma unroll
-          for (int k = 0; k < V; ++k) cval[k] = __double2float_rn(sum[k]);
-        }
-        if (a.dry_run) {
-          if (dims_ok)
-#pragma unroll
-            for (int k = 0; k < V; ++k) bad |= !isfinite(cval[k]);
-          continue;
-        }
-        if (c == 0) {
-          uint32_t delay = 0;
-          if (a.tracked) {
-            if (rv > ver) {
-              if (ln == 0) atomicAdd(&s_resets, 1u);
-            } else {
-              uint64_t gap = ver - rv;
-              delay = static_cast<uint32_t>(gap < kTagRing ? gap : kTagRing);
-              if (gap > 0 && tag != kNoStep && tag >= a.step_tag) delay -= 1;
-            }
-            if (!(ver > 0 && tag == a.step_tag)) {
-              ++ver;
-              tag = a.step_tag;
-            }
-            if (ln == 0) {
-              atomicAdd(&s_hist[delay < 16 ? delay : 16], 1ull);
-              atomicMax(&s_max, delay);
-              if (kDirect && a.out_delays) a.out_delays[entry] = delay;
-            }
-          } else {
-            ++ver;
-          }
-        }
-        if (dims_ok) {
-          if (adagrad) {
-#pragma unroll
-            for (int k = 0; k < V; ++k) {
-              acc[k] = __fadd_rn(acc[k], __fmul_rn(cval[k], cval[k]));
-              float den = __fadd_rn(__fsqrt_rn(acc[k]), kAdagradEps);
-              w[k] = __fsub_rn(w[k], __fdiv_rn(__fmul_rn(a.lr, cval[k]), den));
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < V; ++k) w[k] = __fsub_rn(w[k], __fmul_rn(a.lr, cval[k]));
-          }
-        }
-      }
-      if (a.dry_run) continue;
-      if (dims_ok) {
-        if (kGuard) {
-          row[d0] = w[0];
-          if (adagrad) row[D + d0] = acc[0];
-        } else {
-          store_vec<V>(row + d0, w);
-          if (adagrad) store_vec<V>(row + D + d0, acc);
-        }
-      }
-      if (c == 0 && ln == 0) {
-        t.ver[slot] = ver;
-        t.tag[slot] = tag;
-      }
-    }
+  const uint64_t n = static_cast<uint64_t>(B) * F * D;
+  if (!n) return;
+  if (D % 4 == 0) {
+    check_batch_kernel<4><<<std::min<uint64_t>(ceil_div(n / 4, 256), 148 * 16), 256, 0, st>>>(
+        grads, offsets, n / 4, D, F, mean, ctr);
+  } else {
+    check_batch_kernel<1><<<std::min<uint64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st>>>(
+        grads, offsets, n, D, F, mean, ctr);
   }
-  if (a.dry_run) {
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(&t.ctr[kCtrDivergence], 1ull);
-    return;
-  }
-  __syncthreads();
-  if (a.tracked) {
-    if (threadIdx.x < 17 && s_hist[threadIdx.x])
-      atomicAdd(&t.ctr[kCtrDelayHist + threadIdx.x], s_hist[threadIdx.x]);
-    if (threadIdx.x == 0) {
-      if (s_resets) atomicAdd(&t.ctr[kCtrClockResets], (unsigned long long)s_resets);
-      if (s_max) atomicMax(&t.ctr[kCtrMaxDelay], (unsigned long long)s_max);
-    }
-  }
-}
-
-void launch_update(const DevTable& t, const UpdateArgs& a, bool direct, int sms, cudaStream_t st) {
-  if (!a.n) return;
-  HPS_DISPATCH_DIM(t.D, {
-    uint64_t groups_per_block = 256 / L;
-    uint32_t blocks = std::min<uint64_t>(ceil_div(a.n, groups_per_block), (uint64_t)sms * 8);
-    if (direct) update_kernel<V, L, G, true><<<blocks, 256, 0, st>>>(t, a);
-    else update_kernel<V, L, G, false><<<blocks, 256, 0, st>>>(t, a);
-  });
   HPS_LAUNCH_CHECK();
 }
 
@@ -688,19 +422,6 @@ __global__ void iota_kernel(uint32_t* out, uint64_t n) {
 void launch_iota(uint32_t* out, uint64_t n, cudaStream_t st) {
   if (!n) return;
   iota_kernel<<<std::min<uint64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st>>>(out, n);
-  HPS_LAUNCH_CHECK();
-}
-
-__global__ void copy_u32_kernel(const uint32_t* __restrict__ s, uint32_t* __restrict__ d,
-                                uint64_t n) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    d[i] = s[i];
-}
-
-void launch_copy_u32(const uint32_t* src, uint32_t* dst, uint64_t n, cudaStream_t st) {
-  if (!n) return;
-  copy_u32_kernel<<<std::min<uint64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st>>>(src, dst, n);
   HPS_LAUNCH_CHECK();
 }
 

@@ -210,8 +210,7 @@ Table* table_create(const hps_table_cfg& cfg) {
     d.capacity = static_cast<uint32_t>(C);
     d.S = cfg.shard_count;
     d.opt = cfg.optimizer;
-    HPS_CUDA(cudaMalloc(&d.keys, H * sizeof(uint64_t)));
-    HPS_CUDA(cudaMalloc(&d.vals, H * sizeof(uint32_t)));
+    HPS_CUDA(cudaMalloc(&d.ht, H * sizeof(HashEntry)));
     HPS_CUDA(cudaMalloc(&d.rows, C * d.stride * sizeof(float)));
     HPS_CUDA(cudaMalloc(&d.ver, C * sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.tag, C * sizeof(uint32_t)));
@@ -235,20 +234,20 @@ Table* table_create(const hps_table_cfg& cfg) {
   }
 }
 
-// Empties the index and the row store (LruStore::clear + PsShard state reset).
+// Empties the index and the row store (LruStore::clear + PsShard state reset). Key
+// kEmptyKey and slot kPending are both all-ones, so one memset clears the index.
 void table_clear(Table* t, cudaStream_t st) {
   DevTable& d = t->d;
-  HPS_CUDA(cudaMemsetAsync(d.keys, 0xff, t->ht_size * sizeof(uint64_t), st));
-  HPS_CUDA(cudaMemsetAsync(d.vals, 0xff, t->ht_size * sizeof(uint32_t), st));
+  HPS_CUDA(cudaMemsetAsync(d.ht, 0xff, t->ht_size * sizeof(HashEntry), st));
   HPS_CUDA(cudaMemsetAsync(d.special, 0xff, sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.hwm, 0, sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.ctr + kCtrOverflow, 0, sizeof(unsigned long long), st));
 }
 
 void batch_free(Batch& b) {
-  void* ptrs[] = {b.ids, b.offsets, b.lgrp, b.slot, b.keys_a, b.vals_a, b.keys_b, b.vals_b,
-                  b.heads, b.rv, b.new_slots, b.hist, b.small, b.skeys_a, b.skeys_b,
-                  b.sperm_a, b.sperm_b, b.sstart};
+  void* ptrs[] = {b.offsets, b.lgrp, b.slot, b.keys_a, b.vals_a, b.keys_b, b.vals_b, b.rv,
+                  b.new_slots, b.hist, b.small, b.skeys_a, b.skeys_b, b.sperm_a, b.sperm_b,
+                  b.sstart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   Table* t = b.table;
@@ -267,8 +266,7 @@ void table_destroy(Table* t) {
     t->stage.free_all();
     t->prof.destroy();
     DevTable& d = t->d;
-    void* ptrs[] = {d.keys, d.vals, d.rows, d.ver, d.tag, d.slot_id, d.special, d.hwm, d.ctr,
-                    t->d_salts};
+    void* ptrs[] = {d.ht, d.rows, d.ver, d.tag, d.slot_id, d.special, d.hwm, d.ctr, t->d_salts};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (t->h_ctr) cudaFreeHost(t->h_ctr);
@@ -300,15 +298,19 @@ void table_counters(Table* t, hps_counters* out) {
   for (int i = 0; i < 17; ++i) out->delay_hist[i] = c[kCtrDelayHist + i];
 }
 
-// Reports sticky / per-call data-dependent failures recorded on the device.
-void check_flags(Table* t, cudaStream_t st) {
+// The divergence flag belongs to the push that raised it: it is reported once (by
+// that push, or by the next table sync for an HPS_ASYNC push) and then cleared.
+void check_flags(Table* t, cudaStream_t st, bool divergence) {
   read_counters(t, st);
   if (t->h_ctr[kCtrOverflow])
     throw Error(HPS_E_CONFIG,
                 "embedding table capacity exhausted (" + std::to_string(t->cfg.capacity) +
                     " rows); device tables do not evict -- raise capacity");
-  if (t->h_ctr[kCtrDivergence])
+  if (divergence && t->h_ctr[kCtrDivergence]) {
+    HPS_CUDA(cudaMemsetAsync(t->d.ctr + kCtrDivergence, 0, sizeof(unsigned long long), st));
+    HPS_CUDA(cudaStreamSynchronize(st));
     throw Error(HPS_E_DIVERGENCE, "non-finite gradient contribution; nothing was applied");
+  }
 }
 
 void table_sync(Table* t) {
@@ -332,17 +334,17 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
   if (n > b.cap_N) {
     uint64_t c = 0;
     uint32_t** bufs[] = {&b.lgrp, &b.slot, &b.keys_a, &b.vals_a, &b.keys_b, &b.vals_b,
-                         &b.heads, &b.rv, &b.new_slots};
+                         &b.rv, &b.new_slots};
     for (uint32_t** p : bufs) {
       c = 0;
       ensure(*p, c, n);
     }
-    c = 0;
-    ensure(b.ids, c, n);
     size_t hw = std::max(radix::hist_words<uint32_t>(n), radix::hist_words<uint64_t>(n));
-    c = 0;
-    ensure(b.hist, c, hw);
-    b.hist_cap = hw;
+    if (hw > b.hist_cap) {
+      c = 0;
+      ensure(b.hist, c, hw);
+      b.hist_cap = hw;
+    }
     b.cap_N = n;
   }
   if (BF + 1 > b.cap_BF) {
@@ -379,20 +381,16 @@ static int slot_key_bits(const Table* t) {
   return std::max(1, bits_for(static_cast<uint64_t>(t->cfg.capacity) - 1));
 }
 
-// Sorts the staged (keys_a = slot, vals_a = listing) pairs by slot and finds the
-// segment / pair heads.
-static void sort_and_heads(Batch& b, bool direct, cudaStream_t st) {
+// Stable sort of the staged (keys_a = slot, vals_a = listing) pairs by slot: every
+// row's listings become one contiguous run in apply order.
+static void sort_slots(Batch& b, cudaStream_t st) {
   Table* t = b.table;
-  bool in_b;
-  {
-    ProfScope p(t, "sort", st);
-    in_b = radix::sort_pairs<uint32_t>(b.keys_a, b.vals_a, b.keys_b, b.vals_b,
-                                       static_cast<uint32_t>(b.N), slot_key_bits(t), b.hist, st);
-  }
+  ProfScope p(t, "sort", st);
+  bool in_b = radix::sort_pairs<uint32_t>(b.keys_a, b.vals_a, b.keys_b, b.vals_b,
+                                          static_cast<uint32_t>(b.N), slot_key_bits(t), b.hist,
+                                          st);
   b.sorted_slot = in_b ? b.keys_b : b.keys_a;
   b.sorted_listing = in_b ? b.vals_b : b.vals_a;
-  ProfScope p(t, "heads", st);
-  launch_heads(b.sorted_slot, b.sorted_listing, b.lgrp, b.F, b.N, direct, b.heads, b.small, st);
 }
 
 // EmbeddingWorker::register_sample for a whole batch + the route/dedup/probe half of
@@ -428,12 +426,16 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   b.N = N;
   HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
   launch_expand_groups(b.offsets, static_cast<uint32_t>(BF), b.lgrp, st);
+  const bool permute = d_sk && B > 1;
   {
     ProfScope p(t, "probe", st);
-    launch_probe(t->d, d_ids, N, b.slot, b.new_slots, &b.small[2], st);
+    launch_probe(t->d, d_ids, N, b.slot, permute ? nullptr : b.keys_a,
+                 permute ? nullptr : b.vals_a, b.new_slots, &b.small[2], nullptr, st);
   }
   launch_lazy_init(t->d, b.new_slots, &b.small[2], N, t->sm_count, st);
-  if (d_sk && B > 1) {
+  if (permute) {
+    // Apply order = ascending sample key: enumerate listings sample by sample in key
+    // order before the stable slot sort.
     launch_sample_order(d_sk, B, b.skeys_a, b.sperm_a, st);
     bool in_b = radix::sort_pairs<uint64_t>(b.skeys_a, b.sperm_a, b.skeys_b, b.sperm_b, B, 64,
                                             b.hist, st);
@@ -441,11 +443,8 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     launch_sample_lengths(perm, b.offsets, B, F, b.sstart, st);
     launch_scan_inplace(b.sstart, B, b.sstart + B, st);
     launch_permuted_listing(perm, b.sstart, b.offsets, b.slot, B, F, b.keys_a, b.vals_a, st);
-  } else {
-    launch_copy_u32(b.slot, b.keys_a, N, st);
-    launch_iota(b.vals_a, N, st);
   }
-  sort_and_heads(b, false, st);
+  sort_slots(b, st);
   b.registered = true;
   b.pulled = false;
   stg.finish(st);
@@ -472,8 +471,12 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
                 uint32_t flags, cudaStream_t st) {
   if (!b.registered) throw Error(HPS_E_STALE_SAMPLE, "push: batch not registered");
   Table* t = b.table;
-  if (epoch != t->epoch) {  // PsShard::apply_gradients epoch fence, embedding_ps.hpp:142-145
-    launch_add_counter_from(t->d.ctr, kCtrStaleDrops, &b.small[1], st);
+  if (epoch != t->epoch) {
+    // PsShard::apply_gradients epoch fence (embedding_ps.hpp:142-145): drop every
+    // (sample, unique id) entry of the batch, count them.
+    launch_count_pairs(b.sorted_slot, b.sorted_listing, b.lgrp, b.F, b.N,
+                       t->d.ctr + kCtrStaleDrops, st);
+    if (!(flags & HPS_ASYNC)) HPS_CUDA(cudaStreamSynchronize(st));
     if (accepted) *accepted = 0;
     return;
   }
@@ -491,8 +494,6 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   UpdateArgs a{};
   a.sorted_slot = b.sorted_slot;
   a.sorted_listing = b.sorted_listing;
-  a.heads = b.heads;
-  a.small = b.small;
   a.n = b.N;
   a.lgrp = b.lgrp;
   a.offsets = b.offsets;
@@ -516,18 +517,20 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     launch_update(t->d, a, false, t->sm_count, st);
   }
   if (accepted) *accepted = 1;
-  if (!(flags & HPS_ASYNC)) {
-    stg.finish(st);
-    check_flags(t, st);
-  } else {
-    stg.finish(st);
-  }
+  stg.finish(st);
+  if (!(flags & HPS_ASYNC)) check_flags(t, st);
 }
 
+// (sample, unique id) pairs of the registered batch = optimizer applications a push
+// performs (= delays it records).
 uint64_t batch_pairs(Batch& b) {
-  if (!b.small) return 0;
-  uint32_t p = 0;
-  HPS_CUDA(cudaMemcpy(&p, b.small + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  if (!b.registered) return 0;
+  Table* t = b.table;
+  HPS_CUDA(cudaMemset(t->d.ctr + kCtrScratch, 0, sizeof(unsigned long long)));
+  launch_count_pairs(b.sorted_slot, b.sorted_listing, b.lgrp, b.F, b.N, t->d.ctr + kCtrScratch,
+                     nullptr);
+  unsigned long long p = 0;
+  HPS_CUDA(cudaMemcpy(&p, t->d.ctr + kCtrScratch, sizeof(p), cudaMemcpyDeviceToHost));
   return p;
 }
 
@@ -542,11 +545,12 @@ void table_lookup(Table* t, const uint64_t* ids, uint64_t n, float* out_values,
   float* d_out = static_cast<float*>(stg.out(out_values, n * t->cfg.embedding_dim * sizeof(float)));
   uint64_t* d_ver = static_cast<uint64_t*>(stg.out(out_versions, n * sizeof(uint64_t)));
   HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
-  launch_probe(t->d, d_ids, n, b.slot, b.new_slots, &b.small[2], st);
+  launch_probe(t->d, d_ids, n, b.slot, nullptr, nullptr, b.new_slots, &b.small[2], nullptr, st);
   launch_lazy_init(t->d, b.new_slots, &b.small[2], n, t->sm_count, st);
   launch_gather(t->d, b.slot, n, d_out, d_ver, st);
+  b.registered = false;
   stg.finish(st);
-  check_flags(t, st);
+  check_flags(t, st, false);
 }
 
 void table_peek(Table* t, const uint64_t* ids, uint64_t n, float* out_w, float* out_acc,
@@ -566,10 +570,9 @@ void table_peek(Table* t, const uint64_t* ids, uint64_t n, float* out_w, float* 
 void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64_t* rv, uint64_t n,
                  float lr, uint32_t step_tag, uint32_t epoch, uint32_t* out_delays,
                  int* accepted, uint32_t flags, cudaStream_t st) {
+  Batch& b = t->scratch;
+  batch_reserve(b, n, 0, 0);
   if (epoch != t->epoch) {
-    // Host-known entry count; fold into the device counter.
-    Batch& b = t->scratch;
-    batch_reserve(b, 1, 0, 0);
     uint32_t n32 = static_cast<uint32_t>(n);
     HPS_CUDA(cudaMemcpyAsync(b.small + 1, &n32, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
     launch_add_counter_from(t->d.ctr, kCtrStaleDrops, b.small + 1, st);
@@ -578,8 +581,6 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
     return;
   }
   if (n >= 0xffffffffull) throw Error(HPS_E_PRECONDITION, "apply: too many entries");
-  Batch& b = t->scratch;
-  batch_reserve(b, n, 0, 0);
   const uint32_t D = t->cfg.embedding_dim;
   Stager stg(t->stage);
   const uint64_t* d_ids = static_cast<const uint64_t*>(stg.in(ids, n * sizeof(uint64_t), st));
@@ -592,21 +593,19 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
   launch_check_direct(d_g, n * D, t->d.ctr, st);
   read_counters(t, st);
   if (t->h_ctr[kCtrDivergence]) {
+    HPS_CUDA(cudaMemsetAsync(t->d.ctr + kCtrDivergence, 0, sizeof(unsigned long long), st));
+    stg.finish(st);
     throw Error(HPS_E_DIVERGENCE, "PsShard::apply_gradients: non-finite gradient");
   }
   b.N = n;
   b.B = static_cast<uint32_t>(n);
   b.F = 1;
-  launch_probe(t->d, d_ids, n, b.slot, b.new_slots, &b.small[2], st);
+  launch_probe(t->d, d_ids, n, b.slot, b.keys_a, b.vals_a, b.new_slots, &b.small[2], nullptr, st);
   launch_lazy_init(t->d, b.new_slots, &b.small[2], n, t->sm_count, st);
-  launch_copy_u32(b.slot, b.keys_a, n, st);
-  launch_iota(b.vals_a, n, st);
-  sort_and_heads(b, true, st);
+  sort_slots(b, st);
   UpdateArgs a{};
   a.sorted_slot = b.sorted_slot;
   a.sorted_listing = b.sorted_listing;
-  a.heads = b.heads;
-  a.small = b.small;
   a.n = n;
   a.grads = d_g;
   a.rv64 = d_rv;

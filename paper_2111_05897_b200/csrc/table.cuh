@@ -1,13 +1,13 @@
 // Device-resident embedding table and per-batch plan (host-side objects).
 //
 // HBM layout of one table:
-//   keys[H]      u64  open-addressing id index, H = pow2 >= 2*capacity (load <= 0.5)
-//   vals[H]      u32  slot of keys[h] (kPending while being published)
-//   rows[C][2D]  f32  [w D | acc D] per slot -- the reference row (embedding_ps.hpp:64);
-//                     one contiguous 8D-byte segment, read-modify-written by the update
-//   ver[C]       u32  version (# distinct steps that wrote the row, embedding_ps.hpp:482)
-//   tag[C]       u32  step tag of the latest version bump (replaces the 16-deep ring)
-//   slot_id[C]   u64  id held by a slot (init seed, export)
+//   ht[H]        16 B  open-addressing id index {u64 key, u32 slot}, H = pow2 >= 2*capacity
+//                      (load <= 0.5); one probe = one 32-byte sector
+//   rows[C][2D]  f32   [w D | acc D] per slot -- the reference row (embedding_ps.hpp:64);
+//                      one contiguous 8D-byte segment, read-modify-written by the update
+//   ver[C]       u32   version (# distinct steps that wrote the row, embedding_ps.hpp:482)
+//   tag[C]       u32   step tag of the latest version bump (replaces the 16-deep ring)
+//   slot_id[C]   u64   id held by a slot (init seed, export)
 // Slots are handed out densely from a device high-water mark (lru_store.hpp:98).
 #pragma once
 
@@ -31,16 +31,22 @@ enum CounterIdx : int {
   kCtrNeedExact = 5,   // per-call: bound check inconclusive -> exact dry run
   kCtrMaxDelay = 6,
   kCtrDelayHist = 7,   // 17 words: delays 0..15, >=16
-  kCtrPairs = 24,      // per-call: (sample, unique id) pairs of the last push
+  kCtrScratch = 31,    // per-call scratch (pair counts)
   kCtrCount = 32
 };
 
+// One 16-byte index entry: a probe touches a single 32-byte sector.
+struct __align__(16) HashEntry {
+  unsigned long long key;  // kEmptyKey when free
+  uint32_t slot;           // kPending while the inserting thread publishes it
+  uint32_t pad;
+};
+
 struct DevTable {
-  uint64_t* keys;
-  uint32_t* vals;
+  HashEntry* ht;
   uint64_t ht_mask;
-  int ht_shift;  // 64 - log2(H)
-  uint32_t* special;  // slot of id == kEmptyKey (kAbsent / kInserting / slot)
+  int ht_shift;       // 64 - log2(H)
+  uint32_t* special;  // slot of id == kEmptyKey (kSpecialAbsent / kSpecialInserting / slot)
   float* rows;
   uint32_t D;
   uint32_t stride;  // floats per row (2D)
@@ -79,24 +85,20 @@ struct Batch {
   uint32_t B = 0, F = 0;
   uint64_t N = 0;
   uint64_t cap_N = 0, cap_BF = 0, cap_B = 0;
-  // inputs (device copies when the caller passed host memory)
-  uint64_t* ids = nullptr;        // [N]
-  uint32_t* offsets = nullptr;    // [B*F+1]
-  // derived
+  uint32_t* offsets = nullptr;    // [B*F+1] our copy of the CSR offsets
   uint32_t* lgrp = nullptr;       // [N] listing -> b*F+g
   uint32_t* slot = nullptr;       // [N] listing -> table slot
-  uint32_t* keys_a = nullptr;     // [N] sort ping-pong
-  uint32_t* vals_a = nullptr;
+  uint32_t* keys_a = nullptr;     // [N] sort ping-pong (slot keys)
+  uint32_t* vals_a = nullptr;     //     (listing values)
   uint32_t* keys_b = nullptr;
   uint32_t* vals_b = nullptr;
   const uint32_t* sorted_slot = nullptr;
   const uint32_t* sorted_listing = nullptr;
-  uint32_t* heads = nullptr;      // [N] segment heads (unordered)
   uint32_t* rv = nullptr;         // [N] per-listing read version (u32) from the last pull
   uint32_t* new_slots = nullptr;  // [N] rows inserted by register (lazy-init queue)
   uint32_t* hist = nullptr;
   size_t hist_cap = 0;
-  uint32_t* small = nullptr;      // device scalars: [0]=U, [1]=P, [2]=new_count
+  uint32_t* small = nullptr;      // device scalars: [2] = rows inserted by this register
   // sample-order permutation (sample_keys != NULL)
   uint64_t* skeys_a = nullptr;
   uint64_t* skeys_b = nullptr;
@@ -122,7 +124,6 @@ struct Profiler {
   void destroy();
 };
 
-struct Table;
 struct ProfScope {
   ProfScope(Table* t, const char* name, cudaStream_t st);
   ~ProfScope();
@@ -148,11 +149,14 @@ struct Table {
   unsigned long long* h_ctr = nullptr;  // pinned mirror of the counters
 };
 
-// ---- kernels / launchers (kernels.cu) -------------------------------------------------
+// ---- kernels / launchers (kernels.cu, update.cu) ---------------------------------------
 void launch_route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cudaStream_t st);
 void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st);
+// slots[i] = find_or_insert(ids[i]); when sort_keys/sort_vals are given also writes the
+// (slot, i) pairs the apply-order sort consumes.
 void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* slots,
-                  uint32_t* new_slots, uint32_t* new_count, cudaStream_t st);
+                  uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
+                  uint32_t* new_count, const unsigned long long* gate, cudaStream_t st);
 void launch_lazy_init(const DevTable& t, const uint32_t* new_slots, const uint32_t* new_count,
                       uint64_t max_new, int sms, cudaStream_t st);
 void launch_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* out_values,
@@ -161,9 +165,6 @@ void launch_peek(const DevTable& t, const uint64_t* ids, uint64_t n, float* out_
                  uint64_t* out_versions, uint8_t* out_present, cudaStream_t st);
 void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,
                  int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32, cudaStream_t st);
-void launch_heads(const uint32_t* sorted_slot, const uint32_t* sorted_listing,
-                  const uint32_t* lgrp, uint32_t F, uint64_t n, bool direct, uint32_t* heads,
-                  uint32_t* small, cudaStream_t st);
 void launch_check_direct(const float* grads, uint64_t n_floats, unsigned long long* ctr,
                          cudaStream_t st);
 void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
@@ -172,9 +173,7 @@ void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B,
 struct UpdateArgs {
   const uint32_t* sorted_slot;
   const uint32_t* sorted_listing;
-  const uint32_t* heads;
-  const uint32_t* small;  // [0] = U
-  uint64_t n;             // sorted elements
+  uint64_t n;  // sorted elements
   // batch mode
   const uint32_t* lgrp;
   const uint32_t* offsets;
@@ -192,9 +191,9 @@ struct UpdateArgs {
   int dry_run;  // compute + validate contributions only
 };
 void launch_update(const DevTable& t, const UpdateArgs& a, bool direct, int sms, cudaStream_t st);
+void launch_count_pairs(const uint32_t* ss, const uint32_t* sl, const uint32_t* lgrp, uint32_t F,
+                        uint64_t n, unsigned long long* ctr, cudaStream_t st);
 
-void launch_iota(uint32_t* out, uint64_t n, cudaStream_t st);
-void launch_copy_u32(const uint32_t* src, uint32_t* dst, uint64_t n, cudaStream_t st);
 void launch_sample_order(const uint64_t* sample_keys, uint32_t B, uint64_t* keys_out,
                          uint32_t* perm_out, cudaStream_t st);
 void launch_sample_lengths(const uint32_t* perm, const uint32_t* offsets, uint32_t B, uint32_t F,
@@ -205,5 +204,6 @@ void launch_permuted_listing(const uint32_t* perm, const uint32_t* starts,
                              uint32_t F, uint32_t* keys_out, uint32_t* vals_out, cudaStream_t st);
 void launch_add_counter_from(unsigned long long* ctr, int idx, const uint32_t* src,
                              cudaStream_t st);
+void launch_iota(uint32_t* out, uint64_t n, cudaStream_t st);
 
 }  // namespace hps

@@ -55,7 +55,7 @@ void table_reset(Table* t);
 void read_counters(Table* t, cudaStream_t st);
 void profile_enable(Table* t, bool on);
 void profile_get(Table* t, const char* name, double* ms, uint64_t* count);
-void check_flags(Table* t, cudaStream_t st);
+void check_flags(Table* t, cudaStream_t st, bool divergence = true);
 
 void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B);
 void batch_free(Batch& b);
