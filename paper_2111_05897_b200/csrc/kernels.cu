@@ -139,12 +139,13 @@ __global__ void __launch_bounds__(256)
     probe_kernel(DevTable t, const uint64_t* __restrict__ ids, uint64_t n,
                  uint32_t* __restrict__ slots, uint32_t* __restrict__ sort_keys,
                  uint32_t* __restrict__ sort_vals, uint32_t* __restrict__ new_slots,
-                 uint32_t* __restrict__ new_count, const unsigned long long* gate) {
-  if (gate && ld_volatile(gate)) return;
+                 uint32_t* __restrict__ new_count, bool count) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t s = find_or_insert(t, ids[i], new_slots, new_count, true);
     slots[i] = s;
+    // Batch plan: count the row's listings (fire-and-forget reduction, plan.cu).
+    if (count && slot_ok(t, s)) atomicAdd(&t.cnt[s], 1u);
     if (sort_keys) {
       sort_keys[i] = s;
       sort_vals[i] = static_cast<uint32_t>(i);
@@ -154,10 +155,10 @@ __global__ void __launch_bounds__(256)
 
 void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* slots,
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
-                  uint32_t* new_count, const unsigned long long* gate, cudaStream_t st) {
+                  uint32_t* new_count, bool count, cudaStream_t st) {
   if (!n) return;
   probe_kernel<<<ceil_div(n, 256), 256, 0, st>>>(t, ids, n, slots, sort_keys, sort_vals,
-                                                 new_slots, new_count, gate);
+                                                 new_slots, new_count, count);
   HPS_LAUNCH_CHECK();
 }
 
@@ -182,10 +183,7 @@ __global__ void lazy_init_kernel(DevTable t, const uint32_t* __restrict__ new_sl
       row[d] = init_value(seed, d, lo, span);
       row[t.D + d] = 0.0f;
     }
-    if (lane == 0) {
-      t.ver[slot] = 0;
-      t.tag[slot] = kNoStep;
-    }
+    if (lane == 0) t.vt[slot] = make_uint2(0u, kNoStep);
   }
 }
 
@@ -208,7 +206,7 @@ __global__ void gather_kernel(DevTable t, const uint32_t* __restrict__ slots, ui
     bool ok = slot_ok(t, s);
     const float* row = t.rows + static_cast<uint64_t>(ok ? s : 0) * t.stride;
     for (uint32_t d = lane; d < t.D; d += 32) out[i * t.D + d] = ok ? row[d] : 0.0f;
-    if (out_ver && lane == 0) out_ver[i] = ok ? t.ver[s] : 0;
+    if (out_ver && lane == 0) out_ver[i] = ok ? t.vt[s].x : 0;
   }
 }
 
@@ -236,7 +234,7 @@ __global__ void peek_kernel(DevTable t, const uint64_t* __restrict__ ids, uint64
       if (out_acc) out_acc[i * t.D + d] = ok ? row[t.D + d] : 0.0f;
     }
     if (lane == 0) {
-      if (out_ver) out_ver[i] = ok ? t.ver[s] : 0;
+      if (out_ver) out_ver[i] = ok ? t.vt[s].x : 0;
       if (out_present) out_present[i] = ok ? 1 : 0;
     }
   }
@@ -291,7 +289,7 @@ __global__ void __launch_bounds__(256)
           acc[k] = __dadd_rn(acc[k], static_cast<double>(r1[k]));
         }
         if (c == 0 && ln == 0) {
-          uint32_t v0 = slot_ok(t, s0) ? t.ver[s0] : 0, v1 = slot_ok(t, s1) ? t.ver[s1] : 0;
+          uint32_t v0 = slot_ok(t, s0) ? t.vt[s0].x : 0, v1 = slot_ok(t, s1) ? t.vt[s1].x : 0;
           if (out_rv64) out_rv64[i] = v0, out_rv64[i + 1] = v1;
           if (out_rv32) out_rv32[i] = v0, out_rv32[i + 1] = v1;
         }
@@ -304,7 +302,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int k = 0; k < V; ++k) acc[k] = __dadd_rn(acc[k], static_cast<double>(r0[k]));
         if (c == 0 && ln == 0) {
-          uint32_t v0 = slot_ok(t, s0) ? t.ver[s0] : 0;
+          uint32_t v0 = slot_ok(t, s0) ? t.vt[s0].x : 0;
           if (out_rv64) out_rv64[i] = v0;
           if (out_rv32) out_rv32[i] = v0;
         }

@@ -1,0 +1,136 @@
+// Per-batch apply plan: which listings can be applied independently and which need
+// the ordered per-row recurrence.
+//
+// During the probe every listing adds 1 to its row's batch counter (cnt[slot]). A row
+// listed once in the batch ("single") gets exactly one optimizer application, so its
+// listing needs no ordering at all -- for the one-hot Criteo shape that is >99% of all
+// listings. Listings of rows hit more than once ("multi") are compacted, in listing
+// (= apply) order, by a single-pass chained scan, and only they go through the stable
+// slot sort. The counters are reset by the update that consumes them; a batch that is
+// never pushed leaves them high, which can only move later rows from the single path
+// to the (always correct) multi path.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "radix_sort.cuh"
+#include "table.cuh"
+#include "vec.cuh"
+
+namespace hps {
+
+namespace {
+constexpr int kPlanBlock = 256;
+constexpr int kPlanItems = 8;
+constexpr int kPlanTile = kPlanBlock * kPlanItems;
+}  // namespace
+
+// kind[i] = 1 single / 2 multi; multi listings are written, in listing order, to
+// (mkeys = slot, mvals = listing) and counted into *n_multi. One tile per block,
+// dynamically numbered; tile prefixes by decoupled look-back (status words as in
+// radix_sort.cuh: [63:32] epoch, [31] prefix flag, [30:0] count).
+__global__ void __launch_bounds__(kPlanBlock)
+    classify_kernel(const uint32_t* __restrict__ slots, const uint32_t* __restrict__ cnt,
+                    uint32_t capacity, uint64_t n, uint8_t* __restrict__ kind,
+                    uint32_t* __restrict__ mkeys, uint32_t* __restrict__ mvals,
+                    uint32_t* __restrict__ n_multi, unsigned long long* status,
+                    uint32_t* tile_ctr, uint32_t epoch) {
+  __shared__ uint32_t s_tile, s_warp[kPlanBlock / 32], s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t tiles = static_cast<uint32_t>((n + kPlanTile - 1) / kPlanTile);
+  if (tile >= tiles) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // Blocked layout per warp: lane handles kPlanItems consecutive listings of its warp's
+  // stripe, so the flag order (warp, lane, item) is listing order.
+  const uint64_t base = static_cast<uint64_t>(tile) * kPlanTile +
+                        static_cast<uint64_t>(warp) * 32 * kPlanItems;
+  uint32_t s[kPlanItems];
+  bool m[kPlanItems];
+  uint32_t mine = 0;
+#pragma unroll
+  for (int j = 0; j < kPlanItems; ++j) {
+    // coalesced: item j of every lane is j*32 + lane; remapped below to blocked order
+    uint64_t i = base + static_cast<uint64_t>(lane) * kPlanItems + j;
+    s[j] = i < n ? slots[i] : kInvalidSlot;
+  }
+#pragma unroll
+  for (int j = 0; j < kPlanItems; ++j) {
+    uint64_t i = base + static_cast<uint64_t>(lane) * kPlanItems + j;
+    bool valid = i < n;
+    bool multi = valid && s[j] < capacity && cnt[s[j]] > 1;
+    m[j] = multi;
+    mine += multi;
+    if (valid) kind[i] = multi ? 2 : 1;
+  }
+  // warp-inclusive scan of per-lane counts
+  uint32_t x = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int w = 0; w < kPlanBlock / 32; ++w) {
+      uint32_t c = s_warp[w];
+      s_warp[w] = tot;
+      tot += c;
+    }
+    const unsigned long long ep = static_cast<unsigned long long>(epoch) << 32;
+    volatile unsigned long long* my = status + tile;
+    uint32_t excl = 0;
+    if (tile == 0) {
+      *my = ep | radix::kPrefixFlag | tot;
+    } else {
+      *my = ep | tot;
+      for (int64_t t = static_cast<int64_t>(tile) - 1; t >= 0; --t) {
+        const volatile unsigned long long* st = status + t;
+        unsigned long long v;
+        do {
+          v = *st;
+        } while ((v >> 32) != epoch);
+        excl += static_cast<uint32_t>(v & (radix::kPrefixFlag - 1));
+        if (v & radix::kPrefixFlag) break;
+      }
+      *my = ep | radix::kPrefixFlag | (excl + tot);
+    }
+    s_excl = excl;
+    if (tile == tiles - 1) *n_multi = excl + tot;
+  }
+  __syncthreads();
+  uint32_t pos = s_excl + s_warp[warp] + x - mine;
+#pragma unroll
+  for (int j = 0; j < kPlanItems; ++j) {
+    if (m[j]) {
+      uint64_t i = base + static_cast<uint64_t>(lane) * kPlanItems + j;
+      mkeys[pos] = s[j];
+      mvals[pos] = static_cast<uint32_t>(i);
+      ++pos;
+    }
+  }
+}
+
+void launch_classify(const uint32_t* slots, const uint32_t* cnt, uint32_t capacity, uint64_t n,
+                     uint8_t* kind, uint32_t* mkeys, uint32_t* mvals, uint32_t* n_multi,
+                     unsigned long long* status, uint32_t* tile_ctr, cudaStream_t st) {
+  if (!n) {
+    HPS_CUDA(cudaMemsetAsync(n_multi, 0, sizeof(uint32_t), st));
+    return;
+  }
+  HPS_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st));
+  const uint32_t tiles = ceil_div(n, kPlanTile);
+  const uint32_t epoch = radix::g_epoch.fetch_add(1) + 1;
+  classify_kernel<<<tiles, kPlanBlock, 0, st>>>(slots, cnt, capacity, n, kind, mkeys, mvals,
+                                                n_multi, status, tile_ctr, epoch);
+  HPS_LAUNCH_CHECK();
+}
+
+size_t classify_status_words(uint64_t n) { return 2 * (ceil_div(n, kPlanTile) + 1); }
+
+}  // namespace hps

@@ -1,19 +1,22 @@
-// Stable LSD radix sort of (key, value) pairs, hand-written for sm_100a.
+// Stable LSD radix sort of (key, u32 value) pairs, hand-written for sm_100a
+// ("onesweep": one histogram kernel for all digit passes, then ONE kernel per 8-bit
+// pass whose tiles find their global offsets by decoupled look-back).
 //
-// Used for the two orderings the hot path needs:
-//   * listings grouped by table slot, listing order preserved inside a slot (the
-//     per-row apply order of the ordered optimizer update), u32 keys;
-//   * ids sorted ascending with their positions (batch dedup / compress_indices),
-//     u64 keys.
-// Each 8-bit pass is reduce-then-scan: upsweep (per-tile digit histogram) ->
-// per-digit scan over tiles -> downsweep (stable in-tile ranking with
-// __match_any_sync, staging the tile in shared memory in digit order so the global
-// scatter is written in contiguous runs). Keys/values are read and written once
-// per pass: 2*(sizeof(K)+sizeof(V)) bytes per element per pass.
+// Used for the orderings the hot path needs:
+//   * the listings of rows hit more than once in a batch, grouped by table slot with
+//     listing (= apply) order kept inside a slot (u32 keys);
+//   * ids ascending with their positions (batch dedup / compress_indices, u64 keys).
+// The element count may live in device memory (the multi-listing list is compacted
+// on the device), so a sort never needs a host round trip: the grid is sized for an
+// upper bound and surplus tiles exit. Per pass every key/value is read once and
+// written once (2*(sizeof(K)+4) bytes per element); the look-back touches 8 B per
+// (tile, digit).
 #pragma once
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <atomic>
 
 #include "common.cuh"
 
@@ -24,84 +27,49 @@ constexpr int kBits = 8;
 constexpr int kBins = 1 << kBits;
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
+constexpr int kMaxPasses = 8;
 
 template <typename K>
 struct Tile {
-  static constexpr int kItems = sizeof(K) == 8 ? 8 : 16;
+  static constexpr int kItems = 8;
   static constexpr int kTile = kBlock * kItems;
   static constexpr size_t kSmem =
       kTile * (sizeof(K) + sizeof(uint32_t)) + (kWarps * kBins + 3 * kBins) * sizeof(uint32_t);
 };
+
+// status word: [63:32] epoch of the pass, [31] inclusive-prefix flag, [30:0] count
+constexpr unsigned long long kPrefixFlag = 1ull << 31;
+
+inline std::atomic<uint32_t> g_epoch{1};
 
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
   return static_cast<uint32_t>(key >> shift) & (kBins - 1);
 }
 
-// hist[d * tiles + tile] = count of digit d in tile.
+__device__ __forceinline__ uint32_t count_of(const uint32_t* n_dev, uint32_t n_host) {
+  return n_dev ? *n_dev : n_host;
+}
+
+// Digit histograms of every pass in one read of the keys: hist[p * kBins + d].
 template <typename K>
-__global__ void __launch_bounds__(kBlock) upsweep(const K* __restrict__ keys, uint32_t n, int shift,
-                                                  uint32_t* __restrict__ hist, uint32_t tiles) {
-  constexpr int kTileN = Tile<K>::kTile;
-  __shared__ uint32_t cnt[kWarps][kBins];
-  const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kWarps * kBins; i += kBlock) (&cnt[0][0])[i] = 0;
+__global__ void __launch_bounds__(kBlock)
+    hist_kernel(const K* __restrict__ keys, const uint32_t* n_dev, uint32_t n_host, int passes,
+                uint32_t* __restrict__ hist) {
+  __shared__ uint32_t cnt[kMaxPasses * kBins];
+  const uint32_t n = count_of(n_dev, n_host);
+  for (int i = threadIdx.x; i < passes * kBins; i += kBlock) cnt[i] = 0;
   __syncthreads();
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kTileN;
-#pragma unroll 4
-  for (int j = 0; j < Tile<K>::kItems; ++j) {
-    uint64_t idx = base + static_cast<uint64_t>(j) * kBlock + threadIdx.x;
-    if (idx < n) atomicAdd(&cnt[warp][digit_of(keys[idx], shift)], 1u);
+  for (uint32_t i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) {
+    K k = keys[i];
+    for (int p = 0; p < passes; ++p) atomicAdd(&cnt[p * kBins + digit_of(k, p * kBits)], 1u);
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < kBins; d += kBlock) {
-    uint32_t s = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += cnt[w][d];
-    hist[static_cast<uint64_t>(d) * tiles + blockIdx.x] = s;
-  }
+  for (int i = threadIdx.x; i < passes * kBins; i += kBlock)
+    if (cnt[i]) atomicAdd(&hist[i], cnt[i]);
 }
 
-// One block per digit: exclusive scan of hist[d, 0..tiles) in place; totals[d].
-static __global__ void __launch_bounds__(1024) scan_digits(uint32_t* __restrict__ hist, uint32_t tiles,
-                                                    uint32_t* __restrict__ totals) {
-  __shared__ uint32_t warp_sums[32];
-  __shared__ uint32_t carry;
-  uint32_t* row = hist + static_cast<uint64_t>(blockIdx.x) * tiles;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (uint32_t base = 0; base < tiles; base += 1024) {
-    uint32_t i = base + threadIdx.x;
-    uint32_t v = i < tiles ? row[i] : 0;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_sums[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t s = warp_sums[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-        if (lane >= o) s += y;
-      }
-      warp_sums[lane] = s;  // inclusive
-    }
-    __syncthreads();
-    uint32_t excl = carry + (warp ? warp_sums[warp - 1] : 0) + x - v;
-    if (i < tiles) row[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += warp_sums[31];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) totals[blockIdx.x] = carry;
-}
-
-// Block-wide exclusive scan of one value per thread for the first kBins threads.
+// Block-wide exclusive scan over the kBins values held one per thread.
 __device__ __forceinline__ uint32_t block_excl_scan_bins(uint32_t v, uint32_t* scratch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t x = v;
@@ -120,33 +88,31 @@ __device__ __forceinline__ uint32_t block_excl_scan_bins(uint32_t v, uint32_t* s
 
 template <typename K>
 __global__ void __launch_bounds__(kBlock)
-    downsweep(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-              K* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t n, int shift,
-              const uint32_t* __restrict__ hist, const uint32_t* __restrict__ totals,
-              uint32_t tiles) {
+    pass_kernel(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+                K* __restrict__ keys_out, uint32_t* __restrict__ vals_out, const uint32_t* n_dev,
+                uint32_t n_host, int shift, const uint32_t* __restrict__ hist,
+                unsigned long long* status, uint32_t* tile_ctr, uint32_t epoch) {
   constexpr int kItems = Tile<K>::kItems;
   constexpr int kTileN = Tile<K>::kTile;
   extern __shared__ __align__(16) unsigned char smem[];
   K* skeys = reinterpret_cast<K*>(smem);
   uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + kTileN);
-  uint32_t* wcnt = svals + kTileN;            // [kWarps][kBins]
+  uint32_t* wcnt = svals + kTileN;              // [kWarps][kBins]
   uint32_t* block_off = wcnt + kWarps * kBins;  // [kBins]
   uint32_t* gbase = block_off + kBins;          // [kBins]
-  uint32_t* scratch = gbase + kBins;            // [kBins] (uses 32)
+  uint32_t* scratch = gbase + kBins;            // [kBins] (uses 32 + 1)
+
+  const uint32_t n = count_of(n_dev, n_host);
+  const uint32_t tiles = (n + kTileN - 1) / kTileN;
+  // Dynamic tile order: a tile only ever waits on tiles that were scheduled before it.
+  if (threadIdx.x == 0) scratch[32] = atomicAdd(tile_ctr, 1u);
+  for (int i = threadIdx.x; i < kWarps * kBins; i += kBlock) wcnt[i] = 0;
+  __syncthreads();
+  const uint32_t tile = scratch[32];
+  if (tile >= tiles) return;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kWarps * kBins; i += kBlock) wcnt[i] = 0;
-
-  // Global base of every digit for this tile: digit start + this tile's offset.
-  {
-    uint32_t d = threadIdx.x;  // kBlock == kBins
-    uint32_t tot = totals[d];
-    uint32_t start = block_excl_scan_bins(tot, scratch);
-    gbase[d] = start + hist[static_cast<uint64_t>(d) * tiles + blockIdx.x];
-  }
-  __syncthreads();
-
-  const uint64_t tile_base = static_cast<uint64_t>(blockIdx.x) * kTileN;
+  const uint64_t tile_base = static_cast<uint64_t>(tile) * kTileN;
   const uint64_t warp_base = tile_base + static_cast<uint64_t>(warp) * 32 * kItems;
   K k[kItems];
   uint32_t v[kItems];
@@ -172,75 +138,151 @@ __global__ void __launch_bounds__(kBlock)
     __syncwarp();
   }
   __syncthreads();
-  {
-    uint32_t d = threadIdx.x;
-    uint32_t run = 0;
+  const uint32_t d = threadIdx.x;  // kBlock == kBins: thread d owns digit d below
+  uint32_t tile_cnt = 0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      uint32_t t = wcnt[w * kBins + d];
-      wcnt[w * kBins + d] = run;
-      run += t;
-    }
-    block_off[d] = block_excl_scan_bins(run, scratch);
+  for (int w = 0; w < kWarps; ++w) {
+    uint32_t c = wcnt[w * kBins + d];
+    wcnt[w * kBins + d] = tile_cnt;
+    tile_cnt += c;
   }
+  // Publish this tile's aggregate, then look back for the exclusive prefix.
+  unsigned long long* my = status + static_cast<uint64_t>(tile) * kBins + d;
+  const unsigned long long ep = static_cast<unsigned long long>(epoch) << 32;
+  if (tile == 0) {
+    *reinterpret_cast<volatile unsigned long long*>(my) = ep | kPrefixFlag | tile_cnt;
+  } else {
+    *reinterpret_cast<volatile unsigned long long*>(my) = ep | tile_cnt;
+  }
+  uint32_t excl = 0;
+  if (tile > 0) {
+    for (int64_t t = static_cast<int64_t>(tile) - 1; t >= 0; --t) {
+      const volatile unsigned long long* s = status + static_cast<uint64_t>(t) * kBins + d;
+      unsigned long long x;
+      do {
+        x = *s;
+      } while ((x >> 32) != epoch);
+      excl += static_cast<uint32_t>(x & (kPrefixFlag - 1));
+      if (x & kPrefixFlag) break;
+    }
+    *reinterpret_cast<volatile unsigned long long*>(my) = ep | kPrefixFlag | (excl + tile_cnt);
+  }
+  // Global digit start (exclusive scan of the pass histogram) + this tile's prefix.
+  const uint32_t start = block_excl_scan_bins(hist[d], scratch);
+  gbase[d] = start + excl;
+  block_off[d] = block_excl_scan_bins(tile_cnt, scratch);
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     uint64_t idx = warp_base + static_cast<uint64_t>(j) * 32 + lane;
     if (idx < n) {
-      uint32_t d = digit_of(k[j], shift);
-      uint32_t pos = block_off[d] + wcnt[warp * kBins + d] + r[j];
+      uint32_t dd = digit_of(k[j], shift);
+      uint32_t pos = block_off[dd] + wcnt[warp * kBins + dd] + r[j];
       skeys[pos] = k[j];
       svals[pos] = v[j];
     }
   }
   __syncthreads();
-  const uint32_t tile_n = static_cast<uint32_t>(n - tile_base < (uint64_t)kTileN ? n - tile_base : (uint64_t)kTileN);
+  const uint32_t tile_n =
+      static_cast<uint32_t>(n - tile_base < (uint64_t)kTileN ? n - tile_base : (uint64_t)kTileN);
   for (uint32_t p = threadIdx.x; p < tile_n; p += kBlock) {
     K key = skeys[p];
-    uint32_t d = digit_of(key, shift);
-    uint32_t g = gbase[d] + (p - block_off[d]);
+    uint32_t dd = digit_of(key, shift);
+    uint32_t g = gbase[dd] + (p - block_off[dd]);
     keys_out[g] = key;
     vals_out[g] = svals[p];
   }
 }
 
-// Scratch sizing for sorting n pairs.
+// Scratch words (u32 units) to sort up to n_max pairs: histograms, tile counters and
+// the look-back status words.
 template <typename K>
-inline size_t hist_words(uint64_t n) {
-  uint64_t tiles = (n + Tile<K>::kTile - 1) / Tile<K>::kTile;
-  return static_cast<size_t>(tiles ? tiles : 1) * kBins + kBins;
+inline size_t scratch_words(uint64_t n_max) {
+  uint64_t tiles = (n_max + Tile<K>::kTile - 1) / Tile<K>::kTile;
+  if (tiles == 0) tiles = 1;
+  return kMaxPasses * kBins + kMaxPasses * 2 + tiles * kBins * 2 + 2;
 }
 
-// Sorts (keys, vals) by key bits [0, key_bits). Ping-pongs between the (a) and (b)
-// buffers; returns true when the result lives in the (b) buffers. hist needs
-// hist_words<K>(n) words.
+// Sorts (keys, vals) by key bits [0, key_bits). The element count is n_dev[0] when
+// n_dev is given (device memory, <= n_max) else n_max. Ping-pongs between the (a) and
+// (b) buffers; returns true when the result lives in (b). scratch needs
+// scratch_words<K>(n_max) u32 words (8-byte aligned).
 template <typename K>
-inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b, uint32_t n,
-                       int key_bits, uint32_t* hist, cudaStream_t stream) {
-  if (n <= 1 || key_bits <= 0) return false;
+inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b, uint64_t n_max,
+                       const uint32_t* n_dev, int key_bits, uint32_t* scratch,
+                       cudaStream_t stream, int sms = 148) {
+  if (n_max <= 1 || key_bits <= 0) return false;
   static bool attr_set = false;
   if (!attr_set) {
-    HPS_CUDA(cudaFuncSetAttribute(downsweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HPS_CUDA(cudaFuncSetAttribute(pass_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tile<K>::kSmem)));
     attr_set = true;
   }
-  const uint32_t tiles = ceil_div(n, Tile<K>::kTile);
-  uint32_t* totals = hist + static_cast<size_t>(tiles) * kBins;
+  const int passes = (key_bits + kBits - 1) / kBits;
+  const uint32_t tiles = ceil_div(n_max, Tile<K>::kTile);
+  uint32_t* hist = scratch;                                  // [kMaxPasses][kBins]
+  uint32_t* tile_ctr = hist + kMaxPasses * kBins;            // [kMaxPasses * 2]
+  uint64_t off = (kMaxPasses * kBins + kMaxPasses * 2 + 1) & ~1ull;
+  unsigned long long* status = reinterpret_cast<unsigned long long*>(scratch + off);
+  HPS_CUDA(cudaMemsetAsync(scratch, 0, (kMaxPasses * kBins + kMaxPasses * 2) * sizeof(uint32_t),
+                           stream));
+  const uint32_t n_host = static_cast<uint32_t>(n_max);
+  const uint32_t hblocks = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms) * 4);
+  hist_kernel<K><<<hblocks, kBlock, 0, stream>>>(keys_a, n_dev, n_host, passes, hist);
   bool in_b = false;
-  for (int shift = 0; shift < key_bits; shift += kBits) {
+  for (int p = 0; p < passes; ++p) {
     const K* ki = in_b ? keys_b : keys_a;
     const uint32_t* vi = in_b ? vals_b : vals_a;
     K* ko = in_b ? keys_a : keys_b;
     uint32_t* vo = in_b ? vals_a : vals_b;
-    upsweep<K><<<tiles, kBlock, 0, stream>>>(ki, n, shift, hist, tiles);
-    scan_digits<<<kBins, 1024, 0, stream>>>(hist, tiles, totals);
-    downsweep<K><<<tiles, kBlock, Tile<K>::kSmem, stream>>>(ki, vi, ko, vo, n, shift, hist, totals,
-                                                             tiles);
-    HPS_LAUNCH_CHECK_N(3);
+    const uint32_t epoch = g_epoch.fetch_add(1) + 1;
+    pass_kernel<K><<<tiles, kBlock, Tile<K>::kSmem, stream>>>(
+        ki, vi, ko, vo, n_dev, n_host, p * kBits, hist + p * kBins, status, tile_ctr + p, epoch);
     in_b = !in_b;
   }
+  HPS_LAUNCH_CHECK_N(1 + passes);
   return in_b;
+}
+
+// Exclusive scan of one row of `tiles` u32 per block (blockIdx.x = row), in place;
+// totals[row] receives the row sum. Used for small host-sized scans.
+static __global__ void __launch_bounds__(1024) scan_digits(uint32_t* __restrict__ hist,
+                                                           uint32_t tiles,
+                                                           uint32_t* __restrict__ totals) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t carry;
+  uint32_t* row = hist + static_cast<uint64_t>(blockIdx.x) * tiles;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < tiles; base += 1024) {
+    uint32_t i = base + threadIdx.x;
+    uint32_t v = i < tiles ? row[i] : 0;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t s = warp_sums[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += y;
+      }
+      warp_sums[lane] = s;
+    }
+    __syncthreads();
+    uint32_t excl = carry + (warp ? warp_sums[warp - 1] : 0) + x - v;
+    if (i < tiles) row[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_sums[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) totals[blockIdx.x] = carry;
 }
 
 }  // namespace radix

@@ -212,8 +212,8 @@ Table* table_create(const hps_table_cfg& cfg) {
     d.opt = cfg.optimizer;
     HPS_CUDA(cudaMalloc(&d.ht, H * sizeof(HashEntry)));
     HPS_CUDA(cudaMalloc(&d.rows, C * d.stride * sizeof(float)));
-    HPS_CUDA(cudaMalloc(&d.ver, C * sizeof(uint32_t)));
-    HPS_CUDA(cudaMalloc(&d.tag, C * sizeof(uint32_t)));
+    HPS_CUDA(cudaMalloc(&d.vt, C * sizeof(uint2)));
+    HPS_CUDA(cudaMalloc(&d.cnt, C * sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.slot_id, C * sizeof(uint64_t)));
     HPS_CUDA(cudaMalloc(&d.special, sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.hwm, sizeof(uint32_t)));
@@ -239,6 +239,7 @@ Table* table_create(const hps_table_cfg& cfg) {
 void table_clear(Table* t, cudaStream_t st) {
   DevTable& d = t->d;
   HPS_CUDA(cudaMemsetAsync(d.ht, 0xff, t->ht_size * sizeof(HashEntry), st));
+  HPS_CUDA(cudaMemsetAsync(d.cnt, 0, static_cast<size_t>(d.capacity) * sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.special, 0xff, sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.hwm, 0, sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.ctr + kCtrOverflow, 0, sizeof(unsigned long long), st));
@@ -246,8 +247,8 @@ void table_clear(Table* t, cudaStream_t st) {
 
 void batch_free(Batch& b) {
   void* ptrs[] = {b.offsets, b.lgrp, b.slot, b.keys_a, b.vals_a, b.keys_b, b.vals_b, b.rv,
-                  b.new_slots, b.hist, b.small, b.skeys_a, b.skeys_b, b.sperm_a, b.sperm_b,
-                  b.sstart};
+                  b.new_slots, b.kind, b.hist, b.small, b.skeys_a, b.skeys_b, b.sperm_a,
+                  b.sperm_b, b.sstart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   Table* t = b.table;
@@ -266,7 +267,7 @@ void table_destroy(Table* t) {
     t->stage.free_all();
     t->prof.destroy();
     DevTable& d = t->d;
-    void* ptrs[] = {d.ht, d.rows, d.ver, d.tag, d.slot_id, d.special, d.hwm, d.ctr, t->d_salts};
+    void* ptrs[] = {d.ht, d.rows, d.vt, d.cnt, d.slot_id, d.special, d.hwm, d.ctr, t->d_salts};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (t->h_ctr) cudaFreeHost(t->h_ctr);
@@ -339,7 +340,9 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
       c = 0;
       ensure(*p, c, n);
     }
-    size_t hw = std::max(radix::hist_words<uint32_t>(n), radix::hist_words<uint64_t>(n));
+    c = 0;
+    ensure(b.kind, c, n);
+    size_t hw = radix::scratch_words<uint32_t>(n) + classify_status_words(n) + 2;
     if (hw > b.hist_cap) {
       c = 0;
       ensure(b.hist, c, hw);
@@ -363,7 +366,7 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
     ensure(b.sperm_b, c, B);
     c = 0;
     ensure(b.sstart, c, B + 1);
-    size_t hw = radix::hist_words<uint64_t>(B);
+    size_t hw = radix::scratch_words<uint64_t>(B);
     if (hw > b.hist_cap) {
       c = 0;
       ensure(b.hist, c, hw);
@@ -382,13 +385,13 @@ static int slot_key_bits(const Table* t) {
 }
 
 // Stable sort of the staged (keys_a = slot, vals_a = listing) pairs by slot: every
-// row's listings become one contiguous run in apply order.
-static void sort_slots(Batch& b, cudaStream_t st) {
+// row's listings become one contiguous run in apply order. n_dev: element count in
+// device memory (the compacted multi list), else b.N.
+static void sort_slots(Batch& b, const uint32_t* n_dev, cudaStream_t st) {
   Table* t = b.table;
   ProfScope p(t, "sort", st);
-  bool in_b = radix::sort_pairs<uint32_t>(b.keys_a, b.vals_a, b.keys_b, b.vals_b,
-                                          static_cast<uint32_t>(b.N), slot_key_bits(t), b.hist,
-                                          st);
+  bool in_b = radix::sort_pairs<uint32_t>(b.keys_a, b.vals_a, b.keys_b, b.vals_b, b.N, n_dev,
+                                          slot_key_bits(t), b.hist, st, t->sm_count);
   b.sorted_slot = in_b ? b.keys_b : b.keys_a;
   b.sorted_listing = in_b ? b.vals_b : b.vals_a;
 }
@@ -426,25 +429,38 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   b.N = N;
   HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
   launch_expand_groups(b.offsets, static_cast<uint32_t>(BF), b.lgrp, st);
+  // Sample keys that reorder the batch: every listing takes the sorted (multi) path.
   const bool permute = d_sk && B > 1;
+  b.all_multi = permute;
   {
     ProfScope p(t, "probe", st);
-    launch_probe(t->d, d_ids, N, b.slot, permute ? nullptr : b.keys_a,
-                 permute ? nullptr : b.vals_a, b.new_slots, &b.small[2], nullptr, st);
+    launch_probe(t->d, d_ids, N, b.slot, nullptr, nullptr, b.new_slots, &b.small[2], !permute,
+                 st);
   }
   launch_lazy_init(t->d, b.new_slots, &b.small[2], N, t->sm_count, st);
   if (permute) {
     // Apply order = ascending sample key: enumerate listings sample by sample in key
     // order before the stable slot sort.
     launch_sample_order(d_sk, B, b.skeys_a, b.sperm_a, st);
-    bool in_b = radix::sort_pairs<uint64_t>(b.skeys_a, b.sperm_a, b.skeys_b, b.sperm_b, B, 64,
-                                            b.hist, st);
+    bool in_b = radix::sort_pairs<uint64_t>(b.skeys_a, b.sperm_a, b.skeys_b, b.sperm_b, B,
+                                            nullptr, 64, b.hist, st, t->sm_count);
     const uint32_t* perm = in_b ? b.sperm_b : b.sperm_a;
     launch_sample_lengths(perm, b.offsets, B, F, b.sstart, st);
     launch_scan_inplace(b.sstart, B, b.sstart + B, st);
     launch_permuted_listing(perm, b.sstart, b.offsets, b.slot, B, F, b.keys_a, b.vals_a, st);
+    sort_slots(b, nullptr, st);
+  } else {
+    // Plan: rows listed once apply directly; the rest are compacted in listing order
+    // and sorted by slot (plan.cu).
+    {
+      ProfScope p(t, "plan", st);
+      const size_t sw = (radix::scratch_words<uint32_t>(b.N) + 1) & ~size_t(1);
+      launch_classify(b.slot, t->d.cnt, t->d.capacity, N, b.kind, b.keys_a, b.vals_a,
+                      &b.small[0], reinterpret_cast<unsigned long long*>(b.hist + sw),
+                      &b.small[4], st);
+    }
+    sort_slots(b, &b.small[0], st);
   }
-  sort_slots(b, st);
   b.registered = true;
   b.pulled = false;
   stg.finish(st);
@@ -474,7 +490,8 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   if (epoch != t->epoch) {
     // PsShard::apply_gradients epoch fence (embedding_ps.hpp:142-145): drop every
     // (sample, unique id) entry of the batch, count them.
-    launch_count_pairs(b.sorted_slot, b.sorted_listing, b.lgrp, b.F, b.N,
+    launch_count_pairs(b.all_multi ? nullptr : b.kind, b.N, b.sorted_slot, b.sorted_listing,
+                       b.lgrp, b.F, b.all_multi ? nullptr : &b.small[0], b.N,
                        t->d.ctr + kCtrStaleDrops, st);
     if (!(flags & HPS_ASYNC)) HPS_CUDA(cudaStreamSynchronize(st));
     if (accepted) *accepted = 0;
@@ -495,6 +512,9 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   a.sorted_slot = b.sorted_slot;
   a.sorted_listing = b.sorted_listing;
   a.n = b.N;
+  a.n_dev = b.all_multi ? nullptr : &b.small[0];
+  a.kind = b.kind;
+  a.slots = b.slot;
   a.lgrp = b.lgrp;
   a.offsets = b.offsets;
   a.F = b.F;
@@ -509,11 +529,17 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     a.rv32 = b.rv;
     a.tracked = 1;
   }
-  a.dry_run = 1;  // exact validation, runs only if the bound check was inconclusive
+  // Exact validation (dry runs), executed only if the bound check was inconclusive.
+  a.dry_run = 1;
+  if (!b.all_multi) launch_update_single(t->d, a, t->sm_count, st);
   launch_update(t->d, a, false, t->sm_count, st);
   a.dry_run = 0;
-  {
+  if (!b.all_multi) {
     ProfScope p(t, "update", st);
+    launch_update_single(t->d, a, t->sm_count, st);
+  }
+  {
+    ProfScope p(t, "update_multi", st);
     launch_update(t->d, a, false, t->sm_count, st);
   }
   if (accepted) *accepted = 1;
@@ -527,8 +553,9 @@ uint64_t batch_pairs(Batch& b) {
   if (!b.registered) return 0;
   Table* t = b.table;
   HPS_CUDA(cudaMemset(t->d.ctr + kCtrScratch, 0, sizeof(unsigned long long)));
-  launch_count_pairs(b.sorted_slot, b.sorted_listing, b.lgrp, b.F, b.N, t->d.ctr + kCtrScratch,
-                     nullptr);
+  launch_count_pairs(b.all_multi ? nullptr : b.kind, b.N, b.sorted_slot, b.sorted_listing,
+                     b.lgrp, b.F, b.all_multi ? nullptr : &b.small[0], b.N,
+                     t->d.ctr + kCtrScratch, nullptr);
   unsigned long long p = 0;
   HPS_CUDA(cudaMemcpy(&p, t->d.ctr + kCtrScratch, sizeof(p), cudaMemcpyDeviceToHost));
   return p;
@@ -545,7 +572,7 @@ void table_lookup(Table* t, const uint64_t* ids, uint64_t n, float* out_values,
   float* d_out = static_cast<float*>(stg.out(out_values, n * t->cfg.embedding_dim * sizeof(float)));
   uint64_t* d_ver = static_cast<uint64_t*>(stg.out(out_versions, n * sizeof(uint64_t)));
   HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
-  launch_probe(t->d, d_ids, n, b.slot, nullptr, nullptr, b.new_slots, &b.small[2], nullptr, st);
+  launch_probe(t->d, d_ids, n, b.slot, nullptr, nullptr, b.new_slots, &b.small[2], false, st);
   launch_lazy_init(t->d, b.new_slots, &b.small[2], n, t->sm_count, st);
   launch_gather(t->d, b.slot, n, d_out, d_ver, st);
   b.registered = false;
@@ -600,9 +627,10 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
   b.N = n;
   b.B = static_cast<uint32_t>(n);
   b.F = 1;
-  launch_probe(t->d, d_ids, n, b.slot, b.keys_a, b.vals_a, b.new_slots, &b.small[2], nullptr, st);
+  launch_probe(t->d, d_ids, n, b.slot, b.keys_a, b.vals_a, b.new_slots, &b.small[2], false, st);
   launch_lazy_init(t->d, b.new_slots, &b.small[2], n, t->sm_count, st);
-  sort_slots(b, st);
+  sort_slots(b, nullptr, st);
+  b.all_multi = true;
   UpdateArgs a{};
   a.sorted_slot = b.sorted_slot;
   a.sorted_listing = b.sorted_listing;

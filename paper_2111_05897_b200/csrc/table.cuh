@@ -5,8 +5,9 @@
 //                      (load <= 0.5); one probe = one 32-byte sector
 //   rows[C][2D]  f32   [w D | acc D] per slot -- the reference row (embedding_ps.hpp:64);
 //                      one contiguous 8D-byte segment, read-modify-written by the update
-//   ver[C]       u32   version (# distinct steps that wrote the row, embedding_ps.hpp:482)
-//   tag[C]       u32   step tag of the latest version bump (replaces the 16-deep ring)
+//   vt[C]        u32x2 {version (# distinct steps that wrote the row, embedding_ps.hpp:482),
+//                       step tag of the latest version bump (replaces the 16-deep ring)}
+//   cnt[C]       u32   listings of the row in the batch being planned (0 between batches)
 //   slot_id[C]   u64   id held by a slot (init seed, export)
 // Slots are handed out densely from a device high-water mark (lru_store.hpp:98).
 #pragma once
@@ -50,8 +51,8 @@ struct DevTable {
   float* rows;
   uint32_t D;
   uint32_t stride;  // floats per row (2D)
-  uint32_t* ver;
-  uint32_t* tag;
+  uint2* vt;        // {version, latest bump tag} per slot: one 8-byte word per row
+  uint32_t* cnt;    // per-slot listing counter of the batch being planned (plan.cu)
   uint64_t* slot_id;
   uint32_t capacity;
   uint32_t* hwm;
@@ -96,9 +97,12 @@ struct Batch {
   const uint32_t* sorted_listing = nullptr;
   uint32_t* rv = nullptr;         // [N] per-listing read version (u32) from the last pull
   uint32_t* new_slots = nullptr;  // [N] rows inserted by register (lazy-init queue)
-  uint32_t* hist = nullptr;
+  uint8_t* kind = nullptr;        // [N] plan: 1 = row listed once, 2 = multi (sorted path)
+  uint32_t* hist = nullptr;       // sort / plan scratch
   size_t hist_cap = 0;
-  uint32_t* small = nullptr;      // device scalars: [2] = rows inserted by this register
+  uint32_t* small = nullptr;      // device scalars: [0] = multi listings, [2] = rows inserted,
+                                  // [4] = plan tile counter
+  bool all_multi = false;         // plan skipped: every listing on the sorted path
   // sample-order permutation (sample_keys != NULL)
   uint64_t* skeys_a = nullptr;
   uint64_t* skeys_b = nullptr;
@@ -156,7 +160,7 @@ void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, 
 // (slot, i) pairs the apply-order sort consumes.
 void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* slots,
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
-                  uint32_t* new_count, const unsigned long long* gate, cudaStream_t st);
+                  uint32_t* new_count, bool count, cudaStream_t st);
 void launch_lazy_init(const DevTable& t, const uint32_t* new_slots, const uint32_t* new_count,
                       uint64_t max_new, int sms, cudaStream_t st);
 void launch_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* out_values,
@@ -173,7 +177,10 @@ void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B,
 struct UpdateArgs {
   const uint32_t* sorted_slot;
   const uint32_t* sorted_listing;
-  uint64_t n;  // sorted elements
+  uint64_t n;            // sorted elements (multi kernel) / listings (single kernel)
+  const uint32_t* n_dev; // multi kernel: element count in device memory (overrides n)
+  const uint8_t* kind;   // single kernel: plan kinds per listing
+  const uint32_t* slots; // single kernel: slot per listing
   // batch mode
   const uint32_t* lgrp;
   const uint32_t* offsets;
@@ -191,8 +198,16 @@ struct UpdateArgs {
   int dry_run;  // compute + validate contributions only
 };
 void launch_update(const DevTable& t, const UpdateArgs& a, bool direct, int sms, cudaStream_t st);
-void launch_count_pairs(const uint32_t* ss, const uint32_t* sl, const uint32_t* lgrp, uint32_t F,
-                        uint64_t n, unsigned long long* ctr, cudaStream_t st);
+void launch_update_single(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
+void launch_count_pairs(const uint8_t* kind, uint64_t n_all, const uint32_t* ss,
+                        const uint32_t* sl, const uint32_t* lgrp, uint32_t F,
+                        const uint32_t* n_multi_dev, uint64_t n_multi_host,
+                        unsigned long long* ctr, cudaStream_t st);
+// plan.cu
+void launch_classify(const uint32_t* slots, const uint32_t* cnt, uint32_t capacity, uint64_t n,
+                     uint8_t* kind, uint32_t* mkeys, uint32_t* mvals, uint32_t* n_multi,
+                     unsigned long long* status, uint32_t* tile_ctr, cudaStream_t st);
+size_t classify_status_words(uint64_t n);
 
 void launch_sample_order(const uint64_t* sample_keys, uint32_t B, uint64_t* keys_out,
                          uint32_t* perm_out, cudaStream_t st);
