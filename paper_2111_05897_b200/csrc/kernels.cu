@@ -52,7 +52,8 @@ __device__ uint32_t alloc_slot(const DevTable& t, uint64_t id, uint32_t* new_slo
 // entries; the inserting thread publishes the slot, racing readers of the same id
 // spin on that (single, in-flight) publication.
 __device__ uint32_t find_or_insert(const DevTable& t, uint64_t id, uint32_t* new_slots,
-                                   uint32_t* new_count, bool insert) {
+                                   uint32_t* new_count, bool insert, uint64_t* entry = nullptr) {
+  if (entry) *entry = kSpecialEntry;
   if (id == kEmptyKey) {
     uint32_t s = ld_volatile(t.special);
     if (s == kSpecialAbsent) {
@@ -82,6 +83,7 @@ __device__ uint32_t find_or_insert(const DevTable& t, uint64_t id, uint32_t* new
         uint32_t slot = alloc_slot(t, id, new_slots, new_count);
         __threadfence();
         atomicExch(&e->slot, slot);
+        if (entry) *entry = h;
         return slot;
       }
       k = old;
@@ -90,6 +92,7 @@ __device__ uint32_t find_or_insert(const DevTable& t, uint64_t id, uint32_t* new
     if (k == id) {
       uint32_t v = static_cast<uint32_t>(sv);
       while (v == kPending) v = ld_volatile(&e->slot);
+      if (entry) *entry = h;
       return v;
     }
     h = (h + 1) & t.ht_mask;
@@ -139,13 +142,18 @@ __global__ void __launch_bounds__(256)
     probe_kernel(DevTable t, const uint64_t* __restrict__ ids, uint64_t n,
                  uint32_t* __restrict__ slots, uint32_t* __restrict__ sort_keys,
                  uint32_t* __restrict__ sort_vals, uint32_t* __restrict__ new_slots,
-                 uint32_t* __restrict__ new_count, bool count) {
+                 uint32_t* __restrict__ new_count, uint32_t* __restrict__ eidx) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t s = find_or_insert(t, ids[i], new_slots, new_count, true);
+    uint64_t e;
+    uint32_t s = find_or_insert(t, ids[i], new_slots, new_count, true, &e);
     slots[i] = s;
-    // Batch plan: count the row's listings (fire-and-forget reduction, plan.cu).
-    if (count && slot_ok(t, s)) atomicAdd(&t.cnt[s], 1u);
+    if (eidx) {
+      // Batch plan: count the row's listings in the entry just probed (same sector,
+      // fire-and-forget reduction; plan.cu).
+      eidx[i] = static_cast<uint32_t>(e);
+      if (slot_ok(t, s)) atomicAdd(e == kSpecialEntry ? t.special_cnt : &t.ht[e].cnt, 1u);
+    }
     if (sort_keys) {
       sort_keys[i] = s;
       sort_vals[i] = static_cast<uint32_t>(i);
@@ -155,10 +163,26 @@ __global__ void __launch_bounds__(256)
 
 void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* slots,
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
-                  uint32_t* new_count, bool count, cudaStream_t st) {
+                  uint32_t* new_count, uint32_t* eidx, cudaStream_t st) {
   if (!n) return;
   probe_kernel<<<ceil_div(n, 256), 256, 0, st>>>(t, ids, n, slots, sort_keys, sort_vals,
-                                                 new_slots, new_count, count);
+                                                 new_slots, new_count, eidx);
+  HPS_LAUNCH_CHECK();
+}
+
+// Empty index: every key kEmptyKey, every slot kPending, every batch counter 0.
+__global__ void ht_clear_kernel(HashEntry* __restrict__ ht, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    ulonglong2 v = make_ulonglong2(kEmptyKey, static_cast<unsigned long long>(kPending));
+    *reinterpret_cast<ulonglong2*>(ht + i) = v;
+  }
+}
+
+void launch_ht_clear(const DevTable& t, cudaStream_t st) {
+  const uint64_t n = t.ht_mask + 1;
+  ht_clear_kernel<<<std::min<uint64_t>(ceil_div(n, 256), 148 * 64), 256, 0, st>>>(t.ht, n);
+  HPS_CUDA(cudaMemsetAsync(t.special_cnt, 0, sizeof(uint32_t), st));
   HPS_LAUNCH_CHECK();
 }
 
@@ -245,91 +269,6 @@ void launch_peek(const DevTable& t, const uint64_t* ids, uint64_t n, float* out_
   if (!n) return;
   peek_kernel<<<std::min<uint64_t>(ceil_div(n, 8), 148 * 32), 256, 0, st>>>(
       t, ids, n, out_w, out_acc, out_ver, out_present);
-  HPS_LAUNCH_CHECK();
-}
-
-// ---- pooling (EmbeddingWorker::serve_pull, embedding_worker.hpp:541-557) ----------------
-// One row group per (sample, group) segment: acc_d = sum over listings, in listing
-// order, of (double)row[d] (duplicates counted); out = float(acc * scale) with
-// scale = 1.0/n (mean) or 1.0 (sum); empty segments write zeros. Also emits the
-// per-listing read version (PullResult::read_versions).
-
-template <int V, int L, bool kGuard>
-__global__ void __launch_bounds__(256)
-    pool_kernel(DevTable t, const uint32_t* __restrict__ offsets,
-                const uint32_t* __restrict__ slots, uint32_t BF, int mean,
-                float* __restrict__ out, uint64_t* __restrict__ out_rv64,
-                uint32_t* __restrict__ out_rv32) {
-  using G = Geo<V, L, kGuard>;
-  const int ln = G::lane();
-  const uint32_t D = t.D;
-  const int chunks = kGuard ? (D + G::kSpan - 1) / G::kSpan : 1;
-  for (uint64_t sg = G::group(); sg < BF; sg += G::groups()) {
-    const uint32_t a = offsets[sg], e = offsets[sg + 1];
-    // Empty groups pool to zeros (embedding_worker.hpp:543): keep scale finite there.
-    const double scale = (mean && e > a) ? __drcp_rn(static_cast<double>(e - a)) : 1.0;
-    for (int c = 0; c < chunks; ++c) {
-      const uint32_t d0 = c * G::kSpan + ln * V;
-      if (kGuard && d0 >= D) break;
-      double acc[V];
-#pragma unroll
-      for (int k = 0; k < V; ++k) acc[k] = 0.0;
-      uint32_t i = a;
-      // Two listings in flight per iteration for memory-level parallelism.
-      for (; i + 1 < e; i += 2) {
-        uint32_t s0 = slots[i], s1 = slots[i + 1];
-        float r0[V], r1[V];
-        if (slot_ok(t, s0)) load_vec<V>(t.rows + (uint64_t)s0 * t.stride + d0, r0);
-        else for (int k = 0; k < V; ++k) r0[k] = 0.0f;
-        if (slot_ok(t, s1)) load_vec<V>(t.rows + (uint64_t)s1 * t.stride + d0, r1);
-        else for (int k = 0; k < V; ++k) r1[k] = 0.0f;
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          acc[k] = __dadd_rn(acc[k], static_cast<double>(r0[k]));
-          acc[k] = __dadd_rn(acc[k], static_cast<double>(r1[k]));
-        }
-        if (c == 0 && ln == 0) {
-          uint32_t v0 = slot_ok(t, s0) ? t.vt[s0].x : 0, v1 = slot_ok(t, s1) ? t.vt[s1].x : 0;
-          if (out_rv64) out_rv64[i] = v0, out_rv64[i + 1] = v1;
-          if (out_rv32) out_rv32[i] = v0, out_rv32[i + 1] = v1;
-        }
-      }
-      if (i < e) {
-        uint32_t s0 = slots[i];
-        float r0[V];
-        if (slot_ok(t, s0)) load_vec<V>(t.rows + (uint64_t)s0 * t.stride + d0, r0);
-        else for (int k = 0; k < V; ++k) r0[k] = 0.0f;
-#pragma unroll
-        for (int k = 0; k < V; ++k) acc[k] = __dadd_rn(acc[k], static_cast<double>(r0[k]));
-        if (c == 0 && ln == 0) {
-          uint32_t v0 = slot_ok(t, s0) ? t.vt[s0].x : 0;
-          if (out_rv64) out_rv64[i] = v0;
-          if (out_rv32) out_rv32[i] = v0;
-        }
-      }
-      float o[V];
-#pragma unroll
-      for (int k = 0; k < V; ++k) o[k] = __double2float_rn(__dmul_rn(acc[k], scale));
-      float* dst = out + sg * D + d0;
-      if (kGuard) {
-        for (int k = 0; k < V; ++k)
-          if (d0 + k < D) dst[k] = o[k];
-      } else {
-        store_vec_cs<V>(dst, o);
-      }
-    }
-  }
-}
-
-void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,
-                 int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32, cudaStream_t st) {
-  if (!BF) return;
-  HPS_DISPATCH_DIM(t.D, {
-    uint64_t groups_per_block = 256 / L;
-    uint32_t blocks = std::min<uint64_t>(ceil_div(BF, groups_per_block), 148ull * 32);
-    pool_kernel<V, L, G><<<blocks, 256, 0, st>>>(t, offsets, slots, BF, mean, out, out_rv64,
-                                                 out_rv32);
-  });
   HPS_LAUNCH_CHECK();
 }
 

@@ -1,14 +1,15 @@
 // Per-batch apply plan: which listings can be applied independently and which need
 // the ordered per-row recurrence.
 //
-// During the probe every listing adds 1 to its row's batch counter (cnt[slot]). A row
-// listed once in the batch ("single") gets exactly one optimizer application, so its
-// listing needs no ordering at all -- for the one-hot Criteo shape that is >99% of all
-// listings. Listings of rows hit more than once ("multi") are compacted, in listing
-// (= apply) order, by a single-pass chained scan, and only they go through the stable
-// slot sort. The counters are reset by the update that consumes them; a batch that is
-// never pushed leaves them high, which can only move later rows from the single path
-// to the (always correct) multi path.
+// During the probe every listing adds 1 to its row's batch counter, which lives in
+// the row's hash entry (the sector the probe just read, so counting costs no extra
+// DRAM traffic). A row listed once in the batch ("single") gets exactly one optimizer
+// application, so its listing needs no ordering at all -- for the one-hot Criteo
+// shape that is >99% of all listings. Listings of rows hit more than once ("multi")
+// are compacted, in listing (= apply) order, by a single-pass chained scan, and only
+// they go through the stable slot sort. The counters are reset by the update that
+// consumes them; a batch that is never pushed leaves them high, which can only move
+// later rows from the single path to the (always correct) multi path.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -32,8 +33,8 @@ constexpr int kPlanTile = kPlanBlock * kPlanItems;
 // dynamically numbered; tile prefixes by decoupled look-back (status words as in
 // radix_sort.cuh: [63:32] epoch, [31] prefix flag, [30:0] count).
 __global__ void __launch_bounds__(kPlanBlock)
-    classify_kernel(const uint32_t* __restrict__ slots, const uint32_t* __restrict__ cnt,
-                    uint32_t capacity, uint64_t n, uint8_t* __restrict__ kind,
+    classify_kernel(DevTable t, const uint32_t* __restrict__ slots,
+                    const uint32_t* __restrict__ eidx, uint64_t n, uint8_t* __restrict__ kind,
                     uint32_t* __restrict__ mkeys, uint32_t* __restrict__ mvals,
                     uint32_t* __restrict__ n_multi, unsigned long long* status,
                     uint32_t* tile_ctr, uint32_t epoch) {
@@ -44,27 +45,29 @@ __global__ void __launch_bounds__(kPlanBlock)
   const uint32_t tiles = static_cast<uint32_t>((n + kPlanTile - 1) / kPlanTile);
   if (tile >= tiles) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // Blocked layout per warp: lane handles kPlanItems consecutive listings of its warp's
-  // stripe, so the flag order (warp, lane, item) is listing order.
+  // Lane owns kPlanItems consecutive listings of its warp's stripe, so the flag order
+  // (warp, lane, item) is listing order.
   const uint64_t base = static_cast<uint64_t>(tile) * kPlanTile +
-                        static_cast<uint64_t>(warp) * 32 * kPlanItems;
-  uint32_t s[kPlanItems];
-  bool m[kPlanItems];
-  uint32_t mine = 0;
+                        static_cast<uint64_t>(warp) * 32 * kPlanItems +
+                        static_cast<uint64_t>(lane) * kPlanItems;
+  uint32_t s[kPlanItems], e[kPlanItems], c[kPlanItems];
 #pragma unroll
   for (int j = 0; j < kPlanItems; ++j) {
-    // coalesced: item j of every lane is j*32 + lane; remapped below to blocked order
-    uint64_t i = base + static_cast<uint64_t>(lane) * kPlanItems + j;
-    s[j] = i < n ? slots[i] : kInvalidSlot;
+    const bool valid = base + j < n;
+    s[j] = valid ? slots[base + j] : kInvalidSlot;
+    e[j] = valid ? eidx[base + j] : 0u;
   }
 #pragma unroll
+  for (int j = 0; j < kPlanItems; ++j)
+    c[j] = s[j] < t.capacity ? (e[j] == kSpecialEntry ? *t.special_cnt : t.ht[e[j]].cnt) : 0u;
+  uint32_t mine = 0;
+  uint32_t mbits = 0;
+#pragma unroll
   for (int j = 0; j < kPlanItems; ++j) {
-    uint64_t i = base + static_cast<uint64_t>(lane) * kPlanItems + j;
-    bool valid = i < n;
-    bool multi = valid && s[j] < capacity && cnt[s[j]] > 1;
-    m[j] = multi;
+    const bool multi = c[j] > 1;
+    mbits |= multi ? (1u << j) : 0u;
     mine += multi;
-    if (valid) kind[i] = multi ? 2 : 1;
+    if (base + j < n) kind[base + j] = multi ? 2 : 1;
   }
   // warp-inclusive scan of per-lane counts
   uint32_t x = mine;
@@ -78,9 +81,9 @@ __global__ void __launch_bounds__(kPlanBlock)
   if (threadIdx.x == 0) {
     uint32_t tot = 0;
     for (int w = 0; w < kPlanBlock / 32; ++w) {
-      uint32_t c = s_warp[w];
+      uint32_t cw = s_warp[w];
       s_warp[w] = tot;
-      tot += c;
+      tot += cw;
     }
     const unsigned long long ep = static_cast<unsigned long long>(epoch) << 32;
     volatile unsigned long long* my = status + tile;
@@ -89,8 +92,8 @@ __global__ void __launch_bounds__(kPlanBlock)
       *my = ep | radix::kPrefixFlag | tot;
     } else {
       *my = ep | tot;
-      for (int64_t t = static_cast<int64_t>(tile) - 1; t >= 0; --t) {
-        const volatile unsigned long long* st = status + t;
+      for (int64_t tt = static_cast<int64_t>(tile) - 1; tt >= 0; --tt) {
+        const volatile unsigned long long* st = status + tt;
         unsigned long long v;
         do {
           v = *st;
@@ -107,16 +110,15 @@ __global__ void __launch_bounds__(kPlanBlock)
   uint32_t pos = s_excl + s_warp[warp] + x - mine;
 #pragma unroll
   for (int j = 0; j < kPlanItems; ++j) {
-    if (m[j]) {
-      uint64_t i = base + static_cast<uint64_t>(lane) * kPlanItems + j;
+    if (mbits & (1u << j)) {
       mkeys[pos] = s[j];
-      mvals[pos] = static_cast<uint32_t>(i);
+      mvals[pos] = static_cast<uint32_t>(base + j);
       ++pos;
     }
   }
 }
 
-void launch_classify(const uint32_t* slots, const uint32_t* cnt, uint32_t capacity, uint64_t n,
+void launch_classify(const DevTable& t, const uint32_t* slots, const uint32_t* eidx, uint64_t n,
                      uint8_t* kind, uint32_t* mkeys, uint32_t* mvals, uint32_t* n_multi,
                      unsigned long long* status, uint32_t* tile_ctr, cudaStream_t st) {
   if (!n) {
@@ -126,8 +128,8 @@ void launch_classify(const uint32_t* slots, const uint32_t* cnt, uint32_t capaci
   HPS_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st));
   const uint32_t tiles = ceil_div(n, kPlanTile);
   const uint32_t epoch = radix::g_epoch.fetch_add(1) + 1;
-  classify_kernel<<<tiles, kPlanBlock, 0, st>>>(slots, cnt, capacity, n, kind, mkeys, mvals,
-                                                n_multi, status, tile_ctr, epoch);
+  classify_kernel<<<tiles, kPlanBlock, 0, st>>>(t, slots, eidx, n, kind, mkeys, mvals, n_multi,
+                                                status, tile_ctr, epoch);
   HPS_LAUNCH_CHECK();
 }
 

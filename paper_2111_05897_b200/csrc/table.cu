@@ -177,8 +177,9 @@ Table* table_create(const hps_table_cfg& cfg) {
   if (cfg.shard_count == 0) throw Error(HPS_E_CONFIG, "hps_table_create: shard_count must be positive");
   if (!cfg.shard_salts) throw Error(HPS_E_CONFIG, "hps_table_create: shard_salts required");
   if (cfg.embedding_dim == 0) throw Error(HPS_E_CONFIG, "hps_table_create: embedding_dim must be positive");
-  if (cfg.capacity == 0 || cfg.capacity >= kInvalidSlot)
-    throw Error(HPS_E_CONFIG, "hps_table_create: capacity must be in [1, 2^32-3]");
+  // < 2^31 rows keeps every hash-entry index (H <= 2^32) in 32 bits.
+  if (cfg.capacity == 0 || cfg.capacity >= (1ull << 31))
+    throw Error(HPS_E_CONFIG, "hps_table_create: capacity must be in [1, 2^31)");
   if (cfg.optimizer != HPS_ADAGRAD && cfg.optimizer != HPS_SGD)
     throw Error(HPS_E_CONFIG, "hps_table_create: unknown optimizer");
   if (cfg.world_size == 0 || cfg.owner_rank >= cfg.world_size)
@@ -213,7 +214,7 @@ Table* table_create(const hps_table_cfg& cfg) {
     HPS_CUDA(cudaMalloc(&d.ht, H * sizeof(HashEntry)));
     HPS_CUDA(cudaMalloc(&d.rows, C * d.stride * sizeof(float)));
     HPS_CUDA(cudaMalloc(&d.vt, C * sizeof(uint2)));
-    HPS_CUDA(cudaMalloc(&d.cnt, C * sizeof(uint32_t)));
+    HPS_CUDA(cudaMalloc(&d.special_cnt, sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.slot_id, C * sizeof(uint64_t)));
     HPS_CUDA(cudaMalloc(&d.special, sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.hwm, sizeof(uint32_t)));
@@ -234,21 +235,19 @@ Table* table_create(const hps_table_cfg& cfg) {
   }
 }
 
-// Empties the index and the row store (LruStore::clear + PsShard state reset). Key
-// kEmptyKey and slot kPending are both all-ones, so one memset clears the index.
+// Empties the index and the row store (LruStore::clear + PsShard state reset).
 void table_clear(Table* t, cudaStream_t st) {
   DevTable& d = t->d;
-  HPS_CUDA(cudaMemsetAsync(d.ht, 0xff, t->ht_size * sizeof(HashEntry), st));
-  HPS_CUDA(cudaMemsetAsync(d.cnt, 0, static_cast<size_t>(d.capacity) * sizeof(uint32_t), st));
+  launch_ht_clear(d, st);
   HPS_CUDA(cudaMemsetAsync(d.special, 0xff, sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.hwm, 0, sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.ctr + kCtrOverflow, 0, sizeof(unsigned long long), st));
 }
 
 void batch_free(Batch& b) {
-  void* ptrs[] = {b.offsets, b.lgrp, b.slot, b.keys_a, b.vals_a, b.keys_b, b.vals_b, b.rv,
-                  b.new_slots, b.kind, b.hist, b.small, b.skeys_a, b.skeys_b, b.sperm_a,
-                  b.sperm_b, b.sstart};
+  void* ptrs[] = {b.offsets, b.lgrp,  b.slot, b.eidx,    b.keys_a,  b.vals_a,
+                  b.keys_b,  b.vals_b, b.rv,  b.new_slots, b.kind,  b.hist,
+                  b.small,   b.skeys_a, b.skeys_b, b.sperm_a, b.sperm_b, b.sstart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   Table* t = b.table;
@@ -267,7 +266,8 @@ void table_destroy(Table* t) {
     t->stage.free_all();
     t->prof.destroy();
     DevTable& d = t->d;
-    void* ptrs[] = {d.ht, d.rows, d.vt, d.cnt, d.slot_id, d.special, d.hwm, d.ctr, t->d_salts};
+    void* ptrs[] = {d.ht,      d.rows, d.vt,  d.special_cnt, d.slot_id,
+                    d.special, d.hwm,  d.ctr, t->d_salts};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (t->h_ctr) cudaFreeHost(t->h_ctr);
@@ -334,8 +334,8 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
   uint64_t n = std::max<uint64_t>(N, 1);
   if (n > b.cap_N) {
     uint64_t c = 0;
-    uint32_t** bufs[] = {&b.lgrp, &b.slot, &b.keys_a, &b.vals_a, &b.keys_b, &b.vals_b,
-                         &b.rv, &b.new_slots};
+    uint32_t** bufs[] = {&b.lgrp, &b.slot,   &b.eidx, &b.keys_a,   &b.vals_a,
+                         &b.keys_b, &b.vals_b, &b.rv,   &b.new_slots};
     for (uint32_t** p : bufs) {
       c = 0;
       ensure(*p, c, n);
@@ -434,8 +434,8 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   b.all_multi = permute;
   {
     ProfScope p(t, "probe", st);
-    launch_probe(t->d, d_ids, N, b.slot, nullptr, nullptr, b.new_slots, &b.small[2], !permute,
-                 st);
+    launch_probe(t->d, d_ids, N, b.slot, nullptr, nullptr, b.new_slots, &b.small[2],
+                 permute ? nullptr : b.eidx, st);
   }
   launch_lazy_init(t->d, b.new_slots, &b.small[2], N, t->sm_count, st);
   if (permute) {
@@ -455,7 +455,7 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     {
       ProfScope p(t, "plan", st);
       const size_t sw = (radix::scratch_words<uint32_t>(b.N) + 1) & ~size_t(1);
-      launch_classify(b.slot, t->d.cnt, t->d.capacity, N, b.kind, b.keys_a, b.vals_a,
+      launch_classify(t->d, b.slot, b.eidx, N, b.kind, b.keys_a, b.vals_a,
                       &b.small[0], reinterpret_cast<unsigned long long*>(b.hist + sw),
                       &b.small[4], st);
     }
@@ -475,7 +475,7 @@ void batch_pull(Batch& b, int agg, float* out_pooled, uint64_t* out_rv, cudaStre
   uint64_t* d_rv = static_cast<uint64_t*>(stg.out(out_rv, b.N * sizeof(uint64_t)));
   {
     ProfScope p(t, "pool", st);
-    launch_pool(t->d, b.offsets, b.slot, static_cast<uint32_t>(BF), agg == HPS_MEAN ? 1 : 0,
+    launch_pool(t->d, b.offsets, b.slot, static_cast<uint32_t>(BF), b.N, agg == HPS_MEAN ? 1 : 0,
                 d_out, d_rv, b.rv, st);
   }
   b.pulled = true;
@@ -515,6 +515,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   a.n_dev = b.all_multi ? nullptr : &b.small[0];
   a.kind = b.kind;
   a.slots = b.slot;
+  a.eidx = b.all_multi ? nullptr : b.eidx;
   a.lgrp = b.lgrp;
   a.offsets = b.offsets;
   a.F = b.F;
@@ -572,7 +573,7 @@ void table_lookup(Table* t, const uint64_t* ids, uint64_t n, float* out_values,
   float* d_out = static_cast<float*>(stg.out(out_values, n * t->cfg.embedding_dim * sizeof(float)));
   uint64_t* d_ver = static_cast<uint64_t*>(stg.out(out_versions, n * sizeof(uint64_t)));
   HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
-  launch_probe(t->d, d_ids, n, b.slot, nullptr, nullptr, b.new_slots, &b.small[2], false, st);
+  launch_probe(t->d, d_ids, n, b.slot, nullptr, nullptr, b.new_slots, &b.small[2], nullptr, st);
   launch_lazy_init(t->d, b.new_slots, &b.small[2], n, t->sm_count, st);
   launch_gather(t->d, b.slot, n, d_out, d_ver, st);
   b.registered = false;
@@ -627,7 +628,7 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
   b.N = n;
   b.B = static_cast<uint32_t>(n);
   b.F = 1;
-  launch_probe(t->d, d_ids, n, b.slot, b.keys_a, b.vals_a, b.new_slots, &b.small[2], false, st);
+  launch_probe(t->d, d_ids, n, b.slot, b.keys_a, b.vals_a, b.new_slots, &b.small[2], nullptr, st);
   launch_lazy_init(t->d, b.new_slots, &b.small[2], n, t->sm_count, st);
   sort_slots(b, nullptr, st);
   b.all_multi = true;

@@ -7,7 +7,6 @@
 //                      one contiguous 8D-byte segment, read-modify-written by the update
 //   vt[C]        u32x2 {version (# distinct steps that wrote the row, embedding_ps.hpp:482),
 //                       step tag of the latest version bump (replaces the 16-deep ring)}
-//   cnt[C]       u32   listings of the row in the batch being planned (0 between batches)
 //   slot_id[C]   u64   id held by a slot (init seed, export)
 // Slots are handed out densely from a device high-water mark (lru_store.hpp:98).
 #pragma once
@@ -36,12 +35,15 @@ enum CounterIdx : int {
   kCtrCount = 32
 };
 
-// One 16-byte index entry: a probe touches a single 32-byte sector.
+// One 16-byte index entry: a probe touches a single 32-byte sector. `cnt` counts the
+// row's listings in the batch being planned (plan.cu): it shares the probed sector,
+// so counting costs no extra DRAM traffic; 0 between batches.
 struct __align__(16) HashEntry {
   unsigned long long key;  // kEmptyKey when free
   uint32_t slot;           // kPending while the inserting thread publishes it
-  uint32_t pad;
+  uint32_t cnt;
 };
+constexpr uint32_t kSpecialEntry = 0xffffffffu;  // entry index of id == kEmptyKey
 
 struct DevTable {
   HashEntry* ht;
@@ -51,8 +53,8 @@ struct DevTable {
   float* rows;
   uint32_t D;
   uint32_t stride;  // floats per row (2D)
-  uint2* vt;        // {version, latest bump tag} per slot: one 8-byte word per row
-  uint32_t* cnt;    // per-slot listing counter of the batch being planned (plan.cu)
+  uint2* vt;           // {version, latest bump tag} per slot: one 8-byte word per row
+  uint32_t* special_cnt;  // batch listing counter of id == kEmptyKey (no hash entry)
   uint64_t* slot_id;
   uint32_t capacity;
   uint32_t* hwm;
@@ -89,6 +91,7 @@ struct Batch {
   uint32_t* offsets = nullptr;    // [B*F+1] our copy of the CSR offsets
   uint32_t* lgrp = nullptr;       // [N] listing -> b*F+g
   uint32_t* slot = nullptr;       // [N] listing -> table slot
+  uint32_t* eidx = nullptr;       // [N] listing -> hash entry index (batch counters)
   uint32_t* keys_a = nullptr;     // [N] sort ping-pong (slot keys)
   uint32_t* vals_a = nullptr;     //     (listing values)
   uint32_t* keys_b = nullptr;
@@ -158,9 +161,11 @@ void launch_route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cu
 void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st);
 // slots[i] = find_or_insert(ids[i]); when sort_keys/sort_vals are given also writes the
 // (slot, i) pairs the apply-order sort consumes.
+// eidx != null: also count the row's listings in its hash entry and record the entry.
 void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* slots,
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
-                  uint32_t* new_count, bool count, cudaStream_t st);
+                  uint32_t* new_count, uint32_t* eidx, cudaStream_t st);
+void launch_ht_clear(const DevTable& t, cudaStream_t st);
 void launch_lazy_init(const DevTable& t, const uint32_t* new_slots, const uint32_t* new_count,
                       uint64_t max_new, int sms, cudaStream_t st);
 void launch_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* out_values,
@@ -168,7 +173,8 @@ void launch_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* 
 void launch_peek(const DevTable& t, const uint64_t* ids, uint64_t n, float* out_w, float* out_acc,
                  uint64_t* out_versions, uint8_t* out_present, cudaStream_t st);
 void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,
-                 int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32, cudaStream_t st);
+                 uint64_t N, int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32,
+                 cudaStream_t st);
 void launch_check_direct(const float* grads, uint64_t n_floats, unsigned long long* ctr,
                          cudaStream_t st);
 void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
@@ -181,6 +187,7 @@ struct UpdateArgs {
   const uint32_t* n_dev; // multi kernel: element count in device memory (overrides n)
   const uint8_t* kind;   // single kernel: plan kinds per listing
   const uint32_t* slots; // single kernel: slot per listing
+  const uint32_t* eidx;  // batch mode: hash entry per listing (counter reset); may be null
   // batch mode
   const uint32_t* lgrp;
   const uint32_t* offsets;
@@ -204,7 +211,7 @@ void launch_count_pairs(const uint8_t* kind, uint64_t n_all, const uint32_t* ss,
                         const uint32_t* n_multi_dev, uint64_t n_multi_host,
                         unsigned long long* ctr, cudaStream_t st);
 // plan.cu
-void launch_classify(const uint32_t* slots, const uint32_t* cnt, uint32_t capacity, uint64_t n,
+void launch_classify(const DevTable& t, const uint32_t* slots, const uint32_t* eidx, uint64_t n,
                      uint8_t* kind, uint32_t* mkeys, uint32_t* mvals, uint32_t* n_multi,
                      unsigned long long* status, uint32_t* tile_ctr, cudaStream_t st);
 size_t classify_status_words(uint64_t n);
