@@ -143,10 +143,35 @@ __global__ void __launch_bounds__(256)
                  uint32_t* __restrict__ slots, uint32_t* __restrict__ sort_keys,
                  uint32_t* __restrict__ sort_vals, uint32_t* __restrict__ new_slots,
                  uint32_t* __restrict__ new_count, uint32_t* __restrict__ eidx) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
+  // kProbeILP listings per thread: their first probes are issued back to back (the
+  // common case -- key found in its home entry -- then costs one round trip for all).
+  constexpr int kProbeILP = 4;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x * kProbeILP + threadIdx.x;
+  uint64_t id[kProbeILP], h[kProbeILP];
+  ulonglong2 kv[kProbeILP];
+#pragma unroll
+  for (int k = 0; k < kProbeILP; ++k) {
+    const uint64_t i = base + static_cast<uint64_t>(k) * blockDim.x;
+    id[k] = i < n ? ids[i] : kEmptyKey;
+  }
+#pragma unroll
+  for (int k = 0; k < kProbeILP; ++k) {
+    h[k] = mix64(id[k] ^ kTableHashSalt) >> t.ht_shift;
+    kv[k] = id[k] != kEmptyKey ? __ldcg(reinterpret_cast<const ulonglong2*>(t.ht + h[k]))
+                               : make_ulonglong2(0, 0);
+  }
+#pragma unroll
+  for (int k = 0; k < kProbeILP; ++k) {
+    const uint64_t i = base + static_cast<uint64_t>(k) * blockDim.x;
+    if (i >= n) break;
     uint64_t e;
-    uint32_t s = find_or_insert(t, ids[i], new_slots, new_count, true, &e);
+    uint32_t s;
+    if (id[k] != kEmptyKey && kv[k].x == id[k] && static_cast<uint32_t>(kv[k].y) != kPending) {
+      s = static_cast<uint32_t>(kv[k].y);  // hit in the home entry
+      e = h[k];
+    } else {
+      s = find_or_insert(t, id[k], new_slots, new_count, true, &e);
+    }
     slots[i] = s;
     if (eidx) {
       // Batch plan: count the row's listings in the entry just probed (same sector,
@@ -165,8 +190,8 @@ void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* 
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
                   uint32_t* new_count, uint32_t* eidx, cudaStream_t st) {
   if (!n) return;
-  probe_kernel<<<ceil_div(n, 256), 256, 0, st>>>(t, ids, n, slots, sort_keys, sort_vals,
-                                                 new_slots, new_count, eidx);
+  probe_kernel<<<ceil_div(n, 256 * 4), 256, 0, st>>>(t, ids, n, slots, sort_keys, sort_vals,
+                                                     new_slots, new_count, eidx);
   HPS_LAUNCH_CHECK();
 }
 

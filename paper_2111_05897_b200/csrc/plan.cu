@@ -24,7 +24,7 @@ namespace hps {
 
 namespace {
 constexpr int kPlanBlock = 256;
-constexpr int kPlanItems = 8;
+constexpr int kPlanItems = 4;
 constexpr int kPlanTile = kPlanBlock * kPlanItems;
 }  // namespace
 

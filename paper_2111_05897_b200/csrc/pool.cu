@@ -8,9 +8,8 @@
 // Latency, not bandwidth, is what a naive version loses to: offsets -> slot -> row is
 // a chain of three dependent loads. The slot of a segment's first listing is loaded
 // speculatively at index sg together with the offsets, which is exactly right for
-// one-hot batches (offsets[sg] == sg), so a one-hot segment costs two round trips.
-// The grid covers every segment (no grid-stride loop) so the SMs stay full of
-// independent chains.
+// one-hot batches (offsets[sg] == sg), so a one-hot segment costs two round trips, and
+// every group keeps kPoolILP such segments in flight.
 //
 // HBM per segment (one-hot, D=64): 256 B row read + 256 B pooled write + 8 B version
 // word + 4 B slot.
@@ -25,6 +24,77 @@
 
 namespace hps {
 
+namespace {
+
+constexpr int kPoolILP = 2;
+
+template <int V, bool kGuard>
+__device__ __forceinline__ void write_out(float* dst, const float (&o)[V], uint32_t d0,
+                                          uint32_t D) {
+  if (kGuard) {
+    for (int k = 0; k < V; ++k)
+      if (d0 + k < D) dst[k] = o[k];
+  } else {
+    store_vec_cs<V>(dst, o);
+  }
+}
+
+// Any segment shape (empty, one listing, many listings with duplicates).
+template <int V, int L, bool kGuard>
+__device__ void pool_general(const DevTable& t, const uint32_t* __restrict__ slots, uint64_t sg,
+                             uint32_t a, uint32_t e, double scale, int ln, float* out,
+                             uint64_t* out_rv64, uint32_t* out_rv32) {
+  using G = Geo<V, L, kGuard>;
+  const uint32_t D = t.D;
+  const int chunks = kGuard ? (D + G::kSpan - 1) / G::kSpan : 1;
+  for (int c = 0; c < chunks; ++c) {
+    const uint32_t d0 = c * G::kSpan + ln * V;
+    if (kGuard && d0 >= D) break;
+    double acc[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] = 0.0;
+    uint32_t i = a;
+    // Two listings in flight per iteration for memory-level parallelism.
+    for (; i + 1 < e; i += 2) {
+      uint32_t s0 = slots[i], s1 = slots[i + 1];
+      float r0[V], r1[V];
+      if (slot_ok(t, s0)) load_vec<V>(t.rows + (uint64_t)s0 * t.stride + d0, r0);
+      else for (int k = 0; k < V; ++k) r0[k] = 0.0f;
+      if (slot_ok(t, s1)) load_vec<V>(t.rows + (uint64_t)s1 * t.stride + d0, r1);
+      else for (int k = 0; k < V; ++k) r1[k] = 0.0f;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        acc[k] = __dadd_rn(acc[k], static_cast<double>(r0[k]));
+        acc[k] = __dadd_rn(acc[k], static_cast<double>(r1[k]));
+      }
+      if (c == 0 && ln == 0) {
+        uint32_t v0 = slot_ok(t, s0) ? t.vt[s0].x : 0, v1 = slot_ok(t, s1) ? t.vt[s1].x : 0;
+        if (out_rv64) out_rv64[i] = v0, out_rv64[i + 1] = v1;
+        if (out_rv32) out_rv32[i] = v0, out_rv32[i + 1] = v1;
+      }
+    }
+    if (i < e) {
+      uint32_t s0 = slots[i];
+      float r0[V];
+      if (slot_ok(t, s0)) load_vec<V>(t.rows + (uint64_t)s0 * t.stride + d0, r0);
+      else for (int k = 0; k < V; ++k) r0[k] = 0.0f;
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = __dadd_rn(acc[k], static_cast<double>(r0[k]));
+      if (c == 0 && ln == 0) {
+        uint32_t v0 = slot_ok(t, s0) ? t.vt[s0].x : 0;
+        if (out_rv64) out_rv64[i] = v0;
+        if (out_rv32) out_rv32[i] = v0;
+      }
+    }
+    float o[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) o[k] = __double2float_rn(__dmul_rn(acc[k], scale));
+    write_out<V, kGuard>(out + sg * D + d0, o, d0, D);
+  }
+}
+
+}  // namespace
+
 template <int V, int L, bool kGuard>
 __global__ void __launch_bounds__(256)
     pool_kernel(DevTable t, const uint32_t* __restrict__ offsets,
@@ -34,90 +104,62 @@ __global__ void __launch_bounds__(256)
   using G = Geo<V, L, kGuard>;
   const int ln = G::lane();
   const uint32_t D = t.D;
-  const int chunks = kGuard ? (D + G::kSpan - 1) / G::kSpan : 1;
-  for (uint64_t sg = G::group(); sg < BF; sg += G::groups()) {
-    const uint32_t a = offsets[sg], e = offsets[sg + 1];
-    const uint32_t spec = sg < N ? slots[sg] : 0u;  // speculative: right when a == sg
-    // Empty groups pool to zeros (embedding_worker.hpp:543): keep scale finite there.
-    const double scale = (mean && e > a) ? __drcp_rn(static_cast<double>(e - a)) : 1.0;
-    if (e == a + 1) {
-      // single listing (every segment of a one-hot batch)
-      const uint32_t s = a == sg ? spec : slots[a];
-      const bool ok = slot_ok(t, s);
-      const float* row = t.rows + static_cast<uint64_t>(ok ? s : 0) * t.stride;
-      if (ln == 0) {
-        const uint32_t v = ok ? t.vt[s].x : 0u;
-        if (out_rv64) out_rv64[a] = v;
-        if (out_rv32) out_rv32[a] = v;
-      }
-      for (int c = 0; c < chunks; ++c) {
-        const uint32_t d0 = c * G::kSpan + ln * V;
-        if (kGuard && d0 >= D) break;
-        float r[V], o[V];
-        if (ok) load_vec<V>(row + d0, r);
-        else for (int k = 0; k < V; ++k) r[k] = 0.0f;
+  const uint64_t groups = G::groups();
+  for (uint64_t sg0 = G::group(); sg0 < BF; sg0 += groups * kPoolILP) {
+    uint64_t sg[kPoolILP];
+    uint32_t a[kPoolILP], e[kPoolILP], spec[kPoolILP];
+    bool live[kPoolILP];
 #pragma unroll
-        for (int k = 0; k < V; ++k)
-          o[k] = __double2float_rn(__dmul_rn(__dadd_rn(0.0, static_cast<double>(r[k])), scale));
-        float* dst = out + sg * D + d0;
-        if (kGuard) {
-          for (int k = 0; k < V; ++k)
-            if (d0 + k < D) dst[k] = o[k];
-        } else {
-          store_vec_cs<V>(dst, o);
-        }
-      }
-      continue;
+    for (int u = 0; u < kPoolILP; ++u) {
+      sg[u] = sg0 + u * groups;
+      live[u] = sg[u] < BF;
+      a[u] = live[u] ? offsets[sg[u]] : 0u;
+      e[u] = live[u] ? offsets[sg[u] + 1] : 0u;
+      spec[u] = (live[u] && sg[u] < N) ? slots[sg[u]] : 0u;  // right when a == sg
     }
-    for (int c = 0; c < chunks; ++c) {
-      const uint32_t d0 = c * G::kSpan + ln * V;
-      if (kGuard && d0 >= D) break;
-      double acc[V];
+    uint32_t s[kPoolILP];
+    bool one[kPoolILP];
 #pragma unroll
-      for (int k = 0; k < V; ++k) acc[k] = 0.0;
-      uint32_t i = a;
-      // Two listings in flight per iteration for memory-level parallelism.
-      for (; i + 1 < e; i += 2) {
-        uint32_t s0 = slots[i], s1 = slots[i + 1];
-        float r0[V], r1[V];
-        if (slot_ok(t, s0)) load_vec<V>(t.rows + (uint64_t)s0 * t.stride + d0, r0);
-        else for (int k = 0; k < V; ++k) r0[k] = 0.0f;
-        if (slot_ok(t, s1)) load_vec<V>(t.rows + (uint64_t)s1 * t.stride + d0, r1);
-        else for (int k = 0; k < V; ++k) r1[k] = 0.0f;
+    for (int u = 0; u < kPoolILP; ++u) {
+      one[u] = live[u] && e[u] == a[u] + 1;
+      s[u] = one[u] ? (a[u] == sg[u] ? spec[u] : slots[a[u]]) : 0u;
+    }
+    // single-listing segments (every segment of a one-hot batch): rows in flight together
+    if (!kGuard) {
+      float r[kPoolILP][V];
+      uint32_t ver[kPoolILP];
 #pragma unroll
-        for (int k = 0; k < V; ++k) {
-          acc[k] = __dadd_rn(acc[k], static_cast<double>(r0[k]));
-          acc[k] = __dadd_rn(acc[k], static_cast<double>(r1[k]));
-        }
-        if (c == 0 && ln == 0) {
-          uint32_t v0 = slot_ok(t, s0) ? t.vt[s0].x : 0, v1 = slot_ok(t, s1) ? t.vt[s1].x : 0;
-          if (out_rv64) out_rv64[i] = v0, out_rv64[i + 1] = v1;
-          if (out_rv32) out_rv32[i] = v0, out_rv32[i + 1] = v1;
-        }
+      for (int u = 0; u < kPoolILP; ++u) {
+        if (!one[u]) continue;
+        const bool ok = slot_ok(t, s[u]);
+        if (ok) load_vec<V>(t.rows + static_cast<uint64_t>(s[u]) * t.stride + ln * V, r[u]);
+        else for (int k = 0; k < V; ++k) r[u][k] = 0.0f;
+        ver[u] = (ok && ln == 0) ? t.vt[s[u]].x : 0u;
       }
-      if (i < e) {
-        uint32_t s0 = slots[i];
-        float r0[V];
-        if (slot_ok(t, s0)) load_vec<V>(t.rows + (uint64_t)s0 * t.stride + d0, r0);
-        else for (int k = 0; k < V; ++k) r0[k] = 0.0f;
 #pragma unroll
-        for (int k = 0; k < V; ++k) acc[k] = __dadd_rn(acc[k], static_cast<double>(r0[k]));
-        if (c == 0 && ln == 0) {
-          uint32_t v0 = slot_ok(t, s0) ? t.vt[s0].x : 0;
-          if (out_rv64) out_rv64[i] = v0;
-          if (out_rv32) out_rv32[i] = v0;
-        }
-      }
-      float o[V];
+      for (int u = 0; u < kPoolILP; ++u) {
+        if (!one[u]) continue;
+        // acc = 0.0 + row (turns -0.0 into +0.0 exactly as the reference does), times the
+        // scale of a one-listing group: 1.0/1 (mean) == 1.0 (sum).
+        float o[V];
 #pragma unroll
-      for (int k = 0; k < V; ++k) o[k] = __double2float_rn(__dmul_rn(acc[k], scale));
-      float* dst = out + sg * D + d0;
-      if (kGuard) {
         for (int k = 0; k < V; ++k)
-          if (d0 + k < D) dst[k] = o[k];
-      } else {
-        store_vec_cs<V>(dst, o);
+          o[k] = __double2float_rn(__dmul_rn(__dadd_rn(0.0, static_cast<double>(r[u][k])), 1.0));
+        store_vec_cs<V>(out + sg[u] * D + ln * V, o);
+        if (ln == 0) {
+          if (out_rv64) out_rv64[a[u]] = ver[u];
+          if (out_rv32) out_rv32[a[u]] = ver[u];
+        }
       }
+    }
+#pragma unroll
+    for (int u = 0; u < kPoolILP; ++u) {
+      if (!live[u] || (one[u] && !kGuard)) continue;
+      // Empty groups pool to zeros (embedding_worker.hpp:543): keep scale finite there.
+      const double scale =
+          (mean && e[u] > a[u]) ? __drcp_rn(static_cast<double>(e[u] - a[u])) : 1.0;
+      pool_general<V, L, kGuard>(t, slots, sg[u], a[u], e[u], scale, ln, out, out_rv64,
+                                 out_rv32);
     }
   }
 }
@@ -128,7 +170,8 @@ void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slo
   if (!BF) return;
   HPS_DISPATCH_DIM(t.D, {
     uint64_t groups_per_block = 256 / L;
-    uint32_t blocks = std::min<uint64_t>(ceil_div(BF, groups_per_block), 1u << 30);
+    uint32_t blocks =
+        std::min<uint64_t>(ceil_div(BF, groups_per_block * kPoolILP), 1u << 30);
     pool_kernel<V, L, G><<<blocks, 256, 0, st>>>(t, offsets, slots, BF, N, mean, out, out_rv64,
                                                  out_rv32);
   });
