@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(256)
                  uint32_t* __restrict__ new_count, uint32_t* __restrict__ eidx) {
   // kProbeILP listings per thread: their first probes are issued back to back (the
   // common case -- key found in its home entry -- then costs one round trip for all).
-  constexpr int kProbeILP = 4;
+  constexpr int kProbeILP = 2;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x * kProbeILP + threadIdx.x;
   uint64_t id[kProbeILP], h[kProbeILP];
   ulonglong2 kv[kProbeILP];
@@ -190,7 +190,7 @@ void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* 
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
                   uint32_t* new_count, uint32_t* eidx, cudaStream_t st) {
   if (!n) return;
-  probe_kernel<<<ceil_div(n, 256 * 4), 256, 0, st>>>(t, ids, n, slots, sort_keys, sort_vals,
+  probe_kernel<<<ceil_div(n, 256 * 2), 256, 0, st>>>(t, ids, n, slots, sort_keys, sort_vals,
                                                      new_slots, new_count, eidx);
   HPS_LAUNCH_CHECK();
 }

@@ -7,9 +7,10 @@
 // application, so its listing needs no ordering at all -- for the one-hot Criteo
 // shape that is >99% of all listings. Listings of rows hit more than once ("multi")
 // are compacted, in listing (= apply) order, by a single-pass chained scan, and only
-// they go through the stable slot sort. The counters are reset by the update that
-// consumes them; a batch that is never pushed leaves them high, which can only move
-// later rows from the single path to the (always correct) multi path.
+// they go through the stable slot sort. Single rows' counters are cleared right here;
+// multi rows' by the update that consumes them -- a batch that is never pushed leaves
+// those high, which can only move later rows from the single path to the (always
+// correct) multi path.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -68,6 +69,12 @@ __global__ void __launch_bounds__(kPlanBlock)
     mbits |= multi ? (1u << j) : 0u;
     mine += multi;
     if (base + j < n) kind[base + j] = multi ? 2 : 1;
+    // A single row's counter is read by exactly this listing: clear it now, while its
+    // sector is resident (multi rows are cleared by the update that consumes them).
+    if (c[j] == 1) {
+      if (e[j] == kSpecialEntry) *t.special_cnt = 0;
+      else t.ht[e[j]].cnt = 0;
+    }
   }
   // warp-inclusive scan of per-lane counts
   uint32_t x = mine;

@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kBlock)
                 uint32_t* __restrict__ hist) {
   __shared__ uint32_t cnt[kMaxPasses * kBins];
   const uint32_t n = count_of(n_dev, n_host);
+  if (n_dev && n <= 4096u) return;  // small_sort_kernel (kSmallN) took it
   for (int i = threadIdx.x; i < passes * kBins; i += kBlock) cnt[i] = 0;
   __syncthreads();
   for (uint32_t i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) {
@@ -104,6 +105,7 @@ __global__ void __launch_bounds__(kBlock)
   uint32_t* scratch = gbase + kBins;            // [kBins] (uses 32 + 1)
 
   const uint32_t n = count_of(n_dev, n_host);
+  if (n_dev && n <= 4096u) return;  // small_sort_kernel (kSmallN) took it
   const uint32_t tiles = (n + kTileN - 1) / kTileN;
   // Dynamic tile order: a tile only ever waits on tiles that were scheduled before it.
   if (threadIdx.x == 0) scratch[32] = atomicAdd(tile_ctr, 1u);
@@ -195,6 +197,96 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// Small sorts (n <= kSmallN, the common size of a one-hot batch's multi list) run all
+// passes inside one CTA in shared memory: one launch instead of 1 + passes.
+constexpr int kSmallBlock = 1024;
+constexpr int kSmallItems = 4;
+constexpr uint32_t kSmallN = kSmallBlock * kSmallItems;
+
+template <typename K>
+constexpr size_t small_smem() {
+  return 2 * kSmallN * (sizeof(K) + sizeof(uint32_t)) + (kSmallBlock / 32 + 2) * kBins * 4;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kSmallBlock)
+    small_sort_kernel(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+                      K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+                      const uint32_t* n_dev, uint32_t n_host, int passes) {
+  constexpr int kW = kSmallBlock / 32;
+  const uint32_t n = count_of(n_dev, n_host);
+  if (n > kSmallN) return;  // the multi-kernel path handles it
+  extern __shared__ __align__(16) unsigned char smem[];
+  K* sk = reinterpret_cast<K*>(smem);                              // [2][kSmallN]
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + 2 * kSmallN);    // [2][kSmallN]
+  uint32_t* wc = sv + 2 * kSmallN;                                 // [kW][kBins]
+  uint32_t* dstart = wc + kW * kBins;                              // [kBins]
+  uint32_t* scr = dstart + kBins;                                  // [kBins]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t i = threadIdx.x; i < n; i += kSmallBlock) {
+    sk[i] = keys_in[i];
+    sv[i] = vals_in[i];
+  }
+  int cur = 0;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = p * kBits;
+    for (int i = threadIdx.x; i < kW * kBins; i += kSmallBlock) wc[i] = 0;
+    __syncthreads();
+    K k[kSmallItems];
+    uint32_t v[kSmallItems], r[kSmallItems];
+#pragma unroll
+    for (int j = 0; j < kSmallItems; ++j) {
+      const uint32_t idx = warp * 32 * kSmallItems + j * 32 + lane;
+      const bool ok = idx < n;
+      k[j] = ok ? sk[cur * kSmallN + idx] : K(0);
+      v[j] = ok ? sv[cur * kSmallN + idx] : 0u;
+      const uint32_t d = ok ? digit_of(k[j], shift) : static_cast<uint32_t>(kBins);
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t before = wc[warp * kBins + (d & (kBins - 1))];
+      r[j] = before + __popc(peers & lt_mask);
+      __syncwarp();
+      if (ok && lane == __ffs(peers) - 1) wc[warp * kBins + d] = before + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    uint32_t tot = 0;
+    if (threadIdx.x < kBins) {
+      for (int w = 0; w < kW; ++w) {
+        const uint32_t c = wc[w * kBins + threadIdx.x];
+        wc[w * kBins + threadIdx.x] = tot;
+        tot += c;
+      }
+      scr[threadIdx.x] = tot;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t run = 0;
+      for (int d = 0; d < kBins; ++d) {
+        dstart[d] = run;
+        run += scr[d];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSmallItems; ++j) {
+      const uint32_t idx = warp * 32 * kSmallItems + j * 32 + lane;
+      if (idx < n) {
+        const uint32_t d = digit_of(k[j], shift);
+        const uint32_t pos = dstart[d] + wc[warp * kBins + d] + r[j];
+        sk[(cur ^ 1) * kSmallN + pos] = k[j];
+        sv[(cur ^ 1) * kSmallN + pos] = v[j];
+      }
+    }
+    cur ^= 1;
+    __syncthreads();
+  }
+  for (uint32_t i = threadIdx.x; i < n; i += kSmallBlock) {
+    keys_out[i] = sk[cur * kSmallN + i];
+    vals_out[i] = sv[cur * kSmallN + i];
+  }
+}
+
 // Scratch words (u32 units) to sort up to n_max pairs: histograms, tile counters and
 // the look-back status words.
 template <typename K>
@@ -217,9 +309,22 @@ inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b,
   if (!attr_set) {
     HPS_CUDA(cudaFuncSetAttribute(pass_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(Tile<K>::kSmem)));
+    HPS_CUDA(cudaFuncSetAttribute(small_sort_kernel<K>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(small_smem<K>())));
     attr_set = true;
   }
   const int passes = (key_bits + kBits - 1) / kBits;
+  const bool out_b = (passes & 1) != 0;  // where the multi-kernel path leaves the result
+  // Device-sized (or host-small) sorts first try the one-CTA path; the multi-kernel
+  // kernels below skip themselves when it applied (device count <= kSmallN).
+  if (n_dev || n_max <= kSmallN) {
+    small_sort_kernel<K><<<1, kSmallBlock, small_smem<K>(), stream>>>(
+        keys_a, vals_a, out_b ? keys_b : keys_a, out_b ? vals_b : vals_a, n_dev,
+        static_cast<uint32_t>(n_max), passes);
+    HPS_LAUNCH_CHECK();
+    if (!n_dev || n_max <= kSmallN) return out_b;
+  }
   const uint32_t tiles = ceil_div(n_max, Tile<K>::kTile);
   uint32_t* hist = scratch;                                  // [kMaxPasses][kBins]
   uint32_t* tile_ctr = hist + kMaxPasses * kBins;            // [kMaxPasses * 2]
