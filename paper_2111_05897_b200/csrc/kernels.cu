@@ -321,28 +321,47 @@ void launch_check_direct(const float* grads, uint64_t n, unsigned long long* ctr
 // float narrowing of a contribution: |c| <= sum_g n_g*scale_g*|grad_g|_inf
 // <= F * max_g(n_g*scale_g*|grad_g|_inf); only when that bound reaches 2^127 is the
 // exact dry run of the update kernel requested. One flat, 128-bit-vectorised pass.
-template <int V>
+// Row groups (L lanes x V floats) walk the [B*F][D] gradient rows, kCheckILP rows in
+// flight per group; a row's group size comes from the (L2-resident) offsets.
+template <int V, int L, bool kGuard>
 __global__ void __launch_bounds__(256)
     check_batch_kernel(const float* __restrict__ grads, const uint32_t* __restrict__ offsets,
-                       uint64_t n_vec, uint32_t D, uint32_t F, int mean,
+                       uint64_t rows, uint32_t D, uint32_t F, int mean,
                        unsigned long long* ctr) {
+  using G = Geo<V, L, kGuard>;
+  constexpr int kCheckILP = 4;
+  const int ln = G::lane();
+  const int chunks = kGuard ? (D + G::kSpan - 1) / G::kSpan : 1;
+  const uint64_t groups = G::groups();
   bool bad = false;
   float m = 0.0f;
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n_vec;
-       k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t e = k * V;
-    const uint64_t bg = e / D;
-    const uint32_t n = __ldg(offsets + bg + 1) - __ldg(offsets + bg);
-    float x[V];
-    load_vec_cs<V>(grads + e, x);
-    if (n) {
-      float mm = 0.0f;
+  for (uint64_t r0 = G::group(); r0 < rows; r0 += groups * kCheckILP) {
+    float x[kCheckILP][V];
+    uint32_t n[kCheckILP];
 #pragma unroll
-      for (int j = 0; j < V; ++j) {
-        bad |= !isfinite(x[j]);
-        mm = fmaxf(mm, fabsf(x[j]));
+    for (int u = 0; u < kCheckILP; ++u) {
+      const uint64_t r = r0 + u * groups;
+      n[u] = r < rows ? __ldg(offsets + r + 1) - __ldg(offsets + r) : 0u;
+    }
+    for (int c = 0; c < chunks; ++c) {
+      const uint32_t d0 = c * G::kSpan + ln * V;
+#pragma unroll
+      for (int u = 0; u < kCheckILP; ++u) {
+        const uint64_t r = r0 + u * groups;
+        if (r < rows && (!kGuard || d0 < D)) load_vec_cs<V>(grads + r * D + d0, x[u]);
+        else for (int j = 0; j < V; ++j) x[u][j] = 0.0f;
       }
-      m = fmaxf(m, mean ? mm : mm * static_cast<float>(n));
+#pragma unroll
+      for (int u = 0; u < kCheckILP; ++u) {
+        if (!n[u]) continue;  // empty group: its gradient is never used (:731)
+        float mm = 0.0f;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          bad |= !isfinite(x[u][j]);
+          mm = fmaxf(mm, fabsf(x[u][j]));
+        }
+        m = fmaxf(m, mean ? mm : mm * static_cast<float>(n[u]));
+      }
     }
   }
 #pragma unroll
@@ -361,15 +380,13 @@ __global__ void __launch_bounds__(256)
 
 void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
                         uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st) {
-  const uint64_t n = static_cast<uint64_t>(B) * F * D;
-  if (!n) return;
-  if (D % 4 == 0) {
-    check_batch_kernel<4><<<std::min<uint64_t>(ceil_div(n / 4, 256), 148 * 16), 256, 0, st>>>(
-        grads, offsets, n / 4, D, F, mean, ctr);
-  } else {
-    check_batch_kernel<1><<<std::min<uint64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st>>>(
-        grads, offsets, n, D, F, mean, ctr);
-  }
+  const uint64_t rows = static_cast<uint64_t>(B) * F;
+  if (!rows) return;
+  HPS_DISPATCH_DIM(D, {
+    uint64_t groups_per_block = 256 / L;
+    uint32_t blocks = std::min<uint64_t>(ceil_div(rows, groups_per_block * 4), 148ull * 16);
+    check_batch_kernel<V, L, G><<<blocks, 256, 0, st>>>(grads, offsets, rows, D, F, mean, ctr);
+  });
   HPS_LAUNCH_CHECK();
 }
 

@@ -85,33 +85,24 @@ __global__ void __launch_bounds__(kPlanBlock)
   }
   if (lane == 31) s_warp[warp] = x;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     uint32_t tot = 0;
-    for (int w = 0; w < kPlanBlock / 32; ++w) {
-      uint32_t cw = s_warp[w];
-      s_warp[w] = tot;
-      tot += cw;
-    }
+    for (int w = 0; w < kPlanBlock / 32; ++w) tot += s_warp[w];
     const unsigned long long ep = static_cast<unsigned long long>(epoch) << 32;
     volatile unsigned long long* my = status + tile;
-    uint32_t excl = 0;
-    if (tile == 0) {
-      *my = ep | radix::kPrefixFlag | tot;
-    } else {
-      *my = ep | tot;
-      for (int64_t tt = static_cast<int64_t>(tile) - 1; tt >= 0; --tt) {
-        const volatile unsigned long long* st = status + tt;
-        unsigned long long v;
-        do {
-          v = *st;
-        } while ((v >> 32) != epoch);
-        excl += static_cast<uint32_t>(v & (radix::kPrefixFlag - 1));
-        if (v & radix::kPrefixFlag) break;
+    if (lane == 0) *my = ep | (tile == 0 ? radix::kPrefixFlag : 0ull) | tot;
+    const uint32_t excl = tile == 0 ? 0u : radix::warp_lookback(status, tile, epoch);
+    if (lane == 0) {
+      if (tile > 0) *my = ep | radix::kPrefixFlag | (excl + tot);
+      uint32_t run = 0;
+      for (int w = 0; w < kPlanBlock / 32; ++w) {
+        uint32_t cw = s_warp[w];
+        s_warp[w] = run;
+        run += cw;
       }
-      *my = ep | radix::kPrefixFlag | (excl + tot);
+      s_excl = excl;
+      if (tile == tiles - 1) *n_multi = excl + tot;
     }
-    s_excl = excl;
-    if (tile == tiles - 1) *n_multi = excl + tot;
   }
   __syncthreads();
   uint32_t pos = s_excl + s_warp[warp] + x - mine;

@@ -128,13 +128,14 @@ __global__ void __launch_bounds__(256)
     if (!kGuard) {
       float r[kPoolILP][V];
       uint32_t ver[kPoolILP];
+      const bool want_rv = out_rv64 || out_rv32;
 #pragma unroll
       for (int u = 0; u < kPoolILP; ++u) {
         if (!one[u]) continue;
         const bool ok = slot_ok(t, s[u]);
         if (ok) load_vec<V>(t.rows + static_cast<uint64_t>(s[u]) * t.stride + ln * V, r[u]);
         else for (int k = 0; k < V; ++k) r[u][k] = 0.0f;
-        ver[u] = (ok && ln == 0) ? t.vt[s[u]].x : 0u;
+        ver[u] = (want_rv && ok && ln == 0) ? t.vt[s[u]].x : 0u;
       }
 #pragma unroll
       for (int u = 0; u < kPoolILP; ++u) {
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(256)
         for (int k = 0; k < V; ++k)
           o[k] = __double2float_rn(__dmul_rn(__dadd_rn(0.0, static_cast<double>(r[u][k])), 1.0));
         store_vec_cs<V>(out + sg[u] * D + ln * V, o);
-        if (ln == 0) {
+        if (want_rv && ln == 0) {
           if (out_rv64) out_rv64[a[u]] = ver[u];
           if (out_rv32) out_rv32[a[u]] = ver[u];
         }
@@ -162,6 +163,25 @@ __global__ void __launch_bounds__(256)
                                  out_rv32);
     }
   }
+}
+
+// Read versions of a pulled batch, snapshotted when another push is about to mutate
+// the table before this batch's own push (copy-on-write, table.cu protect_reads).
+__global__ void snapshot_rv_kernel(DevTable t, const uint32_t* __restrict__ slots, uint64_t n,
+                                   uint32_t* __restrict__ rv) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = slots[i];
+    rv[i] = slot_ok(t, s) ? t.vt[s].x : 0u;
+  }
+}
+
+void launch_snapshot_rv(const DevTable& t, const uint32_t* slots, uint64_t n, uint32_t* rv,
+                        cudaStream_t st) {
+  if (!n) return;
+  snapshot_rv_kernel<<<std::min<uint64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st>>>(t, slots,
+                                                                                     n, rv);
+  HPS_LAUNCH_CHECK();
 }
 
 void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,

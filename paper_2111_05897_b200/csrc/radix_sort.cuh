@@ -43,6 +43,33 @@ constexpr unsigned long long kPrefixFlag = 1ull << 31;
 
 inline std::atomic<uint32_t> g_epoch{1};
 
+// Decoupled look-back by one full warp (all 32 lanes call it): returns the exclusive
+// prefix of `tile` over status[0..tile) (one word per tile, published with `epoch`),
+// reading 32 predecessors per round trip instead of one.
+__device__ __forceinline__ uint32_t warp_lookback(const unsigned long long* status, uint32_t tile,
+                                                  uint32_t epoch) {
+  const int lane = threadIdx.x & 31;
+  uint32_t excl = 0;
+  int64_t end = tile;
+  while (end > 0) {
+    const int64_t idx = end - 32 + lane;  // lane 31 = nearest predecessor
+    unsigned long long v = kPrefixFlag;   // below tile 0: an empty prefix
+    if (idx >= 0) {
+      const volatile unsigned long long* s = status + idx;
+      do {
+        v = *s;
+      } while ((v >> 32) != epoch);
+    }
+    const uint32_t pmask = __ballot_sync(0xffffffffu, (v & kPrefixFlag) != 0);
+    const int hi = pmask ? 31 - __clz(pmask) : 0;
+    const uint32_t val = lane >= hi ? static_cast<uint32_t>(v & (kPrefixFlag - 1)) : 0u;
+    excl += __reduce_add_sync(0xffffffffu, val);
+    if (pmask) break;
+    end -= 32;
+  }
+  return excl;
+}
+
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
   return static_cast<uint32_t>(key >> shift) & (kBins - 1);

@@ -244,7 +244,26 @@ void table_clear(Table* t, cudaStream_t st) {
   HPS_CUDA(cudaMemsetAsync(d.ctr + kCtrOverflow, 0, sizeof(unsigned long long), st));
 }
 
+static void forget_outstanding(Batch& b) {
+  if (!b.table) return;
+  auto& v = b.table->outstanding;
+  v.erase(std::remove(v.begin(), v.end(), &b), v.end());
+}
+
+// Copy-on-write of read versions: before any mutation of the table, every batch that
+// was pulled but not yet pushed (other than `except`) materialises its pull-time
+// versions, so its own push can still count staleness delays exactly. In the sync
+// step (pull, push, pull, ...) nothing is ever outstanding and this costs nothing.
+static void protect_reads(Table* t, const Batch* except, cudaStream_t st) {
+  for (Batch* y : t->outstanding) {
+    if (y == except || y->rv_valid || !y->registered) continue;
+    launch_snapshot_rv(t->d, y->slot, y->N, y->rv, st);
+    y->rv_valid = true;
+  }
+}
+
 void batch_free(Batch& b) {
+  forget_outstanding(b);
   void* ptrs[] = {b.offsets, b.lgrp,  b.slot, b.eidx,    b.keys_a,  b.vals_a,
                   b.keys_b,  b.vals_b, b.rv,  b.new_slots, b.kind,  b.hist,
                   b.small,   b.skeys_a, b.skeys_b, b.sperm_a, b.sperm_b, b.sstart};
@@ -406,6 +425,8 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   const uint64_t BF = static_cast<uint64_t>(B) * F;
   if (BF >= 0xffffffffull) throw Error(HPS_E_PRECONDITION, "batch too large (B*F >= 2^32)");
   if (F == 0) throw Error(HPS_E_PRECONDITION, "register: feature group count must be positive");
+  forget_outstanding(b);
+  b.rv_valid = false;
   batch_reserve(b, N, BF, B);
   Stager stg(t->stage);
   const uint64_t* d_ids = static_cast<const uint64_t*>(stg.in(ids, N * sizeof(uint64_t), st));
@@ -473,11 +494,16 @@ void batch_pull(Batch& b, int agg, float* out_pooled, uint64_t* out_rv, cudaStre
   Stager stg(t->stage);
   float* d_out = static_cast<float*>(stg.out(out_pooled, BF * t->cfg.embedding_dim * sizeof(float)));
   uint64_t* d_rv = static_cast<uint64_t*>(stg.out(out_rv, b.N * sizeof(uint64_t)));
+  // Read versions are produced only when the caller asks for them; otherwise the push
+  // takes them from the table (nothing mutated since) or from a snapshot that a
+  // mutation in between forces (protect_reads).
   {
     ProfScope p(t, "pool", st);
     launch_pool(t->d, b.offsets, b.slot, static_cast<uint32_t>(BF), b.N, agg == HPS_MEAN ? 1 : 0,
-                d_out, d_rv, b.rv, st);
+                d_out, d_rv, d_rv ? b.rv : nullptr, st);
   }
+  b.rv_valid = d_rv != nullptr;
+  if (!b.pulled) t->outstanding.push_back(&b);
   b.pulled = true;
   stg.finish(st);
 }
@@ -499,6 +525,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   }
   const uint64_t BF = static_cast<uint64_t>(b.B) * b.F;
   const uint32_t D = t->cfg.embedding_dim;
+  protect_reads(t, &b, st);
   Stager stg(t->stage);
   const float* d_g = static_cast<const float*>(stg.in(grads, BF * D * sizeof(float), st));
   const uint64_t* d_rv = static_cast<const uint64_t*>(stg.in(rv64, b.N * sizeof(uint64_t), st));
@@ -527,8 +554,9 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     a.rv64 = d_rv;
     a.tracked = 1;
   } else if (!untracked && b.pulled) {
-    a.rv32 = b.rv;
     a.tracked = 1;
+    if (b.rv_valid) a.rv32 = b.rv;
+    else a.fresh = 1;  // no mutation since the pull: read version == current version
   }
   // Exact validation (dry runs), executed only if the bound check was inconclusive.
   a.dry_run = 1;
@@ -543,6 +571,9 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     ProfScope p(t, "update_multi", st);
     launch_update(t->d, a, false, t->sm_count, st);
   }
+  forget_outstanding(b);
+  b.pulled = false;
+  b.rv_valid = false;
   if (accepted) *accepted = 1;
   stg.finish(st);
   if (!(flags & HPS_ASYNC)) check_flags(t, st);
@@ -625,6 +656,9 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
     stg.finish(st);
     throw Error(HPS_E_DIVERGENCE, "PsShard::apply_gradients: non-finite gradient");
   }
+  protect_reads(t, nullptr, st);
+  forget_outstanding(b);
+  b.pulled = false;
   b.N = n;
   b.B = static_cast<uint32_t>(n);
   b.F = 1;

@@ -106,6 +106,7 @@ struct Batch {
   uint32_t* small = nullptr;      // device scalars: [0] = multi listings, [2] = rows inserted,
                                   // [4] = plan tile counter
   bool all_multi = false;         // plan skipped: every listing on the sorted path
+  bool rv_valid = false;          // rv holds the pull-time versions (else: no mutation since)
   // sample-order permutation (sample_keys != NULL)
   uint64_t* skeys_a = nullptr;
   uint64_t* skeys_b = nullptr;
@@ -153,6 +154,9 @@ struct Table {
   std::mutex mu;  // one call at a time per table (PsShard's per-shard lock)
   Batch scratch;  // workspace for the stateless entry points
   StagePool stage;
+  // Batches pulled but not yet pushed. Their read versions are only materialised
+  // (snapshot) when some other mutation is about to run before their own push.
+  std::vector<Batch*> outstanding;
   unsigned long long* h_ctr = nullptr;  // pinned mirror of the counters
 };
 
@@ -175,6 +179,8 @@ void launch_peek(const DevTable& t, const uint64_t* ids, uint64_t n, float* out_
 void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,
                  uint64_t N, int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32,
                  cudaStream_t st);
+void launch_snapshot_rv(const DevTable& t, const uint32_t* slots, uint64_t n, uint32_t* rv,
+                        cudaStream_t st);
 void launch_check_direct(const float* grads, uint64_t n_floats, unsigned long long* ctr,
                          cudaStream_t st);
 void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
@@ -202,6 +208,7 @@ struct UpdateArgs {
   float lr;
   uint32_t step_tag;
   int tracked;
+  int fresh;  // tracked, and no mutation since the pull: read version = current version
   int dry_run;  // compute + validate contributions only
 };
 void launch_update(const DevTable& t, const UpdateArgs& a, bool direct, int sms, cudaStream_t st);

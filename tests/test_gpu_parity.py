@@ -430,3 +430,53 @@ def test_compress_indices_vs_oracle_random(hps, seed):
         assert all((x == y).all() for x, y in zip(pa, pb))
     with pytest.raises(hps.PreconditionError):
         hps.compress_indices(np.zeros(0, np.uint64), np.zeros(65537, np.uint32), 65536, 1)
+
+
+# ---------------------------------------------------------------- pipelined batches
+
+
+def test_pipelined_batches_read_versions(hps):
+    """Two batches pulled before either is pushed (bounded staleness 1): the second
+    push must count the first push's bumps as delays (embedding_ps.hpp:454-480). The
+    GPU materialises B's pull-time versions only when A's push is about to mutate."""
+    import oracle as O
+    from paper_2111_05897_b200 import workloads as W
+
+    rng = np.random.default_rng(21)
+    B, F, D = 40, 3, 8
+    salts = [W.mix64_int(5 + s) for s in range(2)]
+    orc = O.Restatement(salts, D, "adagrad")
+    t = hps.ShardSet(2, D, 1 << 12, hps.ADAGRAD, salts=salts)
+    ew_a = hps.EmbeddingWorker(t, hps.MEAN)
+    ew_b = hps.EmbeddingWorker(t, hps.MEAN)
+    for rnd in range(3):
+        ia, oa = W.random_csr(rng, B, F, 4, 30)
+        ib, ob = W.random_csr(rng, B, F, 4, 30)
+        ga = (rng.standard_normal((B, F, D)) * 0.3).astype(np.float32)
+        gb = (rng.standard_normal((B, F, D)) * 0.3).astype(np.float32)
+        pa, rva = orc.pull_batch(B, F, ia, oa.astype(np.uint64), "mean")
+        pb, rvb = orc.pull_batch(B, F, ib, ob.astype(np.uint64), "mean")
+        ew_a.register_batch(ia, oa, B, F)
+        ew_b.register_batch(ib, ob, B, F)
+        assert ew_a.serve_pull().tobytes() == pa.tobytes()
+        assert ew_b.serve_pull().tobytes() == pb.tobytes()
+        _, da = orc.push_batch(B, F, ia, oa.astype(np.uint64), ga, 0.05, 2 * rnd + 1,
+                               read_versions=rva, agg="mean")
+        _, db = orc.push_batch(B, F, ib, ob.astype(np.uint64), gb, 0.05, 2 * rnd + 2,
+                               read_versions=rvb, agg="mean")
+        ew_a.apply_backward(ga, 0.05, 2 * rnd + 1)
+        ew_b.apply_backward(gb, 0.05, 2 * rnd + 2)
+        want = np.bincount(np.minimum(np.concatenate([da, db]), 16), minlength=17)
+        if rnd == 0:
+            hist0 = np.zeros(17, np.int64)
+        got = np.array(t.counters().delay_hist[:], np.int64) - hist0
+        hist0 = np.array(t.counters().delay_hist[:], np.int64)
+        assert (got == want).all(), (got, want)
+        assert want[1:].sum() > 0  # the shared rows really saw a delay
+    ids = np.arange(0, 30, dtype=np.uint64)
+    w, a, v, p = t.peek(ids)
+    wo, ao, vo, po = orc.peek(ids)
+    assert (p == po).all()
+    np.testing.assert_array_equal(w[p], wo[po])
+    np.testing.assert_array_equal(a[p], ao[po])
+    np.testing.assert_array_equal(v[p], vo[po])
