@@ -207,13 +207,13 @@ Table* table_create(const hps_table_cfg& cfg) {
     d.ht_mask = H - 1;
     d.ht_shift = 64 - lg;
     d.D = cfg.embedding_dim;
-    d.stride = 2 * cfg.embedding_dim;
+    d.stride = 2 * cfg.embedding_dim + 4;
     d.capacity = static_cast<uint32_t>(C);
     d.S = cfg.shard_count;
     d.opt = cfg.optimizer;
     HPS_CUDA(cudaMalloc(&d.ht, H * sizeof(HashEntry)));
     HPS_CUDA(cudaMalloc(&d.rows, C * d.stride * sizeof(float)));
-    HPS_CUDA(cudaMalloc(&d.vt, C * sizeof(uint2)));
+    d.vt = VtView{d.rows, d.stride, 2 * d.D};
     HPS_CUDA(cudaMalloc(&d.special_cnt, sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.slot_id, C * sizeof(uint64_t)));
     HPS_CUDA(cudaMalloc(&d.special, sizeof(uint32_t)));
@@ -285,8 +285,8 @@ void table_destroy(Table* t) {
     t->stage.free_all();
     t->prof.destroy();
     DevTable& d = t->d;
-    void* ptrs[] = {d.ht,      d.rows, d.vt,  d.special_cnt, d.slot_id,
-                    d.special, d.hwm,  d.ctr, t->d_salts};
+    void* ptrs[] = {d.ht,  d.rows, d.special_cnt, d.slot_id, d.special,
+                    d.hwm, d.ctr,  t->d_salts};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (t->h_ctr) cudaFreeHost(t->h_ctr);

@@ -3,10 +3,11 @@
 // HBM layout of one table:
 //   ht[H]        16 B  open-addressing id index {u64 key, u32 slot}, H = pow2 >= 2*capacity
 //                      (load <= 0.5); one probe = one 32-byte sector
-//   rows[C][2D]  f32   [w D | acc D] per slot -- the reference row (embedding_ps.hpp:64);
-//                      one contiguous 8D-byte segment, read-modify-written by the update
-//   vt[C]        u32x2 {version (# distinct steps that wrote the row, embedding_ps.hpp:482),
-//                       step tag of the latest version bump (replaces the 16-deep ring)}
+//   rows[C][2D+4] f32  [w D | acc D | header] per slot -- the reference row
+//                      (embedding_ps.hpp:64) plus a 16-byte header {version (# distinct
+//                      steps that wrote the row, embedding_ps.hpp:482), step tag of the
+//                      latest version bump (replaces the 16-deep ring), 0, 0}; one
+//                      contiguous segment, read-modify-written by the update
 //   slot_id[C]   u64   id held by a slot (init seed, export)
 // Slots are handed out densely from a device high-water mark (lru_store.hpp:98).
 #pragma once
@@ -45,6 +46,19 @@ struct __align__(16) HashEntry {
 };
 constexpr uint32_t kSpecialEntry = 0xffffffffu;  // entry index of id == kEmptyKey
 
+// The {version, latest bump tag} word of a row lives in the row's own 16-byte header
+// right after [w | acc]: the update's version read-modify-write then falls in the row's
+// DRAM page instead of costing a separate random access (tools/microbench2.cu: a
+// separate 8-byte version array added ~30% to the update).
+struct VtView {
+  float* rows;
+  uint32_t stride;
+  uint32_t off;  // 2D
+  __host__ __device__ uint2& operator[](uint64_t s) const {
+    return *reinterpret_cast<uint2*>(rows + s * stride + off);
+  }
+};
+
 struct DevTable {
   HashEntry* ht;
   uint64_t ht_mask;
@@ -52,8 +66,8 @@ struct DevTable {
   uint32_t* special;  // slot of id == kEmptyKey (kSpecialAbsent / kSpecialInserting / slot)
   float* rows;
   uint32_t D;
-  uint32_t stride;  // floats per row (2D)
-  uint2* vt;           // {version, latest bump tag} per slot: one 8-byte word per row
+  uint32_t stride;  // floats per row: 2D + 4 ([w D | acc D | header 16 B])
+  VtView vt;        // {version, latest bump tag} in each row's header
   uint32_t* special_cnt;  // batch listing counter of id == kEmptyKey (no hash entry)
   uint64_t* slot_id;
   uint32_t capacity;
