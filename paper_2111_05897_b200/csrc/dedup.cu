@@ -246,7 +246,7 @@ void dedup(const uint64_t* ids, uint64_t n, uint64_t* out_unique, uint32_t* out_
   HPS_CUDA(cudaMemcpyAsync(ka, d_ids, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
   launch_iota(va, n, st);
   int bits = key_bits_of(ka, n, d_or, st);
-  bool in_b = radix::sort_pairs<uint64_t>(ka, va, kb, vb, n, nullptr, bits, hist, st);
+  bool in_b = radix::sort_pairs<uint64_t>(ka, va, kb, vb, n, bits, hist, st);
   const uint64_t* sk = in_b ? kb : ka;
   const uint32_t* sv = in_b ? vb : va;
   dedup_flags_kernel<<<grid_for(n), 256, 0, st>>>(sk, n, head);
@@ -303,14 +303,14 @@ void compress_indices(const uint64_t* ids, uint64_t n, const uint32_t* offsets, 
   launch_iota(va, n, st);
   int bits = key_bits_of(ka, n, d_or, st);
   // Pass 1: stable by id (listing order keeps samples ascending within an id).
-  bool in_b = radix::sort_pairs<uint64_t>(ka, va, kb, vb, n, nullptr, bits, hist, st);
+  bool in_b = radix::sort_pairs<uint64_t>(ka, va, kb, vb, n, bits, hist, st);
   uint32_t* v1 = in_b ? vb : va;
   // Pass 2: stable by group.
   uint32_t* gk = reinterpret_cast<uint32_t*>(in_b ? ka : kb);
   uint32_t* gk2 = reinterpret_cast<uint32_t*>(in_b ? kb : ka) ;
   ci_group_keys_kernel<<<grid_for(n), 256, 0, st>>>(v1, lgrp, G, n, gk);
   uint32_t* v2 = in_b ? va : vb;
-  bool in2 = radix::sort_pairs<uint32_t>(gk, v1, gk2, v2, n, nullptr,
+  bool in2 = radix::sort_pairs<uint32_t>(gk, v1, gk2, v2, n,
                                          std::max(1, bits_for(G - 1)), hist, st);
   const uint32_t* sv = in2 ? v2 : v1;
   ci_flags_kernel<<<grid_for(n), 256, 0, st>>>(sv, d_ids, lgrp, G, n, fl, fl2, gcnt);

@@ -1,16 +1,13 @@
-// Stable LSD radix sort of (key, u32 value) pairs, hand-written for sm_100a
-// ("onesweep": one histogram kernel for all digit passes, then ONE kernel per 8-bit
-// pass whose tiles find their global offsets by decoupled look-back).
+// Stable LSD radix sort of (key, u32 value) pairs, hand-written for sm_100a.
 //
-// Used for the orderings the hot path needs:
-//   * the listings of rows hit more than once in a batch, grouped by table slot with
-//     listing (= apply) order kept inside a slot (u32 keys);
-//   * ids ascending with their positions (batch dedup / compress_indices, u64 keys).
-// The element count may live in device memory (the multi-listing list is compacted
-// on the device), so a sort never needs a host round trip: the grid is sized for an
-// upper bound and surplus tiles exit. Per pass every key/value is read once and
-// written once (2*(sizeof(K)+4) bytes per element); the look-back touches 8 B per
-// (tile, digit).
+// Two shapes:
+//  * small (n <= kSmallN): one CTA sorts in shared memory, every pass in one launch --
+//    the common case of a one-hot batch's multi-listing list;
+//  * large ("onesweep"): one histogram kernel for all digit passes, then ONE kernel
+//    per 8-bit pass whose tiles find their global offsets by decoupled look-back.
+//    Per pass every key/value is read and written once (2*(sizeof(K)+4) B/element).
+// The large path can be gated on a device-side count (run only if *gate > kSmallN)
+// so the host never waits for the device to choose between the two.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -29,6 +26,10 @@ constexpr int kBins = 1 << kBits;
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kMaxPasses = 8;
+
+constexpr int kSmallBlock = 1024;
+constexpr int kSmallItems = 4;
+constexpr uint32_t kSmallN = kSmallBlock * kSmallItems;
 
 template <typename K>
 struct Tile {
@@ -75,18 +76,153 @@ __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
   return static_cast<uint32_t>(key >> shift) & (kBins - 1);
 }
 
-__device__ __forceinline__ uint32_t count_of(const uint32_t* n_dev, uint32_t n_host) {
-  return n_dev ? *n_dev : n_host;
+__device__ __forceinline__ bool gate_open(const uint32_t* gate) {
+  return gate == nullptr || *gate > kSmallN;
 }
+
+// Block-wide exclusive scan over kBins values held by threads 0..kBins-1 (every thread
+// of the block calls it; threads >= kBins pass 0 and get garbage).
+__device__ __forceinline__ uint32_t block_excl_scan_bins(uint32_t v, uint32_t* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31 && warp < kBins / 32) scratch[warp] = x;
+  __syncthreads();
+  uint32_t off = 0;
+  for (int w = 0; w < warp && w < kBins / 32; ++w) off += scratch[w];
+  __syncthreads();
+  return off + x - v;
+}
+
+// ---- small path: all passes in one CTA --------------------------------------------------
+
+// LSD passes over sk/sv (double-buffered in shared memory, n <= kSmallN); returns the
+// buffer index holding the result.
+template <typename K>
+__device__ int smem_lsd(K* sk, uint32_t* sv, uint32_t* wc, uint32_t* dstart, uint32_t* scr,
+                        uint32_t n, int first_shift, int passes) {
+  constexpr int kW = kSmallBlock / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  int cur = 0;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = first_shift + p * kBits;
+    for (int i = threadIdx.x; i < kW * kBins; i += kSmallBlock) wc[i] = 0;
+    __syncthreads();
+    K k[kSmallItems];
+    uint32_t v[kSmallItems], r[kSmallItems];
+#pragma unroll
+    for (int j = 0; j < kSmallItems; ++j) {
+      const uint32_t idx = warp * 32 * kSmallItems + j * 32 + lane;
+      const bool ok = idx < n;
+      k[j] = ok ? sk[cur * kSmallN + idx] : K(0);
+      v[j] = ok ? sv[cur * kSmallN + idx] : 0u;
+      const uint32_t d = ok ? digit_of(k[j], shift) : static_cast<uint32_t>(kBins);
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t before = wc[warp * kBins + (d & (kBins - 1))];
+      r[j] = before + __popc(peers & lt_mask);
+      __syncwarp();
+      if (ok && lane == __ffs(peers) - 1) wc[warp * kBins + d] = before + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    uint32_t tot = 0;
+    if (threadIdx.x < kBins) {
+      for (int w = 0; w < kW; ++w) {
+        const uint32_t c = wc[w * kBins + threadIdx.x];
+        wc[w * kBins + threadIdx.x] = tot;
+        tot += c;
+      }
+    }
+    const uint32_t start = block_excl_scan_bins(threadIdx.x < kBins ? tot : 0u, scr);
+    if (threadIdx.x < kBins) dstart[threadIdx.x] = start;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSmallItems; ++j) {
+      const uint32_t idx = warp * 32 * kSmallItems + j * 32 + lane;
+      if (idx < n) {
+        const uint32_t d = digit_of(k[j], shift);
+        const uint32_t pos = dstart[d] + wc[warp * kBins + d] + r[j];
+        sk[(cur ^ 1) * kSmallN + pos] = k[j];
+        sv[(cur ^ 1) * kSmallN + pos] = v[j];
+      }
+    }
+    cur ^= 1;
+    __syncthreads();
+  }
+  return cur;
+}
+
+template <typename K>
+constexpr size_t small_smem() {
+  return 2 * kSmallN * (sizeof(K) + sizeof(uint32_t)) + (kSmallBlock / 32 + 2) * kBins * 4;
+}
+
+// Host-sized small sort; vals_in == nullptr means values 0..n-1.
+template <typename K>
+__global__ void __launch_bounds__(kSmallBlock)
+    small_sort_kernel(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+                      K* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t n,
+                      int passes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  K* sk = reinterpret_cast<K*>(smem);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + 2 * kSmallN);
+  uint32_t* wc = sv + 2 * kSmallN;
+  uint32_t* dstart = wc + (kSmallBlock / 32) * kBins;
+  uint32_t* scr = dstart + kBins;
+  for (uint32_t i = threadIdx.x; i < n; i += kSmallBlock) {
+    sk[i] = keys_in[i];
+    sv[i] = vals_in ? vals_in[i] : i;
+  }
+  __syncthreads();
+  const int cur = smem_lsd<K>(sk, sv, wc, dstart, scr, n, 0, passes);
+  for (uint32_t i = threadIdx.x; i < n; i += kSmallBlock) {
+    keys_out[i] = sk[cur * kSmallN + i];
+    vals_out[i] = sv[cur * kSmallN + i];
+  }
+}
+
+// Device-sized small sort of composite keys (slot << lbits | listing): runs only when
+// *n_dev <= kSmallN and writes the sorted slots and listings separately.
+static __global__ void __launch_bounds__(kSmallBlock)
+    small_composite_kernel(const unsigned long long* __restrict__ keys, const uint32_t* n_dev,
+                           int lbits, int passes, uint32_t* __restrict__ out_slot,
+                           uint32_t* __restrict__ out_listing) {
+  const uint32_t n = *n_dev;
+  if (n > kSmallN) return;  // the large path (gated on the same count) takes it
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long* sk = reinterpret_cast<unsigned long long*>(smem);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + 2 * kSmallN);
+  uint32_t* wc = sv + 2 * kSmallN;
+  uint32_t* dstart = wc + (kSmallBlock / 32) * kBins;
+  uint32_t* scr = dstart + kBins;
+  for (uint32_t i = threadIdx.x; i < n; i += kSmallBlock) {
+    sk[i] = keys[i];
+    sv[i] = 0;
+  }
+  __syncthreads();
+  const int cur = smem_lsd<unsigned long long>(sk, sv, wc, dstart, scr, n, 0, passes);
+  const unsigned long long lmask = (1ull << lbits) - 1;
+  for (uint32_t i = threadIdx.x; i < n; i += kSmallBlock) {
+    const unsigned long long k = sk[cur * kSmallN + i];
+    out_slot[i] = static_cast<uint32_t>(k >> lbits);
+    out_listing[i] = static_cast<uint32_t>(k & lmask);
+  }
+}
+
+// ---- large path ("onesweep") -------------------------------------------------------------
 
 // Digit histograms of every pass in one read of the keys: hist[p * kBins + d].
 template <typename K>
 __global__ void __launch_bounds__(kBlock)
-    hist_kernel(const K* __restrict__ keys, const uint32_t* n_dev, uint32_t n_host, int passes,
-                uint32_t* __restrict__ hist) {
+    hist_kernel(const K* __restrict__ keys, uint32_t n, int passes, uint32_t* __restrict__ hist,
+                const uint32_t* gate) {
+  if (!gate_open(gate)) return;
   __shared__ uint32_t cnt[kMaxPasses * kBins];
-  const uint32_t n = count_of(n_dev, n_host);
-  if (n_dev && n <= 4096u) return;  // small_sort_kernel (kSmallN) took it
   for (int i = threadIdx.x; i < passes * kBins; i += kBlock) cnt[i] = 0;
   __syncthreads();
   for (uint32_t i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) {
@@ -98,31 +234,16 @@ __global__ void __launch_bounds__(kBlock)
     if (cnt[i]) atomicAdd(&hist[i], cnt[i]);
 }
 
-// Block-wide exclusive scan over the kBins values held one per thread.
-__device__ __forceinline__ uint32_t block_excl_scan_bins(uint32_t v, uint32_t* scratch) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) scratch[warp] = x;
-  __syncthreads();
-  uint32_t off = 0;
-  for (int w = 0; w < warp; ++w) off += scratch[w];
-  __syncthreads();
-  return off + x - v;
-}
-
+// vals_in == nullptr: values are the input positions (pass 0 of an index sort).
 template <typename K>
 __global__ void __launch_bounds__(kBlock)
     pass_kernel(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-                K* __restrict__ keys_out, uint32_t* __restrict__ vals_out, const uint32_t* n_dev,
-                uint32_t n_host, int shift, const uint32_t* __restrict__ hist,
-                unsigned long long* status, uint32_t* tile_ctr, uint32_t epoch) {
+                K* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t n, int shift,
+                const uint32_t* __restrict__ hist, unsigned long long* status, uint32_t* tile_ctr,
+                uint32_t epoch, const uint32_t* gate) {
   constexpr int kItems = Tile<K>::kItems;
   constexpr int kTileN = Tile<K>::kTile;
+  if (!gate_open(gate)) return;
   extern __shared__ __align__(16) unsigned char smem[];
   K* skeys = reinterpret_cast<K*>(smem);
   uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + kTileN);
@@ -131,8 +252,6 @@ __global__ void __launch_bounds__(kBlock)
   uint32_t* gbase = block_off + kBins;          // [kBins]
   uint32_t* scratch = gbase + kBins;            // [kBins] (uses 32 + 1)
 
-  const uint32_t n = count_of(n_dev, n_host);
-  if (n_dev && n <= 4096u) return;  // small_sort_kernel (kSmallN) took it
   const uint32_t tiles = (n + kTileN - 1) / kTileN;
   // Dynamic tile order: a tile only ever waits on tiles that were scheduled before it.
   if (threadIdx.x == 0) scratch[32] = atomicAdd(tile_ctr, 1u);
@@ -152,7 +271,7 @@ __global__ void __launch_bounds__(kBlock)
     uint64_t idx = warp_base + static_cast<uint64_t>(j) * 32 + lane;
     bool ok = idx < n;
     k[j] = ok ? keys_in[idx] : K(0);
-    v[j] = ok ? vals_in[idx] : 0u;
+    v[j] = ok ? (vals_in ? vals_in[idx] : static_cast<uint32_t>(idx)) : 0u;
   }
   const uint32_t lt_mask = (1u << lane) - 1u;
 #pragma unroll
@@ -179,11 +298,8 @@ __global__ void __launch_bounds__(kBlock)
   // Publish this tile's aggregate, then look back for the exclusive prefix.
   unsigned long long* my = status + static_cast<uint64_t>(tile) * kBins + d;
   const unsigned long long ep = static_cast<unsigned long long>(epoch) << 32;
-  if (tile == 0) {
-    *reinterpret_cast<volatile unsigned long long*>(my) = ep | kPrefixFlag | tile_cnt;
-  } else {
-    *reinterpret_cast<volatile unsigned long long*>(my) = ep | tile_cnt;
-  }
+  *reinterpret_cast<volatile unsigned long long*>(my) =
+      ep | (tile == 0 ? kPrefixFlag : 0ull) | tile_cnt;
   uint32_t excl = 0;
   if (tile > 0) {
     for (int64_t t = static_cast<int64_t>(tile) - 1; t >= 0; --t) {
@@ -224,157 +340,89 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
-// Small sorts (n <= kSmallN, the common size of a one-hot batch's multi list) run all
-// passes inside one CTA in shared memory: one launch instead of 1 + passes.
-constexpr int kSmallBlock = 1024;
-constexpr int kSmallItems = 4;
-constexpr uint32_t kSmallN = kSmallBlock * kSmallItems;
-
+// Scratch words (u32 units) to sort up to n pairs on the large path.
 template <typename K>
-constexpr size_t small_smem() {
-  return 2 * kSmallN * (sizeof(K) + sizeof(uint32_t)) + (kSmallBlock / 32 + 2) * kBins * 4;
-}
-
-template <typename K>
-__global__ void __launch_bounds__(kSmallBlock)
-    small_sort_kernel(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-                      K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-                      const uint32_t* n_dev, uint32_t n_host, int passes) {
-  constexpr int kW = kSmallBlock / 32;
-  const uint32_t n = count_of(n_dev, n_host);
-  if (n > kSmallN) return;  // the multi-kernel path handles it
-  extern __shared__ __align__(16) unsigned char smem[];
-  K* sk = reinterpret_cast<K*>(smem);                              // [2][kSmallN]
-  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + 2 * kSmallN);    // [2][kSmallN]
-  uint32_t* wc = sv + 2 * kSmallN;                                 // [kW][kBins]
-  uint32_t* dstart = wc + kW * kBins;                              // [kBins]
-  uint32_t* scr = dstart + kBins;                                  // [kBins]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t i = threadIdx.x; i < n; i += kSmallBlock) {
-    sk[i] = keys_in[i];
-    sv[i] = vals_in[i];
-  }
-  int cur = 0;
-  const uint32_t lt_mask = (1u << lane) - 1u;
-  for (int p = 0; p < passes; ++p) {
-    const int shift = p * kBits;
-    for (int i = threadIdx.x; i < kW * kBins; i += kSmallBlock) wc[i] = 0;
-    __syncthreads();
-    K k[kSmallItems];
-    uint32_t v[kSmallItems], r[kSmallItems];
-#pragma unroll
-    for (int j = 0; j < kSmallItems; ++j) {
-      const uint32_t idx = warp * 32 * kSmallItems + j * 32 + lane;
-      const bool ok = idx < n;
-      k[j] = ok ? sk[cur * kSmallN + idx] : K(0);
-      v[j] = ok ? sv[cur * kSmallN + idx] : 0u;
-      const uint32_t d = ok ? digit_of(k[j], shift) : static_cast<uint32_t>(kBins);
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
-      const uint32_t before = wc[warp * kBins + (d & (kBins - 1))];
-      r[j] = before + __popc(peers & lt_mask);
-      __syncwarp();
-      if (ok && lane == __ffs(peers) - 1) wc[warp * kBins + d] = before + __popc(peers);
-      __syncwarp();
-    }
-    __syncthreads();
-    uint32_t tot = 0;
-    if (threadIdx.x < kBins) {
-      for (int w = 0; w < kW; ++w) {
-        const uint32_t c = wc[w * kBins + threadIdx.x];
-        wc[w * kBins + threadIdx.x] = tot;
-        tot += c;
-      }
-      scr[threadIdx.x] = tot;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t run = 0;
-      for (int d = 0; d < kBins; ++d) {
-        dstart[d] = run;
-        run += scr[d];
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kSmallItems; ++j) {
-      const uint32_t idx = warp * 32 * kSmallItems + j * 32 + lane;
-      if (idx < n) {
-        const uint32_t d = digit_of(k[j], shift);
-        const uint32_t pos = dstart[d] + wc[warp * kBins + d] + r[j];
-        sk[(cur ^ 1) * kSmallN + pos] = k[j];
-        sv[(cur ^ 1) * kSmallN + pos] = v[j];
-      }
-    }
-    cur ^= 1;
-    __syncthreads();
-  }
-  for (uint32_t i = threadIdx.x; i < n; i += kSmallBlock) {
-    keys_out[i] = sk[cur * kSmallN + i];
-    vals_out[i] = sv[cur * kSmallN + i];
-  }
-}
-
-// Scratch words (u32 units) to sort up to n_max pairs: histograms, tile counters and
-// the look-back status words.
-template <typename K>
-inline size_t scratch_words(uint64_t n_max) {
-  uint64_t tiles = (n_max + Tile<K>::kTile - 1) / Tile<K>::kTile;
+inline size_t scratch_words(uint64_t n) {
+  uint64_t tiles = (n + Tile<K>::kTile - 1) / Tile<K>::kTile;
   if (tiles == 0) tiles = 1;
   return kMaxPasses * kBins + kMaxPasses * 2 + tiles * kBins * 2 + 2;
 }
 
-// Sorts (keys, vals) by key bits [0, key_bits). The element count is n_dev[0] when
-// n_dev is given (device memory, <= n_max) else n_max. Ping-pongs between the (a) and
-// (b) buffers; returns true when the result lives in (b). scratch needs
-// scratch_words<K>(n_max) u32 words (8-byte aligned).
 template <typename K>
-inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b, uint64_t n_max,
-                       const uint32_t* n_dev, int key_bits, uint32_t* scratch,
-                       cudaStream_t stream, int sms = 148) {
-  if (n_max <= 1 || key_bits <= 0) return false;
-  static bool attr_set = false;
-  if (!attr_set) {
-    HPS_CUDA(cudaFuncSetAttribute(pass_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(Tile<K>::kSmem)));
-    HPS_CUDA(cudaFuncSetAttribute(small_sort_kernel<K>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(small_smem<K>())));
-    attr_set = true;
-  }
+inline void set_smem_attrs() {
+  static bool done = false;
+  if (done) return;
+  HPS_CUDA(cudaFuncSetAttribute(pass_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(Tile<K>::kSmem)));
+  HPS_CUDA(cudaFuncSetAttribute(small_sort_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(small_smem<K>())));
+  done = true;
+}
+
+// Sorts n (host count) pairs by key bits [0, key_bits). vals_a == nullptr sorts the
+// positions 0..n-1. gate != nullptr: the whole sort runs only if *gate > kSmallN
+// (device-side choice between this and the small composite path). Returns true when
+// the result lives in the (b) buffers. scratch needs scratch_words<K>(n) words.
+// keys_in0 != nullptr: the first pass reads its keys from there (left untouched) and
+// keys_a is only scratch. iota_vals: the values are the positions 0..n-1 (vals_a is
+// then only scratch too).
+template <typename K>
+inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b, uint64_t n,
+                       int key_bits, uint32_t* scratch, cudaStream_t stream, int sms = 148,
+                       const uint32_t* gate = nullptr, const K* keys_in0 = nullptr,
+                       bool iota_vals = false) {
+  if (key_bits <= 0) key_bits = 1;
+  set_smem_attrs<K>();
   const int passes = (key_bits + kBits - 1) / kBits;
-  const bool out_b = (passes & 1) != 0;  // where the multi-kernel path leaves the result
-  // Device-sized (or host-small) sorts first try the one-CTA path; the multi-kernel
-  // kernels below skip themselves when it applied (device count <= kSmallN).
-  if (n_dev || n_max <= kSmallN) {
+  const K* first = keys_in0 ? keys_in0 : keys_a;
+  const uint32_t* first_vals = iota_vals ? nullptr : vals_a;
+  if (!gate && n <= kSmallN) {
+    if (n == 0) return false;
     small_sort_kernel<K><<<1, kSmallBlock, small_smem<K>(), stream>>>(
-        keys_a, vals_a, out_b ? keys_b : keys_a, out_b ? vals_b : vals_a, n_dev,
-        static_cast<uint32_t>(n_max), passes);
+        first, first_vals, keys_b, vals_b, static_cast<uint32_t>(n), passes);
     HPS_LAUNCH_CHECK();
-    if (!n_dev || n_max <= kSmallN) return out_b;
+    return true;
   }
-  const uint32_t tiles = ceil_div(n_max, Tile<K>::kTile);
-  uint32_t* hist = scratch;                                  // [kMaxPasses][kBins]
-  uint32_t* tile_ctr = hist + kMaxPasses * kBins;            // [kMaxPasses * 2]
+  const uint32_t tiles = ceil_div(n, Tile<K>::kTile);
+  uint32_t* hist = scratch;                       // [kMaxPasses][kBins]
+  uint32_t* tile_ctr = hist + kMaxPasses * kBins;  // [kMaxPasses * 2]
   uint64_t off = (kMaxPasses * kBins + kMaxPasses * 2 + 1) & ~1ull;
   unsigned long long* status = reinterpret_cast<unsigned long long*>(scratch + off);
   HPS_CUDA(cudaMemsetAsync(scratch, 0, (kMaxPasses * kBins + kMaxPasses * 2) * sizeof(uint32_t),
                            stream));
-  const uint32_t n_host = static_cast<uint32_t>(n_max);
+  const uint32_t n32 = static_cast<uint32_t>(n);
   const uint32_t hblocks = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms) * 4);
-  hist_kernel<K><<<hblocks, kBlock, 0, stream>>>(keys_a, n_dev, n_host, passes, hist);
+  hist_kernel<K><<<hblocks, kBlock, 0, stream>>>(first, n32, passes, hist, gate);
   bool in_b = false;
   for (int p = 0; p < passes; ++p) {
-    const K* ki = in_b ? keys_b : keys_a;
-    const uint32_t* vi = in_b ? vals_b : vals_a;
+    const K* ki = p == 0 ? first : (in_b ? keys_b : keys_a);
+    const uint32_t* vi = p == 0 ? first_vals : (in_b ? vals_b : vals_a);
     K* ko = in_b ? keys_a : keys_b;
     uint32_t* vo = in_b ? vals_a : vals_b;
     const uint32_t epoch = g_epoch.fetch_add(1) + 1;
     pass_kernel<K><<<tiles, kBlock, Tile<K>::kSmem, stream>>>(
-        ki, vi, ko, vo, n_dev, n_host, p * kBits, hist + p * kBins, status, tile_ctr + p, epoch);
+        ki, vi, ko, vo, n32, p * kBits, hist + p * kBins, status, tile_ctr + p, epoch, gate);
     in_b = !in_b;
   }
   HPS_LAUNCH_CHECK_N(1 + passes);
   return in_b;
+}
+
+// The small composite path (see small_composite_kernel).
+inline void sort_composite_small(const unsigned long long* keys, const uint32_t* n_dev, int lbits,
+                                 int total_bits, uint32_t* out_slot, uint32_t* out_listing,
+                                 cudaStream_t stream) {
+  static bool done = false;
+  if (!done) {
+    HPS_CUDA(cudaFuncSetAttribute(small_composite_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(small_smem<unsigned long long>())));
+    done = true;
+  }
+  const int passes = std::max(1, (total_bits + kBits - 1) / kBits);
+  small_composite_kernel<<<1, kSmallBlock, small_smem<unsigned long long>(), stream>>>(
+      keys, n_dev, lbits, passes, out_slot, out_listing);
+  HPS_LAUNCH_CHECK();
 }
 
 // Exclusive scan of one row of `tiles` u32 per block (blockIdx.x = row), in place;

@@ -266,6 +266,7 @@ void batch_free(Batch& b) {
   forget_outstanding(b);
   void* ptrs[] = {b.offsets, b.lgrp,  b.slot, b.eidx,    b.keys_a,  b.vals_a,
                   b.keys_b,  b.vals_b, b.rv,  b.new_slots, b.kind,  b.hist,
+                  b.mkeys,   b.small_slot, b.small_listing,
                   b.small,   b.skeys_a, b.skeys_b, b.sperm_a, b.sperm_b, b.sstart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -361,7 +362,9 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
     }
     c = 0;
     ensure(b.kind, c, n);
-    size_t hw = radix::scratch_words<uint32_t>(n) + classify_status_words(n) + 2;
+    c = 0;
+    ensure(b.mkeys, c, n);
+    size_t hw = radix::scratch_words<uint32_t>(n);
     if (hw > b.hist_cap) {
       c = 0;
       ensure(b.hist, c, hw);
@@ -396,21 +399,46 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
   if (!b.small) {
     uint64_t c = 0;
     ensure(b.small, c, 8);
+    c = 0;
+    ensure(b.small_slot, c, radix::kSmallN);
+    c = 0;
+    ensure(b.small_listing, c, radix::kSmallN);
   }
+}
+
+// The update arguments describing a registered batch's plan.
+static UpdateArgs plan_args(const Batch& b) {
+  UpdateArgs a{};
+  a.sorted_slot = b.sorted_slot;
+  a.sorted_listing = b.sorted_listing;
+  a.small_slot = b.small_slot;
+  a.small_listing = b.small_listing;
+  a.n = b.N;
+  a.n_dev = b.all_multi ? nullptr : &b.small[0];
+  a.kind = b.kind;
+  a.slots = b.slot;
+  a.eidx = b.all_multi ? nullptr : b.eidx;
+  a.lgrp = b.lgrp;
+  a.offsets = b.offsets;
+  a.F = b.F;
+  return a;
 }
 
 static int slot_key_bits(const Table* t) {
   return std::max(1, bits_for(static_cast<uint64_t>(t->cfg.capacity) - 1));
 }
 
-// Stable sort of the staged (keys_a = slot, vals_a = listing) pairs by slot: every
-// row's listings become one contiguous run in apply order. n_dev: element count in
-// device memory (the compacted multi list), else b.N.
-static void sort_slots(Batch& b, const uint32_t* n_dev, cudaStream_t st) {
+// Stable sort of (slot, listing) pairs by slot: every row's listings become one
+// contiguous run in apply order. keys_in0 = slots to sort (else keys_a); iota: the
+// listings are the positions 0..N-1 (else vals_a); gate = device-side condition
+// (radix_sort.cuh).
+static void sort_slots(Batch& b, const uint32_t* keys_in0, bool iota, const uint32_t* gate,
+                       cudaStream_t st) {
   Table* t = b.table;
   ProfScope p(t, "sort", st);
-  bool in_b = radix::sort_pairs<uint32_t>(b.keys_a, b.vals_a, b.keys_b, b.vals_b, b.N, n_dev,
-                                          slot_key_bits(t), b.hist, st, t->sm_count);
+  bool in_b = radix::sort_pairs<uint32_t>(b.keys_a, b.vals_a, b.keys_b, b.vals_b, b.N,
+                                          slot_key_bits(t), b.hist, st, t->sm_count, gate,
+                                          keys_in0, iota);
   b.sorted_slot = in_b ? b.keys_b : b.keys_a;
   b.sorted_listing = in_b ? b.vals_b : b.vals_a;
 }
@@ -463,24 +491,29 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     // Apply order = ascending sample key: enumerate listings sample by sample in key
     // order before the stable slot sort.
     launch_sample_order(d_sk, B, b.skeys_a, b.sperm_a, st);
-    bool in_b = radix::sort_pairs<uint64_t>(b.skeys_a, b.sperm_a, b.skeys_b, b.sperm_b, B,
-                                            nullptr, 64, b.hist, st, t->sm_count);
+    bool in_b = radix::sort_pairs<uint64_t>(b.skeys_a, b.sperm_a, b.skeys_b, b.sperm_b, B, 64,
+                                            b.hist, st, t->sm_count);
     const uint32_t* perm = in_b ? b.sperm_b : b.sperm_a;
     launch_sample_lengths(perm, b.offsets, B, F, b.sstart, st);
     launch_scan_inplace(b.sstart, B, b.sstart + B, st);
     launch_permuted_listing(perm, b.sstart, b.offsets, b.slot, B, F, b.keys_a, b.vals_a, st);
-    sort_slots(b, nullptr, st);
+    sort_slots(b, nullptr, false, nullptr, st);
   } else {
-    // Plan: rows listed once apply directly; the rest are compacted in listing order
-    // and sorted by slot (plan.cu).
+    // Plan (plan.cu): rows listed once apply directly; the multi listings are ordered
+    // by the one-CTA composite sort, or -- past kSmallN of them -- the whole batch is
+    // slot-sorted instead. Both sorts are launched; the device count picks one.
+    const int lbits = std::max(1, bits_for(N ? N - 1 : 0));
     {
       ProfScope p(t, "plan", st);
-      const size_t sw = (radix::scratch_words<uint32_t>(b.N) + 1) & ~size_t(1);
-      launch_classify(t->d, b.slot, b.eidx, N, b.kind, b.keys_a, b.vals_a,
-                      &b.small[0], reinterpret_cast<unsigned long long*>(b.hist + sw),
-                      &b.small[4], st);
+      launch_classify(t->d, b.slot, b.eidx, N, lbits, b.kind, b.mkeys, &b.small[0], t->sm_count,
+                      st);
     }
-    sort_slots(b, &b.small[0], st);
+    {
+      ProfScope p(t, "sort_small", st);
+      radix::sort_composite_small(b.mkeys, &b.small[0], lbits, lbits + slot_key_bits(t),
+                                  b.small_slot, b.small_listing, st);
+    }
+    sort_slots(b, b.slot, true, &b.small[0], st);
   }
   b.registered = true;
   b.pulled = false;
@@ -516,9 +549,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   if (epoch != t->epoch) {
     // PsShard::apply_gradients epoch fence (embedding_ps.hpp:142-145): drop every
     // (sample, unique id) entry of the batch, count them.
-    launch_count_pairs(b.all_multi ? nullptr : b.kind, b.N, b.sorted_slot, b.sorted_listing,
-                       b.lgrp, b.F, b.all_multi ? nullptr : &b.small[0], b.N,
-                       t->d.ctr + kCtrStaleDrops, st);
+    launch_count_pairs(plan_args(b), t->d.ctr + kCtrStaleDrops, st);
     if (!(flags & HPS_ASYNC)) HPS_CUDA(cudaStreamSynchronize(st));
     if (accepted) *accepted = 0;
     return;
@@ -535,17 +566,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     ProfScope p(t, "check", st);
     launch_check_batch(d_g, b.offsets, b.B, b.F, D, mean, t->d.ctr, st);
   }
-  UpdateArgs a{};
-  a.sorted_slot = b.sorted_slot;
-  a.sorted_listing = b.sorted_listing;
-  a.n = b.N;
-  a.n_dev = b.all_multi ? nullptr : &b.small[0];
-  a.kind = b.kind;
-  a.slots = b.slot;
-  a.eidx = b.all_multi ? nullptr : b.eidx;
-  a.lgrp = b.lgrp;
-  a.offsets = b.offsets;
-  a.F = b.F;
+  UpdateArgs a = plan_args(b);
   a.mean = mean;
   a.grads = d_g;
   a.lr = lr;
@@ -585,9 +606,7 @@ uint64_t batch_pairs(Batch& b) {
   if (!b.registered) return 0;
   Table* t = b.table;
   HPS_CUDA(cudaMemset(t->d.ctr + kCtrScratch, 0, sizeof(unsigned long long)));
-  launch_count_pairs(b.all_multi ? nullptr : b.kind, b.N, b.sorted_slot, b.sorted_listing,
-                     b.lgrp, b.F, b.all_multi ? nullptr : &b.small[0], b.N,
-                     t->d.ctr + kCtrScratch, nullptr);
+  launch_count_pairs(plan_args(b), t->d.ctr + kCtrScratch, nullptr);
   unsigned long long p = 0;
   HPS_CUDA(cudaMemcpy(&p, t->d.ctr + kCtrScratch, sizeof(p), cudaMemcpyDeviceToHost));
   return p;
@@ -664,7 +683,7 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
   b.F = 1;
   launch_probe(t->d, d_ids, n, b.slot, b.keys_a, b.vals_a, b.new_slots, &b.small[2], nullptr, st);
   launch_lazy_init(t->d, b.new_slots, &b.small[2], n, t->sm_count, st);
-  sort_slots(b, nullptr, st);
+  sort_slots(b, nullptr, false, nullptr, st);
   b.all_multi = true;
   UpdateArgs a{};
   a.sorted_slot = b.sorted_slot;

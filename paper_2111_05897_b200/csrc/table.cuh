@@ -115,10 +115,12 @@ struct Batch {
   uint32_t* rv = nullptr;         // [N] per-listing read version (u32) from the last pull
   uint32_t* new_slots = nullptr;  // [N] rows inserted by register (lazy-init queue)
   uint8_t* kind = nullptr;        // [N] plan: 1 = row listed once, 2 = multi (sorted path)
+  unsigned long long* mkeys = nullptr;  // [N] multi listings as (slot << lbits | listing)
+  uint32_t* small_slot = nullptr;       // [kSmallN] multi listings sorted (small path)
+  uint32_t* small_listing = nullptr;
   uint32_t* hist = nullptr;       // sort / plan scratch
   size_t hist_cap = 0;
-  uint32_t* small = nullptr;      // device scalars: [0] = multi listings, [2] = rows inserted,
-                                  // [4] = plan tile counter
+  uint32_t* small = nullptr;      // device scalars: [0] = multi listings, [2] = rows inserted
   bool all_multi = false;         // plan skipped: every listing on the sorted path
   bool rv_valid = false;          // rv holds the pull-time versions (else: no mutation since)
   // sample-order permutation (sample_keys != NULL)
@@ -201,10 +203,15 @@ void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B,
                         uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st);
 
 struct UpdateArgs {
+  // Multi kernel input: either the large-path slot sort of all n listings, or -- when
+  // n_dev is given and *n_dev <= kSmallN -- the small sorted multi list of *n_dev
+  // entries. Single kernel: skips everything when *n_dev > kSmallN (large path).
   const uint32_t* sorted_slot;
   const uint32_t* sorted_listing;
-  uint64_t n;            // sorted elements (multi kernel) / listings (single kernel)
-  const uint32_t* n_dev; // multi kernel: element count in device memory (overrides n)
+  const uint32_t* small_slot;
+  const uint32_t* small_listing;
+  uint64_t n;            // listings of the batch (entries of the direct apply)
+  const uint32_t* n_dev; // multi listings of the plan (device), or null
   const uint8_t* kind;   // single kernel: plan kinds per listing
   const uint32_t* slots; // single kernel: slot per listing
   const uint32_t* eidx;  // batch mode: hash entry per listing (counter reset); may be null
@@ -227,15 +234,11 @@ struct UpdateArgs {
 };
 void launch_update(const DevTable& t, const UpdateArgs& a, bool direct, int sms, cudaStream_t st);
 void launch_update_single(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
-void launch_count_pairs(const uint8_t* kind, uint64_t n_all, const uint32_t* ss,
-                        const uint32_t* sl, const uint32_t* lgrp, uint32_t F,
-                        const uint32_t* n_multi_dev, uint64_t n_multi_host,
-                        unsigned long long* ctr, cudaStream_t st);
+void launch_count_pairs(const UpdateArgs& a, unsigned long long* ctr, cudaStream_t st);
 // plan.cu
 void launch_classify(const DevTable& t, const uint32_t* slots, const uint32_t* eidx, uint64_t n,
-                     uint8_t* kind, uint32_t* mkeys, uint32_t* mvals, uint32_t* n_multi,
-                     unsigned long long* status, uint32_t* tile_ctr, cudaStream_t st);
-size_t classify_status_words(uint64_t n);
+                     int lbits, uint8_t* kind, unsigned long long* mkeys, uint32_t* n_multi,
+                     int sms, cudaStream_t st);
 
 void launch_sample_order(const uint64_t* sample_keys, uint32_t B, uint64_t* keys_out,
                          uint32_t* perm_out, cudaStream_t st);
