@@ -138,11 +138,45 @@ void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, 
 
 // ---- probe / lazy insert ------------------------------------------------------------------
 
+// ---- batch plan, built during the probe -----------------------------------------------
+// A row listed once in the batch ("single") gets exactly one optimizer application, so
+// its listing needs no ordering at all -- for the one-hot Criteo shape that is >99% of
+// all listings. Every listing stamps its row's plan word (HashEntry::sf, in the sector
+// the probe just read): the first listing of the batch installs (stamp, first listing);
+// any later one knows the row is "multi", marks itself, and the first one to set the
+// multi flag also marks the first listing. Multi listings are appended as composite
+// keys for the one-CTA sort while fewer than kSmallN are known (beyond that the whole
+// batch takes the large slot sort, decided on the device). The stamp changes every
+// batch, so plan words never need resetting.
+
+__device__ __forceinline__ void plan_mark(const PlanOut& p, uint32_t slot, uint64_t listing) {
+  p.kind[listing] = 2;
+  if (ld_volatile(p.n_multi) <= radix::kSmallN) {
+    const uint32_t pos = atomicAdd(p.n_multi, 1u);
+    if (pos < radix::kSmallN)
+      p.mkeys[pos] = (static_cast<unsigned long long>(slot) << p.lbits) | listing;
+  }
+}
+
+__device__ __forceinline__ void plan_listing(const PlanOut& p, unsigned long long* sf,
+                                             uint32_t slot, uint64_t i) {
+  const unsigned long long mine = (static_cast<unsigned long long>(p.stamp) << 32) | (i + 1);
+  unsigned long long old = __ldcg(sf);
+  while ((old >> 32) != p.stamp) {  // first listing of the row in this batch (so far)
+    const unsigned long long prev = atomicCAS(sf, old, mine);
+    if (prev == old) return;
+    old = prev;
+  }
+  plan_mark(p, slot, i);
+  if (!(old & kMultiFlag) && !(atomicOr(sf, kMultiFlag) & kMultiFlag))
+    plan_mark(p, slot, (old & (kMultiFlag - 1)) - 1);  // the row's first listing
+}
+
 __global__ void __launch_bounds__(256)
     probe_kernel(DevTable t, const uint64_t* __restrict__ ids, uint64_t n,
                  uint32_t* __restrict__ slots, uint32_t* __restrict__ sort_keys,
                  uint32_t* __restrict__ sort_vals, uint32_t* __restrict__ new_slots,
-                 uint32_t* __restrict__ new_count, uint32_t* __restrict__ eidx) {
+                 uint32_t* __restrict__ new_count, PlanOut plan, bool with_plan) {
   // kProbeILP listings per thread: their first probes are issued back to back (the
   // common case -- key found in its home entry -- then costs one round trip for all).
   constexpr int kProbeILP = 2;
@@ -173,12 +207,8 @@ __global__ void __launch_bounds__(256)
       s = find_or_insert(t, id[k], new_slots, new_count, true, &e);
     }
     slots[i] = s;
-    if (eidx) {
-      // Batch plan: count the row's listings in the entry just probed (same sector,
-      // fire-and-forget reduction; plan.cu).
-      eidx[i] = static_cast<uint32_t>(e);
-      if (slot_ok(t, s)) atomicAdd(e == kSpecialEntry ? t.special_cnt : &t.ht[e].cnt, 1u);
-    }
+    if (with_plan && slot_ok(t, s))
+      plan_listing(plan, e == kSpecialEntry ? t.special_sf : &t.ht[e].sf, s, i);
     if (sort_keys) {
       sort_keys[i] = s;
       sort_vals[i] = static_cast<uint32_t>(i);
@@ -188,26 +218,29 @@ __global__ void __launch_bounds__(256)
 
 void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* slots,
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
-                  uint32_t* new_count, uint32_t* eidx, cudaStream_t st) {
+                  uint32_t* new_count, const PlanOut* plan, cudaStream_t st) {
   if (!n) return;
   probe_kernel<<<ceil_div(n, 256 * 2), 256, 0, st>>>(t, ids, n, slots, sort_keys, sort_vals,
-                                                     new_slots, new_count, eidx);
+                                                     new_slots, new_count,
+                                                     plan ? *plan : PlanOut{}, plan != nullptr);
   HPS_LAUNCH_CHECK();
 }
 
-// Empty index: every key kEmptyKey, every slot kPending, every batch counter 0.
+// Empty index: every key kEmptyKey, every slot kPending, every plan word 0 (stamp 0 is
+// never a batch's stamp).
 __global__ void ht_clear_kernel(HashEntry* __restrict__ ht, uint64_t n) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    ulonglong2 v = make_ulonglong2(kEmptyKey, static_cast<unsigned long long>(kPending));
-    *reinterpret_cast<ulonglong2*>(ht + i) = v;
+    ulonglong2* e = reinterpret_cast<ulonglong2*>(ht + i);
+    e[0] = make_ulonglong2(kEmptyKey, static_cast<unsigned long long>(kPending));
+    e[1] = make_ulonglong2(0ull, 0ull);
   }
 }
 
 void launch_ht_clear(const DevTable& t, cudaStream_t st) {
   const uint64_t n = t.ht_mask + 1;
   ht_clear_kernel<<<std::min<uint64_t>(ceil_div(n, 256), 148 * 64), 256, 0, st>>>(t.ht, n);
-  HPS_CUDA(cudaMemsetAsync(t.special_cnt, 0, sizeof(uint32_t), st));
+  HPS_CUDA(cudaMemsetAsync(t.special_sf, 0, sizeof(unsigned long long), st));
   HPS_LAUNCH_CHECK();
 }
 

@@ -187,28 +187,38 @@ __global__ void __launch_bounds__(kSmallBlock)
 }
 
 // Device-sized small sort of composite keys (slot << lbits | listing): runs only when
-// *n_dev <= kSmallN and writes the sorted slots and listings separately.
+// *n_dev <= kSmallN and writes the sorted slots and listings separately. The keys are
+// unique (the listing is part of them), so an unstable bitonic network in shared
+// memory is exact -- log2(n)^2/2 barrier steps instead of 6-7 full radix passes.
 static __global__ void __launch_bounds__(kSmallBlock)
     small_composite_kernel(const unsigned long long* __restrict__ keys, const uint32_t* n_dev,
-                           int lbits, int passes, uint32_t* __restrict__ out_slot,
+                           int lbits, uint32_t* __restrict__ out_slot,
                            uint32_t* __restrict__ out_listing) {
   const uint32_t n = *n_dev;
-  if (n > kSmallN) return;  // the large path (gated on the same count) takes it
-  extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long* sk = reinterpret_cast<unsigned long long*>(smem);
-  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + 2 * kSmallN);
-  uint32_t* wc = sv + 2 * kSmallN;
-  uint32_t* dstart = wc + (kSmallBlock / 32) * kBins;
-  uint32_t* scr = dstart + kBins;
-  for (uint32_t i = threadIdx.x; i < n; i += kSmallBlock) {
-    sk[i] = keys[i];
-    sv[i] = 0;
-  }
+  if (n > kSmallN || n == 0) return;  // the large path (gated on the same count) takes it
+  __shared__ unsigned long long sk[kSmallN];
+  uint32_t P = 1;
+  while (P < n) P <<= 1;
+  for (uint32_t i = threadIdx.x; i < P; i += kSmallBlock) sk[i] = i < n ? keys[i] : ~0ull;
   __syncthreads();
-  const int cur = smem_lsd<unsigned long long>(sk, sv, wc, dstart, scr, n, 0, passes);
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < P; i += kSmallBlock) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long a = sk[i], b = sk[ixj];
+          if ((a > b) == ((i & k) == 0)) {
+            sk[i] = b;
+            sk[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
   const unsigned long long lmask = (1ull << lbits) - 1;
   for (uint32_t i = threadIdx.x; i < n; i += kSmallBlock) {
-    const unsigned long long k = sk[cur * kSmallN + i];
+    const unsigned long long k = sk[i];
     out_slot[i] = static_cast<uint32_t>(k >> lbits);
     out_listing[i] = static_cast<uint32_t>(k & lmask);
   }
@@ -371,6 +381,7 @@ inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b,
                        int key_bits, uint32_t* scratch, cudaStream_t stream, int sms = 148,
                        const uint32_t* gate = nullptr, const K* keys_in0 = nullptr,
                        bool iota_vals = false) {
+  if (n == 0) return false;
   if (key_bits <= 0) key_bits = 1;
   set_smem_attrs<K>();
   const int passes = (key_bits + kBits - 1) / kBits;
@@ -410,18 +421,10 @@ inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b,
 
 // The small composite path (see small_composite_kernel).
 inline void sort_composite_small(const unsigned long long* keys, const uint32_t* n_dev, int lbits,
-                                 int total_bits, uint32_t* out_slot, uint32_t* out_listing,
+                                 uint32_t* out_slot, uint32_t* out_listing,
                                  cudaStream_t stream) {
-  static bool done = false;
-  if (!done) {
-    HPS_CUDA(cudaFuncSetAttribute(small_composite_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(small_smem<unsigned long long>())));
-    done = true;
-  }
-  const int passes = std::max(1, (total_bits + kBits - 1) / kBits);
-  small_composite_kernel<<<1, kSmallBlock, small_smem<unsigned long long>(), stream>>>(
-      keys, n_dev, lbits, passes, out_slot, out_listing);
+  small_composite_kernel<<<1, kSmallBlock, 0, stream>>>(keys, n_dev, lbits, out_slot,
+                                                        out_listing);
   HPS_LAUNCH_CHECK();
 }
 

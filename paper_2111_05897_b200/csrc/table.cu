@@ -214,7 +214,7 @@ Table* table_create(const hps_table_cfg& cfg) {
     HPS_CUDA(cudaMalloc(&d.ht, H * sizeof(HashEntry)));
     HPS_CUDA(cudaMalloc(&d.rows, C * d.stride * sizeof(float)));
     d.vt = VtView{d.rows, d.stride, 2 * d.D};
-    HPS_CUDA(cudaMalloc(&d.special_cnt, sizeof(uint32_t)));
+    HPS_CUDA(cudaMalloc(&d.special_sf, sizeof(unsigned long long)));
     HPS_CUDA(cudaMalloc(&d.slot_id, C * sizeof(uint64_t)));
     HPS_CUDA(cudaMalloc(&d.special, sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.hwm, sizeof(uint32_t)));
@@ -264,7 +264,7 @@ static void protect_reads(Table* t, const Batch* except, cudaStream_t st) {
 
 void batch_free(Batch& b) {
   forget_outstanding(b);
-  void* ptrs[] = {b.offsets, b.lgrp,  b.slot, b.eidx,    b.keys_a,  b.vals_a,
+  void* ptrs[] = {b.offsets, b.lgrp,  b.slot,   b.keys_a,  b.vals_a,
                   b.keys_b,  b.vals_b, b.rv,  b.new_slots, b.kind,  b.hist,
                   b.mkeys,   b.small_slot, b.small_listing,
                   b.small,   b.skeys_a, b.skeys_b, b.sperm_a, b.sperm_b, b.sstart};
@@ -286,7 +286,7 @@ void table_destroy(Table* t) {
     t->stage.free_all();
     t->prof.destroy();
     DevTable& d = t->d;
-    void* ptrs[] = {d.ht,  d.rows, d.special_cnt, d.slot_id, d.special,
+    void* ptrs[] = {d.ht,  d.rows, d.special_sf, d.slot_id, d.special,
                     d.hwm, d.ctr,  t->d_salts};
     for (void* p : ptrs)
       if (p) cudaFree(p);
@@ -354,7 +354,7 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
   uint64_t n = std::max<uint64_t>(N, 1);
   if (n > b.cap_N) {
     uint64_t c = 0;
-    uint32_t** bufs[] = {&b.lgrp, &b.slot,   &b.eidx, &b.keys_a,   &b.vals_a,
+    uint32_t** bufs[] = {&b.lgrp, &b.slot,   &b.keys_a,   &b.vals_a,
                          &b.keys_b, &b.vals_b, &b.rv,   &b.new_slots};
     for (uint32_t** p : bufs) {
       c = 0;
@@ -417,7 +417,6 @@ static UpdateArgs plan_args(const Batch& b) {
   a.n_dev = b.all_multi ? nullptr : &b.small[0];
   a.kind = b.kind;
   a.slots = b.slot;
-  a.eidx = b.all_multi ? nullptr : b.eidx;
   a.lgrp = b.lgrp;
   a.offsets = b.offsets;
   a.F = b.F;
@@ -481,10 +480,17 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   // Sample keys that reorder the batch: every listing takes the sorted (multi) path.
   const bool permute = d_sk && B > 1;
   b.all_multi = permute;
+  // Plan (see probe_kernel): rows listed once apply directly; the multi listings are
+  // ordered by the one-CTA composite sort, or -- past kSmallN of them -- the whole
+  // batch is slot-sorted instead. Both sorts are launched; the device count picks one.
+  const int lbits = std::max(1, bits_for(N ? N - 1 : 0));
+  PlanOut plan{b.kind, b.mkeys, &b.small[0], ++t->plan_stamp, lbits};
+  if (t->plan_stamp == 0) plan.stamp = t->plan_stamp = 1;  // 0 marks "never listed"
+  if (!permute && N) HPS_CUDA(cudaMemsetAsync(b.kind, 1, N, st));
   {
     ProfScope p(t, "probe", st);
     launch_probe(t->d, d_ids, N, b.slot, nullptr, nullptr, b.new_slots, &b.small[2],
-                 permute ? nullptr : b.eidx, st);
+                 permute ? nullptr : &plan, st);
   }
   launch_lazy_init(t->d, b.new_slots, &b.small[2], N, t->sm_count, st);
   if (permute) {
@@ -499,19 +505,10 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     launch_permuted_listing(perm, b.sstart, b.offsets, b.slot, B, F, b.keys_a, b.vals_a, st);
     sort_slots(b, nullptr, false, nullptr, st);
   } else {
-    // Plan (plan.cu): rows listed once apply directly; the multi listings are ordered
-    // by the one-CTA composite sort, or -- past kSmallN of them -- the whole batch is
-    // slot-sorted instead. Both sorts are launched; the device count picks one.
-    const int lbits = std::max(1, bits_for(N ? N - 1 : 0));
-    {
-      ProfScope p(t, "plan", st);
-      launch_classify(t->d, b.slot, b.eidx, N, lbits, b.kind, b.mkeys, &b.small[0], t->sm_count,
-                      st);
-    }
     {
       ProfScope p(t, "sort_small", st);
-      radix::sort_composite_small(b.mkeys, &b.small[0], lbits, lbits + slot_key_bits(t),
-                                  b.small_slot, b.small_listing, st);
+      radix::sort_composite_small(b.mkeys, &b.small[0], lbits, b.small_slot, b.small_listing,
+                                  st);
     }
     sort_slots(b, b.slot, true, &b.small[0], st);
   }

@@ -36,15 +36,29 @@ enum CounterIdx : int {
   kCtrCount = 32
 };
 
-// One 16-byte index entry: a probe touches a single 32-byte sector. `cnt` counts the
-// row's listings in the batch being planned (plan.cu): it shares the probed sector,
-// so counting costs no extra DRAM traffic; 0 between batches.
-struct __align__(16) HashEntry {
+// One 32-byte index entry = one DRAM sector per probe. `sf` is the row's batch-plan
+// word (stamp of the batch that last listed the row << 32 | multi flag << 31 | first
+// listing + 1), updated by the probe in the sector it just read (see probe_kernel).
+struct __align__(32) HashEntry {
   unsigned long long key;  // kEmptyKey when free
   uint32_t slot;           // kPending while the inserting thread publishes it
-  uint32_t cnt;
+  uint32_t pad0;
+  unsigned long long sf;
+  unsigned long long pad1;
 };
-constexpr uint32_t kSpecialEntry = 0xffffffffu;  // entry index of id == kEmptyKey
+constexpr unsigned long long kMultiFlag = 1ull << 31;
+constexpr uint64_t kSpecialEntry = ~0ull;  // "entry index" of id == kEmptyKey
+
+// Batch plan written by the probe of a register: kind[i] (pre-set to 1) becomes 2 for
+// every listing of a row listed more than once; those listings are appended as
+// composite keys (slot << lbits | listing) while fewer than radix::kSmallN are known.
+struct PlanOut {
+  uint8_t* kind;
+  unsigned long long* mkeys;
+  uint32_t* n_multi;
+  uint32_t stamp;
+  int lbits;
+};
 
 // The {version, latest bump tag} word of a row lives in the row's own 16-byte header
 // right after [w | acc]: the update's version read-modify-write then falls in the row's
@@ -68,7 +82,7 @@ struct DevTable {
   uint32_t D;
   uint32_t stride;  // floats per row: 2D + 4 ([w D | acc D | header 16 B])
   VtView vt;        // {version, latest bump tag} in each row's header
-  uint32_t* special_cnt;  // batch listing counter of id == kEmptyKey (no hash entry)
+  unsigned long long* special_sf;  // plan word of id == kEmptyKey (it has no hash entry)
   uint64_t* slot_id;
   uint32_t capacity;
   uint32_t* hwm;
@@ -105,7 +119,6 @@ struct Batch {
   uint32_t* offsets = nullptr;    // [B*F+1] our copy of the CSR offsets
   uint32_t* lgrp = nullptr;       // [N] listing -> b*F+g
   uint32_t* slot = nullptr;       // [N] listing -> table slot
-  uint32_t* eidx = nullptr;       // [N] listing -> hash entry index (batch counters)
   uint32_t* keys_a = nullptr;     // [N] sort ping-pong (slot keys)
   uint32_t* vals_a = nullptr;     //     (listing values)
   uint32_t* keys_b = nullptr;
@@ -166,6 +179,7 @@ struct Table {
   uint64_t* d_salts = nullptr;
   std::vector<uint64_t> salts;
   uint32_t epoch = 0;
+  uint32_t plan_stamp = 0;  // batch stamp of the last register (HashEntry::sf)
   uint32_t sm_count = 148;
   std::mutex mu;  // one call at a time per table (PsShard's per-shard lock)
   Batch scratch;  // workspace for the stateless entry points
@@ -181,10 +195,10 @@ void launch_route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cu
 void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st);
 // slots[i] = find_or_insert(ids[i]); when sort_keys/sort_vals are given also writes the
 // (slot, i) pairs the apply-order sort consumes.
-// eidx != null: also count the row's listings in its hash entry and record the entry.
+// plan != null: also build the batch plan (PlanOut) while probing.
 void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* slots,
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
-                  uint32_t* new_count, uint32_t* eidx, cudaStream_t st);
+                  uint32_t* new_count, const PlanOut* plan, cudaStream_t st);
 void launch_ht_clear(const DevTable& t, cudaStream_t st);
 void launch_lazy_init(const DevTable& t, const uint32_t* new_slots, const uint32_t* new_count,
                       uint64_t max_new, int sms, cudaStream_t st);
@@ -214,7 +228,6 @@ struct UpdateArgs {
   const uint32_t* n_dev; // multi listings of the plan (device), or null
   const uint8_t* kind;   // single kernel: plan kinds per listing
   const uint32_t* slots; // single kernel: slot per listing
-  const uint32_t* eidx;  // batch mode: hash entry per listing (counter reset); may be null
   // batch mode
   const uint32_t* lgrp;
   const uint32_t* offsets;
@@ -235,10 +248,6 @@ struct UpdateArgs {
 void launch_update(const DevTable& t, const UpdateArgs& a, bool direct, int sms, cudaStream_t st);
 void launch_update_single(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
 void launch_count_pairs(const UpdateArgs& a, unsigned long long* ctr, cudaStream_t st);
-// plan.cu
-void launch_classify(const DevTable& t, const uint32_t* slots, const uint32_t* eidx, uint64_t n,
-                     int lbits, uint8_t* kind, unsigned long long* mkeys, uint32_t* n_multi,
-                     int sms, cudaStream_t st);
 
 void launch_sample_order(const uint64_t* sample_keys, uint32_t B, uint64_t* keys_out,
                          uint32_t* perm_out, cudaStream_t st);
