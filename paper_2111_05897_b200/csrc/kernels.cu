@@ -69,7 +69,9 @@ __device__ uint32_t find_or_insert(const DevTable& t, uint64_t id, uint32_t* new
     }
     return s;
   }
-  uint64_t h = mix64(id ^ kTableHashSalt) >> t.ht_shift;
+  // Probing starts at the first entry of the home 128-byte line (4 entries): a DRAM
+  // access brings the whole line anyway, and the probe kernel's fast path checks it.
+  uint64_t h = (mix64(id ^ kTableHashSalt) >> t.ht_shift) & ~3ull;
   for (uint64_t probes = 0; probes <= t.ht_mask; ++probes) {
     HashEntry* e = &t.ht[h];
     // one 16-byte load brings key and slot together
@@ -182,30 +184,37 @@ __global__ void __launch_bounds__(256)
   constexpr int kProbeILP = 2;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x * kProbeILP + threadIdx.x;
   uint64_t id[kProbeILP], h[kProbeILP];
-  ulonglong2 kv[kProbeILP];
+  ulonglong2 kv[kProbeILP][4];
 #pragma unroll
   for (int k = 0; k < kProbeILP; ++k) {
     const uint64_t i = base + static_cast<uint64_t>(k) * blockDim.x;
     id[k] = i < n ? ids[i] : kEmptyKey;
   }
+  // the home line (4 entries) of every listing, all loads in flight together
 #pragma unroll
   for (int k = 0; k < kProbeILP; ++k) {
-    h[k] = mix64(id[k] ^ kTableHashSalt) >> t.ht_shift;
-    kv[k] = id[k] != kEmptyKey ? __ldcg(reinterpret_cast<const ulonglong2*>(t.ht + h[k]))
-                               : make_ulonglong2(0, 0);
+    h[k] = (mix64(id[k] ^ kTableHashSalt) >> t.ht_shift) & ~3ull;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      kv[k][q] = id[k] != kEmptyKey
+                     ? __ldcg(reinterpret_cast<const ulonglong2*>(t.ht + h[k] + q))
+                     : make_ulonglong2(0, 0);
   }
 #pragma unroll
   for (int k = 0; k < kProbeILP; ++k) {
     const uint64_t i = base + static_cast<uint64_t>(k) * blockDim.x;
     if (i >= n) break;
-    uint64_t e;
-    uint32_t s;
-    if (id[k] != kEmptyKey && kv[k].x == id[k] && static_cast<uint32_t>(kv[k].y) != kPending) {
-      s = static_cast<uint32_t>(kv[k].y);  // hit in the home entry
-      e = h[k];
-    } else {
-      s = find_or_insert(t, id[k], new_slots, new_count, true, &e);
+    uint64_t e = kSpecialEntry;
+    uint32_t s = kPending;
+    if (id[k] != kEmptyKey) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (kv[k][q].x == id[k] && static_cast<uint32_t>(kv[k][q].y) != kPending) {
+          s = static_cast<uint32_t>(kv[k][q].y);  // hit in the home line
+          e = h[k] + q;
+        }
     }
+    if (s == kPending) s = find_or_insert(t, id[k], new_slots, new_count, true, &e);
     slots[i] = s;
     if (with_plan && slot_ok(t, s))
       plan_listing(plan, e == kSpecialEntry ? t.special_sf : &t.ht[e].sf, s, i);

@@ -197,25 +197,30 @@ static __global__ void __launch_bounds__(kSmallBlock)
   const uint32_t n = *n_dev;
   if (n > kSmallN || n == 0) return;  // the large path (gated on the same count) takes it
   __shared__ unsigned long long sk[kSmallN];
-  uint32_t P = 1;
+  uint32_t P = 2;
   while (P < n) P <<= 1;
   for (uint32_t i = threadIdx.x; i < P; i += kSmallBlock) sk[i] = i < n ? keys[i] : ~0ull;
   __syncthreads();
+  // Comparator c of stage (k, j) compares elements i = insert-0-bit(c, j) and i + j. With
+  // j <= 32 a warp's 32 consecutive comparators stay inside one 64-element window, so
+  // those stages only need warp synchronisation.
   for (uint32_t k = 2; k <= P; k <<= 1) {
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = threadIdx.x; i < P; i += kSmallBlock) {
-        const uint32_t ixj = i ^ j;
-        if (ixj > i) {
-          const unsigned long long a = sk[i], b = sk[ixj];
-          if ((a > b) == ((i & k) == 0)) {
-            sk[i] = b;
-            sk[ixj] = a;
-          }
+      for (uint32_t c = threadIdx.x; c < P / 2; c += kSmallBlock) {
+        const uint32_t i = ((c & ~(j - 1)) << 1) | (c & (j - 1));
+        const uint32_t ixj = i + j;
+        const unsigned long long a = sk[i], b = sk[ixj];
+        if ((a > b) == ((i & k) == 0)) {
+          sk[i] = b;
+          sk[ixj] = a;
         }
       }
-      __syncthreads();
+      const uint32_t next_j = j > 1 ? j >> 1 : k;
+      if (j >= 64 || next_j >= 64) __syncthreads();
+      else __syncwarp();
     }
   }
+  __syncthreads();
   const unsigned long long lmask = (1ull << lbits) - 1;
   for (uint32_t i = threadIdx.x; i < n; i += kSmallBlock) {
     const unsigned long long k = sk[i];

@@ -4,6 +4,7 @@
 // hps::Error and never returns status codes itself.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -197,6 +198,10 @@ Table* table_create(const hps_table_cfg& cfg) {
     DeviceGuard g(t->device);
     cudaDeviceProp prop{};
     HPS_CUDA(cudaGetDeviceProperties(&prop, t->device));
+    // Optional L2 fetch-granularity hint (bytes) for random-access-heavy workloads;
+    // a device-wide setting, so only applied when asked for.
+    if (const char* g = getenv("HPS_L2_FETCH_BYTES"))
+      HPS_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, atoi(g)));
     t->sm_count = prop.multiProcessorCount;
     const uint64_t C = cfg.capacity;
     uint64_t H = 1024;
