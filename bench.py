@@ -304,7 +304,7 @@ def main():
         it += 1
     torch.cuda.synchronize()
     regions = {}
-    for r in ("probe", "sort_small", "sort", "pool", "check", "update", "update_multi"):
+    for r in ("probe", "plan", "sort_small", "sort", "pool", "check", "update", "update_multi"):
         tot, cnt = table.profile_get(r)
         regions[r] = (tot / max(cnt, 1), cnt)
     table.profile(False)

@@ -52,8 +52,7 @@ __device__ uint32_t alloc_slot(const DevTable& t, uint64_t id, uint32_t* new_slo
 // entries; the inserting thread publishes the slot, racing readers of the same id
 // spin on that (single, in-flight) publication.
 __device__ uint32_t find_or_insert(const DevTable& t, uint64_t id, uint32_t* new_slots,
-                                   uint32_t* new_count, bool insert, uint64_t* entry = nullptr) {
-  if (entry) *entry = kSpecialEntry;
+                                   uint32_t* new_count, bool insert) {
   if (id == kEmptyKey) {
     uint32_t s = ld_volatile(t.special);
     if (s == kSpecialAbsent) {
@@ -69,9 +68,7 @@ __device__ uint32_t find_or_insert(const DevTable& t, uint64_t id, uint32_t* new
     }
     return s;
   }
-  // Probing starts at the first entry of the home 128-byte line (4 entries): a DRAM
-  // access brings the whole line anyway, and the probe kernel's fast path checks it.
-  uint64_t h = (mix64(id ^ kTableHashSalt) >> t.ht_shift) & ~3ull;
+  uint64_t h = mix64(id ^ kTableHashSalt) >> t.ht_shift;
   for (uint64_t probes = 0; probes <= t.ht_mask; ++probes) {
     HashEntry* e = &t.ht[h];
     // one 16-byte load brings key and slot together
@@ -85,7 +82,6 @@ __device__ uint32_t find_or_insert(const DevTable& t, uint64_t id, uint32_t* new
         uint32_t slot = alloc_slot(t, id, new_slots, new_count);
         __threadfence();
         atomicExch(&e->slot, slot);
-        if (entry) *entry = h;
         return slot;
       }
       k = old;
@@ -94,7 +90,6 @@ __device__ uint32_t find_or_insert(const DevTable& t, uint64_t id, uint32_t* new
     if (k == id) {
       uint32_t v = static_cast<uint32_t>(sv);
       while (v == kPending) v = ld_volatile(&e->slot);
-      if (entry) *entry = h;
       return v;
     }
     h = (h + 1) & t.ht_mask;
@@ -140,84 +135,44 @@ void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, 
 
 // ---- probe / lazy insert ------------------------------------------------------------------
 
-// ---- batch plan, built during the probe -----------------------------------------------
-// A row listed once in the batch ("single") gets exactly one optimizer application, so
-// its listing needs no ordering at all -- for the one-hot Criteo shape that is >99% of
-// all listings. Every listing stamps its row's plan word (HashEntry::sf, in the sector
-// the probe just read): the first listing of the batch installs (stamp, first listing);
-// any later one knows the row is "multi", marks itself, and the first one to set the
-// multi flag also marks the first listing. Multi listings are appended as composite
-// keys for the one-CTA sort while fewer than kSmallN are known (beyond that the whole
-// batch takes the large slot sort, decided on the device). The stamp changes every
-// batch, so plan words never need resetting.
-
-__device__ __forceinline__ void plan_mark(const PlanOut& p, uint32_t slot, uint64_t listing) {
-  p.kind[listing] = 2;
-  if (ld_volatile(p.n_multi) <= radix::kSmallN) {
-    const uint32_t pos = atomicAdd(p.n_multi, 1u);
-    if (pos < radix::kSmallN)
-      p.mkeys[pos] = (static_cast<unsigned long long>(slot) << p.lbits) | listing;
-  }
-}
-
-__device__ __forceinline__ void plan_listing(const PlanOut& p, unsigned long long* sf,
-                                             uint32_t slot, uint64_t i) {
-  const unsigned long long mine = (static_cast<unsigned long long>(p.stamp) << 32) | (i + 1);
-  unsigned long long old = __ldcg(sf);
-  while ((old >> 32) != p.stamp) {  // first listing of the row in this batch (so far)
-    const unsigned long long prev = atomicCAS(sf, old, mine);
-    if (prev == old) return;
-    old = prev;
-  }
-  plan_mark(p, slot, i);
-  if (!(old & kMultiFlag) && !(atomicOr(sf, kMultiFlag) & kMultiFlag))
-    plan_mark(p, slot, (old & (kMultiFlag - 1)) - 1);  // the row's first listing
-}
-
 __global__ void __launch_bounds__(256)
     probe_kernel(DevTable t, const uint64_t* __restrict__ ids, uint64_t n,
                  uint32_t* __restrict__ slots, uint32_t* __restrict__ sort_keys,
                  uint32_t* __restrict__ sort_vals, uint32_t* __restrict__ new_slots,
-                 uint32_t* __restrict__ new_count, PlanOut plan, bool with_plan) {
+                 uint32_t* __restrict__ new_count, bool plan) {
   // kProbeILP listings per thread: their first probes are issued back to back (the
   // common case -- key found in its home entry -- then costs one round trip for all).
   constexpr int kProbeILP = 2;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x * kProbeILP + threadIdx.x;
-  uint64_t id[kProbeILP], h[kProbeILP];
-  ulonglong2 kv[kProbeILP][4];
+  uint64_t id[kProbeILP];
+  ulonglong2 kv[kProbeILP];
 #pragma unroll
   for (int k = 0; k < kProbeILP; ++k) {
     const uint64_t i = base + static_cast<uint64_t>(k) * blockDim.x;
     id[k] = i < n ? ids[i] : kEmptyKey;
   }
-  // the home line (4 entries) of every listing, all loads in flight together
 #pragma unroll
   for (int k = 0; k < kProbeILP; ++k) {
-    h[k] = (mix64(id[k] ^ kTableHashSalt) >> t.ht_shift) & ~3ull;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      kv[k][q] = id[k] != kEmptyKey
-                     ? __ldcg(reinterpret_cast<const ulonglong2*>(t.ht + h[k] + q))
-                     : make_ulonglong2(0, 0);
+    const uint64_t h = mix64(id[k] ^ kTableHashSalt) >> t.ht_shift;
+    kv[k] = id[k] != kEmptyKey ? __ldcg(reinterpret_cast<const ulonglong2*>(t.ht + h))
+                               : make_ulonglong2(0, 0);
   }
 #pragma unroll
   for (int k = 0; k < kProbeILP; ++k) {
     const uint64_t i = base + static_cast<uint64_t>(k) * blockDim.x;
     if (i >= n) break;
-    uint64_t e = kSpecialEntry;
-    uint32_t s = kPending;
-    if (id[k] != kEmptyKey) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (kv[k][q].x == id[k] && static_cast<uint32_t>(kv[k][q].y) != kPending) {
-          s = static_cast<uint32_t>(kv[k][q].y);  // hit in the home line
-          e = h[k] + q;
-        }
-    }
-    if (s == kPending) s = find_or_insert(t, id[k], new_slots, new_count, true, &e);
+    uint32_t s;
+    if (id[k] != kEmptyKey && kv[k].x == id[k] && static_cast<uint32_t>(kv[k].y) != kPending)
+      s = static_cast<uint32_t>(kv[k].y);  // hit in the home entry
+    else
+      s = find_or_insert(t, id[k], new_slots, new_count, true);
     slots[i] = s;
-    if (with_plan && slot_ok(t, s))
-      plan_listing(plan, e == kSpecialEntry ? t.special_sf : &t.ht[e].sf, s, i);
+    // Batch plan (plan.cu): a row seen before in this batch is "multi". Both bitmaps
+    // are L2-resident, so this is one L2 atomic round trip.
+    if (plan && slot_ok(t, s)) {
+      const uint32_t bit = 1u << (s & 31);
+      if (atomicOr(&t.seen[s >> 5], bit) & bit) atomicOr(&t.multi[s >> 5], bit);
+    }
     if (sort_keys) {
       sort_keys[i] = s;
       sort_vals[i] = static_cast<uint32_t>(i);
@@ -227,30 +182,16 @@ __global__ void __launch_bounds__(256)
 
 void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* slots,
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
-                  uint32_t* new_count, const PlanOut* plan, cudaStream_t st) {
+                  uint32_t* new_count, bool plan, cudaStream_t st) {
   if (!n) return;
   probe_kernel<<<ceil_div(n, 256 * 2), 256, 0, st>>>(t, ids, n, slots, sort_keys, sort_vals,
-                                                     new_slots, new_count,
-                                                     plan ? *plan : PlanOut{}, plan != nullptr);
+                                                     new_slots, new_count, plan);
   HPS_LAUNCH_CHECK();
 }
 
-// Empty index: every key kEmptyKey, every slot kPending, every plan word 0 (stamp 0 is
-// never a batch's stamp).
-__global__ void ht_clear_kernel(HashEntry* __restrict__ ht, uint64_t n) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    ulonglong2* e = reinterpret_cast<ulonglong2*>(ht + i);
-    e[0] = make_ulonglong2(kEmptyKey, static_cast<unsigned long long>(kPending));
-    e[1] = make_ulonglong2(0ull, 0ull);
-  }
-}
-
+// Empty index: every key kEmptyKey, every slot kPending (both all-ones).
 void launch_ht_clear(const DevTable& t, cudaStream_t st) {
-  const uint64_t n = t.ht_mask + 1;
-  ht_clear_kernel<<<std::min<uint64_t>(ceil_div(n, 256), 148 * 64), 256, 0, st>>>(t.ht, n);
-  HPS_CUDA(cudaMemsetAsync(t.special_sf, 0, sizeof(unsigned long long), st));
-  HPS_LAUNCH_CHECK();
+  HPS_CUDA(cudaMemsetAsync(t.ht, 0xff, (t.ht_mask + 1) * sizeof(HashEntry), st));
 }
 
 // Lazy init of freshly inserted rows (embedding_ps.hpp:423-432): one warp per row,

@@ -188,44 +188,28 @@ __global__ void __launch_bounds__(kSmallBlock)
 
 // Device-sized small sort of composite keys (slot << lbits | listing): runs only when
 // *n_dev <= kSmallN and writes the sorted slots and listings separately. The keys are
-// unique (the listing is part of them), so an unstable bitonic network in shared
-// memory is exact -- log2(n)^2/2 barrier steps instead of 6-7 full radix passes.
-static __global__ void __launch_bounds__(kSmallBlock)
+// unique (the listing is part of them), so each key's final position is its rank --
+// the number of smaller keys. One warp ranks one key by scanning the (L1-resident)
+// list: O(n^2) comparisons, but spread over the whole GPU with no barrier at all,
+// where a one-CTA sort is bound by a single SM's issue rate.
+constexpr int kRankBlock = 256;
+
+static __global__ void __launch_bounds__(kRankBlock)
     small_composite_kernel(const unsigned long long* __restrict__ keys, const uint32_t* n_dev,
                            int lbits, uint32_t* __restrict__ out_slot,
                            uint32_t* __restrict__ out_listing) {
   const uint32_t n = *n_dev;
-  if (n > kSmallN || n == 0) return;  // the large path (gated on the same count) takes it
-  __shared__ unsigned long long sk[kSmallN];
-  uint32_t P = 2;
-  while (P < n) P <<= 1;
-  for (uint32_t i = threadIdx.x; i < P; i += kSmallBlock) sk[i] = i < n ? keys[i] : ~0ull;
-  __syncthreads();
-  // Comparator c of stage (k, j) compares elements i = insert-0-bit(c, j) and i + j. With
-  // j <= 32 a warp's 32 consecutive comparators stay inside one 64-element window, so
-  // those stages only need warp synchronisation.
-  for (uint32_t k = 2; k <= P; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t c = threadIdx.x; c < P / 2; c += kSmallBlock) {
-        const uint32_t i = ((c & ~(j - 1)) << 1) | (c & (j - 1));
-        const uint32_t ixj = i + j;
-        const unsigned long long a = sk[i], b = sk[ixj];
-        if ((a > b) == ((i & k) == 0)) {
-          sk[i] = b;
-          sk[ixj] = a;
-        }
-      }
-      const uint32_t next_j = j > 1 ? j >> 1 : k;
-      if (j >= 64 || next_j >= 64) __syncthreads();
-      else __syncwarp();
-    }
-  }
-  __syncthreads();
-  const unsigned long long lmask = (1ull << lbits) - 1;
-  for (uint32_t i = threadIdx.x; i < n; i += kSmallBlock) {
-    const unsigned long long k = sk[i];
-    out_slot[i] = static_cast<uint32_t>(k >> lbits);
-    out_listing[i] = static_cast<uint32_t>(k & lmask);
+  if (n > kSmallN) return;  // the large path (gated on the same count) takes it
+  const int lane = threadIdx.x & 31;
+  const uint32_t e = (blockIdx.x * kRankBlock + threadIdx.x) >> 5;
+  if (e >= n) return;
+  const unsigned long long me = keys[e];
+  uint32_t less = 0;
+  for (uint32_t i = lane; i < n; i += 32) less += __ldg(keys + i) < me;
+  less = __reduce_add_sync(0xffffffffu, less);
+  if (lane == 0) {
+    out_slot[less] = static_cast<uint32_t>(me >> lbits);
+    out_listing[less] = static_cast<uint32_t>(me & ((1ull << lbits) - 1));
   }
 }
 
@@ -428,8 +412,8 @@ inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b,
 inline void sort_composite_small(const unsigned long long* keys, const uint32_t* n_dev, int lbits,
                                  uint32_t* out_slot, uint32_t* out_listing,
                                  cudaStream_t stream) {
-  small_composite_kernel<<<1, kSmallBlock, 0, stream>>>(keys, n_dev, lbits, out_slot,
-                                                        out_listing);
+  small_composite_kernel<<<kSmallN * 32 / kRankBlock, kRankBlock, 0, stream>>>(
+      keys, n_dev, lbits, out_slot, out_listing);
   HPS_LAUNCH_CHECK();
 }
 

@@ -219,7 +219,8 @@ Table* table_create(const hps_table_cfg& cfg) {
     HPS_CUDA(cudaMalloc(&d.ht, H * sizeof(HashEntry)));
     HPS_CUDA(cudaMalloc(&d.rows, C * d.stride * sizeof(float)));
     d.vt = VtView{d.rows, d.stride, 2 * d.D};
-    HPS_CUDA(cudaMalloc(&d.special_sf, sizeof(unsigned long long)));
+    HPS_CUDA(cudaMalloc(&d.seen, (C / 32 + 1) * sizeof(uint32_t)));
+    HPS_CUDA(cudaMalloc(&d.multi, (C / 32 + 1) * sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.slot_id, C * sizeof(uint64_t)));
     HPS_CUDA(cudaMalloc(&d.special, sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.hwm, sizeof(uint32_t)));
@@ -244,6 +245,8 @@ Table* table_create(const hps_table_cfg& cfg) {
 void table_clear(Table* t, cudaStream_t st) {
   DevTable& d = t->d;
   launch_ht_clear(d, st);
+  HPS_CUDA(cudaMemsetAsync(d.seen, 0, (d.capacity / 32 + 1) * sizeof(uint32_t), st));
+  HPS_CUDA(cudaMemsetAsync(d.multi, 0, (d.capacity / 32 + 1) * sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.special, 0xff, sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.hwm, 0, sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.ctr + kCtrOverflow, 0, sizeof(unsigned long long), st));
@@ -291,7 +294,7 @@ void table_destroy(Table* t) {
     t->stage.free_all();
     t->prof.destroy();
     DevTable& d = t->d;
-    void* ptrs[] = {d.ht,  d.rows, d.special_sf, d.slot_id, d.special,
+    void* ptrs[] = {d.ht,  d.rows, d.seen, d.multi, d.slot_id, d.special,
                     d.hwm, d.ctr,  t->d_salts};
     for (void* p : ptrs)
       if (p) cudaFree(p);
@@ -485,17 +488,10 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   // Sample keys that reorder the batch: every listing takes the sorted (multi) path.
   const bool permute = d_sk && B > 1;
   b.all_multi = permute;
-  // Plan (see probe_kernel): rows listed once apply directly; the multi listings are
-  // ordered by the one-CTA composite sort, or -- past kSmallN of them -- the whole
-  // batch is slot-sorted instead. Both sorts are launched; the device count picks one.
-  const int lbits = std::max(1, bits_for(N ? N - 1 : 0));
-  PlanOut plan{b.kind, b.mkeys, &b.small[0], ++t->plan_stamp, lbits};
-  if (t->plan_stamp == 0) plan.stamp = t->plan_stamp = 1;  // 0 marks "never listed"
-  if (!permute && N) HPS_CUDA(cudaMemsetAsync(b.kind, 1, N, st));
   {
     ProfScope p(t, "probe", st);
-    launch_probe(t->d, d_ids, N, b.slot, nullptr, nullptr, b.new_slots, &b.small[2],
-                 permute ? nullptr : &plan, st);
+    launch_probe(t->d, d_ids, N, b.slot, nullptr, nullptr, b.new_slots, &b.small[2], !permute,
+                 st);
   }
   launch_lazy_init(t->d, b.new_slots, &b.small[2], N, t->sm_count, st);
   if (permute) {
@@ -510,6 +506,14 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     launch_permuted_listing(perm, b.sstart, b.offsets, b.slot, B, F, b.keys_a, b.vals_a, st);
     sort_slots(b, nullptr, false, nullptr, st);
   } else {
+    // Plan (plan.cu): rows listed once apply directly; the multi listings are ordered
+    // by the small composite sort, or -- past kSmallN of them -- the whole batch is
+    // slot-sorted instead. Both sorts are launched; the device count picks one.
+    const int lbits = std::max(1, bits_for(N ? N - 1 : 0));
+    {
+      ProfScope p(t, "plan", st);
+      launch_classify(t->d, b.slot, N, lbits, b.kind, b.mkeys, &b.small[0], t->sm_count, st);
+    }
     {
       ProfScope p(t, "sort_small", st);
       radix::sort_composite_small(b.mkeys, &b.small[0], lbits, b.small_slot, b.small_listing,
@@ -625,7 +629,7 @@ void table_lookup(Table* t, const uint64_t* ids, uint64_t n, float* out_values,
   float* d_out = static_cast<float*>(stg.out(out_values, n * t->cfg.embedding_dim * sizeof(float)));
   uint64_t* d_ver = static_cast<uint64_t*>(stg.out(out_versions, n * sizeof(uint64_t)));
   HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
-  launch_probe(t->d, d_ids, n, b.slot, nullptr, nullptr, b.new_slots, &b.small[2], nullptr, st);
+  launch_probe(t->d, d_ids, n, b.slot, nullptr, nullptr, b.new_slots, &b.small[2], false, st);
   launch_lazy_init(t->d, b.new_slots, &b.small[2], n, t->sm_count, st);
   launch_gather(t->d, b.slot, n, d_out, d_ver, st);
   b.registered = false;
@@ -683,7 +687,7 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
   b.N = n;
   b.B = static_cast<uint32_t>(n);
   b.F = 1;
-  launch_probe(t->d, d_ids, n, b.slot, b.keys_a, b.vals_a, b.new_slots, &b.small[2], nullptr, st);
+  launch_probe(t->d, d_ids, n, b.slot, b.keys_a, b.vals_a, b.new_slots, &b.small[2], false, st);
   launch_lazy_init(t->d, b.new_slots, &b.small[2], n, t->sm_count, st);
   sort_slots(b, nullptr, false, nullptr, st);
   b.all_multi = true;

@@ -36,28 +36,11 @@ enum CounterIdx : int {
   kCtrCount = 32
 };
 
-// One 32-byte index entry = one DRAM sector per probe. `sf` is the row's batch-plan
-// word (stamp of the batch that last listed the row << 32 | multi flag << 31 | first
-// listing + 1), updated by the probe in the sector it just read (see probe_kernel).
-struct __align__(32) HashEntry {
+// One 16-byte index entry: a probe touches a single 32-byte sector.
+struct __align__(16) HashEntry {
   unsigned long long key;  // kEmptyKey when free
   uint32_t slot;           // kPending while the inserting thread publishes it
-  uint32_t pad0;
-  unsigned long long sf;
-  unsigned long long pad1;
-};
-constexpr unsigned long long kMultiFlag = 1ull << 31;
-constexpr uint64_t kSpecialEntry = ~0ull;  // "entry index" of id == kEmptyKey
-
-// Batch plan written by the probe of a register: kind[i] (pre-set to 1) becomes 2 for
-// every listing of a row listed more than once; those listings are appended as
-// composite keys (slot << lbits | listing) while fewer than radix::kSmallN are known.
-struct PlanOut {
-  uint8_t* kind;
-  unsigned long long* mkeys;
-  uint32_t* n_multi;
-  uint32_t stamp;
-  int lbits;
+  uint32_t pad;
 };
 
 // The {version, latest bump tag} word of a row lives in the row's own 16-byte header
@@ -82,7 +65,10 @@ struct DevTable {
   uint32_t D;
   uint32_t stride;  // floats per row: 2D + 4 ([w D | acc D | header 16 B])
   VtView vt;        // {version, latest bump tag} in each row's header
-  unsigned long long* special_sf;  // plan word of id == kEmptyKey (it has no hash entry)
+  // Batch-plan bitmaps, one bit per slot (2 x capacity/8 bytes: L2-resident): `seen`
+  // = listed by the batch being planned, `multi` = listed more than once (plan.cu).
+  uint32_t* seen;
+  uint32_t* multi;
   uint64_t* slot_id;
   uint32_t capacity;
   uint32_t* hwm;
@@ -179,7 +165,6 @@ struct Table {
   uint64_t* d_salts = nullptr;
   std::vector<uint64_t> salts;
   uint32_t epoch = 0;
-  uint32_t plan_stamp = 0;  // batch stamp of the last register (HashEntry::sf)
   uint32_t sm_count = 148;
   std::mutex mu;  // one call at a time per table (PsShard's per-shard lock)
   Batch scratch;  // workspace for the stateless entry points
@@ -195,10 +180,14 @@ void launch_route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cu
 void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st);
 // slots[i] = find_or_insert(ids[i]); when sort_keys/sort_vals are given also writes the
 // (slot, i) pairs the apply-order sort consumes.
-// plan != null: also build the batch plan (PlanOut) while probing.
+// plan: also mark the rows in the batch-plan bitmaps (plan.cu).
 void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* slots,
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
-                  uint32_t* new_count, const PlanOut* plan, cudaStream_t st);
+                  uint32_t* new_count, bool plan, cudaStream_t st);
+// plan.cu
+void launch_classify(const DevTable& t, const uint32_t* slots, uint64_t n, int lbits,
+                     uint8_t* kind, unsigned long long* mkeys, uint32_t* n_multi, int sms,
+                     cudaStream_t st);
 void launch_ht_clear(const DevTable& t, cudaStream_t st);
 void launch_lazy_init(const DevTable& t, const uint32_t* new_slots, const uint32_t* new_count,
                       uint64_t max_new, int sms, cudaStream_t st);
