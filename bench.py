@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--soak-seconds", type=float, default=2.0)
+    p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
     return p.parse_args()
 
 
@@ -249,14 +250,43 @@ def main():
     pooled = torch.empty((B, F, D), dtype=torch.float32, device=dev)
     ew = hps.EmbeddingWorker(table, agg)
 
-    def step(i):
+    def eager_step(i, s=None):
+        s = s or stream
         ids, offs, n = batches[i % M]
-        ew.register_batch(ids, offs, B, F, stream=stream)
-        ew.serve_pull(out_pooled=pooled, stream=stream)
-        ew.apply_backward(grads[i % M], cfg.lr, step_tag=i + 1, flags=hps.ASYNC, stream=stream)
+        ew.register_batch(ids, offs, B, F, stream=s)
+        ew.serve_pull(out_pooled=pooled, stream=s)
+        # step tags come from the table's device step counter, so graph replays
+        # advance them exactly like eager calls would
+        ew.apply_backward(grads[i % M], cfg.lr, flags=hps.ASYNC | hps.DEVICE_STEP, stream=s)
 
     it = 0
     for _ in range(args.warmup):
+        eager_step(it)
+        it += 1
+    torch.cuda.synchronize()
+    table.sync()
+
+    # One CUDA graph per input batch: the whole step (register + pull + push, ~16
+    # kernels) replays without host launch overhead.
+    graphs, graph_launches = [], []
+    if not args.no_graph:
+        cap = torch.cuda.Stream()
+        for m in range(M):
+            g = torch.cuda.CUDAGraph()
+            l0 = hps.launch_count()
+            with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
+                eager_step(m, torch.cuda.current_stream())
+            graph_launches.append(hps.launch_count() - l0)
+            graphs.append(g)
+        torch.cuda.synchronize()
+
+    def step(i):
+        if graphs:
+            graphs[i % M].replay()
+        else:
+            eager_step(i)
+
+    for _ in range(2):
         step(it)
         it += 1
     torch.cuda.synchronize()
@@ -281,6 +311,8 @@ def main():
     e1.record(stream)
     barrier()
     launches = hps.launch_count() - l0
+    if graphs:  # replays do not pass through the host launch counter
+        launches = sum(graph_launches[i % M] for i in range(it - args.steps, it))
     ms = e0.elapsed_time(e1) / args.steps
     # soak: keep the same step running so the clock sampler sees >= soak-seconds under load
     t_soak = time.perf_counter()
@@ -300,7 +332,7 @@ def main():
     # -- per-kernel timing pass (same steps, events around each region)
     table.profile(True)
     for _ in range(args.steps):
-        step(it)
+        eager_step(it)  # events need the host-side launch sequence (no graph)
         it += 1
     torch.cuda.synchronize()
     regions = {}
@@ -344,7 +376,7 @@ def main():
         for _ in range(2):
             ew.register_batch(h_ids, h_offs, B, F, stream=stream)
             ew.serve_pull(out_pooled=h_pooled, stream=stream)
-            ew.apply_backward(h_grads, cfg.lr, step_tag=it + 1, stream=stream)
+            ew.apply_backward(h_grads, cfg.lr, flags=hps.DEVICE_STEP, stream=stream)
             it += 1
         barrier()
         q0 = torch.cuda.Event(enable_timing=True)
@@ -354,7 +386,7 @@ def main():
         for _ in range(args.e2e_steps):
             ew.register_batch(h_ids, h_offs, B, F, stream=stream)
             ew.serve_pull(out_pooled=h_pooled, stream=stream)
-            ew.apply_backward(h_grads, cfg.lr, step_tag=it + 1, stream=stream)
+            ew.apply_backward(h_grads, cfg.lr, flags=hps.DEVICE_STEP, stream=stream)
             it += 1
         q1.record(stream)
         torch.cuda.synchronize()

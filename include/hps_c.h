@@ -60,6 +60,10 @@ typedef enum hps_aggregation { HPS_MEAN = 0, HPS_SUM = 1 } hps_aggregation; /* M
 
 /* flags */
 #define HPS_ASYNC 1u   /* do not synchronise to report data-dependent errors */
+/* push: take the step tag from the table's device step counter (+1) and advance it
+ * after the update, so a push captured once in a CUDA graph tags every replay with a
+ * new step (the step_tag argument is ignored). hps_table_device_step reads it. */
+#define HPS_DEVICE_STEP 2u
 
 typedef void* hps_stream; /* cudaStream_t */
 
@@ -106,6 +110,7 @@ hps_status hps_table_destroy(hps_table* t);
 hps_status hps_table_counters(hps_table* t, hps_counters* out);
 hps_status hps_table_sync(hps_table* t); /* drain async work, report deferred errors */
 uint32_t hps_table_epoch(const hps_table* t);            /* PsShard::epoch         :91 */
+hps_status hps_table_device_step(hps_table* t, uint32_t* out_step); /* HPS_DEVICE_STEP counter */
 uint32_t hps_table_advance_epoch(hps_table* t);          /* PsShard::advance_epoch :204 */
 hps_status hps_table_reset(hps_table* t);                /* PsShard::reset_for_recovery :193 */
 

@@ -106,6 +106,18 @@ hps_status hps_table_sync(hps_table* t) {
 
 uint32_t hps_table_epoch(const hps_table* t) { return t ? t->impl->epoch : 0u; }
 
+hps_status hps_table_device_step(hps_table* t, uint32_t* out_step) {
+  return guarded([&] {
+    REQUIRE(t && out_step, "hps_table_device_step: null argument");
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::DeviceGuard dg(t->impl->device);
+    HPS_CUDA(cudaDeviceSynchronize());
+    unsigned long long v = 0;
+    HPS_CUDA(cudaMemcpy(&v, t->impl->d.ctr + hps::kCtrStep, sizeof(v), cudaMemcpyDeviceToHost));
+    *out_step = static_cast<uint32_t>(v);
+  });
+}
+
 uint32_t hps_table_advance_epoch(hps_table* t) {
   if (!t) return 0u;
   std::lock_guard<std::mutex> g(t->impl->mu);

@@ -460,4 +460,14 @@ void launch_add_counter_from(unsigned long long* ctr, int idx, const uint32_t* s
   HPS_LAUNCH_CHECK();
 }
 
+__global__ void add_counter_const_kernel(unsigned long long* ctr, int idx, unsigned long long v) {
+  atomicAdd(&ctr[idx], v);
+}
+
+void launch_add_counter_const(unsigned long long* ctr, int idx, unsigned long long v,
+                              cudaStream_t st) {
+  add_counter_const_kernel<<<1, 1, 0, st>>>(ctr, idx, v);
+  HPS_LAUNCH_CHECK();
+}
+
 }  // namespace hps

@@ -577,6 +577,8 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   a.grads = d_g;
   a.lr = lr;
   a.step_tag = step_tag;
+  if (flags & HPS_DEVICE_STEP)
+    a.step_dev = reinterpret_cast<const uint32_t*>(t->d.ctr + kCtrStep);
   if (d_rv) {
     a.rv64 = d_rv;
     a.tracked = 1;
@@ -598,6 +600,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     ProfScope p(t, "update_multi", st);
     launch_update(t->d, a, false, t->sm_count, st);
   }
+  if (flags & HPS_DEVICE_STEP) launch_add_counter_const(t->d.ctr, kCtrStep, 1, st);
   forget_outstanding(b);
   b.pulled = false;
   b.rv_valid = false;

@@ -32,6 +32,7 @@ enum CounterIdx : int {
   kCtrNeedExact = 5,   // per-call: bound check inconclusive -> exact dry run
   kCtrMaxDelay = 6,
   kCtrDelayHist = 7,   // 17 words: delays 0..15, >=16
+  kCtrStep = 30,       // HPS_DEVICE_STEP counter (low 32 bits used)
   kCtrScratch = 31,    // per-call scratch (pair counts)
   kCtrCount = 32
 };
@@ -230,6 +231,7 @@ struct UpdateArgs {
   uint32_t* out_delays;  // direct mode, per entry
   float lr;
   uint32_t step_tag;
+  const uint32_t* step_dev;  // HPS_DEVICE_STEP: tag = *step_dev + 1 (table step counter)
   int tracked;
   int fresh;  // tracked, and no mutation since the pull: read version = current version
   int dry_run;  // compute + validate contributions only
@@ -248,6 +250,8 @@ void launch_permuted_listing(const uint32_t* perm, const uint32_t* starts,
                              uint32_t F, uint32_t* keys_out, uint32_t* vals_out, cudaStream_t st);
 void launch_add_counter_from(unsigned long long* ctr, int idx, const uint32_t* src,
                              cudaStream_t st);
+void launch_add_counter_const(unsigned long long* ctr, int idx, unsigned long long v,
+                              cudaStream_t st);
 void launch_iota(uint32_t* out, uint64_t n, cudaStream_t st);
 
 }  // namespace hps

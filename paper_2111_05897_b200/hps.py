@@ -97,6 +97,7 @@ _ERRORS = {c.code: c for c in (PreconditionError, ConfigError, ProtocolError, Tr
 ADAGRAD, SGD = 0, 1
 MEAN, SUM = 0, 1
 ASYNC = 1
+DEVICE_STEP = 2
 
 # ---- library loading -----------------------------------------------------------------
 
@@ -141,6 +142,7 @@ def lib():
         "hps_table_counters": (st, [vp, C.POINTER(Counters)]),
         "hps_table_sync": (st, [vp]),
         "hps_table_epoch": (u32, [vp]),
+        "hps_table_device_step": (st, [vp, C.POINTER(u32)]),
         "hps_table_advance_epoch": (u32, [vp]),
         "hps_table_reset": (st, [vp]),
         "hps_lookup": (st, [vp, vp, sz, vp, vp, vp]),
@@ -343,6 +345,12 @@ class ShardSet:
 
     def epoch(self) -> int:
         return int(lib().hps_table_epoch(self.h))
+
+    def device_step(self) -> int:
+        """Steps pushed with DEVICE_STEP so far (the table's device step counter)."""
+        v = C.c_uint32(0)
+        check(lib().hps_table_device_step(self.h, C.byref(v)), "device_step")
+        return v.value
 
     def advance_epoch(self) -> int:
         return int(lib().hps_table_advance_epoch(self.h))
