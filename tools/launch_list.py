@@ -18,7 +18,8 @@ for r in rows[1:]:
         continue
     v = float(r[vi].replace(",", ""))
     u = r[unit] if unit is not None else "nsecond"
-    v = v / 1000 if u == "nsecond" else v * (1000 if u == "msecond" else 1)
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+    v = v * scale.get(u, 1.0)
     data.append((r[ki].split("(")[0].replace("void ", "")[:48], v))
 starts = [i for i, (k, _) in enumerate(data) if marker in k]
 if len(starts) >= 2:
