@@ -57,6 +57,19 @@ struct VtView {
   }
 };
 
+// Row pitch: [w D | acc D | header 16 B] padded to whole 128-byte lines (or to a power of
+// two below one line), so a row never straddles more lines than it fills: a D=64 row is
+// 5 lines (640 B) and its weight vector exactly lines 0-1. The unpadded 528-byte pitch
+// made the pool's 256-byte weight read touch 3 lines (160 MB of DRAM reads for 109 MB
+// algorithmic per C2 step, profiles/r1_ncu_full_c2.txt).
+inline uint32_t row_stride_floats(uint32_t D) {
+  uint32_t bytes = 8 * D + 16;
+  if (bytes >= 128) return ((bytes + 127) / 128) * 32;
+  uint32_t p = 16;
+  while (p < bytes) p <<= 1;
+  return p / 4;
+}
+
 struct DevTable {
   HashEntry* ht;
   uint64_t ht_mask;
@@ -64,7 +77,7 @@ struct DevTable {
   uint32_t* special;  // slot of id == kEmptyKey (kSpecialAbsent / kSpecialInserting / slot)
   float* rows;
   uint32_t D;
-  uint32_t stride;  // floats per row: 2D + 4 ([w D | acc D | header 16 B])
+  uint32_t stride;  // floats per row: row_stride_floats(D) ([w D | acc D | header 16 B | pad])
   VtView vt;        // {version, latest bump tag} in each row's header
   // Batch-plan bitmaps, one bit per slot (2 x capacity/8 bytes: L2-resident): `seen`
   // = listed by the batch being planned, `multi` = listed more than once (plan.cu).
