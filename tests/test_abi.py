@@ -71,3 +71,27 @@ def test_product_does_not_link_the_oracle():
     assert "oracle" not in out and "hps_ref" not in out and "hps_oracle" not in out
     syms = subprocess.run(["nm", "-D", LIB], capture_output=True, text=True).stdout
     assert "orc_" not in syms and "ref_" not in syms
+
+
+def _build_compat_smoke(out):
+    subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "compat_smoke.cpp"),
+                    "-L", os.path.dirname(LIB), "-lhps", f"-Wl,-rpath,{os.path.dirname(LIB)}",
+                    "-o", out], check=True)
+
+
+def test_compat_header_compiles_and_links(lib, tmp_path):
+    """include/hps/compat.hpp (the reference's PsShard/ShardSet/EmbeddingWorker shapes over
+    the C ABI) compiles as C++17 and links against libhps.so."""
+    out = str(tmp_path / "compat_smoke")
+    _build_compat_smoke(out)
+    assert os.path.exists(out)
+
+
+@pytest.mark.gpu
+def test_compat_header_runs_reference_cases(lib, tmp_path):
+    out = str(tmp_path / "compat_smoke")
+    _build_compat_smoke(out)
+    r = subprocess.run([out], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "compat_smoke OK" in r.stdout
