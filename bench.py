@@ -193,6 +193,178 @@ def workload_config(cfg, args, ref_sample=None):
     return d
 
 
+# ---------------------------------------------------------------- our arm, N > 1 (sharded)
+
+
+def run_sharded(args, world, rank, local, dev):
+    """C4: the table hash-sharded over the N GPUs (owner = route_shard(id, S) % N), one
+    embedding worker per GPU with its own batch, NCCL all-to-all of ids, rows and
+    (position, contribution) pairs per step (paper_2111_05897_b200/sharded.py)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2111_05897_b200 import hps
+    from paper_2111_05897_b200 import workloads as W
+    from paper_2111_05897_b200.sharded import ShardedEmbeddingWorker
+
+    cfg = W.sharded_config(world)
+    D, F, B = cfg.dim, cfg.features, cfg.batch
+    S = cfg.shards
+    rows = cfg.table_capacity()
+    cap = int(rows / world * 1.01) + (1 << 20)
+    table = hps.ShardSet(S, D, cap, hps.ADAGRAD, salts=cfg.salts(), device=local)
+    stream = torch.cuda.current_stream()
+    # pre-warm: each rank creates the rows it owns (M = 0 lazy inits while timing)
+    t0 = time.perf_counter()
+    chunk = 1 << 24
+    for a in range(0, rows, chunk):
+        n = min(chunk, rows - a)
+        ids = torch.arange(a, a + n, dtype=torch.int64, device=dev)
+        sh = hps.route(ids, S, stream=stream).to(torch.int64)
+        owned = ids[(sh % world) == rank]
+        table.lookup(owned, stream=stream)
+    torch.cuda.synchronize()
+    prewarm_s = time.perf_counter() - t0
+
+    M = args.batches
+    host_batches = [W.make_batch(cfg, 1000 * rank + m) for m in range(M)]
+    batches = [(torch.from_numpy(hb.ids.view(np.int64)).to(dev),
+                torch.from_numpy(hb.offsets.view(np.int32)).to(dev), hb.N) for hb in host_batches]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    grads = [((torch.rand((B, F, D), generator=gen, device=dev) * 2 - 1) * cfg.grad_scale)
+             for _ in range(M)]
+    pooled = torch.empty((B, F, D), dtype=torch.float32, device=dev)
+    ew = ShardedEmbeddingWorker(table, hps.MEAN)
+    tag = [0]
+
+    def step(i):
+        ids, offs, _ = batches[i % M]
+        ew.register_batch(ids, offs, B, F)
+        ew.serve_pull(out_pooled=pooled)
+        tag[0] += 1
+        ew.apply_backward(grads[i % M], cfg.lr, tag[0])
+
+    it = 0
+    for _ in range(args.warmup):
+        step(it)
+        it += 1
+    torch.cuda.synchronize()
+    table.sync()
+    clocks = ClockSampler(local)
+    clocks.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = hps.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    x_ids = x_rows = x_pairs = 0
+    for _ in range(args.steps):
+        step(it)
+        it += 1
+        x_ids += sum(c for d, c in enumerate(ew.send_counts) if d != rank)
+        x_pairs += sum(c for d, c in enumerate(ew.ops.last_pair_counts) if d != rank) \
+            if hasattr(ew.ops, "last_pair_counts") else 0
+    e1.record(stream)
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches = hps.launch_count() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < args.soak_seconds:
+        step(it)
+        it += 1
+        torch.cuda.synchronize()
+    clk = clocks.stop()
+    table.sync()
+    t = torch.tensor([ms], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = world * B * 1000.0 / ms
+
+    # off-rank bytes each GPU sends per step (ids out + rows back + pairs out) ~ NVLink
+    N_avg = float(np.mean([b[2] for b in batches]))
+    U_avg = float(x_ids) / args.steps  # distinct ids this rank sent off-rank per step
+    P_avg = float(x_pairs) / args.steps
+    nvl_bytes = 8 * U_avg + 4 * D * U_avg + (4 + 4 * D) * P_avg
+    O_ = D
+    uniq = float(N_avg)  # one-hot over 125M rows per GPU: ~all listings distinct
+    bytes_step = (8 * N_avg + 8 * N_avg + 12 * uniq + 4 * D * uniq + 4 * B * F * D +
+                  4 * B * F * D + 8 * (D + O_) * uniq)
+    peak, peak_kind = peaks()
+
+    # e2e: host (pinned) inputs copied in and the pooled output copied out every step
+    hb = host_batches[0]
+    h_ids = torch.from_numpy(hb.ids.view(np.int64)).pin_memory()
+    h_offs = torch.from_numpy(hb.offsets.view(np.int32)).pin_memory()
+    h_grads = grads[0].cpu().pin_memory()
+    h_pooled = torch.empty((B, F, D), dtype=torch.float32).pin_memory()
+    d_ids = torch.empty_like(batches[0][0])
+    d_offs = torch.empty_like(batches[0][1])
+    d_grads = torch.empty_like(grads[0])
+
+    def e2e_step():
+        d_ids.copy_(h_ids, non_blocking=True)
+        d_offs.copy_(h_offs, non_blocking=True)
+        ew.register_batch(d_ids, d_offs, B, F)
+        ew.serve_pull(out_pooled=pooled)
+        h_pooled.copy_(pooled, non_blocking=True)
+        d_grads.copy_(h_grads, non_blocking=True)
+        tag[0] += 1
+        ew.apply_backward(d_grads, cfg.lr, tag[0])
+
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e_step()
+        dist.barrier()
+        torch.cuda.synchronize()
+        q0 = torch.cuda.Event(enable_timing=True)
+        q1 = torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        q1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = q0.elapsed_time(q1) / args.e2e_steps
+        t = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+        e2e = {"value": world * B * 1000.0 / e_ms, "unit": "samples/s",
+               "h2d_bytes_per_step": int(8 * hb.N + 4 * (B * F + 1) + 4 * B * F * D),
+               "d2h_bytes_per_step": int(4 * B * F * D),
+               "path": "ShardedEmbeddingWorker with pinned host inputs/outputs per rank"}
+
+    if rank == 0:
+        line = {
+            "metric": "embedding lookup+update samples/sec", "value": value,
+            "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 (fp64 pooling/fan-out)", "data": "synthetic",
+            "config": {"workload": f"c4: per-GPU batch {B}, {F} one-hot features, "
+                                   f"{rows // 1_000_000}M-row table dim {D} hash-sharded over "
+                                   f"{world} GPUs ({S} logical shards), adagrad, mean pooling, "
+                                   f"staleness 0, NCCL all-to-all exchange",
+                       "global_batch": B * world, "rows": rows, "dim": D, "features": F,
+                       "logical_shards": S, "parallelism": f"sharded{world}",
+                       "l2": "per-step footprint > L2 (126 MB); no flush"},
+            "hbm": {"algorithmic_bytes_per_step_per_gpu": bytes_step,
+                    "achieved_gbs_per_gpu": bytes_step / (ms * 1e-3) / 1e9,
+                    "frac_of_peak": bytes_step / (ms * 1e-3) / 1e9 / peak},
+            "roofline": {"bound": "hbm", "kernel": "whole step (per GPU)",
+                         "achieved": bytes_step / (ms * 1e-3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": bytes_step / (ms * 1e-3) / 1e9 / peak,
+                         "traffic": None, "peak_source": peak_kind},
+            "nvlink": {"offrank_bytes_per_step_per_gpu": nvl_bytes,
+                       "achieved_gbs_per_direction": nvl_bytes / (ms * 1e-3) / 1e9,
+                       "frac_of_900": nvl_bytes / (ms * 1e-3) / 1e9 / 900.0},
+            "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk, "prewarm_s": prewarm_s,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------- our arm
 
 
@@ -214,6 +386,8 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        run_sharded(args, world, rank, local, dev)
+        return
     cfg = W.CONFIGS[args.config]
     D, F, B = cfg.dim, cfg.features, cfg.batch
     opt = hps.ADAGRAD if cfg.optimizer == "adagrad" else hps.SGD

@@ -177,6 +177,48 @@ hps_status hps_push_batch(hps_table* t, const uint64_t* ids, size_t n_ids, const
                           const uint64_t* read_versions, const uint64_t* sample_keys, float lr,
                           uint32_t step_tag, uint32_t epoch, int* accepted, hps_stream stream);
 
+/* ---- multi-GPU exchange (hash-sharded tables) -------------------------
+ * A row is owned by rank route_shard(id, S) % world (ShardSet::shard_of,
+ * embedding_ps.hpp:521-523, with the S logical shards spread round-robin over ranks); each
+ * rank's table is created with all S salts and holds the rows it owns. One step of the
+ * reference's E embedding workers in front of a ShardSet (EmbeddingWorker::fetch_rows
+ * :677-704 / push_to_shards :726-775, PsShardService :185-290) becomes, per rank:
+ *   hps_exchange_route    distinct ids of the batch grouped by owner rank
+ *   [all-to-all ids]      -> owner: hps_lookup(recv ids) = rows + versions
+ *   [all-to-all rows]     -> hps_exchange_pool: serve_pull's pooling over the rows
+ *   hps_exchange_pairs    one contribution per (sample, distinct id), grouped by owner
+ *   [all-to-all pairs]    -> owner: hps_table_apply_pairs, applied in (source rank, sample)
+ *                            order = ascending SampleId (rank << 56 | counter)
+ * All buffers are DEVICE pointers; counts are host arrays of `world` entries. The
+ * collectives are the caller's (NCCL); paper_2111_05897_b200/sharded.py drives them. */
+typedef struct hps_exchange hps_exchange;
+hps_status hps_exchange_create(uint32_t world_size, uint32_t shard_count, int32_t aggregation,
+                               int32_t device, hps_exchange** out);
+hps_status hps_exchange_destroy(hps_exchange* x);
+/* out_send_ids[n_ids] (first sum(out_counts) used, owner-major); out_counts[world]. */
+hps_status hps_exchange_route(hps_exchange* x, const uint64_t* ids, size_t n_ids,
+                              const uint32_t* offsets, uint32_t B, uint32_t F,
+                              uint64_t* out_send_ids, uint64_t* out_counts, hps_stream stream);
+/* rows[U*dim] = the owners' rows for send_ids, same order; out_pooled[B*F*dim]. */
+hps_status hps_exchange_pool(hps_exchange* x, const float* rows, uint32_t dim, float* out_pooled,
+                             hps_stream stream);
+/* grads[B*F*dim]; out_pair_pos[P] = index of the pair's id inside its owner's segment of
+ * send_ids; out_contrib[P*dim]; out_pair_counts[world]. Buffers sized for n_ids pairs. */
+hps_status hps_exchange_pairs(hps_exchange* x, const float* grads, uint32_t dim,
+                              uint32_t* out_pair_pos, float* out_contrib,
+                              uint64_t* out_pair_counts, hps_stream stream);
+/* Owner: recv_ids / recv_versions = the ids received by the forward exchange (source-rank
+ * major, id_counts[world]) and the versions hps_lookup returned for them; the pairs
+ * (pair_pos, contrib) received from each source (pair_counts[world]) apply through
+ * PsShard::apply_gradients (:139-162): epoch fence, all-finite validation, ordered update,
+ * version bump per step tag. recv_versions == NULL applies untracked. */
+hps_status hps_table_apply_pairs(hps_table* t, const uint64_t* recv_ids,
+                                 const uint64_t* recv_versions, const uint64_t* id_counts,
+                                 const uint32_t* pair_pos, const float* contrib,
+                                 const uint64_t* pair_counts, uint32_t world, float lr,
+                                 uint32_t step_tag, uint32_t epoch, int* accepted,
+                                 uint32_t flags, hps_stream stream);
+
 /* ---- instrumentation (no reference counterpart) ---------------------------------------- */
 /* Kernels this library has launched in the process (proves which code ran). */
 uint64_t hps_launch_count(void);

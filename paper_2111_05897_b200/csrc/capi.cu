@@ -19,6 +19,10 @@ struct hps_table {
 struct hps_batch {
   hps::Batch impl;
 };
+struct hps_exchange {
+  hps::XBatch impl;
+  std::mutex mu;
+};
 
 namespace {
 
@@ -276,6 +280,85 @@ hps_status hps_push_batch(hps_table* t, const uint64_t* ids, size_t n_ids, const
     hps::batch_register(b, ids, n_ids, offsets, B, F, sample_keys, S(stream));
     hps::batch_push(b, aggregation, grads, lr, step_tag, epoch, read_versions ? 0 : 1,
                     read_versions, accepted, 0, S(stream));
+  });
+}
+
+hps_status hps_exchange_create(uint32_t world_size, uint32_t shard_count, int32_t aggregation,
+                               int32_t device, hps_exchange** out) {
+  return guarded([&] {
+    REQUIRE(out, "hps_exchange_create: null out");
+    REQUIRE(world_size >= 1 && world_size <= hps::kMaxWorld,
+            "hps_exchange_create: world_size must be in [1, 32]");
+    if (shard_count == 0) throw hps::Error(HPS_E_CONFIG, "hps_exchange_create: shard_count must be positive");
+    REQUIRE(aggregation == HPS_MEAN || aggregation == HPS_SUM, "hps_exchange_create: bad aggregation");
+    int dev = device;
+    if (dev < 0) HPS_CUDA(cudaGetDevice(&dev));
+    auto* x = new hps_exchange();
+    x->impl.device = dev;
+    x->impl.G = world_size;
+    x->impl.S = shard_count;
+    x->impl.agg = aggregation;
+    try {
+      hps::xbatch_init(x->impl);
+    } catch (...) {
+      delete x;
+      throw;
+    }
+    *out = x;
+  });
+}
+
+hps_status hps_exchange_destroy(hps_exchange* x) {
+  return guarded([&] { delete x; });
+}
+
+hps_status hps_exchange_route(hps_exchange* x, const uint64_t* ids, size_t n_ids,
+                              const uint32_t* offsets, uint32_t B, uint32_t F,
+                              uint64_t* out_send_ids, uint64_t* out_counts, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(x && offsets && out_counts && (ids || n_ids == 0) && (out_send_ids || n_ids == 0),
+            "hps_exchange_route: null argument");
+    std::lock_guard<std::mutex> g(x->mu);
+    hps::DeviceGuard dg(x->impl.device);
+    hps::xbatch_route(x->impl, ids, n_ids, offsets, B, F, out_send_ids, out_counts, S(stream));
+  });
+}
+
+hps_status hps_exchange_pool(hps_exchange* x, const float* rows, uint32_t dim, float* out_pooled,
+                             hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(x && out_pooled && (rows || x->impl.U == 0), "hps_exchange_pool: null argument");
+    std::lock_guard<std::mutex> g(x->mu);
+    hps::DeviceGuard dg(x->impl.device);
+    hps::xbatch_pool(x->impl, rows, dim, out_pooled, S(stream));
+  });
+}
+
+hps_status hps_exchange_pairs(hps_exchange* x, const float* grads, uint32_t dim,
+                              uint32_t* out_pair_pos, float* out_contrib,
+                              uint64_t* out_pair_counts, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(x && out_pair_counts, "hps_exchange_pairs: null argument");
+    REQUIRE(x->impl.N == 0 || (grads && out_pair_pos && out_contrib),
+            "hps_exchange_pairs: null buffer");
+    std::lock_guard<std::mutex> g(x->mu);
+    hps::DeviceGuard dg(x->impl.device);
+    hps::xbatch_pairs(x->impl, grads, dim, out_pair_pos, out_contrib, out_pair_counts, S(stream));
+  });
+}
+
+hps_status hps_table_apply_pairs(hps_table* t, const uint64_t* recv_ids,
+                                 const uint64_t* recv_versions, const uint64_t* id_counts,
+                                 const uint32_t* pair_pos, const float* contrib,
+                                 const uint64_t* pair_counts, uint32_t world, float lr,
+                                 uint32_t step_tag, uint32_t epoch, int* accepted,
+                                 uint32_t flags, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(t && id_counts && pair_counts, "hps_table_apply_pairs: null argument");
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::DeviceGuard dg(t->impl->device);
+    hps::table_apply_pairs(t->impl, recv_ids, recv_versions, id_counts, pair_pos, contrib,
+                           pair_counts, world, lr, step_tag, epoch, accepted, flags, S(stream));
   });
 }
 

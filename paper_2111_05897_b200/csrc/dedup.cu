@@ -198,6 +198,8 @@ struct Scratch {
 
 uint32_t grid_for(uint64_t n) { return std::max<uint32_t>(1, std::min<uint64_t>(ceil_div(n, 256), 148 * 16)); }
 
+}  // namespace
+
 // out = exclusive scan of in[0..n); returns the total through *total (device).
 void exclusive_scan(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* tile_sums,
                     uint32_t* total, cudaStream_t st) {
@@ -207,6 +209,8 @@ void exclusive_scan(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* til
   tile_scan_kernel<<<tiles, 1024, 0, st>>>(in, n, tile_sums, out);
   HPS_LAUNCH_CHECK_N(3);
 }
+
+namespace {
 
 int key_bits_of(const uint64_t* keys, uint64_t n, unsigned long long* d_or, cudaStream_t st) {
   HPS_CUDA(cudaMemsetAsync(d_or, 0, sizeof(unsigned long long), st));

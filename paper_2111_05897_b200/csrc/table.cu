@@ -294,8 +294,8 @@ void table_destroy(Table* t) {
     t->stage.free_all();
     t->prof.destroy();
     DevTable& d = t->d;
-    void* ptrs[] = {d.ht,  d.rows, d.seen, d.multi, d.slot_id, d.special,
-                    d.hwm, d.ctr,  t->d_salts};
+    void* ptrs[] = {d.ht,  d.rows, d.seen,     d.multi,    d.slot_id, d.special,
+                    d.hwm, d.ctr,  t->d_salts, t->xs.ids, t->xs.rv,  t->xs.bad};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (t->h_ctr) cudaFreeHost(t->h_ctr);

@@ -170,6 +170,15 @@ struct ProfScope {
   cudaEvent_t a = nullptr;
 };
 
+// Owner-side workspace of the multi-GPU exchange (exchange.cu).
+constexpr uint32_t kMaxWorld = 32;
+struct XScratch {
+  uint64_t* ids = nullptr;
+  uint64_t* rv = nullptr;
+  uint32_t* bad = nullptr;
+  uint64_t cap_ids = 0, cap_rv = 0;
+};
+
 struct Table {
   hps_table_cfg cfg{};
   Profiler prof;
@@ -187,6 +196,7 @@ struct Table {
   // (snapshot) when some other mutation is about to run before their own push.
   std::vector<Batch*> outstanding;
   unsigned long long* h_ctr = nullptr;  // pinned mirror of the counters
+  XScratch xs;
 };
 
 // ---- kernels / launchers (kernels.cu, update.cu) ---------------------------------------

@@ -77,10 +77,52 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
 void route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cudaStream_t st);
 
 // dedup.cu
+void exclusive_scan(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* tile_sums,
+                    uint32_t* total, cudaStream_t st);
 void dedup(const uint64_t* ids, uint64_t n, uint64_t* out_unique, uint32_t* out_inverse,
            uint64_t* out_u, cudaStream_t st);
 void compress_indices(const uint64_t* ids, uint64_t n, const uint32_t* offsets, uint32_t B,
                       uint32_t G, uint64_t* group_u_off, uint64_t* unique, uint64_t* post_off,
                       uint16_t* postings, cudaStream_t st);
+
+// exchange.cu -- source-side plan of one multi-GPU step (see hps_c.h hps_exchange_*).
+struct XBatch {
+  int device = 0;
+  int sms = 148;
+  uint32_t G = 1, S = 1;
+  int agg = HPS_MEAN;
+  uint32_t B = 0, F = 0;
+  uint64_t N = 0, U = 0, P = 0;
+  bool pooled_ready = false;
+  uint64_t* hkeys = nullptr;
+  uint32_t* hidx = nullptr;
+  uint32_t* hval = nullptr;
+  uint8_t* dest = nullptr;
+  uint32_t* sendpos = nullptr;
+  uint32_t* offsets = nullptr;
+  uint32_t* lgrp = nullptr;
+  uint32_t *keys_a = nullptr, *vals_a = nullptr, *keys_b = nullptr, *vals_b = nullptr;
+  uint32_t* scratch = nullptr;
+  uint32_t *head = nullptr, *ex = nullptr, *tsum = nullptr;
+  uint32_t* cnt = nullptr;
+  uint32_t* seg = nullptr;
+  uint8_t* dest_of_pos = nullptr;
+  uint64_t* pair_off = nullptr;
+  uint64_t* h_buf = nullptr;
+  uint64_t cap_H = 0, cap_hidx = 0, cap_hval = 0, cap_dest = 0, cap_sendpos = 0, cap_off = 0,
+           cap_lgrp = 0, cap_ka = 0, cap_va = 0, cap_kb = 0, cap_vb = 0, cap_scratch = 0,
+           cap_head = 0, cap_ex = 0, cap_tsum = 0, cap_dop = 0;
+  ~XBatch();
+};
+void xbatch_init(XBatch& x);
+void xbatch_route(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_t* offsets, uint32_t B,
+                  uint32_t F, uint64_t* out_send_ids, uint64_t* out_counts, cudaStream_t st);
+void xbatch_pool(XBatch& x, const float* rows, uint32_t D, float* out_pooled, cudaStream_t st);
+void xbatch_pairs(XBatch& x, const float* grads, uint32_t D, uint32_t* out_pair_pos,
+                  float* out_contrib, uint64_t* out_pair_counts, cudaStream_t st);
+void table_apply_pairs(Table* t, const uint64_t* recv_ids, const uint64_t* recv_versions,
+                       const uint64_t* id_counts, const uint32_t* pair_pos, const float* contrib,
+                       const uint64_t* pair_counts, uint32_t G, float lr, uint32_t step_tag,
+                       uint32_t epoch, int* accepted, uint32_t flags, cudaStream_t st);
 
 }  // namespace hps

@@ -162,6 +162,13 @@ def lib():
         "hps_profile_get": (st, [vp, C.c_char_p, C.POINTER(C.c_double), C.POINTER(u64)]),
         "hps_dedup": (st, [vp, sz, vp, vp, C.POINTER(u64), vp]),
         "hps_compress_indices": (st, [vp, sz, vp, u32, u32, vp, vp, vp, vp, vp]),
+        "hps_exchange_create": (st, [u32, u32, i32, i32, C.POINTER(vp)]),
+        "hps_exchange_destroy": (st, [vp]),
+        "hps_exchange_route": (st, [vp, vp, sz, vp, u32, u32, vp, C.POINTER(u64), vp]),
+        "hps_exchange_pool": (st, [vp, vp, u32, vp, vp]),
+        "hps_exchange_pairs": (st, [vp, vp, u32, vp, vp, C.POINTER(u64), vp]),
+        "hps_table_apply_pairs": (st, [vp, vp, vp, C.POINTER(u64), vp, vp, C.POINTER(u64), u32,
+                                       f32, u32, u32, C.POINTER(C.c_int), u32, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

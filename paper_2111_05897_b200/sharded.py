@@ -1,0 +1,199 @@
+"""Hash-sharded embedding worker over N GPUs.
+
+One process per GPU. Every rank holds the rows it owns -- rank ``route_shard(id, S) %
+world`` (``ShardSet::shard_of``, embedding_ps.hpp:521-523, with the S logical shards
+spread round-robin over the ranks) -- in a local ``hps.ShardSet`` created with all S
+shard salts, and runs one embedding worker over its own batch. A step is the reference's
+E embedding workers in front of a sharded parameter server
+(``EmbeddingWorker::fetch_rows`` embedding_worker.hpp:677-704, ``serve_pull`` :523-571,
+``push_to_shards`` :726-775, ``PsShardService`` :185-290), with the per-frame RPCs
+replaced by three NCCL all-to-alls:
+
+  forward   route (distinct ids grouped by owner) -> all-to-all ids -> owner lookup
+            (find_or_init + gather + versions) -> all-to-all rows -> fp64 pooling
+  backward  pairs (one fp64 chain-rule contribution per (sample, distinct id), grouped
+            by owner) -> all-to-all (position, contribution) -> owner applies them in
+            (source rank, sample) order = ascending SampleId (rank << 56 | counter,
+            core.hpp:98-125; flush order embedding_worker.hpp:788-790)
+
+The local work is hand-written CUDA in libhps.so (``DeviceOps``: hps_exchange_* and
+hps_lookup / hps_table_apply_pairs); the collectives are torch.distributed over NCCL.
+``ShardedEmbeddingWorker`` only sequences the two; ``ops`` is injectable so the
+sequencing itself is testable with a gloo process group on CPU (tests/test_sharded.py
+checks it against the reference's multi-worker semantics with an oracle-backed ops).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import hps
+
+
+class DeviceOps:
+    """The local steps of a sharded step on this rank's GPU (libhps.so)."""
+
+    def __init__(self, table: hps.ShardSet, world: int, aggregation: int):
+        import torch
+
+        self.torch = torch
+        self.table = table
+        self.world = world
+        self.D = table.embedding_dim
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        h = hps.vp()
+        hps.check(hps.lib().hps_exchange_create(world, table.shard_count, aggregation, -1,
+                                                C.byref(h)), "exchange")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            hps.lib().hps_exchange_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _s(self):
+        return self.torch.cuda.current_stream().cuda_stream
+
+    def route(self, ids, offsets, B: int, F: int):
+        t = self.torch
+        n = ids.numel()
+        send = t.empty(max(n, 1), dtype=t.int64, device=self.device)
+        counts = (C.c_uint64 * self.world)()
+        hps.check(hps.lib().hps_exchange_route(self.h, ids.data_ptr(), n, offsets.data_ptr(), B,
+                                               F, send.data_ptr(), counts, self._s()),
+                  "exchange_route")
+        counts = [int(c) for c in counts]
+        return send[:sum(counts)], counts
+
+    def lookup(self, recv_ids):
+        t = self.torch
+        n = recv_ids.numel()
+        rows = t.empty((n, self.D), dtype=t.float32, device=self.device)
+        ver = t.empty(n, dtype=t.int64, device=self.device)
+        if n:
+            self.table.lookup(recv_ids, out_values=rows, out_versions=ver,
+                              stream=self.torch.cuda.current_stream())
+        return rows, ver
+
+    def pool(self, rows, B: int, F: int, out=None):
+        t = self.torch
+        if out is None:
+            out = t.empty((B, F, self.D), dtype=t.float32, device=self.device)
+        hps.check(hps.lib().hps_exchange_pool(self.h, rows.data_ptr() if rows.numel() else None,
+                                              self.D, out.data_ptr(), self._s()), "exchange_pool")
+        return out
+
+    def pairs(self, grads, n_ids: int):
+        t = self.torch
+        grads = grads.contiguous()
+        pos = t.empty(max(n_ids, 1), dtype=t.int32, device=self.device)
+        con = t.empty((max(n_ids, 1), self.D), dtype=t.float32, device=self.device)
+        counts = (C.c_uint64 * self.world)()
+        hps.check(hps.lib().hps_exchange_pairs(self.h, grads.data_ptr(), self.D, pos.data_ptr(),
+                                               con.data_ptr(), counts, self._s()),
+                  "exchange_pairs")
+        counts = [int(c) for c in counts]
+        self.last_pair_counts = counts
+        P = sum(counts)
+        return pos[:P], con[:P], counts
+
+    def apply_pairs(self, recv_ids, recv_versions, id_counts, pair_pos, contrib, pair_counts,
+                    lr: float, step_tag: int, epoch: int, flags: int = 0) -> bool:
+        W = self.world
+        ic = (C.c_uint64 * W)(*id_counts)
+        pc = (C.c_uint64 * W)(*pair_counts)
+        acc = C.c_int(0)
+        hps.check(hps.lib().hps_table_apply_pairs(
+            self.table.h, recv_ids.data_ptr() if recv_ids.numel() else None,
+            recv_versions.data_ptr() if recv_versions is not None and recv_versions.numel()
+            else None, ic, pair_pos.data_ptr() if pair_pos.numel() else None,
+            contrib.data_ptr() if contrib.numel() else None, pc, W, lr, step_tag, epoch,
+            C.byref(acc), flags, self._s()), "apply_pairs")
+        return bool(acc.value)
+
+
+class ShardedEmbeddingWorker:
+    """``register_batch`` / ``serve_pull`` / ``apply_backward`` of one rank's embedding
+    worker over the hash-sharded table (sync order; one batch in flight)."""
+
+    def __init__(self, table: hps.ShardSet, aggregation: int = hps.MEAN, group=None, ops=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        if dist.is_available() and dist.is_initialized():
+            self.world = dist.get_world_size(group)
+            self.rank = dist.get_rank(group)
+        else:
+            self.world, self.rank = 1, 0
+        self.table = table
+        self.aggregation = aggregation
+        self.ops = ops if ops is not None else DeviceOps(table, self.world, aggregation)
+        self.B = self.F = 0
+
+    # -- collectives ------------------------------------------------------------------
+    def _exchange_counts(self, counts):
+        """counts[d] = what this rank sends to d -> what each source sends to this rank."""
+        if self.world == 1:
+            return list(counts)
+        import torch
+
+        dev = self._comm_device()
+        send = torch.tensor(counts, dtype=torch.int64, device=dev)
+        recv = torch.empty_like(send)
+        self.dist.all_to_all_single(recv, send, group=self.group)
+        return [int(x) for x in recv.cpu()]
+
+    def _a2a(self, inp, send_counts, recv_counts):
+        if self.world == 1:
+            return inp
+        import torch
+
+        out = torch.empty((sum(recv_counts),) + tuple(inp.shape[1:]), dtype=inp.dtype,
+                          device=inp.device)
+        self.dist.all_to_all_single(out, inp.contiguous(), output_split_sizes=list(recv_counts),
+                                    input_split_sizes=list(send_counts), group=self.group)
+        return out
+
+    def _comm_device(self):
+        import torch
+
+        backend = self.dist.get_backend(self.group)
+        return torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else "cpu"
+
+    # -- the worker surface ---------------------------------------------------------------
+    def register_batch(self, ids, offsets, B: int, F: int):
+        """Route the batch's ids to their owners and fetch the rows (fetch_rows)."""
+        self.B, self.F, self.n_ids = B, F, ids.numel()
+        send_ids, self.send_counts = self.ops.route(ids, offsets, B, F)
+        self.recv_counts = self._exchange_counts(self.send_counts)
+        self.recv_ids = self._a2a(send_ids, self.send_counts, self.recv_counts)
+        rows, self.recv_versions = self.ops.lookup(self.recv_ids)
+        self.rows = self._a2a(rows, self.recv_counts, self.send_counts)
+
+    def serve_pull(self, out_pooled=None):
+        """Pooled embeddings [B, F, D] of the registered batch (serve_pull)."""
+        return self.ops.pool(self.rows, self.B, self.F, out_pooled)
+
+    def apply_backward(self, grads, lr: float, step_tag: int, epoch: int | None = None,
+                       flags: int = 0) -> bool:
+        """Per-sample gradients [B, F, D] -> owners, applied in ascending SampleId."""
+        pos, con, pair_counts = self.ops.pairs(grads, self.n_ids)
+        recv_pair_counts = self._exchange_counts(pair_counts)
+        rpos = self._a2a(pos, pair_counts, recv_pair_counts)
+        rcon = self._a2a(con, pair_counts, recv_pair_counts)
+        e = self.table.epoch() if epoch is None else epoch
+        return self.ops.apply_pairs(self.recv_ids, self.recv_versions, self.recv_counts, rpos,
+                                    rcon, recv_pair_counts, lr, step_tag, e, flags)
+
+
+def owner_of(ids: np.ndarray, shard_count: int, world: int) -> np.ndarray:
+    """Owner rank of each id (host helper for tests and tools)."""
+    return np.array([hps.route_shard(int(i), shard_count) % world for i in ids], np.int64)

@@ -91,6 +91,13 @@ CONFIGS = {
 }
 
 
+def sharded_config(world: int) -> Config:
+    """C4 at `world` GPUs, weak-scaled: per-GPU batch 16384 of the C2 shape over a table
+    of 125M rows per GPU (1B rows at 8 GPUs), S = 8 logical shards per GPU."""
+    return Config("c4", 16384, 26, 125_000_000 * world, 64, "adagrad", "mean",
+                  shards=8 * world)
+
+
 @dataclass
 class Batch:
     ids: np.ndarray  # uint64 [N]

@@ -1,0 +1,142 @@
+"""TEST INFRASTRUCTURE: one multi-rank sharded-step parity case, run by every rank.
+
+The global batch of step s has W*B samples; rank r serves samples r, r+W, ... -- the
+reference's sample -> embedding-worker assignment (sample i -> EW i % E,
+oracle/ref_driver.cpp; sid = (i % E) << 56 | i / E, data.hpp:392). The expected result
+is the oracle table driven with the whole global batch and those sample keys (pinned
+against the reference's multi-worker run in tests/test_oracle_pinning.py).
+"""
+from __future__ import annotations
+
+import os
+import sys
+import traceback
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+
+def global_batch(step, W, B, F, space, seed=11):
+    rng = np.random.default_rng(seed * 1000 + step)
+    counts = rng.integers(0, 4, W * B * F)
+    counts[rng.random(W * B * F) < 0.5] = 1
+    offs = np.zeros(W * B * F + 1, np.int64)
+    np.cumsum(counts, out=offs[1:])
+    ids = rng.integers(0, space, int(offs[-1])).astype(np.uint64)
+    if len(ids) > 3:
+        ids[rng.integers(0, len(ids), 2)] = np.uint64(0xFFFFFFFFFFFFFFFF)  # the special id
+    return ids, offs, counts
+
+
+def local_part(ids, offs, W, B, F, r):
+    """CSR of samples r, r+W, ... of the global batch."""
+    lid, loff = [], [0]
+    for b in range(r, W * B, W):
+        for f in range(F):
+            sg = b * F + f
+            seg = ids[offs[sg]:offs[sg + 1]]
+            lid.extend(seg.tolist())
+            loff.append(loff[-1] + len(seg))
+    return np.array(lid, np.uint64), np.array(loff, np.int64)
+
+
+def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, agg="mean",
+             opt="adagrad", q=None):
+    try:
+        import torch
+        import torch.distributed as dist
+
+        import oracle as O
+        from paper_2111_05897_b200 import hps
+        from paper_2111_05897_b200.sharded import ShardedEmbeddingWorker
+
+        if use_device:
+            torch.cuda.set_device(rank)
+        dist.init_process_group(backend, init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        S = 8
+        salts = [O.mix64(7 + s) for s in range(S)]
+        exp = O.Restatement(salts, D, opt)  # the whole global batch, one table
+        if use_device:
+            dev = torch.device("cuda", rank)
+            table = hps.ShardSet(S, D, 1 << 14, hps.ADAGRAD if opt == "adagrad" else hps.SGD,
+                                 salts=salts)
+            ew = ShardedEmbeddingWorker(table, hps.MEAN if agg == "mean" else hps.SUM)
+            owner_peek = table.peek
+        else:
+            from sharded_oracle_ops import EpochOnly, OracleOps
+
+            dev = torch.device("cpu")
+            local = O.Restatement(salts, D, opt)
+            ew = ShardedEmbeddingWorker(EpochOnly(local), hps.MEAN if agg == "mean" else hps.SUM,
+                                        ops=OracleOps(local, world, S, D, agg))
+            owner_peek = local.peek
+        seen = set()
+        for s in range(steps):
+            gids, goffs, _ = global_batch(s, world, B, F, 60)
+            rng = np.random.default_rng(500 + s)
+            g_all = (rng.standard_normal((world * B, F, D)) * 0.3).astype(np.float32)
+            sk = np.array([((i % world) << 56) | (i // world) for i in range(world * B)],
+                          np.uint64)
+            pooled_exp, rv_exp = exp.pull_batch(world * B, F, gids, goffs.astype(np.uint64), agg)
+            lid, loff = local_part(gids, goffs, world, B, F, rank)
+            seen.update(int(x) for x in gids)
+            t_ids = torch.from_numpy(lid.view(np.int64).copy()).to(dev)
+            t_off = torch.from_numpy(loff.astype(np.int32)).to(dev)
+            ew.register_batch(t_ids, t_off, B, F)
+            pooled = ew.serve_pull()
+            got = pooled.cpu().numpy()
+            want = pooled_exp[rank::world]
+            assert got.tobytes() == want.tobytes(), f"rank {rank} step {s}: pooled differs"
+            g_local = torch.from_numpy(np.ascontiguousarray(g_all[rank::world])).to(dev)
+            ok = ew.apply_backward(g_local, 0.05, s + 1)
+            assert ok
+            ok2, _ = exp.push_batch(world * B, F, gids, goffs.astype(np.uint64), g_all, 0.05,
+                                    s + 1, read_versions=rv_exp, sample_keys=sk, agg=agg)
+            assert ok2
+        if use_device:
+            torch.cuda.synchronize()
+        mine = np.array(sorted(i for i in seen
+                               if hps.route_shard(i, S) % world == rank), np.uint64)
+        w, a, v, p = owner_peek(mine)
+        we, ae, ve, pe = exp.peek(mine)
+        assert p.all() and pe.all()
+        assert w.tobytes() == we.tobytes(), f"rank {rank}: rows differ"
+        assert a.tobytes() == ae.tobytes(), f"rank {rank}: optimizer state differs"
+        assert (v == ve).all(), f"rank {rank}: versions differ"
+        dist.barrier()
+        dist.destroy_process_group()
+        if q is not None:
+            q.put((rank, "ok", len(mine)))
+    except Exception:
+        if q is not None:
+            q.put((rank, traceback.format_exc(), 0))
+        raise
+
+
+def run_world(world, backend, use_device, timeout=240, **kw):
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=run_rank, args=(r, world, backend, port, use_device),
+                         kwargs=dict(kw, q=q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = []
+    try:
+        for _ in range(world):
+            results.append(q.get(timeout=timeout))
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    return results

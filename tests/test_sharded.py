@@ -1,0 +1,43 @@
+"""Multi-rank sharded step: every rank's pooled output, and the rows,
+optimizer state and versions each owner holds after several steps, equal the oracle
+driven with the whole global batch in ascending-SampleId order (bit-exact).
+
+CPU: the collective sequencing of ShardedEmbeddingWorker over gloo (world 2 and 3) with
+the local steps restated on the CPU (tests/sharded_oracle_ops.py).
+GPU: the same case through libhps.so + NCCL (world 1 on one GPU; world 2 when two GPUs
+are visible)."""
+import pytest
+
+from sharded_case import run_world
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_sequencing_gloo(world):
+    res = run_world(world, "gloo", use_device=False)
+    assert sorted(r for r, _, _ in res) == list(range(world))
+    for r, status, n in res:
+        assert status == "ok", status
+
+
+def test_sharded_sequencing_gloo_sum_sgd():
+    res = run_world(2, "gloo", use_device=False, agg="sum", opt="sgd")
+    for r, status, n in res:
+        assert status == "ok", status
+
+
+@pytest.mark.gpu
+def test_sharded_device_world1():
+    res = run_world(1, "nccl", use_device=True)
+    assert res[0][1] == "ok", res[0][1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("agg,opt", [("mean", "adagrad"), ("sum", "sgd")])
+def test_sharded_device_world2(agg, opt):
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = run_world(2, "nccl", use_device=True, agg=agg, opt=opt)
+    for r, status, n in res:
+        assert status == "ok", status
