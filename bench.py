@@ -264,8 +264,7 @@ def run_sharded(args, world, rank, local, dev):
         step(it)
         it += 1
         x_ids += sum(c for d, c in enumerate(ew.send_counts) if d != rank)
-        x_pairs += sum(c for d, c in enumerate(ew.ops.last_pair_counts) if d != rank) \
-            if hasattr(ew.ops, "last_pair_counts") else 0
+        x_pairs += sum(c for d, c in enumerate(ew.pair_counts) if d != rank)
     e1.record(stream)
     dist.barrier()
     torch.cuda.synchronize()

@@ -121,6 +121,11 @@ hps_status hps_table_reset(hps_table* t);                /* PsShard::reset_for_r
 hps_status hps_lookup(hps_table* t, const uint64_t* ids, size_t n, float* out_values,
                       uint64_t* out_versions, hps_stream stream);
 
+/* hps_lookup with flags: HPS_ASYNC defers the capacity report to hps_table_sync (no host
+ * round trip; used by the owner side of the multi-GPU exchange). */
+hps_status hps_table_gather(hps_table* t, const uint64_t* ids, size_t n, float* out_values,
+                            uint64_t* out_versions, uint32_t flags, hps_stream stream);
+
 /* PsShard::apply_gradients (embedding_ps.hpp:139-162), array-shaped: entry i carries
  * ids[i], grads[i*D..], read_versions[i]. Epoch fence first (*accepted = 0, nothing
  * applied, stale_epoch_drops += n); then every gradient is validated finite before
@@ -195,7 +200,8 @@ typedef struct hps_exchange hps_exchange;
 hps_status hps_exchange_create(uint32_t world_size, uint32_t shard_count, int32_t aggregation,
                                int32_t device, hps_exchange** out);
 hps_status hps_exchange_destroy(hps_exchange* x);
-/* out_send_ids[n_ids] (first sum(out_counts) used, owner-major); out_counts[world]. */
+/* out_send_ids[n_ids] (first sum(out_counts) used, owner-major); out_counts[world]:
+ * a host array (the call synchronises) or a device array (stays stream-ordered). */
 hps_status hps_exchange_route(hps_exchange* x, const uint64_t* ids, size_t n_ids,
                               const uint32_t* offsets, uint32_t B, uint32_t F,
                               uint64_t* out_send_ids, uint64_t* out_counts, hps_stream stream);
@@ -203,7 +209,8 @@ hps_status hps_exchange_route(hps_exchange* x, const uint64_t* ids, size_t n_ids
 hps_status hps_exchange_pool(hps_exchange* x, const float* rows, uint32_t dim, float* out_pooled,
                              hps_stream stream);
 /* grads[B*F*dim]; out_pair_pos[P] = index of the pair's id inside its owner's segment of
- * send_ids; out_contrib[P*dim]; out_pair_counts[world]. Buffers sized for n_ids pairs. */
+ * send_ids; out_contrib[P*dim]; out_pair_counts[world] (host: synchronises; device: no).
+ * Buffers sized for n_ids pairs. */
 hps_status hps_exchange_pairs(hps_exchange* x, const float* grads, uint32_t dim,
                               uint32_t* out_pair_pos, float* out_contrib,
                               uint64_t* out_pair_counts, hps_stream stream);
@@ -211,7 +218,9 @@ hps_status hps_exchange_pairs(hps_exchange* x, const float* grads, uint32_t dim,
  * major, id_counts[world]) and the versions hps_lookup returned for them; the pairs
  * (pair_pos, contrib) received from each source (pair_counts[world]) apply through
  * PsShard::apply_gradients (:139-162): epoch fence, all-finite validation, ordered update,
- * version bump per step tag. recv_versions == NULL applies untracked. */
+ * version bump per step tag. recv_versions == NULL applies untracked. A pair position
+ * outside its source's segment rejects the whole call (HPS_E_PROTOCOL, at once or, with
+ * HPS_ASYNC, from hps_table_sync). */
 hps_status hps_table_apply_pairs(hps_table* t, const uint64_t* recv_ids,
                                  const uint64_t* recv_versions, const uint64_t* id_counts,
                                  const uint32_t* pair_pos, const float* contrib,

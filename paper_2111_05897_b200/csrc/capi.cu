@@ -148,6 +148,17 @@ hps_status hps_lookup(hps_table* t, const uint64_t* ids, size_t n, float* out_va
   });
 }
 
+hps_status hps_table_gather(hps_table* t, const uint64_t* ids, size_t n, float* out_values,
+                            uint64_t* out_versions, uint32_t flags, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(t && (n == 0 || (ids && out_values)), "hps_table_gather: null argument");
+    if (n == 0) return;
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::DeviceGuard dg(t->impl->device);
+    hps::table_lookup(t->impl, ids, n, out_values, out_versions, S(stream), flags);
+  });
+}
+
 hps_status hps_apply(hps_table* t, const uint64_t* ids, const float* grads,
                      const uint64_t* read_versions, size_t n, float lr, uint32_t step_tag,
                      uint32_t epoch, uint32_t* out_delays, int* accepted, uint32_t flags,

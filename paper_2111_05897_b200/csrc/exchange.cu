@@ -200,15 +200,24 @@ __global__ void __launch_bounds__(kXBlock)
   }
 }
 
-// dest per send position (the owner of send_ids[pos]) from the segment table.
-__global__ void x_dest_of_pos_kernel(const uint32_t* __restrict__ seg, uint32_t G, uint64_t U,
+// dest per send position (the owner of send_ids[pos]) from the segment table; U = seg[G]
+// is device-side, the grid covers the host bound n >= U.
+__global__ void x_dest_of_pos_kernel(const uint32_t* __restrict__ seg, uint32_t G, uint64_t n,
                                      uint8_t* __restrict__ out) {
-  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < U;
+  const uint64_t U = seg[G];
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < U && u < n;
        u += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t d = 0;
     while (d + 1 < G && seg[d + 1] <= u) ++d;
     out[u] = static_cast<uint8_t>(d);
   }
+}
+
+// Per-owner counts as u64 into a device array (no host round trip).
+__global__ void x_counts_kernel(const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ off,
+                                uint32_t G, uint64_t* __restrict__ out) {
+  const uint32_t d = threadIdx.x;
+  if (d < G) out[d] = cnt ? cnt[d] : off[d + 1] - off[d];
 }
 
 // Pair offsets per owner: pairs are sorted by send position and owner segments are
@@ -239,25 +248,27 @@ struct Offs {
 };
 
 // Owner side: pair k (received from source r) names entry id_off[r] + pair_pos[k] of
-// the ids this rank received (and looked up) in the forward exchange.
+// the ids this rank received (and looked up) in the forward exchange. The pairs become a
+// batch of P one-listing samples (offsets = 0..P) in arrival order.
 __global__ void x_owner_kernel(const uint64_t* __restrict__ recv_ids,
                                const uint64_t* __restrict__ recv_versions, Offs id_off,
                                Offs pair_off, uint32_t G, const uint32_t* __restrict__ pair_pos,
                                uint64_t P, uint64_t* __restrict__ out_ids,
-                               uint64_t* __restrict__ out_rv, uint32_t* bad) {
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < P;
+                               uint64_t* __restrict__ out_rv, uint32_t* __restrict__ out_off,
+                               unsigned long long* protocol) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k <= P;
        k += (uint64_t)gridDim.x * blockDim.x) {
+    out_off[k] = static_cast<uint32_t>(k);
+    if (k == P) break;
     uint32_t r = 0;
     while (r + 1 < G && pair_off.v[r + 1] <= k) ++r;
-    const uint64_t idx = id_off.v[r] + pair_pos[k];
+    uint64_t idx = id_off.v[r] + pair_pos[k];
     if (idx >= id_off.v[r + 1]) {
-      atomicOr(bad, 1u);
-      out_ids[k] = 0;
-      out_rv[k] = 0;
-      continue;
+      atomicOr(protocol, 1ull);  // gates every update kernel; reported by check_flags
+      idx = id_off.v[r];
     }
-    out_ids[k] = recv_ids[idx];
-    out_rv[k] = recv_versions ? recv_versions[idx] : 0;
+    out_ids[k] = idx < id_off.v[G] ? recv_ids[idx] : 0;
+    out_rv[k] = (recv_versions && idx < id_off.v[G]) ? recv_versions[idx] : 0;
   }
 }
 
@@ -338,15 +349,15 @@ void xbatch_route(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_t* of
       ids, n, x.G, x.hidx, x.hval, x.dest, x.cnt, x.sendpos, out_send_ids, x.seg);
   HPS_LAUNCH_CHECK();
   launch_expand_groups(x.offsets, static_cast<uint32_t>(BF), x.lgrp, st);
+  if (is_device_ptr(out_counts)) {  // stays on the device: no host round trip
+    x_counts_kernel<<<1, 32, 0, st>>>(x.cnt, nullptr, x.G, out_counts);
+    HPS_LAUNCH_CHECK();
+    return;
+  }
   uint32_t* h = reinterpret_cast<uint32_t*>(x.h_buf);
   HPS_CUDA(cudaMemcpyAsync(h, x.cnt, x.G * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   HPS_CUDA(cudaStreamSynchronize(st));
-  uint64_t U = 0;
-  for (uint32_t d = 0; d < x.G; ++d) {
-    out_counts[d] = h[d];
-    U += h[d];
-  }
-  x.U = U;
+  for (uint32_t d = 0; d < x.G; ++d) out_counts[d] = h[d];
 }
 
 void xbatch_pool(XBatch& x, const float* rows, uint32_t D, float* out_pooled, cudaStream_t st) {
@@ -357,7 +368,7 @@ void xbatch_pool(XBatch& x, const float* rows, uint32_t D, float* out_pooled, cu
   view.rows = const_cast<float*>(rows);
   view.D = D;
   view.stride = D;
-  view.capacity = static_cast<uint32_t>(std::min<uint64_t>(x.U, 0xffffffffull));
+  view.capacity = static_cast<uint32_t>(x.N);  // U <= N (U itself may be device-side)
   const uint64_t BF = static_cast<uint64_t>(x.B) * x.F;
   launch_pool(view, x.offsets, x.sendpos, static_cast<uint32_t>(BF), x.N,
               x.agg == HPS_MEAN ? 1 : 0, out_pooled, nullptr, nullptr, st);
@@ -383,17 +394,17 @@ void xbatch_pairs(XBatch& x, const float* grads, uint32_t D, uint32_t* out_pair_
   grow(x.head, x.cap_head, n);
   grow(x.ex, x.cap_ex, n);
   grow(x.tsum, x.cap_tsum, ceil_div(n, 4096) + 2);
-  grow(x.dest_of_pos, x.cap_dop, std::max<uint64_t>(x.U, 1));
+  grow(x.dest_of_pos, x.cap_dop, n);
   // Stable sort of the listings by send position: per distinct id, listings stay in
   // listing (= sample, group, position) order.
   const bool in_b = radix::sort_pairs<uint32_t>(
-      x.keys_a, x.vals_a, x.keys_b, x.vals_b, n, bits_for(x.U ? x.U - 1 : 0), x.scratch, st,
+      x.keys_a, x.vals_a, x.keys_b, x.vals_b, n, bits_for(n - 1), x.scratch, st,
       x.sms, nullptr, x.sendpos, true);
   const uint32_t* spos = in_b ? x.keys_b : x.keys_a;
   const uint32_t* slist = in_b ? x.vals_b : x.vals_a;
   x_pair_flags_kernel<<<grid_n(n, x.sms), kXBlock, 0, st>>>(spos, slist, x.lgrp, x.F, n, x.head);
   exclusive_scan(x.head, x.ex, n, x.tsum, x.tsum + ceil_div(n, 4096), st);
-  x_dest_of_pos_kernel<<<grid_n(x.U, x.sms), kXBlock, 0, st>>>(x.seg, x.G, x.U, x.dest_of_pos);
+  x_dest_of_pos_kernel<<<grid_n(n, x.sms), kXBlock, 0, st>>>(x.seg, x.G, n, x.dest_of_pos);
   HPS_LAUNCH_CHECK_N(2);
   HPS_DISPATCH_DIM(D, {
     const uint32_t blocks = static_cast<uint32_t>(std::max<uint64_t>(
@@ -404,6 +415,11 @@ void xbatch_pairs(XBatch& x, const float* grads, uint32_t D, uint32_t* out_pair_
   });
   x_pair_bounds_kernel<<<1, 64, 0, st>>>(spos, x.ex, x.head, n, x.seg, x.G, x.pair_off);
   HPS_LAUNCH_CHECK_N(2);
+  if (is_device_ptr(out_pair_counts)) {
+    x_counts_kernel<<<1, 32, 0, st>>>(nullptr, x.pair_off, x.G, out_pair_counts);
+    HPS_LAUNCH_CHECK();
+    return;
+  }
   HPS_CUDA(cudaMemcpyAsync(x.h_buf, x.pair_off, (x.G + 1) * sizeof(uint64_t),
                            cudaMemcpyDeviceToHost, st));
   HPS_CUDA(cudaStreamSynchronize(st));
@@ -426,22 +442,24 @@ void table_apply_pairs(Table* t, const uint64_t* recv_ids, const uint64_t* recv_
     po.v[r + 1] = po.v[r] + pair_counts[r];
   }
   const uint64_t P = po.v[G];
+  if (P >= 0xffffffffull) throw Error(HPS_E_PRECONDITION, "apply_pairs: too many pairs");
   XScratch& xs = t->xs;
   grow(xs.ids, xs.cap_ids, P);
   grow(xs.rv, xs.cap_rv, P);
-  if (!xs.bad) HPS_CUDA(cudaMalloc(&xs.bad, sizeof(uint32_t)));
-  HPS_CUDA(cudaMemsetAsync(xs.bad, 0, sizeof(uint32_t), st));
-  if (P) {
-    x_owner_kernel<<<grid_n(P, t->sm_count), kXBlock, 0, st>>>(
-        recv_ids, recv_versions, io, po, G, pair_pos, P, xs.ids, xs.rv, xs.bad);
-    HPS_LAUNCH_CHECK();
-  }
-  uint32_t bad = 0;
-  HPS_CUDA(cudaMemcpyAsync(&bad, xs.bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  HPS_CUDA(cudaStreamSynchronize(st));
-  if (bad) throw Error(HPS_E_PROTOCOL, "apply_pairs: pair position outside its source's ids");
-  table_apply(t, xs.ids, contrib, recv_versions ? xs.rv : nullptr, P, lr, step_tag, epoch,
-              nullptr, accepted, flags, st);
+  grow(xs.off, xs.cap_off, P + 1);
+  x_owner_kernel<<<grid_n(P + 1, t->sm_count), kXBlock, 0, st>>>(
+      recv_ids, recv_versions, io, po, G, pair_pos, P, xs.ids, xs.rv, xs.off,
+      t->d.ctr + kCtrProtocol);
+  HPS_LAUNCH_CHECK();
+  // The pairs as a batch of P one-listing samples, sum aggregation: each contribution is
+  // applied as is (the source's fan-out already produced (float)(0.0 + sum), never -0.0),
+  // per row in arrival order = (source rank, sample) order, through the batch plan
+  // (rows hit once skip the ordering sort).
+  Batch& b = t->scratch;
+  b.agg = HPS_SUM;
+  batch_register(b, xs.ids, P, xs.off, static_cast<uint32_t>(P), 1, nullptr, st);
+  batch_push(b, HPS_SUM, contrib, lr, step_tag, epoch, recv_versions ? 0 : 1,
+             recv_versions ? xs.rv : nullptr, accepted, flags, st);
 }
 
 }  // namespace hps

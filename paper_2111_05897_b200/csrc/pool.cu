@@ -46,6 +46,7 @@ __device__ void pool_general(const DevTable& t, const uint32_t* __restrict__ slo
                              uint64_t* out_rv64, uint32_t* out_rv32) {
   using G = Geo<V, L, kGuard>;
   const uint32_t D = t.D;
+  const bool want_rv = out_rv64 || out_rv32;  // row headers are only read when asked for
   const int chunks = kGuard ? (D + G::kSpan - 1) / G::kSpan : 1;
   for (int c = 0; c < chunks; ++c) {
     const uint32_t d0 = c * G::kSpan + ln * V;
@@ -67,7 +68,7 @@ __device__ void pool_general(const DevTable& t, const uint32_t* __restrict__ slo
         acc[k] = __dadd_rn(acc[k], static_cast<double>(r0[k]));
         acc[k] = __dadd_rn(acc[k], static_cast<double>(r1[k]));
       }
-      if (c == 0 && ln == 0) {
+      if (want_rv && c == 0 && ln == 0) {
         uint32_t v0 = slot_ok(t, s0) ? t.vt[s0].x : 0, v1 = slot_ok(t, s1) ? t.vt[s1].x : 0;
         if (out_rv64) out_rv64[i] = v0, out_rv64[i + 1] = v1;
         if (out_rv32) out_rv32[i] = v0, out_rv32[i + 1] = v1;
@@ -80,7 +81,7 @@ __device__ void pool_general(const DevTable& t, const uint32_t* __restrict__ slo
       else for (int k = 0; k < V; ++k) r0[k] = 0.0f;
 #pragma unroll
       for (int k = 0; k < V; ++k) acc[k] = __dadd_rn(acc[k], static_cast<double>(r0[k]));
-      if (c == 0 && ln == 0) {
+      if (want_rv && c == 0 && ln == 0) {
         uint32_t v0 = slot_ok(t, s0) ? t.vt[s0].x : 0;
         if (out_rv64) out_rv64[i] = v0;
         if (out_rv32) out_rv32[i] = v0;

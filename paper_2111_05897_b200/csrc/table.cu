@@ -295,7 +295,7 @@ void table_destroy(Table* t) {
     t->prof.destroy();
     DevTable& d = t->d;
     void* ptrs[] = {d.ht,  d.rows, d.seen,     d.multi,    d.slot_id, d.special,
-                    d.hwm, d.ctr,  t->d_salts, t->xs.ids, t->xs.rv,  t->xs.bad};
+                    d.hwm, d.ctr,  t->d_salts, t->xs.ids, t->xs.rv,  t->xs.off};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (t->h_ctr) cudaFreeHost(t->h_ctr);
@@ -335,6 +335,12 @@ void check_flags(Table* t, cudaStream_t st, bool divergence) {
     throw Error(HPS_E_CONFIG,
                 "embedding table capacity exhausted (" + std::to_string(t->cfg.capacity) +
                     " rows); device tables do not evict -- raise capacity");
+  if (t->h_ctr[kCtrProtocol]) {
+    HPS_CUDA(cudaMemsetAsync(t->d.ctr + kCtrProtocol, 0, sizeof(unsigned long long), st));
+    HPS_CUDA(cudaStreamSynchronize(st));
+    throw Error(HPS_E_PROTOCOL,
+                "exchange: a pair names an id outside its source's segment; nothing was applied");
+  }
   if (divergence && t->h_ctr[kCtrDivergence]) {
     HPS_CUDA(cudaMemsetAsync(t->d.ctr + kCtrDivergence, 0, sizeof(unsigned long long), st));
     HPS_CUDA(cudaStreamSynchronize(st));
@@ -624,7 +630,7 @@ uint64_t batch_pairs(Batch& b) {
 // ---- PS surface ------------------------------------------------------------------------
 
 void table_lookup(Table* t, const uint64_t* ids, uint64_t n, float* out_values,
-                  uint64_t* out_versions, cudaStream_t st) {
+                  uint64_t* out_versions, cudaStream_t st, uint32_t flags) {
   Batch& b = t->scratch;
   batch_reserve(b, n, 0, 0);
   Stager stg(t->stage);
@@ -637,7 +643,7 @@ void table_lookup(Table* t, const uint64_t* ids, uint64_t n, float* out_values,
   launch_gather(t->d, b.slot, n, d_out, d_ver, st);
   b.registered = false;
   stg.finish(st);
-  check_flags(t, st, false);
+  if (!(flags & HPS_ASYNC)) check_flags(t, st, false);
 }
 
 void table_peek(Table* t, const uint64_t* ids, uint64_t n, float* out_w, float* out_acc,

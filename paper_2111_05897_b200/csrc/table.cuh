@@ -32,6 +32,7 @@ enum CounterIdx : int {
   kCtrNeedExact = 5,   // per-call: bound check inconclusive -> exact dry run
   kCtrMaxDelay = 6,
   kCtrDelayHist = 7,   // 17 words: delays 0..15, >=16
+  kCtrProtocol = 24,   // sticky until reported: malformed exchange input (exchange.cu)
   kCtrStep = 30,       // HPS_DEVICE_STEP counter (low 32 bits used)
   kCtrScratch = 31,    // per-call scratch (pair counts)
   kCtrCount = 32
@@ -175,8 +176,8 @@ constexpr uint32_t kMaxWorld = 32;
 struct XScratch {
   uint64_t* ids = nullptr;
   uint64_t* rv = nullptr;
-  uint32_t* bad = nullptr;
-  uint64_t cap_ids = 0, cap_rv = 0;
+  uint32_t* off = nullptr;
+  uint64_t cap_ids = 0, cap_rv = 0, cap_off = 0;
 };
 
 struct Table {

@@ -68,7 +68,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
 uint64_t batch_pairs(Batch& b);
 
 void table_lookup(Table* t, const uint64_t* ids, uint64_t n, float* out_values,
-                  uint64_t* out_versions, cudaStream_t st);
+                  uint64_t* out_versions, cudaStream_t st, uint32_t flags = 0);
 void table_peek(Table* t, const uint64_t* ids, uint64_t n, float* out_w, float* out_acc,
                 uint64_t* out_versions, uint8_t* out_present, cudaStream_t st);
 void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64_t* rv, uint64_t n,

@@ -146,6 +146,7 @@ def lib():
         "hps_table_advance_epoch": (u32, [vp]),
         "hps_table_reset": (st, [vp]),
         "hps_lookup": (st, [vp, vp, sz, vp, vp, vp]),
+        "hps_table_gather": (st, [vp, vp, sz, vp, vp, u32, vp]),
         "hps_apply": (st, [vp, vp, vp, vp, sz, f32, u32, u32, vp, C.POINTER(C.c_int), u32, vp]),
         "hps_peek": (st, [vp, vp, sz, vp, vp, vp, vp, vp]),
         "hps_batch_create": (st, [vp, i32, C.POINTER(vp)]),
@@ -164,9 +165,9 @@ def lib():
         "hps_compress_indices": (st, [vp, sz, vp, u32, u32, vp, vp, vp, vp, vp]),
         "hps_exchange_create": (st, [u32, u32, i32, i32, C.POINTER(vp)]),
         "hps_exchange_destroy": (st, [vp]),
-        "hps_exchange_route": (st, [vp, vp, sz, vp, u32, u32, vp, C.POINTER(u64), vp]),
+        "hps_exchange_route": (st, [vp, vp, sz, vp, u32, u32, vp, vp, vp]),
         "hps_exchange_pool": (st, [vp, vp, u32, vp, vp]),
-        "hps_exchange_pairs": (st, [vp, vp, u32, vp, vp, C.POINTER(u64), vp]),
+        "hps_exchange_pairs": (st, [vp, vp, u32, vp, vp, vp, vp]),
         "hps_table_apply_pairs": (st, [vp, vp, vp, C.POINTER(u64), vp, vp, C.POINTER(u64), u32,
                                        f32, u32, u32, C.POINTER(C.c_int), u32, vp]),
     }

@@ -62,15 +62,15 @@ class DeviceOps:
         return self.torch.cuda.current_stream().cuda_stream
 
     def route(self, ids, offsets, B: int, F: int):
+        """-> (send_ids buffer [>= U], per-owner counts as a device tensor [world])."""
         t = self.torch
         n = ids.numel()
         send = t.empty(max(n, 1), dtype=t.int64, device=self.device)
-        counts = (C.c_uint64 * self.world)()
+        counts = t.empty(self.world, dtype=t.int64, device=self.device)
         hps.check(hps.lib().hps_exchange_route(self.h, ids.data_ptr(), n, offsets.data_ptr(), B,
-                                               F, send.data_ptr(), counts, self._s()),
+                                               F, send.data_ptr(), counts.data_ptr(), self._s()),
                   "exchange_route")
-        counts = [int(c) for c in counts]
-        return send[:sum(counts)], counts
+        return send, counts
 
     def lookup(self, recv_ids):
         t = self.torch
@@ -78,8 +78,9 @@ class DeviceOps:
         rows = t.empty((n, self.D), dtype=t.float32, device=self.device)
         ver = t.empty(n, dtype=t.int64, device=self.device)
         if n:
-            self.table.lookup(recv_ids, out_values=rows, out_versions=ver,
-                              stream=self.torch.cuda.current_stream())
+            hps.check(hps.lib().hps_table_gather(self.table.h, recv_ids.data_ptr(), n,
+                                                 rows.data_ptr(), ver.data_ptr(), hps.ASYNC,
+                                                 self._s()), "owner lookup")
         return rows, ver
 
     def pool(self, rows, B: int, F: int, out=None):
@@ -91,18 +92,16 @@ class DeviceOps:
         return out
 
     def pairs(self, grads, n_ids: int):
+        """-> (pair_pos buffer, contribution buffer, per-owner pair counts on the device)."""
         t = self.torch
         grads = grads.contiguous()
         pos = t.empty(max(n_ids, 1), dtype=t.int32, device=self.device)
         con = t.empty((max(n_ids, 1), self.D), dtype=t.float32, device=self.device)
-        counts = (C.c_uint64 * self.world)()
+        counts = t.empty(self.world, dtype=t.int64, device=self.device)
         hps.check(hps.lib().hps_exchange_pairs(self.h, grads.data_ptr(), self.D, pos.data_ptr(),
-                                               con.data_ptr(), counts, self._s()),
+                                               con.data_ptr(), counts.data_ptr(), self._s()),
                   "exchange_pairs")
-        counts = [int(c) for c in counts]
-        self.last_pair_counts = counts
-        P = sum(counts)
-        return pos[:P], con[:P], counts
+        return pos, con, counts
 
     def apply_pairs(self, recv_ids, recv_versions, id_counts, pair_pos, contrib, pair_counts,
                     lr: float, step_tag: int, epoch: int, flags: int = 0) -> bool:
@@ -140,16 +139,20 @@ class ShardedEmbeddingWorker:
 
     # -- collectives ------------------------------------------------------------------
     def _exchange_counts(self, counts):
-        """counts[d] = what this rank sends to d -> what each source sends to this rank."""
-        if self.world == 1:
-            return list(counts)
+        """counts[d] = what this rank sends to d (list or tensor) -> (send counts, what each
+        source sends to this rank), both host lists; one device->host copy."""
         import torch
 
+        if self.world == 1:
+            c = [int(x) for x in (counts.tolist() if torch.is_tensor(counts) else counts)]
+            return c, c
         dev = self._comm_device()
-        send = torch.tensor(counts, dtype=torch.int64, device=dev)
+        send = counts.to(dev) if torch.is_tensor(counts) else \
+            torch.tensor(counts, dtype=torch.int64, device=dev)
         recv = torch.empty_like(send)
         self.dist.all_to_all_single(recv, send, group=self.group)
-        return [int(x) for x in recv.cpu()]
+        both = torch.cat([send, recv]).tolist()
+        return [int(x) for x in both[:self.world]], [int(x) for x in both[self.world:]]
 
     def _a2a(self, inp, send_counts, recv_counts):
         if self.world == 1:
@@ -172,9 +175,10 @@ class ShardedEmbeddingWorker:
     def register_batch(self, ids, offsets, B: int, F: int):
         """Route the batch's ids to their owners and fetch the rows (fetch_rows)."""
         self.B, self.F, self.n_ids = B, F, ids.numel()
-        send_ids, self.send_counts = self.ops.route(ids, offsets, B, F)
-        self.recv_counts = self._exchange_counts(self.send_counts)
-        self.recv_ids = self._a2a(send_ids, self.send_counts, self.recv_counts)
+        send_ids, counts = self.ops.route(ids, offsets, B, F)
+        self.send_counts, self.recv_counts = self._exchange_counts(counts)
+        self.recv_ids = self._a2a(send_ids[:sum(self.send_counts)], self.send_counts,
+                                  self.recv_counts)
         rows, self.recv_versions = self.ops.lookup(self.recv_ids)
         self.rows = self._a2a(rows, self.recv_counts, self.send_counts)
 
@@ -183,12 +187,15 @@ class ShardedEmbeddingWorker:
         return self.ops.pool(self.rows, self.B, self.F, out_pooled)
 
     def apply_backward(self, grads, lr: float, step_tag: int, epoch: int | None = None,
-                       flags: int = 0) -> bool:
-        """Per-sample gradients [B, F, D] -> owners, applied in ascending SampleId."""
-        pos, con, pair_counts = self.ops.pairs(grads, self.n_ids)
-        recv_pair_counts = self._exchange_counts(pair_counts)
-        rpos = self._a2a(pos, pair_counts, recv_pair_counts)
-        rcon = self._a2a(con, pair_counts, recv_pair_counts)
+                       flags: int = hps.ASYNC) -> bool:
+        """Per-sample gradients [B, F, D] -> owners, applied in ascending SampleId.
+        Data-dependent errors (non-finite contributions, capacity) surface from
+        ``table.sync()`` unless flags = 0."""
+        pos, con, counts = self.ops.pairs(grads, self.n_ids)
+        self.pair_counts, recv_pair_counts = self._exchange_counts(counts)
+        P = sum(self.pair_counts)
+        rpos = self._a2a(pos[:P], self.pair_counts, recv_pair_counts)
+        rcon = self._a2a(con[:P], self.pair_counts, recv_pair_counts)
         e = self.table.epoch() if epoch is None else epoch
         return self.ops.apply_pairs(self.recv_ids, self.recv_versions, self.recv_counts, rpos,
                                     rcon, recv_pair_counts, lr, step_tag, e, flags)

@@ -99,6 +99,7 @@ def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, ag
             assert ok2
         if use_device:
             torch.cuda.synchronize()
+            table.sync()  # deferred (HPS_ASYNC) errors of the steps surface here
         mine = np.array(sorted(i for i in seen
                                if hps.route_shard(i, S) % world == rank), np.uint64)
         w, a, v, p = owner_peek(mine)
