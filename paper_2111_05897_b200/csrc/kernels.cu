@@ -229,24 +229,65 @@ void launch_lazy_init(const DevTable& t, const uint32_t* new_slots, const uint32
 
 // ---- gather (PsShard::lookup) / peek ---------------------------------------------------
 
-__global__ void gather_kernel(DevTable t, const uint32_t* __restrict__ slots, uint64_t n,
-                              float* __restrict__ out, uint64_t* __restrict__ out_ver) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
-    uint32_t s = slots[i];
-    bool ok = slot_ok(t, s);
-    const float* row = t.rows + static_cast<uint64_t>(ok ? s : 0) * t.stride;
-    for (uint32_t d = lane; d < t.D; d += 32) out[i * t.D + d] = ok ? row[d] : 0.0f;
-    if (out_ver && lane == 0) out_ver[i] = ok ? t.vt[s].x : 0;
+// One row group (L lanes x V floats, 128-bit accesses) per id, kGatherILP ids in flight
+// per group: slot -> row + header are two dependent round trips per id.
+constexpr int kGatherILP = 2;
+
+template <int V, int L, bool kGuard>
+__global__ void __launch_bounds__(256)
+    gather_kernel(DevTable t, const uint32_t* __restrict__ slots, uint64_t n,
+                  float* __restrict__ out, uint64_t* __restrict__ out_ver) {
+  using G = Geo<V, L, kGuard>;
+  const int ln = G::lane();
+  const uint32_t D = t.D;
+  const uint64_t groups = G::groups();
+  for (uint64_t i0 = G::group(); i0 < n; i0 += groups * kGatherILP) {
+    uint32_t s[kGatherILP];
+#pragma unroll
+    for (int u = 0; u < kGatherILP; ++u) {
+      const uint64_t i = i0 + u * groups;
+      s[u] = i < n ? slots[i] : kInvalidSlot;
+    }
+    if constexpr (!kGuard) {
+      float r[kGatherILP][V];
+      uint32_t ver[kGatherILP];
+#pragma unroll
+      for (int u = 0; u < kGatherILP; ++u) {
+        const bool ok = slot_ok(t, s[u]);
+        if (ok) load_vec<V>(t.rows + static_cast<uint64_t>(s[u]) * t.stride + ln * V, r[u]);
+        else for (int k = 0; k < V; ++k) r[u][k] = 0.0f;
+        ver[u] = (out_ver && ok && ln == 0) ? t.vt[s[u]].x : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kGatherILP; ++u) {
+        const uint64_t i = i0 + u * groups;
+        if (i >= n) continue;
+        store_vec_cs<V>(out + i * D + ln * V, r[u]);
+        if (out_ver && ln == 0) out_ver[i] = ver[u];
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kGatherILP; ++u) {
+        const uint64_t i = i0 + u * groups;
+        if (i >= n) continue;
+        const bool ok = slot_ok(t, s[u]);
+        const float* row = t.rows + static_cast<uint64_t>(ok ? s[u] : 0) * t.stride;
+        for (uint32_t d = ln; d < D; d += L) out[i * D + d] = ok ? row[d] : 0.0f;
+        if (out_ver && ln == 0) out_ver[i] = ok ? t.vt[s[u]].x : 0;
+      }
+    }
   }
 }
 
 void launch_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* out,
                    uint64_t* out_ver, cudaStream_t st) {
   if (!n) return;
-  gather_kernel<<<std::min<uint64_t>(ceil_div(n, 8), 148 * 32), 256, 0, st>>>(t, slots, n, out,
-                                                                               out_ver);
+  HPS_DISPATCH_DIM(t.D, {
+    const uint64_t per_block = (256 / L) * kGatherILP;
+    const uint32_t blocks = static_cast<uint32_t>(
+        std::min<uint64_t>(ceil_div(n, per_block), 148ull * 48));
+    gather_kernel<V, L, G><<<blocks, 256, 0, st>>>(t, slots, n, out, out_ver);
+  });
   HPS_LAUNCH_CHECK();
 }
 

@@ -364,9 +364,14 @@ void table_reset(Table* t) {
 
 // ---- batch workspace --------------------------------------------------------------------
 
+// Buffers grow with 25% slack: batch sizes that vary from call to call (exchange
+// receive sides) must not reallocate -- and synchronise the device -- every step.
+static inline uint64_t with_slack(uint64_t n) { return n + n / 4 + 1024; }
+
 void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
   uint64_t n = std::max<uint64_t>(N, 1);
   if (n > b.cap_N) {
+    n = with_slack(n);
     uint64_t c = 0;
     uint32_t** bufs[] = {&b.lgrp, &b.slot,   &b.keys_a,   &b.vals_a,
                          &b.keys_b, &b.vals_b, &b.rv,   &b.new_slots};
@@ -388,10 +393,12 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
   }
   if (BF + 1 > b.cap_BF) {
     uint64_t c = 0;
+    BF = with_slack(BF);
     ensure(b.offsets, c, BF + 1);
     b.cap_BF = BF + 1;
   }
   if (B > b.cap_B) {
+    B = with_slack(B);
     uint64_t c = 0;
     ensure(b.skeys_a, c, B);
     c = 0;

@@ -92,13 +92,15 @@ struct XBatch {
   uint32_t G = 1, S = 1;
   int agg = HPS_MEAN;
   uint32_t B = 0, F = 0;
-  uint64_t N = 0, U = 0, P = 0;
-  bool pooled_ready = false;
-  uint64_t* hkeys = nullptr;
-  uint32_t* hidx = nullptr;
-  uint32_t* hval = nullptr;
-  uint8_t* dest = nullptr;
-  uint32_t* sendpos = nullptr;
+  uint64_t N = 0;
+  int lbits = 1;
+  uint64_t* hkeys = nullptr;    // transient distinct-id set [H+1]
+  uint32_t* hidx = nullptr;     // [N] listing -> set entry | inserter bit
+  uint32_t* hval = nullptr;     // [H+1] entry -> index in its owner's segment
+  uint8_t* hmul = nullptr;      // [H+1] entry listed more than once
+  uint8_t* dest = nullptr;      // [N] owner rank per listing
+  uint32_t* sendpos = nullptr;  // [N] listing -> position in send_ids
+  uint32_t* spair = nullptr;    // [N] single pair index within its owner, or ~0
   uint32_t* offsets = nullptr;
   uint32_t* lgrp = nullptr;
   uint32_t *keys_a = nullptr, *vals_a = nullptr, *keys_b = nullptr, *vals_b = nullptr;
@@ -108,10 +110,13 @@ struct XBatch {
   uint32_t* seg = nullptr;
   uint8_t* dest_of_pos = nullptr;
   uint64_t* pair_off = nullptr;
+  uint32_t* mstart = nullptr;
+  unsigned long long* mkeys = nullptr;
+  uint32_t *sm_pos = nullptr, *sm_list = nullptr;
   uint64_t* h_buf = nullptr;
-  uint64_t cap_H = 0, cap_hidx = 0, cap_hval = 0, cap_dest = 0, cap_sendpos = 0, cap_off = 0,
-           cap_lgrp = 0, cap_ka = 0, cap_va = 0, cap_kb = 0, cap_vb = 0, cap_scratch = 0,
-           cap_head = 0, cap_ex = 0, cap_tsum = 0, cap_dop = 0;
+  uint64_t cap_H = 0, cap_hidx = 0, cap_hval = 0, cap_hmul = 0, cap_dest = 0, cap_sendpos = 0,
+           cap_spair = 0, cap_off = 0, cap_lgrp = 0, cap_ka = 0, cap_va = 0, cap_kb = 0,
+           cap_vb = 0, cap_scratch = 0, cap_head = 0, cap_ex = 0, cap_tsum = 0, cap_dop = 0;
   ~XBatch();
 };
 void xbatch_init(XBatch& x);

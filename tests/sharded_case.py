@@ -44,7 +44,7 @@ def local_part(ids, offs, W, B, F, r):
 
 
 def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, agg="mean",
-             opt="adagrad", q=None):
+             opt="adagrad", space=60, q=None):
     try:
         import torch
         import torch.distributed as dist
@@ -76,7 +76,7 @@ def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, ag
             owner_peek = local.peek
         seen = set()
         for s in range(steps):
-            gids, goffs, _ = global_batch(s, world, B, F, 60)
+            gids, goffs, _ = global_batch(s, world, B, F, space)
             rng = np.random.default_rng(500 + s)
             g_all = (rng.standard_normal((world * B, F, D)) * 0.3).astype(np.float32)
             sk = np.array([((i % world) << 56) | (i // world) for i in range(world * B)],

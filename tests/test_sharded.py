@@ -32,6 +32,14 @@ def test_sharded_device_world1():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("D", [64, 5])
+def test_sharded_device_world1_large_plan(D):
+    """More than 4096 listings of repeated ids: the device-gated radix-sort path."""
+    res = run_world(1, "nccl", use_device=True, B=1500, F=4, D=D, space=2500, steps=2)
+    assert res[0][1] == "ok", res[0][1]
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("agg,opt", [("mean", "adagrad"), ("sum", "sgd")])
 def test_sharded_device_world2(agg, opt):
     import torch
@@ -39,5 +47,16 @@ def test_sharded_device_world2(agg, opt):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     res = run_world(2, "nccl", use_device=True, agg=agg, opt=opt)
+    for r, status, n in res:
+        assert status == "ok", status
+
+
+@pytest.mark.gpu
+def test_sharded_device_world2_large_plan():
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = run_world(2, "nccl", use_device=True, B=800, F=4, D=16, space=2000, steps=2)
     for r, status, n in res:
         assert status == "ok", status
