@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--soak-seconds", type=float, default=2.0)
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
+    p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                   help="N > 1: NVLink peer writes (p2p) or NCCL all-to-alls")
     return p.parse_args()
 
 
@@ -235,7 +237,8 @@ def run_sharded(args, world, rank, local, dev):
     grads = [((torch.rand((B, F, D), generator=gen, device=dev) * 2 - 1) * cfg.grad_scale)
              for _ in range(M)]
     pooled = torch.empty((B, F, D), dtype=torch.float32, device=dev)
-    ew = ShardedEmbeddingWorker(table, hps.MEAN)
+    max_n = max(b[2] for b in batches)
+    ew = ShardedEmbeddingWorker(table, hps.MEAN, transport=args.transport, max_ids=max_n)
     tag = [0]
 
     def step(i):
@@ -259,12 +262,13 @@ def run_sharded(args, world, rank, local, dev):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    x_ids = x_rows = x_pairs = 0
+    x_ids = x_pairs = 0
     for _ in range(args.steps):
         step(it)
         it += 1
-        x_ids += sum(c for d, c in enumerate(ew.send_counts) if d != rank)
-        x_pairs += sum(c for d, c in enumerate(ew.pair_counts) if d != rank)
+        if args.transport == "nccl":
+            x_ids += sum(c for d, c in enumerate(ew.send_counts) if d != rank)
+            x_pairs += sum(c for d, c in enumerate(ew.pair_counts) if d != rank)
     e1.record(stream)
     dist.barrier()
     torch.cuda.synchronize()
@@ -284,8 +288,11 @@ def run_sharded(args, world, rank, local, dev):
 
     # off-rank bytes each GPU sends per step (ids out + rows back + pairs out) ~ NVLink
     N_avg = float(np.mean([b[2] for b in batches]))
-    U_avg = float(x_ids) / args.steps  # distinct ids this rank sent off-rank per step
-    P_avg = float(x_pairs) / args.steps
+    if args.transport == "nccl":
+        U_avg = float(x_ids) / args.steps  # distinct ids this rank sent off-rank per step
+        P_avg = float(x_pairs) / args.steps
+    else:  # one-hot over >= 125M rows per GPU: ~every listing distinct, uniform owners
+        U_avg = P_avg = N_avg * (world - 1) / world
     nvl_bytes = 8 * U_avg + 4 * D * U_avg + (4 + 4 * D) * P_avg
     O_ = D
     uniq = float(N_avg)  # one-hot over 125M rows per GPU: ~all listings distinct
@@ -343,7 +350,8 @@ def run_sharded(args, world, rank, local, dev):
             "config": {"workload": f"c4: per-GPU batch {B}, {F} one-hot features, "
                                    f"{rows // 1_000_000}M-row table dim {D} hash-sharded over "
                                    f"{world} GPUs ({S} logical shards), adagrad, mean pooling, "
-                                   f"staleness 0, NCCL all-to-all exchange",
+                                   f"staleness 0, " + ("NVLink peer-write exchange" if
+                                   args.transport == "p2p" else "NCCL all-to-all exchange"),
                        "global_batch": B * world, "rows": rows, "dim": D, "features": F,
                        "logical_shards": S, "parallelism": f"sharded{world}",
                        "l2": "per-step footprint > L2 (126 MB); no flush"},
@@ -354,7 +362,8 @@ def run_sharded(args, world, rank, local, dev):
                          "achieved": bytes_step / (ms * 1e-3) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": bytes_step / (ms * 1e-3) / 1e9 / peak,
                          "traffic": None, "peak_source": peak_kind},
-            "nvlink": {"offrank_bytes_per_step_per_gpu": nvl_bytes,
+            "nvlink": {"transport": args.transport,
+                       "offrank_bytes_per_step_per_gpu": nvl_bytes,
                        "achieved_gbs_per_direction": nvl_bytes / (ms * 1e-3) / 1e9,
                        "frac_of_900": nvl_bytes / (ms * 1e-3) / 1e9 / 900.0},
             "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches,

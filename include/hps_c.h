@@ -228,6 +228,29 @@ hps_status hps_table_apply_pairs(hps_table* t, const uint64_t* recv_ids,
                                  uint32_t step_tag, uint32_t epoch, int* accepted,
                                  uint32_t flags, hps_stream stream);
 
+/* NVLink peer transport: the same step with every payload written once, directly into the
+ * consumer's HBM over NVLink (CUDA IPC peer mappings), and device-side barriers instead of
+ * collectives -- no NCCL on the data path, one host round trip per step (the owner's pair
+ * count before its apply). Setup, once: hps_exchange_arena allocates this rank's receive
+ * arena for batches of up to max_ids listings and returns its 64-byte IPC handle; the
+ * caller all-gathers the handles and passes them (world x 64 bytes, rank order) to
+ * hps_exchange_connect. Per step, on every rank in the same order:
+ *   hps_exchange_forward   route; ids -> owners' arenas; owners find-or-init and write the
+ *                          rows into the requesters' arenas (= fetch_rows)
+ *   hps_exchange_pool      with rows == NULL: pool from the delivered rows (= serve_pull)
+ *   hps_exchange_backward  pairs -> owners' arenas; owners apply in (source rank, sample)
+ *                          order (= apply_backward + flush_step + PsShard::apply_gradients)
+ * A peer missing a barrier for ~4 s fails the step with HPS_E_SYNC_FAILURE instead of
+ * hanging the device. */
+hps_status hps_exchange_arena(hps_exchange* x, uint64_t max_ids, uint32_t dim, void* out_handle);
+hps_status hps_exchange_connect(hps_exchange* x, uint32_t rank, const void* handles);
+hps_status hps_exchange_forward(hps_exchange* x, hps_table* t, const uint64_t* ids, size_t n_ids,
+                                const uint32_t* offsets, uint32_t B, uint32_t F,
+                                hps_stream stream);
+hps_status hps_exchange_backward(hps_exchange* x, hps_table* t, const float* grads, float lr,
+                                 uint32_t step_tag, uint32_t epoch, int* accepted,
+                                 uint32_t flags, hps_stream stream);
+
 /* ---- instrumentation (no reference counterpart) ---------------------------------------- */
 /* Kernels this library has launched in the process (proves which code ran). */
 uint64_t hps_launch_count(void);

@@ -338,7 +338,7 @@ hps_status hps_exchange_route(hps_exchange* x, const uint64_t* ids, size_t n_ids
 hps_status hps_exchange_pool(hps_exchange* x, const float* rows, uint32_t dim, float* out_pooled,
                              hps_stream stream) {
   return guarded([&] {
-    REQUIRE(x && out_pooled && (rows || x->impl.N == 0), "hps_exchange_pool: null argument");
+    REQUIRE(x && out_pooled, "hps_exchange_pool: null argument");
     std::lock_guard<std::mutex> g(x->mu);
     hps::DeviceGuard dg(x->impl.device);
     hps::xbatch_pool(x->impl, rows, dim, out_pooled, S(stream));
@@ -370,6 +370,48 @@ hps_status hps_table_apply_pairs(hps_table* t, const uint64_t* recv_ids,
     hps::DeviceGuard dg(t->impl->device);
     hps::table_apply_pairs(t->impl, recv_ids, recv_versions, id_counts, pair_pos, contrib,
                            pair_counts, world, lr, step_tag, epoch, accepted, flags, S(stream));
+  });
+}
+
+hps_status hps_exchange_arena(hps_exchange* x, uint64_t max_ids, uint32_t dim, void* out_handle) {
+  return guarded([&] {
+    REQUIRE(x && out_handle, "hps_exchange_arena: null argument");
+    std::lock_guard<std::mutex> g(x->mu);
+    hps::DeviceGuard dg(x->impl.device);
+    hps::xbatch_arena(x->impl, max_ids, dim, out_handle);
+  });
+}
+
+hps_status hps_exchange_connect(hps_exchange* x, uint32_t rank, const void* handles) {
+  return guarded([&] {
+    REQUIRE(x && handles, "hps_exchange_connect: null argument");
+    std::lock_guard<std::mutex> g(x->mu);
+    hps::DeviceGuard dg(x->impl.device);
+    hps::xbatch_connect(x->impl, rank, handles);
+  });
+}
+
+hps_status hps_exchange_forward(hps_exchange* x, hps_table* t, const uint64_t* ids, size_t n_ids,
+                                const uint32_t* offsets, uint32_t B, uint32_t F,
+                                hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(x && t && offsets && (ids || n_ids == 0), "hps_exchange_forward: null argument");
+    std::lock_guard<std::mutex> g(x->mu);
+    std::lock_guard<std::mutex> g2(t->impl->mu);
+    hps::DeviceGuard dg(x->impl.device);
+    hps::xbatch_fwd(x->impl, t->impl, ids, n_ids, offsets, B, F, S(stream));
+  });
+}
+
+hps_status hps_exchange_backward(hps_exchange* x, hps_table* t, const float* grads, float lr,
+                                 uint32_t step_tag, uint32_t epoch, int* accepted,
+                                 uint32_t flags, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(x && t && (grads || x->impl.N == 0), "hps_exchange_backward: null argument");
+    std::lock_guard<std::mutex> g(x->mu);
+    std::lock_guard<std::mutex> g2(t->impl->mu);
+    hps::DeviceGuard dg(x->impl.device);
+    hps::xbatch_bwd(x->impl, t->impl, grads, lr, step_tag, epoch, accepted, flags, S(stream));
   });
 }
 

@@ -22,6 +22,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "common.cuh"
 #include "radix_sort.cuh"
@@ -137,6 +138,11 @@ __device__ __forceinline__ void load_seg(const uint32_t* cnt, uint32_t G, uint32
   __syncthreads();
 }
 
+// Id regions of the owners (peer path): p[d] = owner d's region for this source rank.
+struct PeerIds {
+  uint64_t* p[kMaxWorld];
+};
+
 // Send position per listing, send_ids, and the composite keys (pos << lbits | listing)
 // of listings whose id is listed more than once (while they fit the small sort).
 __global__ void __launch_bounds__(kXBlock)
@@ -145,7 +151,7 @@ __global__ void __launch_bounds__(kXBlock)
                      const uint8_t* __restrict__ dest, const uint32_t* __restrict__ spair,
                      uint32_t* cnt, int lbits, uint32_t* __restrict__ sendpos,
                      uint64_t* __restrict__ send_ids, uint32_t* __restrict__ seg_out,
-                     unsigned long long* __restrict__ mkeys) {
+                     unsigned long long* __restrict__ mkeys, PeerIds pid) {
   __shared__ uint32_t seg[33];
   __shared__ uint32_t s_n, s_base;
   load_seg(cnt, G, seg);
@@ -159,9 +165,13 @@ __global__ void __launch_bounds__(kXBlock)
     bool multi = false;
     if (i < n) {
       const uint32_t code = hidx[i];
-      pos = seg[dest[i]] + hval[code & ~kInserter];
+      const uint32_t d = dest[i], j = hval[code & ~kInserter];
+      pos = seg[d] + j;
       sendpos[i] = pos;
-      if (code & kInserter) send_ids[pos] = ids[i];
+      if (code & kInserter) {
+        if (send_ids) send_ids[pos] = ids[i];
+        else pid.p[d][j] = ids[i];  // straight into owner d's id region for this rank
+      }
       multi = spair[i] == kNoPair;
       if (multi) r = atomicAdd(&s_n, 1u);
     }
@@ -234,6 +244,14 @@ __global__ void x_pair_bounds_kernel(const uint32_t* __restrict__ spos,
   }
 }
 
+// Where owner d's pairs go: contribution rows c[d][k * D ...] and positions p[d][k] for
+// k = base[d] + index -- one local buffer for all owners (NCCL path) or each owner's
+// peer-mapped receive arena (NVLink path).
+struct PairOut {
+  float* c[kMaxWorld];
+  uint32_t* p[kMaxWorld];
+};
+
 template <int V, bool GEN>
 __device__ __forceinline__ void put_row(float* dst, const float (&o)[V]) {
   if constexpr (GEN) {
@@ -252,8 +270,7 @@ __global__ void __launch_bounds__(kXBlock)
                          const uint32_t* __restrict__ sendpos, const uint32_t* __restrict__ lgrp,
                          const uint32_t* __restrict__ offsets, uint64_t n, uint32_t D, int mean,
                          const float* __restrict__ grads, const uint32_t* __restrict__ seg,
-                         const uint64_t* __restrict__ pair_off, uint32_t* __restrict__ pair_pos,
-                         float* __restrict__ contrib) {
+                         const uint64_t* __restrict__ base, PairOut po) {
   const uint32_t lane = threadIdx.x % L;
   const uint64_t groups = (uint64_t)gridDim.x * (kXBlock / L);
   for (uint64_t i = blockIdx.x * (uint64_t)(kXBlock / L) + threadIdx.x / L; i < n;
@@ -261,9 +278,9 @@ __global__ void __launch_bounds__(kXBlock)
     const uint32_t sp = spair[i];
     if (sp == kNoPair) continue;
     const uint32_t d = dest[i];
-    const uint64_t out = pair_off[d] + sp;
+    const uint64_t out = base[d] + sp;
     const uint32_t g = lgrp[i];
-    if (lane == 0) pair_pos[out] = sendpos[i] - seg[d];
+    if (lane == 0) po.p[d][out] = sendpos[i] - seg[d];
     const double scale = mean ? 1.0 / static_cast<double>(offsets[g + 1] - offsets[g]) : 1.0;
     for (uint32_t d0 = lane * V; d0 < D; d0 += L * V) {
       const float* src = grads + static_cast<uint64_t>(g) * D + d0;
@@ -276,7 +293,7 @@ __global__ void __launch_bounds__(kXBlock)
 #pragma unroll
       for (int v = 0; v < V; ++v)
         o[v] = __double2float_rn(__dadd_rn(0.0, __dmul_rn(static_cast<double>(x[v]), scale)));
-      put_row<V, GEN>(contrib + out * D + d0, o);
+      put_row<V, GEN>(po.c[d] + out * D + d0, o);
     }
   }
 }
@@ -292,9 +309,8 @@ __global__ void __launch_bounds__(kXBlock)
                         uint32_t F, uint64_t n_host, const uint32_t* __restrict__ cnt,
                         uint32_t D, int mean, const float* __restrict__ grads,
                         const uint8_t* __restrict__ dest_of_pos,
-                        const uint32_t* __restrict__ seg, const uint64_t* __restrict__ pair_off,
-                        const uint32_t* __restrict__ mstart, uint32_t* __restrict__ pair_pos,
-                        float* __restrict__ contrib) {
+                        const uint32_t* __restrict__ seg, const uint64_t* __restrict__ base,
+                        const uint32_t* __restrict__ mstart, PairOut po) {
   const uint32_t nm = cnt[kCntMulti];
   const uint64_t n = nm > radix::kSmallN ? n_host : nm;
   const uint32_t lane = threadIdx.x % L;
@@ -305,8 +321,8 @@ __global__ void __launch_bounds__(kXBlock)
     const uint32_t pos = spos[p];
     const uint32_t sample = lgrp[slist[p]] / F;
     const uint32_t d = dest_of_pos[pos];
-    const uint64_t out = pair_off[d] + cnt[kCntSingle + d] + (ex[p] - mstart[d]);
-    if (lane == 0) pair_pos[out] = pos - seg[d];
+    const uint64_t out = base[d] + cnt[kCntSingle + d] + (ex[p] - mstart[d]);
+    if (lane == 0) po.p[d][out] = pos - seg[d];
     for (uint32_t d0 = lane * V; d0 < D; d0 += L * V) {
       double acc[V];
 #pragma unroll
@@ -330,7 +346,7 @@ __global__ void __launch_bounds__(kXBlock)
       float o[V];
 #pragma unroll
       for (int v = 0; v < V; ++v) o[v] = __double2float_rn(acc[v]);
-      put_row<V, GEN>(contrib + out * D + d0, o);
+      put_row<V, GEN>(po.c[d] + out * D + d0, o);
     }
   }
 }
@@ -379,7 +395,8 @@ struct Offs {
 // batch of P one-listing samples (offsets = 0..P) in arrival order.
 __global__ void x_owner_kernel(const uint64_t* __restrict__ recv_ids,
                                const uint64_t* __restrict__ recv_versions, Offs id_off,
-                               Offs pair_off, uint32_t G, const uint32_t* __restrict__ pair_pos,
+                               Offs id_end, Offs pair_off, uint32_t G,
+                               const uint32_t* __restrict__ pair_pos,
                                uint64_t P, uint64_t* __restrict__ out_ids,
                                uint64_t* __restrict__ out_rv, uint32_t* __restrict__ out_off,
                                unsigned long long* protocol) {
@@ -390,12 +407,12 @@ __global__ void x_owner_kernel(const uint64_t* __restrict__ recv_ids,
     uint32_t r = 0;
     while (r + 1 < G && pair_off.v[r + 1] <= k) ++r;
     uint64_t idx = id_off.v[r] + pair_pos[k];
-    if (idx >= id_off.v[r + 1]) {
+    if (idx >= id_end.v[r]) {
       atomicOr(protocol, 1ull);  // gates every update kernel; reported by check_flags
       idx = id_off.v[r];
     }
-    out_ids[k] = idx < id_off.v[G] ? recv_ids[idx] : 0;
-    out_rv[k] = (recv_versions && idx < id_off.v[G]) ? recv_versions[idx] : 0;
+    out_ids[k] = idx < id_end.v[r] ? recv_ids[idx] : 0;
+    out_rv[k] = (recv_versions && idx < id_end.v[r]) ? recv_versions[idx] : 0;
   }
 }
 
@@ -419,6 +436,12 @@ void grow(T*& p, uint64_t& cap, uint64_t want) {
 
 XBatch::~XBatch() {
   DeviceGuard g(device);
+  cudaDeviceSynchronize();
+  for (uint32_t r = 0; r < G && r < kMaxWorld; ++r)
+    if (peer[r] && peer[r] != arena) cudaIpcCloseMemHandle(peer[r]);
+  if (arena) cudaFree(arena);
+  if (xbase) cudaFree(xbase);
+  if (fail) cudaFree(fail);
   void* ps[] = {hkeys,  hidx,   hval,   hmul,    dest,    sendpos, spair, offsets, lgrp,
                 keys_a, vals_a, keys_b, vals_b,  scratch, head,    ex,    tsum,    cnt,
                 seg,    dest_of_pos,    pair_off, mkeys,  mstart,  sm_pos, sm_list};
@@ -447,12 +470,16 @@ static void require_device(const void* p, const char* what) {
     throw Error(HPS_E_PRECONDITION, std::string(what) + ": device pointer required");
 }
 
-void xbatch_route(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_t* offsets, uint32_t B,
-                  uint32_t F, uint64_t* out_send_ids, uint64_t* out_counts, cudaStream_t st) {
-  require_device(ids, "hps_exchange_route ids");
-  require_device(offsets, "hps_exchange_route offsets");
-  require_device(out_send_ids, "hps_exchange_route send_ids");
-  if (n >= (1ull << 31)) throw Error(HPS_E_PRECONDITION, "hps_exchange_route: too many ids");
+// ---- shared cores of the two transports ---------------------------------------------------
+
+// Distinct ids grouped by owner: send positions, segment table, and the ids themselves
+// either into send_ids (NCCL path) or straight into each owner's id region (peer path).
+static void route_core(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_t* offsets,
+                       uint32_t B, uint32_t F, uint64_t* send_ids, const PeerIds& pid,
+                       cudaStream_t st) {
+  require_device(ids, "exchange ids");
+  require_device(offsets, "exchange offsets");
+  if (n >= (1ull << 31)) throw Error(HPS_E_PRECONDITION, "exchange: too many ids");
   const uint64_t BF = static_cast<uint64_t>(B) * F;
   x.N = n;
   x.B = B;
@@ -483,10 +510,72 @@ void xbatch_route(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_t* of
     HPS_LAUNCH_CHECK_N(2);
   }
   x_scatter_kernel<<<grid_n(std::max<uint64_t>(n, 1), x.sms), kXBlock, 0, st>>>(
-      ids, n, x.G, x.hidx, x.hval, x.dest, x.spair, x.cnt, x.lbits, x.sendpos, out_send_ids,
-      x.seg, x.mkeys);
+      ids, n, x.G, x.hidx, x.hval, x.dest, x.spair, x.cnt, x.lbits, x.sendpos, send_ids, x.seg,
+      x.mkeys, pid);
   HPS_LAUNCH_CHECK();
   launch_expand_groups(x.offsets, static_cast<uint32_t>(BF), x.lgrp, st);
+}
+
+// Pair ordering and counts up to (not including) the emit kernels: x.pair_off = owners'
+// pair offsets in a concatenated layout. Returns the sorted list (spos, slist).
+static void pairs_core(XBatch& x, const uint32_t** spos_out, const uint32_t** slist_out,
+                       cudaStream_t st) {
+  const uint64_t n = x.N;
+  grow(x.keys_a, x.cap_ka, n);
+  grow(x.vals_a, x.cap_va, n);
+  grow(x.keys_b, x.cap_kb, n);
+  grow(x.vals_b, x.cap_vb, n);
+  grow(x.scratch, x.cap_scratch, radix::scratch_words<uint32_t>(n));
+  grow(x.head, x.cap_head, n);
+  grow(x.ex, x.cap_ex, n);
+  grow(x.tsum, x.cap_tsum, ceil_div(n, 4096) + 2);
+  grow(x.dest_of_pos, x.cap_dop, n);
+  const uint32_t* n_multi = x.cnt + kCntMulti;
+  // small path: rank sort of the multi listings' composite keys (no-op when large)
+  radix::sort_composite_small(x.mkeys, n_multi, x.lbits, x.sm_pos, x.sm_list, st);
+  // large path: stable radix sort of every listing by send position (no-op when small)
+  const bool in_b = radix::sort_pairs<uint32_t>(x.keys_a, x.vals_a, x.keys_b, x.vals_b, n,
+                                                x.lbits, x.scratch, st, x.sms, n_multi,
+                                                x.sendpos, true);
+  uint32_t* spos = in_b ? x.keys_b : x.keys_a;
+  uint32_t* slist = in_b ? x.vals_b : x.vals_a;
+  x_pick_small_kernel<<<ceil_div(radix::kSmallN, kXBlock), kXBlock, 0, st>>>(
+      n_multi, x.sm_pos, x.sm_list, spos, slist);
+  x_pair_flags_kernel<<<grid_n(n, x.sms), kXBlock, 0, st>>>(spos, slist, x.lgrp, x.spair, x.F,
+                                                            n, n_multi, x.head);
+  exclusive_scan(x.head, x.ex, n, x.tsum, x.tsum + ceil_div(n, 4096), st);
+  x_dest_of_pos_kernel<<<grid_n(n, x.sms), kXBlock, 0, st>>>(x.seg, x.G, n, x.dest_of_pos);
+  x_pair_bounds_kernel<<<1, 64, 0, st>>>(spos, x.ex, x.head, n, x.cnt, x.seg, x.G, x.pair_off,
+                                         x.mstart);
+  HPS_LAUNCH_CHECK_N(4);
+  *spos_out = spos;
+  *slist_out = slist;
+}
+
+static void emit_pairs(XBatch& x, const float* grads, uint32_t D, const uint32_t* spos,
+                       const uint32_t* slist, const uint64_t* base, const PairOut& po,
+                       cudaStream_t st) {
+  const uint64_t n = x.N;
+  const int mean = x.agg == HPS_MEAN ? 1 : 0;
+  HPS_DISPATCH_DIM(D, {
+    const uint32_t blocks = static_cast<uint32_t>(std::max<uint64_t>(
+        1, std::min<uint64_t>(ceil_div(n, kXBlock / L), uint64_t(x.sms) * 16)));
+    x_single_emit_kernel<V, L, G><<<blocks, kXBlock, 0, st>>>(
+        x.spair, x.dest, x.sendpos, x.lgrp, x.offsets, n, D, mean, grads, x.seg, base, po);
+    x_multi_emit_kernel<V, L, G><<<blocks, kXBlock, 0, st>>>(
+        spos, slist, x.head, x.ex, x.lgrp, x.offsets, x.F, n, x.cnt, D, mean, grads,
+        x.dest_of_pos, x.seg, base, x.mstart, po);
+  });
+  HPS_LAUNCH_CHECK_N(2);
+}
+
+// ---- NCCL transport (the caller moves the buffers) -------------------------------------
+
+void xbatch_route(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_t* offsets, uint32_t B,
+                  uint32_t F, uint64_t* out_send_ids, uint64_t* out_counts, cudaStream_t st) {
+  require_device(out_send_ids, "hps_exchange_route send_ids");
+  if (n && !out_send_ids) throw Error(HPS_E_PRECONDITION, "hps_exchange_route: null send_ids");
+  route_core(x, ids, n, offsets, B, F, out_send_ids, PeerIds{}, st);
   if (is_device_ptr(out_counts)) {  // stays on the device: no host round trip
     x_counts_kernel<<<1, 32, 0, st>>>(x.cnt, nullptr, x.G, out_counts);
     HPS_LAUNCH_CHECK();
@@ -499,9 +588,11 @@ void xbatch_route(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_t* of
 }
 
 void xbatch_pool(XBatch& x, const float* rows, uint32_t D, float* out_pooled, cudaStream_t st) {
+  if (!rows) rows = x.arena_rows;  // peer path: the owners delivered into the arena
   require_device(rows, "hps_exchange_pool rows");
   require_device(out_pooled, "hps_exchange_pool out");
   if (!D) throw Error(HPS_E_PRECONDITION, "hps_exchange_pool: dim must be positive");
+  if (x.N && !rows) throw Error(HPS_E_PRECONDITION, "hps_exchange_pool: no rows");
   DevTable view{};
   view.rows = const_cast<float*>(rows);
   view.D = D;
@@ -523,8 +614,7 @@ void xbatch_pairs(XBatch& x, const float* grads, uint32_t D, uint32_t* out_pair_
   require_device(out_pair_pos, "hps_exchange_pairs pair_pos");
   require_device(out_contrib, "hps_exchange_pairs contrib");
   if (!D) throw Error(HPS_E_PRECONDITION, "hps_exchange_pairs: dim must be positive");
-  const uint64_t n = x.N;
-  if (n == 0) {
+  if (x.N == 0) {
     if (is_device_ptr(out_pair_counts)) {
       HPS_CUDA(cudaMemsetAsync(out_pair_counts, 0, x.G * sizeof(uint64_t), st));
     } else {
@@ -532,48 +622,11 @@ void xbatch_pairs(XBatch& x, const float* grads, uint32_t D, uint32_t* out_pair_
     }
     return;
   }
-  grow(x.keys_a, x.cap_ka, n);
-  grow(x.vals_a, x.cap_va, n);
-  grow(x.keys_b, x.cap_kb, n);
-  grow(x.vals_b, x.cap_vb, n);
-  grow(x.scratch, x.cap_scratch, radix::scratch_words<uint32_t>(n));
-  grow(x.head, x.cap_head, n);
-  grow(x.ex, x.cap_ex, n);
-  grow(x.tsum, x.cap_tsum, ceil_div(n, 4096) + 2);
-  grow(x.dest_of_pos, x.cap_dop, n);
-  const uint32_t* n_multi = x.cnt + kCntMulti;
-  // small path: rank sort of the multi listings' composite keys (no-op when large)
-  radix::sort_composite_small(x.mkeys, n_multi, x.lbits, x.sm_pos, x.sm_list, st);
-  // large path: stable radix sort of every listing by send position (no-op when small)
-  const bool in_b = radix::sort_pairs<uint32_t>(x.keys_a, x.vals_a, x.keys_b, x.vals_b, n,
-                                                x.lbits, x.scratch, st, x.sms, n_multi,
-                                                x.sendpos, true);
-  // Both paths write the same buffers downstream; the kernels pick by the device count.
-  // The small path's results are copied over the large path's output buffers' heads.
-  uint32_t* spos = in_b ? x.keys_b : x.keys_a;
-  uint32_t* slist = in_b ? x.vals_b : x.vals_a;
-  x_pick_small_kernel<<<ceil_div(radix::kSmallN, kXBlock), kXBlock, 0, st>>>(
-      n_multi, x.sm_pos, x.sm_list, spos, slist);
-  const uint64_t nh = n;  // host bound of the live list
-  x_pair_flags_kernel<<<grid_n(nh, x.sms), kXBlock, 0, st>>>(spos, slist, x.lgrp, x.spair, x.F,
-                                                             nh, n_multi, x.head);
-  exclusive_scan(x.head, x.ex, nh, x.tsum, x.tsum + ceil_div(nh, 4096), st);
-  x_dest_of_pos_kernel<<<grid_n(n, x.sms), kXBlock, 0, st>>>(x.seg, x.G, n, x.dest_of_pos);
-  x_pair_bounds_kernel<<<1, 64, 0, st>>>(spos, x.ex, x.head, nh, x.cnt, x.seg, x.G, x.pair_off,
-                                         x.mstart);
-  HPS_LAUNCH_CHECK_N(4);
-  const int mean = x.agg == HPS_MEAN ? 1 : 0;
-  HPS_DISPATCH_DIM(D, {
-    const uint32_t blocks = static_cast<uint32_t>(std::max<uint64_t>(
-        1, std::min<uint64_t>(ceil_div(n, kXBlock / L), uint64_t(x.sms) * 16)));
-    x_single_emit_kernel<V, L, G><<<blocks, kXBlock, 0, st>>>(
-        x.spair, x.dest, x.sendpos, x.lgrp, x.offsets, n, D, mean, grads, x.seg, x.pair_off,
-        out_pair_pos, out_contrib);
-    x_multi_emit_kernel<V, L, G><<<blocks, kXBlock, 0, st>>>(
-        spos, slist, x.head, x.ex, x.lgrp, x.offsets, x.F, nh, x.cnt, D, mean, grads,
-        x.dest_of_pos, x.seg, x.pair_off, x.mstart, out_pair_pos, out_contrib);
-  });
-  HPS_LAUNCH_CHECK_N(2);
+  const uint32_t *spos, *slist;
+  pairs_core(x, &spos, &slist, st);
+  PairOut po{};
+  for (uint32_t d = 0; d < x.G; ++d) po.c[d] = out_contrib, po.p[d] = out_pair_pos;
+  emit_pairs(x, grads, D, spos, slist, x.pair_off, po, st);
   if (is_device_ptr(out_pair_counts)) {
     x_counts_kernel<<<1, 32, 0, st>>>(nullptr, x.pair_off, x.G, out_pair_counts);
     HPS_LAUNCH_CHECK();
@@ -585,20 +638,13 @@ void xbatch_pairs(XBatch& x, const float* grads, uint32_t D, uint32_t* out_pair_
   for (uint32_t d = 0; d < x.G; ++d) out_pair_counts[d] = x.h_buf[d + 1] - x.h_buf[d];
 }
 
-void table_apply_pairs(Table* t, const uint64_t* recv_ids, const uint64_t* recv_versions,
-                       const uint64_t* id_counts, const uint32_t* pair_pos, const float* contrib,
-                       const uint64_t* pair_counts, uint32_t G, float lr, uint32_t step_tag,
-                       uint32_t epoch, int* accepted, uint32_t flags, cudaStream_t st) {
-  require_device(recv_ids, "hps_table_apply_pairs recv_ids");
-  require_device(recv_versions, "hps_table_apply_pairs recv_versions");
-  require_device(pair_pos, "hps_table_apply_pairs pair_pos");
-  require_device(contrib, "hps_table_apply_pairs contrib");
-  if (G == 0 || G > kMaxWorld) throw Error(HPS_E_PRECONDITION, "apply_pairs: bad world size");
-  Offs io{}, po{};
-  for (uint32_t r = 0; r < G; ++r) {
-    io.v[r + 1] = io.v[r] + id_counts[r];
-    po.v[r + 1] = po.v[r] + pair_counts[r];
-  }
+// Owner side, shared by both transports: pairs (source-rank major) -> a batch of P
+// one-listing samples applied through the batch plan.
+static void owner_apply(Table* t, const uint64_t* recv_ids, const uint64_t* recv_versions,
+                        const Offs& io, const Offs& ie, const Offs& po, uint32_t G,
+                        const uint32_t* pair_pos, const float* contrib, float lr,
+                        uint32_t step_tag, uint32_t epoch, int* accepted, uint32_t flags,
+                        cudaStream_t st) {
   const uint64_t P = po.v[G];
   if (P >= 0xffffffffull) throw Error(HPS_E_PRECONDITION, "apply_pairs: too many pairs");
   XScratch& xs = t->xs;
@@ -606,7 +652,7 @@ void table_apply_pairs(Table* t, const uint64_t* recv_ids, const uint64_t* recv_
   grow(xs.rv, xs.cap_rv, P);
   grow(xs.off, xs.cap_off, P + 1);
   x_owner_kernel<<<grid_n(P + 1, t->sm_count), kXBlock, 0, st>>>(
-      recv_ids, recv_versions, io, po, G, pair_pos, P, xs.ids, xs.rv, xs.off,
+      recv_ids, recv_versions, io, ie, po, G, pair_pos, P, xs.ids, xs.rv, xs.off,
       t->d.ctr + kCtrProtocol);
   HPS_LAUNCH_CHECK();
   // The pairs as a batch of P one-listing samples, sum aggregation: each contribution is
@@ -618,6 +664,298 @@ void table_apply_pairs(Table* t, const uint64_t* recv_ids, const uint64_t* recv_
   batch_register(b, xs.ids, P, xs.off, static_cast<uint32_t>(P), 1, nullptr, st);
   batch_push(b, HPS_SUM, contrib, lr, step_tag, epoch, recv_versions ? 0 : 1,
              recv_versions ? xs.rv : nullptr, accepted, flags, st);
+}
+
+void table_apply_pairs(Table* t, const uint64_t* recv_ids, const uint64_t* recv_versions,
+                       const uint64_t* id_counts, const uint32_t* pair_pos, const float* contrib,
+                       const uint64_t* pair_counts, uint32_t G, float lr, uint32_t step_tag,
+                       uint32_t epoch, int* accepted, uint32_t flags, cudaStream_t st) {
+  require_device(recv_ids, "hps_table_apply_pairs recv_ids");
+  require_device(recv_versions, "hps_table_apply_pairs recv_versions");
+  require_device(pair_pos, "hps_table_apply_pairs pair_pos");
+  require_device(contrib, "hps_table_apply_pairs contrib");
+  if (G == 0 || G > kMaxWorld) throw Error(HPS_E_PRECONDITION, "apply_pairs: bad world size");
+  Offs io{}, ie{}, po{};
+  for (uint32_t r = 0; r < G; ++r) {
+    io.v[r + 1] = io.v[r] + id_counts[r];
+    ie.v[r] = io.v[r + 1];
+    po.v[r + 1] = po.v[r] + pair_counts[r];
+  }
+  owner_apply(t, recv_ids, recv_versions, io, ie, po, G, pair_pos, contrib, lr, step_tag, epoch,
+              accepted, flags, st);
+}
+
+// ---- NVLink peer transport -------------------------------------------------------------
+// Every rank owns one arena (cudaMalloc, exported by CUDA IPC, opened by every peer):
+//   hdr      XHdr: barrier arrivals + per-source counts (written by peers)
+//   ids      [W][Nmax] u64   region r: the distinct ids source r asks this rank for
+//   rows     [Nmax][D] f32   this rank's rows, in its send order (written by the owners)
+//   ppos     [W*Nmax]  u32   pairs this rank owns, source-rank major (written by sources)
+//   contrib  [W*Nmax][D] f32
+//   oslot    [W][Nmax] u32   owner-local: slot of each received id
+//   orv      [W][Nmax] u64   owner-local: version read for it (the pairs' read version)
+//   oids     [W][Nmax] u64   owner-local copy of the id regions (sources may overwrite the
+//   ocnt     [W] u32         regions and counts with the next step once this one's last
+//                            barrier is passed, while the owner still applies)
+// A step writes every payload once, directly into the consumer's HBM over NVLink; the
+// only synchronisation is a device-side barrier through the hdr flags.
+
+struct PeerHdrs {
+  XHdr* h[kMaxWorld];
+};
+struct PeerRows {
+  float* p[kMaxWorld];
+};
+
+constexpr long long kBarrierTimeoutCycles = 8'000'000'000ll;  // ~4 s: never hang the GPU
+
+// All ranks: arrive (release, system scope) at every peer, then wait (acquire) for
+// every peer's arrival at this rank. A peer that never arrives trips the timeout, which
+// flags the table (updates are gated off) and surfaces as HPS_E_SYNC_FAILURE.
+__global__ void x_barrier_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
+                                 unsigned long long epoch, unsigned long long* fail) {
+  const uint32_t t = threadIdx.x;
+  __threadfence_system();
+  __syncthreads();
+  if (t < W) {
+    unsigned long long* f = &ph.h[t]->bar[rank];
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
+  }
+  if (t < W) {
+    const unsigned long long* f = &ph.h[rank]->bar[t];
+    const long long t0 = clock64();
+    while (true) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if (v >= epoch) break;
+      if (clock64() - t0 > kBarrierTimeoutCycles) {
+        atomicExch(&ph.h[rank]->err, 1u);
+        atomicOr(fail, 1ull);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+__global__ void x_fwd_hdr_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
+                                 const uint32_t* __restrict__ cnt,
+                                 const uint32_t* __restrict__ seg) {
+  const uint32_t d = threadIdx.x;
+  if (d < W) {
+    ph.h[d]->fwd_cnt[rank] = cnt[d];
+    ph.h[d]->fwd_seg[rank] = seg[d];
+  }
+}
+
+__global__ void x_bwd_hdr_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
+                                 const uint64_t* __restrict__ pair_off) {
+  const uint32_t d = threadIdx.x;
+  if (d < W) ph.h[d]->bwd_cnt[rank] = static_cast<uint32_t>(pair_off[d + 1] - pair_off[d]);
+}
+
+// Where this rank's pairs start in each owner's (source-rank major) pair arrays.
+__global__ void x_bwd_base_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
+                                  uint64_t* __restrict__ base) {
+  const uint32_t d = threadIdx.x;
+  if (d < W) {
+    uint64_t b = 0;
+    for (uint32_t r = 0; r < rank; ++r) b += ld_volatile(&ph.h[d]->bwd_cnt[r]);
+    base[d] = b;
+  }
+}
+
+// Owner: the rows (and versions) of the ids source r asked for, written straight into
+// source r's rows buffer at its segment for this owner.
+template <int V, int L, bool kGuard>
+__global__ void __launch_bounds__(256)
+    x_owner_gather_kernel(DevTable t, const uint32_t* __restrict__ oslot, uint64_t stride,
+                          const XHdr* __restrict__ hdr, PeerRows pr,
+                          uint64_t* __restrict__ orv) {
+  using Gm = Geo<V, L, kGuard>;
+  const uint32_t r = blockIdx.y;
+  const uint64_t n = ld_volatile(&hdr->fwd_cnt[r]);
+  const uint64_t seg = ld_volatile(&hdr->fwd_seg[r]);
+  const uint32_t D = t.D;
+  const int ln = Gm::lane();
+  const uint64_t gid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
+  const uint64_t groups = static_cast<uint64_t>(gridDim.x) * blockDim.x / L;
+  float* dst_base = pr.p[r] + seg * D;
+  for (uint64_t j = gid; j < n; j += groups) {
+    const uint32_t s = oslot[r * stride + j];
+    const bool ok = slot_ok(t, s);
+    const float* row = t.rows + static_cast<uint64_t>(ok ? s : 0) * t.stride;
+    if constexpr (!kGuard) {
+      float v[V];
+      if (ok) load_vec<V>(row + ln * V, v);
+      else for (int k = 0; k < V; ++k) v[k] = 0.0f;
+      store_vec<V>(dst_base + j * D + ln * V, v);
+    } else {
+      for (uint32_t d = ln; d < D; d += L) dst_base[j * D + d] = ok ? row[d] : 0.0f;
+    }
+    if (ln == 0) orv[r * stride + j] = ok ? t.vt[s].x : 0;
+  }
+}
+
+static size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
+
+void xbatch_arena(XBatch& x, uint64_t max_ids, uint32_t D, void* out_handle) {
+  if (x.arena) throw Error(HPS_E_PRECONDITION, "exchange arena already created");
+  if (!max_ids || !D) throw Error(HPS_E_PRECONDITION, "exchange arena: empty");
+  const uint64_t W = x.G, M = max_ids;
+  size_t o = al256(sizeof(XHdr));
+  x.off_ids = o;     o += al256(W * M * 8);
+  x.off_rows = o;    o += al256(M * D * 4);
+  x.off_ppos = o;    o += al256(W * M * 4);
+  x.off_contrib = o; o += al256(W * M * D * 4);
+  x.off_oslot = o;   o += al256(W * M * 4);
+  x.off_orv = o;     o += al256(W * M * 8);
+  x.off_oids = o;    o += al256(W * M * 8);
+  x.off_ocnt = o;    o += al256(kMaxWorld * 4);
+  x.arena_bytes = o;
+  x.max_ids = M;
+  x.arena_dim = D;
+  HPS_CUDA(cudaMalloc(&x.arena, o));
+  HPS_CUDA(cudaMemset(x.arena, 0, al256(sizeof(XHdr))));
+  HPS_CUDA(cudaMalloc(&x.xbase, 33 * sizeof(uint64_t)));
+  HPS_CUDA(cudaMalloc(&x.fail, sizeof(unsigned long long)));
+  HPS_CUDA(cudaMemset(x.fail, 0, sizeof(unsigned long long)));
+  x.arena_rows = reinterpret_cast<float*>(x.arena + x.off_rows);
+  cudaIpcMemHandle_t h;
+  HPS_CUDA(cudaIpcGetMemHandle(&h, x.arena));
+  memcpy(out_handle, &h, sizeof(h));
+}
+
+void xbatch_connect(XBatch& x, uint32_t rank, const void* handles) {
+  if (!x.arena) throw Error(HPS_E_PRECONDITION, "exchange connect: create the arena first");
+  if (rank >= x.G) throw Error(HPS_E_PRECONDITION, "exchange connect: bad rank");
+  x.rank = rank;
+  const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+  for (uint32_t r = 0; r < x.G; ++r) {
+    if (r == rank) {
+      x.peer[r] = x.arena;
+      continue;
+    }
+    void* p = nullptr;
+    HPS_CUDA(cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess));
+    x.peer[r] = static_cast<uint8_t*>(p);
+  }
+  x.connected = true;
+}
+
+static PeerHdrs peer_hdrs(const XBatch& x) {
+  PeerHdrs ph{};
+  for (uint32_t r = 0; r < x.G; ++r) ph.h[r] = reinterpret_cast<XHdr*>(x.peer[r]);
+  return ph;
+}
+
+static void barrier(XBatch& x, cudaStream_t st) {
+  ++x.epoch;
+  x_barrier_kernel<<<1, 32, 0, st>>>(peer_hdrs(x), x.G, x.rank, x.epoch, x.fail);
+  HPS_LAUNCH_CHECK();
+}
+
+static void require_connected(const XBatch& x, uint32_t D, uint64_t n) {
+  if (!x.connected) throw Error(HPS_E_PRECONDITION, "exchange: peer transport not connected");
+  if (D != x.arena_dim) throw Error(HPS_E_PRECONDITION, "exchange: dim differs from the arena's");
+  if (n > x.max_ids) throw Error(HPS_E_PRECONDITION, "exchange: batch exceeds the arena size");
+}
+
+static void check_fail(XBatch& x, cudaStream_t st) {
+  HPS_CUDA(cudaMemcpyAsync(x.h_buf + 64, x.fail, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+  HPS_CUDA(cudaStreamSynchronize(st));
+  if (x.h_buf[64])
+    throw Error(HPS_E_SYNC_FAILURE, "exchange: a peer did not reach the barrier (timeout)");
+}
+
+void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint32_t* offsets,
+                uint32_t B, uint32_t F, cudaStream_t st) {
+  require_connected(x, t->cfg.embedding_dim, n);
+  const uint64_t M = x.max_ids;
+  PeerIds pid{};
+  for (uint32_t d = 0; d < x.G; ++d)
+    pid.p[d] = reinterpret_cast<uint64_t*>(x.peer[d] + x.off_ids) + x.rank * M;
+  route_core(x, ids, n, offsets, B, F, nullptr, pid, st);
+  const PeerHdrs ph = peer_hdrs(x);
+  x_fwd_hdr_kernel<<<1, 32, 0, st>>>(ph, x.G, x.rank, x.cnt, x.seg);
+  HPS_LAUNCH_CHECK();
+  barrier(x, st);  // every id region and count has landed
+  // owner: find-or-init the ids every source asked for, rows straight back to them
+  XHdr* mine = ph.h[x.rank];
+  uint32_t* oslot = reinterpret_cast<uint32_t*>(x.arena + x.off_oslot);
+  uint64_t* orv = reinterpret_cast<uint64_t*>(x.arena + x.off_orv);
+  Batch& b = t->scratch;
+  batch_reserve(b, x.G * M, 0, 0);
+  b.registered = false;
+  HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
+  launch_probe_regions(t->d, reinterpret_cast<const uint64_t*>(x.arena + x.off_ids), M, x.G,
+                       mine, oslot, reinterpret_cast<uint64_t*>(x.arena + x.off_oids),
+                       reinterpret_cast<uint32_t*>(x.arena + x.off_ocnt), b.new_slots,
+                       &b.small[2], t->sm_count, st);
+  launch_lazy_init(t->d, b.new_slots, &b.small[2], x.G * M, t->sm_count, st);
+  PeerRows pr{};
+  for (uint32_t r = 0; r < x.G; ++r) pr.p[r] = reinterpret_cast<float*>(x.peer[r] + x.off_rows);
+  HPS_DISPATCH_DIM(t->d.D, {
+    const uint32_t bx = static_cast<uint32_t>(std::max<uint64_t>(
+        1, std::min<uint64_t>(ceil_div(M, 256 / L), uint64_t(t->sm_count) * 16 / x.G + 1)));
+    x_owner_gather_kernel<V, L, G><<<dim3(bx, x.G), 256, 0, st>>>(t->d, oslot, M, mine, pr, orv);
+  });
+  HPS_LAUNCH_CHECK();
+  barrier(x, st);  // every owner's rows have landed in this rank's rows buffer
+}
+
+void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step_tag,
+                uint32_t epoch, int* accepted, uint32_t flags, cudaStream_t st) {
+  const uint32_t D = t->cfg.embedding_dim;
+  require_connected(x, D, x.N);
+  require_device(grads, "hps_exchange_bwd grads");
+  const uint64_t M = x.max_ids;
+  const PeerHdrs ph = peer_hdrs(x);
+  const uint32_t *spos = nullptr, *slist = nullptr;
+  if (x.N) {
+    pairs_core(x, &spos, &slist, st);
+  } else {
+    HPS_CUDA(cudaMemsetAsync(x.pair_off, 0, 33 * sizeof(uint64_t), st));
+  }
+  x_bwd_hdr_kernel<<<1, 32, 0, st>>>(ph, x.G, x.rank, x.pair_off);
+  HPS_LAUNCH_CHECK();
+  barrier(x, st);  // every owner knows how many pairs each source sends
+  x_bwd_base_kernel<<<1, 32, 0, st>>>(ph, x.G, x.rank, x.xbase);
+  HPS_LAUNCH_CHECK();
+  if (x.N) {
+    PairOut po{};
+    for (uint32_t d = 0; d < x.G; ++d) {
+      po.c[d] = reinterpret_cast<float*>(x.peer[d] + x.off_contrib);
+      po.p[d] = reinterpret_cast<uint32_t*>(x.peer[d] + x.off_ppos);
+    }
+    emit_pairs(x, grads, D, spos, slist, x.xbase, po, st);
+  }
+  barrier(x, st);  // every pair has landed at its owner
+  // owner: how many pairs arrived from each source (one host round trip), then apply
+  // (bwd_cnt is safe to read: no source can write the next step's before this rank
+  // reaches the next step's first barrier; fwd counts/ids come from the owner-local copy.)
+  XHdr* mine = ph.h[x.rank];
+  HPS_CUDA(cudaMemcpyAsync(x.h_buf, x.arena + x.off_ocnt, kMaxWorld * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, st));
+  HPS_CUDA(cudaMemcpyAsync(x.h_buf + 16, mine->bwd_cnt, kMaxWorld * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, st));
+  check_fail(x, st);  // synchronises
+  const uint32_t* hc = reinterpret_cast<const uint32_t*>(x.h_buf);
+  const uint32_t* hb = reinterpret_cast<const uint32_t*>(x.h_buf + 16);
+  Offs io{}, ie{}, po{};
+  for (uint32_t r = 0; r < x.G; ++r) {
+    io.v[r] = r * M;
+    ie.v[r] = r * M + hc[r];
+    po.v[r + 1] = po.v[r] + hb[r];
+  }
+  owner_apply(t, reinterpret_cast<const uint64_t*>(x.arena + x.off_oids),
+              reinterpret_cast<const uint64_t*>(x.arena + x.off_orv), io, ie, po, x.G,
+              reinterpret_cast<const uint32_t*>(x.arena + x.off_ppos),
+              reinterpret_cast<const float*>(x.arena + x.off_contrib), lr, step_tag, epoch,
+              accepted, flags, st);
 }
 
 }  // namespace hps

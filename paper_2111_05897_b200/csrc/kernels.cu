@@ -189,6 +189,37 @@ void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* 
   HPS_LAUNCH_CHECK();
 }
 
+__global__ void __launch_bounds__(256)
+    probe_regions_kernel(DevTable t, const uint64_t* __restrict__ ids, uint64_t stride,
+                         const XHdr* __restrict__ hdr, uint32_t* __restrict__ slots,
+                         uint64_t* __restrict__ ids_copy, uint32_t* __restrict__ cnt_copy,
+                         uint32_t* __restrict__ new_slots, uint32_t* __restrict__ new_count) {
+  const uint32_t r = blockIdx.y;
+  const uint64_t n = ld_volatile(&hdr->fwd_cnt[r]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt_copy[r] = static_cast<uint32_t>(n);
+  const uint64_t* rid = ids + r * stride;
+  uint32_t* rs = slots + r * stride;
+  uint64_t* rc = ids_copy + r * stride;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t id = rid[j];
+    rc[j] = id;
+    rs[j] = find_or_insert(t, id, new_slots, new_count, true);
+  }
+}
+
+void launch_probe_regions(const DevTable& t, const uint64_t* ids, uint64_t stride, uint32_t W,
+                          const XHdr* hdr, uint32_t* slots, uint64_t* ids_copy,
+                          uint32_t* cnt_copy, uint32_t* new_slots, uint32_t* new_count, int sms,
+                          cudaStream_t st) {
+  if (!stride || !W) return;
+  const uint32_t bx = static_cast<uint32_t>(
+      std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(stride, 256), (uint64_t)sms * 8 / W + 1)));
+  probe_regions_kernel<<<dim3(bx, W), 256, 0, st>>>(t, ids, stride, hdr, slots, ids_copy,
+                                                    cnt_copy, new_slots, new_count);
+  HPS_LAUNCH_CHECK();
+}
+
 // Empty index: every key kEmptyKey, every slot kPending (both all-ones).
 void launch_ht_clear(const DevTable& t, cudaStream_t st) {
   HPS_CUDA(cudaMemsetAsync(t.ht, 0xff, (t.ht_mask + 1) * sizeof(HashEntry), st));

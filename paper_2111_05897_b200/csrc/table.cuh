@@ -173,6 +173,16 @@ struct ProfScope {
 
 // Owner-side workspace of the multi-GPU exchange (exchange.cu).
 constexpr uint32_t kMaxWorld = 32;
+
+// Header of a rank's peer-mapped exchange arena (exchange.cu). Peers write into it over
+// NVLink: barrier arrivals, and per source rank the counts of what it delivered.
+struct alignas(128) XHdr {
+  unsigned long long bar[kMaxWorld];  // bar[r] = last barrier epoch rank r reached
+  uint32_t fwd_cnt[kMaxWorld];        // ids source r wrote into my id region r
+  uint32_t fwd_seg[kMaxWorld];        // where my rows go in source r's rows buffer
+  uint32_t bwd_cnt[kMaxWorld];        // pairs source r sends me
+  uint32_t err;                       // barrier timeout seen by this rank
+};
 struct XScratch {
   uint64_t* ids = nullptr;
   uint64_t* rv = nullptr;
@@ -201,6 +211,13 @@ struct Table {
 };
 
 // ---- kernels / launchers (kernels.cu, update.cu) ---------------------------------------
+// Owner side of the peer exchange: slots[r * stride + j] = find_or_insert(ids[r * stride + j])
+// for j < hdr->fwd_cnt[r], r < W (counts are device-side); the ids and counts are also
+// copied to owner-local memory (peers may overwrite the regions once the step moves on).
+void launch_probe_regions(const DevTable& t, const uint64_t* ids, uint64_t stride, uint32_t W,
+                          const XHdr* hdr, uint32_t* slots, uint64_t* ids_copy,
+                          uint32_t* cnt_copy, uint32_t* new_slots, uint32_t* new_count, int sms,
+                          cudaStream_t st);
 void launch_route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cudaStream_t st);
 void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st);
 // slots[i] = find_or_insert(ids[i]); when sort_keys/sort_vals are given also writes the

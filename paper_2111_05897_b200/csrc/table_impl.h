@@ -114,6 +114,18 @@ struct XBatch {
   unsigned long long* mkeys = nullptr;
   uint32_t *sm_pos = nullptr, *sm_list = nullptr;
   uint64_t* h_buf = nullptr;
+  // peer (NVLink) transport
+  uint8_t* arena = nullptr;
+  uint8_t* peer[kMaxWorld] = {};
+  float* arena_rows = nullptr;
+  size_t arena_bytes = 0, off_ids = 0, off_rows = 0, off_ppos = 0, off_contrib = 0,
+         off_oslot = 0, off_orv = 0, off_oids = 0, off_ocnt = 0;
+  uint64_t max_ids = 0;
+  uint32_t arena_dim = 0, rank = 0;
+  bool connected = false;
+  unsigned long long epoch = 0;
+  uint64_t* xbase = nullptr;
+  unsigned long long* fail = nullptr;
   uint64_t cap_H = 0, cap_hidx = 0, cap_hval = 0, cap_hmul = 0, cap_dest = 0, cap_sendpos = 0,
            cap_spair = 0, cap_off = 0, cap_lgrp = 0, cap_ka = 0, cap_va = 0, cap_kb = 0,
            cap_vb = 0, cap_scratch = 0, cap_head = 0, cap_ex = 0, cap_tsum = 0, cap_dop = 0;
@@ -125,6 +137,12 @@ void xbatch_route(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_t* of
 void xbatch_pool(XBatch& x, const float* rows, uint32_t D, float* out_pooled, cudaStream_t st);
 void xbatch_pairs(XBatch& x, const float* grads, uint32_t D, uint32_t* out_pair_pos,
                   float* out_contrib, uint64_t* out_pair_counts, cudaStream_t st);
+void xbatch_arena(XBatch& x, uint64_t max_ids, uint32_t D, void* out_handle);
+void xbatch_connect(XBatch& x, uint32_t rank, const void* handles);
+void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint32_t* offsets,
+                uint32_t B, uint32_t F, cudaStream_t st);
+void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step_tag,
+                uint32_t epoch, int* accepted, uint32_t flags, cudaStream_t st);
 void table_apply_pairs(Table* t, const uint64_t* recv_ids, const uint64_t* recv_versions,
                        const uint64_t* id_counts, const uint32_t* pair_pos, const float* contrib,
                        const uint64_t* pair_counts, uint32_t G, float lr, uint32_t step_tag,

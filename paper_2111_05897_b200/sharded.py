@@ -9,18 +9,22 @@ E embedding workers in front of a sharded parameter server
 ``push_to_shards`` :726-775, ``PsShardService`` :185-290), with the per-frame RPCs
 replaced by three NCCL all-to-alls:
 
-  forward   route (distinct ids grouped by owner) -> all-to-all ids -> owner lookup
-            (find_or_init + gather + versions) -> all-to-all rows -> fp64 pooling
+  forward   route (distinct ids grouped by owner) -> ids to owners -> owner lookup
+            (find_or_init + gather + versions) -> rows back -> fp64 pooling
   backward  pairs (one fp64 chain-rule contribution per (sample, distinct id), grouped
-            by owner) -> all-to-all (position, contribution) -> owner applies them in
+            by owner) -> (position, contribution) to owners -> owner applies them in
             (source rank, sample) order = ascending SampleId (rank << 56 | counter,
             core.hpp:98-125; flush order embedding_worker.hpp:788-790)
 
-The local work is hand-written CUDA in libhps.so (``DeviceOps``: hps_exchange_* and
-hps_lookup / hps_table_apply_pairs); the collectives are torch.distributed over NCCL.
-``ShardedEmbeddingWorker`` only sequences the two; ``ops`` is injectable so the
-sequencing itself is testable with a gloo process group on CPU (tests/test_sharded.py
-checks it against the reference's multi-worker semantics with an oracle-backed ops).
+Two transports move the payloads:
+  "p2p"   (default on GPUs) the kernels write every payload once, straight into the
+          consumer's HBM over NVLink (CUDA IPC peer mappings of a per-rank arena), with
+          device-side barriers -- no collective on the data path, one host round trip per
+          step (hps_exchange_forward / _pool / _backward in libhps.so).
+  "nccl"  torch.distributed all-to-alls between the local kernels (hps_exchange_route /
+          _pool / _pairs, hps_table_gather / hps_table_apply_pairs); ``ops`` is injectable
+          so this sequencing is testable with gloo on CPU (tests/test_sharded.py checks it
+          against the reference's multi-worker semantics with an oracle-backed ops).
 """
 from __future__ import annotations
 
@@ -118,11 +122,60 @@ class DeviceOps:
         return bool(acc.value)
 
 
+class PeerExchange:
+    """The NVLink peer transport (libhps.so hps_exchange_arena/connect/forward/backward)."""
+
+    def __init__(self, ops: DeviceOps, dist, group, rank: int, max_ids: int):
+        import torch
+
+        self.ops = ops
+        self.max_ids = max_ids
+        handle = (C.c_uint8 * 64)()
+        hps.check(hps.lib().hps_exchange_arena(ops.h, max_ids, ops.D, handle), "exchange arena")
+        mine = bytes(handle)
+        world = ops.world
+        if world > 1:
+            got = [None] * world
+            dist.all_gather_object(got, mine, group=group)
+        else:
+            got = [mine]
+        allh = (C.c_uint8 * (64 * world)).from_buffer_copy(b"".join(got))
+        hps.check(hps.lib().hps_exchange_connect(ops.h, rank, allh), "exchange connect")
+        torch.cuda.synchronize()
+
+    def forward(self, ids, offsets, B, F):
+        o = self.ops
+        hps.check(hps.lib().hps_exchange_forward(o.h, o.table.h, ids.data_ptr(), ids.numel(),
+                                                 offsets.data_ptr(), B, F, o._s()),
+                  "exchange forward")
+
+    def pool(self, B, F, out=None):
+        o = self.ops
+        t = o.torch
+        if out is None:
+            out = t.empty((B, F, o.D), dtype=t.float32, device=o.device)
+        hps.check(hps.lib().hps_exchange_pool(o.h, None, o.D, out.data_ptr(), o._s()),
+                  "exchange pool")
+        return out
+
+    def backward(self, grads, lr, step_tag, epoch, flags):
+        o = self.ops
+        acc = C.c_int(0)
+        hps.check(hps.lib().hps_exchange_backward(o.h, o.table.h, grads.contiguous().data_ptr(),
+                                                  lr, step_tag, epoch, C.byref(acc), flags,
+                                                  o._s()), "exchange backward")
+        return bool(acc.value)
+
+
 class ShardedEmbeddingWorker:
     """``register_batch`` / ``serve_pull`` / ``apply_backward`` of one rank's embedding
-    worker over the hash-sharded table (sync order; one batch in flight)."""
+    worker over the hash-sharded table (sync order; one batch in flight).
 
-    def __init__(self, table: hps.ShardSet, aggregation: int = hps.MEAN, group=None, ops=None):
+    transport: "p2p" (NVLink peer writes; needs ``max_ids`` >= listings per batch) or
+    "nccl" (all-to-alls); default "p2p" unless ``ops`` is injected."""
+
+    def __init__(self, table: hps.ShardSet, aggregation: int = hps.MEAN, group=None, ops=None,
+                 transport: str | None = None, max_ids: int | None = None):
         import torch.distributed as dist
 
         self.dist = dist
@@ -134,8 +187,11 @@ class ShardedEmbeddingWorker:
             self.world, self.rank = 1, 0
         self.table = table
         self.aggregation = aggregation
+        self.transport = transport or ("nccl" if ops is not None else "p2p")
         self.ops = ops if ops is not None else DeviceOps(table, self.world, aggregation)
         self.B = self.F = 0
+        self.peer = None
+        self.max_ids = max_ids
 
     # -- collectives ------------------------------------------------------------------
     def _exchange_counts(self, counts):
@@ -175,6 +231,12 @@ class ShardedEmbeddingWorker:
     def register_batch(self, ids, offsets, B: int, F: int):
         """Route the batch's ids to their owners and fetch the rows (fetch_rows)."""
         self.B, self.F, self.n_ids = B, F, ids.numel()
+        if self.transport == "p2p":
+            if self.peer is None:
+                self.peer = PeerExchange(self.ops, self.dist, self.group, self.rank,
+                                         self.max_ids or max(ids.numel(), 1))
+            self.peer.forward(ids, offsets, B, F)
+            return
         send_ids, counts = self.ops.route(ids, offsets, B, F)
         self.send_counts, self.recv_counts = self._exchange_counts(counts)
         self.recv_ids = self._a2a(send_ids[:sum(self.send_counts)], self.send_counts,
@@ -184,6 +246,8 @@ class ShardedEmbeddingWorker:
 
     def serve_pull(self, out_pooled=None):
         """Pooled embeddings [B, F, D] of the registered batch (serve_pull)."""
+        if self.transport == "p2p":
+            return self.peer.pool(self.B, self.F, out_pooled)
         return self.ops.pool(self.rows, self.B, self.F, out_pooled)
 
     def apply_backward(self, grads, lr: float, step_tag: int, epoch: int | None = None,
@@ -191,6 +255,9 @@ class ShardedEmbeddingWorker:
         """Per-sample gradients [B, F, D] -> owners, applied in ascending SampleId.
         Data-dependent errors (non-finite contributions, capacity) surface from
         ``table.sync()`` unless flags = 0."""
+        if self.transport == "p2p":
+            e = self.table.epoch() if epoch is None else epoch
+            return self.peer.backward(grads, lr, step_tag, e, flags)
         pos, con, counts = self.ops.pairs(grads, self.n_ids)
         self.pair_counts, recv_pair_counts = self._exchange_counts(counts)
         P = sum(self.pair_counts)

@@ -44,7 +44,7 @@ def local_part(ids, offs, W, B, F, r):
 
 
 def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, agg="mean",
-             opt="adagrad", space=60, q=None):
+             opt="adagrad", space=60, transport="p2p", q=None):
     try:
         import torch
         import torch.distributed as dist
@@ -64,7 +64,8 @@ def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, ag
             dev = torch.device("cuda", rank)
             table = hps.ShardSet(S, D, 1 << 14, hps.ADAGRAD if opt == "adagrad" else hps.SGD,
                                  salts=salts)
-            ew = ShardedEmbeddingWorker(table, hps.MEAN if agg == "mean" else hps.SUM)
+            ew = ShardedEmbeddingWorker(table, hps.MEAN if agg == "mean" else hps.SUM,
+                                        transport=transport, max_ids=world * B * F * 4)
             owner_peek = table.peek
         else:
             from sharded_oracle_ops import EpochOnly, OracleOps

@@ -25,38 +25,47 @@ def test_sharded_sequencing_gloo_sum_sgd():
         assert status == "ok", status
 
 
+TRANSPORTS = ["p2p", "nccl"]
+
+
 @pytest.mark.gpu
-def test_sharded_device_world1():
-    res = run_world(1, "nccl", use_device=True)
+@pytest.mark.parametrize("transport", TRANSPORTS)
+def test_sharded_device_world1(transport):
+    res = run_world(1, "nccl", use_device=True, transport=transport)
     assert res[0][1] == "ok", res[0][1]
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("transport", TRANSPORTS)
 @pytest.mark.parametrize("D", [64, 5])
-def test_sharded_device_world1_large_plan(D):
+def test_sharded_device_world1_large_plan(D, transport):
     """More than 4096 listings of repeated ids: the device-gated radix-sort path."""
-    res = run_world(1, "nccl", use_device=True, B=1500, F=4, D=D, space=2500, steps=2)
+    res = run_world(1, "nccl", use_device=True, B=1500, F=4, D=D, space=2500, steps=2,
+                    transport=transport)
     assert res[0][1] == "ok", res[0][1]
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("transport", TRANSPORTS)
 @pytest.mark.parametrize("agg,opt", [("mean", "adagrad"), ("sum", "sgd")])
-def test_sharded_device_world2(agg, opt):
+def test_sharded_device_world2(agg, opt, transport):
     import torch
 
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
-    res = run_world(2, "nccl", use_device=True, agg=agg, opt=opt)
+    res = run_world(2, "nccl", use_device=True, agg=agg, opt=opt, transport=transport)
     for r, status, n in res:
         assert status == "ok", status
 
 
 @pytest.mark.gpu
-def test_sharded_device_world2_large_plan():
+@pytest.mark.parametrize("transport", TRANSPORTS)
+def test_sharded_device_world2_large_plan(transport):
     import torch
 
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
-    res = run_world(2, "nccl", use_device=True, B=800, F=4, D=16, space=2000, steps=2)
+    res = run_world(2, "nccl", use_device=True, B=800, F=4, D=16, space=2000, steps=2,
+                    transport=transport)
     for r, status, n in res:
         assert status == "ok", status

@@ -26,11 +26,13 @@ table = hps.ShardSet(S, D, int(rows / world * 1.05) + (1 << 20), hps.ADAGRAD, sa
 hb = [W.make_batch(cfg, 1000 * rank + m) for m in range(3)]
 bs = [(torch.from_numpy(h.ids.view(np.int64)).to(dev), torch.from_numpy(h.offsets.view(np.int32)).to(dev)) for h in hb]
 grads = torch.rand((B, F, D), device=dev) * 0.02 - 0.01
-ew = ShardedEmbeddingWorker(table, hps.MEAN)
+transport = os.environ.get("TRANSPORT", "nccl")
+ew = ShardedEmbeddingWorker(table, hps.MEAN, transport=transport,
+                            max_ids=max(int(h.N) for h in hb))
 pooled = torch.empty((B, F, D), device=dev)
 ops = ew.ops
 names = ["route", "cnt1", "a2a_ids", "lookup", "a2a_rows", "pool", "pairs", "cnt2", "a2a_pos",
-         "a2a_con", "apply"]
+         "a2a_con", "apply"] if transport == "nccl" else ["fwd", "pool", "bwd"]
 acc = {n: 0.0 for n in names}
 wall = 0.0
 steps = 12
@@ -41,6 +43,16 @@ for it in range(steps + 3):
     dist.barrier()
     t0 = time.perf_counter()
     ev[0].record()
+    if transport == "p2p":
+        ew.register_batch(ids, offs, B, F); ev[1].record()
+        ew.serve_pull(out_pooled=pooled); ev[2].record()
+        ew.apply_backward(grads, 0.05, it + 1); ev[3].record()
+        torch.cuda.synchronize()
+        if it >= 3:
+            wall += time.perf_counter() - t0
+            for k, n in enumerate(names):
+                acc[n] += ev[k].elapsed_time(ev[k + 1])
+        continue
     send, counts = ops.route(ids, offs, B, F); ev[1].record()
     sc, rc = ew._exchange_counts(counts); ev[2].record()
     rid = ew._a2a(send[:sum(sc)], sc, rc); ev[3].record()
@@ -62,7 +74,7 @@ for it in range(steps + 3):
 table.sync()
 if rank == 0:
     tot = sum(acc.values()) / steps
-    print(f"world={world} per-step device {tot:.3f} ms, wall {1000 * wall / steps:.3f} ms")
+    print(f"transport={transport} world={world} per-step device {tot:.3f} ms, wall {1000 * wall / steps:.3f} ms")
     for n in names:
         print(f"  {n:9s} {acc[n] / steps:7.3f} ms")
 dist.destroy_process_group()
