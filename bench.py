@@ -241,15 +241,45 @@ def run_sharded(args, world, rank, local, dev):
     ew = ShardedEmbeddingWorker(table, hps.MEAN, transport=args.transport, max_ids=max_n)
     tag = [0]
 
-    def step(i):
+    p2p = args.transport == "p2p"
+
+    def eager_step(i):
         ids, offs, _ = batches[i % M]
         ew.register_batch(ids, offs, B, F)
         ew.serve_pull(out_pooled=pooled)
         tag[0] += 1
-        ew.apply_backward(grads[i % M], cfg.lr, tag[0])
+        # p2p: step tags from the table's device counter (graph replays advance it)
+        ew.apply_backward(grads[i % M], cfg.lr, tag[0],
+                          flags=hps.ASYNC | (hps.DEVICE_STEP if p2p else 0))
 
     it = 0
     for _ in range(args.warmup):
+        eager_step(it)
+        it += 1
+    torch.cuda.synchronize()
+    table.sync()
+    # p2p: the whole sharded step (route, peer writes, device barriers, owner apply) is
+    # stream-ordered without host round trips -> one CUDA graph per input batch.
+    graphs, graph_launches = [], []
+    if p2p and not args.no_graph:
+        cs = torch.cuda.Stream()
+        for m in range(M):
+            g = torch.cuda.CUDAGraph()
+            l0 = hps.launch_count()
+            with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+                eager_step(m)
+            graph_launches.append(hps.launch_count() - l0)
+            graphs.append(g)
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    def step(i):
+        if graphs:
+            graphs[i % M].replay()
+        else:
+            eager_step(i)
+
+    for _ in range(2):
         step(it)
         it += 1
     torch.cuda.synchronize()
@@ -273,6 +303,8 @@ def run_sharded(args, world, rank, local, dev):
     dist.barrier()
     torch.cuda.synchronize()
     launches = hps.launch_count() - l0
+    if graphs:
+        launches = sum(graph_launches[i % M] for i in range(it - args.steps, it))
     ms = e0.elapsed_time(e1) / args.steps
     t_soak = time.perf_counter()
     while time.perf_counter() - t_soak < args.soak_seconds:
@@ -318,7 +350,8 @@ def run_sharded(args, world, rank, local, dev):
         h_pooled.copy_(pooled, non_blocking=True)
         d_grads.copy_(h_grads, non_blocking=True)
         tag[0] += 1
-        ew.apply_backward(d_grads, cfg.lr, tag[0])
+        ew.apply_backward(d_grads, cfg.lr, tag[0],
+                          flags=hps.ASYNC | (hps.DEVICE_STEP if p2p else 0))
 
     e2e = None
     if args.e2e_steps > 0:

@@ -441,7 +441,7 @@ XBatch::~XBatch() {
     if (peer[r] && peer[r] != arena) cudaIpcCloseMemHandle(peer[r]);
   if (arena) cudaFree(arena);
   if (xbase) cudaFree(xbase);
-  if (fail) cudaFree(fail);
+  if (dev_epoch) cudaFree(dev_epoch);
   void* ps[] = {hkeys,  hidx,   hval,   hmul,    dest,    sendpos, spair, offsets, lgrp,
                 keys_a, vals_a, keys_b, vals_b,  scratch, head,    ex,    tsum,    cnt,
                 seg,    dest_of_pos,    pair_off, mkeys,  mstart,  sm_pos, sm_list};
@@ -703,6 +703,44 @@ void table_apply_pairs(Table* t, const uint64_t* recv_ids, const uint64_t* recv_
 struct PeerHdrs {
   XHdr* h[kMaxWorld];
 };
+
+// Owner (peer path): the pairs that arrived -- source-rank major, counts bwd_cnt[r] --
+// become a batch of device-counted one-listing samples: ids / read versions of the ids
+// each pair names, offsets[k] = min(k, P) for k <= cap (samples past P are empty).
+__global__ void x_owner_dyn_kernel(const XHdr* __restrict__ hdr,
+                                   const uint32_t* __restrict__ ocnt, uint32_t W,
+                                   uint64_t stride, const uint64_t* __restrict__ oids,
+                                   const uint64_t* __restrict__ orv,
+                                   const uint32_t* __restrict__ pair_pos, uint64_t cap,
+                                   uint64_t* __restrict__ out_ids, uint64_t* __restrict__ out_rv,
+                                   uint32_t* __restrict__ out_off,
+                                   unsigned long long* protocol) {
+  __shared__ uint64_t po[kMaxWorld + 1];
+  if (threadIdx.x == 0) {
+    uint64_t run = 0;
+    for (uint32_t r = 0; r < W; ++r) {
+      po[r] = run;
+      run += ld_volatile(&hdr->bwd_cnt[r]);
+    }
+    po[W] = run;
+  }
+  __syncthreads();
+  const uint64_t P = min(po[W], cap);
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k <= cap;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    out_off[k] = static_cast<uint32_t>(min(k, P));
+    if (k >= P) continue;
+    uint32_t r = 0;
+    while (r + 1 < W && po[r + 1] <= k) ++r;
+    uint32_t j = pair_pos[k];
+    if (j >= ocnt[r]) {
+      atomicOr(protocol, 1ull);
+      j = 0;
+    }
+    out_ids[k] = oids[r * stride + j];
+    out_rv[k] = orv[r * stride + j];
+  }
+}
 struct PeerRows {
   float* p[kMaxWorld];
 };
@@ -713,10 +751,15 @@ constexpr long long kBarrierTimeoutCycles = 8'000'000'000ll;  // ~4 s: never han
 // every peer's arrival at this rank. A peer that never arrives trips the timeout, which
 // flags the table (updates are gated off) and surfaces as HPS_E_SYNC_FAILURE.
 __global__ void x_barrier_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
-                                 unsigned long long epoch, unsigned long long* fail) {
+                                 unsigned long long* epoch_ctr, unsigned long long* fail) {
+  __shared__ unsigned long long s_epoch;
   const uint32_t t = threadIdx.x;
+  // The epoch lives on the device, so a barrier captured in a CUDA graph advances it on
+  // every replay (every rank runs the same sequence of barriers).
+  if (t == 0) s_epoch = ++*epoch_ctr;
   __threadfence_system();
   __syncthreads();
+  const unsigned long long epoch = s_epoch;
   if (t < W) {
     unsigned long long* f = &ph.h[t]->bar[rank];
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
@@ -820,8 +863,8 @@ void xbatch_arena(XBatch& x, uint64_t max_ids, uint32_t D, void* out_handle) {
   HPS_CUDA(cudaMalloc(&x.arena, o));
   HPS_CUDA(cudaMemset(x.arena, 0, al256(sizeof(XHdr))));
   HPS_CUDA(cudaMalloc(&x.xbase, 33 * sizeof(uint64_t)));
-  HPS_CUDA(cudaMalloc(&x.fail, sizeof(unsigned long long)));
-  HPS_CUDA(cudaMemset(x.fail, 0, sizeof(unsigned long long)));
+  HPS_CUDA(cudaMalloc(&x.dev_epoch, sizeof(unsigned long long)));
+  HPS_CUDA(cudaMemset(x.dev_epoch, 0, sizeof(unsigned long long)));
   x.arena_rows = reinterpret_cast<float*>(x.arena + x.off_rows);
   cudaIpcMemHandle_t h;
   HPS_CUDA(cudaIpcGetMemHandle(&h, x.arena));
@@ -851,9 +894,11 @@ static PeerHdrs peer_hdrs(const XBatch& x) {
   return ph;
 }
 
-static void barrier(XBatch& x, cudaStream_t st) {
-  ++x.epoch;
-  x_barrier_kernel<<<1, 32, 0, st>>>(peer_hdrs(x), x.G, x.rank, x.epoch, x.fail);
+// A timeout flags the table (kCtrProtocol): the step's updates are gated off and the
+// failure surfaces from the next synchronising call.
+static void barrier(XBatch& x, Table* t, cudaStream_t st) {
+  x_barrier_kernel<<<1, 32, 0, st>>>(peer_hdrs(x), x.G, x.rank, x.dev_epoch,
+                                     t->d.ctr + kCtrProtocol);
   HPS_LAUNCH_CHECK();
 }
 
@@ -861,14 +906,6 @@ static void require_connected(const XBatch& x, uint32_t D, uint64_t n) {
   if (!x.connected) throw Error(HPS_E_PRECONDITION, "exchange: peer transport not connected");
   if (D != x.arena_dim) throw Error(HPS_E_PRECONDITION, "exchange: dim differs from the arena's");
   if (n > x.max_ids) throw Error(HPS_E_PRECONDITION, "exchange: batch exceeds the arena size");
-}
-
-static void check_fail(XBatch& x, cudaStream_t st) {
-  HPS_CUDA(cudaMemcpyAsync(x.h_buf + 64, x.fail, sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, st));
-  HPS_CUDA(cudaStreamSynchronize(st));
-  if (x.h_buf[64])
-    throw Error(HPS_E_SYNC_FAILURE, "exchange: a peer did not reach the barrier (timeout)");
 }
 
 void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint32_t* offsets,
@@ -882,7 +919,7 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
   const PeerHdrs ph = peer_hdrs(x);
   x_fwd_hdr_kernel<<<1, 32, 0, st>>>(ph, x.G, x.rank, x.cnt, x.seg);
   HPS_LAUNCH_CHECK();
-  barrier(x, st);  // every id region and count has landed
+  barrier(x, t, st);  // every id region and count has landed
   // owner: find-or-init the ids every source asked for, rows straight back to them
   XHdr* mine = ph.h[x.rank];
   uint32_t* oslot = reinterpret_cast<uint32_t*>(x.arena + x.off_oslot);
@@ -904,7 +941,7 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
     x_owner_gather_kernel<V, L, G><<<dim3(bx, x.G), 256, 0, st>>>(t->d, oslot, M, mine, pr, orv);
   });
   HPS_LAUNCH_CHECK();
-  barrier(x, st);  // every owner's rows have landed in this rank's rows buffer
+  barrier(x, t, st);  // every owner's rows have landed in this rank's rows buffer
 }
 
 void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step_tag,
@@ -922,7 +959,7 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
   }
   x_bwd_hdr_kernel<<<1, 32, 0, st>>>(ph, x.G, x.rank, x.pair_off);
   HPS_LAUNCH_CHECK();
-  barrier(x, st);  // every owner knows how many pairs each source sends
+  barrier(x, t, st);  // every owner knows how many pairs each source sends
   x_bwd_base_kernel<<<1, 32, 0, st>>>(ph, x.G, x.rank, x.xbase);
   HPS_LAUNCH_CHECK();
   if (x.N) {
@@ -933,29 +970,27 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
     }
     emit_pairs(x, grads, D, spos, slist, x.xbase, po, st);
   }
-  barrier(x, st);  // every pair has landed at its owner
-  // owner: how many pairs arrived from each source (one host round trip), then apply
-  // (bwd_cnt is safe to read: no source can write the next step's before this rank
-  // reaches the next step's first barrier; fwd counts/ids come from the owner-local copy.)
+  barrier(x, t, st);  // every pair has landed at its owner
+  // owner: a device-counted batch of the pairs that arrived (no host round trip: the
+  // whole step stays stream-ordered and capturable in a CUDA graph)
   XHdr* mine = ph.h[x.rank];
-  HPS_CUDA(cudaMemcpyAsync(x.h_buf, x.arena + x.off_ocnt, kMaxWorld * sizeof(uint32_t),
-                           cudaMemcpyDeviceToHost, st));
-  HPS_CUDA(cudaMemcpyAsync(x.h_buf + 16, mine->bwd_cnt, kMaxWorld * sizeof(uint32_t),
-                           cudaMemcpyDeviceToHost, st));
-  check_fail(x, st);  // synchronises
-  const uint32_t* hc = reinterpret_cast<const uint32_t*>(x.h_buf);
-  const uint32_t* hb = reinterpret_cast<const uint32_t*>(x.h_buf + 16);
-  Offs io{}, ie{}, po{};
-  for (uint32_t r = 0; r < x.G; ++r) {
-    io.v[r] = r * M;
-    ie.v[r] = r * M + hc[r];
-    po.v[r + 1] = po.v[r] + hb[r];
-  }
-  owner_apply(t, reinterpret_cast<const uint64_t*>(x.arena + x.off_oids),
-              reinterpret_cast<const uint64_t*>(x.arena + x.off_orv), io, ie, po, x.G,
-              reinterpret_cast<const uint32_t*>(x.arena + x.off_ppos),
-              reinterpret_cast<const float*>(x.arena + x.off_contrib), lr, step_tag, epoch,
-              accepted, flags, st);
+  const uint64_t cap = x.G * M;
+  XScratch& xs = t->xs;
+  grow(xs.ids, xs.cap_ids, cap);
+  grow(xs.rv, xs.cap_rv, cap);
+  grow(xs.off, xs.cap_off, cap + 1);
+  x_owner_dyn_kernel<<<grid_n(cap + 1, t->sm_count), kXBlock, 0, st>>>(
+      mine, reinterpret_cast<const uint32_t*>(x.arena + x.off_ocnt), x.G, M,
+      reinterpret_cast<const uint64_t*>(x.arena + x.off_oids),
+      reinterpret_cast<const uint64_t*>(x.arena + x.off_orv),
+      reinterpret_cast<const uint32_t*>(x.arena + x.off_ppos), cap, xs.ids, xs.rv, xs.off,
+      t->d.ctr + kCtrProtocol);
+  HPS_LAUNCH_CHECK();
+  Batch& b = t->scratch;
+  b.agg = HPS_SUM;
+  batch_register(b, xs.ids, cap, xs.off, static_cast<uint32_t>(cap), 1, nullptr, st, true);
+  batch_push(b, HPS_SUM, reinterpret_cast<const float*>(x.arena + x.off_contrib), lr, step_tag,
+             epoch, 0, xs.rv, accepted, flags, st);
 }
 
 }  // namespace hps

@@ -139,7 +139,9 @@ __global__ void __launch_bounds__(256)
     probe_kernel(DevTable t, const uint64_t* __restrict__ ids, uint64_t n,
                  uint32_t* __restrict__ slots, uint32_t* __restrict__ sort_keys,
                  uint32_t* __restrict__ sort_vals, uint32_t* __restrict__ new_slots,
-                 uint32_t* __restrict__ new_count, bool plan) {
+                 uint32_t* __restrict__ new_count, bool plan, const uint32_t* n_dev) {
+  // n_dev: the live listing count is device-side (<= n); listings past it get no row.
+  const uint64_t n_live = n_dev ? min(n, static_cast<uint64_t>(*n_dev)) : n;
   // kProbeILP listings per thread: their first probes are issued back to back (the
   // common case -- key found in its home entry -- then costs one round trip for all).
   constexpr int kProbeILP = 2;
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int k = 0; k < kProbeILP; ++k) {
     const uint64_t i = base + static_cast<uint64_t>(k) * blockDim.x;
-    id[k] = i < n ? ids[i] : kEmptyKey;
+    id[k] = i < n_live ? ids[i] : kEmptyKey;
   }
 #pragma unroll
   for (int k = 0; k < kProbeILP; ++k) {
@@ -162,7 +164,9 @@ __global__ void __launch_bounds__(256)
     const uint64_t i = base + static_cast<uint64_t>(k) * blockDim.x;
     if (i >= n) break;
     uint32_t s;
-    if (id[k] != kEmptyKey && kv[k].x == id[k] && static_cast<uint32_t>(kv[k].y) != kPending)
+    if (i >= n_live)
+      s = kInvalidSlot;
+    else if (id[k] != kEmptyKey && kv[k].x == id[k] && static_cast<uint32_t>(kv[k].y) != kPending)
       s = static_cast<uint32_t>(kv[k].y);  // hit in the home entry
     else
       s = find_or_insert(t, id[k], new_slots, new_count, true);
@@ -182,10 +186,10 @@ __global__ void __launch_bounds__(256)
 
 void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* slots,
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
-                  uint32_t* new_count, bool plan, cudaStream_t st) {
+                  uint32_t* new_count, bool plan, cudaStream_t st, const uint32_t* n_dev) {
   if (!n) return;
   probe_kernel<<<ceil_div(n, 256 * 2), 256, 0, st>>>(t, ids, n, slots, sort_keys, sort_vals,
-                                                     new_slots, new_count, plan);
+                                                     new_slots, new_count, plan, n_dev);
   HPS_LAUNCH_CHECK();
 }
 
@@ -403,7 +407,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int u = 0; u < kCheckILP; ++u) {
         const uint64_t r = r0 + u * groups;
-        if (r < rows && (!kGuard || d0 < D)) load_vec_cs<V>(grads + r * D + d0, x[u]);
+        if (n[u] && (!kGuard || d0 < D)) load_vec_cs<V>(grads + r * D + d0, x[u]);
         else for (int j = 0; j < V; ++j) x[u][j] = 0.0f;
       }
 #pragma unroll

@@ -339,7 +339,8 @@ void check_flags(Table* t, cudaStream_t st, bool divergence) {
     HPS_CUDA(cudaMemsetAsync(t->d.ctr + kCtrProtocol, 0, sizeof(unsigned long long), st));
     HPS_CUDA(cudaStreamSynchronize(st));
     throw Error(HPS_E_PROTOCOL,
-                "exchange: a pair names an id outside its source's segment; nothing was applied");
+                "exchange failed (a pair named an id outside its source's segment, or a peer "
+                "missed a barrier); the step's updates were not applied");
   }
   if (divergence && t->h_ctr[kCtrDivergence]) {
     HPS_CUDA(cudaMemsetAsync(t->d.ctr + kCtrDivergence, 0, sizeof(unsigned long long), st));
@@ -467,7 +468,7 @@ static void sort_slots(Batch& b, const uint32_t* keys_in0, bool iota, const uint
 // serve_pull: after this, every listing has its slot (rows lazily initialised) and the
 // listings are grouped per row in apply order.
 void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* offsets, uint32_t B,
-                    uint32_t F, const uint64_t* sample_keys, cudaStream_t st) {
+                    uint32_t F, const uint64_t* sample_keys, cudaStream_t st, bool dynamic) {
   Table* t = b.table;
   if (N >= 0xffffffffull) throw Error(HPS_E_PRECONDITION, "batch too large (>= 2^32 listings)");
   const uint64_t BF = static_cast<uint64_t>(B) * F;
@@ -503,8 +504,9 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   b.all_multi = permute;
   {
     ProfScope p(t, "probe", st);
+    // dynamic: N is only a bound; the live listing count is offsets[B*F] on the device
     launch_probe(t->d, d_ids, N, b.slot, nullptr, nullptr, b.new_slots, &b.small[2], !permute,
-                 st);
+                 st, dynamic ? b.offsets + BF : nullptr);
   }
   launch_lazy_init(t->d, b.new_slots, &b.small[2], N, t->sm_count, st);
   if (permute) {

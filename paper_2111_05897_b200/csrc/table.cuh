@@ -225,7 +225,8 @@ void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, 
 // plan: also mark the rows in the batch-plan bitmaps (plan.cu).
 void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* slots,
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
-                  uint32_t* new_count, bool plan, cudaStream_t st);
+                  uint32_t* new_count, bool plan, cudaStream_t st,
+                  const uint32_t* n_dev = nullptr);
 // plan.cu
 void launch_classify(const DevTable& t, const uint32_t* slots, uint64_t n, int lbits,
                      uint8_t* kind, unsigned long long* mkeys, uint32_t* n_multi, int sms,

@@ -59,8 +59,11 @@ void check_flags(Table* t, cudaStream_t st, bool divergence = true);
 
 void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B);
 void batch_free(Batch& b);
+// dynamic: N and B are bounds; offsets (device) end at the live count (offsets[B*F]),
+// samples past it are empty -- a batch whose size is only known on the device.
 void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* offsets, uint32_t B,
-                    uint32_t F, const uint64_t* sample_keys, cudaStream_t st);
+                    uint32_t F, const uint64_t* sample_keys, cudaStream_t st,
+                    bool dynamic = false);
 void batch_pull(Batch& b, int agg, float* out_pooled, uint64_t* out_rv, cudaStream_t st);
 void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_tag,
                 uint32_t epoch, int untracked, const uint64_t* rv64, int* accepted,
@@ -123,9 +126,8 @@ struct XBatch {
   uint64_t max_ids = 0;
   uint32_t arena_dim = 0, rank = 0;
   bool connected = false;
-  unsigned long long epoch = 0;
   uint64_t* xbase = nullptr;
-  unsigned long long* fail = nullptr;
+  unsigned long long* dev_epoch = nullptr;
   uint64_t cap_H = 0, cap_hidx = 0, cap_hval = 0, cap_hmul = 0, cap_dest = 0, cap_sendpos = 0,
            cap_spair = 0, cap_off = 0, cap_lgrp = 0, cap_ka = 0, cap_va = 0, cap_kb = 0,
            cap_vb = 0, cap_scratch = 0, cap_head = 0, cap_ex = 0, cap_tsum = 0, cap_dop = 0;

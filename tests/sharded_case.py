@@ -19,10 +19,11 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 
-def global_batch(step, W, B, F, space, seed=11):
+def global_batch(step, W, B, F, space, seed=11, fixed_shape=False):
     rng = np.random.default_rng(seed * 1000 + step)
-    counts = rng.integers(0, 4, W * B * F)
-    counts[rng.random(W * B * F) < 0.5] = 1
+    crng = np.random.default_rng(seed) if fixed_shape else rng
+    counts = crng.integers(0, 4, W * B * F)
+    counts[crng.random(W * B * F) < 0.5] = 1
     offs = np.zeros(W * B * F + 1, np.int64)
     np.cumsum(counts, out=offs[1:])
     ids = rng.integers(0, space, int(offs[-1])).astype(np.uint64)
@@ -44,7 +45,7 @@ def local_part(ids, offs, W, B, F, r):
 
 
 def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, agg="mean",
-             opt="adagrad", space=60, transport="p2p", q=None):
+             opt="adagrad", space=60, transport="p2p", graph=False, q=None):
     try:
         import torch
         import torch.distributed as dist
@@ -76,8 +77,10 @@ def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, ag
                                         ops=OracleOps(local, world, S, D, agg))
             owner_peek = local.peek
         seen = set()
+        cg = None  # graph mode: one step captured at s == 1, replayed on new inputs
+        flags = hps.ASYNC | hps.DEVICE_STEP if graph else hps.ASYNC
         for s in range(steps):
-            gids, goffs, _ = global_batch(s, world, B, F, space)
+            gids, goffs, _ = global_batch(s, world, B, F, space, fixed_shape=graph)
             rng = np.random.default_rng(500 + s)
             g_all = (rng.standard_normal((world * B, F, D)) * 0.3).astype(np.float32)
             sk = np.array([((i % world) << 56) | (i // world) for i in range(world * B)],
@@ -85,16 +88,35 @@ def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, ag
             pooled_exp, rv_exp = exp.pull_batch(world * B, F, gids, goffs.astype(np.uint64), agg)
             lid, loff = local_part(gids, goffs, world, B, F, rank)
             seen.update(int(x) for x in gids)
-            t_ids = torch.from_numpy(lid.view(np.int64).copy()).to(dev)
-            t_off = torch.from_numpy(loff.astype(np.int32)).to(dev)
-            ew.register_batch(t_ids, t_off, B, F)
-            pooled = ew.serve_pull()
-            got = pooled.cpu().numpy()
+            n_ids = torch.from_numpy(lid.view(np.int64).copy())
+            n_off = torch.from_numpy(loff.astype(np.int32))
+            n_g = torch.from_numpy(np.ascontiguousarray(g_all[rank::world]))
+            if graph and s >= 1:
+                t_ids.copy_(n_ids)
+                t_off.copy_(n_off)
+                g_local.copy_(n_g)
+                if cg is None:
+                    torch.cuda.synchronize()
+                    cg = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(cg, capture_error_mode="thread_local"):
+                        ew.register_batch(t_ids, t_off, B, F)
+                        ew.serve_pull(out_pooled=pooled)
+                        ew.apply_backward(g_local, 0.05, 0, flags=flags)
+                cg.replay()  # (capture itself does not run the kernels)
+            else:
+                t_ids, t_off, g_local = n_ids.to(dev), n_off.to(dev), n_g.to(dev)
+                ew.register_batch(t_ids, t_off, B, F)
+                pooled = ew.serve_pull()
+            if not (graph and s >= 1):
+                got = pooled.cpu().numpy()
+            else:
+                torch.cuda.synchronize()
+                got = pooled.cpu().numpy()
             want = pooled_exp[rank::world]
             assert got.tobytes() == want.tobytes(), f"rank {rank} step {s}: pooled differs"
-            g_local = torch.from_numpy(np.ascontiguousarray(g_all[rank::world])).to(dev)
-            ok = ew.apply_backward(g_local, 0.05, s + 1)
-            assert ok
+            if not (graph and s >= 1):
+                ok = ew.apply_backward(g_local, 0.05, s + 1, flags=flags)
+                assert ok
             ok2, _ = exp.push_batch(world * B, F, gids, goffs.astype(np.uint64), g_all, 0.05,
                                     s + 1, read_versions=rv_exp, sample_keys=sk, agg=agg)
             assert ok2

@@ -69,3 +69,15 @@ def test_sharded_device_world2_large_plan(transport):
                     transport=transport)
     for r, status, n in res:
         assert status == "ok", status
+
+
+@pytest.mark.gpu
+def test_sharded_p2p_cuda_graph_replay():
+    """The peer-transport step has no host round trip: captured once in a CUDA graph and
+    replayed on new inputs it stays bit-exact (device barrier epochs and step tags)."""
+    import torch
+
+    world = 2 if torch.cuda.device_count() >= 2 else 1
+    res = run_world(world, "nccl", use_device=True, transport="p2p", graph=True, steps=4, B=16)
+    for r, status, n in res:
+        assert status == "ok", status
