@@ -738,7 +738,7 @@ __global__ void x_owner_dyn_kernel(const XHdr* __restrict__ hdr,
       j = 0;
     }
     out_ids[k] = oids[r * stride + j];
-    out_rv[k] = orv[r * stride + j];
+    if (orv) out_rv[k] = orv[r * stride + j];
   }
 }
 struct PeerRows {
@@ -838,7 +838,7 @@ __global__ void __launch_bounds__(256)
     } else {
       for (uint32_t d = ln; d < D; d += L) dst_base[j * D + d] = ok ? row[d] : 0.0f;
     }
-    if (ln == 0) orv[r * stride + j] = ok ? t.vt[s].x : 0;
+    if (ln == 0 && orv) orv[r * stride + j] = ok ? vt_read(t, s).x : 0;
   }
 }
 
@@ -923,7 +923,6 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
   // owner: find-or-init the ids every source asked for, rows straight back to them
   XHdr* mine = ph.h[x.rank];
   uint32_t* oslot = reinterpret_cast<uint32_t*>(x.arena + x.off_oslot);
-  uint64_t* orv = reinterpret_cast<uint64_t*>(x.arena + x.off_orv);
   Batch& b = t->scratch;
   batch_reserve(b, x.G * M, 0, 0);
   b.registered = false;
@@ -938,7 +937,9 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
   HPS_DISPATCH_DIM(t->d.D, {
     const uint32_t bx = static_cast<uint32_t>(std::max<uint64_t>(
         1, std::min<uint64_t>(ceil_div(M, 256 / L), uint64_t(t->sm_count) * 16 / x.G + 1)));
-    x_owner_gather_kernel<V, L, G><<<dim3(bx, x.G), 256, 0, st>>>(t->d, oslot, M, mine, pr, orv);
+    // (no read versions: the owner applies in fresh mode, see xbatch_bwd)
+    x_owner_gather_kernel<V, L, G><<<dim3(bx, x.G), 256, 0, st>>>(t->d, oslot, M, mine, pr,
+                                                                   nullptr);
   });
   HPS_LAUNCH_CHECK();
   barrier(x, t, st);  // every owner's rows have landed in this rank's rows buffer
@@ -981,16 +982,21 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
   grow(xs.off, xs.cap_off, cap + 1);
   x_owner_dyn_kernel<<<grid_n(cap + 1, t->sm_count), kXBlock, 0, st>>>(
       mine, reinterpret_cast<const uint32_t*>(x.arena + x.off_ocnt), x.G, M,
-      reinterpret_cast<const uint64_t*>(x.arena + x.off_oids),
-      reinterpret_cast<const uint64_t*>(x.arena + x.off_orv),
+      reinterpret_cast<const uint64_t*>(x.arena + x.off_oids), nullptr,
       reinterpret_cast<const uint32_t*>(x.arena + x.off_ppos), cap, xs.ids, xs.rv, xs.off,
       t->d.ctr + kCtrProtocol);
   HPS_LAUNCH_CHECK();
   Batch& b = t->scratch;
   b.agg = HPS_SUM;
   batch_register(b, xs.ids, cap, xs.off, static_cast<uint32_t>(cap), 1, nullptr, st, true);
+  // Fresh mode: every pair's read version is the row's version before this apply. The
+  // forward read the rows at their current versions and nothing mutates this table
+  // between a step's forward and its apply (one batch in flight per exchange), so this
+  // is the version the forward read -- without carrying it through the arena.
+  b.pulled = true;
+  b.rv_valid = false;
   batch_push(b, HPS_SUM, reinterpret_cast<const float*>(x.arena + x.off_contrib), lr, step_tag,
-             epoch, 0, xs.rv, accepted, flags, st);
+             epoch, 0, nullptr, accepted, flags, st);
 }
 
 }  // namespace hps

@@ -248,9 +248,10 @@ __global__ void lazy_init_kernel(DevTable t, const uint32_t* __restrict__ new_sl
     float* row = t.rows + static_cast<uint64_t>(slot) * t.stride;
     for (uint32_t d = lane; d < t.D; d += 32) {
       row[d] = init_value(seed, d, lo, span);
-      row[t.D + d] = 0.0f;
+      // svt: version 0, tag kNoStep (all ones) -> sign bits of elements 4l+2, 4l+3
+      row[t.D + d] = (t.svt && d < 64 && (d & 3) >= 2) ? -0.0f : 0.0f;
     }
-    if (lane == 0) t.vt[slot] = make_uint2(0u, kNoStep);
+    if (lane == 0 && !t.svt) t.vt[slot] = make_uint2(0u, kNoStep);
   }
 }
 
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(256)
         const bool ok = slot_ok(t, s[u]);
         if (ok) load_vec<V>(t.rows + static_cast<uint64_t>(s[u]) * t.stride + ln * V, r[u]);
         else for (int k = 0; k < V; ++k) r[u][k] = 0.0f;
-        ver[u] = (out_ver && ok && ln == 0) ? t.vt[s[u]].x : 0u;
+        ver[u] = (out_ver && ok && ln == 0) ? vt_read(t, s[u]).x : 0u;
       }
 #pragma unroll
       for (int u = 0; u < kGatherILP; ++u) {
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(256)
         const bool ok = slot_ok(t, s[u]);
         const float* row = t.rows + static_cast<uint64_t>(ok ? s[u] : 0) * t.stride;
         for (uint32_t d = ln; d < D; d += L) out[i * D + d] = ok ? row[d] : 0.0f;
-        if (out_ver && ln == 0) out_ver[i] = ok ? t.vt[s[u]].x : 0;
+        if (out_ver && ln == 0) out_ver[i] = ok ? vt_read(t, s[u]).x : 0;
       }
     }
   }
@@ -339,10 +340,10 @@ __global__ void peek_kernel(DevTable t, const uint64_t* __restrict__ ids, uint64
     const float* row = t.rows + static_cast<uint64_t>(ok ? s : 0) * t.stride;
     for (uint32_t d = lane; d < t.D; d += 32) {
       if (out_w) out_w[i * t.D + d] = ok ? row[d] : 0.0f;
-      if (out_acc) out_acc[i * t.D + d] = ok ? row[t.D + d] : 0.0f;
+      if (out_acc) out_acc[i * t.D + d] = ok ? (t.svt ? fabsf(row[t.D + d]) : row[t.D + d]) : 0.0f;
     }
     if (lane == 0) {
-      if (out_ver) out_ver[i] = ok ? t.vt[s].x : 0;
+      if (out_ver) out_ver[i] = ok ? vt_read(t, s).x : 0;
       if (out_present) out_present[i] = ok ? 1 : 0;
     }
   }
@@ -397,17 +398,20 @@ __global__ void __launch_bounds__(256)
   for (uint64_t r0 = G::group(); r0 < rows; r0 += groups * kCheckILP) {
     float x[kCheckILP][V];
     uint32_t n[kCheckILP];
+    // Rows are walked last to first: the update that follows reads the gradients first
+    // to last, so the rows it needs first are the ones this pass left most recently in
+    // L2 (the gradient block is about the size of L2).
 #pragma unroll
     for (int u = 0; u < kCheckILP; ++u) {
-      const uint64_t r = r0 + u * groups;
-      n[u] = r < rows ? __ldg(offsets + r + 1) - __ldg(offsets + r) : 0u;
+      const uint64_t q = r0 + u * groups, r = rows - 1 - q;
+      n[u] = q < rows ? __ldg(offsets + r + 1) - __ldg(offsets + r) : 0u;
     }
     for (int c = 0; c < chunks; ++c) {
       const uint32_t d0 = c * G::kSpan + ln * V;
 #pragma unroll
       for (int u = 0; u < kCheckILP; ++u) {
-        const uint64_t r = r0 + u * groups;
-        if (n[u] && (!kGuard || d0 < D)) load_vec_cs<V>(grads + r * D + d0, x[u]);
+        const uint64_t r = rows - 1 - (r0 + u * groups);
+        if (n[u] && (!kGuard || d0 < D)) load_vec<V>(grads + r * D + d0, x[u]);  // keep in L2
         else for (int j = 0; j < V; ++j) x[u][j] = 0.0f;
       }
 #pragma unroll

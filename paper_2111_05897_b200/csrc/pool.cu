@@ -69,7 +69,7 @@ __device__ void pool_general(const DevTable& t, const uint32_t* __restrict__ slo
         acc[k] = __dadd_rn(acc[k], static_cast<double>(r1[k]));
       }
       if (want_rv && c == 0 && ln == 0) {
-        uint32_t v0 = slot_ok(t, s0) ? t.vt[s0].x : 0, v1 = slot_ok(t, s1) ? t.vt[s1].x : 0;
+        uint32_t v0 = slot_ok(t, s0) ? vt_read(t, s0).x : 0, v1 = slot_ok(t, s1) ? vt_read(t, s1).x : 0;
         if (out_rv64) out_rv64[i] = v0, out_rv64[i + 1] = v1;
         if (out_rv32) out_rv32[i] = v0, out_rv32[i + 1] = v1;
       }
@@ -82,7 +82,7 @@ __device__ void pool_general(const DevTable& t, const uint32_t* __restrict__ slo
 #pragma unroll
       for (int k = 0; k < V; ++k) acc[k] = __dadd_rn(acc[k], static_cast<double>(r0[k]));
       if (want_rv && c == 0 && ln == 0) {
-        uint32_t v0 = slot_ok(t, s0) ? t.vt[s0].x : 0;
+        uint32_t v0 = slot_ok(t, s0) ? vt_read(t, s0).x : 0;
         if (out_rv64) out_rv64[i] = v0;
         if (out_rv32) out_rv32[i] = v0;
       }
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256, 6)
         const bool ok = slot_ok(t, s[u]);
         if (ok) load_vec<V>(t.rows + static_cast<uint64_t>(s[u]) * t.stride + ln * V, r[u]);
         else for (int k = 0; k < V; ++k) r[u][k] = 0.0f;
-        ver[u] = (want_rv && ok && ln == 0) ? t.vt[s[u]].x : 0u;
+        ver[u] = (want_rv && ok && ln == 0) ? vt_read(t, s[u]).x : 0u;
       }
 #pragma unroll
       for (int u = 0; u < kPoolILP; ++u) {
@@ -173,7 +173,7 @@ __global__ void snapshot_rv_kernel(DevTable t, const uint32_t* __restrict__ slot
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t s = slots[i];
-    rv[i] = slot_ok(t, s) ? t.vt[s].x : 0u;
+    rv[i] = slot_ok(t, s) ? vt_read(t, s).x : 0u;
   }
 }
 

@@ -212,7 +212,8 @@ Table* table_create(const hps_table_cfg& cfg) {
     d.ht_mask = H - 1;
     d.ht_shift = 64 - lg;
     d.D = cfg.embedding_dim;
-    d.stride = row_stride_floats(cfg.embedding_dim);
+    d.svt = uses_svt(cfg.embedding_dim, cfg.optimizer);
+    d.stride = row_stride_floats(cfg.embedding_dim, d.svt);
     d.capacity = static_cast<uint32_t>(C);
     d.S = cfg.shard_count;
     d.opt = cfg.optimizer;

@@ -63,7 +63,15 @@ struct VtView {
 // 5 lines (640 B) and its weight vector exactly lines 0-1. The unpadded 528-byte pitch
 // made the pool's 256-byte weight read touch 3 lines (160 MB of DRAM reads for 109 MB
 // algorithmic per C2 step, profiles/r1_ncu_full_c2.txt).
-inline uint32_t row_stride_floats(uint32_t D) {
+// Adagrad tables with D in {64, 128} keep {version, tag} in the sign bits of the first 64
+// optimizer-state floats instead of a header (svt): the accumulator is a sum of squares,
+// so its sign bit is otherwise always 0, and the update -- which reads and writes every
+// accumulator anyway -- saves a whole extra random line per row (23 us of 132 us per C2
+// step, measured). Rows are then exactly [w D | acc D] = 512 B (D=64).
+inline bool uses_svt(uint32_t D, int opt) { return opt == HPS_ADAGRAD && (D == 64 || D == 128); }
+
+inline uint32_t row_stride_floats(uint32_t D, bool svt = false) {
+  if (svt) return 2 * D;
   uint32_t bytes = 8 * D + 16;
   if (bytes >= 128) return ((bytes + 127) / 128) * 32;
   uint32_t p = 16;
@@ -79,7 +87,8 @@ struct DevTable {
   float* rows;
   uint32_t D;
   uint32_t stride;  // floats per row: row_stride_floats(D) ([w D | acc D | header 16 B | pad])
-  VtView vt;        // {version, latest bump tag} in each row's header
+  VtView vt;        // {version, latest bump tag} in each row's header (unless svt)
+  bool svt;         // versions in the accumulators' sign bits (uses_svt)
   // Batch-plan bitmaps, one bit per slot (2 x capacity/8 bytes: L2-resident): `seen`
   // = listed by the batch being planned, `multi` = listed more than once (plan.cu).
   uint32_t* seen;
@@ -209,6 +218,28 @@ struct Table {
   unsigned long long* h_ctr = nullptr;  // pinned mirror of the counters
   XScratch xs;
 };
+
+#ifdef __CUDACC__
+// svt encoding: accumulator element 4l + k (l < 16) carries, in its sign bit, bit l of
+// k = 0: version low half, 1: version high half, 2: tag low half, 3: tag high half.
+__device__ __forceinline__ uint32_t sign_of(float x) { return __float_as_uint(x) >> 31; }
+__device__ __forceinline__ float with_sign(float mag, uint32_t bit) {
+  return __uint_as_float((__float_as_uint(mag) & 0x7fffffffu) | (bit << 31));
+}
+// One thread reads a row's {version, tag} (header, or the 64 sign bits).
+__device__ __forceinline__ uint2 vt_read(const DevTable& t, uint32_t s) {
+  if (!t.svt) return t.vt[s];
+  const float4* a = reinterpret_cast<const float4*>(t.rows + static_cast<uint64_t>(s) * t.stride + t.D);
+  uint32_t ver = 0, tag = 0;
+#pragma unroll
+  for (int l = 0; l < 16; ++l) {
+    const float4 q = a[l];
+    ver |= (sign_of(q.x) << l) | (sign_of(q.y) << (16 + l));
+    tag |= (sign_of(q.z) << l) | (sign_of(q.w) << (16 + l));
+  }
+  return make_uint2(ver, tag);
+}
+#endif
 
 // ---- kernels / launchers (kernels.cu, update.cu) ---------------------------------------
 // Owner side of the peer exchange: slots[r * stride + j] = find_or_insert(ids[r * stride + j])

@@ -24,7 +24,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhps.so")
+# HPS_LIB: an alternative build of the same library (profiling experiments only)
+LIB_PATH = os.environ.get("HPS_LIB") or os.path.join(_HERE, "libhps.so")
 
 # ---- errors (errors.hpp:22-107) ------------------------------------------------------
 
