@@ -398,20 +398,17 @@ __global__ void __launch_bounds__(256)
   for (uint64_t r0 = G::group(); r0 < rows; r0 += groups * kCheckILP) {
     float x[kCheckILP][V];
     uint32_t n[kCheckILP];
-    // Rows are walked last to first: the update that follows reads the gradients first
-    // to last, so the rows it needs first are the ones this pass left most recently in
-    // L2 (the gradient block is about the size of L2).
 #pragma unroll
     for (int u = 0; u < kCheckILP; ++u) {
-      const uint64_t q = r0 + u * groups, r = rows - 1 - q;
-      n[u] = q < rows ? __ldg(offsets + r + 1) - __ldg(offsets + r) : 0u;
+      const uint64_t r = r0 + u * groups;
+      n[u] = r < rows ? __ldg(offsets + r + 1) - __ldg(offsets + r) : 0u;
     }
     for (int c = 0; c < chunks; ++c) {
       const uint32_t d0 = c * G::kSpan + ln * V;
 #pragma unroll
       for (int u = 0; u < kCheckILP; ++u) {
-        const uint64_t r = rows - 1 - (r0 + u * groups);
-        if (n[u] && (!kGuard || d0 < D)) load_vec<V>(grads + r * D + d0, x[u]);  // keep in L2
+        const uint64_t r = r0 + u * groups;
+        if (n[u] && (!kGuard || d0 < D)) load_vec_cs<V>(grads + r * D + d0, x[u]);
         else for (int j = 0; j < V; ++j) x[u][j] = 0.0f;
       }
 #pragma unroll
