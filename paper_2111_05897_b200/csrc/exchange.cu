@@ -440,6 +440,7 @@ XBatch::~XBatch() {
   for (uint32_t r = 0; r < G && r < kMaxWorld; ++r)
     if (peer[r] && peer[r] != arena) cudaIpcCloseMemHandle(peer[r]);
   if (arena) cudaFree(arena);
+  if (side) cudaStreamDestroy(side);
   if (xbase) cudaFree(xbase);
   if (dev_epoch) cudaFree(dev_epoch);
   void* ps[] = {hkeys,  hidx,   hval,   hmul,    dest,    sendpos, spair, offsets, lgrp,
@@ -533,10 +534,14 @@ static void pairs_core(XBatch& x, const uint32_t** spos_out, const uint32_t** sl
   const uint32_t* n_multi = x.cnt + kCntMulti;
   // small path: rank sort of the multi listings' composite keys (no-op when large)
   radix::sort_composite_small(x.mkeys, n_multi, x.lbits, x.sm_pos, x.sm_list, st);
-  // large path: stable radix sort of every listing by send position (no-op when small)
-  const bool in_b = radix::sort_pairs<uint32_t>(x.keys_a, x.vals_a, x.keys_b, x.vals_b, n,
-                                                x.lbits, x.scratch, st, x.sms, n_multi,
-                                                x.sendpos, true);
+  // large path: stable radix sort of every listing by send position, only when the
+  // device count says so (a conditional graph node under capture)
+  const bool in_b = ((x.lbits + radix::kBits - 1) / radix::kBits) & 1;
+  radix::sort_scratch_zero(x.scratch, st);
+  run_if(x.side, st, n_multi, false, radix::kSmallN, [&](cudaStream_t s) {
+    radix::sort_pairs<uint32_t>(x.keys_a, x.vals_a, x.keys_b, x.vals_b, n, x.lbits, x.scratch,
+                                s, x.sms, n_multi, x.sendpos, true, false);
+  });
   uint32_t* spos = in_b ? x.keys_b : x.keys_a;
   uint32_t* slist = in_b ? x.vals_b : x.vals_a;
   x_pick_small_kernel<<<ceil_div(radix::kSmallN, kXBlock), kXBlock, 0, st>>>(

@@ -369,7 +369,7 @@ template <typename K>
 inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b, uint64_t n,
                        int key_bits, uint32_t* scratch, cudaStream_t stream, int sms = 148,
                        const uint32_t* gate = nullptr, const K* keys_in0 = nullptr,
-                       bool iota_vals = false) {
+                       bool iota_vals = false, bool zero_scratch = true) {
   if (n == 0) return false;
   if (key_bits <= 0) key_bits = 1;
   set_smem_attrs<K>();
@@ -388,8 +388,9 @@ inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b,
   uint32_t* tile_ctr = hist + kMaxPasses * kBins;  // [kMaxPasses * 2]
   uint64_t off = (kMaxPasses * kBins + kMaxPasses * 2 + 1) & ~1ull;
   unsigned long long* status = reinterpret_cast<unsigned long long*>(scratch + off);
-  HPS_CUDA(cudaMemsetAsync(scratch, 0, (kMaxPasses * kBins + kMaxPasses * 2) * sizeof(uint32_t),
-                           stream));
+  if (zero_scratch)  // (else the caller zeroed it: see sort_scratch_zero)
+    HPS_CUDA(cudaMemsetAsync(scratch, 0,
+                             (kMaxPasses * kBins + kMaxPasses * 2) * sizeof(uint32_t), stream));
   const uint32_t n32 = static_cast<uint32_t>(n);
   const uint32_t hblocks = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms) * 4);
   hist_kernel<K><<<hblocks, kBlock, 0, stream>>>(first, n32, passes, hist, gate);
@@ -406,6 +407,13 @@ inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b,
   }
   HPS_LAUNCH_CHECK_N(1 + passes);
   return in_b;
+}
+
+// The large path's scratch counters, zeroed ahead of a sort_pairs(zero_scratch = false)
+// (a sort captured inside a conditional graph body launches kernels only).
+inline void sort_scratch_zero(uint32_t* scratch, cudaStream_t stream) {
+  HPS_CUDA(cudaMemsetAsync(scratch, 0, (kMaxPasses * kBins + kMaxPasses * 2) * sizeof(uint32_t),
+                           stream));
 }
 
 // The small composite path (see small_composite_kernel).

@@ -300,6 +300,7 @@ void table_destroy(Table* t) {
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (t->h_ctr) cudaFreeHost(t->h_ctr);
+    if (t->side) cudaStreamDestroy(t->side);
   }
   delete t;
 }
@@ -454,15 +455,40 @@ static int slot_key_bits(const Table* t) {
 // contiguous run in apply order. keys_in0 = slots to sort (else keys_a); iota: the
 // listings are the positions 0..N-1 (else vals_a); gate = device-side condition
 // (radix_sort.cuh).
+__global__ void set_cond_kernel(cudaGraphConditionalHandle h, const void* val, int is64,
+                                unsigned long long thresh) {
+  const unsigned long long v =
+      is64 ? *static_cast<const unsigned long long*>(val) : *static_cast<const uint32_t*>(val);
+  cudaGraphSetConditional(h, v > thresh ? 1u : 0u);
+}
+
+void launch_set_cond(cudaGraphConditionalHandle h, const void* val, bool is64,
+                     unsigned long long thresh, cudaStream_t st) {
+  set_cond_kernel<<<1, 1, 0, st>>>(h, val, is64 ? 1 : 0, thresh);
+  HPS_LAUNCH_CHECK();
+}
+
 static void sort_slots(Batch& b, const uint32_t* keys_in0, bool iota, const uint32_t* gate,
                        cudaStream_t st) {
   Table* t = b.table;
   ProfScope p(t, "sort", st);
-  bool in_b = radix::sort_pairs<uint32_t>(b.keys_a, b.vals_a, b.keys_b, b.vals_b, b.N,
-                                          slot_key_bits(t), b.hist, st, t->sm_count, gate,
-                                          keys_in0, iota);
-  b.sorted_slot = in_b ? b.keys_b : b.keys_a;
-  b.sorted_listing = in_b ? b.vals_b : b.vals_a;
+  const int kb = slot_key_bits(t);
+  const int passes = (kb + radix::kBits - 1) / radix::kBits;
+  b.sorted_slot = (passes & 1) ? b.keys_b : b.keys_a;
+  b.sorted_listing = (passes & 1) ? b.vals_b : b.vals_a;
+  auto sort = [&](cudaStream_t s, bool zero) {
+    bool in_b = radix::sort_pairs<uint32_t>(b.keys_a, b.vals_a, b.keys_b, b.vals_b, b.N, kb,
+                                            b.hist, s, t->sm_count, gate, keys_in0, iota, zero);
+    b.sorted_slot = in_b ? b.keys_b : b.keys_a;
+    b.sorted_listing = in_b ? b.vals_b : b.vals_a;
+  };
+  if (!gate) {
+    sort(st, true);
+    return;
+  }
+  // gated large path (device count of multi listings > kSmallN): a conditional node
+  radix::sort_scratch_zero(b.hist, st);
+  run_if(t->side, st, gate, false, radix::kSmallN, [&](cudaStream_t s) { sort(s, false); });
 }
 
 // EmbeddingWorker::register_sample for a whole batch + the route/dedup/probe half of
@@ -605,8 +631,10 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   }
   // Exact validation (dry runs), executed only if the bound check was inconclusive.
   a.dry_run = 1;
-  if (!b.all_multi) launch_update_single(t->d, a, t->sm_count, st);
-  launch_update(t->d, a, false, t->sm_count, st);
+  run_if(t->side, st, t->d.ctr + kCtrNeedExact, true, 0, [&](cudaStream_t s) {
+    if (!b.all_multi) launch_update_single(t->d, a, t->sm_count, s);
+    launch_update(t->d, a, false, t->sm_count, s);
+  });
   a.dry_run = 0;
   if (!b.all_multi) {
     ProfScope p(t, "update", st);

@@ -210,6 +210,7 @@ struct Table {
   uint32_t epoch = 0;
   uint32_t sm_count = 148;
   std::mutex mu;  // one call at a time per table (PsShard's per-shard lock)
+  cudaStream_t side = nullptr;  // captures the bodies of conditional graph nodes
   Batch scratch;  // workspace for the stateless entry points
   StagePool stage;
   // Batches pulled but not yet pushed. Their read versions are only materialised

@@ -46,6 +46,51 @@ class Stager {
   bool sync_needed_ = false;
 };
 
+// ---- device-decided work (table.cu) ----------------------------------------------------
+void launch_set_cond(cudaGraphConditionalHandle h, const void* val, bool is64,
+                     unsigned long long thresh, cudaStream_t st);
+
+// Eager: `body` is launched on st as is (its kernels read the gate themselves and exit
+// when it is closed). Under CUDA-graph capture: a conditional IF node whose body graph is
+// captured from `body`, switched by a one-thread kernel comparing *val (u32 or u64) with
+// thresh -- a closed gate then costs no launches at all. `side` is a stream owned by the
+// caller (used for the body's capture only).
+template <class Fn>
+void run_if(cudaStream_t& side, cudaStream_t st, const void* val, bool is64,
+            unsigned long long thresh, Fn&& body) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  HPS_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusActive) {
+    body(st);
+    return;
+  }
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  unsigned long long id = 0;
+  HPS_CUDA(cudaStreamGetCaptureInfo(st, &cs, &id, &g, &deps, &nd));
+  cudaGraphConditionalHandle h;
+  HPS_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+  launch_set_cond(h, val, is64, thresh, st);
+  HPS_CUDA(cudaStreamGetCaptureInfo(st, &cs, &id, &g, &deps, &nd));
+  cudaGraphNodeParams p{};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeIf;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  HPS_CUDA(cudaGraphAddNode(&node, g, deps, nd, &p));
+  if (!side) HPS_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  HPS_CUDA(cudaStreamBeginCaptureToGraph(side, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeThreadLocal));
+  const uint64_t l0 = g_launches.load();
+  body(side);
+  g_launches.store(l0);  // a conditional body only runs when its gate opens
+  cudaGraph_t body_graph = nullptr;
+  HPS_CUDA(cudaStreamEndCapture(side, &body_graph));
+  HPS_CUDA(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+}
+
 Table* table_create(const hps_table_cfg& cfg);
 void table_destroy(Table* t);
 void table_clear(Table* t, cudaStream_t st);
@@ -117,6 +162,7 @@ struct XBatch {
   unsigned long long* mkeys = nullptr;
   uint32_t *sm_pos = nullptr, *sm_list = nullptr;
   uint64_t* h_buf = nullptr;
+  cudaStream_t side = nullptr;  // captures conditional graph bodies
   // peer (NVLink) transport
   uint8_t* arena = nullptr;
   uint8_t* peer[kMaxWorld] = {};

@@ -547,3 +547,78 @@ def test_cuda_graph_replay_matches_oracle(hps):
     np.testing.assert_array_equal(w[p], wo[po_])
     np.testing.assert_array_equal(a[p], ao[po_])
     np.testing.assert_array_equal(v[p], vo[po_])
+
+
+def _graph_case(hps, B, F, D, space, agg, opt, grad_fn, steps=3, seed=5):
+    """Register/pull/push captured once in a CUDA graph and replayed on new inputs copied
+    into the captured buffers; bit-exact with the oracle stepping eagerly."""
+    import torch
+
+    import oracle as O
+    from paper_2111_05897_b200 import workloads as W
+
+    rng = np.random.default_rng(seed)
+    salts = [W.mix64_int(3 + s) for s in range(4)]
+    orc = O.Restatement(salts, D, "adagrad" if opt == hps.ADAGRAD else "sgd")
+    t = hps.ShardSet(4, D, 1 << 16, opt, salts=salts)
+    ew = hps.EmbeddingWorker(t, agg)
+    dev = torch.device("cuda:0")
+    offs = np.arange(B * F + 1, dtype=np.uint32) * 2  # two listings per group
+    N = int(offs[-1])
+    ids_t = torch.zeros(N, dtype=torch.int64, device=dev)
+    offs_t = torch.from_numpy(offs.view(np.int32)).to(dev)
+    g_t = torch.zeros((B, F, D), dtype=torch.float32, device=dev)
+    pooled_t = torch.zeros((B, F, D), dtype=torch.float32, device=dev)
+    aggs = "mean" if agg == hps.MEAN else "sum"
+
+    def step(s):
+        ew.register_batch(ids_t, offs_t, B, F, stream=s)
+        ew.serve_pull(out_pooled=pooled_t, stream=s)
+        ew.apply_backward(g_t, 0.05, flags=hps.ASYNC | hps.DEVICE_STEP, stream=s)
+
+    graph = None
+    for k in range(steps):
+        ids = rng.integers(0, space, N).astype(np.uint64)
+        g = grad_fn(rng, (B, F, D))
+        ids_t.copy_(torch.from_numpy(ids.view(np.int64)))
+        g_t.copy_(torch.from_numpy(g))
+        if k == 0:
+            step(torch.cuda.current_stream())
+        else:
+            if graph is None:
+                torch.cuda.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+                    step(torch.cuda.current_stream())
+            graph.replay()
+        torch.cuda.synchronize()
+        po, rvo = orc.pull_batch(B, F, ids, offs.astype(np.uint64), aggs)
+        assert pooled_t.cpu().numpy().tobytes() == po.tobytes(), f"step {k}"
+        orc.push_batch(B, F, ids, offs.astype(np.uint64), g, 0.05, k + 1, read_versions=rvo,
+                       agg=aggs)
+    t.sync()
+    keys = np.arange(space, dtype=np.uint64)
+    w, a, v, p = t.peek(keys)
+    wo, ao, vo, po_ = orc.peek(keys)
+    assert (p == po_).all()
+    np.testing.assert_array_equal(w[p], wo[po_])
+    np.testing.assert_array_equal(a[p], ao[po_])
+    np.testing.assert_array_equal(v[p], vo[po_])
+
+
+def test_cuda_graph_large_plan_conditional(hps):
+    """> 4096 listings of repeated rows: the radix-sort path runs inside a conditional
+    graph node on every replay."""
+    _graph_case(hps, 1024, 4, 64, 1500, hps.MEAN, hps.ADAGRAD,
+                lambda r, sh: (r.standard_normal(sh) * 0.1).astype(np.float32))
+
+
+def test_cuda_graph_need_exact_conditional(hps):
+    """Gradients near the float range make the bound check inconclusive: the exact dry
+    run executes inside its conditional graph node (and passes), then the update runs."""
+    def huge(r, sh):
+        g = (r.standard_normal(sh) * 0.1).astype(np.float32)
+        g[:, 0, 0] = np.float32(1e38)
+        g[:, 1, 0] = np.float32(-1e38)
+        return g
+    _graph_case(hps, 64, 4, 16, 40, hps.SUM, hps.SGD, huge)
