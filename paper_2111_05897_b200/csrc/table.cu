@@ -301,6 +301,9 @@ void table_destroy(Table* t) {
       if (p) cudaFree(p);
     if (t->h_ctr) cudaFreeHost(t->h_ctr);
     if (t->side) cudaStreamDestroy(t->side);
+    if (t->aux) cudaStreamDestroy(t->aux);
+    if (t->ev_fork) cudaEventDestroy(t->ev_fork);
+    if (t->ev_join) cudaEventDestroy(t->ev_join);
   }
   delete t;
 }
@@ -637,10 +640,27 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   });
   a.dry_run = 0;
   if (!b.all_multi) {
-    ProfScope p(t, "update", st);
-    launch_update_single(t->d, a, t->sm_count, st);
-  }
-  {
+    // Rows listed more than once (ordered chains, latency-bound, few) and rows listed
+    // once are disjoint: the multi chains run on a second stream beside the single pass
+    // (fork/join events; under graph capture two parallel branches).
+    if (!t->aux) {
+      HPS_CUDA(cudaStreamCreateWithFlags(&t->aux, cudaStreamNonBlocking));
+      HPS_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
+      HPS_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
+    }
+    HPS_CUDA(cudaEventRecord(t->ev_fork, st));
+    HPS_CUDA(cudaStreamWaitEvent(t->aux, t->ev_fork, 0));
+    {
+      ProfScope p(t, "update_multi", t->aux);
+      launch_update(t->d, a, false, t->sm_count, t->aux);
+    }
+    {
+      ProfScope p(t, "update", st);
+      launch_update_single(t->d, a, t->sm_count, st);
+    }
+    HPS_CUDA(cudaEventRecord(t->ev_join, t->aux));
+    HPS_CUDA(cudaStreamWaitEvent(st, t->ev_join, 0));
+  } else {
     ProfScope p(t, "update_multi", st);
     launch_update(t->d, a, false, t->sm_count, st);
   }

@@ -211,6 +211,8 @@ struct Table {
   uint32_t sm_count = 148;
   std::mutex mu;  // one call at a time per table (PsShard's per-shard lock)
   cudaStream_t side = nullptr;  // captures the bodies of conditional graph nodes
+  cudaStream_t aux = nullptr;   // update_multi beside update_single
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   Batch scratch;  // workspace for the stateless entry points
   StagePool stage;
   // Batches pulled but not yet pushed. Their read versions are only materialised
