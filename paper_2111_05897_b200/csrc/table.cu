@@ -505,19 +505,8 @@ static void ensure_aux(Table* t) {
 
 // Work on st that reads or changes the batch plan (or its bitmaps) waits for the last
 // plan built on the aux stream.
-// Only within the same capture (or both outside any): a plan recorded eagerly before a
-// capture began has completed (capture starts from an idle device), and an event recorded
-// inside a capture cannot be waited on from outside it.
-static unsigned long long capture_id(cudaStream_t st) {
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  unsigned long long id = 0;
-  HPS_CUDA(cudaStreamGetCaptureInfo(st, &cs, &id, nullptr, nullptr, nullptr));
-  return cs == cudaStreamCaptureStatusActive ? id : 0ull;
-}
-
 void wait_plan(Table* t, cudaStream_t st) {
-  if (t->plan_pending && capture_id(st) == t->plan_capture)
-    HPS_CUDA(cudaStreamWaitEvent(st, t->ev_plan, 0));
+  if (t->plan_pending) HPS_CUDA(cudaStreamWaitEvent(st, t->ev_plan, 0));
 }
 
 // EmbeddingWorker::register_sample for a whole batch + the route/dedup/probe half of
@@ -600,7 +589,6 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     sort_slots(b, b.slot, true, &b.small[0], ps);
     HPS_CUDA(cudaEventRecord(t->ev_plan, ps));
     t->plan_pending = true;
-    t->plan_capture = capture_id(st);
   }
   b.registered = true;
   b.pulled = false;
@@ -711,7 +699,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
 uint64_t batch_pairs(Batch& b) {
   if (!b.registered) return 0;
   Table* t = b.table;
-  if (t->plan_pending && t->plan_capture == 0) HPS_CUDA(cudaEventSynchronize(t->ev_plan));
+  if (t->plan_pending) HPS_CUDA(cudaEventSynchronize(t->ev_plan));
   HPS_CUDA(cudaMemset(t->d.ctr + kCtrScratch, 0, sizeof(unsigned long long)));
   launch_count_pairs(plan_args(b), t->d.ctr + kCtrScratch, nullptr);
   unsigned long long p = 0;

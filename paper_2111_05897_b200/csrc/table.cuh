@@ -215,7 +215,6 @@ struct Table {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_plan = nullptr;  // last batch plan built on aux (see wait_plan)
   bool plan_pending = false;
-  unsigned long long plan_capture = 0;  // capture id ev_plan was recorded in (0 = eager)
   Batch scratch;  // workspace for the stateless entry points
   StagePool stage;
   // Batches pulled but not yet pushed. Their read versions are only materialised
