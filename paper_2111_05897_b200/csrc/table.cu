@@ -304,7 +304,6 @@ void table_destroy(Table* t) {
     if (t->aux) cudaStreamDestroy(t->aux);
     if (t->ev_fork) cudaEventDestroy(t->ev_fork);
     if (t->ev_join) cudaEventDestroy(t->ev_join);
-    if (t->ev_plan) cudaEventDestroy(t->ev_plan);
   }
   delete t;
 }
@@ -495,20 +494,6 @@ static void sort_slots(Batch& b, const uint32_t* keys_in0, bool iota, const uint
   run_if(t->side, st, gate, false, radix::kSmallN, [&](cudaStream_t s) { sort(s, false); });
 }
 
-static void ensure_aux(Table* t) {
-  if (t->aux) return;
-  HPS_CUDA(cudaStreamCreateWithFlags(&t->aux, cudaStreamNonBlocking));
-  HPS_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
-  HPS_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
-  HPS_CUDA(cudaEventCreateWithFlags(&t->ev_plan, cudaEventDisableTiming));
-}
-
-// Work on st that reads or changes the batch plan (or its bitmaps) waits for the last
-// plan built on the aux stream.
-void wait_plan(Table* t, cudaStream_t st) {
-  if (t->plan_pending) HPS_CUDA(cudaStreamWaitEvent(st, t->ev_plan, 0));
-}
-
 // EmbeddingWorker::register_sample for a whole batch + the route/dedup/probe half of
 // serve_pull: after this, every listing has its slot (rows lazily initialised) and the
 // listings are grouped per row in apply order.
@@ -522,7 +507,6 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   forget_outstanding(b);
   b.rv_valid = false;
   batch_reserve(b, N, BF, B);
-  wait_plan(t, st);  // the previous batch's plan clears plan bits this probe sets
   Stager stg(t->stage);
   const uint64_t* d_ids = static_cast<const uint64_t*>(stg.in(ids, N * sizeof(uint64_t), st));
   if (!is_device_ptr(offsets)) {
@@ -570,25 +554,17 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     // Plan (plan.cu): rows listed once apply directly; the multi listings are ordered
     // by the small composite sort, or -- past kSmallN of them -- the whole batch is
     // slot-sorted instead. Both sorts are launched; the device count picks one.
-    // Only the push consumes the plan: it runs on the aux stream, beside the pull's
-    // pooling (which needs the slots only); batch_push and the next register wait for it.
     const int lbits = std::max(1, bits_for(N ? N - 1 : 0));
-    ensure_aux(t);
-    HPS_CUDA(cudaEventRecord(t->ev_fork, st));
-    HPS_CUDA(cudaStreamWaitEvent(t->aux, t->ev_fork, 0));
-    cudaStream_t ps = t->aux;
     {
-      ProfScope p(t, "plan", ps);
-      launch_classify(t->d, b.slot, N, lbits, b.kind, b.mkeys, &b.small[0], t->sm_count, ps);
+      ProfScope p(t, "plan", st);
+      launch_classify(t->d, b.slot, N, lbits, b.kind, b.mkeys, &b.small[0], t->sm_count, st);
     }
     {
-      ProfScope p(t, "sort_small", ps);
+      ProfScope p(t, "sort_small", st);
       radix::sort_composite_small(b.mkeys, &b.small[0], lbits, b.small_slot, b.small_listing,
-                                  ps);
+                                  st);
     }
-    sort_slots(b, b.slot, true, &b.small[0], ps);
-    HPS_CUDA(cudaEventRecord(t->ev_plan, ps));
-    t->plan_pending = true;
+    sort_slots(b, b.slot, true, &b.small[0], st);
   }
   b.registered = true;
   b.pulled = false;
@@ -621,7 +597,6 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
                 uint32_t flags, cudaStream_t st) {
   if (!b.registered) throw Error(HPS_E_STALE_SAMPLE, "push: batch not registered");
   Table* t = b.table;
-  wait_plan(t, st);
   if (epoch != t->epoch) {
     // PsShard::apply_gradients epoch fence (embedding_ps.hpp:142-145): drop every
     // (sample, unique id) entry of the batch, count them.
@@ -668,7 +643,11 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     // Rows listed more than once (ordered chains, latency-bound, few) and rows listed
     // once are disjoint: the multi chains run on a second stream beside the single pass
     // (fork/join events; under graph capture two parallel branches).
-    ensure_aux(t);
+    if (!t->aux) {
+      HPS_CUDA(cudaStreamCreateWithFlags(&t->aux, cudaStreamNonBlocking));
+      HPS_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
+      HPS_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
+    }
     HPS_CUDA(cudaEventRecord(t->ev_fork, st));
     HPS_CUDA(cudaStreamWaitEvent(t->aux, t->ev_fork, 0));
     {
@@ -699,7 +678,6 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
 uint64_t batch_pairs(Batch& b) {
   if (!b.registered) return 0;
   Table* t = b.table;
-  if (t->plan_pending) HPS_CUDA(cudaEventSynchronize(t->ev_plan));
   HPS_CUDA(cudaMemset(t->d.ctr + kCtrScratch, 0, sizeof(unsigned long long)));
   launch_count_pairs(plan_args(b), t->d.ctr + kCtrScratch, nullptr);
   unsigned long long p = 0;

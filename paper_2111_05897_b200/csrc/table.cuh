@@ -213,8 +213,6 @@ struct Table {
   cudaStream_t side = nullptr;  // captures the bodies of conditional graph nodes
   cudaStream_t aux = nullptr;   // update_multi beside update_single
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaEvent_t ev_plan = nullptr;  // last batch plan built on aux (see wait_plan)
-  bool plan_pending = false;
   Batch scratch;  // workspace for the stateless entry points
   StagePool stage;
   // Batches pulled but not yet pushed. Their read versions are only materialised

@@ -96,7 +96,6 @@ void run_if(cudaStream_t& side, cudaStream_t st, const void* val, bool is64,
   HPS_CUDA(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
 }
 
-void wait_plan(Table* t, cudaStream_t st);
 Table* table_create(const hps_table_cfg& cfg);
 void table_destroy(Table* t);
 void table_clear(Table* t, cudaStream_t st);
