@@ -275,7 +275,7 @@ void batch_free(Batch& b) {
   forget_outstanding(b);
   void* ptrs[] = {b.offsets, b.lgrp,  b.slot,   b.keys_a,  b.vals_a,
                   b.keys_b,  b.vals_b, b.rv,  b.new_slots, b.kind,  b.hist,
-                  b.mkeys,   b.small_slot, b.small_listing,
+                  b.mkeys,   b.hot, b.small_slot, b.small_listing,
                   b.small,   b.skeys_a, b.skeys_b, b.sperm_a, b.sperm_b, b.sstart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -389,6 +389,8 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
     ensure(b.kind, c, n);
     c = 0;
     ensure(b.mkeys, c, n);
+    c = 0;
+    ensure(b.hot, c, n / kHotRun + 1);
     size_t hw = radix::scratch_words<uint32_t>(n);
     if (hw > b.hist_cap) {
       c = 0;
@@ -639,6 +641,13 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     launch_update(t->d, a, false, t->sm_count, s);
   });
   a.dry_run = 0;
+  if (t->cfg.embedding_dim <= kHotMaxDim) {
+    // hot-row hand-off list (update_multi -> update_hot), counter in b.small[4]
+    a.hot = b.hot;
+    a.n_hot = &b.small[4];
+    a.hot_cap = static_cast<uint32_t>(b.N / kHotRun + 1);
+    HPS_CUDA(cudaMemsetAsync(a.n_hot, 0, sizeof(uint32_t), st));
+  }
   if (!b.all_multi) {
     // Rows listed more than once (ordered chains, latency-bound, few) and rows listed
     // once are disjoint: the multi chains run on a second stream beside the single pass
@@ -653,6 +662,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     {
       ProfScope p(t, "update_multi", t->aux);
       launch_update(t->d, a, false, t->sm_count, t->aux);
+      launch_update_hot(t->d, a, t->sm_count, t->aux);
     }
     {
       ProfScope p(t, "update", st);
@@ -663,6 +673,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   } else {
     ProfScope p(t, "update_multi", st);
     launch_update(t->d, a, false, t->sm_count, st);
+    launch_update_hot(t->d, a, t->sm_count, st);
   }
   if (flags & HPS_DEVICE_STEP) launch_add_counter_const(t->d.ctr, kCtrStep, 1, st);
   forget_outstanding(b);

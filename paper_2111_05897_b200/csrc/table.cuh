@@ -139,6 +139,7 @@ struct Batch {
   uint32_t* new_slots = nullptr;  // [N] rows inserted by register (lazy-init queue)
   uint8_t* kind = nullptr;        // [N] plan: 1 = row listed once, 2 = multi (sorted path)
   unsigned long long* mkeys = nullptr;  // [N] multi listings as (slot << lbits | listing)
+  uint32_t* hot = nullptr;        // [N / kHotRun + 1] sorted-list starts of hot rows
   uint32_t* small_slot = nullptr;       // [kSmallN] multi listings sorted (small path)
   uint32_t* small_listing = nullptr;
   uint32_t* hist = nullptr;       // sort / plan scratch
@@ -311,7 +312,15 @@ struct UpdateArgs {
   int tracked;
   int fresh;  // tracked, and no mutation since the pull: read version = current version
   int dry_run;  // compute + validate contributions only
+  // Hot rows (runs of >= kHotRun listings on the sorted path): update_multi hands them to
+  // update_hot (one block per row, contributions staged in shared memory); null = off.
+  uint32_t* hot;
+  uint32_t* n_hot;
+  uint32_t hot_cap;
 };
+constexpr uint32_t kHotRun = 64;
+constexpr uint32_t kHotMaxDim = 128;  // update_hot stages [256][D] floats in shared memory
+void launch_update_hot(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
 void launch_update(const DevTable& t, const UpdateArgs& a, bool direct, int sms, cudaStream_t st);
 void launch_update_single(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
 void launch_count_pairs(const UpdateArgs& a, unsigned long long* ctr, cudaStream_t st);

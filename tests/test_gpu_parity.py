@@ -126,9 +126,14 @@ def test_sync_two_workers_sample_keys(hps):
     _sync_vs_oracle(hps, B=33, F=2, D=8, S=2, opt="adagrad", agg="mean", steps=3, E=2, seed=4)
 
 
-def test_hot_rows_long_chains(hps):
-    # every row hit by hundreds of samples per step: the ordered per-row recurrence
-    _sync_vs_oracle(hps, B=2048, F=2, D=64, S=1, opt="adagrad", agg="mean", steps=2, seed=5,
+@pytest.mark.parametrize("D,opt,agg", [(64, "adagrad", "mean"), (16, "sgd", "sum"),
+                                       (5, "adagrad", "sum"), (128, "adagrad", "mean"),
+                                       (200, "sgd", "mean")])
+def test_hot_rows_long_chains(hps, D, opt, agg):
+    # every row hit by thousands of listings per step: hot rows (update_hot: contributions
+    # staged in shared memory, one thread per dimension for the ordered recurrence);
+    # D = 200 exceeds the staging limit and stays on the inline multi path
+    _sync_vs_oracle(hps, B=2048, F=2, D=D, S=1, opt=opt, agg=agg, steps=2, seed=5,
                     id_space=4, max_per_group=5)
 
 
