@@ -233,13 +233,22 @@ __global__ void __launch_bounds__(kBlock)
     if (cnt[i]) atomicAdd(&hist[i], cnt[i]);
 }
 
+// Optional output of the final pass (hps batch plan): meta.out[g] = lgrp[v] | (size of
+// group lgrp[v]) << 32 for the value v sorted to position g -- what the ordered update
+// reads per position, computed where the random lookups overlap the scatter.
+struct SortMeta {
+  const uint32_t* lgrp = nullptr;
+  const uint32_t* offsets = nullptr;
+  uint64_t* out = nullptr;
+};
+
 // vals_in == nullptr: values are the input positions (pass 0 of an index sort).
 template <typename K>
 __global__ void __launch_bounds__(kBlock)
     pass_kernel(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                 K* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t n, int shift,
                 const uint32_t* __restrict__ hist, unsigned long long* status, uint32_t* tile_ctr,
-                uint32_t epoch, const uint32_t* gate) {
+                uint32_t epoch, const uint32_t* gate, const SortMeta meta) {
   constexpr int kItems = Tile<K>::kItems;
   constexpr int kTileN = Tile<K>::kTile;
   if (!gate_open(gate)) return;
@@ -336,6 +345,10 @@ __global__ void __launch_bounds__(kBlock)
     uint32_t g = gbase[dd] + (p - block_off[dd]);
     keys_out[g] = key;
     vals_out[g] = svals[p];
+    if (meta.out) {  // final pass: per sorted position, the listing's group and its size
+      const uint32_t lg = meta.lgrp[svals[p]];
+      meta.out[g] = lg | (static_cast<uint64_t>(meta.offsets[lg + 1] - meta.offsets[lg]) << 32);
+    }
   }
 }
 
@@ -369,7 +382,8 @@ template <typename K>
 inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b, uint64_t n,
                        int key_bits, uint32_t* scratch, cudaStream_t stream, int sms = 148,
                        const uint32_t* gate = nullptr, const K* keys_in0 = nullptr,
-                       bool iota_vals = false, bool zero_scratch = true) {
+                       bool iota_vals = false, bool zero_scratch = true,
+                       SortMeta meta = SortMeta{}) {
   if (n == 0) return false;
   if (key_bits <= 0) key_bits = 1;
   set_smem_attrs<K>();
@@ -402,7 +416,8 @@ inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b,
     uint32_t* vo = in_b ? vals_a : vals_b;
     const uint32_t epoch = g_epoch.fetch_add(1) + 1;
     pass_kernel<K><<<tiles, kBlock, Tile<K>::kSmem, stream>>>(
-        ki, vi, ko, vo, n32, p * kBits, hist + p * kBins, status, tile_ctr + p, epoch, gate);
+        ki, vi, ko, vo, n32, p * kBits, hist + p * kBins, status, tile_ctr + p, epoch, gate,
+        p == passes - 1 ? meta : SortMeta{});
     in_b = !in_b;
   }
   HPS_LAUNCH_CHECK_N(1 + passes);

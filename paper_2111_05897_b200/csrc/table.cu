@@ -275,7 +275,7 @@ void batch_free(Batch& b) {
   forget_outstanding(b);
   void* ptrs[] = {b.offsets, b.lgrp,  b.slot,   b.keys_a,  b.vals_a,
                   b.keys_b,  b.vals_b, b.rv,  b.new_slots, b.kind,  b.hist,
-                  b.mkeys,   b.hot, b.small_slot, b.small_listing,
+                  b.mkeys,   b.hot, b.meta, b.small_slot, b.small_listing,
                   b.small,   b.skeys_a, b.skeys_b, b.sperm_a, b.sperm_b, b.sstart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -391,6 +391,8 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
     ensure(b.mkeys, c, n);
     c = 0;
     ensure(b.hot, c, n / kHotRun + 1);
+    c = 0;
+    ensure(b.meta, c, n);
     size_t hw = radix::scratch_words<uint32_t>(n);
     if (hw > b.hist_cap) {
       c = 0;
@@ -449,6 +451,7 @@ static UpdateArgs plan_args(const Batch& b) {
   a.lgrp = b.lgrp;
   a.offsets = b.offsets;
   a.F = b.F;
+  a.meta = b.meta_ok ? b.meta : nullptr;
   return a;
 }
 
@@ -474,16 +477,26 @@ void launch_set_cond(cudaGraphConditionalHandle h, const void* val, bool is64,
 }
 
 static void sort_slots(Batch& b, const uint32_t* keys_in0, bool iota, const uint32_t* gate,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool plan_meta = false) {
   Table* t = b.table;
   ProfScope p(t, "sort", st);
   const int kb = slot_key_bits(t);
   const int passes = (kb + radix::kBits - 1) / radix::kBits;
   b.sorted_slot = (passes & 1) ? b.keys_b : b.keys_a;
   b.sorted_listing = (passes & 1) ? b.vals_b : b.vals_a;
+  radix::SortMeta meta;
+  // batch plans (not the direct apply): per-position metadata, produced by the large
+  // path's final pass (the single-CTA small sort does not)
+  b.meta_ok = plan_meta && (gate || b.N > radix::kSmallN);
+  if (b.meta_ok) {
+    meta.lgrp = b.lgrp;
+    meta.offsets = b.offsets;
+    meta.out = b.meta;
+  }
   auto sort = [&](cudaStream_t s, bool zero) {
     bool in_b = radix::sort_pairs<uint32_t>(b.keys_a, b.vals_a, b.keys_b, b.vals_b, b.N, kb,
-                                            b.hist, s, t->sm_count, gate, keys_in0, iota, zero);
+                                            b.hist, s, t->sm_count, gate, keys_in0, iota, zero,
+                                            meta);
     b.sorted_slot = in_b ? b.keys_b : b.keys_a;
     b.sorted_listing = in_b ? b.vals_b : b.vals_a;
   };
@@ -551,7 +564,7 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     launch_sample_lengths(perm, b.offsets, B, F, b.sstart, st);
     launch_scan_inplace(b.sstart, B, b.sstart + B, st);
     launch_permuted_listing(perm, b.sstart, b.offsets, b.slot, B, F, b.keys_a, b.vals_a, st);
-    sort_slots(b, nullptr, false, nullptr, st);
+    sort_slots(b, nullptr, false, nullptr, st, true);
   } else {
     // Plan (plan.cu): rows listed once apply directly; the multi listings are ordered
     // by the small composite sort, or -- past kSmallN of them -- the whole batch is
@@ -566,7 +579,7 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
       radix::sort_composite_small(b.mkeys, &b.small[0], lbits, b.small_slot, b.small_listing,
                                   st);
     }
-    sort_slots(b, b.slot, true, &b.small[0], st);
+    sort_slots(b, b.slot, true, &b.small[0], st, true);
   }
   b.registered = true;
   b.pulled = false;

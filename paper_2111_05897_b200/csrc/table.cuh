@@ -140,6 +140,8 @@ struct Batch {
   uint8_t* kind = nullptr;        // [N] plan: 1 = row listed once, 2 = multi (sorted path)
   unsigned long long* mkeys = nullptr;  // [N] multi listings as (slot << lbits | listing)
   uint32_t* hot = nullptr;        // [N / kHotRun + 1] sorted-list starts of hot rows
+  uint64_t* meta = nullptr;       // [N] large path: per sorted position, group | size << 32
+  bool meta_ok = false;
   uint32_t* small_slot = nullptr;       // [kSmallN] multi listings sorted (small path)
   uint32_t* small_listing = nullptr;
   uint32_t* hist = nullptr;       // sort / plan scratch
@@ -317,6 +319,8 @@ struct UpdateArgs {
   uint32_t* hot;
   uint32_t* n_hot;
   uint32_t hot_cap;
+  // large (sorted) path: per sorted position, the listing's group | group size << 32
+  const uint64_t* meta;
 };
 constexpr uint32_t kHotRun = 64;
 constexpr uint32_t kHotMaxDim = 128;  // update_hot stages [256][D] floats in shared memory
