@@ -657,9 +657,9 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   if (t->cfg.embedding_dim <= kHotMaxDim) {
     // hot-row hand-off list (update_multi -> update_hot), counter in b.small[4]
     a.hot = b.hot;
-    a.n_hot = &b.small[4];
+    a.n_hot = &b.small[4];  // [4] hot rows listed, [5] hot rows claimed (update_hot)
     a.hot_cap = static_cast<uint32_t>(b.N / kHotRun + 1);
-    HPS_CUDA(cudaMemsetAsync(a.n_hot, 0, sizeof(uint32_t), st));
+    HPS_CUDA(cudaMemsetAsync(a.n_hot, 0, 2 * sizeof(uint32_t), st));
   }
   if (!b.all_multi) {
     // Rows listed more than once (ordered chains, latency-bound, few) and rows listed
