@@ -97,7 +97,7 @@ __device__ void pool_general(const DevTable& t, const uint32_t* __restrict__ slo
 }  // namespace
 
 template <int V, int L, bool kGuard>
-__global__ void __launch_bounds__(256, 6)
+__global__ void __launch_bounds__(256, 8)
     pool_kernel(DevTable t, const uint32_t* __restrict__ offsets,
                 const uint32_t* __restrict__ slots, uint32_t BF, uint64_t N, int mean,
                 float* __restrict__ out, uint64_t* __restrict__ out_rv64,
