@@ -719,7 +719,9 @@ __global__ void x_owner_dyn_kernel(const XHdr* __restrict__ hdr,
                                    const uint32_t* __restrict__ pair_pos, uint64_t cap,
                                    uint64_t* __restrict__ out_ids, uint64_t* __restrict__ out_rv,
                                    uint32_t* __restrict__ out_off,
-                                   unsigned long long* protocol) {
+                                   unsigned long long* protocol, DevTable t,
+                                   const uint32_t* __restrict__ oslot,
+                                   uint32_t* __restrict__ out_slot) {
   __shared__ uint64_t po[kMaxWorld + 1];
   if (threadIdx.x == 0) {
     uint64_t run = 0;
@@ -734,7 +736,10 @@ __global__ void x_owner_dyn_kernel(const XHdr* __restrict__ hdr,
   for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k <= cap;
        k += (uint64_t)gridDim.x * blockDim.x) {
     out_off[k] = static_cast<uint32_t>(min(k, P));
-    if (k >= P) continue;
+    if (k >= P) {
+      if (out_slot && k < cap) out_slot[k] = kInvalidSlot;
+      continue;
+    }
     uint32_t r = 0;
     while (r + 1 < W && po[r + 1] <= k) ++r;
     uint32_t j = pair_pos[k];
@@ -744,6 +749,16 @@ __global__ void x_owner_dyn_kernel(const XHdr* __restrict__ hdr,
     }
     out_ids[k] = oids[r * stride + j];
     if (orv) out_rv[k] = orv[r * stride + j];
+    if (out_slot) {
+      // the forward already found (or created) the row: reuse its slot instead of a
+      // second hash probe, and mark the batch-plan bits the probe would have (plan.cu)
+      const uint32_t s = oslot[r * stride + j];
+      out_slot[k] = s;
+      if (slot_ok(t, s)) {
+        const uint32_t bit = 1u << (s & 31);
+        if (atomicOr(&t.seen[s >> 5], bit) & bit) atomicOr(&t.multi[s >> 5], bit);
+      }
+    }
   }
 }
 struct PeerRows {
@@ -985,15 +1000,18 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
   grow(xs.ids, xs.cap_ids, cap);
   grow(xs.rv, xs.cap_rv, cap);
   grow(xs.off, xs.cap_off, cap + 1);
+  Batch& b = t->scratch;
+  b.agg = HPS_SUM;
+  batch_reserve(b, cap, cap, cap);
   x_owner_dyn_kernel<<<grid_n(cap + 1, t->sm_count), kXBlock, 0, st>>>(
       mine, reinterpret_cast<const uint32_t*>(x.arena + x.off_ocnt), x.G, M,
       reinterpret_cast<const uint64_t*>(x.arena + x.off_oids), nullptr,
       reinterpret_cast<const uint32_t*>(x.arena + x.off_ppos), cap, xs.ids, xs.rv, xs.off,
-      t->d.ctr + kCtrProtocol);
+      t->d.ctr + kCtrProtocol, t->d, reinterpret_cast<const uint32_t*>(x.arena + x.off_oslot),
+      b.slot);
   HPS_LAUNCH_CHECK();
-  Batch& b = t->scratch;
-  b.agg = HPS_SUM;
-  batch_register(b, xs.ids, cap, xs.off, static_cast<uint32_t>(cap), 1, nullptr, st, true);
+  batch_register(b, xs.ids, cap, xs.off, static_cast<uint32_t>(cap), 1, nullptr, st, true,
+                 /*slots_ready=*/true);
   // Fresh mode: every pair's read version is the row's version before this apply. The
   // forward read the rows at their current versions and nothing mutates this table
   // between a step's forward and its apply (one batch in flight per exchange), so this

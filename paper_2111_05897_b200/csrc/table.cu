@@ -513,7 +513,8 @@ static void sort_slots(Batch& b, const uint32_t* keys_in0, bool iota, const uint
 // serve_pull: after this, every listing has its slot (rows lazily initialised) and the
 // listings are grouped per row in apply order.
 void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* offsets, uint32_t B,
-                    uint32_t F, const uint64_t* sample_keys, cudaStream_t st, bool dynamic) {
+                    uint32_t F, const uint64_t* sample_keys, cudaStream_t st, bool dynamic,
+                    bool slots_ready) {
   Table* t = b.table;
   if (N >= 0xffffffffull) throw Error(HPS_E_PRECONDITION, "batch too large (>= 2^32 listings)");
   const uint64_t BF = static_cast<uint64_t>(B) * F;
@@ -523,7 +524,8 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   b.rv_valid = false;
   batch_reserve(b, N, BF, B);
   Stager stg(t->stage);
-  const uint64_t* d_ids = static_cast<const uint64_t*>(stg.in(ids, N * sizeof(uint64_t), st));
+  const uint64_t* d_ids =
+      slots_ready ? nullptr : static_cast<const uint64_t*>(stg.in(ids, N * sizeof(uint64_t), st));
   if (!is_device_ptr(offsets)) {
     if (offsets[BF] != N || offsets[0] != 0)
       throw Error(HPS_E_PRECONDITION, "register: offsets[B*F] must equal n_ids and offsets[0] 0");
@@ -547,13 +549,15 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   // Sample keys that reorder the batch: every listing takes the sorted (multi) path.
   const bool permute = d_sk && B > 1;
   b.all_multi = permute;
-  {
-    ProfScope p(t, "probe", st);
-    // dynamic: N is only a bound; the live listing count is offsets[B*F] on the device
-    launch_probe(t->d, d_ids, N, b.slot, nullptr, nullptr, b.new_slots, &b.small[2], !permute,
-                 st, dynamic ? b.offsets + BF : nullptr);
+  if (!slots_ready) {
+    {
+      ProfScope p(t, "probe", st);
+      // dynamic: N is only a bound; the live listing count is offsets[B*F] on the device
+      launch_probe(t->d, d_ids, N, b.slot, nullptr, nullptr, b.new_slots, &b.small[2],
+                   !permute, st, dynamic ? b.offsets + BF : nullptr);
+    }
+    launch_lazy_init(t->d, b.new_slots, &b.small[2], N, t->sm_count, st);
   }
-  launch_lazy_init(t->d, b.new_slots, &b.small[2], N, t->sm_count, st);
   if (permute) {
     // Apply order = ascending sample key: enumerate listings sample by sample in key
     // order before the stable slot sort.

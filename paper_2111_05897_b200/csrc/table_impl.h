@@ -111,9 +111,11 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B);
 void batch_free(Batch& b);
 // dynamic: N and B are bounds; offsets (device) end at the live count (offsets[B*F]),
 // samples past it are empty -- a batch whose size is only known on the device.
+// slots_ready: b.slot already holds every listing's slot and the plan bits are marked
+// (the exchange owner reuses its forward probe); ids are then not read.
 void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* offsets, uint32_t B,
                     uint32_t F, const uint64_t* sample_keys, cudaStream_t st,
-                    bool dynamic = false);
+                    bool dynamic = false, bool slots_ready = false);
 void batch_pull(Batch& b, int agg, float* out_pooled, uint64_t* out_rv, cudaStream_t st);
 void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_tag,
                 uint32_t epoch, int untracked, const uint64_t* rv64, int* accepted,
