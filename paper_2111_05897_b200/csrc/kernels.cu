@@ -387,9 +387,16 @@ template <int V, int L, bool kGuard>
 __global__ void __launch_bounds__(256)
     check_batch_kernel(const float* __restrict__ grads, const uint32_t* __restrict__ offsets,
                        uint64_t rows, uint32_t D, uint32_t F, int mean,
-                       unsigned long long* ctr) {
+                       unsigned long long* ctr, float* __restrict__ cbuf,
+                       const uint32_t* __restrict__ inv, const uint32_t* gate) {
   using G = Geo<V, L, kGuard>;
   constexpr int kCheckILP = 4;
+  // large plan: also scatter every listing's contribution to its sorted position, so the
+  // ordered updates read contributions contiguously instead of chasing groups per pair
+  __shared__ int s_write;
+  if (threadIdx.x == 0) s_write = cbuf && (!gate || ld_volatile(gate) > radix::kSmallN);
+  __syncthreads();
+  const bool write_c = s_write != 0;
   const int ln = G::lane();
   const int chunks = kGuard ? (D + G::kSpan - 1) / G::kSpan : 1;
   const uint64_t groups = G::groups();
@@ -410,6 +417,24 @@ __global__ void __launch_bounds__(256)
         const uint64_t r = r0 + u * groups;
         if (n[u] && (!kGuard || d0 < D)) load_vec_cs<V>(grads + r * D + d0, x[u]);
         else for (int j = 0; j < V; ++j) x[u][j] = 0.0f;
+      }
+      if (write_c) {
+#pragma unroll
+        for (int u = 0; u < kCheckILP; ++u) {
+          if (!n[u] || (kGuard && d0 >= D)) continue;
+          const uint64_t r = r0 + u * groups;
+          const double scale = mean ? __drcp_rn(static_cast<double>(n[u])) : 1.0;
+          float c[V];
+#pragma unroll
+          for (int j = 0; j < V; ++j)
+            c[j] = __double2float_rn(__dadd_rn(0.0, __dmul_rn(static_cast<double>(x[u][j]), scale)));
+          const uint32_t a0 = __ldg(offsets + r);
+          for (uint32_t i = a0; i < a0 + n[u]; ++i) {
+            float* dst = cbuf + static_cast<uint64_t>(inv[i]) * D + d0;
+            if (kGuard) dst[0] = c[0];
+            else store_vec<V>(dst, c);
+          }
+        }
       }
 #pragma unroll
       for (int u = 0; u < kCheckILP; ++u) {
@@ -439,13 +464,15 @@ __global__ void __launch_bounds__(256)
 }
 
 void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
-                        uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st) {
+                        uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st,
+                        float* cbuf, const uint32_t* inv, const uint32_t* gate) {
   const uint64_t rows = static_cast<uint64_t>(B) * F;
   if (!rows) return;
   HPS_DISPATCH_DIM(D, {
     uint64_t groups_per_block = 256 / L;
     uint32_t blocks = std::min<uint64_t>(ceil_div(rows, groups_per_block * 4), 148ull * 16);
-    check_batch_kernel<V, L, G><<<blocks, 256, 0, st>>>(grads, offsets, rows, D, F, mean, ctr);
+    check_batch_kernel<V, L, G><<<blocks, 256, 0, st>>>(grads, offsets, rows, D, F, mean, ctr,
+                                                        cbuf, inv, gate);
   });
   HPS_LAUNCH_CHECK();
 }

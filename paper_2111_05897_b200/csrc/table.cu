@@ -275,7 +275,7 @@ void batch_free(Batch& b) {
   forget_outstanding(b);
   void* ptrs[] = {b.offsets, b.lgrp,  b.slot,   b.keys_a,  b.vals_a,
                   b.keys_b,  b.vals_b, b.rv,  b.new_slots, b.kind,  b.hist,
-                  b.mkeys,   b.hot, b.meta, b.small_slot, b.small_listing,
+                  b.mkeys,   b.hot, b.meta, b.inv, b.cbuf, b.small_slot, b.small_listing,
                   b.small,   b.skeys_a, b.skeys_b, b.sperm_a, b.sperm_b, b.sstart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -393,6 +393,8 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
     ensure(b.hot, c, n / kHotRun + 1);
     c = 0;
     ensure(b.meta, c, n);
+    c = 0;
+    ensure(b.inv, c, n);
     size_t hw = radix::scratch_words<uint32_t>(n);
     if (hw > b.hist_cap) {
       c = 0;
@@ -452,6 +454,7 @@ static UpdateArgs plan_args(const Batch& b) {
   a.offsets = b.offsets;
   a.F = b.F;
   a.meta = b.meta_ok ? b.meta : nullptr;
+  a.cbuf = b.meta_ok ? b.cbuf : nullptr;
   return a;
 }
 
@@ -492,6 +495,15 @@ static void sort_slots(Batch& b, const uint32_t* keys_in0, bool iota, const uint
     meta.lgrp = b.lgrp;
     meta.offsets = b.offsets;
     meta.out = b.meta;
+    meta.inv = b.inv;
+    // contribution buffer (grown, never shrunk): the large plan's updates read it
+    const uint64_t want = b.N * t->cfg.embedding_dim;
+    if (want > b.cap_cbuf) {
+      if (b.cbuf) HPS_CUDA(cudaFree(b.cbuf));
+      b.cbuf = nullptr;
+      HPS_CUDA(cudaMalloc(&b.cbuf, want * sizeof(float)));
+      b.cap_cbuf = want;
+    }
   }
   auto sort = [&](cudaStream_t s, bool zero) {
     bool in_b = radix::sort_pairs<uint32_t>(b.keys_a, b.vals_a, b.keys_b, b.vals_b, b.N, kb,
@@ -634,7 +646,9 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   const int mean = agg == HPS_MEAN ? 1 : 0;
   {
     ProfScope p(t, "check", st);
-    launch_check_batch(d_g, b.offsets, b.B, b.F, D, mean, t->d.ctr, st);
+    launch_check_batch(d_g, b.offsets, b.B, b.F, D, mean, t->d.ctr, st,
+                       b.meta_ok ? b.cbuf : nullptr, b.inv,
+                       b.all_multi ? nullptr : &b.small[0]);
   }
   UpdateArgs a = plan_args(b);
   a.mean = mean;

@@ -142,6 +142,9 @@ struct Batch {
   uint32_t* hot = nullptr;        // [N / kHotRun + 1] sorted-list starts of hot rows
   uint64_t* meta = nullptr;       // [N] large path: per sorted position, group | size << 32
   bool meta_ok = false;
+  uint32_t* inv = nullptr;        // [N] large path: sorted position of each listing
+  float* cbuf = nullptr;          // [N][D] large path: contribution per sorted position
+  uint64_t cap_cbuf = 0;
   uint32_t* small_slot = nullptr;       // [kSmallN] multi listings sorted (small path)
   uint32_t* small_listing = nullptr;
   uint32_t* hist = nullptr;       // sort / plan scratch
@@ -282,8 +285,12 @@ void launch_snapshot_rv(const DevTable& t, const uint32_t* slots, uint64_t n, ui
                         cudaStream_t st);
 void launch_check_direct(const float* grads, uint64_t n_floats, unsigned long long* ctr,
                          cudaStream_t st);
+// cbuf/inv (optional, large plan only): also writes every listing's contribution to
+// cbuf[inv[listing]] when the plan gate (*gate > kSmallN, or gate == null) is open.
 void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
-                        uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st);
+                        uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st,
+                        float* cbuf = nullptr, const uint32_t* inv = nullptr,
+                        const uint32_t* gate = nullptr);
 
 struct UpdateArgs {
   // Multi kernel input: either the large-path slot sort of all n listings, or -- when
@@ -321,6 +328,9 @@ struct UpdateArgs {
   uint32_t hot_cap;
   // large (sorted) path: per sorted position, the listing's group | group size << 32
   const uint64_t* meta;
+  // large path: per sorted position, float(0.0 + (double)g * scale) of its listing, written
+  // by the validation pass (right for pairs of one listing; longer pairs are summed here)
+  const float* cbuf;
 };
 constexpr uint32_t kHotRun = 64;
 constexpr uint32_t kHotMaxDim = 128;  // update_hot stages [256][D] floats in shared memory
