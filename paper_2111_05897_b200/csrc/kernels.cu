@@ -384,7 +384,7 @@ void launch_check_direct(const float* grads, uint64_t n, unsigned long long* ctr
 // Row groups (L lanes x V floats) walk the [B*F][D] gradient rows, kCheckILP rows in
 // flight per group; a row's group size comes from the (L2-resident) offsets.
 template <int V, int L, bool kGuard>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 6)
     check_batch_kernel(const float* __restrict__ grads, const uint32_t* __restrict__ offsets,
                        uint64_t rows, uint32_t D, uint32_t F, int mean,
                        unsigned long long* ctr, float* __restrict__ cbuf,
