@@ -275,7 +275,7 @@ void batch_free(Batch& b) {
   forget_outstanding(b);
   void* ptrs[] = {b.offsets, b.lgrp,  b.slot,   b.keys_a,  b.vals_a,
                   b.keys_b,  b.vals_b, b.rv,  b.new_slots, b.kind,  b.hist,
-                  b.mkeys,   b.hot, b.meta, b.inv, b.cbuf, b.small_slot, b.small_listing,
+                  b.mkeys,   b.hot, b.mlist, b.meta, b.inv, b.cbuf, b.small_slot, b.small_listing,
                   b.small,   b.skeys_a, b.skeys_b, b.sperm_a, b.sperm_b, b.sstart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -391,6 +391,8 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
     ensure(b.mkeys, c, n);
     c = 0;
     ensure(b.hot, c, n / kHotRun + 1);
+    c = 0;
+    ensure(b.mlist, c, n / 2 + 1);
     c = 0;
     ensure(b.meta, c, n);
     c = 0;
@@ -677,7 +679,12 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     a.hot = b.hot;
     a.n_hot = &b.small[4];  // [4] hot rows listed, [5] hot rows claimed (update_hot)
     a.hot_cap = static_cast<uint32_t>(b.N / kHotRun + 1);
-    HPS_CUDA(cudaMemsetAsync(a.n_hot, 0, 2 * sizeof(uint32_t), st));
+    if (b.meta_ok) {  // sorted (large) plans list their multi rows (runs_kernel)
+      a.mlist = b.mlist;
+      a.n_mlist = &b.small[6];
+      a.mlist_cap = static_cast<uint32_t>(b.N / 2 + 1);
+    }
+    HPS_CUDA(cudaMemsetAsync(a.n_hot, 0, 3 * sizeof(uint32_t), st));
   }
   if (!b.all_multi) {
     // Rows listed more than once (ordered chains, latency-bound, few) and rows listed
@@ -692,6 +699,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     HPS_CUDA(cudaStreamWaitEvent(t->aux, t->ev_fork, 0));
     {
       ProfScope p(t, "update_multi", t->aux);
+      launch_runs(a, t->sm_count, t->aux);
       launch_update(t->d, a, false, t->sm_count, t->aux);
       launch_update_hot(t->d, a, t->sm_count, t->aux);
     }
@@ -703,6 +711,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     HPS_CUDA(cudaStreamWaitEvent(st, t->ev_join, 0));
   } else {
     ProfScope p(t, "update_multi", st);
+    launch_runs(a, t->sm_count, st);
     launch_update(t->d, a, false, t->sm_count, st);
     launch_update_hot(t->d, a, t->sm_count, st);
   }

@@ -140,6 +140,7 @@ struct Batch {
   uint8_t* kind = nullptr;        // [N] plan: 1 = row listed once, 2 = multi (sorted path)
   unsigned long long* mkeys = nullptr;  // [N] multi listings as (slot << lbits | listing)
   uint32_t* hot = nullptr;        // [N / kHotRun + 1] sorted-list starts of hot rows
+  uint32_t* mlist = nullptr;      // [N / 2 + 1] sorted-list starts of other multi rows
   uint64_t* meta = nullptr;       // [N] large path: per sorted position, group | size << 32
   bool meta_ok = false;
   uint32_t* inv = nullptr;        // [N] large path: sorted position of each listing
@@ -326,6 +327,10 @@ struct UpdateArgs {
   uint32_t* hot;
   uint32_t* n_hot;
   uint32_t hot_cap;
+  // large plan: rows of 2..kHotRun-1 listings (runs_kernel -> update_multi); null = scan
+  uint32_t* mlist;
+  uint32_t* n_mlist;
+  uint32_t mlist_cap;
   // large (sorted) path: per sorted position, the listing's group | group size << 32
   const uint64_t* meta;
   // large path: per sorted position, float(0.0 + (double)g * scale) of its listing, written
@@ -335,6 +340,7 @@ struct UpdateArgs {
 constexpr uint32_t kHotRun = 64;
 constexpr uint32_t kHotMaxDim = 128;  // update_hot stages [256][D] floats in shared memory
 void launch_update_hot(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
+void launch_runs(const UpdateArgs& a, int sms, cudaStream_t st);
 void launch_update(const DevTable& t, const UpdateArgs& a, bool direct, int sms, cudaStream_t st);
 void launch_update_single(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
 void launch_count_pairs(const UpdateArgs& a, unsigned long long* ctr, cudaStream_t st);
