@@ -392,7 +392,7 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
     c = 0;
     ensure(b.hot, c, n / kHotRun + 1);
     c = 0;
-    ensure(b.mlist, c, n / 2 + 1);
+    ensure(b.mlist, c, n + 1);
     c = 0;
     ensure(b.meta, c, n);
     c = 0;
@@ -682,7 +682,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     if (b.meta_ok) {  // sorted (large) plans list their multi rows (runs_kernel)
       a.mlist = b.mlist;
       a.n_mlist = &b.small[6];
-      a.mlist_cap = static_cast<uint32_t>(b.N / 2 + 1);
+      a.mlist_cap = static_cast<uint32_t>(b.N + 1);  // (sample-key plans list singles too)
     }
     HPS_CUDA(cudaMemsetAsync(a.n_hot, 0, 3 * sizeof(uint32_t), st));
   }

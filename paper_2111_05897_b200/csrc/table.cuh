@@ -140,7 +140,7 @@ struct Batch {
   uint8_t* kind = nullptr;        // [N] plan: 1 = row listed once, 2 = multi (sorted path)
   unsigned long long* mkeys = nullptr;  // [N] multi listings as (slot << lbits | listing)
   uint32_t* hot = nullptr;        // [N / kHotRun + 1] sorted-list starts of hot rows
-  uint32_t* mlist = nullptr;      // [N / 2 + 1] sorted-list starts of other multi rows
+  uint32_t* mlist = nullptr;      // [N + 1] sorted-list starts of the other listed rows
   uint64_t* meta = nullptr;       // [N] large path: per sorted position, group | size << 32
   bool meta_ok = false;
   uint32_t* inv = nullptr;        // [N] large path: sorted position of each listing
