@@ -433,7 +433,7 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
   }
   if (!b.small) {
     uint64_t c = 0;
-    ensure(b.small, c, 8);
+    ensure(b.small, c, 16);
     c = 0;
     ensure(b.small_slot, c, radix::kSmallN);
     c = 0;
@@ -675,9 +675,11 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   });
   a.dry_run = 0;
   if (t->cfg.embedding_dim <= kHotMaxDim) {
-    // hot-row hand-off list (update_multi -> update_hot), counter in b.small[4]
+    // hot-row hand-off list (runs_kernel -> update_hot)
     a.hot = b.hot;
-    a.n_hot = &b.small[4];  // [4] hot rows listed, [5] hot rows claimed (update_hot)
+    // hot-row counters live in b.small[8..10]: [8] hot rows listed, [9] claimed by
+    // update_hot, [10] very hot rows (listed from the end); [6] the multi-list count
+    a.n_hot = &b.small[8];
     a.hot_cap = static_cast<uint32_t>(b.N / kHotRun + 1);
     if (b.meta_ok) {  // sorted (large) plans list their multi rows (runs_kernel)
       a.mlist = b.mlist;
@@ -685,6 +687,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
       a.mlist_cap = static_cast<uint32_t>(b.N + 1);  // (sample-key plans list singles too)
     }
     HPS_CUDA(cudaMemsetAsync(a.n_hot, 0, 3 * sizeof(uint32_t), st));
+    HPS_CUDA(cudaMemsetAsync(&b.small[6], 0, sizeof(uint32_t), st));
   }
   if (!b.all_multi) {
     // Rows listed more than once (ordered chains, latency-bound, few) and rows listed

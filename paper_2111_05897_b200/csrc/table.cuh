@@ -150,7 +150,7 @@ struct Batch {
   uint32_t* small_listing = nullptr;
   uint32_t* hist = nullptr;       // sort / plan scratch
   size_t hist_cap = 0;
-  uint32_t* small = nullptr;      // device scalars: [0] = multi listings, [2] = rows inserted
+  uint32_t* small = nullptr;      // device scalars: [0] multi listings, [2] rows inserted, [6] multi-list rows, [8..10] hot lists
   bool all_multi = false;         // plan skipped: every listing on the sorted path
   bool rv_valid = false;          // rv holds the pull-time versions (else: no mutation since)
   // sample-order permutation (sample_keys != NULL)
@@ -338,6 +338,7 @@ struct UpdateArgs {
   const float* cbuf;
 };
 constexpr uint32_t kHotRun = 64;
+constexpr uint32_t kVeryHotRun = 1024;
 constexpr uint32_t kHotMaxDim = 128;  // update_hot stages [256][D] floats in shared memory
 void launch_update_hot(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
 void launch_runs(const UpdateArgs& a, int sms, cudaStream_t st);
