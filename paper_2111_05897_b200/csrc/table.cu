@@ -686,8 +686,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
       a.n_mlist = &b.small[6];
       a.mlist_cap = static_cast<uint32_t>(b.N + 1);  // (sample-key plans list singles too)
     }
-    HPS_CUDA(cudaMemsetAsync(a.n_hot, 0, 3 * sizeof(uint32_t), st));
-    HPS_CUDA(cudaMemsetAsync(&b.small[6], 0, sizeof(uint32_t), st));
+    HPS_CUDA(cudaMemsetAsync(&b.small[6], 0, 5 * sizeof(uint32_t), st));  // [6..10], one node
   }
   if (!b.all_multi) {
     // Rows listed more than once (ordered chains, latency-bound, few) and rows listed
