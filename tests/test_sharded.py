@@ -81,3 +81,30 @@ def test_sharded_p2p_cuda_graph_replay():
     res = run_world(world, "nccl", use_device=True, transport="p2p", graph=True, steps=4, B=16)
     for r, status, n in res:
         assert status == "ok", status
+
+
+@pytest.mark.gpu
+def test_apply_pairs_rejects_positions_outside_the_source_segment():
+    """A pair naming an id outside its source's segment fails the whole apply
+    (HPS_E_PROTOCOL) and leaves every row untouched."""
+    import numpy as np
+    import torch
+
+    import oracle as O
+    from paper_2111_05897_b200 import hps
+    from paper_2111_05897_b200.sharded import DeviceOps
+
+    dev = torch.device("cuda:0")
+    salts = [O.mix64(7 + s) for s in range(4)]
+    table = hps.ShardSet(4, 8, 1 << 12, hps.SGD, salts=salts)
+    ops = DeviceOps(table, 1, hps.SUM)
+    ids = torch.tensor([11, 12, 13], dtype=torch.int64, device=dev)
+    rows, ver = ops.lookup(ids)
+    torch.cuda.synchronize()
+    before = table.peek(np.array([11, 12, 13], np.uint64))[0]
+    pos = torch.tensor([0, 5], dtype=torch.int32, device=dev)  # 5 is outside [0, 3)
+    con = torch.ones((2, 8), dtype=torch.float32, device=dev)
+    with pytest.raises(hps.ProtocolError):
+        ops.apply_pairs(ids, ver, [3], pos, con, [2], 0.5, 1, table.epoch(), flags=0)
+    after = table.peek(np.array([11, 12, 13], np.uint64))[0]
+    assert before.tobytes() == after.tobytes()
