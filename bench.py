@@ -246,7 +246,8 @@ def run_sharded(args, world, rank, local, dev):
     def eager_step(i):
         ids, offs, _ = batches[i % M]
         ew.register_batch(ids, offs, B, F)
-        ew.serve_pull(out_pooled=pooled)
+        # p2p: the pooled batch stays in the exchange arena (zero-copy view)
+        ew.serve_pull(out_pooled=None if p2p else pooled)
         tag[0] += 1
         # p2p: step tags from the table's device counter (graph replays advance it)
         ew.apply_backward(grads[i % M], cfg.lr, tag[0],
@@ -346,8 +347,7 @@ def run_sharded(args, world, rank, local, dev):
         d_ids.copy_(h_ids, non_blocking=True)
         d_offs.copy_(h_offs, non_blocking=True)
         ew.register_batch(d_ids, d_offs, B, F)
-        ew.serve_pull(out_pooled=pooled)
-        h_pooled.copy_(pooled, non_blocking=True)
+        h_pooled.copy_(ew.serve_pull(out_pooled=None if p2p else pooled), non_blocking=True)
         d_grads.copy_(h_grads, non_blocking=True)
         tag[0] += 1
         ew.apply_backward(d_grads, cfg.lr, tag[0],

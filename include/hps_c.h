@@ -234,7 +234,8 @@ hps_status hps_table_apply_pairs(hps_table* t, const uint64_t* recv_ids,
  * count before its apply). Setup, once: hps_exchange_arena allocates this rank's receive
  * arena for batches of up to max_ids listings and returns its 64-byte IPC handle; the
  * caller all-gathers the handles and passes them (world x 64 bytes, rank order) to
- * hps_exchange_connect. Per step, on every rank in the same order:
+ * hps_exchange_connect (max_groups >= B*F enables the owners' direct pooling of
+ * one-listing groups). Per step, on every rank in the same order:
  *   hps_exchange_forward   route; ids -> owners' arenas; owners find-or-init and write the
  *                          rows into the requesters' arenas (= fetch_rows)
  *   hps_exchange_pool      with rows == NULL: pool from the delivered rows (= serve_pull)
@@ -242,7 +243,12 @@ hps_status hps_table_apply_pairs(hps_table* t, const uint64_t* recv_ids,
  *                          order (= apply_backward + flush_step + PsShard::apply_gradients)
  * A peer missing a barrier for ~4 s fails the step with HPS_E_SYNC_FAILURE instead of
  * hanging the device. */
-hps_status hps_exchange_arena(hps_exchange* x, uint64_t max_ids, uint32_t dim, void* out_handle);
+hps_status hps_exchange_arena(hps_exchange* x, uint64_t max_ids, uint64_t max_groups,
+                              uint32_t dim, void* out_handle);
+/* The arena's pooled buffer [max_groups][dim]: hps_exchange_pool(x, NULL, dim, NULL)
+ * leaves the pooled batch there (zero-copy; valid until the next forward). The owners
+ * write one-listing groups into it directly during the forward. */
+hps_status hps_exchange_pooled(hps_exchange* x, float** out);
 hps_status hps_exchange_connect(hps_exchange* x, uint32_t rank, const void* handles);
 hps_status hps_exchange_forward(hps_exchange* x, hps_table* t, const uint64_t* ids, size_t n_ids,
                                 const uint32_t* offsets, uint32_t B, uint32_t F,

@@ -373,12 +373,21 @@ hps_status hps_table_apply_pairs(hps_table* t, const uint64_t* recv_ids,
   });
 }
 
-hps_status hps_exchange_arena(hps_exchange* x, uint64_t max_ids, uint32_t dim, void* out_handle) {
+hps_status hps_exchange_arena(hps_exchange* x, uint64_t max_ids, uint64_t max_groups,
+                              uint32_t dim, void* out_handle) {
   return guarded([&] {
     REQUIRE(x && out_handle, "hps_exchange_arena: null argument");
     std::lock_guard<std::mutex> g(x->mu);
     hps::DeviceGuard dg(x->impl.device);
-    hps::xbatch_arena(x->impl, max_ids, dim, out_handle);
+    hps::xbatch_arena(x->impl, max_ids, max_groups, dim, out_handle);
+  });
+}
+
+hps_status hps_exchange_pooled(hps_exchange* x, float** out) {
+  return guarded([&] {
+    REQUIRE(x && out, "hps_exchange_pooled: null argument");
+    REQUIRE(x->impl.arena, "hps_exchange_pooled: no arena");
+    *out = reinterpret_cast<float*>(x->impl.arena + x->impl.off_pooled);
   });
 }
 

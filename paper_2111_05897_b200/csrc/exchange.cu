@@ -141,6 +141,7 @@ __device__ __forceinline__ void load_seg(const uint32_t* cnt, uint32_t G, uint32
 // Id regions of the owners (peer path): p[d] = owner d's region for this source rank.
 struct PeerIds {
   uint64_t* p[kMaxWorld];
+  uint32_t* tg[kMaxWorld];  // (direct pooling) per id: the requester's group to write, or ~0
 };
 
 // Send position per listing, send_ids, and the composite keys (pos << lbits | listing)
@@ -151,7 +152,9 @@ __global__ void __launch_bounds__(kXBlock)
                      const uint8_t* __restrict__ dest, const uint32_t* __restrict__ spair,
                      uint32_t* cnt, int lbits, uint32_t* __restrict__ sendpos,
                      uint64_t* __restrict__ send_ids, uint32_t* __restrict__ seg_out,
-                     unsigned long long* __restrict__ mkeys, PeerIds pid) {
+                     unsigned long long* __restrict__ mkeys, PeerIds pid,
+                     const uint32_t* __restrict__ lgrp, const uint32_t* __restrict__ offsets,
+                     uint8_t* __restrict__ gdirect) {
   __shared__ uint32_t seg[33];
   __shared__ uint32_t s_n, s_base;
   load_seg(cnt, G, seg);
@@ -169,8 +172,19 @@ __global__ void __launch_bounds__(kXBlock)
       pos = seg[d] + j;
       sendpos[i] = pos;
       if (code & kInserter) {
-        if (send_ids) send_ids[pos] = ids[i];
-        else pid.p[d][j] = ids[i];  // straight into owner d's id region for this rank
+        if (send_ids) {
+          send_ids[pos] = ids[i];
+        } else {
+          pid.p[d][j] = ids[i];  // straight into owner d's id region for this rank
+          if (gdirect) {
+            // an id listed once, alone in its group: its pooled value is the row itself,
+            // which the owner writes straight into this rank's pooled output
+            const uint32_t lg = lgrp[i];
+            const bool direct = spair[i] != kNoPair && offsets[lg + 1] - offsets[lg] == 1;
+            pid.tg[d][j] = direct ? lg : 0xffffffffu;
+            if (direct) gdirect[lg] = 1;
+          }
+        }
       }
       multi = spair[i] == kNoPair;
       if (multi) r = atomicAdd(&s_n, 1u);
@@ -440,6 +454,7 @@ XBatch::~XBatch() {
   for (uint32_t r = 0; r < G && r < kMaxWorld; ++r)
     if (peer[r] && peer[r] != arena) cudaIpcCloseMemHandle(peer[r]);
   if (arena) cudaFree(arena);
+  if (gdirect) cudaFree(gdirect);
   if (side) cudaStreamDestroy(side);
   if (xbase) cudaFree(xbase);
   if (dev_epoch) cudaFree(dev_epoch);
@@ -510,11 +525,16 @@ static void route_core(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_
                                                           x.hval, x.dest, x.spair, x.cnt);
     HPS_LAUNCH_CHECK_N(2);
   }
+  launch_expand_groups(x.offsets, static_cast<uint32_t>(BF), x.lgrp, st);
+  uint8_t* gdirect = nullptr;
+  if (!send_ids && x.direct_ok) {
+    gdirect = x.gdirect;
+    HPS_CUDA(cudaMemsetAsync(gdirect, 0, BF, st));
+  }
   x_scatter_kernel<<<grid_n(std::max<uint64_t>(n, 1), x.sms), kXBlock, 0, st>>>(
       ids, n, x.G, x.hidx, x.hval, x.dest, x.spair, x.cnt, x.lbits, x.sendpos, send_ids, x.seg,
-      x.mkeys, pid);
+      x.mkeys, pid, x.lgrp, x.offsets, gdirect);
   HPS_LAUNCH_CHECK();
-  launch_expand_groups(x.offsets, static_cast<uint32_t>(BF), x.lgrp, st);
 }
 
 // Pair ordering and counts up to (not including) the emit kernels: x.pair_off = owners'
@@ -593,7 +613,31 @@ void xbatch_route(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_t* of
 }
 
 void xbatch_pool(XBatch& x, const float* rows, uint32_t D, float* out_pooled, cudaStream_t st) {
-  if (!rows) rows = x.arena_rows;  // peer path: the owners delivered into the arena
+  const bool peer = !rows;
+  if (peer) {  // peer path: the owners delivered into the arena
+    rows = x.arena_rows;
+    if (!x.connected) throw Error(HPS_E_PRECONDITION, "hps_exchange_pool: no rows");
+    // pool into the arena's pooled buffer (where the owners wrote the one-listing groups),
+    // then hand it over (zero-copy when the caller asks for the arena buffer itself)
+    const uint64_t BF = static_cast<uint64_t>(x.B) * x.F;
+    float* arena_pooled = reinterpret_cast<float*>(x.arena + x.off_pooled);
+    if (x.direct_ok) {
+      DevTable view{};
+      view.rows = const_cast<float*>(rows);
+      view.D = D;
+      view.stride = D;
+      view.capacity = static_cast<uint32_t>(x.N);
+      launch_pool(view, x.offsets, x.sendpos, static_cast<uint32_t>(BF), x.N,
+                  x.agg == HPS_MEAN ? 1 : 0, arena_pooled, nullptr, nullptr, st, x.gdirect);
+      if (out_pooled && out_pooled != arena_pooled) {
+        require_device(out_pooled, "hps_exchange_pool out");
+        HPS_CUDA(cudaMemcpyAsync(out_pooled, arena_pooled, BF * D * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, st));
+      }
+      return;
+    }
+    if (!out_pooled) out_pooled = arena_pooled;
+  }
   require_device(rows, "hps_exchange_pool rows");
   require_device(out_pooled, "hps_exchange_pool out");
   if (!D) throw Error(HPS_E_PRECONDITION, "hps_exchange_pool: dim must be positive");
@@ -836,7 +880,8 @@ template <int V, int L, bool kGuard>
 __global__ void __launch_bounds__(256)
     x_owner_gather_kernel(DevTable t, const uint32_t* __restrict__ oslot, uint64_t stride,
                           const XHdr* __restrict__ hdr, PeerRows pr,
-                          uint64_t* __restrict__ orv) {
+                          uint64_t* __restrict__ orv, PeerRows pooled,
+                          const uint32_t* __restrict__ tgt) {
   using Gm = Geo<V, L, kGuard>;
   const uint32_t r = blockIdx.y;
   const uint64_t n = ld_volatile(&hdr->fwd_cnt[r]);
@@ -850,13 +895,23 @@ __global__ void __launch_bounds__(256)
     const uint32_t s = oslot[r * stride + j];
     const bool ok = slot_ok(t, s);
     const float* row = t.rows + static_cast<uint64_t>(ok ? s : 0) * t.stride;
+    // a one-listing group of the requester: its pooled value float(0.0 + (double)row),
+    // i.e. row + 0.0f, goes straight into the requester's pooled output
+    const uint32_t g = pooled.p[r] ? tgt[r * stride + j] : 0xffffffffu;
+    float* dst = g != 0xffffffffu ? pooled.p[r] + static_cast<uint64_t>(g) * D
+                                  : dst_base + j * D;
     if constexpr (!kGuard) {
       float v[V];
       if (ok) load_vec<V>(row + ln * V, v);
       else for (int k = 0; k < V; ++k) v[k] = 0.0f;
-      store_vec<V>(dst_base + j * D + ln * V, v);
+      if (g != 0xffffffffu)
+        for (int k = 0; k < V; ++k) v[k] = __fadd_rn(v[k], 0.0f);
+      store_vec<V>(dst + ln * V, v);
     } else {
-      for (uint32_t d = ln; d < D; d += L) dst_base[j * D + d] = ok ? row[d] : 0.0f;
+      for (uint32_t d = ln; d < D; d += L) {
+        const float v = ok ? row[d] : 0.0f;
+        dst[d] = g != 0xffffffffu ? __fadd_rn(v, 0.0f) : v;
+      }
     }
     if (ln == 0 && orv) orv[r * stride + j] = ok ? vt_read(t, s).x : 0;
   }
@@ -864,7 +919,7 @@ __global__ void __launch_bounds__(256)
 
 static size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
 
-void xbatch_arena(XBatch& x, uint64_t max_ids, uint32_t D, void* out_handle) {
+void xbatch_arena(XBatch& x, uint64_t max_ids, uint64_t max_groups, uint32_t D, void* out_handle) {
   if (x.arena) throw Error(HPS_E_PRECONDITION, "exchange arena already created");
   if (!max_ids || !D) throw Error(HPS_E_PRECONDITION, "exchange arena: empty");
   const uint64_t W = x.G, M = max_ids;
@@ -877,7 +932,11 @@ void xbatch_arena(XBatch& x, uint64_t max_ids, uint32_t D, void* out_handle) {
   x.off_orv = o;     o += al256(W * M * 8);
   x.off_oids = o;    o += al256(W * M * 8);
   x.off_ocnt = o;    o += al256(kMaxWorld * 4);
+  x.off_tgt = o;     o += al256(W * M * 4);
+  x.off_pooled = o;  o += al256(static_cast<size_t>(max_groups) * D * 4);
   x.arena_bytes = o;
+  x.max_groups = max_groups;
+  HPS_CUDA(cudaMalloc(&x.gdirect, std::max<uint64_t>(max_groups, 1)));
   x.max_ids = M;
   x.arena_dim = D;
   HPS_CUDA(cudaMalloc(&x.arena, o));
@@ -933,8 +992,13 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
   require_connected(x, t->cfg.embedding_dim, n);
   const uint64_t M = x.max_ids;
   PeerIds pid{};
-  for (uint32_t d = 0; d < x.G; ++d)
+  for (uint32_t d = 0; d < x.G; ++d) {
     pid.p[d] = reinterpret_cast<uint64_t*>(x.peer[d] + x.off_ids) + x.rank * M;
+    pid.tg[d] = reinterpret_cast<uint32_t*>(x.peer[d] + x.off_tgt) + x.rank * M;
+  }
+  // one-listing groups are pooled by their rows' owners when the arena's pooled buffer
+  // holds the batch (every rank takes the same decision: same batch shapes)
+  x.direct_ok = static_cast<uint64_t>(B) * F <= x.max_groups;
   route_core(x, ids, n, offsets, B, F, nullptr, pid, st);
   const PeerHdrs ph = peer_hdrs(x);
   x_fwd_hdr_kernel<<<1, 32, 0, st>>>(ph, x.G, x.rank, x.cnt, x.seg);
@@ -952,14 +1016,18 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
                        reinterpret_cast<uint32_t*>(x.arena + x.off_ocnt), b.new_slots,
                        &b.small[2], t->sm_count, st);
   launch_lazy_init(t->d, b.new_slots, &b.small[2], x.G * M, t->sm_count, st);
-  PeerRows pr{};
-  for (uint32_t r = 0; r < x.G; ++r) pr.p[r] = reinterpret_cast<float*>(x.peer[r] + x.off_rows);
+  PeerRows pr{}, pp{};
+  for (uint32_t r = 0; r < x.G; ++r) {
+    pr.p[r] = reinterpret_cast<float*>(x.peer[r] + x.off_rows);
+    pp.p[r] = reinterpret_cast<float*>(x.peer[r] + x.off_pooled);
+  }
   HPS_DISPATCH_DIM(t->d.D, {
     const uint32_t bx = static_cast<uint32_t>(std::max<uint64_t>(
         1, std::min<uint64_t>(ceil_div(M, 256 / L), uint64_t(t->sm_count) * 16 / x.G + 1)));
     // (no read versions: the owner applies in fresh mode, see xbatch_bwd)
-    x_owner_gather_kernel<V, L, G><<<dim3(bx, x.G), 256, 0, st>>>(t->d, oslot, M, mine, pr,
-                                                                   nullptr);
+    x_owner_gather_kernel<V, L, G><<<dim3(bx, x.G), 256, 0, st>>>(
+        t->d, oslot, M, mine, pr, nullptr, x.direct_ok ? pp : PeerRows{},
+        reinterpret_cast<const uint32_t*>(x.arena + x.off_tgt));
   });
   HPS_LAUNCH_CHECK();
   barrier(x, t, st);  // every owner's rows have landed in this rank's rows buffer

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256, 8)
     pool_kernel(DevTable t, const uint32_t* __restrict__ offsets,
                 const uint32_t* __restrict__ slots, uint32_t BF, uint64_t N, int mean,
                 float* __restrict__ out, uint64_t* __restrict__ out_rv64,
-                uint32_t* __restrict__ out_rv32) {
+                uint32_t* __restrict__ out_rv32, const uint8_t* __restrict__ skip) {
   using G = Geo<V, L, kGuard>;
   const int ln = G::lane();
   const uint32_t D = t.D;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256, 8)
 #pragma unroll
     for (int u = 0; u < kPoolILP; ++u) {
       sg[u] = sg0 + u * groups;
-      live[u] = sg[u] < BF;
+      live[u] = sg[u] < BF && !(skip && skip[sg[u]]);  // skip: written by the row's owner
       a[u] = live[u] ? offsets[sg[u]] : 0u;
       e[u] = live[u] ? offsets[sg[u] + 1] : 0u;
       spec[u] = (live[u] && sg[u] < N) ? slots[sg[u]] : 0u;  // right when a == sg
@@ -187,14 +187,14 @@ void launch_snapshot_rv(const DevTable& t, const uint32_t* slots, uint64_t n, ui
 
 void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,
                  uint64_t N, int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32,
-                 cudaStream_t st) {
+                 cudaStream_t st, const uint8_t* skip) {
   if (!BF) return;
   HPS_DISPATCH_DIM(t.D, {
     uint64_t groups_per_block = 256 / L;
     uint32_t blocks =
         std::min<uint64_t>(ceil_div(BF, groups_per_block * kPoolILP), 1u << 30);
     pool_kernel<V, L, G><<<blocks, 256, 0, st>>>(t, offsets, slots, BF, N, mean, out, out_rv64,
-                                                 out_rv32);
+                                                 out_rv32, skip);
   });
   HPS_LAUNCH_CHECK();
 }

@@ -279,9 +279,11 @@ void launch_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* 
                    uint64_t* out_versions, cudaStream_t st);
 void launch_peek(const DevTable& t, const uint64_t* ids, uint64_t n, float* out_w, float* out_acc,
                  uint64_t* out_versions, uint8_t* out_present, cudaStream_t st);
+// skip (optional): groups whose pooled value is already in `out` (one-listing groups the
+// exchange owners wrote directly).
 void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,
                  uint64_t N, int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32,
-                 cudaStream_t st);
+                 cudaStream_t st, const uint8_t* skip = nullptr);
 void launch_snapshot_rv(const DevTable& t, const uint32_t* slots, uint64_t n, uint32_t* rv,
                         cudaStream_t st);
 void launch_check_direct(const float* grads, uint64_t n_floats, unsigned long long* ctr,

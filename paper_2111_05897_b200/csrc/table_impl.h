@@ -175,7 +175,11 @@ struct XBatch {
   uint8_t* peer[kMaxWorld] = {};
   float* arena_rows = nullptr;
   size_t arena_bytes = 0, off_ids = 0, off_rows = 0, off_ppos = 0, off_contrib = 0,
-         off_oslot = 0, off_orv = 0, off_oids = 0, off_ocnt = 0;
+         off_oslot = 0, off_orv = 0, off_oids = 0, off_ocnt = 0,
+         off_tgt = 0, off_pooled = 0;
+  uint64_t max_groups = 0;
+  bool direct_ok = false;
+  uint8_t* gdirect = nullptr;  // [max_groups] groups the owners pooled this step
   uint64_t max_ids = 0;
   uint32_t arena_dim = 0, rank = 0;
   bool connected = false;
@@ -192,7 +196,7 @@ void xbatch_route(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_t* of
 void xbatch_pool(XBatch& x, const float* rows, uint32_t D, float* out_pooled, cudaStream_t st);
 void xbatch_pairs(XBatch& x, const float* grads, uint32_t D, uint32_t* out_pair_pos,
                   float* out_contrib, uint64_t* out_pair_counts, cudaStream_t st);
-void xbatch_arena(XBatch& x, uint64_t max_ids, uint32_t D, void* out_handle);
+void xbatch_arena(XBatch& x, uint64_t max_ids, uint64_t max_groups, uint32_t D, void* out_handle);
 void xbatch_connect(XBatch& x, uint32_t rank, const void* handles);
 void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint32_t* offsets,
                 uint32_t B, uint32_t F, cudaStream_t st);

@@ -169,7 +169,8 @@ def lib():
         "hps_exchange_route": (st, [vp, vp, sz, vp, u32, u32, vp, vp, vp]),
         "hps_exchange_pool": (st, [vp, vp, u32, vp, vp]),
         "hps_exchange_pairs": (st, [vp, vp, u32, vp, vp, vp, vp]),
-        "hps_exchange_arena": (st, [vp, u64, u32, vp]),
+        "hps_exchange_arena": (st, [vp, u64, u64, u32, vp]),
+        "hps_exchange_pooled": (st, [vp, C.POINTER(vp)]),
         "hps_exchange_connect": (st, [vp, u32, vp]),
         "hps_exchange_forward": (st, [vp, vp, vp, sz, vp, u32, u32, vp]),
         "hps_exchange_backward": (st, [vp, vp, vp, f32, u32, u32, C.POINTER(C.c_int), u32, vp]),

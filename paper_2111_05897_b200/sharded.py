@@ -122,16 +122,28 @@ class DeviceOps:
         return bool(acc.value)
 
 
+class _DeviceArray:
+    """A raw device float32 buffer for torch.as_tensor (zero-copy)."""
+
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
 class PeerExchange:
     """The NVLink peer transport (libhps.so hps_exchange_arena/connect/forward/backward)."""
 
-    def __init__(self, ops: DeviceOps, dist, group, rank: int, max_ids: int):
+    def __init__(self, ops: DeviceOps, dist, group, rank: int, max_ids: int, max_groups: int):
         import torch
 
         self.ops = ops
         self.max_ids = max_ids
         handle = (C.c_uint8 * 64)()
-        hps.check(hps.lib().hps_exchange_arena(ops.h, max_ids, ops.D, handle), "exchange arena")
+        hps.check(hps.lib().hps_exchange_arena(ops.h, max_ids, max_groups, ops.D, handle),
+                  "exchange arena")
+        ptr = hps.vp()
+        hps.check(hps.lib().hps_exchange_pooled(ops.h, C.byref(ptr)), "exchange pooled")
+        self.pooled_ptr = ptr.value
         mine = bytes(handle)
         world = ops.world
         if world > 1:
@@ -150,13 +162,15 @@ class PeerExchange:
                   "exchange forward")
 
     def pool(self, B, F, out=None):
+        """Pooled [B, F, D]: a zero-copy view of the arena's pooled buffer (valid until the
+        next forward) when out is None, else copied into out."""
         o = self.ops
-        t = o.torch
-        if out is None:
-            out = t.empty((B, F, o.D), dtype=t.float32, device=o.device)
-        hps.check(hps.lib().hps_exchange_pool(o.h, None, o.D, out.data_ptr(), o._s()),
-                  "exchange pool")
-        return out
+        hps.check(hps.lib().hps_exchange_pool(o.h, None, o.D,
+                                              out.data_ptr() if out is not None else None,
+                                              o._s()), "exchange pool")
+        if out is not None:
+            return out
+        return o.torch.as_tensor(_DeviceArray(self.pooled_ptr, (B, F, o.D)), device=o.device)
 
     def backward(self, grads, lr, step_tag, epoch, flags):
         o = self.ops
@@ -175,7 +189,8 @@ class ShardedEmbeddingWorker:
     "nccl" (all-to-alls); default "p2p" unless ``ops`` is injected."""
 
     def __init__(self, table: hps.ShardSet, aggregation: int = hps.MEAN, group=None, ops=None,
-                 transport: str | None = None, max_ids: int | None = None):
+                 transport: str | None = None, max_ids: int | None = None,
+                 max_groups: int | None = None):
         import torch.distributed as dist
 
         self.dist = dist
@@ -192,6 +207,7 @@ class ShardedEmbeddingWorker:
         self.B = self.F = 0
         self.peer = None
         self.max_ids = max_ids
+        self.max_groups = max_groups
 
     # -- collectives ------------------------------------------------------------------
     def _exchange_counts(self, counts):
@@ -234,7 +250,8 @@ class ShardedEmbeddingWorker:
         if self.transport == "p2p":
             if self.peer is None:
                 self.peer = PeerExchange(self.ops, self.dist, self.group, self.rank,
-                                         self.max_ids or max(ids.numel(), 1))
+                                         self.max_ids or max(ids.numel(), 1),
+                                         max(self.max_groups or 0, B * F))
             self.peer.forward(ids, offsets, B, F)
             return
         send_ids, counts = self.ops.route(ids, offsets, B, F)
