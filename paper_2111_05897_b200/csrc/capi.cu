@@ -338,7 +338,7 @@ hps_status hps_exchange_route(hps_exchange* x, const uint64_t* ids, size_t n_ids
 hps_status hps_exchange_pool(hps_exchange* x, const float* rows, uint32_t dim, float* out_pooled,
                              hps_stream stream) {
   return guarded([&] {
-    REQUIRE(x && out_pooled, "hps_exchange_pool: null argument");
+    REQUIRE(x && (out_pooled || !rows), "hps_exchange_pool: null argument");
     std::lock_guard<std::mutex> g(x->mu);
     hps::DeviceGuard dg(x->impl.device);
     hps::xbatch_pool(x->impl, rows, dim, out_pooled, S(stream));
