@@ -742,10 +742,13 @@ void table_apply_pairs(Table* t, const uint64_t* recv_ids, const uint64_t* recv_
 //   ppos     [W*Nmax]  u32   pairs this rank owns, source-rank major (written by sources)
 //   contrib  [W*Nmax][D] f32
 //   oslot    [W][Nmax] u32   owner-local: slot of each received id
-//   orv      [W][Nmax] u64   owner-local: version read for it (the pairs' read version)
 //   oids     [W][Nmax] u64   owner-local copy of the id regions (sources may overwrite the
 //   ocnt     [W] u32         regions and counts with the next step once this one's last
 //                            barrier is passed, while the owner still applies)
+//   tgt      [W][Nmax] u32   per received id: the source's one-listing group to write
+//                            the row into directly, or ~0 (written by sources)
+//   pooled   [max_groups][D] f32  this rank's pooled batch (owners write the one-listing
+//                            groups, hps_exchange_pool the rest)
 // A step writes every payload once, directly into the consumer's HBM over NVLink; the
 // only synchronisation is a device-side barrier through the hdr flags.
 
@@ -929,7 +932,6 @@ void xbatch_arena(XBatch& x, uint64_t max_ids, uint64_t max_groups, uint32_t D, 
   x.off_ppos = o;    o += al256(W * M * 4);
   x.off_contrib = o; o += al256(W * M * D * 4);
   x.off_oslot = o;   o += al256(W * M * 4);
-  x.off_orv = o;     o += al256(W * M * 8);
   x.off_oids = o;    o += al256(W * M * 8);
   x.off_ocnt = o;    o += al256(kMaxWorld * 4);
   x.off_tgt = o;     o += al256(W * M * 4);

@@ -175,7 +175,7 @@ struct XBatch {
   uint8_t* peer[kMaxWorld] = {};
   float* arena_rows = nullptr;
   size_t arena_bytes = 0, off_ids = 0, off_rows = 0, off_ppos = 0, off_contrib = 0,
-         off_oslot = 0, off_orv = 0, off_oids = 0, off_ocnt = 0,
+         off_oslot = 0, off_oids = 0, off_ocnt = 0,
          off_tgt = 0, off_pooled = 0;
   uint64_t max_groups = 0;
   bool direct_ok = false;
