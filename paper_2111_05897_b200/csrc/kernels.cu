@@ -117,19 +117,25 @@ void launch_route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cu
 
 // ---- CSR expansion: listing -> (sample*F + group) ---------------------------------------
 
+// kind (optional): bit 2 marks a listing that is alone in its group (its contribution
+// scale is 1 under mean pooling too), for the plan (plan.cu) and update_single.
 __global__ void expand_groups_kernel(const uint32_t* __restrict__ offsets, uint32_t BF,
-                                     uint32_t* __restrict__ lgrp) {
+                                     uint32_t* __restrict__ lgrp, uint8_t* __restrict__ kind) {
   for (uint32_t sg = blockIdx.x * blockDim.x + threadIdx.x; sg < BF;
        sg += gridDim.x * blockDim.x) {
     uint32_t a = offsets[sg], e = offsets[sg + 1];
-    for (uint32_t i = a; i < e; ++i) lgrp[i] = sg;
+    for (uint32_t i = a; i < e; ++i) {
+      lgrp[i] = sg;
+      if (kind) kind[i] = e - a == 1 ? kKindAlone : 0;
+    }
   }
 }
 
-void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st) {
+void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st,
+                          uint8_t* kind) {
   if (!BF) return;
   expand_groups_kernel<<<std::min<uint64_t>(ceil_div(BF, 256), 148 * 16), 256, 0, st>>>(
-      offsets, BF, lgrp);
+      offsets, BF, lgrp, kind);
   HPS_LAUNCH_CHECK();
 }
 

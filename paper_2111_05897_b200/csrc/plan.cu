@@ -55,7 +55,8 @@ __global__ void __launch_bounds__(kPlanBlock)
       const bool multi = (w[j] >> (s[j] & 31)) & 1u;
       mbits |= multi ? 1u << j : 0u;
       mine += multi;
-      if (i < n) kind[i] = s[j] < t.capacity ? (multi ? 2 : 1) : 0;
+      if (i < n)  // (keeps expand_groups' kKindAlone bit)
+        kind[i] = (kind[i] & kKindAlone) | (s[j] < t.capacity ? (multi ? 2 : 1) : 0);
       if (s[j] < t.capacity) atomicAnd(&t.seen[s[j] >> 5], ~(1u << (s[j] & 31)));
     }
     // block-aggregated append position (order is restored by the composite sort);

@@ -559,7 +559,7 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   b.F = F;
   b.N = N;
   HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
-  launch_expand_groups(b.offsets, static_cast<uint32_t>(BF), b.lgrp, st);
+  launch_expand_groups(b.offsets, static_cast<uint32_t>(BF), b.lgrp, st, b.kind);
   // Sample keys that reorder the batch: every listing takes the sorted (multi) path.
   const bool permute = d_sk && B > 1;
   b.all_multi = permute;

@@ -260,7 +260,11 @@ void launch_probe_regions(const DevTable& t, const uint64_t* ids, uint64_t strid
                           uint32_t* cnt_copy, uint32_t* new_slots, uint32_t* new_count, int sms,
                           cudaStream_t st);
 void launch_route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cudaStream_t st);
-void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st);
+// Plan kinds per listing: low bits 1 = row listed once in the batch, 2 = more than once,
+// 0 = no row; kKindAlone = the listing is alone in its (sample, group).
+constexpr uint8_t kKindAlone = 4;
+void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st,
+                          uint8_t* kind = nullptr);
 // slots[i] = find_or_insert(ids[i]); when sort_keys/sort_vals are given also writes the
 // (slot, i) pairs the apply-order sort consumes.
 // plan: also mark the rows in the batch-plan bitmaps (plan.cu).
