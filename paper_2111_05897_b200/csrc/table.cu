@@ -801,6 +801,25 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
     stg.finish(st);
     throw Error(HPS_E_DIVERGENCE, "PsShard::apply_gradients: non-finite gradient");
   }
+  if (!d_dl) {
+    // No per-entry delays wanted: the entries as a batch of one-listing samples (sum
+    // aggregation: each contribution applied as given) through the batch plan -- rows
+    // listed once skip the ordering sort; repeated ids apply in array order.
+    XScratch& xs = t->xs;
+    if (n + 1 > xs.cap_off) {
+      if (xs.off) HPS_CUDA(cudaFree(xs.off));
+      xs.off = nullptr;
+      HPS_CUDA(cudaMalloc(&xs.off, (n + 1 + n / 4 + 1024) * sizeof(uint32_t)));
+      xs.cap_off = n + 1 + n / 4 + 1024;
+    }
+    launch_iota(xs.off, n + 1, st);
+    b.agg = HPS_SUM;
+    batch_register(b, d_ids, n, xs.off, static_cast<uint32_t>(n), 1, nullptr, st);
+    batch_push(b, HPS_SUM, d_g, lr, step_tag, epoch, d_rv ? 0 : 1, d_rv, accepted, flags, st);
+    b.registered = false;
+    stg.finish(st);
+    return;
+  }
   protect_reads(t, nullptr, st);
   forget_outstanding(b);
   b.pulled = false;

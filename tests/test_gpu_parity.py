@@ -246,6 +246,35 @@ def test_direct_apply_delays_and_versions(hps):
     np.testing.assert_array_equal(v, vo)
 
 
+@pytest.mark.parametrize("D,n,space", [(64, 20000, 5000), (3, 300, 40), (16, 9000, 60)])
+def test_direct_apply_without_delays_batch_path(hps, D, n, space):
+    """apply_gradients without per-entry delays runs through the batch plan (singles,
+    repeated ids in array order, >4096 repeated listings -> sorted path); same rows,
+    accumulators and versions as the oracle, and the same delay histogram."""
+    import oracle as O
+
+    t = hps.ShardSet(2, D, 1 << 16, hps.ADAGRAD, salts=[5, 6])
+    orc = O.Restatement([5, 6], D, "adagrad")
+    rng = np.random.default_rng(D)
+    for step in range(1, 4):
+        ids = rng.integers(0, space, n).astype(np.uint64)
+        g = (rng.standard_normal((n, D)) * 0.2).astype(np.float32)
+        _, vg = t.lookup(ids)
+        _, vo = orc.lookup(ids)
+        assert (vg == vo).all()
+        rv = np.maximum(vo.astype(np.int64) - (step % 2), 0).astype(np.uint64)
+        okg, _ = t.apply_gradients(ids, g, rv, 0.1, step, want_delays=False)
+        oko, _ = orc.apply(ids, g, rv, 0.1, step)
+        assert okg and oko
+    keys = np.arange(space, dtype=np.uint64)
+    w, a, v, p = t.peek(keys)
+    wo, ao, vo, po = orc.peek(keys)
+    assert (p == po).all()
+    np.testing.assert_array_equal(w[p], wo[po])
+    np.testing.assert_array_equal(a[p], ao[po])
+    np.testing.assert_array_equal(v[p], vo[po])
+
+
 def test_reference_staleness_cases(hps):
     # test_embedding_ps.cpp:171-211 restated through the C ABI.
     t = hps.ShardSet(1, 2, 16, hps.ADAGRAD, salts=[11])

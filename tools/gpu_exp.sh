@@ -1,7 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
 A="--steps 50 --warmup 5 --e2e-steps 0 --no-cpu-baseline --soak-seconds 0"
-for v in base v4 base v4; do
+for v in base old base old; do
   if [ $v = base ]; then L=""; else L=tools/exp/libhps_$v.so; fi
   HPS_LIB=$L timeout 300 python bench.py $A >> gpurun_out/exp_$v.log 2>&1
 done
