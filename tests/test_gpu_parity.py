@@ -656,3 +656,44 @@ def test_cuda_graph_need_exact_conditional(hps):
         g[:, 1, 0] = np.float32(-1e38)
         return g
     _graph_case(hps, 64, 4, 16, 40, hps.SUM, hps.SGD, huge)
+
+
+def test_stale_multi_bits_from_unapplied_batch(hps):
+    """A batch registered (rows listed twice) but dropped by the epoch fence leaves its
+    plan bits set; a later large-plan batch listing such a row once still applies it."""
+    import oracle as O
+
+    D = 16
+    t = hps.ShardSet(1, D, 1 << 16, hps.ADAGRAD, salts=[9])
+    orc = O.Restatement([9], D, "adagrad")
+    ew = hps.EmbeddingWorker(t, hps.SUM)
+    rng = np.random.default_rng(4)
+    # batch A: ids 0..99 each listed twice; pulled, then pushed with a stale epoch
+    idsA = np.repeat(np.arange(100, dtype=np.uint64), 2)
+    offA = np.arange(len(idsA) + 1, dtype=np.uint32)
+    ew.register_batch(idsA, offA, len(idsA), 1)
+    ew.serve_pull()
+    t.advance_epoch()
+    orc.advance_epoch()
+    gA = rng.standard_normal((len(idsA), 1, D)).astype(np.float32)
+    assert not ew.apply_backward(gA, 0.1, 1, epoch=0)
+    orc.lookup(np.arange(100, dtype=np.uint64))  # the pull's lazy inits
+    # batch B: ids 0..99 once each, plus > 4096 listings of repeated ids 1000..1999
+    idsB = np.concatenate([np.arange(100, dtype=np.uint64),
+                           np.repeat(np.arange(1000, 2000, dtype=np.uint64), 5)])
+    offB = np.arange(len(idsB) + 1, dtype=np.uint32)
+    gB = rng.standard_normal((len(idsB), 1, D)).astype(np.float32)
+    ew.register_batch(idsB, offB, len(idsB), 1)
+    pooled = ew.serve_pull()
+    po, rvo = orc.pull_batch(len(idsB), 1, idsB, offB.astype(np.uint64), "sum")
+    assert pooled.tobytes() == po.tobytes()
+    assert ew.apply_backward(gB, 0.1, 2)
+    ok, _ = orc.push_batch(len(idsB), 1, idsB, offB.astype(np.uint64), gB, 0.1, 2,
+                           read_versions=rvo, agg="sum")
+    assert ok
+    keys = np.concatenate([np.arange(100), np.arange(1000, 2000)]).astype(np.uint64)
+    w, a, v, _ = t.peek(keys)
+    wo, ao, vo, _ = orc.peek(keys)
+    np.testing.assert_array_equal(w, wo)
+    np.testing.assert_array_equal(a, ao)
+    np.testing.assert_array_equal(v, vo)
