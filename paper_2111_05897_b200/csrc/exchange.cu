@@ -978,6 +978,7 @@ static PeerHdrs peer_hdrs(const XBatch& x) {
 // A timeout flags the table (kCtrProtocol): the step's updates are gated off and the
 // failure surfaces from the next synchronising call.
 static void barrier(XBatch& x, Table* t, cudaStream_t st) {
+  ProfScope p(t, "x_barrier", st);
   x_barrier_kernel<<<1, 32, 0, st>>>(peer_hdrs(x), x.G, x.rank, x.dev_epoch,
                                      t->d.ctr + kCtrProtocol);
   HPS_LAUNCH_CHECK();
@@ -1001,10 +1002,13 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
   // one-listing groups are pooled by their rows' owners when the arena's pooled buffer
   // holds the batch (every rank takes the same decision: same batch shapes)
   x.direct_ok = static_cast<uint64_t>(B) * F <= x.max_groups;
-  route_core(x, ids, n, offsets, B, F, nullptr, pid, st);
   const PeerHdrs ph = peer_hdrs(x);
-  x_fwd_hdr_kernel<<<1, 32, 0, st>>>(ph, x.G, x.rank, x.cnt, x.seg);
-  HPS_LAUNCH_CHECK();
+  {
+    ProfScope p(t, "x_route", st);
+    route_core(x, ids, n, offsets, B, F, nullptr, pid, st);
+    x_fwd_hdr_kernel<<<1, 32, 0, st>>>(ph, x.G, x.rank, x.cnt, x.seg);
+    HPS_LAUNCH_CHECK();
+  }
   barrier(x, t, st);  // every id region and count has landed
   // owner: find-or-init the ids every source asked for, rows straight back to them
   XHdr* mine = ph.h[x.rank];
@@ -1013,25 +1017,31 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
   batch_reserve(b, x.G * M, 0, 0);
   b.registered = false;
   HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
-  launch_probe_regions(t->d, reinterpret_cast<const uint64_t*>(x.arena + x.off_ids), M, x.G,
-                       mine, oslot, reinterpret_cast<uint64_t*>(x.arena + x.off_oids),
-                       reinterpret_cast<uint32_t*>(x.arena + x.off_ocnt), b.new_slots,
-                       &b.small[2], t->sm_count, st);
-  launch_lazy_init(t->d, b.new_slots, &b.small[2], x.G * M, t->sm_count, st);
+  {
+    ProfScope p(t, "x_owner_probe", st);
+    launch_probe_regions(t->d, reinterpret_cast<const uint64_t*>(x.arena + x.off_ids), M, x.G,
+                         mine, oslot, reinterpret_cast<uint64_t*>(x.arena + x.off_oids),
+                         reinterpret_cast<uint32_t*>(x.arena + x.off_ocnt), b.new_slots,
+                         &b.small[2], t->sm_count, st);
+    launch_lazy_init(t->d, b.new_slots, &b.small[2], x.G * M, t->sm_count, st);
+  }
   PeerRows pr{}, pp{};
   for (uint32_t r = 0; r < x.G; ++r) {
     pr.p[r] = reinterpret_cast<float*>(x.peer[r] + x.off_rows);
     pp.p[r] = reinterpret_cast<float*>(x.peer[r] + x.off_pooled);
   }
-  HPS_DISPATCH_DIM(t->d.D, {
-    const uint32_t bx = static_cast<uint32_t>(std::max<uint64_t>(
-        1, std::min<uint64_t>(ceil_div(M, 256 / L), uint64_t(t->sm_count) * 16 / x.G + 1)));
-    // (no read versions: the owner applies in fresh mode, see xbatch_bwd)
-    x_owner_gather_kernel<V, L, G><<<dim3(bx, x.G), 256, 0, st>>>(
-        t->d, oslot, M, mine, pr, nullptr, x.direct_ok ? pp : PeerRows{},
-        reinterpret_cast<const uint32_t*>(x.arena + x.off_tgt));
-  });
-  HPS_LAUNCH_CHECK();
+  {
+    ProfScope p(t, "x_owner_gather", st);
+    HPS_DISPATCH_DIM(t->d.D, {
+      const uint32_t bx = static_cast<uint32_t>(std::max<uint64_t>(
+          1, std::min<uint64_t>(ceil_div(M, 256 / L), uint64_t(t->sm_count) * 16 / x.G + 1)));
+      // (no read versions: the owner applies in fresh mode, see xbatch_bwd)
+      x_owner_gather_kernel<V, L, G><<<dim3(bx, x.G), 256, 0, st>>>(
+          t->d, oslot, M, mine, pr, nullptr, x.direct_ok ? pp : PeerRows{},
+          reinterpret_cast<const uint32_t*>(x.arena + x.off_tgt));
+    });
+    HPS_LAUNCH_CHECK();
+  }
   barrier(x, t, st);  // every owner's rows have landed in this rank's rows buffer
 }
 
@@ -1044,6 +1054,7 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
   const PeerHdrs ph = peer_hdrs(x);
   const uint32_t *spos = nullptr, *slist = nullptr;
   if (x.N) {
+    ProfScope p(t, "x_pairs", st);
     pairs_core(x, &spos, &slist, st);
   } else {
     HPS_CUDA(cudaMemsetAsync(x.pair_off, 0, 33 * sizeof(uint64_t), st));
@@ -1059,9 +1070,11 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
       po.c[d] = reinterpret_cast<float*>(x.peer[d] + x.off_contrib);
       po.p[d] = reinterpret_cast<uint32_t*>(x.peer[d] + x.off_ppos);
     }
+    ProfScope p(t, "x_emit", st);
     emit_pairs(x, grads, D, spos, slist, x.xbase, po, st);
   }
   barrier(x, t, st);  // every pair has landed at its owner
+  ProfScope p_apply(t, "x_owner_apply", st);
   // owner: a device-counted batch of the pairs that arrived (no host round trip: the
   // whole step stays stream-ordered and capturable in a CUDA graph)
   XHdr* mine = ph.h[x.rank];

@@ -72,9 +72,26 @@ for it in range(steps + 3):
         for k, n in enumerate(names):
             acc[n] += ev[k].elapsed_time(ev[k + 1])
 table.sync()
+# library-side regions of the p2p step (events on the stream, eager steps)
+prof = {}
+if transport == "p2p":
+    table.profile(True)
+    for it in range(6):
+        ids, offs = bs[it % 3]
+        ew.register_batch(ids, offs, B, F)
+        ew.serve_pull()
+        ew.apply_backward(grads, 0.05, 1000 + it)
+    torch.cuda.synchronize()
+    for r in ("x_route", "x_barrier", "x_owner_probe", "x_owner_gather", "x_pairs", "x_emit",
+              "x_owner_apply", "plan", "sort_small", "sort", "check", "update", "update_multi"):
+        ms_, cnt_ = table.profile_get(r)
+        prof[r] = ms_ / 6
+    table.profile(False)
 if rank == 0:
     tot = sum(acc.values()) / steps
     print(f"transport={transport} world={world} per-step device {tot:.3f} ms, wall {1000 * wall / steps:.3f} ms")
     for n in names:
         print(f"  {n:9s} {acc[n] / steps:7.3f} ms")
+    for r, v in prof.items():
+        print(f"    region {r:15s} {v:7.3f} ms/step")
 dist.destroy_process_group()
