@@ -394,7 +394,9 @@ __global__ void __launch_bounds__(256, 6)
     check_batch_kernel(const float* __restrict__ grads, const uint32_t* __restrict__ offsets,
                        uint64_t rows, uint32_t D, uint32_t F, int mean,
                        unsigned long long* ctr, float* __restrict__ cbuf,
-                       const uint32_t* __restrict__ inv, const uint32_t* gate) {
+                       const uint32_t* __restrict__ inv, const uint32_t* gate,
+                       const uint32_t* rows_live) {
+  if (rows_live) rows = min(rows, static_cast<uint64_t>(*rows_live));
   using G = Geo<V, L, kGuard>;
   constexpr int kCheckILP = 4;
   // large plan: also scatter every listing's contribution to its sorted position, so the
@@ -471,14 +473,15 @@ __global__ void __launch_bounds__(256, 6)
 
 void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
                         uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st,
-                        float* cbuf, const uint32_t* inv, const uint32_t* gate) {
+                        float* cbuf, const uint32_t* inv, const uint32_t* gate,
+                        const uint32_t* rows_live) {
   const uint64_t rows = static_cast<uint64_t>(B) * F;
   if (!rows) return;
   HPS_DISPATCH_DIM(D, {
     uint64_t groups_per_block = 256 / L;
     uint32_t blocks = std::min<uint64_t>(ceil_div(rows, groups_per_block * 4), 148ull * 16);
     check_batch_kernel<V, L, G><<<blocks, 256, 0, st>>>(grads, offsets, rows, D, F, mean, ctr,
-                                                        cbuf, inv, gate);
+                                                        cbuf, inv, gate, rows_live);
   });
   HPS_LAUNCH_CHECK();
 }

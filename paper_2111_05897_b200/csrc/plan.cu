@@ -32,7 +32,8 @@ constexpr int kPlanItems = 4;
 __global__ void __launch_bounds__(kPlanBlock)
     classify_kernel(DevTable t, const uint32_t* __restrict__ slots, uint64_t n, int lbits,
                     uint8_t* __restrict__ kind, unsigned long long* __restrict__ mkeys,
-                    uint32_t* __restrict__ n_multi) {
+                    uint32_t* __restrict__ n_multi, const uint32_t* n_live) {
+  if (n_live) n = min(n, static_cast<uint64_t>(*n_live));
   __shared__ uint32_t s_warp[kPlanBlock / 32];
   __shared__ uint32_t s_base;
   __shared__ bool s_open;
@@ -97,12 +98,13 @@ __global__ void __launch_bounds__(kPlanBlock)
 
 void launch_classify(const DevTable& t, const uint32_t* slots, uint64_t n, int lbits,
                      uint8_t* kind, unsigned long long* mkeys, uint32_t* n_multi, int sms,
-                     cudaStream_t st) {
+                     cudaStream_t st, const uint32_t* n_live) {
   HPS_CUDA(cudaMemsetAsync(n_multi, 0, sizeof(uint32_t), st));
   if (!n) return;
   const uint32_t blocks =
       std::min<uint64_t>(ceil_div(n, kPlanBlock * kPlanItems), static_cast<uint64_t>(sms) * 8);
-  classify_kernel<<<blocks, kPlanBlock, 0, st>>>(t, slots, n, lbits, kind, mkeys, n_multi);
+  classify_kernel<<<blocks, kPlanBlock, 0, st>>>(t, slots, n, lbits, kind, mkeys, n_multi,
+                                                  n_live);
   HPS_LAUNCH_CHECK();
 }
 

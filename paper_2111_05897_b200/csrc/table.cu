@@ -457,6 +457,7 @@ static UpdateArgs plan_args(const Batch& b) {
   a.F = b.F;
   a.meta = b.meta_ok ? b.meta : nullptr;
   a.cbuf = b.meta_ok ? b.cbuf : nullptr;
+  a.n_live = b.n_live;
   return a;
 }
 
@@ -558,6 +559,7 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   b.B = B;
   b.F = F;
   b.N = N;
+  b.n_live = dynamic ? b.offsets + BF : nullptr;
   HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
   launch_expand_groups(b.offsets, static_cast<uint32_t>(BF), b.lgrp, st, b.kind);
   // Sample keys that reorder the batch: every listing takes the sorted (multi) path.
@@ -590,7 +592,8 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     const int lbits = std::max(1, bits_for(N ? N - 1 : 0));
     {
       ProfScope p(t, "plan", st);
-      launch_classify(t->d, b.slot, N, lbits, b.kind, b.mkeys, &b.small[0], t->sm_count, st);
+      launch_classify(t->d, b.slot, N, lbits, b.kind, b.mkeys, &b.small[0], t->sm_count, st,
+                      b.n_live);
     }
     {
       ProfScope p(t, "sort_small", st);
@@ -650,7 +653,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     ProfScope p(t, "check", st);
     launch_check_batch(d_g, b.offsets, b.B, b.F, D, mean, t->d.ctr, st,
                        b.meta_ok ? b.cbuf : nullptr, b.inv,
-                       b.all_multi ? nullptr : &b.small[0]);
+                       b.all_multi ? nullptr : &b.small[0], b.n_live);
   }
   UpdateArgs a = plan_args(b);
   a.mean = mean;

@@ -143,6 +143,9 @@ struct Batch {
   uint32_t* mlist = nullptr;      // [N + 1] sorted-list starts of the other listed rows
   uint64_t* meta = nullptr;       // [N] large path: per sorted position, group | size << 32
   bool meta_ok = false;
+  // dynamic batches (one listing per live group, live groups first): the live count is
+  // offsets[B*F] on the device; kernels bound their loops by it
+  const uint32_t* n_live = nullptr;
   uint32_t* inv = nullptr;        // [N] large path: sorted position of each listing
   float* cbuf = nullptr;          // [N][D] large path: contribution per sorted position
   uint64_t cap_cbuf = 0;
@@ -275,7 +278,7 @@ void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* 
 // plan.cu
 void launch_classify(const DevTable& t, const uint32_t* slots, uint64_t n, int lbits,
                      uint8_t* kind, unsigned long long* mkeys, uint32_t* n_multi, int sms,
-                     cudaStream_t st);
+                     cudaStream_t st, const uint32_t* n_live = nullptr);
 void launch_ht_clear(const DevTable& t, cudaStream_t st);
 void launch_lazy_init(const DevTable& t, const uint32_t* new_slots, const uint32_t* new_count,
                       uint64_t max_new, int sms, cudaStream_t st);
@@ -297,7 +300,7 @@ void launch_check_direct(const float* grads, uint64_t n_floats, unsigned long lo
 void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
                         uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st,
                         float* cbuf = nullptr, const uint32_t* inv = nullptr,
-                        const uint32_t* gate = nullptr);
+                        const uint32_t* gate = nullptr, const uint32_t* rows_live = nullptr);
 
 struct UpdateArgs {
   // Multi kernel input: either the large-path slot sort of all n listings, or -- when
@@ -339,6 +342,8 @@ struct UpdateArgs {
   uint32_t mlist_cap;
   // large (sorted) path: per sorted position, the listing's group | group size << 32
   const uint64_t* meta;
+  // dynamic batches: live listings (= live groups) on the device; null = a.n
+  const uint32_t* n_live;
   // large path: per sorted position, float(0.0 + (double)g * scale) of its listing, written
   // by the validation pass (right for pairs of one listing; longer pairs are summed here)
   const float* cbuf;
