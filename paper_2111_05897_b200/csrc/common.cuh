@@ -13,6 +13,7 @@
 #include <atomic>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "../../include/hps_c.h"
 
@@ -52,6 +53,38 @@ inline std::atomic<unsigned long long> g_launches{0};
     HPS_CUDA(cudaGetLastError());                                  \
   } while (0)
 #define HPS_LAUNCH_CHECK() HPS_LAUNCH_CHECK_N(1)
+
+// Programmatic dependent launch (PDL). Every kernel of the library starts with
+// pdl_entry(): griddepcontrol.wait (the previous grid of the stream has completed and
+// its writes are visible -- so nothing a kernel reads can race its predecessor, and by
+// induction any earlier kernel), then griddepcontrol.launch_dependents (the next grid
+// may be scheduled now). launch() issues kernels with the programmatic-serialization
+// attribute, so the next kernel's launch and block rasterisation overlap this one's
+// tail instead of following its completion; a step is ~18 short dependent kernels,
+// most of them a few microseconds. Outside a PDL launch both instructions are no-ops.
+// HPS_PDL=0 turns the attribute off (A/B measurement).
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                   cudaStream_t st, Args&&... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  HPS_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x += kGamma;

@@ -23,6 +23,7 @@ constexpr int kScanTile = 4096;
 
 __global__ void or_reduce_kernel(const uint64_t* __restrict__ k, uint64_t n,
                                  unsigned long long* out) {
+  pdl_entry();
   uint64_t acc = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -34,6 +35,7 @@ __global__ void or_reduce_kernel(const uint64_t* __restrict__ k, uint64_t n,
 
 __global__ void tile_sum_kernel(const uint32_t* __restrict__ in, uint64_t n,
                                 uint32_t* __restrict__ sums) {
+  pdl_entry();
   __shared__ uint32_t s[32];
   uint64_t base = (uint64_t)blockIdx.x * kScanTile;
   uint32_t acc = 0;
@@ -56,6 +58,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
                                                          uint64_t n,
                                                          const uint32_t* __restrict__ offs,
                                                          uint32_t* __restrict__ out) {
+  pdl_entry();
   __shared__ uint32_t ws[32];
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile + threadIdx.x * 4;
   uint32_t v[4];
@@ -93,6 +96,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
 // group changes (key2) and, separately, a posting head when the sample changes.
 __global__ void dedup_flags_kernel(const uint64_t* __restrict__ keys, uint64_t n,
                                    uint32_t* __restrict__ head) {
+  pdl_entry();
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
        p += (uint64_t)gridDim.x * blockDim.x)
     head[p] = (p == 0 || keys[p] != keys[p - 1]) ? 1u : 0u;
@@ -104,6 +108,7 @@ __global__ void dedup_emit_kernel(const uint64_t* __restrict__ keys,
                                   const uint32_t* __restrict__ excl, uint64_t n,
                                   uint64_t* __restrict__ unique, uint32_t* __restrict__ inverse,
                                   uint64_t* __restrict__ out_u) {
+  pdl_entry();
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
        p += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t u = excl[p] + head[p] - 1;
@@ -115,6 +120,7 @@ __global__ void dedup_emit_kernel(const uint64_t* __restrict__ keys,
 
 __global__ void ci_expand_kernel(const uint32_t* __restrict__ off, uint32_t B, uint32_t G,
                                  uint32_t* __restrict__ lgrp) {
+  pdl_entry();
   for (uint32_t sg = blockIdx.x * blockDim.x + threadIdx.x; sg < B * G;
        sg += gridDim.x * blockDim.x)
     for (uint32_t i = off[sg]; i < off[sg + 1]; ++i) lgrp[i] = sg;
@@ -123,6 +129,7 @@ __global__ void ci_expand_kernel(const uint32_t* __restrict__ off, uint32_t B, u
 __global__ void ci_group_keys_kernel(const uint32_t* __restrict__ vals,
                                      const uint32_t* __restrict__ lgrp, uint32_t G, uint64_t n,
                                      uint32_t* __restrict__ gkeys) {
+  pdl_entry();
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
        p += (uint64_t)gridDim.x * blockDim.x)
     gkeys[p] = lgrp[vals[p]] % G;
@@ -135,6 +142,7 @@ __global__ void ci_flags_kernel(const uint32_t* __restrict__ vals,
                                 const uint32_t* __restrict__ lgrp, uint32_t G, uint64_t n,
                                 uint32_t* __restrict__ uflag, uint32_t* __restrict__ pflag,
                                 uint32_t* __restrict__ group_cnt) {
+  pdl_entry();
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
        p += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t i = vals[p];
@@ -159,6 +167,7 @@ __global__ void ci_emit_kernel(const uint32_t* __restrict__ vals, const uint64_t
                                const uint32_t* __restrict__ pflag,
                                const uint32_t* __restrict__ pex, uint64_t* __restrict__ unique,
                                uint64_t* __restrict__ post_off, uint16_t* __restrict__ postings) {
+  pdl_entry();
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
        p += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t i = vals[p];
@@ -173,6 +182,7 @@ __global__ void ci_emit_kernel(const uint32_t* __restrict__ vals, const uint64_t
 
 __global__ void ci_group_off_kernel(const uint32_t* __restrict__ cnt, uint32_t G,
                                     uint64_t* __restrict__ out) {
+  pdl_entry();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     uint64_t run = 0;
     out[0] = 0;
@@ -204,9 +214,9 @@ uint32_t grid_for(uint64_t n) { return std::max<uint32_t>(1, std::min<uint64_t>(
 void exclusive_scan(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* tile_sums,
                     uint32_t* total, cudaStream_t st) {
   uint32_t tiles = ceil_div(n, kScanTile);
-  tile_sum_kernel<<<tiles, 256, 0, st>>>(in, n, tile_sums);
-  radix::scan_digits<<<1, 1024, 0, st>>>(tile_sums, tiles, total);
-  tile_scan_kernel<<<tiles, 1024, 0, st>>>(in, n, tile_sums, out);
+  launch(tile_sum_kernel, tiles, 256, 0, st, in, n, tile_sums);
+  launch(radix::scan_digits, 1, 1024, 0, st, tile_sums, tiles, total);
+  launch(tile_scan_kernel, tiles, 1024, 0, st, in, n, tile_sums, out);
   HPS_LAUNCH_CHECK_N(3);
 }
 
@@ -214,7 +224,7 @@ namespace {
 
 int key_bits_of(const uint64_t* keys, uint64_t n, unsigned long long* d_or, cudaStream_t st) {
   HPS_CUDA(cudaMemsetAsync(d_or, 0, sizeof(unsigned long long), st));
-  or_reduce_kernel<<<grid_for(n), 256, 0, st>>>(keys, n, d_or);
+  launch(or_reduce_kernel, grid_for(n), 256, 0, st, keys, n, d_or);
   unsigned long long h = 0;
   HPS_CUDA(cudaMemcpyAsync(&h, d_or, sizeof(h), cudaMemcpyDeviceToHost, st));
   HPS_CUDA(cudaStreamSynchronize(st));
@@ -253,9 +263,9 @@ void dedup(const uint64_t* ids, uint64_t n, uint64_t* out_unique, uint32_t* out_
   bool in_b = radix::sort_pairs<uint64_t>(ka, va, kb, vb, n, bits, hist, st);
   const uint64_t* sk = in_b ? kb : ka;
   const uint32_t* sv = in_b ? vb : va;
-  dedup_flags_kernel<<<grid_for(n), 256, 0, st>>>(sk, n, head);
+  launch(dedup_flags_kernel, grid_for(n), 256, 0, st, sk, n, head);
   exclusive_scan(head, ex, n, tsum, tsum + ceil_div(n, kScanTile), st);
-  dedup_emit_kernel<<<grid_for(n), 256, 0, st>>>(sk, sv, head, ex, n, d_uni, d_inv, d_u);
+  launch(dedup_emit_kernel, grid_for(n), 256, 0, st, sk, sv, head, ex, n, d_uni, d_inv, d_u);
   HPS_LAUNCH_CHECK();
   HPS_CUDA(cudaMemcpyAsync(out_u, d_u, sizeof(uint64_t),
                            is_device_ptr(out_u) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
@@ -285,7 +295,7 @@ void compress_indices(const uint64_t* ids, uint64_t n, const uint32_t* offsets, 
   uint32_t* gcnt = s.get<uint32_t>(0, G + 1);
   HPS_CUDA(cudaMemsetAsync(gcnt, 0, (G + 1) * sizeof(uint32_t), st));
   if (n == 0) {
-    ci_group_off_kernel<<<1, 32, 0, st>>>(gcnt, G, d_guo);
+    launch(ci_group_off_kernel, 1, 32, 0, st, gcnt, G, d_guo);
     HPS_CUDA(cudaMemsetAsync(d_po, 0, sizeof(uint64_t), st));
     stg.finish(st);
     return;
@@ -302,7 +312,7 @@ void compress_indices(const uint64_t* ids, uint64_t n, const uint32_t* offsets, 
   uint32_t* ex2 = s.get<uint32_t>(10, n);
   uint32_t* tsum = s.get<uint32_t>(11, 2 * (ceil_div(n, kScanTile) + 1));
   unsigned long long* d_or = reinterpret_cast<unsigned long long*>(kb);  // reused before sorting
-  ci_expand_kernel<<<grid_for(BG), 256, 0, st>>>(d_off, B, G, lgrp);
+  launch(ci_expand_kernel, grid_for(BG), 256, 0, st, d_off, B, G, lgrp);
   HPS_CUDA(cudaMemcpyAsync(ka, d_ids, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
   launch_iota(va, n, st);
   int bits = key_bits_of(ka, n, d_or, st);
@@ -312,18 +322,18 @@ void compress_indices(const uint64_t* ids, uint64_t n, const uint32_t* offsets, 
   // Pass 2: stable by group.
   uint32_t* gk = reinterpret_cast<uint32_t*>(in_b ? ka : kb);
   uint32_t* gk2 = reinterpret_cast<uint32_t*>(in_b ? kb : ka) ;
-  ci_group_keys_kernel<<<grid_for(n), 256, 0, st>>>(v1, lgrp, G, n, gk);
+  launch(ci_group_keys_kernel, grid_for(n), 256, 0, st, v1, lgrp, G, n, gk);
   uint32_t* v2 = in_b ? va : vb;
   bool in2 = radix::sort_pairs<uint32_t>(gk, v1, gk2, v2, n,
                                          std::max(1, bits_for(G - 1)), hist, st);
   const uint32_t* sv = in2 ? v2 : v1;
-  ci_flags_kernel<<<grid_for(n), 256, 0, st>>>(sv, d_ids, lgrp, G, n, fl, fl2, gcnt);
+  launch(ci_flags_kernel, grid_for(n), 256, 0, st, sv, d_ids, lgrp, G, n, fl, fl2, gcnt);
   uint32_t tiles = ceil_div(n, kScanTile);
   exclusive_scan(fl, ex, n, tsum, tsum + tiles, st);
   exclusive_scan(fl2, ex2, n, tsum + tiles + 1, tsum + 2 * tiles + 1, st);
-  ci_emit_kernel<<<grid_for(n), 256, 0, st>>>(sv, d_ids, lgrp, G, n, fl, ex, fl2, ex2, d_uni, d_po,
+  launch(ci_emit_kernel, grid_for(n), 256, 0, st, sv, d_ids, lgrp, G, n, fl, ex, fl2, ex2, d_uni, d_po,
                                                d_ps);
-  ci_group_off_kernel<<<1, 32, 0, st>>>(gcnt, G, d_guo);
+  launch(ci_group_off_kernel, 1, 32, 0, st, gcnt, G, d_guo);
   HPS_LAUNCH_CHECK();
   HPS_CUDA(cudaStreamSynchronize(st));
   stg.finish(st);

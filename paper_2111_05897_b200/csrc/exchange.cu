@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(kXBlock)
     x_insert_kernel(const uint64_t* __restrict__ ids, uint64_t n, uint64_t* hkeys,
                     uint64_t mask, int shift, uint32_t* special, uint32_t* __restrict__ hidx,
                     uint8_t* __restrict__ hmul) {
+  pdl_entry();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t id = ids[i];
@@ -91,6 +92,7 @@ __global__ void __launch_bounds__(kXBlock)
                     const uint32_t* __restrict__ hidx, const uint8_t* __restrict__ hmul,
                     uint32_t* __restrict__ hval, uint8_t* __restrict__ dest,
                     uint32_t* __restrict__ spair, uint32_t* cnt) {
+  pdl_entry();
   __shared__ uint32_t bc[32], gb[32], sc[32], sb[32];
   for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < n;
        base += (uint64_t)gridDim.x * blockDim.x) {
@@ -155,6 +157,7 @@ __global__ void __launch_bounds__(kXBlock)
                      unsigned long long* __restrict__ mkeys, PeerIds pid,
                      const uint32_t* __restrict__ lgrp, const uint32_t* __restrict__ offsets,
                      uint8_t* __restrict__ gdirect) {
+  pdl_entry();
   __shared__ uint32_t seg[33];
   __shared__ uint32_t s_n, s_base;
   load_seg(cnt, G, seg);
@@ -207,6 +210,7 @@ __global__ void x_pair_flags_kernel(const uint32_t* __restrict__ spos,
                                     const uint32_t* __restrict__ spair, uint32_t F,
                                     uint64_t n_host, const uint32_t* __restrict__ n_multi,
                                     uint32_t* __restrict__ head) {
+  pdl_entry();
   const bool large = *n_multi > radix::kSmallN;
   const uint64_t n = large ? n_host : *n_multi;
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n_host;
@@ -229,6 +233,7 @@ __global__ void x_pair_bounds_kernel(const uint32_t* __restrict__ spos,
                                      const uint32_t* __restrict__ seg, uint32_t G,
                                      uint64_t* __restrict__ pair_off,
                                      uint32_t* __restrict__ mstart) {
+  pdl_entry();
   __shared__ uint32_t ms[33];
   const uint32_t nm = cnt[kCntMulti];
   const uint64_t n = nm > radix::kSmallN ? n_host : nm;
@@ -285,6 +290,7 @@ __global__ void __launch_bounds__(kXBlock)
                          const uint32_t* __restrict__ offsets, uint64_t n, uint32_t D, int mean,
                          const float* __restrict__ grads, const uint32_t* __restrict__ seg,
                          const uint64_t* __restrict__ base, PairOut po) {
+  pdl_entry();
   const uint32_t lane = threadIdx.x % L;
   const uint64_t groups = (uint64_t)gridDim.x * (kXBlock / L);
   for (uint64_t i = blockIdx.x * (uint64_t)(kXBlock / L) + threadIdx.x / L; i < n;
@@ -325,6 +331,7 @@ __global__ void __launch_bounds__(kXBlock)
                         const uint8_t* __restrict__ dest_of_pos,
                         const uint32_t* __restrict__ seg, const uint64_t* __restrict__ base,
                         const uint32_t* __restrict__ mstart, PairOut po) {
+  pdl_entry();
   const uint32_t nm = cnt[kCntMulti];
   const uint64_t n = nm > radix::kSmallN ? n_host : nm;
   const uint32_t lane = threadIdx.x % L;
@@ -369,6 +376,7 @@ __global__ void __launch_bounds__(kXBlock)
 // is device-side, the grid covers the host bound n >= U.
 __global__ void x_dest_of_pos_kernel(const uint32_t* __restrict__ seg, uint32_t G, uint64_t n,
                                      uint8_t* __restrict__ out) {
+  pdl_entry();
   const uint64_t U = seg[G];
   for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < U && u < n;
        u += (uint64_t)gridDim.x * blockDim.x) {
@@ -381,6 +389,7 @@ __global__ void x_dest_of_pos_kernel(const uint32_t* __restrict__ seg, uint32_t 
 // Per-owner counts as u64 into a device array (no host round trip).
 __global__ void x_counts_kernel(const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ off,
                                 uint32_t G, uint64_t* __restrict__ out) {
+  pdl_entry();
   const uint32_t d = threadIdx.x;
   if (d < G) out[d] = cnt ? cnt[d] : off[d + 1] - off[d];
 }
@@ -391,6 +400,7 @@ __global__ void x_pick_small_kernel(const uint32_t* __restrict__ n_multi,
                                     const uint32_t* __restrict__ sm_pos,
                                     const uint32_t* __restrict__ sm_list,
                                     uint32_t* __restrict__ spos, uint32_t* __restrict__ slist) {
+  pdl_entry();
   const uint32_t nm = *n_multi;
   if (nm > radix::kSmallN) return;
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -414,6 +424,7 @@ __global__ void x_owner_kernel(const uint64_t* __restrict__ recv_ids,
                                uint64_t P, uint64_t* __restrict__ out_ids,
                                uint64_t* __restrict__ out_rv, uint32_t* __restrict__ out_off,
                                unsigned long long* protocol) {
+  pdl_entry();
   for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k <= P;
        k += (uint64_t)gridDim.x * blockDim.x) {
     out_off[k] = static_cast<uint32_t>(k);
@@ -519,9 +530,9 @@ static void route_core(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_
   if (n) {
     HPS_CUDA(cudaMemsetAsync(x.hkeys, 0xff, H * sizeof(uint64_t), st));
     HPS_CUDA(cudaMemsetAsync(x.hmul, 0, H + 1, st));
-    x_insert_kernel<<<grid_n(n, x.sms), kXBlock, 0, st>>>(ids, n, x.hkeys, H - 1, 64 - lg,
+    launch(x_insert_kernel, grid_n(n, x.sms), kXBlock, 0, st, ids, n, x.hkeys, H - 1, 64 - lg,
                                                           x.cnt + kCntSpecial, x.hidx, x.hmul);
-    x_number_kernel<<<grid_n(n, x.sms), kXBlock, 0, st>>>(ids, n, x.S, x.G, x.hidx, x.hmul,
+    launch(x_number_kernel, grid_n(n, x.sms), kXBlock, 0, st, ids, n, x.S, x.G, x.hidx, x.hmul,
                                                           x.hval, x.dest, x.spair, x.cnt);
     HPS_LAUNCH_CHECK_N(2);
   }
@@ -531,7 +542,7 @@ static void route_core(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_
     gdirect = x.gdirect;
     HPS_CUDA(cudaMemsetAsync(gdirect, 0, BF, st));
   }
-  x_scatter_kernel<<<grid_n(std::max<uint64_t>(n, 1), x.sms), kXBlock, 0, st>>>(
+  launch(x_scatter_kernel, grid_n(std::max<uint64_t>(n, 1), x.sms), kXBlock, 0, st, 
       ids, n, x.G, x.hidx, x.hval, x.dest, x.spair, x.cnt, x.lbits, x.sendpos, send_ids, x.seg,
       x.mkeys, pid, x.lgrp, x.offsets, gdirect);
   HPS_LAUNCH_CHECK();
@@ -564,13 +575,13 @@ static void pairs_core(XBatch& x, const uint32_t** spos_out, const uint32_t** sl
   });
   uint32_t* spos = in_b ? x.keys_b : x.keys_a;
   uint32_t* slist = in_b ? x.vals_b : x.vals_a;
-  x_pick_small_kernel<<<ceil_div(radix::kSmallN, kXBlock), kXBlock, 0, st>>>(
+  launch(x_pick_small_kernel, ceil_div(radix::kSmallN, kXBlock), kXBlock, 0, st, 
       n_multi, x.sm_pos, x.sm_list, spos, slist);
-  x_pair_flags_kernel<<<grid_n(n, x.sms), kXBlock, 0, st>>>(spos, slist, x.lgrp, x.spair, x.F,
+  launch(x_pair_flags_kernel, grid_n(n, x.sms), kXBlock, 0, st, spos, slist, x.lgrp, x.spair, x.F,
                                                             n, n_multi, x.head);
   exclusive_scan(x.head, x.ex, n, x.tsum, x.tsum + ceil_div(n, 4096), st);
-  x_dest_of_pos_kernel<<<grid_n(n, x.sms), kXBlock, 0, st>>>(x.seg, x.G, n, x.dest_of_pos);
-  x_pair_bounds_kernel<<<1, 64, 0, st>>>(spos, x.ex, x.head, n, x.cnt, x.seg, x.G, x.pair_off,
+  launch(x_dest_of_pos_kernel, grid_n(n, x.sms), kXBlock, 0, st, x.seg, x.G, n, x.dest_of_pos);
+  launch(x_pair_bounds_kernel, 1, 64, 0, st, spos, x.ex, x.head, n, x.cnt, x.seg, x.G, x.pair_off,
                                          x.mstart);
   HPS_LAUNCH_CHECK_N(4);
   *spos_out = spos;
@@ -585,9 +596,9 @@ static void emit_pairs(XBatch& x, const float* grads, uint32_t D, const uint32_t
   HPS_DISPATCH_DIM(D, {
     const uint32_t blocks = static_cast<uint32_t>(std::max<uint64_t>(
         1, std::min<uint64_t>(ceil_div(n, kXBlock / L), uint64_t(x.sms) * 16)));
-    x_single_emit_kernel<V, L, G><<<blocks, kXBlock, 0, st>>>(
+    launch(x_single_emit_kernel<V, L, G>, blocks, kXBlock, 0, st, 
         x.spair, x.dest, x.sendpos, x.lgrp, x.offsets, n, D, mean, grads, x.seg, base, po);
-    x_multi_emit_kernel<V, L, G><<<blocks, kXBlock, 0, st>>>(
+    launch(x_multi_emit_kernel<V, L, G>, blocks, kXBlock, 0, st, 
         spos, slist, x.head, x.ex, x.lgrp, x.offsets, x.F, n, x.cnt, D, mean, grads,
         x.dest_of_pos, x.seg, base, x.mstart, po);
   });
@@ -602,7 +613,7 @@ void xbatch_route(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_t* of
   if (n && !out_send_ids) throw Error(HPS_E_PRECONDITION, "hps_exchange_route: null send_ids");
   route_core(x, ids, n, offsets, B, F, out_send_ids, PeerIds{}, st);
   if (is_device_ptr(out_counts)) {  // stays on the device: no host round trip
-    x_counts_kernel<<<1, 32, 0, st>>>(x.cnt, nullptr, x.G, out_counts);
+    launch(x_counts_kernel, 1, 32, 0, st, x.cnt, nullptr, x.G, out_counts);
     HPS_LAUNCH_CHECK();
     return;
   }
@@ -677,7 +688,7 @@ void xbatch_pairs(XBatch& x, const float* grads, uint32_t D, uint32_t* out_pair_
   for (uint32_t d = 0; d < x.G; ++d) po.c[d] = out_contrib, po.p[d] = out_pair_pos;
   emit_pairs(x, grads, D, spos, slist, x.pair_off, po, st);
   if (is_device_ptr(out_pair_counts)) {
-    x_counts_kernel<<<1, 32, 0, st>>>(nullptr, x.pair_off, x.G, out_pair_counts);
+    launch(x_counts_kernel, 1, 32, 0, st, nullptr, x.pair_off, x.G, out_pair_counts);
     HPS_LAUNCH_CHECK();
     return;
   }
@@ -700,7 +711,7 @@ static void owner_apply(Table* t, const uint64_t* recv_ids, const uint64_t* recv
   grow(xs.ids, xs.cap_ids, P);
   grow(xs.rv, xs.cap_rv, P);
   grow(xs.off, xs.cap_off, P + 1);
-  x_owner_kernel<<<grid_n(P + 1, t->sm_count), kXBlock, 0, st>>>(
+  launch(x_owner_kernel, grid_n(P + 1, t->sm_count), kXBlock, 0, st, 
       recv_ids, recv_versions, io, ie, po, G, pair_pos, P, xs.ids, xs.rv, xs.off,
       t->d.ctr + kCtrProtocol);
   HPS_LAUNCH_CHECK();
@@ -769,6 +780,7 @@ __global__ void x_owner_dyn_kernel(const XHdr* __restrict__ hdr,
                                    unsigned long long* protocol, DevTable t,
                                    const uint32_t* __restrict__ oslot,
                                    uint32_t* __restrict__ out_slot) {
+  pdl_entry();
   __shared__ uint64_t po[kMaxWorld + 1];
   if (threadIdx.x == 0) {
     uint64_t run = 0;
@@ -819,6 +831,7 @@ constexpr long long kBarrierTimeoutCycles = 8'000'000'000ll;  // ~4 s: never han
 // flags the table (updates are gated off) and surfaces as HPS_E_SYNC_FAILURE.
 __global__ void x_barrier_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
                                  unsigned long long* epoch_ctr, unsigned long long* fail) {
+  pdl_entry();
   __shared__ unsigned long long s_epoch;
   const uint32_t t = threadIdx.x;
   // The epoch lives on the device, so a barrier captured in a CUDA graph advances it on
@@ -853,6 +866,7 @@ __global__ void x_barrier_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
 __global__ void x_fwd_hdr_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
                                  const uint32_t* __restrict__ cnt,
                                  const uint32_t* __restrict__ seg) {
+  pdl_entry();
   const uint32_t d = threadIdx.x;
   if (d < W) {
     ph.h[d]->fwd_cnt[rank] = cnt[d];
@@ -862,6 +876,7 @@ __global__ void x_fwd_hdr_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
 
 __global__ void x_bwd_hdr_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
                                  const uint64_t* __restrict__ pair_off) {
+  pdl_entry();
   const uint32_t d = threadIdx.x;
   if (d < W) ph.h[d]->bwd_cnt[rank] = static_cast<uint32_t>(pair_off[d + 1] - pair_off[d]);
 }
@@ -869,6 +884,7 @@ __global__ void x_bwd_hdr_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
 // Where this rank's pairs start in each owner's (source-rank major) pair arrays.
 __global__ void x_bwd_base_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
                                   uint64_t* __restrict__ base) {
+  pdl_entry();
   const uint32_t d = threadIdx.x;
   if (d < W) {
     uint64_t b = 0;
@@ -885,6 +901,7 @@ __global__ void __launch_bounds__(256)
                           const XHdr* __restrict__ hdr, PeerRows pr,
                           uint64_t* __restrict__ orv, PeerRows pooled,
                           const uint32_t* __restrict__ tgt) {
+  pdl_entry();
   using Gm = Geo<V, L, kGuard>;
   const uint32_t r = blockIdx.y;
   const uint64_t n = ld_volatile(&hdr->fwd_cnt[r]);
@@ -979,7 +996,7 @@ static PeerHdrs peer_hdrs(const XBatch& x) {
 // failure surfaces from the next synchronising call.
 static void barrier(XBatch& x, Table* t, cudaStream_t st) {
   ProfScope p(t, "x_barrier", st);
-  x_barrier_kernel<<<1, 32, 0, st>>>(peer_hdrs(x), x.G, x.rank, x.dev_epoch,
+  launch(x_barrier_kernel, 1, 32, 0, st, peer_hdrs(x), x.G, x.rank, x.dev_epoch,
                                      t->d.ctr + kCtrProtocol);
   HPS_LAUNCH_CHECK();
 }
@@ -1006,7 +1023,7 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
   {
     ProfScope p(t, "x_route", st);
     route_core(x, ids, n, offsets, B, F, nullptr, pid, st);
-    x_fwd_hdr_kernel<<<1, 32, 0, st>>>(ph, x.G, x.rank, x.cnt, x.seg);
+    launch(x_fwd_hdr_kernel, 1, 32, 0, st, ph, x.G, x.rank, x.cnt, x.seg);
     HPS_LAUNCH_CHECK();
   }
   barrier(x, t, st);  // every id region and count has landed
@@ -1036,7 +1053,7 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
       const uint32_t bx = static_cast<uint32_t>(std::max<uint64_t>(
           1, std::min<uint64_t>(ceil_div(M, 256 / L), uint64_t(t->sm_count) * 16 / x.G + 1)));
       // (no read versions: the owner applies in fresh mode, see xbatch_bwd)
-      x_owner_gather_kernel<V, L, G><<<dim3(bx, x.G), 256, 0, st>>>(
+      launch(x_owner_gather_kernel<V, L, G>, dim3(bx, x.G), 256, 0, st, 
           t->d, oslot, M, mine, pr, nullptr, x.direct_ok ? pp : PeerRows{},
           reinterpret_cast<const uint32_t*>(x.arena + x.off_tgt));
     });
@@ -1059,10 +1076,10 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
   } else {
     HPS_CUDA(cudaMemsetAsync(x.pair_off, 0, 33 * sizeof(uint64_t), st));
   }
-  x_bwd_hdr_kernel<<<1, 32, 0, st>>>(ph, x.G, x.rank, x.pair_off);
+  launch(x_bwd_hdr_kernel, 1, 32, 0, st, ph, x.G, x.rank, x.pair_off);
   HPS_LAUNCH_CHECK();
   barrier(x, t, st);  // every owner knows how many pairs each source sends
-  x_bwd_base_kernel<<<1, 32, 0, st>>>(ph, x.G, x.rank, x.xbase);
+  launch(x_bwd_base_kernel, 1, 32, 0, st, ph, x.G, x.rank, x.xbase);
   HPS_LAUNCH_CHECK();
   if (x.N) {
     PairOut po{};
@@ -1086,7 +1103,7 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
   Batch& b = t->scratch;
   b.agg = HPS_SUM;
   batch_reserve(b, cap, cap, cap);
-  x_owner_dyn_kernel<<<grid_n(cap + 1, t->sm_count), kXBlock, 0, st>>>(
+  launch(x_owner_dyn_kernel, grid_n(cap + 1, t->sm_count), kXBlock, 0, st, 
       mine, reinterpret_cast<const uint32_t*>(x.arena + x.off_ocnt), x.G, M,
       reinterpret_cast<const uint64_t*>(x.arena + x.off_oids), nullptr,
       reinterpret_cast<const uint32_t*>(x.arena + x.off_ppos), cap, xs.ids, xs.rv, xs.off,

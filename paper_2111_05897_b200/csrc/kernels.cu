@@ -104,6 +104,7 @@ __device__ uint32_t find_or_insert(const DevTable& t, uint64_t id, uint32_t* new
 
 __global__ void route_kernel(const uint64_t* __restrict__ ids, uint64_t n, uint32_t S,
                              uint32_t* __restrict__ out) {
+  pdl_entry();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
     out[i] = route_shard(ids[i], S);
@@ -111,7 +112,7 @@ __global__ void route_kernel(const uint64_t* __restrict__ ids, uint64_t n, uint3
 
 void launch_route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cudaStream_t st) {
   if (!n) return;
-  route_kernel<<<std::min<uint64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st>>>(ids, n, S, out);
+  launch(route_kernel, std::min<uint64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st, ids, n, S, out);
   HPS_LAUNCH_CHECK();
 }
 
@@ -121,6 +122,7 @@ void launch_route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cu
 // scale is 1 under mean pooling too), for the plan (plan.cu) and update_single.
 __global__ void expand_groups_kernel(const uint32_t* __restrict__ offsets, uint32_t BF,
                                      uint32_t* __restrict__ lgrp, uint8_t* __restrict__ kind) {
+  pdl_entry();
   for (uint32_t sg = blockIdx.x * blockDim.x + threadIdx.x; sg < BF;
        sg += gridDim.x * blockDim.x) {
     uint32_t a = offsets[sg], e = offsets[sg + 1];
@@ -134,7 +136,7 @@ __global__ void expand_groups_kernel(const uint32_t* __restrict__ offsets, uint3
 void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st,
                           uint8_t* kind) {
   if (!BF) return;
-  expand_groups_kernel<<<std::min<uint64_t>(ceil_div(BF, 256), 148 * 16), 256, 0, st>>>(
+  launch(expand_groups_kernel, std::min<uint64_t>(ceil_div(BF, 256), 148 * 16), 256, 0, st, 
       offsets, BF, lgrp, kind);
   HPS_LAUNCH_CHECK();
 }
@@ -146,6 +148,7 @@ __global__ void __launch_bounds__(256)
                  uint32_t* __restrict__ slots, uint32_t* __restrict__ sort_keys,
                  uint32_t* __restrict__ sort_vals, uint32_t* __restrict__ new_slots,
                  uint32_t* __restrict__ new_count, bool plan, const uint32_t* n_dev) {
+  pdl_entry();
   // n_dev: the live listing count is device-side (<= n); listings past it get no row.
   const uint64_t n_live = n_dev ? min(n, static_cast<uint64_t>(*n_dev)) : n;
   // kProbeILP listings per thread: their first probes are issued back to back (the
@@ -194,7 +197,7 @@ void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* 
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
                   uint32_t* new_count, bool plan, cudaStream_t st, const uint32_t* n_dev) {
   if (!n) return;
-  probe_kernel<<<ceil_div(n, 256 * 2), 256, 0, st>>>(t, ids, n, slots, sort_keys, sort_vals,
+  launch(probe_kernel, ceil_div(n, 256 * 2), 256, 0, st, t, ids, n, slots, sort_keys, sort_vals,
                                                      new_slots, new_count, plan, n_dev);
   HPS_LAUNCH_CHECK();
 }
@@ -204,6 +207,7 @@ __global__ void __launch_bounds__(256)
                          const XHdr* __restrict__ hdr, uint32_t* __restrict__ slots,
                          uint64_t* __restrict__ ids_copy, uint32_t* __restrict__ cnt_copy,
                          uint32_t* __restrict__ new_slots, uint32_t* __restrict__ new_count) {
+  pdl_entry();
   const uint32_t r = blockIdx.y;
   const uint64_t n = ld_volatile(&hdr->fwd_cnt[r]);
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt_copy[r] = static_cast<uint32_t>(n);
@@ -225,7 +229,7 @@ void launch_probe_regions(const DevTable& t, const uint64_t* ids, uint64_t strid
   if (!stride || !W) return;
   const uint32_t bx = static_cast<uint32_t>(
       std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(stride, 256), (uint64_t)sms * 8 / W + 1)));
-  probe_regions_kernel<<<dim3(bx, W), 256, 0, st>>>(t, ids, stride, hdr, slots, ids_copy,
+  launch(probe_regions_kernel, dim3(bx, W), 256, 0, st, t, ids, stride, hdr, slots, ids_copy,
                                                     cnt_copy, new_slots, new_count);
   HPS_LAUNCH_CHECK();
 }
@@ -240,6 +244,7 @@ void launch_ht_clear(const DevTable& t, cudaStream_t st) {
 // (embedding_ps.hpp:420) advances by the number of rows initialised.
 __global__ void lazy_init_kernel(DevTable t, const uint32_t* __restrict__ new_slots,
                                  const uint32_t* __restrict__ new_count) {
+  pdl_entry();
   const uint32_t cnt = *new_count;
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -265,7 +270,7 @@ void launch_lazy_init(const DevTable& t, const uint32_t* new_slots, const uint32
                       uint64_t max_new, int sms, cudaStream_t st) {
   if (!max_new) return;
   uint32_t blocks = std::min<uint64_t>(ceil_div(max_new, 8), (uint64_t)sms * 8);
-  lazy_init_kernel<<<blocks, 256, 0, st>>>(t, new_slots, new_count);
+  launch(lazy_init_kernel, blocks, 256, 0, st, t, new_slots, new_count);
   HPS_LAUNCH_CHECK();
 }
 
@@ -279,6 +284,7 @@ template <int V, int L, bool kGuard>
 __global__ void __launch_bounds__(256)
     gather_kernel(DevTable t, const uint32_t* __restrict__ slots, uint64_t n,
                   float* __restrict__ out, uint64_t* __restrict__ out_ver) {
+  pdl_entry();
   using G = Geo<V, L, kGuard>;
   const int ln = G::lane();
   const uint32_t D = t.D;
@@ -328,7 +334,7 @@ void launch_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* 
     const uint64_t per_block = (256 / L) * kGatherILP;
     const uint32_t blocks = static_cast<uint32_t>(
         std::min<uint64_t>(ceil_div(n, per_block), 148ull * 48));
-    gather_kernel<V, L, G><<<blocks, 256, 0, st>>>(t, slots, n, out, out_ver);
+    launch(gather_kernel<V, L, G>, blocks, 256, 0, st, t, slots, n, out, out_ver);
   });
   HPS_LAUNCH_CHECK();
 }
@@ -336,6 +342,7 @@ void launch_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* 
 __global__ void peek_kernel(DevTable t, const uint64_t* __restrict__ ids, uint64_t n,
                             float* __restrict__ out_w, float* __restrict__ out_acc,
                             uint64_t* __restrict__ out_ver, uint8_t* __restrict__ out_present) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
@@ -358,7 +365,7 @@ __global__ void peek_kernel(DevTable t, const uint64_t* __restrict__ ids, uint64
 void launch_peek(const DevTable& t, const uint64_t* ids, uint64_t n, float* out_w, float* out_acc,
                  uint64_t* out_ver, uint8_t* out_present, cudaStream_t st) {
   if (!n) return;
-  peek_kernel<<<std::min<uint64_t>(ceil_div(n, 8), 148 * 32), 256, 0, st>>>(
+  launch(peek_kernel, std::min<uint64_t>(ceil_div(n, 8), 148 * 32), 256, 0, st, 
       t, ids, n, out_w, out_acc, out_ver, out_present);
   HPS_LAUNCH_CHECK();
 }
@@ -367,6 +374,7 @@ void launch_peek(const DevTable& t, const uint64_t* ids, uint64_t n, float* out_
 
 __global__ void check_direct_kernel(const float* __restrict__ g, uint64_t n,
                                     unsigned long long* ctr) {
+  pdl_entry();
   bool bad = false;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -377,7 +385,7 @@ __global__ void check_direct_kernel(const float* __restrict__ g, uint64_t n,
 void launch_check_direct(const float* grads, uint64_t n, unsigned long long* ctr,
                          cudaStream_t st) {
   if (!n) return;
-  check_direct_kernel<<<std::min<uint64_t>(ceil_div(n, 256), 148 * 8), 256, 0, st>>>(grads, n,
+  launch(check_direct_kernel, std::min<uint64_t>(ceil_div(n, 256), 148 * 8), 256, 0, st, grads, n,
                                                                                       ctr);
   HPS_LAUNCH_CHECK();
 }
@@ -396,6 +404,7 @@ __global__ void __launch_bounds__(256, 6)
                        unsigned long long* ctr, float* __restrict__ cbuf,
                        const uint32_t* __restrict__ inv, const uint32_t* gate,
                        const uint32_t* rows_live) {
+  pdl_entry();
   if (rows_live) rows = min(rows, static_cast<uint64_t>(*rows_live));
   using G = Geo<V, L, kGuard>;
   constexpr int kCheckILP = 4;
@@ -480,7 +489,7 @@ void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B,
   HPS_DISPATCH_DIM(D, {
     uint64_t groups_per_block = 256 / L;
     uint32_t blocks = std::min<uint64_t>(ceil_div(rows, groups_per_block * 4), 148ull * 16);
-    check_batch_kernel<V, L, G><<<blocks, 256, 0, st>>>(grads, offsets, rows, D, F, mean, ctr,
+    launch(check_batch_kernel<V, L, G>, blocks, 256, 0, st, grads, offsets, rows, D, F, mean, ctr,
                                                         cbuf, inv, gate, rows_live);
   });
   HPS_LAUNCH_CHECK();
@@ -489,6 +498,7 @@ void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B,
 // ---- small helpers --------------------------------------------------------------------
 
 __global__ void iota_kernel(uint32_t* out, uint64_t n) {
+  pdl_entry();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
     out[i] = static_cast<uint32_t>(i);
@@ -496,12 +506,13 @@ __global__ void iota_kernel(uint32_t* out, uint64_t n) {
 
 void launch_iota(uint32_t* out, uint64_t n, cudaStream_t st) {
   if (!n) return;
-  iota_kernel<<<std::min<uint64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st>>>(out, n);
+  launch(iota_kernel, std::min<uint64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st, out, n);
   HPS_LAUNCH_CHECK();
 }
 
 __global__ void sample_order_kernel(const uint64_t* __restrict__ sk, uint32_t B,
                                     uint64_t* __restrict__ keys, uint32_t* __restrict__ perm) {
+  pdl_entry();
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
     keys[b] = sk[b];
     perm[b] = b;
@@ -511,13 +522,14 @@ __global__ void sample_order_kernel(const uint64_t* __restrict__ sk, uint32_t B,
 void launch_sample_order(const uint64_t* sk, uint32_t B, uint64_t* keys, uint32_t* perm,
                          cudaStream_t st) {
   if (!B) return;
-  sample_order_kernel<<<ceil_div(B, 256), 256, 0, st>>>(sk, B, keys, perm);
+  launch(sample_order_kernel, ceil_div(B, 256), 256, 0, st, sk, B, keys, perm);
   HPS_LAUNCH_CHECK();
 }
 
 __global__ void sample_lengths_kernel(const uint32_t* __restrict__ perm,
                                       const uint32_t* __restrict__ off, uint32_t B, uint32_t F,
                                       uint32_t* __restrict__ lens) {
+  pdl_entry();
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < B; r += gridDim.x * blockDim.x) {
     uint64_t b = perm[r];
     lens[r] = off[(b + 1) * F] - off[b * F];
@@ -527,12 +539,12 @@ __global__ void sample_lengths_kernel(const uint32_t* __restrict__ perm,
 void launch_sample_lengths(const uint32_t* perm, const uint32_t* off, uint32_t B, uint32_t F,
                            uint32_t* lens, cudaStream_t st) {
   if (!B) return;
-  sample_lengths_kernel<<<ceil_div(B, 256), 256, 0, st>>>(perm, off, B, F, lens);
+  launch(sample_lengths_kernel, ceil_div(B, 256), 256, 0, st, perm, off, B, F, lens);
   HPS_LAUNCH_CHECK();
 }
 
 void launch_scan_inplace(uint32_t* data, uint32_t n, uint32_t* total, cudaStream_t st) {
-  radix::scan_digits<<<1, 1024, 0, st>>>(data, n, total);
+  launch(radix::scan_digits, 1, 1024, 0, st, data, n, total);
   HPS_LAUNCH_CHECK();
 }
 
@@ -542,6 +554,7 @@ __global__ void permuted_listing_kernel(const uint32_t* __restrict__ perm,
                                         const uint32_t* __restrict__ slots, uint32_t B,
                                         uint32_t F, uint32_t* __restrict__ keys,
                                         uint32_t* __restrict__ vals) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < B; r += warps) {
@@ -558,28 +571,30 @@ void launch_permuted_listing(const uint32_t* perm, const uint32_t* starts, const
                              const uint32_t* slots, uint32_t B, uint32_t F, uint32_t* keys,
                              uint32_t* vals, cudaStream_t st) {
   if (!B) return;
-  permuted_listing_kernel<<<std::min<uint64_t>(ceil_div(B, 8), 148 * 16), 256, 0, st>>>(
+  launch(permuted_listing_kernel, std::min<uint64_t>(ceil_div(B, 8), 148 * 16), 256, 0, st, 
       perm, starts, off, slots, B, F, keys, vals);
   HPS_LAUNCH_CHECK();
 }
 
 __global__ void add_counter_kernel(unsigned long long* ctr, int idx, const uint32_t* src) {
+  pdl_entry();
   atomicAdd(&ctr[idx], (unsigned long long)*src);
 }
 
 void launch_add_counter_from(unsigned long long* ctr, int idx, const uint32_t* src,
                              cudaStream_t st) {
-  add_counter_kernel<<<1, 1, 0, st>>>(ctr, idx, src);
+  launch(add_counter_kernel, 1, 1, 0, st, ctr, idx, src);
   HPS_LAUNCH_CHECK();
 }
 
 __global__ void add_counter_const_kernel(unsigned long long* ctr, int idx, unsigned long long v) {
+  pdl_entry();
   atomicAdd(&ctr[idx], v);
 }
 
 void launch_add_counter_const(unsigned long long* ctr, int idx, unsigned long long v,
                               cudaStream_t st) {
-  add_counter_const_kernel<<<1, 1, 0, st>>>(ctr, idx, v);
+  launch(add_counter_const_kernel, 1, 1, 0, st, ctr, idx, v);
   HPS_LAUNCH_CHECK();
 }
 

@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(kPlanBlock)
     classify_kernel(DevTable t, const uint32_t* __restrict__ slots, uint64_t n, int lbits,
                     uint8_t* __restrict__ kind, unsigned long long* __restrict__ mkeys,
                     uint32_t* __restrict__ n_multi, const uint32_t* n_live) {
+  pdl_entry();
   if (n_live) n = min(n, static_cast<uint64_t>(*n_live));
   __shared__ uint32_t s_warp[kPlanBlock / 32];
   __shared__ uint32_t s_base;
@@ -103,7 +104,7 @@ void launch_classify(const DevTable& t, const uint32_t* slots, uint64_t n, int l
   if (!n) return;
   const uint32_t blocks =
       std::min<uint64_t>(ceil_div(n, kPlanBlock * kPlanItems), static_cast<uint64_t>(sms) * 8);
-  classify_kernel<<<blocks, kPlanBlock, 0, st>>>(t, slots, n, lbits, kind, mkeys, n_multi,
+  launch(classify_kernel, blocks, kPlanBlock, 0, st, t, slots, n, lbits, kind, mkeys, n_multi,
                                                   n_live);
   HPS_LAUNCH_CHECK();
 }

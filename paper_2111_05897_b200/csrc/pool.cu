@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(256, 8)
                 const uint32_t* __restrict__ slots, uint32_t BF, uint64_t N, int mean,
                 float* __restrict__ out, uint64_t* __restrict__ out_rv64,
                 uint32_t* __restrict__ out_rv32, const uint8_t* __restrict__ skip) {
+  pdl_entry();
   using G = Geo<V, L, kGuard>;
   const int ln = G::lane();
   const uint32_t D = t.D;
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(256, 8)
 // the table before this batch's own push (copy-on-write, table.cu protect_reads).
 __global__ void snapshot_rv_kernel(DevTable t, const uint32_t* __restrict__ slots, uint64_t n,
                                    uint32_t* __restrict__ rv) {
+  pdl_entry();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t s = slots[i];
@@ -180,7 +182,7 @@ __global__ void snapshot_rv_kernel(DevTable t, const uint32_t* __restrict__ slot
 void launch_snapshot_rv(const DevTable& t, const uint32_t* slots, uint64_t n, uint32_t* rv,
                         cudaStream_t st) {
   if (!n) return;
-  snapshot_rv_kernel<<<std::min<uint64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st>>>(t, slots,
+  launch(snapshot_rv_kernel, std::min<uint64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st, t, slots,
                                                                                      n, rv);
   HPS_LAUNCH_CHECK();
 }
@@ -193,7 +195,7 @@ void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slo
     uint64_t groups_per_block = 256 / L;
     uint32_t blocks =
         std::min<uint64_t>(ceil_div(BF, groups_per_block * kPoolILP), 1u << 30);
-    pool_kernel<V, L, G><<<blocks, 256, 0, st>>>(t, offsets, slots, BF, N, mean, out, out_rv64,
+    launch(pool_kernel<V, L, G>, blocks, 256, 0, st, t, offsets, slots, BF, N, mean, out, out_rv64,
                                                  out_rv32, skip);
   });
   HPS_LAUNCH_CHECK();

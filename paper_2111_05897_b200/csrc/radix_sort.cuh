@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(kSmallBlock)
     small_sort_kernel(const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                       K* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t n,
                       int passes) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem[];
   K* sk = reinterpret_cast<K*>(smem);
   uint32_t* sv = reinterpret_cast<uint32_t*>(sk + 2 * kSmallN);
@@ -198,6 +199,7 @@ static __global__ void __launch_bounds__(kRankBlock)
     small_composite_kernel(const unsigned long long* __restrict__ keys, const uint32_t* n_dev,
                            int lbits, uint32_t* __restrict__ out_slot,
                            uint32_t* __restrict__ out_listing) {
+  pdl_entry();
   const uint32_t n = *n_dev;
   if (n > kSmallN) return;  // the large path (gated on the same count) takes it
   const int lane = threadIdx.x & 31;
@@ -220,6 +222,7 @@ template <typename K>
 __global__ void __launch_bounds__(kBlock)
     hist_kernel(const K* __restrict__ keys, uint32_t n, int passes, uint32_t* __restrict__ hist,
                 const uint32_t* gate) {
+  pdl_entry();
   if (!gate_open(gate)) return;
   __shared__ uint32_t cnt[kMaxPasses * kBins];
   for (int i = threadIdx.x; i < passes * kBins; i += kBlock) cnt[i] = 0;
@@ -250,6 +253,7 @@ __global__ void __launch_bounds__(kBlock)
                 K* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t n, int shift,
                 const uint32_t* __restrict__ hist, unsigned long long* status, uint32_t* tile_ctr,
                 uint32_t epoch, const uint32_t* gate, const SortMeta meta) {
+  pdl_entry();
   constexpr int kItems = Tile<K>::kItems;
   constexpr int kTileN = Tile<K>::kTile;
   if (!gate_open(gate)) return;
@@ -394,7 +398,7 @@ inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b,
   const uint32_t* first_vals = iota_vals ? nullptr : vals_a;
   if (!gate && n <= kSmallN) {
     if (n == 0) return false;
-    small_sort_kernel<K><<<1, kSmallBlock, small_smem<K>(), stream>>>(
+    launch(small_sort_kernel<K>, 1, kSmallBlock, small_smem<K>(), stream, 
         first, first_vals, keys_b, vals_b, static_cast<uint32_t>(n), passes);
     HPS_LAUNCH_CHECK();
     return true;
@@ -409,7 +413,7 @@ inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b,
                              (kMaxPasses * kBins + kMaxPasses * 2) * sizeof(uint32_t), stream));
   const uint32_t n32 = static_cast<uint32_t>(n);
   const uint32_t hblocks = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms) * 4);
-  hist_kernel<K><<<hblocks, kBlock, 0, stream>>>(first, n32, passes, hist, gate);
+  launch(hist_kernel<K>, hblocks, kBlock, 0, stream, first, n32, passes, hist, gate);
   bool in_b = false;
   for (int p = 0; p < passes; ++p) {
     const K* ki = p == 0 ? first : (in_b ? keys_b : keys_a);
@@ -417,7 +421,7 @@ inline bool sort_pairs(K* keys_a, uint32_t* vals_a, K* keys_b, uint32_t* vals_b,
     K* ko = in_b ? keys_a : keys_b;
     uint32_t* vo = in_b ? vals_a : vals_b;
     const uint32_t epoch = g_epoch.fetch_add(1) + 1;
-    pass_kernel<K><<<tiles, kBlock, Tile<K>::kSmem, stream>>>(
+    launch(pass_kernel<K>, tiles, kBlock, Tile<K>::kSmem, stream, 
         ki, vi, ko, vo, n32, p * kBits, hist + p * kBins, status, tile_ctr + p, epoch, gate,
         p == passes - 1 ? meta : SortMeta{});
     in_b = !in_b;
@@ -437,7 +441,7 @@ inline void sort_scratch_zero(uint32_t* scratch, cudaStream_t stream) {
 inline void sort_composite_small(const unsigned long long* keys, const uint32_t* n_dev, int lbits,
                                  uint32_t* out_slot, uint32_t* out_listing,
                                  cudaStream_t stream) {
-  small_composite_kernel<<<kSmallN * 32 / kRankBlock, kRankBlock, 0, stream>>>(
+  launch(small_composite_kernel, kSmallN * 32 / kRankBlock, kRankBlock, 0, stream, 
       keys, n_dev, lbits, out_slot, out_listing);
   HPS_LAUNCH_CHECK();
 }
@@ -447,6 +451,7 @@ inline void sort_composite_small(const unsigned long long* keys, const uint32_t*
 static __global__ void __launch_bounds__(1024) scan_digits(uint32_t* __restrict__ hist,
                                                            uint32_t tiles,
                                                            uint32_t* __restrict__ totals) {
+  pdl_entry();
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t carry;
   uint32_t* row = hist + static_cast<uint64_t>(blockIdx.x) * tiles;

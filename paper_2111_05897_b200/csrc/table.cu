@@ -17,6 +17,14 @@
 
 namespace hps {
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HPS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // ---- pointer staging --------------------------------------------------------------------
 
 PtrKind ptr_kind(const void* p) {
