@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -38,7 +39,9 @@ def parse():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
+    p.add_argument("--staleness", type=int, default=None,
+                   help="c5: embedding staleness (default 4 on one GPU; 0 when sharded)")
     p.add_argument("--batches", type=int, default=8, help="distinct batches cycled")
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -193,6 +196,163 @@ def workload_config(cfg, args, ref_sample=None):
     if ref_sample:
         d["reference_sample_batch"] = ref_sample
     return d
+
+
+# ---------------------------------------------------------------- C5: the hybrid step
+
+
+def run_hybrid(args, world, rank, local, dev):
+    """C5: embedding lookup + dense tower (1677 -> 64 -> 32 -> 1, fp32 cuBLAS) + the
+    reference's canonical dense all-reduce + embedding update (HybridTrainer). One GPU:
+    local table, bounded staleness (default 4: the embedding stream runs up to 4 steps
+    ahead of the dense stream). N GPUs: the hash-sharded table (one batch in flight, so
+    staleness 0) and the dense gradient all-reduced every step."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2111_05897_b200 import hps
+    from paper_2111_05897_b200 import workloads as W
+    from paper_2111_05897_b200.hybrid import HybridTrainer
+    from paper_2111_05897_b200.sharded import ShardedEmbeddingWorker
+
+    if world > 1:
+        cfg = W.sharded_config(world)
+        tau = 0 if args.staleness is None else args.staleness
+    else:
+        cfg = W.CONFIGS["c5"]
+        tau = W.C5_STALENESS if args.staleness is None else args.staleness
+    D, F, B, S = cfg.dim, cfg.features, cfg.batch, cfg.shards
+    rows = cfg.table_capacity()
+    cap = int(rows / world * 1.01) + (1 << 20) if world > 1 else rows
+    table = hps.ShardSet(S, D, cap, hps.ADAGRAD, salts=cfg.salts(), device=local)
+    stream = torch.cuda.current_stream()
+    t0 = time.perf_counter()
+    chunk = 1 << 23
+    for a in range(0, rows, chunk):
+        n = min(chunk, rows - a)
+        ids = torch.arange(a, a + n, dtype=torch.int64, device=dev)
+        if world > 1:
+            ids = ids[(hps.route(ids, S, stream=stream).to(torch.int64) % world) == rank]
+        table.lookup(ids, stream=stream)
+    torch.cuda.synchronize()
+    prewarm_s = time.perf_counter() - t0
+    M = args.batches
+    data = []
+    for m in range(M):
+        hb = W.make_batch(cfg, 1000 * rank + m)
+        x, y = W.make_dense_inputs(cfg, hb)
+        data.append(tuple(torch.from_numpy(a).to(dev) for a in
+                          (hb.ids.view(np.int64), hb.offsets.view(np.int32), x, y)))
+    sharded = None
+    if world > 1:
+        sharded = ShardedEmbeddingWorker(table, hps.MEAN, transport=args.transport,
+                                         max_ids=max(int(d[0].numel()) for d in data))
+    use_graph = not args.no_graph
+    tr = HybridTrainer(table, F, W.C5_NON_ID, hidden=W.C5_HIDDEN, dense_lr=cfg.lr,
+                       embedding_lr=cfg.lr, staleness=tau, sharded_worker=sharded,
+                       device_step=use_graph)
+    torch.backends.cuda.matmul.allow_tf32 = False  # fp32 dense tower, as the reference
+    it = 0
+    for _ in range(args.warmup):
+        tr.step(*data[it % M])
+        it += 1
+    tr.sync()
+    torch.cuda.synchronize()
+    table.sync()
+    # One CUDA graph per step of the cycle (lcm of the batch count and tau + 1: the step
+    # index picks the batch and the in-flight slot): register + pull(s) and push(s-tau) on
+    # the embedding stream, the dense step on the dense stream, forked and joined inside
+    # the graph -- so push(s-tau) overlaps dense(s) without host launch overhead.
+    graphs, losses_g, graph_launches = [], [], []
+    if use_graph:
+        cyc = M * (tau + 1) // math.gcd(M, tau + 1)
+        cs = torch.cuda.Stream()
+        with torch.cuda.stream(cs):
+            for j in range(cyc):
+                g = torch.cuda.CUDAGraph()
+                l0 = hps.launch_count()
+                with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+                    losses_g.append(tr.step(*data[(it + j) % M]))
+                    tr.sync()
+                graph_launches.append(hps.launch_count() - l0)
+                graphs.append(g)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def run_step(i):
+        if graphs:
+            graphs[(i - it0) % len(graphs)].replay()
+            return losses_g[(i - it0) % len(graphs)]
+        return tr.step(*data[i % M])
+
+    it0 = it
+    for _ in range(len(graphs) or 2):
+        run_step(it)
+        it += 1
+    tr.sync()
+    torch.cuda.synchronize()
+    table.sync()
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = hps.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    losses = []
+    for _ in range(args.steps):
+        v = run_step(it)
+        losses.append(v.clone() if graphs else v)
+        it += 1
+    tr.sync()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = hps.launch_count() - l0
+    if graphs:  # replays do not pass through the host launch counter
+        launches = sum(graph_launches[(i - it0) % len(graphs)] for i in range(it - args.steps, it))
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if not graphs:
+        tr.flush()
+    torch.cuda.synchronize()
+    table.sync()
+    loss_vals = [float(v) for v in losses]
+    value = world * B * 1000.0 / ms
+    if rank == 0:
+        params = tr.tower.param_count
+        line = {
+            "metric": "hybrid training samples/sec (embedding lookup+update + dense tower)",
+            "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 pooling/fan-out)",
+            "data": "synthetic (teacher labels)",
+            "config": {"workload": f"c5: batch {B}/GPU, {F} one-hot features, "
+                                   f"{rows // 1_000_000}M-row table dim {D}, adagrad, mean "
+                                   f"pooling, staleness {tau}, dense 1677-64-32-1 fp32 SGD, "
+                                   f"canonical all-reduce",
+                       "global_batch": B * world, "dense_params": params,
+                       "parallelism": f"dp{world} + hash-sharded embeddings" if world > 1
+                       else "single", "staleness": tau},
+            "loss_first_last": [loss_vals[0], loss_vals[-1]],
+            "gpu_launches": launches, "clocks": clk, "prewarm_s": prewarm_s,
+            "cpu_baseline": None, "e2e": None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        # the graphs hold NCCL work: release them, then leave without tearing the
+        # communicator down under them
+        graphs.clear()
+        torch.cuda.synchronize()
+        dist.barrier()
+        sys.stdout.flush()
+        os._exit(0)
 
 
 # ---------------------------------------------------------------- our arm, N > 1 (sharded)
@@ -427,6 +587,10 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    if args.config == "c5":
+        run_hybrid(args, world, rank, local, dev)
+        return
+    if world > 1:
         run_sharded(args, world, rank, local, dev)
         return
     cfg = W.CONFIGS[args.config]

@@ -125,6 +125,15 @@ def reference_lib():
         lib.ref_compress_indices.restype = C.c_int
         lib.ref_compress_indices.argtypes = [C.c_uint32, C.c_uint32, u64p, u64p, u64p, u64p, u64p,
                                              u16p]
+        lib.ref_dense_init.restype = C.c_int64
+        lib.ref_dense_init.argtypes = [u64p, C.c_uint32, C.c_uint64, f32p, C.c_uint64]
+        lib.ref_dense_fwd_bwd.restype = C.c_int
+        lib.ref_dense_fwd_bwd.argtypes = [u64p, C.c_uint32, f32p, C.c_uint32, f32p, f32p, f32p,
+                                          f32p, f32p, f32p]
+        lib.ref_allreduce.restype = C.c_int
+        lib.ref_allreduce.argtypes = [C.c_uint32, C.c_uint64, f32p, f32p]
+        lib.ref_sgd_step.restype = C.c_int
+        lib.ref_sgd_step.argtypes = [f32p, f32p, C.c_uint64, C.c_float]
         lib._typed = True
     return lib
 
@@ -401,3 +410,55 @@ def parse_hps1(buf: bytes) -> dict:
     for s in live_slots:
         res[int(ids[s])] = (rows[s, :dim].copy(), rows[s, dim:].copy(), int(vers[s]))
     return dict(dim=dim, capacity=cap, salt=salt, epoch=epoch, rows=res)
+
+
+# ---- dense tower (the reference's DenseNet / AllReduceHub, C5) ---------------------------
+
+
+def _ref_rc(rc, what):
+    if rc:
+        raise OracleError(rc, f"{what}: {reference_lib().ref_last_error().decode()}")
+
+
+def ref_dense_init(dims, init_seed: int) -> np.ndarray:
+    """DenseNet(dims, Rng(mix64(init_seed))) params (nn_worker.hpp:331-336)."""
+    lib = reference_lib()
+    d = _u64(np.asarray(dims))
+    n = lib.ref_dense_init(_p(d, u64p), len(d), init_seed, None, 0)
+    _ref_rc(0 if n >= 0 else -n, "dense_init")
+    out = np.zeros(n, np.float32)
+    lib.ref_dense_init(_p(d, u64p), len(d), init_seed, _p(out, f32p), n)
+    return out
+
+
+def ref_dense_fwd_bwd(dims, params, inputs, labels):
+    """batch_forward_backward (dense_nn.hpp:218-246) -> (loss, probs, dense_grad, input_grads)."""
+    lib = reference_lib()
+    d = _u64(np.asarray(dims))
+    params, inputs, labels = _f32(params), _f32(inputs), _f32(labels)
+    B = len(labels)
+    loss = C.c_float(0)
+    probs = np.zeros(B, np.float32)
+    dg = np.zeros(len(params), np.float32)
+    ig = np.zeros((B, int(dims[0])), np.float32)
+    _ref_rc(lib.ref_dense_fwd_bwd(_p(d, u64p), len(d), _p(params, f32p), B, _p(inputs, f32p),
+                                  _p(labels, f32p), C.byref(loss), _p(probs, f32p), _p(dg, f32p),
+                                  _p(ig, f32p)), "dense_fwd_bwd")
+    return loss.value, probs, dg, ig
+
+
+def ref_allreduce(parts) -> np.ndarray:
+    """AllReduceHub canonical mean (nn_worker.hpp:214-226) of parts[K, n]."""
+    parts = _f32(parts)
+    K, n = parts.shape
+    out = np.zeros(n, np.float32)
+    _ref_rc(reference_lib().ref_allreduce(K, n, _p(parts, f32p), _p(out, f32p)), "allreduce")
+    return out
+
+
+def ref_sgd_step(params, grad, lr: float) -> np.ndarray:
+    """sgd_step (dense_nn.hpp:263-273) on a copy of params."""
+    p = _f32(params).copy()
+    g = _f32(grad)
+    _ref_rc(reference_lib().ref_sgd_step(_p(p, f32p), _p(g, f32p), len(p), lr), "sgd_step")
+    return p

@@ -26,9 +26,11 @@
 
 #include "hybridps/codec.hpp"
 #include "hybridps/core.hpp"
+#include "hybridps/dense_nn.hpp"
 #include "hybridps/embedding_ps.hpp"
 #include "hybridps/embedding_worker.hpp"
 #include "hybridps/errors.hpp"
+#include "hybridps/nn_worker.hpp"
 #include "hybridps/transport.hpp"
 
 using namespace hybridps;
@@ -292,4 +294,73 @@ int ref_compress_indices(uint32_t B, uint32_t G, const uint64_t* ids, const uint
   });
 }
 
+// ---- dense tower (the C5 hybrid step) ----------------------------
+
+// DenseNet(dims, Rng(mix64(init_seed))) as NnWorker builds it (nn_worker.hpp:331-336,
+// dense_nn.hpp:42-66); dims = input + hidden widths (the output unit is appended).
+// Returns the parameter count; copies the params when cap is large enough.
+int64_t ref_dense_init(const uint64_t* dims, uint32_t ndims, uint64_t init_seed, float* out,
+                       uint64_t cap) {
+  int64_t n = -1;
+  int rc = guarded([&] {
+    std::vector<size_t> d(dims, dims + ndims);
+    Rng rng(mix64(init_seed));
+    DenseNet<float> net(d, rng);
+    n = static_cast<int64_t>(net.param_count());
+    if (out && cap >= net.param_count())
+      std::memcpy(out, net.params().data(), net.param_count() * sizeof(float));
+  });
+  return rc ? -rc : n;
+}
+
+// batch_forward_backward (dense_nn.hpp:218-246) of a net holding `params`: mean BCE
+// loss, probabilities, mean-loss dense gradient, per-sample input gradients.
+int ref_dense_fwd_bwd(const uint64_t* dims, uint32_t ndims, const float* params, uint32_t B,
+                      const float* inputs, const float* labels, float* out_loss,
+                      float* out_probs, float* out_dense_grad, float* out_input_grads) {
+  return guarded([&] {
+    std::vector<size_t> d(dims, dims + ndims);
+    Rng rng(0);
+    DenseNet<float> net(d, rng);
+    std::memcpy(net.params().data(), params, net.param_count() * sizeof(float));
+    const size_t in = d.front();
+    std::vector<std::vector<float>> x(B);
+    std::vector<float> y(labels, labels + B);
+    for (uint32_t i = 0; i < B; ++i) x[i].assign(inputs + i * in, inputs + (i + 1) * in);
+    BatchResult<float> r = batch_forward_backward(net, x, y);
+    *out_loss = r.mean_loss;
+    std::memcpy(out_probs, r.probs.data(), B * sizeof(float));
+    std::memcpy(out_dense_grad, r.dense_grad.data(), r.dense_grad.size() * sizeof(float));
+    for (uint32_t i = 0; i < B; ++i)
+      std::memcpy(out_input_grads + i * in, r.input_grads[i].data(), in * sizeof(float));
+  });
+}
+
+// AllReduceHub::reduce (nn_worker.hpp:85-87, canonical_mean :214-226): K ranks on K
+// threads contribute parts[k*n .. (k+1)*n); out = the canonical mean every rank receives.
+int ref_allreduce(uint32_t K, uint64_t n, const float* parts, float* out) {
+  return guarded([&] {
+    AllReduceHub hub(K);
+    std::vector<std::vector<float>> res(K);
+    std::vector<std::thread> th;
+    for (uint32_t k = 0; k < K; ++k)
+      th.emplace_back([&, k] {
+        std::vector<float> g(parts + k * n, parts + (k + 1) * n);
+        res[k] = hub.reduce(k, 0, g);
+      });
+    for (auto& t : th) t.join();
+    std::memcpy(out, res[0].data(), n * sizeof(float));
+  });
+}
+
+// sgd_step (dense_nn.hpp:263-273): params -= lr * grad, refusing non-finite gradients.
+int ref_sgd_step(float* params, const float* grad, uint64_t n, float lr) {
+  return guarded([&] {
+    std::vector<float> p(params, params + n), g(grad, grad + n);
+    sgd_step(p, g, lr);
+    std::memcpy(params, p.data(), n * sizeof(float));
+  });
+}
+
 }  // extern "C"
+

@@ -88,7 +88,15 @@ CONFIGS = {
     "c2": Config("c2", 16384, 26, 100_000_000, 64, "adagrad", "mean"),
     "c3": Config("c3", 16384, 26, 100_000_000, 64, "adagrad", "mean", multi_hot=50.0, zipf=1.1),
     "c4": Config("c4", 16384, 26, 1_000_000_000, 64, "adagrad", "mean"),
+    # C5: the C2/C4 embedding shape + the dense tower (hybrid step); 13 Criteo dense
+    # features; the reference NN worker's default hidden widths {64, 32}
+    # (orchestrator.hpp:94) -> a 3-layer MLP (1677 -> 64 -> 32 -> 1).
+    "c5": Config("c5", 16384, 26, 100_000_000, 64, "adagrad", "mean"),
 }
+
+C5_NON_ID = 13
+C5_HIDDEN = (64, 32)
+C5_STALENESS = 4
 
 
 def sharded_config(world: int) -> Config:
@@ -237,3 +245,27 @@ def random_csr(rng: np.random.Generator, B: int, F: int, max_per_group: int, id_
     np.cumsum(counts, out=offsets[1:])
     flat = np.concatenate(ids) if ids else np.zeros(0, np.uint64)
     return flat.astype(np.uint64), offsets
+
+
+def make_dense_inputs(cfg: Config, batch: Batch, non_id_dim: int = C5_NON_ID,
+                      teacher_scale: float = 8.0):
+    """Non-id features U(-1, 1) and teacher labels for a batch (the reference's synthetic
+    CTR stream, data.hpp:105-186, in spirit: a fixed per-id latent and a fixed linear map,
+    label ~ Bernoulli(sigmoid(logit))). Returns (non_id [B, nd] f32, labels [B] f32)."""
+    B, F = batch.B, batch.F
+    step = batch.meta.get("step", 0)
+    non_id = (-1.0 + 2.0 * uniform01(cfg.seed ^ 0xD5, B * non_id_dim, step * B * non_id_dim))
+    non_id = non_id.reshape(B, non_id_dim)
+    # per-id latent in [-1, 1), mean over each group's listings, summed over groups
+    lat = (mix64(batch.ids ^ np.uint64(0x7465616368657200)) >> np.uint64(11)).astype(
+        np.float64) * 2.0**-53 * 2.0 - 1.0
+    offs = batch.offsets.astype(np.int64)
+    sums = np.add.reduceat(lat, np.minimum(offs[:-1], len(lat) - 1)) if len(lat) else \
+        np.zeros(B * F)
+    cnt = np.diff(offs)
+    sums = np.where(cnt > 0, sums / np.maximum(cnt, 1), 0.0).reshape(B, F)
+    wf = -1.0 + 2.0 * uniform01(cfg.seed ^ 0x7E, F + non_id_dim)
+    logit = teacher_scale / np.sqrt(F + non_id_dim) * (sums @ wf[:F] + non_id @ wf[F:])
+    u = uniform01(cfg.seed ^ 0x1AB, B, step * B)
+    labels = (u < 1.0 / (1.0 + np.exp(-logit))).astype(np.float32)
+    return non_id.astype(np.float32), labels
