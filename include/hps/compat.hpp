@@ -223,7 +223,27 @@ class Table {
 class PsShard : public Table {
  public:
   explicit PsShard(const PsShardConfig& cfg)
-      : Table({cfg.rng_salt}, cfg.capacity, cfg.embedding_dim, cfg.optimizer, cfg.device) {}
+      : Table({cfg.rng_salt}, cfg.capacity, cfg.embedding_dim, cfg.optimizer, cfg.device),
+        capacity_(cfg.capacity) {}
+
+  // PsShard::save_checkpoint (embedding_ps.hpp:222-260): the HPS1 image, its size.
+  size_t save_checkpoint(std::vector<uint8_t>& out) const {
+    uint64_t n = 0;
+    check(hps_table_checkpoint_save(handle(), 0, capacity_, nullptr, 0, &n));
+    out.assign(n, 0);
+    check(hps_table_checkpoint_save(handle(), 0, capacity_, out.data(), n, &n));
+    return n;
+  }
+  // recover_from_checkpoint (:280-292): state reverts to the image, the epoch advances
+  // past the live one (CheckpointCorruptError on a bad image; nothing changes then).
+  void recover_from_checkpoint(const std::vector<uint8_t>& buf) {
+    const void* p = buf.data();
+    const uint64_t n = buf.size();
+    check(hps_table_checkpoint_load(handle(), &p, &n, 1, 1));
+  }
+
+ private:
+  uint32_t capacity_;
 };
 
 // ShardSet(shard_count, base) (embedding_ps.hpp:506-516): shard i salt = mix64(base + i),

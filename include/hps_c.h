@@ -114,6 +114,28 @@ hps_status hps_table_device_step(hps_table* t, uint32_t* out_step); /* HPS_DEVIC
 uint32_t hps_table_advance_epoch(hps_table* t);          /* PsShard::advance_epoch :204 */
 hps_status hps_table_reset(hps_table* t);                /* PsShard::reset_for_recovery :193 */
 
+/* ---- checkpoints (PsShard::save_checkpoint / load_checkpoint / recover_from_checkpoint,
+ * embedding_ps.hpp:209-402): HPS1 images, one per logical shard ------------------------- */
+/* The HPS1 image of logical shard `shard`: the reference's 64-byte header (magic, format
+ * 1, optimizer, dim, capacity, salt, hwm, recency head/tail, free head, live count, epoch,
+ * evictions, FNV-1a checksum) and flat arrays ids, prev, next, versions, rows [w|acc].
+ * Rows are listed in slot (first insertion) order; the recency chain runs from the newest
+ * slot (head) to the oldest (tail). shard_capacity goes into the header (0 = the table's
+ * capacity). *out_bytes = image size; the image is written when buf != NULL and
+ * cap >= *out_bytes. Synchronises the device. */
+hps_status hps_table_checkpoint_save(hps_table* t, uint32_t shard, uint32_t shard_capacity,
+                                     void* buf, uint64_t cap, uint64_t* out_bytes);
+/* Adopt `count` HPS1 images (host buffers) as the table's whole content: every image is
+ * validated first like PsShard::parse + LruStore::restore (magic, format, checksum,
+ * optimizer and dim vs the table, length, recency chain and free list) and matched to a
+ * shard by its salt -- any failure returns HPS_E_CHECKPOINT_CORRUPT / HPS_E_CONFIG and
+ * changes nothing. Then the table is cleared and the images' live rows (weights,
+ * accumulators, versions; latest-bump tags reset, adopt_locked :390-402) inserted.
+ * recover = 0: load_checkpoint (epoch = the images' epoch); 1: recover_from_checkpoint
+ * (epoch = max(live, image) + 1, so in-flight pushes of the old epoch are dropped). */
+hps_status hps_table_checkpoint_load(hps_table* t, const void* const* images,
+                                     const uint64_t* sizes, uint32_t count, int recover);
+
 /* ---- parameter-server surface --------------------------------------------------------- */
 /* PsShard::lookup (embedding_ps.hpp:105-114) / ShardSet::lookup (:531-541): duplicates
  * allowed, misses lazily initialised (find_or_init :417-434). out_values[n*D];

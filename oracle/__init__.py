@@ -125,6 +125,8 @@ def reference_lib():
         lib.ref_compress_indices.restype = C.c_int
         lib.ref_compress_indices.argtypes = [C.c_uint32, C.c_uint32, u64p, u64p, u64p, u64p, u64p,
                                              u16p]
+        lib.ref_shard_import.restype = C.c_int
+        lib.ref_shard_import.argtypes = [C.c_void_p, C.c_uint32, u8p, C.c_uint64, C.c_int]
         lib.ref_dense_init.restype = C.c_int64
         lib.ref_dense_init.argtypes = [u64p, C.c_uint32, C.c_uint64, f32p, C.c_uint64]
         lib.ref_dense_fwd_bwd.restype = C.c_int
@@ -375,6 +377,13 @@ class Reference:
         buf = np.zeros(n, np.uint8)
         self.lib.ref_shard_export(self.h, s, _p(buf, u8p), n)
         return buf.tobytes()
+
+    def shard_import(self, s, image: bytes, validate_only: bool = False):
+        """recover_from_checkpoint (embedding_ps.hpp:280-292) of shard s from an HPS1 image
+        (validate_only: PsShard::load_checkpoint into a discarded shard)."""
+        buf = np.frombuffer(image, np.uint8).copy()
+        self._check(self.lib.ref_shard_import(self.h, s, _p(buf, u8p), len(buf),
+                                              int(validate_only)), "shard_import")
 
     def state(self):
         """{id: (w[D], acc[D], version)} over every shard, from HPS1 images."""

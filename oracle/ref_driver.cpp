@@ -263,6 +263,18 @@ int64_t ref_shard_export(void* h, uint32_t s, uint8_t* buf, uint64_t cap) {
   return static_cast<int64_t>(out.size());
 }
 
+// PsShard::recover_from_checkpoint (embedding_ps.hpp:280-292) of shard s from an HPS1
+// image; validate_only != 0: PsShard::load_checkpoint (:262-268) into a fresh shard that
+// is discarded (the parse/restore validation alone).
+int ref_shard_import(void* h, uint32_t s, const uint8_t* buf, uint64_t n, int validate_only) {
+  RefTable* t = static_cast<RefTable*>(h);
+  return guarded([&] {
+    std::vector<uint8_t> img(buf, buf + n);
+    if (validate_only) (void)PsShard::load_checkpoint(img);
+    else t->shards.at(s)->recover_from_checkpoint(img);
+  });
+}
+
 // compress_indices (codec.hpp:123-156) over a CSR batch. Outputs, all caller-sized
 // for the worst case (N listings): group_u_off[G+1], unique[<=N], post_off[<=N+1]
 // (relative to the flat postings array), postings[<=N] (u16 sample indices).

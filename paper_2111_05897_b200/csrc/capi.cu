@@ -136,6 +136,26 @@ hps_status hps_table_reset(hps_table* t) {
   });
 }
 
+hps_status hps_table_checkpoint_save(hps_table* t, uint32_t shard, uint32_t shard_capacity,
+                                     void* buf, uint64_t cap, uint64_t* out_bytes) {
+  return guarded([&] {
+    REQUIRE(t && out_bytes, "hps_table_checkpoint_save: null argument");
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    *out_bytes = hps::table_ckpt_save(t->impl, shard, shard_capacity,
+                                      static_cast<uint8_t*>(buf), cap);
+  });
+}
+
+hps_status hps_table_checkpoint_load(hps_table* t, const void* const* images,
+                                     const uint64_t* sizes, uint32_t count, int recover) {
+  return guarded([&] {
+    REQUIRE(t && (count == 0 || (images && sizes)), "hps_table_checkpoint_load: null argument");
+    std::lock_guard<std::mutex> g(t->impl->mu);
+    hps::table_ckpt_load(t->impl, reinterpret_cast<const uint8_t* const*>(images), sizes, count,
+                         recover);
+  });
+}
+
 hps_status hps_lookup(hps_table* t, const uint64_t* ids, size_t n, float* out_values,
                       uint64_t* out_versions, hps_stream stream) {
   return guarded([&] {

@@ -370,6 +370,76 @@ void launch_peek(const DevTable& t, const uint64_t* ids, uint64_t n, float* out_
   HPS_LAUNCH_CHECK();
 }
 
+// ---- checkpoint images (PsShard::save_checkpoint / adopt, embedding_ps.hpp:222-260,390-402)
+
+// Rows of `slots` as the HPS1 body stores them: [w D | acc D] (accumulators without the
+// svt sign bits) and the version. One warp per row.
+__global__ void ckpt_gather_kernel(DevTable t, const uint32_t* __restrict__ slots, uint64_t n,
+                                   float* __restrict__ rows2d, uint64_t* __restrict__ vers) {
+  pdl_entry();
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    const uint32_t s = slots[i];
+    const float* row = t.rows + static_cast<uint64_t>(s) * t.stride;
+    float* o = rows2d + i * 2 * t.D;
+    for (uint32_t d = lane; d < t.D; d += 32) {
+      o[d] = row[d];
+      o[t.D + d] = t.svt ? fabsf(row[t.D + d]) : row[t.D + d];
+    }
+    if (lane == 0) vers[i] = vt_read(t, s).x;
+  }
+}
+
+// Adopt rows: find-or-insert each id, then write its weights, accumulators and version;
+// the latest-bump tag is reset (adopt_locked refills the tag ring with kNoStep, :400).
+__global__ void ckpt_restore_kernel(DevTable t, const uint64_t* __restrict__ ids,
+                                    const float* __restrict__ rows2d,
+                                    const uint64_t* __restrict__ vers, uint64_t n,
+                                    uint32_t* new_slots, uint32_t* new_count) {
+  pdl_entry();
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    uint32_t s = 0;
+    if (lane == 0) s = find_or_insert(t, ids[i], new_slots, new_count, true);
+    s = __shfl_sync(0xffffffffu, s, 0);
+    if (!slot_ok(t, s)) continue;  // capacity: kCtrOverflow is set
+    const uint32_t ver = static_cast<uint32_t>(vers[i]);
+    float* row = t.rows + static_cast<uint64_t>(s) * t.stride;
+    const float* src = rows2d + i * 2 * t.D;
+    for (uint32_t d = lane; d < t.D; d += 32) {
+      row[d] = src[d];
+      float a = src[t.D + d];
+      if (t.svt && d < 64) {
+        const uint32_t l = d >> 2, k = d & 3;
+        const uint32_t word = k == 0 ? (ver & 0xffffu) : k == 1 ? (ver >> 16)
+                            : k == 2 ? (kNoStep & 0xffffu) : (kNoStep >> 16);
+        a = with_sign(a, (word >> l) & 1u);
+      }
+      row[t.D + d] = a;
+    }
+    if (lane == 0 && !t.svt) t.vt[s] = make_uint2(ver, kNoStep);
+  }
+}
+
+void launch_ckpt_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* rows2d,
+                        uint64_t* vers, cudaStream_t st) {
+  if (!n) return;
+  launch(ckpt_gather_kernel, std::min<uint64_t>(ceil_div(n, 8), 148 * 32), 256, 0, st, t, slots,
+         n, rows2d, vers);
+  HPS_LAUNCH_CHECK();
+}
+
+void launch_ckpt_restore(const DevTable& t, const uint64_t* ids, const float* rows2d,
+                         const uint64_t* vers, uint64_t n, uint32_t* new_slots,
+                         uint32_t* new_count, cudaStream_t st) {
+  if (!n) return;
+  launch(ckpt_restore_kernel, std::min<uint64_t>(ceil_div(n, 8), 148 * 32), 256, 0, st, t, ids,
+         rows2d, vers, n, new_slots, new_count);
+  HPS_LAUNCH_CHECK();
+}
+
 // ---- validation before mutation (embedding_ps.hpp:146-153) --------------------------------
 
 __global__ void check_direct_kernel(const float* __restrict__ g, uint64_t n,

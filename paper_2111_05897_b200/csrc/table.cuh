@@ -291,6 +291,12 @@ void launch_peek(const DevTable& t, const uint64_t* ids, uint64_t n, float* out_
 void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,
                  uint64_t N, int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32,
                  cudaStream_t st, const uint8_t* skip = nullptr);
+// checkpoint images (kernels.cu): gather [w | acc] + version of slots; adopt rows
+void launch_ckpt_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* rows2d,
+                        uint64_t* vers, cudaStream_t st);
+void launch_ckpt_restore(const DevTable& t, const uint64_t* ids, const float* rows2d,
+                         const uint64_t* vers, uint64_t n, uint32_t* new_slots,
+                         uint32_t* new_count, cudaStream_t st);
 void launch_snapshot_rv(const DevTable& t, const uint32_t* slots, uint64_t n, uint32_t* rv,
                         cudaStream_t st);
 void launch_check_direct(const float* grads, uint64_t n_floats, unsigned long long* ctr,

@@ -102,6 +102,12 @@ void table_clear(Table* t, cudaStream_t st);
 void table_counters(Table* t, hps_counters* out);
 void table_sync(Table* t);
 void table_reset(Table* t);
+// checkpoint.cu: HPS1 image of logical shard `shard` (returns its size; writes it when
+// buf holds cap >= size bytes); adopt a set of images (validated first, atomically).
+uint64_t table_ckpt_save(Table* t, uint32_t shard, uint32_t shard_capacity, uint8_t* buf,
+                         uint64_t cap);
+void table_ckpt_load(Table* t, const uint8_t* const* images, const uint64_t* sizes,
+                     uint32_t count, int recover);
 void read_counters(Table* t, cudaStream_t st);
 void profile_enable(Table* t, bool on);
 void profile_get(Table* t, const char* name, double* ms, uint64_t* count);

@@ -146,6 +146,8 @@ def lib():
         "hps_table_device_step": (st, [vp, C.POINTER(u32)]),
         "hps_table_advance_epoch": (u32, [vp]),
         "hps_table_reset": (st, [vp]),
+        "hps_table_checkpoint_save": (st, [vp, u32, u32, vp, u64, C.POINTER(u64)]),
+        "hps_table_checkpoint_load": (st, [vp, C.POINTER(vp), C.POINTER(u64), u32, C.c_int]),
         "hps_lookup": (st, [vp, vp, sz, vp, vp, vp]),
         "hps_table_gather": (st, [vp, vp, sz, vp, vp, u32, vp]),
         "hps_apply": (st, [vp, vp, vp, vp, sz, f32, u32, u32, vp, C.POINTER(C.c_int), u32, vp]),
@@ -374,6 +376,25 @@ class ShardSet:
 
     def sync(self):
         check(lib().hps_table_sync(self.h), "sync")
+
+    # PsShard::save_checkpoint (embedding_ps.hpp:222-260), per logical shard
+    def save_checkpoint(self, shard: int = 0, shard_capacity: int = 0) -> bytes:
+        n = C.c_uint64(0)
+        check(lib().hps_table_checkpoint_save(self.h, shard, shard_capacity, None, 0,
+                                              C.byref(n)), "save_checkpoint")
+        buf = (C.c_uint8 * max(n.value, 1))()
+        check(lib().hps_table_checkpoint_save(self.h, shard, shard_capacity, buf, n.value,
+                                              C.byref(n)), "save_checkpoint")
+        return bytes(buf)[:n.value]
+
+    # PsShard::load_checkpoint / recover_from_checkpoint (:262-300) for the whole table
+    def load_checkpoint(self, images, recover: bool = False):
+        images = [bytes(im) for im in images]
+        bufs = [C.create_string_buffer(im, len(im)) for im in images]
+        ptrs = (vp * max(len(bufs), 1))(*[C.cast(b, vp) for b in bufs])
+        sizes = (C.c_uint64 * max(len(bufs), 1))(*[len(im) for im in images])
+        check(lib().hps_table_checkpoint_load(self.h, ptrs, sizes, len(images), int(recover)),
+              "load_checkpoint")
 
     def profile(self, enable: bool = True):
         check(lib().hps_profile_enable(self.h, int(enable)), "profile")

@@ -79,6 +79,27 @@ int main() {
   ew.flush_step_marker(1, 0);
   auto row2 = set.lookup({10});
   for (int d = 0; d < 8; ++d) EXPECT(row2[10][d] == row[10][d] - 0.5f * 0.25f);
+
+  // checkpoint round trip (test_embedding_ps.cpp:243-391): save, corrupt -> rejected and
+  // unchanged, recover -> same row, epoch past the live one
+  std::vector<uint8_t> img;
+  EXPECT(ps.save_checkpoint(img) == img.size() && img.size() > 64);
+  EXPECT(std::memcmp(img.data(), "HPS1", 4) == 0);
+  std::vector<uint8_t> broken = img;
+  broken[70] ^= 1;
+  threw = false;
+  try {
+    ps.recover_from_checkpoint(broken);
+  } catch (const CheckpointCorruptError&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  const uint32_t e_live = ps.epoch();
+  ps.recover_from_checkpoint(img);
+  EXPECT(ps.epoch() == e_live + 1);
+  std::vector<float> restored(4);
+  ps.lookup({42}, restored.data(), ver.data());
+  EXPECT(std::memcmp(restored.data(), after.data(), sizeof(float) * 4) == 0 && ver[0] == 1);
   if (fails == 0) std::printf("compat_smoke OK\n");
   return fails ? 1 : 0;
 }
