@@ -38,8 +38,10 @@ constexpr int kXBlock = 256;
 constexpr uint32_t kInserter = 0x80000000u;
 constexpr uint32_t kNoPair = 0xffffffffu;
 // x.cnt layout (u32 words): [0,32) distinct ids per owner, [32] special-id claim,
-// [33] listings of multi-listed ids, [64,96) single pairs per owner.
-constexpr int kCntSpecial = 32, kCntMulti = 33, kCntSingle = 64, kCntWords = 128;
+// [33] listings of multi-listed ids, [64,96) single pairs per owner, [100] groups left
+// for the requester's own pooling (glist).
+constexpr int kCntSpecial = 32, kCntMulti = 33, kCntSingle = 64, kCntGlist = 100,
+              kCntWords = 128;
 
 // Distinct ids: a transient open-addressing set (keys only). The entry index of each
 // listing's id is recorded; the thread whose CAS claimed the entry is its inserter and
@@ -198,6 +200,25 @@ __global__ void __launch_bounds__(kXBlock)
     if (multi && s_base + r < radix::kSmallN)
       mkeys[s_base + r] = (static_cast<unsigned long long>(pos) << lbits) | i;
     __syncthreads();
+  }
+}
+
+// Groups the owners did not pool (gdirect == 0: empty groups, several listings, or an id
+// listed more than once) -> glist, warp-aggregated appends; the requester pools only those.
+__global__ void x_glist_kernel(const uint8_t* __restrict__ gdirect, uint64_t BF,
+                               uint32_t* __restrict__ glist, uint32_t* cnt) {
+  pdl_entry();
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < BF;
+       base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = base + threadIdx.x;
+    const bool want = g < BF && !gdirect[g];
+    const unsigned m = __ballot_sync(0xffffffffu, want);
+    if (!m) continue;
+    uint32_t b = 0;
+    if (lane == __ffs(m) - 1) b = atomicAdd(&cnt[kCntGlist], __popc(m));
+    b = __shfl_sync(0xffffffffu, b, __ffs(m) - 1);
+    if (want) glist[b + __popc(m & ((1u << lane) - 1))] = static_cast<uint32_t>(g);
   }
 }
 
@@ -466,7 +487,11 @@ XBatch::~XBatch() {
     if (peer[r] && peer[r] != arena) cudaIpcCloseMemHandle(peer[r]);
   if (arena) cudaFree(arena);
   if (gdirect) cudaFree(gdirect);
+  if (glist) cudaFree(glist);
   if (side) cudaStreamDestroy(side);
+  if (aux) cudaStreamDestroy(aux);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   if (xbase) cudaFree(xbase);
   if (dev_epoch) cudaFree(dev_epoch);
   void* ps[] = {hkeys,  hidx,   hval,   hmul,    dest,    sendpos, spair, offsets, lgrp,
@@ -546,6 +571,11 @@ static void route_core(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_
       ids, n, x.G, x.hidx, x.hval, x.dest, x.spair, x.cnt, x.lbits, x.sendpos, send_ids, x.seg,
       x.mkeys, pid, x.lgrp, x.offsets, gdirect);
   HPS_LAUNCH_CHECK();
+  if (gdirect) {
+    launch(x_glist_kernel, grid_n(std::max<uint64_t>(BF, 1), x.sms), kXBlock, 0, st, gdirect, BF,
+           x.glist, x.cnt);
+    HPS_LAUNCH_CHECK();
+  }
 }
 
 // Pair ordering and counts up to (not including) the emit kernels: x.pair_off = owners'
@@ -639,7 +669,8 @@ void xbatch_pool(XBatch& x, const float* rows, uint32_t D, float* out_pooled, cu
       view.stride = D;
       view.capacity = static_cast<uint32_t>(x.N);
       launch_pool(view, x.offsets, x.sendpos, static_cast<uint32_t>(BF), x.N,
-                  x.agg == HPS_MEAN ? 1 : 0, arena_pooled, nullptr, nullptr, st, x.gdirect);
+                  x.agg == HPS_MEAN ? 1 : 0, arena_pooled, nullptr, nullptr, st, x.glist,
+                  x.cnt + kCntGlist);
       if (out_pooled && out_pooled != arena_pooled) {
         require_device(out_pooled, "hps_exchange_pool out");
         HPS_CUDA(cudaMemcpyAsync(out_pooled, arena_pooled, BF * D * sizeof(float),
@@ -956,6 +987,7 @@ void xbatch_arena(XBatch& x, uint64_t max_ids, uint64_t max_groups, uint32_t D, 
   x.arena_bytes = o;
   x.max_groups = max_groups;
   HPS_CUDA(cudaMalloc(&x.gdirect, std::max<uint64_t>(max_groups, 1)));
+  HPS_CUDA(cudaMalloc(&x.glist, std::max<uint64_t>(max_groups, 1) * sizeof(uint32_t)));
   x.max_ids = M;
   x.arena_dim = D;
   HPS_CUDA(cudaMalloc(&x.arena, o));
@@ -1026,6 +1058,26 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
     launch(x_fwd_hdr_kernel, 1, 32, 0, st, ph, x.G, x.rank, x.cnt, x.seg);
     HPS_LAUNCH_CHECK();
   }
+  // The pair plan of the backward (push_to_shards' per-sample dedup) depends only on the
+  // routed batch: it runs on a second stream beside the owner lookup and the row
+  // delivery (latency-bound sorts overlapping an NVLink-bound gather), joined before the
+  // forward returns.
+  x.pairs_ready = false;
+  if (n) {
+    if (!x.aux) {
+      HPS_CUDA(cudaStreamCreateWithFlags(&x.aux, cudaStreamNonBlocking));
+      HPS_CUDA(cudaEventCreateWithFlags(&x.ev_fork, cudaEventDisableTiming));
+      HPS_CUDA(cudaEventCreateWithFlags(&x.ev_join, cudaEventDisableTiming));
+    }
+    HPS_CUDA(cudaEventRecord(x.ev_fork, st));
+    HPS_CUDA(cudaStreamWaitEvent(x.aux, x.ev_fork, 0));
+    {
+      ProfScope p(t, "x_pairs", x.aux);
+      pairs_core(x, &x.pairs_spos, &x.pairs_slist, x.aux);
+    }
+    HPS_CUDA(cudaEventRecord(x.ev_join, x.aux));
+    x.pairs_ready = true;
+  }
   barrier(x, t, st);  // every id region and count has landed
   // owner: find-or-init the ids every source asked for, rows straight back to them
   XHdr* mine = ph.h[x.rank];
@@ -1060,6 +1112,7 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
     HPS_LAUNCH_CHECK();
   }
   barrier(x, t, st);  // every owner's rows have landed in this rank's rows buffer
+  if (x.pairs_ready) HPS_CUDA(cudaStreamWaitEvent(st, x.ev_join, 0));
 }
 
 void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step_tag,
@@ -1070,7 +1123,11 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
   const uint64_t M = x.max_ids;
   const PeerHdrs ph = peer_hdrs(x);
   const uint32_t *spos = nullptr, *slist = nullptr;
-  if (x.N) {
+  if (x.N && x.pairs_ready) {  // planned beside the forward (xbatch_fwd)
+    spos = x.pairs_spos;
+    slist = x.pairs_slist;
+    x.pairs_ready = false;
+  } else if (x.N) {
     ProfScope p(t, "x_pairs", st);
     pairs_core(x, &spos, &slist, st);
   } else {

@@ -96,25 +96,30 @@ __device__ void pool_general(const DevTable& t, const uint32_t* __restrict__ slo
 
 }  // namespace
 
-template <int V, int L, bool kGuard>
+// kList: pool only the groups listed in glist[0 .. *glist_n) (the exchange's groups that
+// their rows' owners did not already write).
+template <int V, int L, bool kGuard, bool kList>
 __global__ void __launch_bounds__(256, 8)
     pool_kernel(DevTable t, const uint32_t* __restrict__ offsets,
                 const uint32_t* __restrict__ slots, uint32_t BF, uint64_t N, int mean,
                 float* __restrict__ out, uint64_t* __restrict__ out_rv64,
-                uint32_t* __restrict__ out_rv32, const uint8_t* __restrict__ skip) {
+                uint32_t* __restrict__ out_rv32, const uint32_t* __restrict__ glist,
+                const uint32_t* __restrict__ glist_n) {
   pdl_entry();
   using G = Geo<V, L, kGuard>;
   const int ln = G::lane();
   const uint32_t D = t.D;
   const uint64_t groups = G::groups();
-  for (uint64_t sg0 = G::group(); sg0 < BF; sg0 += groups * kPoolILP) {
+  const uint64_t count = kList ? *glist_n : BF;
+  for (uint64_t k0 = G::group(); k0 < count; k0 += groups * kPoolILP) {
     uint64_t sg[kPoolILP];
     uint32_t a[kPoolILP], e[kPoolILP], spec[kPoolILP];
     bool live[kPoolILP];
 #pragma unroll
     for (int u = 0; u < kPoolILP; ++u) {
-      sg[u] = sg0 + u * groups;
-      live[u] = sg[u] < BF && !(skip && skip[sg[u]]);  // skip: written by the row's owner
+      const uint64_t k = k0 + u * groups;
+      live[u] = k < count;
+      sg[u] = kList ? (live[u] ? glist[k] : 0u) : k;
       a[u] = live[u] ? offsets[sg[u]] : 0u;
       e[u] = live[u] ? offsets[sg[u] + 1] : 0u;
       spec[u] = (live[u] && sg[u] < N) ? slots[sg[u]] : 0u;  // right when a == sg
@@ -189,14 +194,22 @@ void launch_snapshot_rv(const DevTable& t, const uint32_t* slots, uint64_t n, ui
 
 void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,
                  uint64_t N, int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32,
-                 cudaStream_t st, const uint8_t* skip) {
+                 cudaStream_t st, const uint32_t* glist, const uint32_t* glist_n) {
   if (!BF) return;
   HPS_DISPATCH_DIM(t.D, {
     uint64_t groups_per_block = 256 / L;
-    uint32_t blocks =
-        std::min<uint64_t>(ceil_div(BF, groups_per_block * kPoolILP), 1u << 30);
-    launch(pool_kernel<V, L, G>, blocks, 256, 0, st, t, offsets, slots, BF, N, mean, out, out_rv64,
-                                                 out_rv32, skip);
+    if (glist) {
+      // list length is device-side: one wave of blocks strides over it
+      const uint32_t blocks = std::min<uint64_t>(ceil_div(BF, groups_per_block * kPoolILP),
+                                                 148ull * 8);
+      launch(pool_kernel<V, L, G, true>, blocks, 256, 0, st, t, offsets, slots, BF, N, mean, out,
+             out_rv64, out_rv32, glist, glist_n);
+    } else {
+      uint32_t blocks =
+          std::min<uint64_t>(ceil_div(BF, groups_per_block * kPoolILP), 1u << 30);
+      launch(pool_kernel<V, L, G, false>, blocks, 256, 0, st, t, offsets, slots, BF, N, mean,
+             out, out_rv64, out_rv32, nullptr, nullptr);
+    }
   });
   HPS_LAUNCH_CHECK();
 }

@@ -286,11 +286,12 @@ void launch_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* 
                    uint64_t* out_versions, cudaStream_t st);
 void launch_peek(const DevTable& t, const uint64_t* ids, uint64_t n, float* out_w, float* out_acc,
                  uint64_t* out_versions, uint8_t* out_present, cudaStream_t st);
-// skip (optional): groups whose pooled value is already in `out` (one-listing groups the
-// exchange owners wrote directly).
+// glist/glist_n (optional): pool only the listed groups (device-side count); the others'
+// pooled values are already in `out` (one-listing groups the exchange owners wrote).
 void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,
                  uint64_t N, int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32,
-                 cudaStream_t st, const uint8_t* skip = nullptr);
+                 cudaStream_t st, const uint32_t* glist = nullptr,
+                 const uint32_t* glist_n = nullptr);
 // checkpoint images (kernels.cu): gather [w | acc] + version of slots; adopt rows
 void launch_ckpt_gather(const DevTable& t, const uint32_t* slots, uint64_t n, float* rows2d,
                         uint64_t* vers, cudaStream_t st);

@@ -186,6 +186,13 @@ struct XBatch {
   uint64_t max_groups = 0;
   bool direct_ok = false;
   uint8_t* gdirect = nullptr;  // [max_groups] groups the owners pooled this step
+  uint32_t* glist = nullptr;   // [max_groups] the other groups (pooled here), count in cnt
+  // peer step: the pair plan runs on `aux` beside the owner lookup/gather (fork/join
+  // events inside the forward, so a captured forward is self-contained)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool pairs_ready = false;
+  const uint32_t *pairs_spos = nullptr, *pairs_slist = nullptr;
   uint64_t max_ids = 0;
   uint32_t arena_dim = 0, rank = 0;
   bool connected = false;
