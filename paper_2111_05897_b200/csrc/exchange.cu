@@ -290,7 +290,21 @@ __global__ void x_pair_bounds_kernel(const uint32_t* __restrict__ spos,
 struct PairOut {
   float* c[kMaxWorld];
   uint32_t* p[kMaxWorld];
+  // peer path: owner d's XHdr::bad word for this source, and the barrier epoch of this
+  // emit (the validation PsShard::apply_gradients does before mutating, :146-153, done
+  // here while the contributions are formed; the owner reads the words after the barrier)
+  uint32_t* bad[kMaxWorld];
+  const unsigned long long* epoch;
 };
+
+template <int V>
+__device__ __forceinline__ void flag_nonfinite(const PairOut& po, uint32_t d, const float (&o)[V]) {
+  if (!po.epoch) return;
+  bool bad = false;
+#pragma unroll
+  for (int v = 0; v < V; ++v) bad |= !isfinite(o[v]);
+  if (bad) *reinterpret_cast<volatile uint32_t*>(po.bad[d]) = static_cast<uint32_t>(*po.epoch);
+}
 
 template <int V, bool GEN>
 __device__ __forceinline__ void put_row(float* dst, const float (&o)[V]) {
@@ -335,6 +349,7 @@ __global__ void __launch_bounds__(kXBlock)
       for (int v = 0; v < V; ++v)
         o[v] = __double2float_rn(__dadd_rn(0.0, __dmul_rn(static_cast<double>(x[v]), scale)));
       put_row<V, GEN>(po.c[d] + out * D + d0, o);
+      flag_nonfinite<V>(po, d, o);
     }
   }
 }
@@ -389,6 +404,7 @@ __global__ void __launch_bounds__(kXBlock)
 #pragma unroll
       for (int v = 0; v < V; ++v) o[v] = __double2float_rn(acc[v]);
       put_row<V, GEN>(po.c[d] + out * D + d0, o);
+      flag_nonfinite<V>(po, d, o);
     }
   }
 }
@@ -810,9 +826,18 @@ __global__ void x_owner_dyn_kernel(const XHdr* __restrict__ hdr,
                                    uint32_t* __restrict__ out_off,
                                    unsigned long long* protocol, DevTable t,
                                    const uint32_t* __restrict__ oslot,
-                                   uint32_t* __restrict__ out_slot) {
+                                   uint32_t* __restrict__ out_slot,
+                                   const unsigned long long* epoch) {
   pdl_entry();
   __shared__ uint64_t po[kMaxWorld + 1];
+  if (epoch && blockIdx.x == 0 && threadIdx.x == 0) {
+    // the sources validated the contributions while emitting them (one barrier ago)
+    const uint32_t e = static_cast<uint32_t>(*epoch - 1);
+    bool bad = false;
+    for (uint32_t r = 0; r < W; ++r) bad |= ld_volatile(&hdr->bad[r]) == e;
+    t.ctr[kCtrDivergence] = bad ? 1ull : 0ull;
+    t.ctr[kCtrNeedExact] = 0ull;  // a contribution that is finite applies as is
+  }
   if (threadIdx.x == 0) {
     uint64_t run = 0;
     for (uint32_t r = 0; r < W; ++r) {
@@ -1143,7 +1168,9 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
     for (uint32_t d = 0; d < x.G; ++d) {
       po.c[d] = reinterpret_cast<float*>(x.peer[d] + x.off_contrib);
       po.p[d] = reinterpret_cast<uint32_t*>(x.peer[d] + x.off_ppos);
+      po.bad[d] = &ph.h[d]->bad[x.rank];
     }
+    po.epoch = x.dev_epoch;
     ProfScope p(t, "x_emit", st);
     emit_pairs(x, grads, D, spos, slist, x.xbase, po, st);
   }
@@ -1165,7 +1192,7 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
       reinterpret_cast<const uint64_t*>(x.arena + x.off_oids), nullptr,
       reinterpret_cast<const uint32_t*>(x.arena + x.off_ppos), cap, xs.ids, xs.rv, xs.off,
       t->d.ctr + kCtrProtocol, t->d, reinterpret_cast<const uint32_t*>(x.arena + x.off_oslot),
-      b.slot);
+      b.slot, x.dev_epoch);
   HPS_LAUNCH_CHECK();
   batch_register(b, xs.ids, cap, xs.off, static_cast<uint32_t>(cap), 1, nullptr, st, true,
                  /*slots_ready=*/true);
@@ -1176,7 +1203,7 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
   b.pulled = true;
   b.rv_valid = false;
   batch_push(b, HPS_SUM, reinterpret_cast<const float*>(x.arena + x.off_contrib), lr, step_tag,
-             epoch, 0, nullptr, accepted, flags, st);
+             epoch, 0, nullptr, accepted, flags | kPushPrechecked, st);
 }
 
 }  // namespace hps

@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(256, 6)
                        uint64_t rows, uint32_t D, uint32_t F, int mean,
                        unsigned long long* ctr, float* __restrict__ cbuf,
                        const uint32_t* __restrict__ inv, const uint32_t* gate,
-                       const uint32_t* rows_live) {
+                       const uint32_t* rows_live, int scatter_only) {
   pdl_entry();
   if (rows_live) rows = min(rows, static_cast<uint64_t>(*rows_live));
   using G = Geo<V, L, kGuard>;
@@ -484,6 +484,7 @@ __global__ void __launch_bounds__(256, 6)
   if (threadIdx.x == 0) s_write = cbuf && (!gate || ld_volatile(gate) > radix::kSmallN);
   __syncthreads();
   const bool write_c = s_write != 0;
+  if (scatter_only && !write_c) return;
   const int ln = G::lane();
   const int chunks = kGuard ? (D + G::kSpan - 1) / G::kSpan : 1;
   const uint64_t groups = G::groups();
@@ -553,14 +554,16 @@ __global__ void __launch_bounds__(256, 6)
 void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
                         uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st,
                         float* cbuf, const uint32_t* inv, const uint32_t* gate,
-                        const uint32_t* rows_live) {
+                        const uint32_t* rows_live, bool scatter_only) {
   const uint64_t rows = static_cast<uint64_t>(B) * F;
   if (!rows) return;
+  if (scatter_only && !cbuf) return;
   HPS_DISPATCH_DIM(D, {
     uint64_t groups_per_block = 256 / L;
     uint32_t blocks = std::min<uint64_t>(ceil_div(rows, groups_per_block * 4), 148ull * 16);
     launch(check_batch_kernel<V, L, G>, blocks, 256, 0, st, grads, offsets, rows, D, F, mean, ctr,
-                                                        cbuf, inv, gate, rows_live);
+                                                        cbuf, inv, gate, rows_live,
+                                                        scatter_only ? 1 : 0);
   });
   HPS_LAUNCH_CHECK();
 }

@@ -655,13 +655,17 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   Stager stg(t->stage);
   const float* d_g = static_cast<const float*>(stg.in(grads, BF * D * sizeof(float), st));
   const uint64_t* d_rv = static_cast<const uint64_t*>(stg.in(rv64, b.N * sizeof(uint64_t), st));
-  HPS_CUDA(cudaMemsetAsync(t->d.ctr + kCtrDivergence, 0, 2 * sizeof(unsigned long long), st));
+  // kPushPrechecked (exchange owners): the divergence / need-exact words were set by the
+  // owner's batch assembly from what the sources found while emitting
+  const bool prechecked = (flags & kPushPrechecked) != 0;
+  if (!prechecked)
+    HPS_CUDA(cudaMemsetAsync(t->d.ctr + kCtrDivergence, 0, 2 * sizeof(unsigned long long), st));
   const int mean = agg == HPS_MEAN ? 1 : 0;
   {
     ProfScope p(t, "check", st);
     launch_check_batch(d_g, b.offsets, b.B, b.F, D, mean, t->d.ctr, st,
                        b.meta_ok ? b.cbuf : nullptr, b.inv,
-                       b.all_multi ? nullptr : &b.small[0], b.n_live);
+                       b.all_multi ? nullptr : &b.small[0], b.n_live, prechecked);
   }
   UpdateArgs a = plan_args(b);
   a.mean = mean;

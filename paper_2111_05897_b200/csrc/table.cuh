@@ -200,6 +200,8 @@ struct alignas(128) XHdr {
   uint32_t fwd_cnt[kMaxWorld];        // ids source r wrote into my id region r
   uint32_t fwd_seg[kMaxWorld];        // where my rows go in source r's rows buffer
   uint32_t bwd_cnt[kMaxWorld];        // pairs source r sends me
+  uint32_t bad[kMaxWorld];            // = the emit's barrier epoch if source r sent me a
+                                      //   non-finite contribution in that step
   uint32_t err;                       // barrier timeout seen by this rank
 };
 struct XScratch {
@@ -304,10 +306,14 @@ void launch_check_direct(const float* grads, uint64_t n_floats, unsigned long lo
                          cudaStream_t st);
 // cbuf/inv (optional, large plan only): also writes every listing's contribution to
 // cbuf[inv[listing]] when the plan gate (*gate > kSmallN, or gate == null) is open.
+// scatter_only: the caller validated the contributions already (exchange owners: the
+// sources checked them while emitting); only the large plan's scatter runs, and the
+// launch is a no-op when the plan is small.
 void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
                         uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st,
                         float* cbuf = nullptr, const uint32_t* inv = nullptr,
-                        const uint32_t* gate = nullptr, const uint32_t* rows_live = nullptr);
+                        const uint32_t* gate = nullptr, const uint32_t* rows_live = nullptr,
+                        bool scatter_only = false);
 
 struct UpdateArgs {
   // Multi kernel input: either the large-path slot sort of all n listings, or -- when

@@ -45,7 +45,7 @@ def local_part(ids, offs, W, B, F, r):
 
 
 def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, agg="mean",
-             opt="adagrad", space=60, transport="p2p", graph=False, q=None):
+             opt="adagrad", space=60, transport="p2p", graph=False, nan_step=-1, q=None):
     try:
         import torch
         import torch.distributed as dist
@@ -83,6 +83,9 @@ def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, ag
             gids, goffs, _ = global_batch(s, world, B, F, space, fixed_shape=graph)
             rng = np.random.default_rng(500 + s)
             g_all = (rng.standard_normal((world * B, F, D)) * 0.3).astype(np.float32)
+            if s == nan_step:  # one non-finite gradient of the first non-empty group
+                g0 = int(np.argmax(np.diff(goffs) > 0))
+                g_all[g0 // F, g0 % F, D // 2] = np.nan
             sk = np.array([((i % world) << 56) | (i // world) for i in range(world * B)],
                           np.uint64)
             pooled_exp, rv_exp = exp.pull_batch(world * B, F, gids, goffs.astype(np.uint64), agg)
@@ -117,6 +120,17 @@ def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, ag
             if not (graph and s >= 1):
                 ok = ew.apply_backward(g_local, 0.05, s + 1, flags=flags)
                 assert ok
+            if s == nan_step:
+                # world 1: the (only) owner rejects the whole step -- nothing applied, the
+                # DivergenceError surfaces from the next synchronising call
+                assert world == 1 and use_device
+                torch.cuda.synchronize()
+                try:
+                    table.sync()
+                    raise AssertionError("non-finite contribution not reported")
+                except hps.DivergenceError:
+                    pass
+                continue
             ok2, _ = exp.push_batch(world * B, F, gids, goffs.astype(np.uint64), g_all, 0.05,
                                     s + 1, read_versions=rv_exp, sample_keys=sk, agg=agg)
             assert ok2

@@ -38,6 +38,17 @@ def test_sharded_device_world1(transport):
 @pytest.mark.gpu
 @pytest.mark.parametrize("transport", TRANSPORTS)
 @pytest.mark.parametrize("D", [64, 5])
+def test_sharded_device_world1_nonfinite_rejected(D, transport):
+    """A non-finite contribution at step 1: the owner applies nothing of that step (the
+    sources validate while emitting on the p2p path, the owner's check on nccl); the
+    steps before and after match the oracle that skipped it."""
+    res = run_world(1, "nccl", use_device=True, D=D, steps=3, nan_step=1, transport=transport)
+    assert res[0][1] == "ok", res[0][1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("transport", TRANSPORTS)
+@pytest.mark.parametrize("D", [64, 5])
 def test_sharded_device_world1_large_plan(D, transport):
     """More than 4096 listings of repeated ids: the device-gated radix-sort path."""
     res = run_world(1, "nccl", use_device=True, B=1500, F=4, D=D, space=2500, steps=2,
