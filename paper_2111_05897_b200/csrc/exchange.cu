@@ -1136,8 +1136,16 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
     });
     HPS_LAUNCH_CHECK();
   }
-  barrier(x, t, st);  // every owner's rows have landed in this rank's rows buffer
+  // The backward's pair counts are known once the pair plan has finished: they ride on
+  // this barrier instead of one of their own. (Safe against the next step: a source
+  // writes step s+1's counts only after the first barrier of s+1, which every owner
+  // reaches after its step-s apply has read them.)
   if (x.pairs_ready) HPS_CUDA(cudaStreamWaitEvent(st, x.ev_join, 0));
+  else HPS_CUDA(cudaMemsetAsync(x.pair_off, 0, 33 * sizeof(uint64_t), st));
+  launch(x_bwd_hdr_kernel, 1, 32, 0, st, ph, x.G, x.rank, x.pair_off);
+  HPS_LAUNCH_CHECK();
+  x.counts_sent = true;
+  barrier(x, t, st);  // every owner's rows have landed in this rank's rows buffer
 }
 
 void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step_tag,
@@ -1147,20 +1155,12 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
   require_device(grads, "hps_exchange_bwd grads");
   const uint64_t M = x.max_ids;
   const PeerHdrs ph = peer_hdrs(x);
-  const uint32_t *spos = nullptr, *slist = nullptr;
-  if (x.N && x.pairs_ready) {  // planned beside the forward (xbatch_fwd)
-    spos = x.pairs_spos;
-    slist = x.pairs_slist;
-    x.pairs_ready = false;
-  } else if (x.N) {
-    ProfScope p(t, "x_pairs", st);
-    pairs_core(x, &spos, &slist, st);
-  } else {
-    HPS_CUDA(cudaMemsetAsync(x.pair_off, 0, 33 * sizeof(uint64_t), st));
-  }
-  launch(x_bwd_hdr_kernel, 1, 32, 0, st, ph, x.G, x.rank, x.pair_off);
-  HPS_LAUNCH_CHECK();
-  barrier(x, t, st);  // every owner knows how many pairs each source sends
+  // the pair plan ran beside the forward, whose last barrier also delivered the counts
+  if (!x.counts_sent) throw Error(HPS_E_PRECONDITION, "exchange backward: no forward for this batch");
+  x.counts_sent = false;
+  const uint32_t* spos = x.pairs_spos;
+  const uint32_t* slist = x.pairs_slist;
+  x.pairs_ready = false;
   launch(x_bwd_base_kernel, 1, 32, 0, st, ph, x.G, x.rank, x.xbase);
   HPS_LAUNCH_CHECK();
   if (x.N) {

@@ -682,13 +682,16 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     if (b.rv_valid) a.rv32 = b.rv;
     else a.fresh = 1;  // no mutation since the pull: read version == current version
   }
-  // Exact validation (dry runs), executed only if the bound check was inconclusive.
-  a.dry_run = 1;
-  run_if(t->side, st, t->d.ctr + kCtrNeedExact, true, 0, [&](cudaStream_t s) {
-    if (!b.all_multi) launch_update_single(t->d, a, t->sm_count, s);
-    launch_update(t->d, a, false, t->sm_count, s);
-  });
-  a.dry_run = 0;
+  // Exact validation (dry runs), executed only if the bound check was inconclusive
+  // (never for prechecked contributions: a finite contribution applies as is).
+  if (!prechecked) {
+    a.dry_run = 1;
+    run_if(t->side, st, t->d.ctr + kCtrNeedExact, true, 0, [&](cudaStream_t s) {
+      if (!b.all_multi) launch_update_single(t->d, a, t->sm_count, s);
+      launch_update(t->d, a, false, t->sm_count, s);
+    });
+    a.dry_run = 0;
+  }
   if (t->cfg.embedding_dim <= kHotMaxDim) {
     // hot-row hand-off list (runs_kernel -> update_hot)
     a.hot = b.hot;

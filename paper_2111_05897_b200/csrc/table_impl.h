@@ -194,6 +194,7 @@ struct XBatch {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool pairs_ready = false;
+  bool counts_sent = false;  // the forward delivered this batch's pair counts
   const uint32_t *pairs_spos = nullptr, *pairs_slist = nullptr;
   uint64_t max_ids = 0;
   uint32_t arena_dim = 0, rank = 0;
