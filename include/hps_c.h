@@ -293,6 +293,20 @@ hps_status hps_profile_get(hps_table* t, const char* region, double* total_ms, u
  * Device or host pointers. */
 hps_status hps_dedup(const uint64_t* ids, size_t n, uint64_t* out_unique, uint32_t* out_inverse,
                      uint64_t* out_u, hps_stream stream);
+/* The reference's lossy value codec, one block per row of block_len floats (codec.hpp:
+ * 208-261; per embedding row on the wire, embedding_worker.hpp:48-85):
+ * compress_values: out_scales[r] = kappa / ||row r||_inf (1.0 for an all-zero row),
+ * out_payload[r*block_len + i] = binary16 bits of v*scale, round to nearest even
+ * (float_to_half_bits :35-73) -- bit-identical to the reference. kappa <= 0 or a
+ * non-finite input -> HPS_E_PRECONDITION. decompress_values: out = widened / scale; a
+ * scale that is not finite and > 0, or a non-finite widened value -> HPS_E_PROTOCOL.
+ * Host or device buffers; synchronises the stream (errors are reported). */
+hps_status hps_compress_values(const float* values, uint64_t rows, uint32_t block_len,
+                               float kappa, float* out_scales, uint16_t* out_payload,
+                               hps_stream stream);
+hps_status hps_decompress_values(const float* scales, const uint16_t* payload, uint64_t rows,
+                                 uint32_t block_len, float* out, hps_stream stream);
+
 /* compress_indices (codec.hpp:123-156): per group g, unique ids ascending
  * (unique[group_u_off[g] .. group_u_off[g+1]]) each with its ascending postings
  * (postings[post_off[k] .. post_off[k+1]], u16 sample indices, within-sample duplicates

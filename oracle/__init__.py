@@ -127,6 +127,10 @@ def reference_lib():
                                              u16p]
         lib.ref_shard_import.restype = C.c_int
         lib.ref_shard_import.argtypes = [C.c_void_p, C.c_uint32, u8p, C.c_uint64, C.c_int]
+        lib.ref_compress_values.restype = C.c_int
+        lib.ref_compress_values.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_float, f32p, u16p]
+        lib.ref_decompress_values.restype = C.c_int
+        lib.ref_decompress_values.argtypes = [f32p, u16p, C.c_uint64, C.c_uint32, f32p]
         lib.ref_dense_init.restype = C.c_int64
         lib.ref_dense_init.argtypes = [u64p, C.c_uint32, C.c_uint64, f32p, C.c_uint64]
         lib.ref_dense_fwd_bwd.restype = C.c_int
@@ -471,3 +475,44 @@ def ref_sgd_step(params, grad, lr: float) -> np.ndarray:
     g = _f32(grad)
     _ref_rc(reference_lib().ref_sgd_step(_p(p, f32p), _p(g, f32p), len(p), lr), "sgd_step")
     return p
+
+
+# ---- value codec (codec.hpp:30-103, 208-261) ---------------------------------------------
+
+
+def ref_compress_values(v, kappa: float = 1024.0):
+    """The reference's compress_values per row of v[rows, len] -> (scales, payload u16)."""
+    v = _f32(np.atleast_2d(v))
+    rows, n = v.shape
+    sc = np.zeros(rows, np.float32)
+    pl = np.zeros((rows, n), np.uint16)
+    _ref_rc(reference_lib().ref_compress_values(_p(v, f32p), rows, n, kappa, _p(sc, f32p),
+                                                _p(pl, u16p)), "compress_values")
+    return sc, pl
+
+
+def ref_decompress_values(scales, payload):
+    sc = _f32(scales)
+    pl = np.ascontiguousarray(np.atleast_2d(payload), np.uint16)
+    out = np.zeros(pl.shape, np.float32)
+    _ref_rc(reference_lib().ref_decompress_values(_p(sc, f32p), _p(pl, u16p), pl.shape[0],
+                                                  pl.shape[1], _p(out, f32p)), "decompress_values")
+    return out
+
+
+def compress_values_np(v, kappa: float = 1024.0):
+    """Restatement (numpy): scale = kappa / max|row| (1 for a zero row) in float32, payload =
+    binary16 of v*scale (IEEE round-to-nearest-even with subnormals, as float_to_half_bits),
+    an all-zero row -> +0 payload."""
+    v = np.atleast_2d(np.asarray(v, np.float32))
+    m = np.abs(v).max(axis=1)
+    zero = m == 0
+    scale = np.where(zero, np.float32(1.0), np.float32(kappa) / np.where(zero, 1, m)).astype(np.float32)
+    pl = (v * scale[:, None]).astype(np.float16).view(np.uint16)
+    pl[zero] = 0
+    return scale, pl
+
+
+def decompress_values_np(scales, payload):
+    w = np.asarray(payload, np.uint16).view(np.float16).astype(np.float32)
+    return (w / np.asarray(scales, np.float32)[:, None]).astype(np.float32)

@@ -275,6 +275,32 @@ int ref_shard_import(void* h, uint32_t s, const uint8_t* buf, uint64_t n, int va
   });
 }
 
+// compress_values / decompress_values (codec.hpp:222-261), one block per row of len.
+int ref_compress_values(const float* v, uint64_t rows, uint32_t len, float kappa, float* scales,
+                        uint16_t* payload) {
+  return guarded([&] {
+    for (uint64_t r = 0; r < rows; ++r) {
+      CompressedBlock b = compress_values(std::vector<float>(v + r * len, v + (r + 1) * len), kappa);
+      scales[r] = b.scale;
+      std::memcpy(payload + r * len, b.payload.data(), len * sizeof(uint16_t));
+    }
+  });
+}
+
+int ref_decompress_values(const float* scales, const uint16_t* payload, uint64_t rows,
+                          uint32_t len, float* out) {
+  return guarded([&] {
+    for (uint64_t r = 0; r < rows; ++r) {
+      CompressedBlock b;
+      b.scale = scales[r];
+      b.block_len = len;
+      b.payload.assign(payload + r * len, payload + (r + 1) * len);
+      std::vector<float> o = decompress_values(b);
+      std::memcpy(out + r * len, o.data(), len * sizeof(float));
+    }
+  });
+}
+
 // compress_indices (codec.hpp:123-156) over a CSR batch. Outputs, all caller-sized
 // for the worst case (N listings): group_u_off[G+1], unique[<=N], post_off[<=N+1]
 // (relative to the flat postings array), postings[<=N] (u16 sample indices).

@@ -471,6 +471,25 @@ hps_status hps_dedup(const uint64_t* ids, size_t n, uint64_t* out_unique, uint32
   });
 }
 
+hps_status hps_compress_values(const float* values, uint64_t rows, uint32_t block_len,
+                               float kappa, float* out_scales, uint16_t* out_payload,
+                               hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(rows == 0 || block_len == 0 || (values && out_scales && out_payload),
+            "hps_compress_values: null buffer");
+    hps::compress_values(values, rows, block_len, kappa, out_scales, out_payload, S(stream));
+  });
+}
+
+hps_status hps_decompress_values(const float* scales, const uint16_t* payload, uint64_t rows,
+                                 uint32_t block_len, float* out, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(rows == 0 || block_len == 0 || (scales && payload && out),
+            "hps_decompress_values: null buffer");
+    hps::decompress_values(scales, payload, rows, block_len, out, S(stream));
+  });
+}
+
 hps_status hps_compress_indices(const uint64_t* ids, size_t n_ids, const uint32_t* offsets,
                                 uint32_t B, uint32_t G, uint64_t* group_u_off, uint64_t* unique,
                                 uint64_t* post_off, uint16_t* postings, hps_stream stream) {

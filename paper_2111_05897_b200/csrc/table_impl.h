@@ -102,6 +102,11 @@ void table_clear(Table* t, cudaStream_t st);
 void table_counters(Table* t, hps_counters* out);
 void table_sync(Table* t);
 void table_reset(Table* t);
+// codec.cu: compress_values / decompress_values (codec.hpp:222-261), one block per row
+void compress_values(const float* v, uint64_t rows, uint32_t len, float kappa, float* scales,
+                     uint16_t* payload, cudaStream_t st);
+void decompress_values(const float* scales, const uint16_t* payload, uint64_t rows, uint32_t len,
+                       float* out, cudaStream_t st);
 // checkpoint.cu: HPS1 image of logical shard `shard` (returns its size; writes it when
 // buf holds cap >= size bytes); adopt a set of images (validated first, atomically).
 uint64_t table_ckpt_save(Table* t, uint32_t shard, uint32_t shard_capacity, uint8_t* buf,

@@ -146,6 +146,8 @@ def lib():
         "hps_table_device_step": (st, [vp, C.POINTER(u32)]),
         "hps_table_advance_epoch": (u32, [vp]),
         "hps_table_reset": (st, [vp]),
+        "hps_compress_values": (st, [vp, u64, u32, f32, vp, vp, vp]),
+        "hps_decompress_values": (st, [vp, vp, u64, u32, vp, vp]),
         "hps_table_checkpoint_save": (st, [vp, u32, u32, vp, u64, C.POINTER(u64)]),
         "hps_table_checkpoint_load": (st, [vp, C.POINTER(vp), C.POINTER(u64), u32, C.c_int]),
         "hps_lookup": (st, [vp, vp, sz, vp, vp, vp]),
@@ -280,6 +282,45 @@ def dedup(ids, stream=None):
     check(lib().hps_dedup(_ptr(ids), n, _ptr(uniq), _ptr(inv), C.byref(u), _stream_ptr(stream)),
           "dedup")
     return uniq[: u.value], inv[:n]
+
+
+KAPPA = 1024.0  # kDefaultKappa codec.hpp:214
+
+
+def compress_values(values, kappa: float = KAPPA, stream=None):
+    """compress_values (codec.hpp:222-241) per row of a [rows, block_len] f32 array ->
+    (scales [rows] f32, payload [rows, block_len] u16 binary16 bits). numpy in -> numpy out;
+    a torch CUDA tensor in -> torch outputs on the device."""
+    v = _prep(values, np.float32)
+    rows, blen = (v.shape[0], int(np.prod(v.shape[1:]))) if v.ndim > 1 else (1, v.shape[0])
+    if _is_np(v):
+        scales = np.zeros(rows, np.float32)
+        payload = np.zeros((rows, blen), np.uint16)
+    else:
+        import torch
+
+        scales = torch.empty(rows, dtype=torch.float32, device=v.device)
+        payload = torch.empty((rows, blen), dtype=torch.int16, device=v.device)
+    check(lib().hps_compress_values(_ptr(v), rows, blen, kappa, _ptr(scales), _ptr(payload),
+                                    _stream_ptr(stream)), "compress_values")
+    return scales, payload
+
+
+def decompress_values(scales, payload, stream=None):
+    """decompress_values (codec.hpp:244-261) -> [rows, block_len] f32."""
+    if _is_np(payload):
+        payload = np.ascontiguousarray(payload, np.uint16)
+        scales = np.ascontiguousarray(scales, np.float32)
+        out = np.zeros(payload.shape, np.float32)
+    else:
+        import torch
+
+        out = torch.empty(payload.shape, dtype=torch.float32, device=payload.device)
+    rows = payload.shape[0]
+    blen = int(np.prod(payload.shape[1:]))
+    check(lib().hps_decompress_values(_ptr(scales), _ptr(payload), rows, blen, _ptr(out),
+                                      _stream_ptr(stream)), "decompress_values")
+    return out
 
 
 def compress_indices(ids, offsets, B: int, G: int, stream=None):
