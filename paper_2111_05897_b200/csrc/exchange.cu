@@ -328,6 +328,47 @@ __global__ void __launch_bounds__(kXBlock)
   pdl_entry();
   const uint32_t lane = threadIdx.x % L;
   const uint64_t groups = (uint64_t)gridDim.x * (kXBlock / L);
+  if constexpr (!GEN) {
+    // kEmitILP pairs in flight per lane group (metadata loads, gradient loads, then the
+    // mostly remote stores), as in the owner gather
+    constexpr int kEmitILP = 4;
+    for (uint64_t i0 = blockIdx.x * (uint64_t)(kXBlock / L) + threadIdx.x / L; i0 < n;
+         i0 += groups * kEmitILP) {
+      uint32_t sp[kEmitILP], dd[kEmitILP], gg[kEmitILP], cntg[kEmitILP];
+#pragma unroll
+      for (int u = 0; u < kEmitILP; ++u) {
+        const uint64_t i = i0 + u * groups;
+        sp[u] = i < n ? spair[i] : kNoPair;
+        dd[u] = sp[u] != kNoPair ? dest[i] : 0u;
+        gg[u] = sp[u] != kNoPair ? lgrp[i] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kEmitILP; ++u)
+        cntg[u] = (sp[u] != kNoPair && mean) ? offsets[gg[u] + 1] - offsets[gg[u]] : 1u;
+      for (uint32_t d0 = lane * V; d0 < D; d0 += L * V) {
+        float x[kEmitILP][V];
+#pragma unroll
+        for (int u = 0; u < kEmitILP; ++u) {
+          if (sp[u] != kNoPair) load_vec<V>(grads + static_cast<uint64_t>(gg[u]) * D + d0, x[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kEmitILP; ++u) {
+          if (sp[u] == kNoPair) continue;
+          const uint32_t d = dd[u];
+          const uint64_t out = base[d] + sp[u];
+          if (lane == 0 && d0 == lane * V) po.p[d][out] = sendpos[i0 + u * groups] - seg[d];
+          const double scale = mean ? 1.0 / static_cast<double>(cntg[u]) : 1.0;
+          float o[V];
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            o[v] = __double2float_rn(__dadd_rn(0.0, __dmul_rn(static_cast<double>(x[u][v]), scale)));
+          put_row<V, GEN>(po.c[d] + out * D + d0, o);
+          flag_nonfinite<V>(po, d, o);
+        }
+      }
+    }
+    return;
+  }
   for (uint64_t i = blockIdx.x * (uint64_t)(kXBlock / L) + threadIdx.x / L; i < n;
        i += groups) {
     const uint32_t sp = spair[i];
@@ -967,6 +1008,45 @@ __global__ void __launch_bounds__(256)
   const uint64_t gid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
   const uint64_t groups = static_cast<uint64_t>(gridDim.x) * blockDim.x / L;
   float* dst_base = pr.p[r] + seg * D;
+  if constexpr (!kGuard) {
+    // kGatherILP rows in flight per lane group: the slot / target loads, then the row
+    // loads, then the (mostly remote, NVLink) stores -- independent chains, so the
+    // random-row latency overlaps instead of serialising per row
+    constexpr int kGatherILP = 4;
+    for (uint64_t j0 = gid; j0 < n; j0 += groups * kGatherILP) {
+      uint32_t s[kGatherILP], g[kGatherILP];
+      bool live[kGatherILP];
+#pragma unroll
+      for (int u = 0; u < kGatherILP; ++u) {
+        const uint64_t j = j0 + u * groups;
+        live[u] = j < n;
+        s[u] = live[u] ? oslot[r * stride + j] : 0u;
+        g[u] = (live[u] && pooled.p[r]) ? tgt[r * stride + j] : 0xffffffffu;
+      }
+      float v[kGatherILP][V];
+#pragma unroll
+      for (int u = 0; u < kGatherILP; ++u) {
+        if (live[u] && slot_ok(t, s[u]))
+          load_vec<V>(t.rows + static_cast<uint64_t>(s[u]) * t.stride + ln * V, v[u]);
+        else
+          for (int k = 0; k < V; ++k) v[u][k] = 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < kGatherILP; ++u) {
+        if (!live[u]) continue;
+        const uint64_t j = j0 + u * groups;
+        // a one-listing group of the requester: its pooled value float(0.0 + (double)row),
+        // i.e. row + 0.0f, goes straight into the requester's pooled output
+        float* dst = g[u] != 0xffffffffu ? pooled.p[r] + static_cast<uint64_t>(g[u]) * D
+                                         : dst_base + j * D;
+        if (g[u] != 0xffffffffu)
+          for (int k = 0; k < V; ++k) v[u][k] = __fadd_rn(v[u][k], 0.0f);
+        store_vec<V>(dst + ln * V, v[u]);
+        if (ln == 0 && orv) orv[r * stride + j] = slot_ok(t, s[u]) ? vt_read(t, s[u]).x : 0;
+      }
+    }
+    return;
+  }
   for (uint64_t j = gid; j < n; j += groups) {
     const uint32_t s = oslot[r * stride + j];
     const bool ok = slot_ok(t, s);
