@@ -261,6 +261,21 @@ void table_clear(Table* t, cudaStream_t st) {
   HPS_CUDA(cudaMemsetAsync(d.ctr + kCtrOverflow, 0, sizeof(unsigned long long), st));
 }
 
+static void ensure_aux(Table* t) {
+  if (t->aux) return;
+  HPS_CUDA(cudaStreamCreateWithFlags(&t->aux, cudaStreamNonBlocking));
+  HPS_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
+  HPS_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
+  HPS_CUDA(cudaEventCreateWithFlags(&t->ev_sort, cudaEventDisableTiming));
+}
+
+// The batch's large-plan sort (forked by batch_register) has finished before `st` goes on.
+static void join_sort(Batch& b, cudaStream_t st) {
+  if (!b.sort_pending) return;
+  HPS_CUDA(cudaStreamWaitEvent(st, b.table->ev_sort, 0));
+  b.sort_pending = false;
+}
+
 static void forget_outstanding(Batch& b) {
   if (!b.table) return;
   auto& v = b.table->outstanding;
@@ -312,6 +327,7 @@ void table_destroy(Table* t) {
     if (t->aux) cudaStreamDestroy(t->aux);
     if (t->ev_fork) cudaEventDestroy(t->ev_fork);
     if (t->ev_join) cudaEventDestroy(t->ev_join);
+    if (t->ev_sort) cudaEventDestroy(t->ev_sort);
   }
   delete t;
 }
@@ -543,6 +559,7 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   const uint64_t BF = static_cast<uint64_t>(B) * F;
   if (BF >= 0xffffffffull) throw Error(HPS_E_PRECONDITION, "batch too large (B*F >= 2^32)");
   if (F == 0) throw Error(HPS_E_PRECONDITION, "register: feature group count must be positive");
+  join_sort(b, st);
   forget_outstanding(b);
   b.rv_valid = false;
   batch_reserve(b, N, BF, B);
@@ -608,7 +625,15 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
       radix::sort_composite_small(b.mkeys, &b.small[0], lbits, b.small_slot, b.small_listing,
                                   st);
     }
-    sort_slots(b, b.slot, true, &b.small[0], st, true);
+    // The gated large sort (a no-op unless the device count of multi listings exceeds
+    // kSmallN) needs only the slots; the pooling does not need it. It runs on the aux
+    // stream beside the pull and is joined by the pull / push (join_sort).
+    ensure_aux(t);
+    HPS_CUDA(cudaEventRecord(t->ev_fork, st));
+    HPS_CUDA(cudaStreamWaitEvent(t->aux, t->ev_fork, 0));
+    sort_slots(b, b.slot, true, &b.small[0], t->aux, true);
+    HPS_CUDA(cudaEventRecord(t->ev_sort, t->aux));
+    b.sort_pending = true;
   }
   b.registered = true;
   b.pulled = false;
@@ -633,6 +658,7 @@ void batch_pull(Batch& b, int agg, float* out_pooled, uint64_t* out_rv, cudaStre
   b.rv_valid = d_rv != nullptr;
   if (!b.pulled) t->outstanding.push_back(&b);
   b.pulled = true;
+  join_sort(b, st);  // the forward is self-contained (capturable on its own)
   stg.finish(st);
 }
 
@@ -641,6 +667,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
                 uint32_t flags, cudaStream_t st) {
   if (!b.registered) throw Error(HPS_E_STALE_SAMPLE, "push: batch not registered");
   Table* t = b.table;
+  join_sort(b, st);
   if (epoch != t->epoch) {
     // PsShard::apply_gradients epoch fence (embedding_ps.hpp:142-145): drop every
     // (sample, unique id) entry of the batch, count them.
@@ -710,11 +737,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     // Rows listed more than once (ordered chains, latency-bound, few) and rows listed
     // once are disjoint: the multi chains run on a second stream beside the single pass
     // (fork/join events; under graph capture two parallel branches).
-    if (!t->aux) {
-      HPS_CUDA(cudaStreamCreateWithFlags(&t->aux, cudaStreamNonBlocking));
-      HPS_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
-      HPS_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
-    }
+    ensure_aux(t);
     HPS_CUDA(cudaEventRecord(t->ev_fork, st));
     HPS_CUDA(cudaStreamWaitEvent(t->aux, t->ev_fork, 0));
     {
@@ -749,6 +772,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
 uint64_t batch_pairs(Batch& b) {
   if (!b.registered) return 0;
   Table* t = b.table;
+  join_sort(b, nullptr);
   HPS_CUDA(cudaMemset(t->d.ctr + kCtrScratch, 0, sizeof(unsigned long long)));
   launch_count_pairs(plan_args(b), t->d.ctr + kCtrScratch, nullptr);
   unsigned long long p = 0;

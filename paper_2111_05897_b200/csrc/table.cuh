@@ -164,6 +164,8 @@ struct Batch {
   uint32_t* sstart = nullptr;
   bool pulled = false;
   bool registered = false;
+  bool sort_pending = false;      // the plan's gated large sort runs on the table's aux
+                                  // stream beside the pooling; joined before its use
 };
 
 // Optional per-region CUDA-event timing on the launching stream (hps_profile_*).
@@ -224,7 +226,7 @@ struct Table {
   std::mutex mu;  // one call at a time per table (PsShard's per-shard lock)
   cudaStream_t side = nullptr;  // captures the bodies of conditional graph nodes
   cudaStream_t aux = nullptr;   // update_multi beside update_single
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sort = nullptr;
   Batch scratch;  // workspace for the stateless entry points
   StagePool stage;
   // Batches pulled but not yet pushed. Their read versions are only materialised
