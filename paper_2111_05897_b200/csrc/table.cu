@@ -628,12 +628,20 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     // The gated large sort (a no-op unless the device count of multi listings exceeds
     // kSmallN) needs only the slots; the pooling does not need it. It runs on the aux
     // stream beside the pull and is joined by the pull / push (join_sort).
-    ensure_aux(t);
-    HPS_CUDA(cudaEventRecord(t->ev_fork, st));
-    HPS_CUDA(cudaStreamWaitEvent(t->aux, t->ev_fork, 0));
-    sort_slots(b, b.slot, true, &b.small[0], t->aux, true);
-    HPS_CUDA(cudaEventRecord(t->ev_sort, t->aux));
-    b.sort_pending = true;
+    static const bool fork = [] {  // HPS_SORT_FORK=0: in line (A/B measurement)
+      const char* e = getenv("HPS_SORT_FORK");
+      return !(e && e[0] == '0');
+    }();
+    if (fork) {
+      ensure_aux(t);
+      HPS_CUDA(cudaEventRecord(t->ev_fork, st));
+      HPS_CUDA(cudaStreamWaitEvent(t->aux, t->ev_fork, 0));
+      sort_slots(b, b.slot, true, &b.small[0], t->aux, true);
+      HPS_CUDA(cudaEventRecord(t->ev_sort, t->aux));
+      b.sort_pending = true;
+    } else {
+      sort_slots(b, b.slot, true, &b.small[0], st, true);
+    }
   }
   b.registered = true;
   b.pulled = false;
