@@ -203,10 +203,10 @@ def workload_config(cfg, args, ref_sample=None):
 
 def run_hybrid(args, world, rank, local, dev):
     """C5: embedding lookup + dense tower (1677 -> 64 -> 32 -> 1, fp32 cuBLAS) + the
-    reference's canonical dense all-reduce + embedding update (HybridTrainer). One GPU:
-    local table, bounded staleness (default 4: the embedding stream runs up to 4 steps
-    ahead of the dense stream). N GPUs: the hash-sharded table (one batch in flight, so
-    staleness 0) and the dense gradient all-reduced every step."""
+    reference's canonical dense all-reduce + embedding update (HybridTrainer), bounded
+    staleness (default 4: the embedding stream runs up to 4 steps ahead of the dense
+    stream). One GPU: local table. N GPUs: the hash-sharded table (one exchange per batch
+    in flight) and the dense gradient all-reduced every step."""
     import torch
     import torch.distributed as dist
 
@@ -217,7 +217,7 @@ def run_hybrid(args, world, rank, local, dev):
 
     if world > 1:
         cfg = W.sharded_config(world)
-        tau = 0 if args.staleness is None else args.staleness
+        tau = W.C5_STALENESS if args.staleness is None else args.staleness
     else:
         cfg = W.CONFIGS["c5"]
         tau = W.C5_STALENESS if args.staleness is None else args.staleness
@@ -244,12 +244,13 @@ def run_hybrid(args, world, rank, local, dev):
         data.append(tuple(torch.from_numpy(a).to(dev) for a in
                           (hb.ids.view(np.int64), hb.offsets.view(np.int32), x, y)))
     sharded = None
-    if world > 1:
-        sharded = ShardedEmbeddingWorker(table, hps.MEAN, transport=args.transport,
-                                         max_ids=max(int(d[0].numel()) for d in data))
+    if world > 1:  # one hash-sharded worker (exchange arena) per batch in flight
+        sharded = [ShardedEmbeddingWorker(table, hps.MEAN, transport=args.transport,
+                                          max_ids=max(int(d[0].numel()) for d in data))
+                   for _ in range(tau + 1)]
     use_graph = not args.no_graph
     tr = HybridTrainer(table, F, W.C5_NON_ID, hidden=W.C5_HIDDEN, dense_lr=cfg.lr,
-                       embedding_lr=cfg.lr, staleness=tau, sharded_worker=sharded,
+                       embedding_lr=cfg.lr, staleness=tau, sharded_workers=sharded,
                        device_step=use_graph)
     torch.backends.cuda.matmul.allow_tf32 = False  # fp32 dense tower, as the reference
     it = 0

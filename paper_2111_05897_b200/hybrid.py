@@ -23,8 +23,11 @@ step's plan and read versions until its push (``protect_reads`` snapshots the re
 versions a later mutation would otherwise hide).
 
 Multi-GPU: the dense gradient goes through ``dense.allreduce_mean`` (the reference's
-canonical mean, bit-exact) and the embeddings through the hash-sharded worker
-(``sharded.ShardedEmbeddingWorker``), which holds one batch in flight: tau = 0 there.
+canonical mean, bit-exact) and the embeddings through hash-sharded workers
+(``sharded.ShardedEmbeddingWorker``): one per in-flight batch (tau + 1, each with its own
+exchange arena and device barriers), used round-robin like the local worker handles. The
+owners apply in the exchange's fresh mode, so the staleness delay statistics of the
+sharded path count the batch's own step only (values and versions are exact).
 """
 from __future__ import annotations
 
@@ -38,14 +41,16 @@ class HybridTrainer:
     def __init__(self, table: hps.ShardSet, groups: int, non_id_dim: int, hidden=(64, 32),
                  dense_lr: float = 0.05, embedding_lr: float = 0.05, staleness: int = 0,
                  aggregation: int = hps.MEAN, init_seed: int = 0, group=None,
-                 sharded_worker=None, device_step: bool = False):
+                 sharded_worker=None, device_step: bool = False, sharded_workers=None):
         import torch
 
         if staleness < 0:
             raise hps.ConfigError("staleness must be >= 0")
-        if sharded_worker is not None and staleness != 0:
-            raise hps.ConfigError("the sharded embedding worker holds one batch in flight: "
-                                  "staleness must be 0")
+        if sharded_worker is not None:
+            sharded_workers = [sharded_worker]
+        if sharded_workers is not None and len(sharded_workers) != staleness + 1:
+            raise hps.ConfigError("sharded training needs one embedding worker per batch in "
+                                  f"flight: {staleness + 1} for staleness {staleness}")
         self.torch = torch
         self.table = table
         self.F = groups
@@ -57,8 +62,8 @@ class HybridTrainer:
         self.group = group
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.tower = DenseTower(groups * self.D + non_id_dim, hidden, init_seed, self.device)
-        self.sharded = sharded_worker
-        self.workers = [] if sharded_worker is not None else \
+        self.sharded = sharded_workers
+        self.workers = [] if sharded_workers is not None else \
             [hps.EmbeddingWorker(table, aggregation) for _ in range(staleness + 1)]
         self.emb_stream = torch.cuda.Stream()
         self.dense_stream = torch.cuda.Stream()
@@ -93,7 +98,7 @@ class HybridTrainer:
         g = b["grads"]  # per-sample embedding gradients, [B][F][D]
         with t.cuda.stream(self.emb_stream):
             if self.sharded is not None:
-                self.sharded.apply_backward(g, self.embedding_lr, s + 1, flags=self.flags)
+                self.sharded[k].apply_backward(g, self.embedding_lr, s + 1, flags=self.flags)
             else:
                 self.workers[k].apply_backward(g, self.embedding_lr, s + 1, flags=self.flags,
                                                stream=self.emb_stream)
@@ -119,8 +124,11 @@ class HybridTrainer:
         # embedding stream: register + pull(s), then the push tau steps behind
         with t.cuda.stream(self.emb_stream):
             if self.sharded is not None:
-                self.sharded.register_batch(ids, offsets, B, self.F)
-                self.sharded.serve_pull(out_pooled=b["pooled"])
+                w = self.sharded[k]
+                w.register_batch(ids, offsets, B, self.F)
+                # zero-copy view of the exchange's pooled buffer: valid until this worker's
+                # next forward, tau + 1 steps later, after the dense step consumed it
+                b["view"] = w.serve_pull()
             else:
                 w = self.workers[k]
                 w.register_batch(ids, offsets, B, self.F, stream=self.emb_stream)
@@ -130,7 +138,8 @@ class HybridTrainer:
         with t.cuda.stream(self.dense_stream):
             self.dense_stream.wait_event(b["pulled"])
             x = b["x"]
-            x[:, :self.F * self.D].copy_(b["pooled"].view(B, -1))
+            pooled = b["view"] if self.sharded is not None else b["pooled"]
+            x[:, :self.F * self.D].copy_(pooled.reshape(B, -1))
             x[:, self.F * self.D:].copy_(non_id)
             loss, _, _ = self.tower.forward_backward(x, labels, input_grad=b["grads"].view(B, -1),
                                                      input_cols=self.F * self.D)

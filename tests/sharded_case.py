@@ -178,3 +178,112 @@ def run_world(world, backend, use_device, timeout=240, **kw):
             if p.is_alive():
                 p.kill()
     return results
+
+
+def run_hybrid_rank(rank, world, port, tau=2, D=8, B=12, F=3, nd=2, steps=6, space=60, q=None):
+    """The sharded hybrid step (HybridTrainer over tau + 1 exchanges): every rank records the
+    embedding gradients its dense tower produced; the owners' rows must equal the oracle
+    table driven with the global batches and those gradients in the staleness-tau order
+    (pull(s) before push(s - tau)), and the dense parameters must agree across ranks."""
+    try:
+        import torch
+        import torch.distributed as dist
+
+        import oracle as O
+        from paper_2111_05897_b200 import hps
+        from paper_2111_05897_b200.hybrid import HybridTrainer
+        from paper_2111_05897_b200.sharded import ShardedEmbeddingWorker
+
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        S = 8
+        salts = [O.mix64(7 + s) for s in range(S)]
+        dev = torch.device("cuda", rank)
+        table = hps.ShardSet(S, D, 1 << 14, hps.ADAGRAD, salts=salts)
+        ews = [ShardedEmbeddingWorker(table, hps.MEAN, max_ids=world * B * F * 4)
+               for _ in range(tau + 1)]
+        tr = HybridTrainer(table, F, nd, hidden=(8,), dense_lr=0.1, embedding_lr=0.2,
+                           staleness=tau, sharded_workers=ews, init_seed=3)
+        batches, my_grads = [], []
+        for s in range(steps):
+            gids, goffs, _ = global_batch(s, world, B, F, space)
+            lid, loff = local_part(gids, goffs, world, B, F, rank)
+            rng = np.random.default_rng(900 + 10 * s + rank)
+            x = (rng.random((B, nd)) * 2 - 1).astype(np.float32)
+            y = (rng.random(B) > 0.5).astype(np.float32)
+            tr.step(torch.from_numpy(lid.view(np.int64)).to(dev),
+                    torch.from_numpy(loff.astype(np.int32)).to(dev),
+                    torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev))
+            tr.sync()
+            torch.cuda.synchronize()
+            my_grads.append(tr._buf(s % (tau + 1), B)["grads"].cpu().numpy().copy())
+            batches.append((gids, goffs))
+        tr.flush()
+        torch.cuda.synchronize()
+        table.sync()
+        allg = [None] * world
+        dist.all_gather_object(allg, my_grads)
+        params = [None] * world
+        dist.all_gather_object(params, tr.tower.params.cpu().numpy().tobytes())
+        assert all(p == params[0] for p in params), "dense replicas diverged"
+        # oracle: global batch, sample i = rank i % W's local sample i // W
+        exp = O.Restatement(salts, D, "adagrad")
+        sk = np.array([((i % world) << 56) | (i // world) for i in range(world * B)], np.uint64)
+        pending = []
+        for s, (gids, goffs) in enumerate(batches):
+            _, rv = exp.pull_batch(world * B, F, gids, goffs.astype(np.uint64), "mean")
+            g = np.zeros((world * B, F, D), np.float32)
+            for r in range(world):
+                g[r::world] = allg[r][s]
+            pending.append((s, gids, goffs, g, rv))
+            if len(pending) > tau:
+                ps, pg, po, pgr, prv = pending.pop(0)
+                ok, _ = exp.push_batch(world * B, F, pg, po.astype(np.uint64), pgr, 0.2, ps + 1,
+                                       read_versions=prv, sample_keys=sk, agg="mean")
+                assert ok
+        for ps, pg, po, pgr, prv in pending:
+            exp.push_batch(world * B, F, pg, po.astype(np.uint64), pgr, 0.2, ps + 1,
+                           read_versions=prv, sample_keys=sk, agg="mean")
+        seen = set(int(i) for gids, _ in batches for i in gids)
+        mine = np.array(sorted(i for i in seen if hps.route_shard(i, S) % world == rank),
+                        np.uint64)
+        w, a, v, p = table.peek(mine)
+        we, ae, ve, pe = exp.peek(mine)
+        assert p.all() and pe.all()
+        assert w.tobytes() == we.tobytes(), f"rank {rank}: rows differ"
+        assert a.tobytes() == ae.tobytes(), f"rank {rank}: optimizer state differs"
+        assert (v == ve).all(), f"rank {rank}: versions differ"
+        dist.barrier()
+        dist.destroy_process_group()
+        if q is not None:
+            q.put((rank, "ok", len(mine)))
+    except Exception:
+        if q is not None:
+            q.put((rank, traceback.format_exc(), 0))
+        raise
+
+
+def run_hybrid_world(world, timeout=300, **kw):
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=run_hybrid_rank, args=(r, world, port), kwargs=dict(kw, q=q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = []
+    try:
+        for _ in range(world):
+            results.append(q.get(timeout=timeout))
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    return results

@@ -119,3 +119,19 @@ def test_apply_pairs_rejects_positions_outside_the_source_segment():
         ops.apply_pairs(ids, ver, [3], pos, con, [2], 0.5, 1, table.epoch(), flags=0)
     after = table.peek(np.array([11, 12, 13], np.uint64))[0]
     assert before.tobytes() == after.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,tau", [(1, 2), (2, 0), (2, 2)])
+def test_sharded_hybrid_staleness(world, tau):
+    """HybridTrainer over tau + 1 hash-sharded workers: owners' rows bit-exact vs the
+    oracle driven with the recorded embedding gradients in staleness order; the dense
+    replicas identical (canonical all-reduce)."""
+    import torch
+
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    from sharded_case import run_hybrid_world
+
+    res = run_hybrid_world(world, tau=tau)
+    assert all(r[1] == "ok" for r in res), [r[1] for r in res]
