@@ -79,6 +79,7 @@ class DenseTower:
             self.gb.append(self.grad[off:off + fo])
             off += fo
         self.param_count = off
+        self._ones = {}
 
     def forward_backward(self, x, labels, input_grad=None, input_cols: int | None = None):
         """batch_forward_backward (dense_nn.hpp:218-246): mean BCE loss of the batch.
@@ -86,15 +87,29 @@ class DenseTower:
         (mean_loss [device scalar], probs [B], input_grad [B, input_cols]). The loss
         derivative at the logit is (p - y) / B; the clamp only binds where the loss
         saturates. ``input_cols`` limits the input gradient to the leading columns (the
-        embedding slice: split_group_grads dense_nn.hpp:251-261 drops the non-id tail)."""
+        embedding slice: split_group_grads dense_nn.hpp:251-261 drops the non-id tail).
+
+        ``x`` may be a list of column blocks ([pooled embeddings, non-id features]): the
+        first layer then multiplies each block by its slice of W0 (no concatenated copy of
+        the input), and its weight gradient is assembled from the blocks' products."""
         t = self.torch
-        B = x.shape[0]
+        parts = list(x) if isinstance(x, (list, tuple)) else [x]
+        B = parts[0].shape[0]
         if B == 0:
             raise PreconditionError("batch_forward_backward: empty batch")
+        widths = [p_.shape[1] for p_ in parts]
         L = len(self.W)
-        acts, pre = [x], []
-        h = x
-        for l in range(L):
+        pre, acts = [], [None]
+        # layer 0 over the column blocks
+        z = t.addmm(self.b[0], parts[0], self.W[0][:, :widths[0]].t())
+        c0 = widths[0]
+        for p_, w_ in zip(parts[1:], widths[1:]):
+            z.addmm_(p_, self.W[0][:, c0:c0 + w_].t())
+            c0 += w_
+        pre.append(z)
+        h = t.relu(z) if L > 1 else z
+        acts.append(h)
+        for l in range(1, L):
             z = t.addmm(self.b[l], h, self.W[l].t())
             pre.append(z)
             h = t.relu(z) if l + 1 < L else z
@@ -106,16 +121,55 @@ class DenseTower:
         mean_loss = loss.sum() * (1.0 / B)
         delta = ((prob - labels) * (1.0 / B)).unsqueeze(1)
         for l in range(L - 1, -1, -1):
-            t.mm(delta.t(), acts[l], out=self.gW[l])
+            if l == 0:
+                if len(parts) == 1:
+                    self._weight_grad(delta, parts[0], self.gW[0])
+                else:
+                    c0 = 0
+                    for p_, w_ in zip(parts, widths):
+                        blk = t.empty((delta.shape[1], w_), dtype=delta.dtype,
+                                      device=delta.device)
+                        self._weight_grad(delta, p_, blk)
+                        self.gW[0][:, c0:c0 + w_].copy_(blk)
+                        c0 += w_
+            else:
+                self._weight_grad(delta, acts[l], self.gW[l])
             t.sum(delta, 0, out=self.gb[l])
             if l == 0:
-                cols = x.shape[1] if input_cols is None else input_cols
+                cols = sum(widths) if input_cols is None else input_cols
                 if input_grad is None:
-                    input_grad = t.empty((B, cols), dtype=x.dtype, device=x.device)
+                    input_grad = t.empty((B, cols), dtype=delta.dtype, device=delta.device)
                 t.mm(delta, self.W[0][:, :cols], out=input_grad)
                 break
             delta = t.mm(delta, self.W[l]).mul_(pre[l - 1] > 0)
         return mean_loss, prob, input_grad
+
+    def _weight_grad(self, delta, a, out):
+        """out = delta^T a, a reduction over the batch (K = B) into a small [out, in]
+        matrix: a plain GEMM gets only a handful of output tiles (64 x 1677 -> 27 CTAs
+        for 148 SMs), so the batch is split into chunks reduced as one batched GEMM and
+        their partial products summed (split-K; fp32 throughout)."""
+        t = self.torch
+        B = delta.shape[0]
+        c = 1
+        for cand in (16, 8, 4, 2):
+            if B % cand == 0 and B // cand >= 512:
+                c = cand
+                break
+        if c == 1:
+            t.mm(delta.t(), a, out=out)
+            return
+        part = t.bmm(delta.view(c, B // c, -1).transpose(1, 2), a.view(c, B // c, -1))
+        # sum of the c partial products as a GEMM with a ones row (a strided reduction
+        # over the leading dimension is slower)
+        key = (c, part.dtype, part.device)
+        ones = self._ones.get(key)
+        if ones is None:
+            ones = self._ones[key] = t.ones((1, c), dtype=part.dtype, device=part.device)
+        if out.is_contiguous():
+            t.mm(ones, part.view(c, -1), out=out.view(1, -1))
+        else:
+            out.copy_(t.mm(ones, part.view(c, -1)).view_as(out))
 
     def sgd_step(self, grad, lr: float, finite=None):
         """sgd_step (dense_nn.hpp:263-273): p -= lr * g (both ops rounded). Non-finite

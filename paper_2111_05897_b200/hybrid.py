@@ -81,8 +81,6 @@ class HybridTrainer:
             t = self.torch
             self._bufs[key] = dict(
                 pooled=t.empty((B, self.F, self.D), dtype=t.float32, device=self.device),
-                x=t.empty((B, self.F * self.D + self.non_id_dim), dtype=t.float32,
-                          device=self.device),
                 grads=t.empty((B, self.F, self.D), dtype=t.float32, device=self.device),
                 pulled=t.cuda.Event(), graded=t.cuda.Event())
         return self._bufs[key]
@@ -137,12 +135,11 @@ class HybridTrainer:
         # dense stream: forward/backward, synchronous dense all-reduce, SGD
         with t.cuda.stream(self.dense_stream):
             self.dense_stream.wait_event(b["pulled"])
-            x = b["x"]
             pooled = b["view"] if self.sharded is not None else b["pooled"]
-            x[:, :self.F * self.D].copy_(pooled.reshape(B, -1))
-            x[:, self.F * self.D:].copy_(non_id)
-            loss, _, _ = self.tower.forward_backward(x, labels, input_grad=b["grads"].view(B, -1),
-                                                     input_cols=self.F * self.D)
+            # the dense input [pooled | non-id] as two column blocks (no concatenated copy)
+            loss, _, _ = self.tower.forward_backward(
+                [pooled.reshape(B, -1), non_id], labels, input_grad=b["grads"].view(B, -1),
+                input_cols=self.F * self.D)
             g = allreduce_mean(self.tower.grad, self.group)
             finite = t.isfinite(g).all()
             self.tower.sgd_step(g, self.dense_lr, finite=finite)

@@ -48,6 +48,14 @@ def test_dense_forward_backward_matches_reference(B):
     _, _, ig2 = t.forward_backward(torch.from_numpy(x), torch.from_numpy(y), input_cols=24)
     assert ig2.shape == (B, 24)
     np.testing.assert_allclose(ig2.numpy(), ig.numpy()[:, :24], rtol=FWD_RTOL, atol=1e-8)
+    # the input as column blocks [embeddings | non-id] (the hybrid trainer's form)
+    t3 = dense.DenseTower(40, (16, 8), 3, device="cpu")
+    l3, p3, ig3 = t3.forward_backward([torch.from_numpy(x[:, :24].copy()),
+                                       torch.from_numpy(x[:, 24:].copy())],
+                                      torch.from_numpy(y), input_cols=24)
+    np.testing.assert_allclose(float(l3), rl, rtol=FWD_RTOL)
+    np.testing.assert_allclose(t3.grad.numpy(), rg, rtol=FWD_RTOL, atol=1e-7)
+    np.testing.assert_allclose(ig3.numpy(), rig[:, :24], rtol=FWD_RTOL, atol=1e-8)
 
 
 @pytest.mark.parametrize("K", [1, 2, 3, 5, 8])
