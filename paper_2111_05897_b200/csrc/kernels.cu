@@ -502,8 +502,10 @@ __global__ void __launch_bounds__(256, 6)
       const uint32_t d0 = c * G::kSpan + ln * V;
 #pragma unroll
       for (int u = 0; u < kCheckILP; ++u) {
+        // issued without waiting for the group sizes (an empty group's row is read and
+        // ignored below): the gradient stream does not serialise behind the offsets
         const uint64_t r = r0 + u * groups;
-        if (n[u] && (!kGuard || d0 < D)) load_vec_cs<V>(grads + r * D + d0, x[u]);
+        if (r < rows && (!kGuard || d0 < D)) load_vec_cs<V>(grads + r * D + d0, x[u]);
         else for (int j = 0; j < V; ++j) x[u][j] = 0.0f;
       }
       if (write_c) {
