@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--soak-seconds", type=float, default=2.0)
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
+    p.add_argument("--no-pipeline", action="store_true",
+                   help="C2: register each batch in line instead of beside the previous push")
     p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                    help="N > 1: NVLink peer writes (p2p) or NCCL all-to-alls")
     return p.parse_args()
@@ -646,23 +648,58 @@ def main():
     torch.cuda.synchronize()
     table.sync()
 
-    # One CUDA graph per input batch: the whole step (register + pull + push, ~16
-    # kernels) replays without host launch overhead.
+    # Pipelined sync steps (default): the next batch's register (probe, plan, sorts --
+    # latency-bound, no row data) runs on a second stream beside this batch's pull and
+    # push, like the reference's register_sample buffering upcoming samples while the
+    # current step trains; every pull still follows the previous push (exact sync
+    # semantics: the next pull is issued after this push on the main stream). Two
+    # embedding-worker handles alternate; each batch has its own plan bitmaps.
+    pipe = not args.no_pipeline and M % 2 == 0
+    ews = [hps.EmbeddingWorker(table, agg) for _ in range(2)] if pipe else []
+    side = torch.cuda.Stream() if pipe else None
+
+    def pipe_step(i, s):
+        nxt = i + 1
+        side.wait_stream(s)
+        ids1, offs1, _ = batches[nxt % M]
+        ews[nxt % 2].register_batch(ids1, offs1, B, F, stream=side)
+        w = ews[i % 2]
+        w.serve_pull(out_pooled=pooled, stream=s)
+        w.apply_backward(grads[i % M], cfg.lr, flags=hps.ASYNC | hps.DEVICE_STEP, stream=s)
+        s.wait_stream(side)
+
+    if pipe:
+        ids0, offs0, _ = batches[it % M]
+        ews[it % 2].register_batch(ids0, offs0, B, F, stream=stream)
+        for _ in range(2):
+            pipe_step(it, stream)
+            it += 1
+        torch.cuda.synchronize()
+        table.sync()
+
+    # One CUDA graph per input batch: the whole step (~20 kernels) replays without host
+    # launch overhead.
     graphs, graph_launches = [], []
+    it_g = it
     if not args.no_graph:
         cap = torch.cuda.Stream()
         for m in range(M):
             g = torch.cuda.CUDAGraph()
             l0 = hps.launch_count()
             with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
-                eager_step(m, torch.cuda.current_stream())
+                if pipe:
+                    pipe_step(it_g + m, torch.cuda.current_stream())
+                else:
+                    eager_step(m, torch.cuda.current_stream())
             graph_launches.append(hps.launch_count() - l0)
             graphs.append(g)
         torch.cuda.synchronize()
 
     def step(i):
         if graphs:
-            graphs[i % M].replay()
+            graphs[(i - it_g) % M if pipe else i % M].replay()
+        elif pipe:
+            pipe_step(i, stream)
         else:
             eager_step(i)
 
@@ -692,7 +729,8 @@ def main():
     barrier()
     launches = hps.launch_count() - l0
     if graphs:  # replays do not pass through the host launch counter
-        launches = sum(graph_launches[i % M] for i in range(it - args.steps, it))
+        launches = sum(graph_launches[((i - it_g) if pipe else i) % M]
+                       for i in range(it - args.steps, it))
     ms = e0.elapsed_time(e1) / args.steps
     # soak: keep the same step running so the clock sampler sees >= soak-seconds under load
     t_soak = time.perf_counter()
@@ -803,7 +841,10 @@ def main():
             "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32 (fp64 pooling/fan-out)", "data": "synthetic",
-            "config": workload_config(cfg, args),
+            "config": dict(workload_config(cfg, args),
+                           schedule=("sync steps; each batch registered (probe + plan) beside "
+                                     "the previous batch's push, its pull after that push"
+                                     if pipe else "sync steps, in line")),
             "hbm": {"algorithmic_bytes_per_step": bytes_step,
                     "achieved_gbs": bytes_step / (ms * 1e-3) / 1e9,
                     "frac_of_peak": bytes_step / (ms * 1e-3) / 1e9 / peak,

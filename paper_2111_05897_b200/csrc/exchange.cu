@@ -1271,7 +1271,7 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
       mine, reinterpret_cast<const uint32_t*>(x.arena + x.off_ocnt), x.G, M,
       reinterpret_cast<const uint64_t*>(x.arena + x.off_oids), nullptr,
       reinterpret_cast<const uint32_t*>(x.arena + x.off_ppos), cap, xs.ids, xs.rv, xs.off,
-      t->d.ctr + kCtrProtocol, t->d, reinterpret_cast<const uint32_t*>(x.arena + x.off_oslot),
+      t->d.ctr + kCtrProtocol, batch_plan_view(b), reinterpret_cast<const uint32_t*>(x.arena + x.off_oslot),
       b.slot, x.dev_epoch);
   HPS_LAUNCH_CHECK();
   batch_register(b, xs.ids, cap, xs.off, static_cast<uint32_t>(cap), 1, nullptr, st, true,

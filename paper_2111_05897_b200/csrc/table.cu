@@ -270,10 +270,29 @@ static void ensure_aux(Table* t) {
 }
 
 // The batch's large-plan sort (forked by batch_register) has finished before `st` goes on.
+// Nothing to wait for when a later push already joined the aux stream's work (which
+// includes this sort) into `st` -- e.g. the next batch registered beside this push.
 static void join_sort(Batch& b, cudaStream_t st) {
   if (!b.sort_pending) return;
-  HPS_CUDA(cudaStreamWaitEvent(st, b.table->ev_sort, 0));
+  Table* t = b.table;
   b.sort_pending = false;
+  if (t->aux_joined == st && t->aux_joined_seq >= b.sort_seq) return;
+  HPS_CUDA(cudaStreamWaitEvent(st, t->ev_sort, 0));
+}
+
+DevTable batch_plan_view(Batch& b) {
+  Table* t = b.table;
+  if (!b.seen) {
+    const size_t words = t->d.capacity / 32 + 1;
+    HPS_CUDA(cudaMalloc(&b.seen, words * sizeof(uint32_t)));
+    HPS_CUDA(cudaMalloc(&b.multi, words * sizeof(uint32_t)));
+    HPS_CUDA(cudaMemset(b.seen, 0, words * sizeof(uint32_t)));
+    HPS_CUDA(cudaMemset(b.multi, 0, words * sizeof(uint32_t)));
+  }
+  DevTable d = t->d;
+  d.seen = b.seen;
+  d.multi = b.multi;
+  return d;
 }
 
 static void forget_outstanding(Batch& b) {
@@ -296,6 +315,9 @@ static void protect_reads(Table* t, const Batch* except, cudaStream_t st) {
 
 void batch_free(Batch& b) {
   forget_outstanding(b);
+  if (b.seen) cudaFree(b.seen);
+  if (b.multi) cudaFree(b.multi);
+  b.seen = b.multi = nullptr;
   void* ptrs[] = {b.offsets, b.lgrp,  b.slot,   b.keys_a,  b.vals_a,
                   b.keys_b,  b.vals_b, b.rv,  b.new_slots, b.kind,  b.hist,
                   b.mkeys,   b.hot, b.mlist, b.meta, b.inv, b.cbuf, b.small_slot, b.small_listing,
@@ -563,6 +585,7 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   forget_outstanding(b);
   b.rv_valid = false;
   batch_reserve(b, N, BF, B);
+  const DevTable pv = batch_plan_view(b);
   Stager stg(t->stage);
   const uint64_t* d_ids =
       slots_ready ? nullptr : static_cast<const uint64_t*>(stg.in(ids, N * sizeof(uint64_t), st));
@@ -594,7 +617,7 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     {
       ProfScope p(t, "probe", st);
       // dynamic: N is only a bound; the live listing count is offsets[B*F] on the device
-      launch_probe(t->d, d_ids, N, b.slot, nullptr, nullptr, b.new_slots, &b.small[2],
+      launch_probe(pv, d_ids, N, b.slot, nullptr, nullptr, b.new_slots, &b.small[2],
                    !permute, st, dynamic ? b.offsets + BF : nullptr);
     }
     launch_lazy_init(t->d, b.new_slots, &b.small[2], N, t->sm_count, st);
@@ -617,7 +640,7 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     const int lbits = std::max(1, bits_for(N ? N - 1 : 0));
     {
       ProfScope p(t, "plan", st);
-      launch_classify(t->d, b.slot, N, lbits, b.kind, b.mkeys, &b.small[0], t->sm_count, st,
+      launch_classify(pv, b.slot, N, lbits, b.kind, b.mkeys, &b.small[0], t->sm_count, st,
                       b.n_live);
     }
     {
@@ -639,6 +662,7 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
       sort_slots(b, b.slot, true, &b.small[0], t->aux, true);
       HPS_CUDA(cudaEventRecord(t->ev_sort, t->aux));
       b.sort_pending = true;
+      b.sort_seq = ++t->aux_seq;
     } else {
       sort_slots(b, b.slot, true, &b.small[0], st, true);
     }
@@ -703,6 +727,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
                        b.all_multi ? nullptr : &b.small[0], b.n_live, prechecked);
   }
   UpdateArgs a = plan_args(b);
+  const DevTable pv = batch_plan_view(b);
   a.mean = mean;
   a.grads = d_g;
   a.lr = lr;
@@ -722,8 +747,8 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   if (!prechecked) {
     a.dry_run = 1;
     run_if(t->side, st, t->d.ctr + kCtrNeedExact, true, 0, [&](cudaStream_t s) {
-      if (!b.all_multi) launch_update_single(t->d, a, t->sm_count, s);
-      launch_update(t->d, a, false, t->sm_count, s);
+      if (!b.all_multi) launch_update_single(pv, a, t->sm_count, s);
+      launch_update(pv, a, false, t->sm_count, s);
     });
     a.dry_run = 0;
   }
@@ -751,20 +776,23 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     {
       ProfScope p(t, "update_multi", t->aux);
       launch_runs(a, t->sm_count, t->aux);
-      launch_update(t->d, a, false, t->sm_count, t->aux);
-      launch_update_hot(t->d, a, t->sm_count, t->aux);
+      launch_update(pv, a, false, t->sm_count, t->aux);
+      launch_update_hot(pv, a, t->sm_count, t->aux);
     }
     {
       ProfScope p(t, "update", st);
-      launch_update_single(t->d, a, t->sm_count, st);
+      launch_update_single(pv, a, t->sm_count, st);
     }
     HPS_CUDA(cudaEventRecord(t->ev_join, t->aux));
     HPS_CUDA(cudaStreamWaitEvent(st, t->ev_join, 0));
+    // every aux fork so far (this push's and earlier registers' sorts) is now in `st`
+    t->aux_joined_seq = ++t->aux_seq;
+    t->aux_joined = st;
   } else {
     ProfScope p(t, "update_multi", st);
     launch_runs(a, t->sm_count, st);
-    launch_update(t->d, a, false, t->sm_count, st);
-    launch_update_hot(t->d, a, t->sm_count, st);
+    launch_update(pv, a, false, t->sm_count, st);
+    launch_update_hot(pv, a, t->sm_count, st);
   }
   if (flags & HPS_DEVICE_STEP) launch_add_counter_const(t->d.ctr, kCtrStep, 1, st);
   forget_outstanding(b);

@@ -166,6 +166,11 @@ struct Batch {
   bool registered = false;
   bool sort_pending = false;      // the plan's gated large sort runs on the table's aux
                                   // stream beside the pooling; joined before its use
+  uint64_t sort_seq = 0;          // its position in the aux stream's work (Table::aux_seq)
+  // Per-batch plan bitmaps (1 bit per slot: listed / listed more than once), so the plan
+  // of the next batch can be built while this batch's update runs.
+  uint32_t* seen = nullptr;
+  uint32_t* multi = nullptr;
 };
 
 // Optional per-region CUDA-event timing on the launching stream (hps_profile_*).
@@ -227,6 +232,10 @@ struct Table {
   cudaStream_t side = nullptr;  // captures the bodies of conditional graph nodes
   cudaStream_t aux = nullptr;   // update_multi beside update_single
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sort = nullptr;
+  // aux-stream bookkeeping: forks so far, and the newest fork some push already joined
+  // back into stream `aux_joined` (later work there needs no further join)
+  uint64_t aux_seq = 0, aux_joined_seq = 0;
+  cudaStream_t aux_joined = nullptr;
   Batch scratch;  // workspace for the stateless entry points
   StagePool stage;
   // Batches pulled but not yet pushed. Their read versions are only materialised

@@ -119,6 +119,8 @@ void profile_get(Table* t, const char* name, double* ms, uint64_t* count);
 void check_flags(Table* t, cudaStream_t st, bool divergence = true);
 
 void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B);
+// The table view a batch's plan kernels use: the table with the batch's own plan bitmaps.
+DevTable batch_plan_view(Batch& b);
 void batch_free(Batch& b);
 // dynamic: N and B are bounds; offsets (device) end at the live count (offsets[B*F]),
 // samples past it are empty -- a batch whose size is only known on the device.

@@ -697,3 +697,85 @@ def test_stale_multi_bits_from_unapplied_batch(hps):
     np.testing.assert_array_equal(w, wo)
     np.testing.assert_array_equal(a, ao)
     np.testing.assert_array_equal(v, vo)
+
+
+def _pipelined_case(hps, B, F, D, space, steps, graph, seed=41):
+    """bench.py's pipelined sync schedule: batch s+1 is registered on a second stream
+    beside batch s's pull + push (two worker handles alternating, each with its own plan
+    bitmaps), and pull(s+1) follows push(s) on the main stream. Pooled outputs and the
+    final rows must equal the oracle stepping in plain sync order."""
+    import torch
+
+    import oracle as O
+    from paper_2111_05897_b200 import workloads as W
+
+    rng = np.random.default_rng(seed)
+    salts = [W.mix64_int(5 + s) for s in range(4)]
+    orc = O.Restatement(salts, D, "adagrad")
+    t = hps.ShardSet(4, D, 1 << 16, hps.ADAGRAD, salts=salts)
+    ews = [hps.EmbeddingWorker(t, hps.MEAN) for _ in range(2)]
+    dev = torch.device("cuda:0")
+    main = torch.cuda.Stream()
+    side = torch.cuda.Stream()
+    offs = (np.arange(B * F + 1, dtype=np.uint32) * 2)  # two listings per group
+    N = int(offs[-1])
+    data = []
+    for _ in range(steps + 1):
+        ids = rng.integers(0, space, N).astype(np.uint64)
+        g = (rng.standard_normal((B, F, D)) * 0.2).astype(np.float32)
+        data.append((ids, g))
+    # device copies (one buffer per batch: the pipeline keeps two batches in flight)
+    d_ids = [torch.from_numpy(x[0].view(np.int64)).to(dev) for x in data]
+    d_g = [torch.from_numpy(x[1]).to(dev) for x in data]
+    offs_t = torch.from_numpy(offs.view(np.int32)).to(dev)
+    pooled = [torch.zeros((B, F, D), dtype=torch.float32, device=dev) for _ in range(steps)]
+
+    def pipe_step(i, s):
+        side.wait_stream(s)
+        if i + 1 < len(data):
+            ews[(i + 1) % 2].register_batch(d_ids[i + 1], offs_t, B, F, stream=side)
+        ews[i % 2].serve_pull(out_pooled=pooled[i], stream=s)
+        ews[i % 2].apply_backward(d_g[i], 0.05, flags=hps.ASYNC | hps.DEVICE_STEP, stream=s)
+        s.wait_stream(side)
+
+    torch.cuda.synchronize()
+    with torch.cuda.stream(main):
+        ews[0].register_batch(d_ids[0], offs_t, B, F, stream=main)
+        for i in range(steps):
+            if graph and i >= 1:
+                g_ = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g_, stream=main, capture_error_mode="thread_local"):
+                    pipe_step(i, main)
+                g_.replay()
+                main.synchronize()
+            else:
+                pipe_step(i, main)
+    torch.cuda.synchronize()
+    t.sync()
+    for i in range(steps):
+        ids, g = data[i]
+        po, rvo = orc.pull_batch(B, F, ids, offs.astype(np.uint64), "mean")
+        assert pooled[i].cpu().numpy().tobytes() == po.tobytes(), f"step {i}: pooled differs"
+        orc.push_batch(B, F, ids, offs.astype(np.uint64), g, 0.05, i + 1, read_versions=rvo,
+                       agg="mean")
+    keys = np.arange(space, dtype=np.uint64)
+    w, a, v, p = t.peek(keys)
+    wo, ao, vo, po_ = orc.peek(keys)
+    # the last registered batch (steps) inserted rows the oracle never pulled: compare
+    # the rows both hold
+    both = p & po_
+    np.testing.assert_array_equal(w[both], wo[both])
+    np.testing.assert_array_equal(a[both], ao[both])
+    np.testing.assert_array_equal(v[both], vo[both])
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_pipelined_register_beside_push(hps, graph):
+    _pipelined_case(hps, 64, 4, 16, 300, steps=6, graph=graph)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_pipelined_register_beside_push_large_plan(hps, graph):
+    """> 4096 listings of repeated rows: the forked large sort of the next batch runs
+    while this batch's update chains run on the same aux stream."""
+    _pipelined_case(hps, 1024, 4, 64, 1500, steps=4, graph=graph)
