@@ -422,16 +422,49 @@ def run_sharded(args, world, rank, local, dev):
         it += 1
     torch.cuda.synchronize()
     table.sync()
+    # Pipelined sync steps (p2p, default): two exchanges alternate; the next batch's
+    # routing + pair plan (phase 1 of its forward: no barrier, no table access) runs on
+    # a second stream beside this batch's owner lookup, pull and backward.
+    pipe = p2p and not args.no_pipeline and M % 2 == 0
+    ews = [ew, ShardedEmbeddingWorker(table, hps.MEAN, transport=args.transport,
+                                      max_ids=max_n)] if pipe else []
+    side = torch.cuda.Stream() if pipe else None
+
+    def pipe_step(i):
+        cur = torch.cuda.current_stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            ids1, offs1, _ = batches[(i + 1) % M]
+            ews[(i + 1) % 2].prefetch(ids1, offs1, B, F)
+        w = ews[i % 2]
+        w.register_prefetched()
+        w.serve_pull(out_pooled=None)
+        tag[0] += 1
+        w.apply_backward(grads[i % M], cfg.lr, tag[0], flags=hps.ASYNC | hps.DEVICE_STEP)
+        cur.wait_stream(side)
+
+    if pipe:
+        ids0, offs0, _ = batches[it % M]
+        ews[it % 2].prefetch(ids0, offs0, B, F)
+        for _ in range(2):
+            pipe_step(it)
+            it += 1
+        torch.cuda.synchronize()
+        table.sync()
     # p2p: the whole sharded step (route, peer writes, device barriers, owner apply) is
     # stream-ordered without host round trips -> one CUDA graph per input batch.
     graphs, graph_launches = [], []
+    it_g = it
     if p2p and not args.no_graph:
         cs = torch.cuda.Stream()
         for m in range(M):
             g = torch.cuda.CUDAGraph()
             l0 = hps.launch_count()
             with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
-                eager_step(m)
+                if pipe:
+                    pipe_step(it_g + m)
+                else:
+                    eager_step(m)
             graph_launches.append(hps.launch_count() - l0)
             graphs.append(g)
         torch.cuda.synchronize()
@@ -439,7 +472,9 @@ def run_sharded(args, world, rank, local, dev):
 
     def step(i):
         if graphs:
-            graphs[i % M].replay()
+            graphs[(i - it_g) % M if pipe else i % M].replay()
+        elif pipe:
+            pipe_step(i)
         else:
             eager_step(i)
 
@@ -468,7 +503,8 @@ def run_sharded(args, world, rank, local, dev):
     torch.cuda.synchronize()
     launches = hps.launch_count() - l0
     if graphs:
-        launches = sum(graph_launches[i % M] for i in range(it - args.steps, it))
+        launches = sum(graph_launches[((i - it_g) if pipe else i) % M]
+                       for i in range(it - args.steps, it))
     ms = e0.elapsed_time(e1) / args.steps
     t_soak = time.perf_counter()
     while time.perf_counter() - t_soak < args.soak_seconds:

@@ -432,6 +432,28 @@ hps_status hps_exchange_forward(hps_exchange* x, hps_table* t, const uint64_t* i
   });
 }
 
+hps_status hps_exchange_prefetch(hps_exchange* x, hps_table* t, const uint64_t* ids, size_t n_ids,
+                                 const uint32_t* offsets, uint32_t B, uint32_t F,
+                                 hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(x && t && offsets && (ids || n_ids == 0), "hps_exchange_prefetch: null argument");
+    std::lock_guard<std::mutex> g(x->mu);
+    std::lock_guard<std::mutex> g2(t->impl->mu);
+    hps::DeviceGuard dg(x->impl.device);
+    hps::xbatch_prefetch(x->impl, t->impl, ids, n_ids, offsets, B, F, S(stream));
+  });
+}
+
+hps_status hps_exchange_forward_prefetched(hps_exchange* x, hps_table* t, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(x && t, "hps_exchange_forward_prefetched: null argument");
+    std::lock_guard<std::mutex> g(x->mu);
+    std::lock_guard<std::mutex> g2(t->impl->mu);
+    hps::DeviceGuard dg(x->impl.device);
+    hps::xbatch_fwd_prefetched(x->impl, t->impl, S(stream));
+  });
+}
+
 hps_status hps_exchange_backward(hps_exchange* x, hps_table* t, const float* grads, float lr,
                                  uint32_t step_tag, uint32_t epoch, int* accepted,
                                  uint32_t flags, hps_stream stream) {

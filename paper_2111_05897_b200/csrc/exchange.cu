@@ -1144,8 +1144,13 @@ static void require_connected(const XBatch& x, uint32_t D, uint64_t n) {
   if (n > x.max_ids) throw Error(HPS_E_PRECONDITION, "exchange: batch exceeds the arena size");
 }
 
-void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint32_t* offsets,
-                uint32_t B, uint32_t F, cudaStream_t st) {
+// Forward, phase 1 (no barrier, no table access): route the batch -- distinct ids straight
+// into their owners' id regions, counts into their headers -- and plan the backward's
+// pairs. fork_pairs: the pair plan on the exchange's aux stream (joined by phase 2),
+// else on `st` itself (a prefetch stream already beside the critical path).
+static void fwd_route_phase(XBatch& x, Table* t, const uint64_t* ids, uint64_t n,
+                            const uint32_t* offsets, uint32_t B, uint32_t F, cudaStream_t st,
+                            bool fork_pairs) {
   require_connected(x, t->cfg.embedding_dim, n);
   const uint64_t M = x.max_ids;
   PeerIds pid{};
@@ -1168,7 +1173,12 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
   // delivery (latency-bound sorts overlapping an NVLink-bound gather), joined before the
   // forward returns.
   x.pairs_ready = false;
-  if (n) {
+  x.pairs_forked = false;
+  if (n && !fork_pairs) {
+    ProfScope p(t, "x_pairs", st);
+    pairs_core(x, &x.pairs_spos, &x.pairs_slist, st);
+    x.pairs_ready = true;
+  } else if (n) {
     if (!x.aux) {
       HPS_CUDA(cudaStreamCreateWithFlags(&x.aux, cudaStreamNonBlocking));
       HPS_CUDA(cudaEventCreateWithFlags(&x.ev_fork, cudaEventDisableTiming));
@@ -1182,7 +1192,16 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
     }
     HPS_CUDA(cudaEventRecord(x.ev_join, x.aux));
     x.pairs_ready = true;
+    x.pairs_forked = true;
   }
+}
+
+// Forward, phase 2: the first barrier (ids and counts landed), owner lookup of what every
+// source asked for, rows (and one-listing groups' pooled values) straight back to the
+// sources, the pair counts, the second barrier.
+static void fwd_finish_phase(XBatch& x, Table* t, cudaStream_t st) {
+  const uint64_t M = x.max_ids;
+  const PeerHdrs ph = peer_hdrs(x);
   barrier(x, t, st);  // every id region and count has landed
   // owner: find-or-init the ids every source asked for, rows straight back to them
   XHdr* mine = ph.h[x.rank];
@@ -1220,12 +1239,33 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
   // this barrier instead of one of their own. (Safe against the next step: a source
   // writes step s+1's counts only after the first barrier of s+1, which every owner
   // reaches after its step-s apply has read them.)
-  if (x.pairs_ready) HPS_CUDA(cudaStreamWaitEvent(st, x.ev_join, 0));
-  else HPS_CUDA(cudaMemsetAsync(x.pair_off, 0, 33 * sizeof(uint64_t), st));
+  if (x.pairs_ready && x.pairs_forked) HPS_CUDA(cudaStreamWaitEvent(st, x.ev_join, 0));
+  else if (!x.pairs_ready) HPS_CUDA(cudaMemsetAsync(x.pair_off, 0, 33 * sizeof(uint64_t), st));
   launch(x_bwd_hdr_kernel, 1, 32, 0, st, ph, x.G, x.rank, x.pair_off);
   HPS_LAUNCH_CHECK();
   x.counts_sent = true;
   barrier(x, t, st);  // every owner's rows have landed in this rank's rows buffer
+}
+
+void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint32_t* offsets,
+                uint32_t B, uint32_t F, cudaStream_t st) {
+  require_connected(x, t->cfg.embedding_dim, n);
+  x.prefetched = false;
+  fwd_route_phase(x, t, ids, n, offsets, B, F, st, /*fork_pairs=*/true);
+  fwd_finish_phase(x, t, st);
+}
+
+void xbatch_prefetch(XBatch& x, Table* t, const uint64_t* ids, uint64_t n,
+                     const uint32_t* offsets, uint32_t B, uint32_t F, cudaStream_t st) {
+  require_connected(x, t->cfg.embedding_dim, n);
+  fwd_route_phase(x, t, ids, n, offsets, B, F, st, /*fork_pairs=*/false);
+  x.prefetched = true;
+}
+
+void xbatch_fwd_prefetched(XBatch& x, Table* t, cudaStream_t st) {
+  if (!x.prefetched) throw Error(HPS_E_PRECONDITION, "exchange: no prefetched batch");
+  x.prefetched = false;
+  fwd_finish_phase(x, t, st);
 }
 
 void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step_tag,

@@ -202,6 +202,8 @@ struct XBatch {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool pairs_ready = false;
   bool counts_sent = false;  // the forward delivered this batch's pair counts
+  bool pairs_forked = false; // the pair plan ran on `aux` (phase 2 joins it)
+  bool prefetched = false;   // phase 1 of the next forward done (hps_exchange_prefetch)
   const uint32_t *pairs_spos = nullptr, *pairs_slist = nullptr;
   uint64_t max_ids = 0;
   uint32_t arena_dim = 0, rank = 0;
@@ -223,6 +225,11 @@ void xbatch_arena(XBatch& x, uint64_t max_ids, uint64_t max_groups, uint32_t D, 
 void xbatch_connect(XBatch& x, uint32_t rank, const void* handles);
 void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint32_t* offsets,
                 uint32_t B, uint32_t F, cudaStream_t st);
+// the forward in two phases: route + pair plan (no barrier: may run on a stream beside
+// the previous batch's backward), then the rest (after that backward on the same rank)
+void xbatch_prefetch(XBatch& x, Table* t, const uint64_t* ids, uint64_t n,
+                     const uint32_t* offsets, uint32_t B, uint32_t F, cudaStream_t st);
+void xbatch_fwd_prefetched(XBatch& x, Table* t, cudaStream_t st);
 void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step_tag,
                 uint32_t epoch, int* accepted, uint32_t flags, cudaStream_t st);
 void table_apply_pairs(Table* t, const uint64_t* recv_ids, const uint64_t* recv_versions,

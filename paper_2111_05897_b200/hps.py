@@ -177,6 +177,8 @@ def lib():
         "hps_exchange_pooled": (st, [vp, C.POINTER(vp)]),
         "hps_exchange_connect": (st, [vp, u32, vp]),
         "hps_exchange_forward": (st, [vp, vp, vp, sz, vp, u32, u32, vp]),
+        "hps_exchange_prefetch": (st, [vp, vp, vp, sz, vp, u32, u32, vp]),
+        "hps_exchange_forward_prefetched": (st, [vp, vp, vp]),
         "hps_exchange_backward": (st, [vp, vp, vp, f32, u32, u32, C.POINTER(C.c_int), u32, vp]),
         "hps_table_apply_pairs": (st, [vp, vp, vp, C.POINTER(u64), vp, vp, C.POINTER(u64), u32,
                                        f32, u32, u32, C.POINTER(C.c_int), u32, vp]),

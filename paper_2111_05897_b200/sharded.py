@@ -161,6 +161,17 @@ class PeerExchange:
                                                  offsets.data_ptr(), B, F, o._s()),
                   "exchange forward")
 
+    def prefetch(self, ids, offsets, B, F):
+        o = self.ops
+        hps.check(hps.lib().hps_exchange_prefetch(o.h, o.table.h, ids.data_ptr(), ids.numel(),
+                                                  offsets.data_ptr(), B, F, o._s()),
+                  "exchange prefetch")
+
+    def forward_prefetched(self):
+        o = self.ops
+        hps.check(hps.lib().hps_exchange_forward_prefetched(o.h, o.table.h, o._s()),
+                  "exchange forward (prefetched)")
+
     def pool(self, B, F, out=None):
         """Pooled [B, F, D]: a zero-copy view of the arena's pooled buffer (valid until the
         next forward) when out is None, else copied into out."""
@@ -260,6 +271,24 @@ class ShardedEmbeddingWorker:
                                   self.recv_counts)
         rows, self.recv_versions = self.ops.lookup(self.recv_ids)
         self.rows = self._a2a(rows, self.recv_counts, self.send_counts)
+
+    def prefetch(self, ids, offsets, B: int, F: int):
+        """Phase 1 of register_batch (p2p): route the batch and plan its backward pairs --
+        no barrier and no table access, so it may run on a stream beside the previous
+        batch's backward. Complete it with register_prefetched() after that backward."""
+        if self.transport != "p2p":
+            raise hps.PreconditionError("prefetch needs the p2p transport")
+        if self.peer is None:
+            self.peer = PeerExchange(self.ops, self.dist, self.group, self.rank,
+                                     self.max_ids or max(ids.numel(), 1),
+                                     max(self.max_groups or 0, B * F))
+        self._pending = (B, F, ids.numel())
+        self.peer.prefetch(ids, offsets, B, F)
+
+    def register_prefetched(self):
+        """Phase 2: owner lookup and row delivery of the prefetched batch (fetch_rows)."""
+        self.B, self.F, self.n_ids = self._pending
+        self.peer.forward_prefetched()
 
     def serve_pull(self, out_pooled=None):
         """Pooled embeddings [B, F, D] of the registered batch (serve_pull)."""

@@ -287,3 +287,103 @@ def run_hybrid_world(world, timeout=300, **kw):
             if p.is_alive():
                 p.kill()
     return results
+
+
+def run_pipelined_rank(rank, world, port, D=8, B=12, F=3, steps=5, space=60, q=None):
+    """bench.py's pipelined sharded schedule: two workers (exchanges) alternate; batch s+1
+    is prefetched (routed, pairs planned) on a second stream beside batch s's lookup,
+    pull and backward. Pooled outputs and the owners' rows must equal the oracle driven
+    with the global batches in plain sync order."""
+    try:
+        import torch
+        import torch.distributed as dist
+
+        import oracle as O
+        from paper_2111_05897_b200 import hps
+        from paper_2111_05897_b200.sharded import ShardedEmbeddingWorker
+
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        S = 8
+        salts = [O.mix64(7 + s) for s in range(S)]
+        exp = O.Restatement(salts, D, "adagrad")
+        dev = torch.device("cuda", rank)
+        table = hps.ShardSet(S, D, 1 << 14, hps.ADAGRAD, salts=salts)
+        ews = [ShardedEmbeddingWorker(table, hps.MEAN, max_ids=world * B * F * 4)
+               for _ in range(2)]
+        data = []
+        for s in range(steps):
+            gids, goffs, _ = global_batch(s, world, B, F, space)
+            lid, loff = local_part(gids, goffs, world, B, F, rank)
+            rng = np.random.default_rng(500 + s)
+            g_all = (rng.standard_normal((world * B, F, D)) * 0.3).astype(np.float32)
+            data.append((gids, goffs, torch.from_numpy(lid.view(np.int64).copy()).to(dev),
+                         torch.from_numpy(loff.astype(np.int32)).to(dev), g_all,
+                         torch.from_numpy(np.ascontiguousarray(g_all[rank::world])).to(dev)))
+        sk = np.array([((i % world) << 56) | (i // world) for i in range(world * B)], np.uint64)
+        main = torch.cuda.current_stream()
+        side = torch.cuda.Stream()
+        ews[0].prefetch(data[0][2], data[0][3], B, F)
+        seen = set()
+        for s in range(steps):
+            side.wait_stream(main)
+            if s + 1 < steps:
+                with torch.cuda.stream(side):
+                    ews[(s + 1) % 2].prefetch(data[s + 1][2], data[s + 1][3], B, F)
+            w = ews[s % 2]
+            w.register_prefetched()
+            pooled = w.serve_pull()
+            gids, goffs, _, _, g_all, g_local = data[s]
+            got = pooled.cpu().numpy()
+            pooled_exp, rv_exp = exp.pull_batch(world * B, F, gids, goffs.astype(np.uint64),
+                                                "mean")
+            assert got.tobytes() == pooled_exp[rank::world].tobytes(), f"step {s}: pooled"
+            assert w.apply_backward(g_local, 0.05, s + 1)
+            main.wait_stream(side)
+            exp.push_batch(world * B, F, gids, goffs.astype(np.uint64), g_all, 0.05, s + 1,
+                           read_versions=rv_exp, sample_keys=sk, agg="mean")
+            seen.update(int(x) for x in gids)
+        torch.cuda.synchronize()
+        table.sync()
+        mine = np.array(sorted(i for i in seen if hps.route_shard(i, S) % world == rank),
+                        np.uint64)
+        w_, a_, v_, p_ = table.peek(mine)
+        we, ae, ve, pe = exp.peek(mine)
+        assert p_.all() and pe.all()
+        assert w_.tobytes() == we.tobytes(), f"rank {rank}: rows differ"
+        assert a_.tobytes() == ae.tobytes(), f"rank {rank}: optimizer state differs"
+        assert (v_ == ve).all(), f"rank {rank}: versions differ"
+        dist.barrier()
+        dist.destroy_process_group()
+        if q is not None:
+            q.put((rank, "ok", len(mine)))
+    except Exception:
+        if q is not None:
+            q.put((rank, traceback.format_exc(), 0))
+        raise
+
+
+def run_pipelined_world(world, timeout=300, **kw):
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=run_pipelined_rank, args=(r, world, port), kwargs=dict(kw, q=q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = []
+    try:
+        for _ in range(world):
+            results.append(q.get(timeout=timeout))
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    return results

@@ -135,3 +135,19 @@ def test_sharded_hybrid_staleness(world, tau):
 
     res = run_hybrid_world(world, tau=tau)
     assert all(r[1] == "ok" for r in res), [r[1] for r in res]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,D", [(1, 8), (2, 8), (2, 64)])
+def test_sharded_pipelined_prefetch(world, D):
+    """Two exchanges alternate; the next batch is prefetched (routed, pairs planned) on a
+    second stream beside this batch's forward completion, pull and backward: bit-exact
+    with the oracle in sync order."""
+    import torch
+
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    from sharded_case import run_pipelined_world
+
+    res = run_pipelined_world(world, D=D)
+    assert all(r[1] == "ok" for r in res), [r[1] for r in res]
