@@ -267,12 +267,13 @@ hps_status hps_table_apply_pairs(hps_table* t, const uint64_t* recv_ids,
  * hanging the device. */
 hps_status hps_exchange_arena(hps_exchange* x, uint64_t max_ids, uint64_t max_groups,
                               uint32_t dim, void* out_handle);
-/* hps_exchange_forward in two phases, so the next batch's routing can run beside the
- * current batch's backward (no barrier, no table access in phase 1): prefetch routes the
- * batch (distinct ids into their owners' id regions) and plans its backward pairs;
- * forward_prefetched completes the forward (owner lookup, rows back, barriers). Every
- * rank issues both; phase 2 must follow this rank's previous backward on its stream and
- * phase 1 must be ordered before phase 2 (same stream, or joined). */
+/* hps_exchange_forward in two phases, so the next batch's routing and owner lookup can run
+ * beside the current batch's backward: prefetch routes the batch (distinct ids into their
+ * owners' id regions), plans its backward pairs, passes the first device barrier and
+ * finds-or-inits the ids every source asked for (no existing row is read or written);
+ * forward_prefetched delivers the rows and passes the second barrier. Every rank issues
+ * both; phase 2 must follow this rank's previous backward on its stream and phase 1 must
+ * be ordered before phase 2 (same stream, or joined). */
 hps_status hps_exchange_prefetch(hps_exchange* x, hps_table* t, const uint64_t* ids, size_t n_ids,
                                  const uint32_t* offsets, uint32_t B, uint32_t F,
                                  hps_stream stream);

@@ -545,6 +545,7 @@ XBatch::~XBatch() {
   if (arena) cudaFree(arena);
   if (gdirect) cudaFree(gdirect);
   if (glist) cudaFree(glist);
+  if (pnew) cudaFree(pnew);
   if (side) cudaStreamDestroy(side);
   if (aux) cudaStreamDestroy(aux);
   if (ev_fork) cudaEventDestroy(ev_fork);
@@ -1199,25 +1200,35 @@ static void fwd_route_phase(XBatch& x, Table* t, const uint64_t* ids, uint64_t n
 // Forward, phase 2: the first barrier (ids and counts landed), owner lookup of what every
 // source asked for, rows (and one-listing groups' pooled values) straight back to the
 // sources, the pair counts, the second barrier.
-static void fwd_finish_phase(XBatch& x, Table* t, cudaStream_t st) {
+// Forward, phase 1b: the first barrier (every source's ids and counts landed), then the
+// owner's find-or-init of what every source asked for (hash probe + lazy init of new
+// rows: no existing row is read or written, so it may run beside another batch's
+// apply). The new-row list is the exchange's own (not the table's scratch batch).
+static void fwd_probe_phase(XBatch& x, Table* t, cudaStream_t st) {
   const uint64_t M = x.max_ids;
   const PeerHdrs ph = peer_hdrs(x);
   barrier(x, t, st);  // every id region and count has landed
-  // owner: find-or-init the ids every source asked for, rows straight back to them
   XHdr* mine = ph.h[x.rank];
   uint32_t* oslot = reinterpret_cast<uint32_t*>(x.arena + x.off_oslot);
-  Batch& b = t->scratch;
-  batch_reserve(b, x.G * M, 0, 0);
-  b.registered = false;
-  HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
+  grow(x.pnew, x.cap_pnew, x.G * M + 1);
+  HPS_CUDA(cudaMemsetAsync(x.pnew, 0, sizeof(uint32_t), st));  // [0] = new-row count
   {
     ProfScope p(t, "x_owner_probe", st);
     launch_probe_regions(t->d, reinterpret_cast<const uint64_t*>(x.arena + x.off_ids), M, x.G,
                          mine, oslot, reinterpret_cast<uint64_t*>(x.arena + x.off_oids),
-                         reinterpret_cast<uint32_t*>(x.arena + x.off_ocnt), b.new_slots,
-                         &b.small[2], t->sm_count, st);
-    launch_lazy_init(t->d, b.new_slots, &b.small[2], x.G * M, t->sm_count, st);
+                         reinterpret_cast<uint32_t*>(x.arena + x.off_ocnt), x.pnew + 1,
+                         x.pnew, t->sm_count, st);
+    launch_lazy_init(t->d, x.pnew + 1, x.pnew, x.G * M, t->sm_count, st);
   }
+}
+
+// Forward, phase 2: rows (and one-listing groups' pooled values) straight back to the
+// sources -- after this rank's previous apply -- the pair counts, the second barrier.
+static void fwd_finish_phase(XBatch& x, Table* t, cudaStream_t st) {
+  const uint64_t M = x.max_ids;
+  const PeerHdrs ph = peer_hdrs(x);
+  XHdr* mine = ph.h[x.rank];
+  uint32_t* oslot = reinterpret_cast<uint32_t*>(x.arena + x.off_oslot);
   PeerRows pr{}, pp{};
   for (uint32_t r = 0; r < x.G; ++r) {
     pr.p[r] = reinterpret_cast<float*>(x.peer[r] + x.off_rows);
@@ -1252,6 +1263,7 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
   require_connected(x, t->cfg.embedding_dim, n);
   x.prefetched = false;
   fwd_route_phase(x, t, ids, n, offsets, B, F, st, /*fork_pairs=*/true);
+  fwd_probe_phase(x, t, st);
   fwd_finish_phase(x, t, st);
 }
 
@@ -1259,6 +1271,7 @@ void xbatch_prefetch(XBatch& x, Table* t, const uint64_t* ids, uint64_t n,
                      const uint32_t* offsets, uint32_t B, uint32_t F, cudaStream_t st) {
   require_connected(x, t->cfg.embedding_dim, n);
   fwd_route_phase(x, t, ids, n, offsets, B, F, st, /*fork_pairs=*/false);
+  fwd_probe_phase(x, t, st);
   x.prefetched = true;
 }
 

@@ -204,6 +204,8 @@ struct XBatch {
   bool counts_sent = false;  // the forward delivered this batch's pair counts
   bool pairs_forked = false; // the pair plan ran on `aux` (phase 2 joins it)
   bool prefetched = false;   // phase 1 of the next forward done (hps_exchange_prefetch)
+  uint32_t* pnew = nullptr;  // owner probe: [0] new-row count, then the new rows' slots
+  uint64_t cap_pnew = 0;
   const uint32_t *pairs_spos = nullptr, *pairs_slist = nullptr;
   uint64_t max_ids = 0;
   uint32_t arena_dim = 0, rank = 0;
