@@ -80,7 +80,10 @@ class HybridTrainer:
         if key not in self._bufs:
             t = self.torch
             self._bufs[key] = dict(
-                pooled=t.empty((B, self.F, self.D), dtype=t.float32, device=self.device),
+                # local workers pull into this buffer; sharded workers hand out a view of
+                # their exchange arena instead
+                pooled=None if self.sharded is not None else
+                t.empty((B, self.F, self.D), dtype=t.float32, device=self.device),
                 grads=t.empty((B, self.F, self.D), dtype=t.float32, device=self.device),
                 pulled=t.cuda.Event(), graded=t.cuda.Event())
         return self._bufs[key]
