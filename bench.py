@@ -718,7 +718,10 @@ def main():
     graphs, graph_launches = [], []
     it_g = it
     if not args.no_graph:
-        cap = torch.cuda.Stream()
+        # stream priority of the step's own work (pull + push) vs the next batch's
+        # register; measured: equal priorities are fastest (profiles/r1_prio_ab.txt)
+        prio = int(os.environ.get("HPS_MAIN_PRIORITY", "0")) if pipe else 0
+        cap = torch.cuda.Stream(priority=prio)
         for m in range(M):
             g = torch.cuda.CUDAGraph()
             l0 = hps.launch_count()
