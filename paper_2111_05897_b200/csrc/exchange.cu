@@ -38,10 +38,14 @@ constexpr int kXBlock = 256;
 constexpr uint32_t kInserter = 0x80000000u;
 constexpr uint32_t kNoPair = 0xffffffffu;
 // x.cnt layout (u32 words): [0,32) distinct ids per owner, [32] special-id claim,
-// [33] listings of multi-listed ids, [64,96) single pairs per owner, [100] groups left
-// for the requester's own pooling (glist).
-constexpr int kCntSpecial = 32, kCntMulti = 33, kCntSingle = 64, kCntGlist = 100,
-              kCntWords = 128;
+// [33] listings of multi-listed ids, [34] groups left for the requester's own pooling
+// (glist), [64,96) ids listed once per owner (= single pairs), [96,128) multi-listed ids
+// per owner. Within an owner's segment the ids listed once come first, numbered like
+// their pairs, so a single pair's position needs no word of its own on the peer path.
+constexpr int kCntSpecial = 32, kCntMulti = 33, kCntGlist = 34, kCntSingle = 64,
+              kCntMultiIds = 96, kCntWords = 128;
+// hval of an id listed more than once: its index among its owner's multi-listed ids
+constexpr uint32_t kMultiIdx = 0x80000000u;
 
 // Distinct ids: a transient open-addressing set (keys only). The entry index of each
 // listing's id is recorded; the thread whose CAS claimed the entry is its inserter and
@@ -95,13 +99,13 @@ __global__ void __launch_bounds__(kXBlock)
                     uint32_t* __restrict__ hval, uint8_t* __restrict__ dest,
                     uint32_t* __restrict__ spair, uint32_t* cnt) {
   pdl_entry();
-  __shared__ uint32_t bc[32], gb[32], sc[32], sb[32];
+  __shared__ uint32_t bc[32], mc[32], mb[32], sc[32], sb[32];
   for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < n;
        base += (uint64_t)gridDim.x * blockDim.x) {
-    if (threadIdx.x < G) bc[threadIdx.x] = 0, sc[threadIdx.x] = 0;
+    if (threadIdx.x < G) bc[threadIdx.x] = 0, sc[threadIdx.x] = 0, mc[threadIdx.x] = 0;
     __syncthreads();
     const uint64_t i = base + threadIdx.x;
-    uint32_t d = 0, r = 0, q = 0, code = 0;
+    uint32_t d = 0, q = 0, code = 0;
     bool single = false;
     const bool valid = i < n;
     if (valid) {
@@ -109,20 +113,25 @@ __global__ void __launch_bounds__(kXBlock)
       d = route_shard(ids[i], S) % G;
       dest[i] = static_cast<uint8_t>(d);
       if (code & kInserter) {
-        r = atomicAdd(&bc[d], 1u);
+        atomicAdd(&bc[d], 1u);
         single = hmul[code & ~kInserter] == 0;
-        if (single) q = atomicAdd(&sc[d], 1u);
+        q = single ? atomicAdd(&sc[d], 1u) : atomicAdd(&mc[d], 1u);
       }
     }
     __syncthreads();
     if (threadIdx.x < G) {
-      gb[threadIdx.x] = bc[threadIdx.x] ? atomicAdd(&cnt[threadIdx.x], bc[threadIdx.x]) : 0;
+      if (bc[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], bc[threadIdx.x]);
       sb[threadIdx.x] =
           sc[threadIdx.x] ? atomicAdd(&cnt[kCntSingle + threadIdx.x], sc[threadIdx.x]) : 0;
+      mb[threadIdx.x] =
+          mc[threadIdx.x] ? atomicAdd(&cnt[kCntMultiIds + threadIdx.x], mc[threadIdx.x]) : 0;
     }
     __syncthreads();
     if (valid) {
-      if (code & kInserter) hval[code & ~kInserter] = gb[d] + r;
+      // ids listed once: index = their pair index; multi-listed: placed after all of
+      // the owner's ids listed once (x_scatter resolves kMultiIdx)
+      if (code & kInserter)
+        hval[code & ~kInserter] = single ? sb[d] + q : (kMultiIdx | (mb[d] + q));
       spair[i] = single ? sb[d] + q : kNoPair;
     }
     __syncthreads();
@@ -160,9 +169,11 @@ __global__ void __launch_bounds__(kXBlock)
                      const uint32_t* __restrict__ lgrp, const uint32_t* __restrict__ offsets,
                      uint8_t* __restrict__ gdirect) {
   pdl_entry();
-  __shared__ uint32_t seg[33];
+  __shared__ uint32_t seg[33], s_single[32];
   __shared__ uint32_t s_n, s_base;
   load_seg(cnt, G, seg);
+  if (threadIdx.x < G) s_single[threadIdx.x] = cnt[kCntSingle + threadIdx.x];
+  __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x <= G) seg_out[threadIdx.x] = seg[threadIdx.x];
   for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < n;
        base += (uint64_t)gridDim.x * blockDim.x) {
@@ -173,7 +184,8 @@ __global__ void __launch_bounds__(kXBlock)
     bool multi = false;
     if (i < n) {
       const uint32_t code = hidx[i];
-      const uint32_t d = dest[i], j = hval[code & ~kInserter];
+      const uint32_t d = dest[i], hv = hval[code & ~kInserter];
+      const uint32_t j = (hv & kMultiIdx) ? s_single[d] + (hv & ~kMultiIdx) : hv;
       pos = seg[d] + j;
       sendpos[i] = pos;
       if (code & kInserter) {
@@ -295,6 +307,9 @@ struct PairOut {
   // here while the contributions are formed; the owner reads the words after the barrier)
   uint32_t* bad[kMaxWorld];
   const unsigned long long* epoch;
+  // write single pairs' positions (NCCL path); the peer path's owners derive them (a
+  // single pair's index is its id's index in the owner segment)
+  int single_pos;
 };
 
 template <int V>
@@ -356,7 +371,8 @@ __global__ void __launch_bounds__(kXBlock)
           if (sp[u] == kNoPair) continue;
           const uint32_t d = dd[u];
           const uint64_t out = base[d] + sp[u];
-          if (lane == 0 && d0 == lane * V) po.p[d][out] = sendpos[i0 + u * groups] - seg[d];
+          if (po.single_pos && lane == 0 && d0 == lane * V)
+            po.p[d][out] = sendpos[i0 + u * groups] - seg[d];
           const double scale = mean ? 1.0 / static_cast<double>(cntg[u]) : 1.0;
           float o[V];
 #pragma unroll
@@ -376,7 +392,7 @@ __global__ void __launch_bounds__(kXBlock)
     const uint32_t d = dest[i];
     const uint64_t out = base[d] + sp;
     const uint32_t g = lgrp[i];
-    if (lane == 0) po.p[d][out] = sendpos[i] - seg[d];
+    if (po.single_pos && lane == 0) po.p[d][out] = sendpos[i] - seg[d];
     const double scale = mean ? 1.0 / static_cast<double>(offsets[g + 1] - offsets[g]) : 1.0;
     for (uint32_t d0 = lane * V; d0 < D; d0 += L * V) {
       const float* src = grads + static_cast<uint64_t>(g) * D + d0;
@@ -774,6 +790,7 @@ void xbatch_pairs(XBatch& x, const float* grads, uint32_t D, uint32_t* out_pair_
   const uint32_t *spos, *slist;
   pairs_core(x, &spos, &slist, st);
   PairOut po{};
+  po.single_pos = 1;
   for (uint32_t d = 0; d < x.G; ++d) po.c[d] = out_contrib, po.p[d] = out_pair_pos;
   emit_pairs(x, grads, D, spos, slist, x.pair_off, po, st);
   if (is_device_ptr(out_pair_counts)) {
@@ -872,6 +889,7 @@ __global__ void x_owner_dyn_kernel(const XHdr* __restrict__ hdr,
                                    const unsigned long long* epoch) {
   pdl_entry();
   __shared__ uint64_t po[kMaxWorld + 1];
+  __shared__ uint32_t ps[kMaxWorld];
   if (epoch && blockIdx.x == 0 && threadIdx.x == 0) {
     // the sources validated the contributions while emitting them (one barrier ago)
     const uint32_t e = static_cast<uint32_t>(*epoch - 1);
@@ -885,6 +903,7 @@ __global__ void x_owner_dyn_kernel(const XHdr* __restrict__ hdr,
     for (uint32_t r = 0; r < W; ++r) {
       po[r] = run;
       run += ld_volatile(&hdr->bwd_cnt[r]);
+      ps[r] = ld_volatile(&hdr->bwd_single[r]);
     }
     po[W] = run;
   }
@@ -899,7 +918,9 @@ __global__ void x_owner_dyn_kernel(const XHdr* __restrict__ hdr,
     }
     uint32_t r = 0;
     while (r + 1 < W && po[r + 1] <= k) ++r;
-    uint32_t j = pair_pos[k];
+    // a source's first ps[r] pairs are its ids listed once, numbered like those ids
+    const uint64_t kk = k - po[r];
+    uint32_t j = kk < ps[r] ? static_cast<uint32_t>(kk) : pair_pos[k];
     if (j >= ocnt[r]) {
       atomicOr(protocol, 1ull);
       j = 0;
@@ -973,10 +994,14 @@ __global__ void x_fwd_hdr_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
 }
 
 __global__ void x_bwd_hdr_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
-                                 const uint64_t* __restrict__ pair_off) {
+                                 const uint64_t* __restrict__ pair_off,
+                                 const uint32_t* __restrict__ cnt) {
   pdl_entry();
   const uint32_t d = threadIdx.x;
-  if (d < W) ph.h[d]->bwd_cnt[rank] = static_cast<uint32_t>(pair_off[d + 1] - pair_off[d]);
+  if (d < W) {
+    ph.h[d]->bwd_cnt[rank] = static_cast<uint32_t>(pair_off[d + 1] - pair_off[d]);
+    ph.h[d]->bwd_single[rank] = cnt[kCntSingle + d];  // its first pairs: no position word
+  }
 }
 
 // Where this rank's pairs start in each owner's (source-rank major) pair arrays.
@@ -1252,7 +1277,8 @@ static void fwd_finish_phase(XBatch& x, Table* t, cudaStream_t st) {
   // reaches after its step-s apply has read them.)
   if (x.pairs_ready && x.pairs_forked) HPS_CUDA(cudaStreamWaitEvent(st, x.ev_join, 0));
   else if (!x.pairs_ready) HPS_CUDA(cudaMemsetAsync(x.pair_off, 0, 33 * sizeof(uint64_t), st));
-  launch(x_bwd_hdr_kernel, 1, 32, 0, st, ph, x.G, x.rank, x.pair_off);
+  if (!x.pairs_ready) HPS_CUDA(cudaMemsetAsync(x.cnt + kCntSingle, 0, 32 * sizeof(uint32_t), st));
+  launch(x_bwd_hdr_kernel, 1, 32, 0, st, ph, x.G, x.rank, x.pair_off, x.cnt);
   HPS_LAUNCH_CHECK();
   x.counts_sent = true;
   barrier(x, t, st);  // every owner's rows have landed in this rank's rows buffer

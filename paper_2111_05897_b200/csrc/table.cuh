@@ -207,6 +207,7 @@ struct alignas(128) XHdr {
   uint32_t fwd_cnt[kMaxWorld];        // ids source r wrote into my id region r
   uint32_t fwd_seg[kMaxWorld];        // where my rows go in source r's rows buffer
   uint32_t bwd_cnt[kMaxWorld];        // pairs source r sends me
+  uint32_t bwd_single[kMaxWorld];     // ... of which its first ones are single pairs
   uint32_t bad[kMaxWorld];            // = the emit's barrier epoch if source r sent me a
                                       //   non-finite contribution in that step
   uint32_t err;                       // barrier timeout seen by this rank
