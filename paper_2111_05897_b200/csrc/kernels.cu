@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(256, 6)
                        uint64_t rows, uint32_t D, uint32_t F, int mean,
                        unsigned long long* ctr, float* __restrict__ cbuf,
                        const uint32_t* __restrict__ inv, const uint32_t* gate,
-                       const uint32_t* rows_live, int scatter_only) {
+                       const uint32_t* rows_live, int scatter_only, int l2_mode) {
   pdl_entry();
   if (rows_live) rows = min(rows, static_cast<uint64_t>(*rows_live));
   using G = Geo<V, L, kGuard>;
@@ -505,7 +506,17 @@ __global__ void __launch_bounds__(256, 6)
         // issued without waiting for the group sizes (an empty group's row is read and
         // ignored below): the gradient stream does not serialise behind the offsets
         const uint64_t r = r0 + u * groups;
-        if (r < rows && (!kGuard || d0 < D)) load_vec_cs<V>(grads + r * D + d0, x[u]);
+        if (r < rows && (!kGuard || d0 < D)) {
+          // l2_mode (HPS_CHECK_L2): 0 streaming, 1 default, 2/3/4 evict_last for 100/50/25%
+          // of the lines -- how much of the gradient stream the update kernel re-reads
+          // (once per unique row) should find in L2. Default 3: update 111 -> 107 us,
+          // check 30 -> 32 us (profiles/r1_check_l2_ab.txt)
+          if (l2_mode == 0) load_vec_cs<V>(grads + r * D + d0, x[u]);
+          else if (l2_mode == 1) load_vec<V>(grads + r * D + d0, x[u]);
+          else if (l2_mode == 2) load_vec_keep<V>(grads + r * D + d0, x[u]);
+          else if (l2_mode == 3) load_vec_keep<V, 50>(grads + r * D + d0, x[u]);
+          else load_vec_keep<V, 25>(grads + r * D + d0, x[u]);
+        }
         else for (int j = 0; j < V; ++j) x[u][j] = 0.0f;
       }
       if (write_c) {
@@ -553,6 +564,14 @@ __global__ void __launch_bounds__(256, 6)
   }
 }
 
+static int check_l2_mode() {
+  static const int m = [] {
+    const char* e = getenv("HPS_CHECK_L2");
+    return e ? atoi(e) : 3;  // profiles/r1_check_l2_ab.txt
+  }();
+  return m;
+}
+
 void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
                         uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st,
                         float* cbuf, const uint32_t* inv, const uint32_t* gate,
@@ -565,7 +584,7 @@ void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B,
     uint32_t blocks = std::min<uint64_t>(ceil_div(rows, groups_per_block * 4), 148ull * 16);
     launch(check_batch_kernel<V, L, G>, blocks, 256, 0, st, grads, offsets, rows, D, F, mean, ctr,
                                                         cbuf, inv, gate, rows_live,
-                                                        scatter_only ? 1 : 0);
+                                                        scatter_only ? 1 : 0, check_l2_mode());
   });
   HPS_LAUNCH_CHECK();
 }

@@ -43,6 +43,21 @@ __device__ __forceinline__ void load_vec_cs(const float* p, float (&v)[V]) {
   }
 }
 
+// Load with an L2 evict_last policy: data read again by a later kernel of the same step.
+template <int V, int kPct = 100>
+__device__ __forceinline__ void load_vec_keep(const float* p, float (&v)[V]) {
+  if constexpr (V == 4) {
+    asm volatile(
+        "{.reg .b64 pol;\n\t"
+        "createpolicy.fractional.L2::evict_last.L2::evict_first.b64 pol, %5;\n\t"
+        "ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], pol;}"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+        : "l"(p), "f"(kPct / 100.0f));
+  } else {
+    load_vec<V>(p, v);
+  }
+}
+
 template <int V>
 __device__ __forceinline__ void store_vec(float* p, const float (&v)[V]) {
   if constexpr (V == 4) {
