@@ -15,6 +15,7 @@
 // word + 4 B slot.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(256, 8)
                 const uint32_t* __restrict__ slots, uint32_t BF, uint64_t N, int mean,
                 float* __restrict__ out, uint64_t* __restrict__ out_rv64,
                 uint32_t* __restrict__ out_rv32, const uint32_t* __restrict__ glist,
-                const uint32_t* __restrict__ glist_n) {
+                const uint32_t* __restrict__ glist_n, int l2_mode) {
   pdl_entry();
   using G = Geo<V, L, kGuard>;
   const int ln = G::lane();
@@ -140,8 +141,17 @@ __global__ void __launch_bounds__(256, 8)
       for (int u = 0; u < kPoolILP; ++u) {
         if (!one[u]) continue;
         const bool ok = slot_ok(t, s[u]);
-        if (ok) load_vec<V>(t.rows + static_cast<uint64_t>(s[u]) * t.stride + ln * V, r[u]);
-        else for (int k = 0; k < V; ++k) r[u][k] = 0.0f;
+        if (ok) {
+          // l2_mode (HPS_POOL_L2): 0 default, 2/3/4 evict_last on 100/50/25% of the lines --
+          // how much of the gathered weights the push's update should find in L2
+          const float* src = t.rows + static_cast<uint64_t>(s[u]) * t.stride + ln * V;
+          if (l2_mode == 0) load_vec<V>(src, r[u]);
+          else if (l2_mode == 2) load_vec_keep<V>(src, r[u]);
+          else if (l2_mode == 3) load_vec_keep<V, 50>(src, r[u]);
+          else load_vec_keep<V, 25>(src, r[u]);
+        } else {
+          for (int k = 0; k < V; ++k) r[u][k] = 0.0f;
+        }
         ver[u] = (want_rv && ok && ln == 0) ? vt_read(t, s[u]).x : 0u;
       }
 #pragma unroll
@@ -192,6 +202,14 @@ void launch_snapshot_rv(const DevTable& t, const uint32_t* slots, uint64_t n, ui
   HPS_LAUNCH_CHECK();
 }
 
+static int pool_l2_mode() {
+  static const int m = [] {
+    const char* e = getenv("HPS_POOL_L2");
+    return e ? atoi(e) : 0;
+  }();
+  return m;
+}
+
 void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,
                  uint64_t N, int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32,
                  cudaStream_t st, const uint32_t* glist, const uint32_t* glist_n) {
@@ -203,12 +221,12 @@ void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slo
       const uint32_t blocks = std::min<uint64_t>(ceil_div(BF, groups_per_block * kPoolILP),
                                                  148ull * 8);
       launch(pool_kernel<V, L, G, true>, blocks, 256, 0, st, t, offsets, slots, BF, N, mean, out,
-             out_rv64, out_rv32, glist, glist_n);
+             out_rv64, out_rv32, glist, glist_n, pool_l2_mode());
     } else {
       uint32_t blocks =
           std::min<uint64_t>(ceil_div(BF, groups_per_block * kPoolILP), 1u << 30);
       launch(pool_kernel<V, L, G, false>, blocks, 256, 0, st, t, offsets, slots, BF, N, mean,
-             out, out_rv64, out_rv32, nullptr, nullptr);
+             out, out_rv64, out_rv32, nullptr, nullptr, pool_l2_mode());
     }
   });
   HPS_LAUNCH_CHECK();
