@@ -44,6 +44,48 @@ def local_part(ids, offs, W, B, F, r):
     return np.array(lid, np.uint64), np.array(loff, np.int64)
 
 
+def _spawn_world(target, world, timeout, args_of, kw, attempts=3):
+    """Runs target(*args_of(rank, port), **kw, q=q) in `world` spawned processes on a fresh
+    rendezvous port. A rank that fails stops the wait (its peers would block in the
+    rendezvous); a port another process took between the probe and the bind
+    (EADDRINUSE) retries on a new port."""
+    import multiprocessing as mp
+    import queue
+    import socket
+
+    for attempt in range(attempts):
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        procs = [ctx.Process(target=target, args=args_of(r, port), kwargs=dict(kw, q=q))
+                 for r in range(world)]
+        for p in procs:
+            p.start()
+        results = []
+        try:
+            for _ in range(world):
+                try:
+                    r = q.get(timeout=timeout)
+                except queue.Empty:
+                    break
+                results.append(r)
+                if r[1] != "ok":
+                    break
+        finally:
+            for p in procs:
+                p.join(timeout=1 if len(results) < world else 30)
+                if p.is_alive():
+                    p.kill()
+        if any("EADDRINUSE" in str(r[1]) for r in results) and attempt + 1 < attempts:
+            continue
+        if len(results) < world and all(r[1] == "ok" for r in results):
+            raise TimeoutError(f"{world - len(results)} rank(s) reported nothing in {timeout} s")
+        return results
+    return results
+
+
 def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, agg="mean",
              opt="adagrad", space=60, transport="p2p", graph=False, nan_step=-1, q=None):
     try:
@@ -156,28 +198,7 @@ def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, ag
 
 
 def run_world(world, backend, use_device, timeout=240, **kw):
-    import multiprocessing as mp
-    import socket
-
-    with socket.socket() as sk:
-        sk.bind(("127.0.0.1", 0))
-        port = sk.getsockname()[1]
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=run_rank, args=(r, world, backend, port, use_device),
-                         kwargs=dict(kw, q=q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    results = []
-    try:
-        for _ in range(world):
-            results.append(q.get(timeout=timeout))
-    finally:
-        for p in procs:
-            p.join(timeout=30)
-            if p.is_alive():
-                p.kill()
-    return results
+    return _spawn_world(run_rank, world, timeout, lambda r, port: (r, world, backend, port, use_device), kw)
 
 
 def run_hybrid_rank(rank, world, port, tau=2, D=8, B=12, F=3, nd=2, steps=6, space=60, q=None):
@@ -265,28 +286,7 @@ def run_hybrid_rank(rank, world, port, tau=2, D=8, B=12, F=3, nd=2, steps=6, spa
 
 
 def run_hybrid_world(world, timeout=300, **kw):
-    import multiprocessing as mp
-    import socket
-
-    with socket.socket() as sk:
-        sk.bind(("127.0.0.1", 0))
-        port = sk.getsockname()[1]
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=run_hybrid_rank, args=(r, world, port), kwargs=dict(kw, q=q))
-             for r in range(world)]
-    for p in procs:
-        p.start()
-    results = []
-    try:
-        for _ in range(world):
-            results.append(q.get(timeout=timeout))
-    finally:
-        for p in procs:
-            p.join(timeout=30)
-            if p.is_alive():
-                p.kill()
-    return results
+    return _spawn_world(run_hybrid_rank, world, timeout, lambda r, port: (r, world, port), kw)
 
 
 def run_pipelined_rank(rank, world, port, D=8, B=12, F=3, steps=5, space=60, q=None):
@@ -365,25 +365,4 @@ def run_pipelined_rank(rank, world, port, D=8, B=12, F=3, steps=5, space=60, q=N
 
 
 def run_pipelined_world(world, timeout=300, **kw):
-    import multiprocessing as mp
-    import socket
-
-    with socket.socket() as sk:
-        sk.bind(("127.0.0.1", 0))
-        port = sk.getsockname()[1]
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=run_pipelined_rank, args=(r, world, port), kwargs=dict(kw, q=q))
-             for r in range(world)]
-    for p in procs:
-        p.start()
-    results = []
-    try:
-        for _ in range(world):
-            results.append(q.get(timeout=timeout))
-    finally:
-        for p in procs:
-            p.join(timeout=30)
-            if p.is_alive():
-                p.kill()
-    return results
+    return _spawn_world(run_pipelined_rank, world, timeout, lambda r, port: (r, world, port), kw)
