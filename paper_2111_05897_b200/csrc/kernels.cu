@@ -572,6 +572,14 @@ static int check_l2_mode() {
   return m;
 }
 
+static uint64_t check_blocks_per_sm() {
+  static const uint64_t m = [] {
+    const char* e = getenv("HPS_CHECK_BPS");
+    return static_cast<uint64_t>(e ? std::max(1, atoi(e)) : 16);
+  }();
+  return m;
+}
+
 void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
                         uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st,
                         float* cbuf, const uint32_t* inv, const uint32_t* gate,
@@ -581,7 +589,8 @@ void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B,
   if (scatter_only && !cbuf) return;
   HPS_DISPATCH_DIM(D, {
     uint64_t groups_per_block = 256 / L;
-    uint32_t blocks = std::min<uint64_t>(ceil_div(rows, groups_per_block * 4), 148ull * 16);
+    uint32_t blocks = std::min<uint64_t>(ceil_div(rows, groups_per_block * 4),
+                                         148ull * check_blocks_per_sm());
     launch(check_batch_kernel<V, L, G>, blocks, 256, 0, st, grads, offsets, rows, D, F, mean, ctr,
                                                         cbuf, inv, gate, rows_live,
                                                         scatter_only ? 1 : 0, check_l2_mode());
