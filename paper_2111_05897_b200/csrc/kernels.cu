@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(256, 6)
         // ignored below): the gradient stream does not serialise behind the offsets
         const uint64_t r = r0 + u * groups;
         if (r < rows && (!kGuard || d0 < D)) {
-          // l2_mode (HPS_CHECK_L2): 0 streaming, 1 default, 2/3/4 evict_last for 100/50/25%
+          // l2_mode (HPS_CHECK_L2): 0 streaming, 1 default, 2/3/4/5 evict_last for 100/50/25/75%
           // of the lines -- how much of the gradient stream the update kernel re-reads
           // (once per unique row) should find in L2. Default 3: update 111 -> 107 us,
           // check 30 -> 32 us (profiles/r1_check_l2_ab.txt)
@@ -515,6 +515,7 @@ __global__ void __launch_bounds__(256, 6)
           else if (l2_mode == 1) load_vec<V>(grads + r * D + d0, x[u]);
           else if (l2_mode == 2) load_vec_keep<V>(grads + r * D + d0, x[u]);
           else if (l2_mode == 3) load_vec_keep<V, 50>(grads + r * D + d0, x[u]);
+          else if (l2_mode == 5) load_vec_keep<V, 75>(grads + r * D + d0, x[u]);
           else load_vec_keep<V, 25>(grads + r * D + d0, x[u]);
         }
         else for (int j = 0; j < V; ++j) x[u][j] = 0.0f;
