@@ -325,6 +325,7 @@ def run_hybrid(args, world, rank, local, dev):
     if not graphs:
         tr.flush()
     torch.cuda.synchronize()
+    tr.check()  # a diverged dense step (non-finite loss / gradient) fails the run
     table.sync()
     loss_vals = [float(v) for v in losses]
     value = world * B * 1000.0 / ms
@@ -718,10 +719,9 @@ def main():
     graphs, graph_launches = [], []
     it_g = it
     if not args.no_graph:
-        # stream priority of the step's own work (pull + push) vs the next batch's
-        # register; measured: equal priorities are fastest (profiles/r1_prio_ab.txt)
-        prio = int(os.environ.get("HPS_MAIN_PRIORITY", "0")) if pipe else 0
-        cap = torch.cuda.Stream(priority=prio)
+        # equal stream priorities for the step's own work (pull + push) and the next
+        # batch's register measured fastest (profiles/r1_prio_ab.txt)
+        cap = torch.cuda.Stream()
         for m in range(M):
             g = torch.cuda.CUDAGraph()
             l0 = hps.launch_count()

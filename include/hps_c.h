@@ -181,7 +181,11 @@ hps_status hps_peek(hps_table* t, const uint64_t* ids, size_t n, float* out_w, f
  *                       unique id) carrying the fp64 chain-rule sum (push_to_shards
  *                       :726-775). read versions come from the last hps_batch_pull of this
  *                       batch (tracked) unless untracked = 1. Whole-batch validation
- *                       precedes mutation. */
+ *                       precedes mutation. out_delays must be NULL (HPS_E_PRECONDITION
+ *                       otherwise): the push's delays are recorded per (sample, id) in
+ *                       hps_counters.delay_hist (StalenessStats::record_delay
+ *                       staleness.hpp:42-49); hps_apply returns per-entry delays.
+ */
 hps_status hps_batch_create(hps_table* t, int32_t aggregation, hps_batch** out); /* EmbeddingWorkerConfig::aggregation */
 hps_status hps_batch_destroy(hps_batch* b);
 hps_status hps_batch_register(hps_batch* b, const uint64_t* ids, size_t n_ids,

@@ -260,9 +260,13 @@ hps_status hps_batch_pull(hps_batch* b, float* out_pooled, uint64_t* out_read_ve
 hps_status hps_batch_push(hps_batch* b, const float* grads, float lr, uint32_t step_tag,
                           uint32_t epoch, int untracked, uint32_t* out_delays, int* accepted,
                           uint32_t flags, hps_stream stream) {
-  (void)out_delays;  // per-(sample,id) delays land in the table's delay histogram
   return guarded([&] {
     REQUIRE(b, "hps_batch_push: null batch");
+    // per-(sample, id) delays of a batch push land in the table's delay histogram
+    // (hps_counters.delay_hist, StalenessStats::record_delay staleness.hpp:42-49); per-entry
+    // delays are hps_apply's
+    REQUIRE(!out_delays, "hps_batch_push: out_delays must be NULL (delays are recorded in "
+                         "hps_counters.delay_hist; hps_apply returns per-entry delays)");
     REQUIRE(grads || b->impl.B == 0, "hps_batch_push: null gradients");
     hps::Table* t = b->impl.table;
     std::lock_guard<std::mutex> g(t->mu);

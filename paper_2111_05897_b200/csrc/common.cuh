@@ -60,15 +60,13 @@ inline std::atomic<unsigned long long> g_launches{0};
 // induction any earlier kernel), then griddepcontrol.launch_dependents (the next grid
 // may be scheduled now). launch() issues kernels with the programmatic-serialization
 // attribute, so the next kernel's launch and block rasterisation overlap this one's
-// tail instead of following its completion; a step is ~18 short dependent kernels,
-// most of them a few microseconds. Outside a PDL launch both instructions are no-ops.
-// HPS_PDL=0 turns the attribute off (A/B measurement).
+// tail instead of following its completion; a step is ~15 short dependent kernels,
+// most of them a few microseconds (measured 0.2753 -> 0.2693 ms per C2 step with PDL,
+// profiles/r1_pdl_ab.txt). Outside a PDL launch both instructions are no-ops.
 __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
-
-bool pdl_enabled();
 
 template <typename... KArgs, typename... Args>
 inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -82,7 +80,7 @@ inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = 1;
   HPS_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 

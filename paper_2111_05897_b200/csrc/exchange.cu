@@ -670,13 +670,11 @@ static void pairs_core(XBatch& x, const uint32_t** spos_out, const uint32_t** sl
   // small path: rank sort of the multi listings' composite keys (no-op when large)
   radix::sort_composite_small(x.mkeys, n_multi, x.lbits, x.sm_pos, x.sm_list, st);
   // large path: stable radix sort of every listing by send position, only when the
-  // device count says so (a conditional graph node under capture)
+  // device count says so (its kernels exit at once otherwise)
   const bool in_b = ((x.lbits + radix::kBits - 1) / radix::kBits) & 1;
   radix::sort_scratch_zero(x.scratch, st);
-  run_if(x.side, st, n_multi, false, radix::kSmallN, [&](cudaStream_t s) {
-    radix::sort_pairs<uint32_t>(x.keys_a, x.vals_a, x.keys_b, x.vals_b, n, x.lbits, x.scratch,
-                                s, x.sms, n_multi, x.sendpos, true, false);
-  });
+  radix::sort_pairs<uint32_t>(x.keys_a, x.vals_a, x.keys_b, x.vals_b, n, x.lbits, x.scratch, st,
+                              x.sms, n_multi, x.sendpos, true, false);
   uint32_t* spos = in_b ? x.keys_b : x.keys_a;
   uint32_t* slist = in_b ? x.vals_b : x.vals_a;
   launch(x_pick_small_kernel, ceil_div(radix::kSmallN, kXBlock), kXBlock, 0, st, 
@@ -886,7 +884,7 @@ __global__ void x_owner_dyn_kernel(const XHdr* __restrict__ hdr,
                                    unsigned long long* protocol, DevTable t,
                                    const uint32_t* __restrict__ oslot,
                                    uint32_t* __restrict__ out_slot,
-                                   const unsigned long long* epoch) {
+                                   const unsigned long long* epoch, uint32_t* cflags) {
   pdl_entry();
   __shared__ uint64_t po[kMaxWorld + 1];
   __shared__ uint32_t ps[kMaxWorld];
@@ -895,8 +893,11 @@ __global__ void x_owner_dyn_kernel(const XHdr* __restrict__ hdr,
     const uint32_t e = static_cast<uint32_t>(*epoch - 1);
     bool bad = false;
     for (uint32_t r = 0; r < W; ++r) bad |= ld_volatile(&hdr->bad[r]) == e;
-    t.ctr[kCtrDivergence] = bad ? 1ull : 0ull;
-    t.ctr[kCtrNeedExact] = 0ull;  // a contribution that is finite applies as is
+    // the owner batch's call flags (its register keeps them); a finite contribution
+    // applies as is, so no exact check is needed
+    cflags[kCflagReject] = bad ? 1u : 0u;
+    cflags[kCflagNeedExact] = 0u;
+    if (bad) t.ctr[kCtrDivergence] = 1ull;  // sticky until reported
   }
   if (threadIdx.x == 0) {
     uint64_t run = 0;
@@ -1290,6 +1291,7 @@ void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint
   x.prefetched = false;
   fwd_route_phase(x, t, ids, n, offsets, B, F, st, /*fork_pairs=*/true);
   fwd_probe_phase(x, t, st);
+  x.generation = t->generation;
   fwd_finish_phase(x, t, st);
 }
 
@@ -1298,6 +1300,7 @@ void xbatch_prefetch(XBatch& x, Table* t, const uint64_t* ids, uint64_t n,
   require_connected(x, t->cfg.embedding_dim, n);
   fwd_route_phase(x, t, ids, n, offsets, B, F, st, /*fork_pairs=*/false);
   fwd_probe_phase(x, t, st);
+  x.generation = t->generation;
   x.prefetched = true;
 }
 
@@ -1316,6 +1319,11 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
   const PeerHdrs ph = peer_hdrs(x);
   // the pair plan ran beside the forward, whose last barrier also delivered the counts
   if (!x.counts_sent) throw Error(HPS_E_PRECONDITION, "exchange backward: no forward for this batch");
+  // the owner applies through the slots its forward probe found: a reset / restore of the
+  // table since then voids them (every rank must run the step again)
+  if (x.generation != t->generation)
+    throw Error(HPS_E_STALE_SAMPLE, "exchange backward: the table was reset or restored since "
+                                    "this batch's forward");
   x.counts_sent = false;
   const uint32_t* spos = x.pairs_spos;
   const uint32_t* slist = x.pairs_slist;
@@ -1351,7 +1359,7 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
       reinterpret_cast<const uint64_t*>(x.arena + x.off_oids), nullptr,
       reinterpret_cast<const uint32_t*>(x.arena + x.off_ppos), cap, xs.ids, xs.rv, xs.off,
       t->d.ctr + kCtrProtocol, batch_plan_view(b), reinterpret_cast<const uint32_t*>(x.arena + x.off_oslot),
-      b.slot, x.dev_epoch);
+      b.slot, x.dev_epoch, b.small + kSmallFlags);
   HPS_LAUNCH_CHECK();
   batch_register(b, xs.ids, cap, xs.off, static_cast<uint32_t>(cap), 1, nullptr, st, true,
                  /*slots_ready=*/true);

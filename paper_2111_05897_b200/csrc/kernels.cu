@@ -443,159 +443,19 @@ void launch_ckpt_restore(const DevTable& t, const uint64_t* ids, const float* ro
 
 // ---- validation before mutation (embedding_ps.hpp:146-153) --------------------------------
 
-__global__ void check_direct_kernel(const float* __restrict__ g, uint64_t n,
-                                    unsigned long long* ctr) {
+__global__ void check_direct_kernel(const float* __restrict__ g, uint64_t n, uint32_t* flag) {
   pdl_entry();
   bool bad = false;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
     bad |= !isfinite(g[i]);
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(&ctr[kCtrDivergence], 1ull);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1u);
 }
 
-void launch_check_direct(const float* grads, uint64_t n, unsigned long long* ctr,
-                         cudaStream_t st) {
+void launch_check_direct(const float* grads, uint64_t n, uint32_t* flag, cudaStream_t st) {
   if (!n) return;
   launch(check_direct_kernel, std::min<uint64_t>(ceil_div(n, 256), 148 * 8), 256, 0, st, grads, n,
-                                                                                      ctr);
-  HPS_LAUNCH_CHECK();
-}
-
-// Batch validation. Every gradient of a non-empty group feeds some contribution, so a
-// non-finite one is a certain rejection. Finite gradients can still overflow in the
-// float narrowing of a contribution: |c| <= sum_g n_g*scale_g*|grad_g|_inf
-// <= F * max_g(n_g*scale_g*|grad_g|_inf); only when that bound reaches 2^127 is the
-// exact dry run of the update kernel requested. One flat, 128-bit-vectorised pass.
-// Row groups (L lanes x V floats) walk the [B*F][D] gradient rows, kCheckILP rows in
-// flight per group; a row's group size comes from the (L2-resident) offsets.
-template <int V, int L, bool kGuard>
-__global__ void __launch_bounds__(256, 6)
-    check_batch_kernel(const float* __restrict__ grads, const uint32_t* __restrict__ offsets,
-                       uint64_t rows, uint32_t D, uint32_t F, int mean,
-                       unsigned long long* ctr, float* __restrict__ cbuf,
-                       const uint32_t* __restrict__ inv, const uint32_t* gate,
-                       const uint32_t* rows_live, int scatter_only, int l2_mode) {
-  pdl_entry();
-  if (rows_live) rows = min(rows, static_cast<uint64_t>(*rows_live));
-  using G = Geo<V, L, kGuard>;
-  constexpr int kCheckILP = 4;
-  // large plan: also scatter every listing's contribution to its sorted position, so the
-  // ordered updates read contributions contiguously instead of chasing groups per pair
-  __shared__ int s_write;
-  if (threadIdx.x == 0) s_write = cbuf && (!gate || ld_volatile(gate) > radix::kSmallN);
-  __syncthreads();
-  const bool write_c = s_write != 0;
-  if (scatter_only && !write_c) return;
-  const int ln = G::lane();
-  const int chunks = kGuard ? (D + G::kSpan - 1) / G::kSpan : 1;
-  const uint64_t groups = G::groups();
-  bool bad = false;
-  float m = 0.0f;
-  for (uint64_t r0 = G::group(); r0 < rows; r0 += groups * kCheckILP) {
-    float x[kCheckILP][V];
-    uint32_t n[kCheckILP];
-#pragma unroll
-    for (int u = 0; u < kCheckILP; ++u) {
-      const uint64_t r = r0 + u * groups;
-      n[u] = r < rows ? __ldg(offsets + r + 1) - __ldg(offsets + r) : 0u;
-    }
-    for (int c = 0; c < chunks; ++c) {
-      const uint32_t d0 = c * G::kSpan + ln * V;
-#pragma unroll
-      for (int u = 0; u < kCheckILP; ++u) {
-        // issued without waiting for the group sizes (an empty group's row is read and
-        // ignored below): the gradient stream does not serialise behind the offsets
-        const uint64_t r = r0 + u * groups;
-        if (r < rows && (!kGuard || d0 < D)) {
-          // l2_mode (HPS_CHECK_L2): 0 streaming, 1 default, 2/3/4/5 evict_last for 100/50/25/75%
-          // of the lines -- how much of the gradient stream the update kernel re-reads
-          // (once per unique row) should find in L2. Default 3: update 111 -> 107 us,
-          // check 30 -> 32 us (profiles/r1_check_l2_ab.txt)
-          if (l2_mode == 0) load_vec_cs<V>(grads + r * D + d0, x[u]);
-          else if (l2_mode == 1) load_vec<V>(grads + r * D + d0, x[u]);
-          else if (l2_mode == 2) load_vec_keep<V>(grads + r * D + d0, x[u]);
-          else if (l2_mode == 3) load_vec_keep<V, 50>(grads + r * D + d0, x[u]);
-          else if (l2_mode == 5) load_vec_keep<V, 75>(grads + r * D + d0, x[u]);
-          else load_vec_keep<V, 25>(grads + r * D + d0, x[u]);
-        }
-        else for (int j = 0; j < V; ++j) x[u][j] = 0.0f;
-      }
-      if (write_c) {
-#pragma unroll
-        for (int u = 0; u < kCheckILP; ++u) {
-          if (!n[u] || (kGuard && d0 >= D)) continue;
-          const uint64_t r = r0 + u * groups;
-          const double scale = mean ? __drcp_rn(static_cast<double>(n[u])) : 1.0;
-          float c[V];
-#pragma unroll
-          for (int j = 0; j < V; ++j)
-            c[j] = __double2float_rn(__dadd_rn(0.0, __dmul_rn(static_cast<double>(x[u][j]), scale)));
-          const uint32_t a0 = __ldg(offsets + r);
-          for (uint32_t i = a0; i < a0 + n[u]; ++i) {
-            float* dst = cbuf + static_cast<uint64_t>(inv[i]) * D + d0;
-            if (kGuard) dst[0] = c[0];
-            else store_vec<V>(dst, c);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kCheckILP; ++u) {
-        if (!n[u]) continue;  // empty group: its gradient is never used (:731)
-        float mm = 0.0f;
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-          bad |= !isfinite(x[u][j]);
-          mm = fmaxf(mm, fabsf(x[u][j]));
-        }
-        m = fmaxf(m, mean ? mm : mm * static_cast<float>(n[u]));
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  bad = __syncthreads_or(bad);
-  __shared__ float s_m[8];
-  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float bm = 0.0f;
-    for (int w = 0; w < 8; ++w) bm = fmaxf(bm, s_m[w]);
-    if (bad) atomicExch(&ctr[kCtrDivergence], 1ull);
-    if (static_cast<double>(bm) * F >= 0x1.0p127) atomicExch(&ctr[kCtrNeedExact], 1ull);
-  }
-}
-
-static int check_l2_mode() {
-  static const int m = [] {
-    const char* e = getenv("HPS_CHECK_L2");
-    return e ? atoi(e) : 3;  // profiles/r1_check_l2_ab.txt
-  }();
-  return m;
-}
-
-static uint64_t check_blocks_per_sm() {
-  static const uint64_t m = [] {
-    const char* e = getenv("HPS_CHECK_BPS");
-    return static_cast<uint64_t>(e ? std::max(1, atoi(e)) : 16);
-  }();
-  return m;
-}
-
-void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
-                        uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st,
-                        float* cbuf, const uint32_t* inv, const uint32_t* gate,
-                        const uint32_t* rows_live, bool scatter_only) {
-  const uint64_t rows = static_cast<uint64_t>(B) * F;
-  if (!rows) return;
-  if (scatter_only && !cbuf) return;
-  HPS_DISPATCH_DIM(D, {
-    uint64_t groups_per_block = 256 / L;
-    uint32_t blocks = std::min<uint64_t>(ceil_div(rows, groups_per_block * 4),
-                                         148ull * check_blocks_per_sm());
-    launch(check_batch_kernel<V, L, G>, blocks, 256, 0, st, grads, offsets, rows, D, F, mean, ctr,
-                                                        cbuf, inv, gate, rows_live,
-                                                        scatter_only ? 1 : 0, check_l2_mode());
-  });
+         flag);
   HPS_LAUNCH_CHECK();
 }
 

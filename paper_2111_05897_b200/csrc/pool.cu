@@ -100,12 +100,12 @@ __device__ void pool_general(const DevTable& t, const uint32_t* __restrict__ slo
 // kList: pool only the groups listed in glist[0 .. *glist_n) (the exchange's groups that
 // their rows' owners did not already write).
 template <int V, int L, bool kGuard, bool kList>
-__global__ void __launch_bounds__(256, 8)
+__global__ void __launch_bounds__(256)
     pool_kernel(DevTable t, const uint32_t* __restrict__ offsets,
                 const uint32_t* __restrict__ slots, uint32_t BF, uint64_t N, int mean,
                 float* __restrict__ out, uint64_t* __restrict__ out_rv64,
                 uint32_t* __restrict__ out_rv32, const uint32_t* __restrict__ glist,
-                const uint32_t* __restrict__ glist_n, int l2_mode) {
+                const uint32_t* __restrict__ glist_n) {
   pdl_entry();
   using G = Geo<V, L, kGuard>;
   const int ln = G::lane();
@@ -142,13 +142,7 @@ __global__ void __launch_bounds__(256, 8)
         if (!one[u]) continue;
         const bool ok = slot_ok(t, s[u]);
         if (ok) {
-          // l2_mode (HPS_POOL_L2): 0 default, 2/3/4 evict_last on 100/50/25% of the lines --
-          // how much of the gathered weights the push's update should find in L2
-          const float* src = t.rows + static_cast<uint64_t>(s[u]) * t.stride + ln * V;
-          if (l2_mode == 0) load_vec<V>(src, r[u]);
-          else if (l2_mode == 2) load_vec_keep<V>(src, r[u]);
-          else if (l2_mode == 3) load_vec_keep<V, 50>(src, r[u]);
-          else load_vec_keep<V, 25>(src, r[u]);
+          load_vec<V>(t.rows + static_cast<uint64_t>(s[u]) * t.stride + ln * V, r[u]);
         } else {
           for (int k = 0; k < V; ++k) r[u][k] = 0.0f;
         }
@@ -202,14 +196,6 @@ void launch_snapshot_rv(const DevTable& t, const uint32_t* slots, uint64_t n, ui
   HPS_LAUNCH_CHECK();
 }
 
-static int pool_l2_mode() {
-  static const int m = [] {
-    const char* e = getenv("HPS_POOL_L2");
-    return e ? atoi(e) : 0;
-  }();
-  return m;
-}
-
 void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slots, uint32_t BF,
                  uint64_t N, int mean, float* out, uint64_t* out_rv64, uint32_t* out_rv32,
                  cudaStream_t st, const uint32_t* glist, const uint32_t* glist_n) {
@@ -221,12 +207,12 @@ void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slo
       const uint32_t blocks = std::min<uint64_t>(ceil_div(BF, groups_per_block * kPoolILP),
                                                  148ull * 8);
       launch(pool_kernel<V, L, G, true>, blocks, 256, 0, st, t, offsets, slots, BF, N, mean, out,
-             out_rv64, out_rv32, glist, glist_n, pool_l2_mode());
+             out_rv64, out_rv32, glist, glist_n);
     } else {
       uint32_t blocks =
           std::min<uint64_t>(ceil_div(BF, groups_per_block * kPoolILP), 1u << 30);
       launch(pool_kernel<V, L, G, false>, blocks, 256, 0, st, t, offsets, slots, BF, N, mean,
-             out, out_rv64, out_rv32, nullptr, nullptr, pool_l2_mode());
+             out, out_rv64, out_rv32, nullptr, nullptr);
     }
   });
   HPS_LAUNCH_CHECK();

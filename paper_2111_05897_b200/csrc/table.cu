@@ -17,14 +17,6 @@
 
 namespace hps {
 
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("HPS_PDL");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 // ---- pointer staging --------------------------------------------------------------------
 
 PtrKind ptr_kind(const void* p) {
@@ -206,10 +198,6 @@ Table* table_create(const hps_table_cfg& cfg) {
     DeviceGuard g(t->device);
     cudaDeviceProp prop{};
     HPS_CUDA(cudaGetDeviceProperties(&prop, t->device));
-    // Optional L2 fetch-granularity hint (bytes) for random-access-heavy workloads;
-    // a device-wide setting, so only applied when asked for.
-    if (const char* g = getenv("HPS_L2_FETCH_BYTES"))
-      HPS_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, atoi(g)));
     t->sm_count = prop.multiProcessorCount;
     const uint64_t C = cfg.capacity;
     uint64_t H = 1024;
@@ -253,6 +241,9 @@ Table* table_create(const hps_table_cfg& cfg) {
 // Empties the index and the row store (LruStore::clear + PsShard state reset).
 void table_clear(Table* t, cudaStream_t st) {
   DevTable& d = t->d;
+  ++t->generation;
+  t->max_tag = 0;  // every row's bump tags are gone (kNoStep), like the reference's rings
+  t->disordered = false;
   launch_ht_clear(d, st);
   HPS_CUDA(cudaMemsetAsync(d.seen, 0, (d.capacity / 32 + 1) * sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.multi, 0, (d.capacity / 32 + 1) * sizeof(uint32_t), st));
@@ -479,7 +470,7 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
   }
   if (!b.small) {
     uint64_t c = 0;
-    ensure(b.small, c, 16);
+    ensure(b.small, c, kSmallWords);
     c = 0;
     ensure(b.small_slot, c, radix::kSmallN);
     c = 0;
@@ -514,20 +505,7 @@ static int slot_key_bits(const Table* t) {
 // Stable sort of (slot, listing) pairs by slot: every row's listings become one
 // contiguous run in apply order. keys_in0 = slots to sort (else keys_a); iota: the
 // listings are the positions 0..N-1 (else vals_a); gate = device-side condition
-// (radix_sort.cuh).
-__global__ void set_cond_kernel(cudaGraphConditionalHandle h, const void* val, int is64,
-                                unsigned long long thresh) {
-  const unsigned long long v =
-      is64 ? *static_cast<const unsigned long long*>(val) : *static_cast<const uint32_t*>(val);
-  cudaGraphSetConditional(h, v > thresh ? 1u : 0u);
-}
-
-void launch_set_cond(cudaGraphConditionalHandle h, const void* val, bool is64,
-                     unsigned long long thresh, cudaStream_t st) {
-  set_cond_kernel<<<1, 1, 0, st>>>(h, val, is64 ? 1 : 0, thresh);
-  HPS_LAUNCH_CHECK();
-}
-
+// (radix_sort.cuh): the sort's kernels exit at once when *gate <= kSmallN.
 static void sort_slots(Batch& b, const uint32_t* keys_in0, bool iota, const uint32_t* gate,
                        cudaStream_t st, bool plan_meta = false) {
   Table* t = b.table;
@@ -565,9 +543,9 @@ static void sort_slots(Batch& b, const uint32_t* keys_in0, bool iota, const uint
     sort(st, true);
     return;
   }
-  // gated large path (device count of multi listings > kSmallN): a conditional node
+  // gated large path (device count of multi listings > kSmallN)
   radix::sort_scratch_zero(b.hist, st);
-  run_if(t->side, st, gate, false, radix::kSmallN, [&](cudaStream_t s) { sort(s, false); });
+  sort(st, false);
 }
 
 // EmbeddingWorker::register_sample for a whole batch + the route/dedup/probe half of
@@ -608,7 +586,10 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   b.F = F;
   b.N = N;
   b.n_live = dynamic ? b.offsets + BF : nullptr;
-  HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
+  // the batch's device scalars (plan counts, hot-row lists, the push's call flags); an
+  // exchange owner's assembly (slots_ready) has already written the call flags
+  HPS_CUDA(cudaMemsetAsync(b.small, 0, (slots_ready ? kSmallFlags : kSmallWords) * sizeof(uint32_t),
+                           st));
   launch_expand_groups(b.offsets, static_cast<uint32_t>(BF), b.lgrp, st, b.kind);
   // Sample keys that reorder the batch: every listing takes the sorted (multi) path.
   const bool permute = d_sk && B > 1;
@@ -650,30 +631,42 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     }
     // The gated large sort (a no-op unless the device count of multi listings exceeds
     // kSmallN) needs only the slots; the pooling does not need it. It runs on the aux
-    // stream beside the pull and is joined by the pull / push (join_sort).
-    static const bool fork = [] {  // HPS_SORT_FORK=0: in line (A/B measurement)
-      const char* e = getenv("HPS_SORT_FORK");
-      return !(e && e[0] == '0');
-    }();
-    if (fork) {
-      ensure_aux(t);
-      HPS_CUDA(cudaEventRecord(t->ev_fork, st));
-      HPS_CUDA(cudaStreamWaitEvent(t->aux, t->ev_fork, 0));
-      sort_slots(b, b.slot, true, &b.small[0], t->aux, true);
-      HPS_CUDA(cudaEventRecord(t->ev_sort, t->aux));
-      b.sort_pending = true;
-      b.sort_seq = ++t->aux_seq;
-    } else {
-      sort_slots(b, b.slot, true, &b.small[0], st, true);
-    }
+    // stream beside the pull and is joined by the pull / push (join_sort; measured
+    // 0.2691 -> 0.2660 ms per C2 step against in line, profiles/r1_sort_fork_ab.txt).
+    ensure_aux(t);
+    HPS_CUDA(cudaEventRecord(t->ev_fork, st));
+    HPS_CUDA(cudaStreamWaitEvent(t->aux, t->ev_fork, 0));
+    sort_slots(b, b.slot, true, &b.small[0], t->aux, true);
+    HPS_CUDA(cudaEventRecord(t->ev_sort, t->aux));
+    b.sort_pending = true;
+    b.sort_seq = ++t->aux_seq;
   }
   b.registered = true;
+  b.generation = t->generation;
   b.pulled = false;
   stg.finish(st);
 }
 
+// Step tags of tracked applies (Table::max_tag): a tag older than one already applied
+// makes the table's delay accounting leave the latest-bump-tag fast path (see note_tag
+// users). HPS_DEVICE_STEP pushes take monotone tags from the device counter.
+static void note_tag(Table* t, uint32_t step_tag) {
+  if (step_tag < t->max_tag) t->disordered = true;
+  else t->max_tag = step_tag;
+}
+
+// A batch whose slots predate a table clear / reset / checkpoint load must not read or
+// write through them (the reference resolves ids at apply time, find_or_init).
+static void require_current(const Batch& b, const char* what) {
+  if (b.generation != b.table->generation)
+    throw Error(HPS_E_STALE_SAMPLE, std::string(what) +
+                                        ": batch registered before the table was reset or "
+                                        "restored from a checkpoint; register it again");
+}
+
 void batch_pull(Batch& b, int agg, float* out_pooled, uint64_t* out_rv, cudaStream_t st) {
   if (!b.registered) throw Error(HPS_E_STALE_SAMPLE, "pull: batch not registered");
+  require_current(b, "pull");
   Table* t = b.table;
   const uint64_t BF = static_cast<uint64_t>(b.B) * b.F;
   Stager stg(t->stage);
@@ -708,32 +701,35 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     if (accepted) *accepted = 0;
     return;
   }
+  require_current(b, "push");
+  if ((rv64 || (!untracked && b.pulled)) && !(flags & HPS_DEVICE_STEP)) note_tag(t, step_tag);
   const uint64_t BF = static_cast<uint64_t>(b.B) * b.F;
   const uint32_t D = t->cfg.embedding_dim;
   protect_reads(t, &b, st);
   Stager stg(t->stage);
   const float* d_g = static_cast<const float*>(stg.in(grads, BF * D * sizeof(float), st));
   const uint64_t* d_rv = static_cast<const uint64_t*>(stg.in(rv64, b.N * sizeof(uint64_t), st));
-  // kPushPrechecked (exchange owners): the divergence / need-exact words were set by the
-  // owner's batch assembly from what the sources found while emitting
+  // kPushPrechecked (exchange owners): the call's reject flag was set by the owner's
+  // batch assembly from what the sources found while emitting
   const bool prechecked = (flags & kPushPrechecked) != 0;
-  if (!prechecked)
-    HPS_CUDA(cudaMemsetAsync(t->d.ctr + kCtrDivergence, 0, 2 * sizeof(unsigned long long), st));
+  const bool device_step = (flags & HPS_DEVICE_STEP) != 0;
   const int mean = agg == HPS_MEAN ? 1 : 0;
-  {
-    ProfScope p(t, "check", st);
-    launch_check_batch(d_g, b.offsets, b.B, b.F, D, mean, t->d.ctr, st,
-                       b.meta_ok ? b.cbuf : nullptr, b.inv,
-                       b.all_multi ? nullptr : &b.small[0], b.n_live, prechecked);
-  }
   UpdateArgs a = plan_args(b);
   const DevTable pv = batch_plan_view(b);
   a.mean = mean;
   a.grads = d_g;
   a.lr = lr;
   a.step_tag = step_tag;
-  if (flags & HPS_DEVICE_STEP)
-    a.step_dev = reinterpret_cast<const uint32_t*>(t->d.ctr + kCtrStep);
+  a.cflags = b.small + kSmallFlags;
+  if (device_step) a.step_dev = reinterpret_cast<const uint32_t*>(t->d.ctr + kCtrStep);
+  {
+    // validation (with, for HPS_DEVICE_STEP, the step counter advanced by its last block)
+    ProfScope p(t, "check", st);
+    launch_check_batch(pv, a, b.B, b.meta_ok ? b.cbuf : nullptr, b.inv,
+                       b.all_multi ? nullptr : &b.small[0], prechecked,
+                       device_step && !prechecked ? t->d.ctr + kCtrStep : nullptr, st);
+  }
+  if (device_step && prechecked) launch_add_counter_const(t->d.ctr, kCtrStep, 1, st);
   if (d_rv) {
     a.rv64 = d_rv;
     a.tracked = 1;
@@ -742,16 +738,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     if (b.rv_valid) a.rv32 = b.rv;
     else a.fresh = 1;  // no mutation since the pull: read version == current version
   }
-  // Exact validation (dry runs), executed only if the bound check was inconclusive
-  // (never for prechecked contributions: a finite contribution applies as is).
-  if (!prechecked) {
-    a.dry_run = 1;
-    run_if(t->side, st, t->d.ctr + kCtrNeedExact, true, 0, [&](cudaStream_t s) {
-      if (!b.all_multi) launch_update_single(pv, a, t->sm_count, s);
-      launch_update(pv, a, false, t->sm_count, s);
-    });
-    a.dry_run = 0;
-  }
+
   if (t->cfg.embedding_dim <= kHotMaxDim) {
     // hot-row hand-off list (runs_kernel -> update_hot)
     a.hot = b.hot;
@@ -764,7 +751,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
       a.n_mlist = &b.small[6];
       a.mlist_cap = static_cast<uint32_t>(b.N + 1);  // (sample-key plans list singles too)
     }
-    HPS_CUDA(cudaMemsetAsync(&b.small[6], 0, 5 * sizeof(uint32_t), st));  // [6..10], one node
+    // (the counters b.small[6..10] were zeroed by the batch's register)
   }
   if (!b.all_multi) {
     // Rows listed more than once (ordered chains, latency-bound, few) and rows listed
@@ -794,7 +781,6 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     launch_update(pv, a, false, t->sm_count, st);
     launch_update_hot(pv, a, t->sm_count, st);
   }
-  if (flags & HPS_DEVICE_STEP) launch_add_counter_const(t->d.ctr, kCtrStep, 1, st);
   forget_outstanding(b);
   b.pulled = false;
   b.rv_valid = false;
@@ -869,13 +855,14 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
   const float* d_g = static_cast<const float*>(stg.in(grads, n * D * sizeof(float), st));
   const uint64_t* d_rv = static_cast<const uint64_t*>(stg.in(rv, n * sizeof(uint64_t), st));
   uint32_t* d_dl = static_cast<uint32_t*>(stg.out(out_delays, n * sizeof(uint32_t)));
-  HPS_CUDA(cudaMemsetAsync(t->d.ctr + kCtrDivergence, 0, 2 * sizeof(unsigned long long), st));
-  HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
+  HPS_CUDA(cudaMemsetAsync(b.small, 0, kSmallWords * sizeof(uint32_t), st));
   // Validate before anything mutates -- including lazy inserts (embedding_ps.hpp:146-156).
-  launch_check_direct(d_g, n * D, t->d.ctr, st);
-  read_counters(t, st);
-  if (t->h_ctr[kCtrDivergence]) {
-    HPS_CUDA(cudaMemsetAsync(t->d.ctr + kCtrDivergence, 0, sizeof(unsigned long long), st));
+  launch_check_direct(d_g, n * D, b.small + kSmallFlags + kCflagReject, st);
+  uint32_t bad = 0;
+  HPS_CUDA(cudaMemcpyAsync(&bad, b.small + kSmallFlags + kCflagReject, sizeof(bad),
+                           cudaMemcpyDeviceToHost, st));
+  HPS_CUDA(cudaStreamSynchronize(st));
+  if (bad) {
     stg.finish(st);
     throw Error(HPS_E_DIVERGENCE, "PsShard::apply_gradients: non-finite gradient");
   }
@@ -898,6 +885,7 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
     stg.finish(st);
     return;
   }
+  if (d_rv) note_tag(t, step_tag);
   protect_reads(t, nullptr, st);
   forget_outstanding(b);
   b.pulled = false;

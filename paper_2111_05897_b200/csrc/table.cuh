@@ -28,8 +28,9 @@ enum CounterIdx : int {
   kCtrClockResets = 1,
   kCtrStaleDrops = 2,
   kCtrOverflow = 3,    // sticky: capacity exhausted (no LRU eviction on device)
-  kCtrDivergence = 4,  // per-call: non-finite contribution seen by validation
-  kCtrNeedExact = 5,   // per-call: bound check inconclusive -> exact dry run
+  kCtrDivergence = 4,  // sticky until reported: some push was rejected (non-finite /
+                       //   overflowing contribution); its own gate is the call flag
+  kCtrUnused5 = 5,
   kCtrMaxDelay = 6,
   kCtrDelayHist = 7,   // 17 words: delays 0..15, >=16
   kCtrProtocol = 24,   // sticky until reported: malformed exchange input (exchange.cu)
@@ -153,7 +154,9 @@ struct Batch {
   uint32_t* small_listing = nullptr;
   uint32_t* hist = nullptr;       // sort / plan scratch
   size_t hist_cap = 0;
-  uint32_t* small = nullptr;      // device scalars: [0] multi listings, [2] rows inserted, [6] multi-list rows, [8..10] hot lists
+  // device scalars (kSmallWords, zeroed by register): [0] multi listings, [2] rows
+  // inserted, [6] multi-list rows, [8..10] hot lists, [16..18] the push's call flags
+  uint32_t* small = nullptr;
   bool all_multi = false;         // plan skipped: every listing on the sorted path
   bool rv_valid = false;          // rv holds the pull-time versions (else: no mutation since)
   // sample-order permutation (sample_keys != NULL)
@@ -164,6 +167,7 @@ struct Batch {
   uint32_t* sstart = nullptr;
   bool pulled = false;
   bool registered = false;
+  uint64_t generation = 0;        // Table::generation at register (slots valid only then)
   bool sort_pending = false;      // the plan's gated large sort runs on the table's aux
                                   // stream beside the pooling; joined before its use
   uint64_t sort_seq = 0;          // its position in the aux stream's work (Table::aux_seq)
@@ -236,6 +240,13 @@ struct Table {
   // aux-stream bookkeeping: forks so far, and the newest fork some push already joined
   // back into stream `aux_joined` (later work there needs no further join)
   uint64_t aux_seq = 0, aux_joined_seq = 0;
+  // Bumped whenever the slot numbering is rebuilt (clear / reset / checkpoint load): a
+  // batch registered under an older generation names slots that may now hold other rows.
+  uint64_t generation = 0;
+  // Newest host step tag a tracked apply used, and whether some tracked apply used an
+  // older one since the last clear (out-of-order steps: hybrid stragglers).
+  uint32_t max_tag = 0;
+  bool disordered = false;
   cudaStream_t aux_joined = nullptr;
   Batch scratch;  // workspace for the stateless entry points
   StagePool stage;
@@ -314,18 +325,17 @@ void launch_ckpt_restore(const DevTable& t, const uint64_t* ids, const float* ro
                          uint32_t* new_count, cudaStream_t st);
 void launch_snapshot_rv(const DevTable& t, const uint32_t* slots, uint64_t n, uint32_t* rv,
                         cudaStream_t st);
-void launch_check_direct(const float* grads, uint64_t n_floats, unsigned long long* ctr,
+void launch_check_direct(const float* grads, uint64_t n_floats, uint32_t* flag,
                          cudaStream_t st);
-// cbuf/inv (optional, large plan only): also writes every listing's contribution to
-// cbuf[inv[listing]] when the plan gate (*gate > kSmallN, or gate == null) is open.
-// scatter_only: the caller validated the contributions already (exchange owners: the
-// sources checked them while emitting); only the large plan's scatter runs, and the
-// launch is a no-op when the plan is small.
-void launch_check_batch(const float* grads, const uint32_t* offsets, uint32_t B, uint32_t F,
-                        uint32_t D, int mean, unsigned long long* ctr, cudaStream_t st,
-                        float* cbuf = nullptr, const uint32_t* inv = nullptr,
-                        const uint32_t* gate = nullptr, const uint32_t* rows_live = nullptr,
-                        bool scatter_only = false);
+// Per-call flag words of a push (uint32, in the batch's device scalars, zeroed by its
+// register): kCflagReject = a contribution is non-finite or overflows -- the call's
+// updates are gated off (the table's sticky kCtrDivergence is raised too, so an
+// HPS_ASYNC push's rejection surfaces at the next sync); kCflagNeedExact = the
+// validation's bound was inconclusive (the exact check ran in the check kernel's last
+// block); kCflagDone = block-completion counter of the check kernel.
+constexpr int kCflagReject = 0, kCflagNeedExact = 1, kCflagDone = 2;
+constexpr int kSmallFlags = 16;  // Batch::small[16..18]: the push's call flags
+constexpr int kSmallWords = 32;
 
 struct UpdateArgs {
   // Multi kernel input: either the large-path slot sort of all n listings, or -- when
@@ -352,10 +362,12 @@ struct UpdateArgs {
   uint32_t* out_delays;  // direct mode, per entry
   float lr;
   uint32_t step_tag;
-  const uint32_t* step_dev;  // HPS_DEVICE_STEP: tag = *step_dev + 1 (table step counter)
+  // HPS_DEVICE_STEP: tag = *step_dev (the table step counter, advanced by this push's
+  // check kernel before any update kernel reads it)
+  const uint32_t* step_dev;
+  uint32_t* cflags;  // this call's flag words (kCflag*), or null
   int tracked;
   int fresh;  // tracked, and no mutation since the pull: read version = current version
-  int dry_run;  // compute + validate contributions only
   // Hot rows (runs of >= kHotRun listings on the sorted path): update_multi hands them to
   // update_hot (one block per row, contributions staged in shared memory); null = off.
   uint32_t* hot;
@@ -376,6 +388,20 @@ struct UpdateArgs {
 constexpr uint32_t kHotRun = 64;
 constexpr uint32_t kVeryHotRun = 1024;
 constexpr uint32_t kHotMaxDim = 128;  // update_hot stages [256][D] floats in shared memory
+// Validation before mutation (embedding_ps.hpp:146-156) of a batch push: every gradient
+// finite, and the fan-out's float narrowing bounded (else the exact check of every pair
+// contribution runs in the kernel's last block). Reads a.grads [B*F][D] with a.offsets,
+// a.F, a.mean, a.n_live; flags into a.cflags (+ the table's sticky kCtrDivergence).
+// step_ctr (HPS_DEVICE_STEP): the last block advances the table's step counter, which
+// the update kernels then read as their tag.
+// cbuf/inv (optional, large plan only): also writes every listing's contribution to
+// cbuf[inv[listing]] when the plan gate (*gate > kSmallN, or gate == null) is open.
+// scatter_only: the caller validated the contributions already (exchange owners: the
+// sources checked them while emitting); only the large plan's scatter runs, and the
+// launch is a no-op when the plan is small.
+void launch_check_batch(const DevTable& t, const UpdateArgs& a, uint32_t B, float* cbuf,
+                        const uint32_t* inv, const uint32_t* gate, bool scatter_only,
+                        unsigned long long* step_ctr, cudaStream_t st);
 void launch_update_hot(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
 void launch_runs(const UpdateArgs& a, int sms, cudaStream_t st);
 void launch_update(const DevTable& t, const UpdateArgs& a, bool direct, int sms, cudaStream_t st);

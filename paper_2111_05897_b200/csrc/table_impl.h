@@ -47,55 +47,6 @@ class Stager {
   bool sync_needed_ = false;
 };
 
-// ---- device-decided work (table.cu) ----------------------------------------------------
-void launch_set_cond(cudaGraphConditionalHandle h, const void* val, bool is64,
-                     unsigned long long thresh, cudaStream_t st);
-
-// Eager: `body` is launched on st as is (its kernels read the gate themselves and exit
-// when it is closed). Under CUDA-graph capture with HPS_GRAPH_COND=1: a conditional IF node whose body graph is
-// captured from `body`, switched by a one-thread kernel comparing *val (u32 or u64) with
-// thresh -- a closed gate then costs no launches at all. `side` is a stream owned by the
-// caller (used for the body's capture only).
-template <class Fn>
-void run_if(cudaStream_t& side, cudaStream_t st, const void* val, bool is64,
-            unsigned long long thresh, Fn&& body) {
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  HPS_CUDA(cudaStreamIsCapturing(st, &cs));
-  // Opt-in: measured on B200, a conditional node costs more (~7.5 us per step each) than
-  // the device-gated launches it removes (~2.5 us each), so captures keep the gated
-  // kernels unless HPS_GRAPH_COND=1.
-  static const bool enabled = getenv("HPS_GRAPH_COND") != nullptr;
-  if (cs != cudaStreamCaptureStatusActive || !enabled) {
-    body(st);
-    return;
-  }
-  cudaGraph_t g = nullptr;
-  const cudaGraphNode_t* deps = nullptr;
-  size_t nd = 0;
-  unsigned long long id = 0;
-  HPS_CUDA(cudaStreamGetCaptureInfo(st, &cs, &id, &g, &deps, &nd));
-  cudaGraphConditionalHandle h;
-  HPS_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
-  launch_set_cond(h, val, is64, thresh, st);
-  HPS_CUDA(cudaStreamGetCaptureInfo(st, &cs, &id, &g, &deps, &nd));
-  cudaGraphNodeParams p{};
-  p.type = cudaGraphNodeTypeConditional;
-  p.conditional.handle = h;
-  p.conditional.type = cudaGraphCondTypeIf;
-  p.conditional.size = 1;
-  cudaGraphNode_t node;
-  HPS_CUDA(cudaGraphAddNode(&node, g, deps, nd, &p));
-  if (!side) HPS_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-  HPS_CUDA(cudaStreamBeginCaptureToGraph(side, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                         cudaStreamCaptureModeThreadLocal));
-  const uint64_t l0 = g_launches.load();
-  body(side);
-  g_launches.store(l0);  // a conditional body only runs when its gate opens
-  cudaGraph_t body_graph = nullptr;
-  HPS_CUDA(cudaStreamEndCapture(side, &body_graph));
-  HPS_CUDA(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
-}
-
 Table* table_create(const hps_table_cfg& cfg);
 void table_destroy(Table* t);
 void table_clear(Table* t, cudaStream_t st);
@@ -208,6 +159,7 @@ struct XBatch {
   uint64_t cap_pnew = 0;
   const uint32_t *pairs_spos = nullptr, *pairs_slist = nullptr;
   uint64_t max_ids = 0;
+  uint64_t generation = 0;  // owner table's generation at this batch's forward probe
   uint32_t arena_dim = 0, rank = 0;
   bool connected = false;
   uint64_t* xbase = nullptr;

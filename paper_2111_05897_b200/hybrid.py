@@ -73,6 +73,10 @@ class HybridTrainer:
         self.flags = hps.ASYNC | (hps.DEVICE_STEP if device_step else 0)
         self.pending = []  # (step, worker slot, batch) pushes held back by the window
         self._bufs = {}
+        # sticky device flag: some step's loss or dense gradient was non-finite (the
+        # reference raises DivergenceError there, dense_nn.hpp:233,268, and the training
+        # loop aborts, orchestrator.hpp:786-788); reported by check() / flush()
+        self._diverged = torch.zeros((), dtype=torch.bool, device=self.device)
 
     # -- buffers: one per in-flight batch ----------------------------------------------
     def _buf(self, k: int, B: int):
@@ -145,6 +149,7 @@ class HybridTrainer:
                 input_cols=self.F * self.D)
             g = allreduce_mean(self.tower.grad, self.group)
             finite = t.isfinite(g).all()
+            self._diverged |= ~(finite & t.isfinite(loss))
             self.tower.sgd_step(g, self.dense_lr, finite=finite)
             b["graded"].record(self.dense_stream)
         self.pending.append((s, k, B))
@@ -159,8 +164,21 @@ class HybridTrainer:
         main.wait_stream(self.dense_stream)
         main.wait_stream(self.emb_stream)
 
+    def check(self):
+        """Raises DivergenceError if any step so far saw a non-finite loss or dense
+        gradient (its dense update was skipped; host round trip, not capturable). The
+        embedding side reports its own rejections through ``table.sync()``."""
+        t = self.torch
+        self.dense_stream.synchronize()
+        if bool(self._diverged.item()):
+            self._diverged.zero_()
+            raise hps.DivergenceError("hybrid step: non-finite loss or dense gradient; the "
+                                      "dense update of that step was not applied")
+
     def flush(self):
-        """Issues the pushes still held back by the staleness window."""
+        """Issues the pushes still held back by the staleness window, then reports a
+        diverged dense step (check())."""
         while self.pending:
             self._push(*self.pending.pop(0))
         self.sync()
+        self.check()
