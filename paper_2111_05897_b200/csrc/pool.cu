@@ -55,37 +55,28 @@ __device__ void pool_general(const DevTable& t, const uint32_t* __restrict__ slo
     double acc[V];
 #pragma unroll
     for (int k = 0; k < V; ++k) acc[k] = 0.0;
-    uint32_t i = a;
-    // Two listings in flight per iteration for memory-level parallelism.
-    for (; i + 1 < e; i += 2) {
-      uint32_t s0 = slots[i], s1 = slots[i + 1];
-      float r0[V], r1[V];
-      if (slot_ok(t, s0)) load_vec<V>(t.rows + (uint64_t)s0 * t.stride + d0, r0);
-      else for (int k = 0; k < V; ++k) r0[k] = 0.0f;
-      if (slot_ok(t, s1)) load_vec<V>(t.rows + (uint64_t)s1 * t.stride + d0, r1);
-      else for (int k = 0; k < V; ++k) r1[k] = 0.0f;
+    // Four listings in flight per iteration for memory-level parallelism; the fp64 sum
+    // still runs in listing order.
+    for (uint32_t i0 = a; i0 < e; i0 += 4) {
+      uint32_t sl[4];
+      float r[4][V];
 #pragma unroll
-      for (int k = 0; k < V; ++k) {
-        acc[k] = __dadd_rn(acc[k], static_cast<double>(r0[k]));
-        acc[k] = __dadd_rn(acc[k], static_cast<double>(r1[k]));
-      }
-      if (want_rv && c == 0 && ln == 0) {
-        uint32_t v0 = slot_ok(t, s0) ? vt_read(t, s0).x : 0, v1 = slot_ok(t, s1) ? vt_read(t, s1).x : 0;
-        if (out_rv64) out_rv64[i] = v0, out_rv64[i + 1] = v1;
-        if (out_rv32) out_rv32[i] = v0, out_rv32[i + 1] = v1;
-      }
-    }
-    if (i < e) {
-      uint32_t s0 = slots[i];
-      float r0[V];
-      if (slot_ok(t, s0)) load_vec<V>(t.rows + (uint64_t)s0 * t.stride + d0, r0);
-      else for (int k = 0; k < V; ++k) r0[k] = 0.0f;
+      for (int u = 0; u < 4; ++u) sl[u] = i0 + u < e ? slots[i0 + u] : kInvalidSlot;
 #pragma unroll
-      for (int k = 0; k < V; ++k) acc[k] = __dadd_rn(acc[k], static_cast<double>(r0[k]));
-      if (want_rv && c == 0 && ln == 0) {
-        uint32_t v0 = slot_ok(t, s0) ? vt_read(t, s0).x : 0;
-        if (out_rv64) out_rv64[i] = v0;
-        if (out_rv32) out_rv32[i] = v0;
+      for (int u = 0; u < 4; ++u) {
+        if (slot_ok(t, sl[u])) load_vec<V>(t.rows + (uint64_t)sl[u] * t.stride + d0, r[u]);
+        else for (int k = 0; k < V; ++k) r[u][k] = 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i0 + u >= e) break;
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] = __dadd_rn(acc[k], static_cast<double>(r[u][k]));
+        if (want_rv && c == 0 && ln == 0) {
+          const uint32_t v0 = slot_ok(t, sl[u]) ? vt_read(t, sl[u]).x : 0;
+          if (out_rv64) out_rv64[i0 + u] = v0;
+          if (out_rv32) out_rv32[i0 + u] = v0;
+        }
       }
     }
     float o[V];
@@ -96,6 +87,92 @@ __device__ void pool_general(const DevTable& t, const uint32_t* __restrict__ slo
 }
 
 }  // namespace
+
+// Warp-cooperative pooling (D a multiple of 4 up to 128, or 1 / 2): a warp takes 32
+// consecutive segments; lane l loads segment l's bounds and -- when it is a one-listing
+// segment, every segment of a one-hot batch -- its slot (and read version), coalesced.
+// Then the warp's row groups (L lanes x V floats, G per warp) gather those rows, kB rows
+// in flight per lane with their owners' slots by shuffle, and write out[sg] = row + 0.0f:
+// the fp64 sum of one listing, (float)((0.0 + (double)x) * 1.0), is x with -0.0 -> +0.0.
+// The other segments (empty, several listings) go to pool_general group by group.
+// kList: pool only the groups listed in glist[0 .. *glist_n) (the exchange's groups that
+// their rows' owners did not already write).
+template <int V, int L, bool kList>
+__global__ void __launch_bounds__(256)
+    pool_warp_kernel(DevTable t, const uint32_t* __restrict__ offsets,
+                     const uint32_t* __restrict__ slots, uint32_t BF, uint64_t N, int mean,
+                     float* __restrict__ out, uint64_t* __restrict__ out_rv64,
+                     uint32_t* __restrict__ out_rv32, const uint32_t* __restrict__ glist,
+                     const uint32_t* __restrict__ glist_n) {
+  pdl_entry();
+  constexpr int G = 32 / L;      // row groups per warp
+  constexpr int kPer = 32 / G;   // one-listing segments per group per chunk
+  constexpr int kB = kPer < 8 ? kPer : 8;
+  const uint32_t lane = threadIdx.x & 31, grp = lane / L, ln = lane % L;
+  const uint32_t D = t.D;
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t count = kList ? *glist_n : BF;
+  const bool want_rv = out_rv64 || out_rv32;
+  for (uint64_t c0 = warp * 32; c0 < count; c0 += warps * 32) {
+    const uint64_t k = c0 + lane;
+    const bool live = k < count;
+    const uint32_t sg = kList ? (live ? glist[k] : 0u) : static_cast<uint32_t>(k);
+    const uint32_t a = live ? offsets[sg] : 0u, e = live ? offsets[sg + 1] : 0u;
+    const bool one = live && e == a + 1;
+    const uint32_t slot = one ? slots[a] : kInvalidSlot;
+    if (want_rv && one) {
+      const uint32_t v = slot_ok(t, slot) ? vt_read(t, slot).x : 0u;
+      if (out_rv64) out_rv64[a] = v;
+      if (out_rv32) out_rv32[a] = v;
+    }
+#pragma unroll
+    for (int i0 = 0; i0 < kPer; i0 += kB) {
+      float r[kB][V];
+      uint32_t so[kB];
+      bool on[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int j = (i0 + u) * G + grp;
+        const uint32_t s = __shfl_sync(0xffffffffu, slot, j);
+        so[u] = __shfl_sync(0xffffffffu, sg, j);
+        on[u] = __shfl_sync(0xffffffffu, one ? 1 : 0, j) != 0;
+        if (on[u] && slot_ok(t, s)) load_vec<V>(t.rows + static_cast<uint64_t>(s) * t.stride + ln * V, r[u]);
+        else for (int q = 0; q < V; ++q) r[u][q] = 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        if (!on[u]) continue;
+        float o[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) o[q] = __fadd_rn(r[u][q], 0.0f);
+        store_vec_cs<V>(out + static_cast<uint64_t>(so[u]) * D + ln * V, o);
+      }
+    }
+    // empty and several-listing segments: the g-th pending one goes to group g
+    uint32_t rest = __ballot_sync(0xffffffffu, live && !one);
+    while (rest) {
+      uint32_t pick = rest;
+      int mine = -1;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int j = pick ? __ffs(pick) - 1 : -1;
+        if (g == static_cast<int>(grp)) mine = j;
+        if (pick) pick &= pick - 1;
+      }
+      rest = pick;
+      const int src = mine < 0 ? 0 : mine;
+      const uint32_t msg = __shfl_sync(0xffffffffu, sg, src);
+      const uint32_t ma = __shfl_sync(0xffffffffu, a, src);
+      const uint32_t me = __shfl_sync(0xffffffffu, e, src);
+      if (mine >= 0) {
+        // Empty groups pool to zeros (embedding_worker.hpp:543): keep scale finite there.
+        const double scale = (mean && me > ma) ? __drcp_rn(static_cast<double>(me - ma)) : 1.0;
+        pool_general<V, L, false>(t, slots, msg, ma, me, scale, ln, out, out_rv64, out_rv32);
+      }
+    }
+  }
+}
 
 // kList: pool only the groups listed in glist[0 .. *glist_n) (the exchange's groups that
 // their rows' owners did not already write).
@@ -201,18 +278,28 @@ void launch_pool(const DevTable& t, const uint32_t* offsets, const uint32_t* slo
                  cudaStream_t st, const uint32_t* glist, const uint32_t* glist_n) {
   if (!BF) return;
   HPS_DISPATCH_DIM(t.D, {
-    uint64_t groups_per_block = 256 / L;
-    if (glist) {
-      // list length is device-side: one wave of blocks strides over it
+    if constexpr (!G) {
+      // warp-cooperative: one resident wave of blocks strides over 32-segment chunks
+      static int per_sm = 0;
+      auto k = glist ? pool_warp_kernel<V, L, true> : pool_warp_kernel<V, L, false>;
+      if (!per_sm) HPS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0));
+      int dev = 0, sms = 148;
+      HPS_CUDA(cudaGetDevice(&dev));
+      HPS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const uint32_t blocks = static_cast<uint32_t>(std::max<uint64_t>(
+          1, std::min<uint64_t>(ceil_div(BF, 256), static_cast<uint64_t>(sms) * per_sm)));
+      launch(k, blocks, 256, 0, st, t, offsets, slots, BF, N, mean, out, out_rv64, out_rv32,
+             glist, glist_n);
+    } else {
+      uint64_t groups_per_block = 256 / L;
       const uint32_t blocks = std::min<uint64_t>(ceil_div(BF, groups_per_block * kPoolILP),
                                                  148ull * 8);
-      launch(pool_kernel<V, L, G, true>, blocks, 256, 0, st, t, offsets, slots, BF, N, mean, out,
-             out_rv64, out_rv32, glist, glist_n);
-    } else {
-      uint32_t blocks =
-          std::min<uint64_t>(ceil_div(BF, groups_per_block * kPoolILP), 1u << 30);
-      launch(pool_kernel<V, L, G, false>, blocks, 256, 0, st, t, offsets, slots, BF, N, mean,
-             out, out_rv64, out_rv32, nullptr, nullptr);
+      if (glist)
+        launch(pool_kernel<V, L, G, true>, blocks, 256, 0, st, t, offsets, slots, BF, N, mean,
+               out, out_rv64, out_rv32, glist, glist_n);
+      else
+        launch(pool_kernel<V, L, G, false>, blocks, 256, 0, st, t, offsets, slots, BF, N, mean,
+               out, out_rv64, out_rv32, nullptr, nullptr);
     }
   });
   HPS_LAUNCH_CHECK();

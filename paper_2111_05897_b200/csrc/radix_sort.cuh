@@ -243,7 +243,6 @@ struct SortMeta {
   const uint32_t* lgrp = nullptr;
   const uint32_t* offsets = nullptr;
   uint64_t* out = nullptr;
-  uint32_t* inv = nullptr;  // inv[v] = g: the sorted position of each value (optional)
 };
 
 // vals_in == nullptr: values are the input positions (pass 0 of an index sort).
@@ -353,7 +352,6 @@ __global__ void __launch_bounds__(kBlock)
     if (meta.out) {  // final pass: per sorted position, the listing's group and its size
       const uint32_t lg = meta.lgrp[svals[p]];
       meta.out[g] = lg | (static_cast<uint64_t>(meta.offsets[lg + 1] - meta.offsets[lg]) << 32);
-      if (meta.inv) meta.inv[svals[p]] = g;
     }
   }
 }

@@ -219,6 +219,7 @@ Table* table_create(const hps_table_cfg& cfg) {
     HPS_CUDA(cudaMalloc(&d.seen, (C / 32 + 1) * sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.multi, (C / 32 + 1) * sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.slot_id, C * sizeof(uint64_t)));
+    HPS_CUDA(cudaMalloc(&d.ring, C * kTagRing * sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.special, sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.hwm, sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.ctr, kCtrCount * sizeof(unsigned long long)));
@@ -244,6 +245,7 @@ void table_clear(Table* t, cudaStream_t st) {
   ++t->generation;
   t->max_tag = 0;  // every row's bump tags are gone (kNoStep), like the reference's rings
   t->disordered = false;
+  t->untracked_seen = false;
   launch_ht_clear(d, st);
   HPS_CUDA(cudaMemsetAsync(d.seen, 0, (d.capacity / 32 + 1) * sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.multi, 0, (d.capacity / 32 + 1) * sizeof(uint32_t), st));
@@ -311,7 +313,7 @@ void batch_free(Batch& b) {
   b.seen = b.multi = nullptr;
   void* ptrs[] = {b.offsets, b.lgrp,  b.slot,   b.keys_a,  b.vals_a,
                   b.keys_b,  b.vals_b, b.rv,  b.new_slots, b.kind,  b.hist,
-                  b.mkeys,   b.hot, b.mlist, b.meta, b.inv, b.cbuf, b.small_slot, b.small_listing,
+                  b.mkeys,   b.hot, b.mlist, b.meta, b.small_slot, b.small_listing,
                   b.small,   b.skeys_a, b.skeys_b, b.sperm_a, b.sperm_b, b.sstart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -331,7 +333,7 @@ void table_destroy(Table* t) {
     t->stage.free_all();
     t->prof.destroy();
     DevTable& d = t->d;
-    void* ptrs[] = {d.ht,  d.rows, d.seen,     d.multi,    d.slot_id, d.special,
+    void* ptrs[] = {d.ht,  d.rows, d.seen,     d.multi,    d.slot_id, d.ring, d.special,
                     d.hwm, d.ctr,  t->d_salts, t->xs.ids, t->xs.rv,  t->xs.off};
     for (void* p : ptrs)
       if (p) cudaFree(p);
@@ -432,8 +434,6 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
     ensure(b.mlist, c, n + 1);
     c = 0;
     ensure(b.meta, c, n);
-    c = 0;
-    ensure(b.inv, c, n);
     size_t hw = radix::scratch_words<uint32_t>(n);
     if (hw > b.hist_cap) {
       c = 0;
@@ -493,7 +493,6 @@ static UpdateArgs plan_args(const Batch& b) {
   a.offsets = b.offsets;
   a.F = b.F;
   a.meta = b.meta_ok ? b.meta : nullptr;
-  a.cbuf = b.meta_ok ? b.cbuf : nullptr;
   a.n_live = b.n_live;
   return a;
 }
@@ -522,15 +521,6 @@ static void sort_slots(Batch& b, const uint32_t* keys_in0, bool iota, const uint
     meta.lgrp = b.lgrp;
     meta.offsets = b.offsets;
     meta.out = b.meta;
-    meta.inv = b.inv;
-    // contribution buffer (grown, never shrunk): the large plan's updates read it
-    const uint64_t want = b.N * t->cfg.embedding_dim;
-    if (want > b.cap_cbuf) {
-      if (b.cbuf) HPS_CUDA(cudaFree(b.cbuf));
-      b.cbuf = nullptr;
-      HPS_CUDA(cudaMalloc(&b.cbuf, want * sizeof(float)));
-      b.cap_cbuf = want;
-    }
   }
   auto sort = [&](cudaStream_t s, bool zero) {
     bool in_b = radix::sort_pairs<uint32_t>(b.keys_a, b.vals_a, b.keys_b, b.vals_b, b.N, kb,
@@ -722,14 +712,13 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
   a.step_tag = step_tag;
   a.cflags = b.small + kSmallFlags;
   if (device_step) a.step_dev = reinterpret_cast<const uint32_t*>(t->d.ctr + kCtrStep);
-  {
+  if (!prechecked) {
     // validation (with, for HPS_DEVICE_STEP, the step counter advanced by its last block)
     ProfScope p(t, "check", st);
-    launch_check_batch(pv, a, b.B, b.meta_ok ? b.cbuf : nullptr, b.inv,
-                       b.all_multi ? nullptr : &b.small[0], prechecked,
-                       device_step && !prechecked ? t->d.ctr + kCtrStep : nullptr, st);
+    launch_check_batch(pv, a, b.B, device_step ? t->d.ctr + kCtrStep : nullptr, st);
+  } else if (device_step) {
+    launch_add_counter_const(t->d.ctr, kCtrStep, 1, st);
   }
-  if (device_step && prechecked) launch_add_counter_const(t->d.ctr, kCtrStep, 1, st);
   if (d_rv) {
     a.rv64 = d_rv;
     a.tracked = 1;
@@ -738,6 +727,8 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     if (b.rv_valid) a.rv32 = b.rv;
     else a.fresh = 1;  // no mutation since the pull: read version == current version
   }
+  if (!a.tracked) t->untracked_seen = true;
+  a.exact = t->disordered || t->untracked_seen;
 
   if (t->cfg.embedding_dim <= kHotMaxDim) {
     // hot-row hand-off list (runs_kernel -> update_hot)
@@ -903,6 +894,8 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
   a.grads = d_g;
   a.rv64 = d_rv;
   a.tracked = d_rv ? 1 : 0;
+  if (!d_rv) t->untracked_seen = true;
+  a.exact = t->disordered || t->untracked_seen;
   a.out_delays = d_dl;
   a.lr = lr;
   a.step_tag = step_tag;

@@ -95,6 +95,11 @@ struct DevTable {
   uint32_t* seen;
   uint32_t* multi;
   uint64_t* slot_id;
+  // [C][kTagRing] step tags of each row's latest version bumps (PsShard::tag_ring_
+  // embedding_ps.hpp:493-494): written at every bump (one 4-byte store), read only when
+  // the delay needs the exact count (UpdateArgs::exact) or an untracked write moves the
+  // version onto an older ring entry.
+  uint32_t* ring;
   uint32_t capacity;
   uint32_t* hwm;
   unsigned long long* ctr;
@@ -147,9 +152,6 @@ struct Batch {
   // dynamic batches (one listing per live group, live groups first): the live count is
   // offsets[B*F] on the device; kernels bound their loops by it
   const uint32_t* n_live = nullptr;
-  uint32_t* inv = nullptr;        // [N] large path: sorted position of each listing
-  float* cbuf = nullptr;          // [N][D] large path: contribution per sorted position
-  uint64_t cap_cbuf = 0;
   uint32_t* small_slot = nullptr;       // [kSmallN] multi listings sorted (small path)
   uint32_t* small_listing = nullptr;
   uint32_t* hist = nullptr;       // sort / plan scratch
@@ -247,6 +249,7 @@ struct Table {
   // older one since the last clear (out-of-order steps: hybrid stragglers).
   uint32_t max_tag = 0;
   bool disordered = false;
+  bool untracked_seen = false;  // some untracked write (version += 1 without a ring entry)
   cudaStream_t aux_joined = nullptr;
   Batch scratch;  // workspace for the stateless entry points
   StagePool stage;
@@ -368,6 +371,9 @@ struct UpdateArgs {
   uint32_t* cflags;  // this call's flag words (kCflag*), or null
   int tracked;
   int fresh;  // tracked, and no mutation since the pull: read version = current version
+  // count delays from the tag ring (count_delay exactly) instead of the latest bump tag:
+  // needed once step tags went out of order or untracked writes happened on the table
+  int exact;
   // Hot rows (runs of >= kHotRun listings on the sorted path): update_multi hands them to
   // update_hot (one block per row, contributions staged in shared memory); null = off.
   uint32_t* hot;
@@ -381,9 +387,6 @@ struct UpdateArgs {
   const uint64_t* meta;
   // dynamic batches: live listings (= live groups) on the device; null = a.n
   const uint32_t* n_live;
-  // large path: per sorted position, float(0.0 + (double)g * scale) of its listing, written
-  // by the validation pass (right for pairs of one listing; longer pairs are summed here)
-  const float* cbuf;
 };
 constexpr uint32_t kHotRun = 64;
 constexpr uint32_t kVeryHotRun = 1024;
@@ -394,13 +397,7 @@ constexpr uint32_t kHotMaxDim = 128;  // update_hot stages [256][D] floats in sh
 // a.F, a.mean, a.n_live; flags into a.cflags (+ the table's sticky kCtrDivergence).
 // step_ctr (HPS_DEVICE_STEP): the last block advances the table's step counter, which
 // the update kernels then read as their tag.
-// cbuf/inv (optional, large plan only): also writes every listing's contribution to
-// cbuf[inv[listing]] when the plan gate (*gate > kSmallN, or gate == null) is open.
-// scatter_only: the caller validated the contributions already (exchange owners: the
-// sources checked them while emitting); only the large plan's scatter runs, and the
-// launch is a no-op when the plan is small.
-void launch_check_batch(const DevTable& t, const UpdateArgs& a, uint32_t B, float* cbuf,
-                        const uint32_t* inv, const uint32_t* gate, bool scatter_only,
+void launch_check_batch(const DevTable& t, const UpdateArgs& a, uint32_t B,
                         unsigned long long* step_ctr, cudaStream_t st);
 void launch_update_hot(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
 void launch_runs(const UpdateArgs& a, int sms, cudaStream_t st);
