@@ -194,7 +194,8 @@ def workload_config(cfg, args, ref_sample=None):
          "global_batch": cfg.batch * args.gpus, "rows": cfg.table_capacity(), "dim": cfg.dim,
          "features": cfg.features, "logical_shards": cfg.shards,
          "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single",
-         "l2": "per-step footprint > L2 (126 MB); no flush"}
+         "l2": "per-step footprint > L2 (126 MB); no flush",
+         "table": "in-order step tags, latest-bump-tag delays (no HPS_TABLE_TAG_RING)"}
     if ref_sample:
         d["reference_sample_batch"] = ref_sample
     return d
@@ -226,7 +227,10 @@ def run_hybrid(args, world, rank, local, dev):
     D, F, B, S = cfg.dim, cfg.features, cfg.batch, cfg.shards
     rows = cfg.table_capacity()
     cap = int(rows / world * 1.01) + (1 << 20) if world > 1 else rows
-    table = hps.ShardSet(S, D, cap, hps.ADAGRAD, salts=cfg.salts(), device=local)
+    # in-order step tags (one pipeline, device step counter): each row's latest bump tag
+    # counts delays exactly, no tag ring needed (it would refuse out-of-order tags)
+    table = hps.ShardSet(S, D, cap, hps.ADAGRAD, salts=cfg.salts(), device=local,
+                         tag_ring=False)
     stream = torch.cuda.current_stream()
     t0 = time.perf_counter()
     chunk = 1 << 23
@@ -378,7 +382,10 @@ def run_sharded(args, world, rank, local, dev):
     S = cfg.shards
     rows = cfg.table_capacity()
     cap = int(rows / world * 1.01) + (1 << 20)
-    table = hps.ShardSet(S, D, cap, hps.ADAGRAD, salts=cfg.salts(), device=local)
+    # in-order step tags (one pipeline, device step counter): each row's latest bump tag
+    # counts delays exactly, no tag ring needed (it would refuse out-of-order tags)
+    table = hps.ShardSet(S, D, cap, hps.ADAGRAD, salts=cfg.salts(), device=local,
+                         tag_ring=False)
     stream = torch.cuda.current_stream()
     # pre-warm: each rank creates the rows it owns (M = 0 lazy inits while timing)
     t0 = time.perf_counter()
@@ -638,7 +645,10 @@ def main():
     opt = hps.ADAGRAD if cfg.optimizer == "adagrad" else hps.SGD
     agg = hps.MEAN if cfg.aggregation == "mean" else hps.SUM
     cap = cfg.table_capacity()
-    table = hps.ShardSet(cfg.shards, D, cap, opt, salts=cfg.salts(), device=local)
+    # in-order step tags (one pipeline, device step counter): each row's latest bump tag
+    # counts delays exactly, no tag ring needed (it would refuse out-of-order tags)
+    table = hps.ShardSet(cfg.shards, D, cap, opt, salts=cfg.salts(), device=local,
+                         tag_ring=False)
     stream = torch.cuda.current_stream()
 
     # -- pre-warm: every row of the table exists before timing (M = 0 misses).

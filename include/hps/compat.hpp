@@ -122,6 +122,7 @@ inline TablePtr make_table(const std::vector<uint64_t>& salts, uint64_t capacity
   c.device = device;
   c.owner_rank = 0;
   c.world_size = 1;
+  c.flags = HPS_TABLE_TAG_RING;  // PsShard's exact count_delay for any step-tag order
   hps_table* t = nullptr;
   check(hps_table_create(&c, &t));
   return TablePtr(t);

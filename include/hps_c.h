@@ -35,7 +35,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define HPS_ABI_VERSION 1
+#define HPS_ABI_VERSION 2
 
 typedef enum hps_status {
   HPS_OK = 0,
@@ -79,7 +79,21 @@ typedef struct hps_table_cfg {
   int32_t device;              /* CUDA ordinal; -1 = current device */
   uint32_t owner_rank;         /* 0 for a single-device table */
   uint32_t world_size;         /* 1 for a single-device table */
+  uint32_t flags;              /* HPS_TABLE_* */
+  uint32_t reserved0;          /* 0 */
+  uint64_t shard_capacity;     /* HPS_TABLE_LRU: rows per logical shard (PsShardConfig::capacity) */
 } hps_table_cfg;
+
+/* Table flags.
+ * HPS_TABLE_TAG_RING: keep every row's 16-deep ring of version-bump step tags
+ *   (PsShard::tag_ring_, embedding_ps.hpp:493-494; one 4-byte store per bump), so
+ *   count_delay is exact for any order of step tags and for tracked writes after
+ *   untracked ones (apply_gradients_map). Without it each row keeps its latest bump tag
+ *   only -- exact for in-order tags, which every stream-ordered pipeline produces -- and
+ *   a tracked apply it could not count exactly (a step tag older than one the table
+ *   already applied, or any tracked apply after an untracked write since the last
+ *   clear) is refused with HPS_E_CLOCK before anything mutates. */
+#define HPS_TABLE_TAG_RING 1u
 
 typedef struct hps_counters {
   uint64_t misses;            /* PsShard::miss_count          embedding_ps.hpp:79 */

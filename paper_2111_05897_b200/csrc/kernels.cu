@@ -263,7 +263,7 @@ __global__ void lazy_init_kernel(DevTable t, const uint32_t* __restrict__ new_sl
       // svt: version 0, tag kNoStep (all ones) -> sign bits of elements 4l+2, 4l+3
       row[t.D + d] = (t.svt && d < 64 && (d & 3) >= 2) ? -0.0f : 0.0f;
     }
-    if (lane < kTagRing) t.ring[static_cast<uint64_t>(slot) * kTagRing + lane] = kNoStep;
+    if (t.ring && lane < kTagRing) t.ring[static_cast<uint64_t>(slot) * kTagRing + lane] = kNoStep;
     if (lane == 0 && !t.svt) t.vt[slot] = make_uint2(0u, kNoStep);
   }
 }
@@ -421,7 +421,7 @@ __global__ void ckpt_restore_kernel(DevTable t, const uint64_t* __restrict__ ids
       }
       row[t.D + d] = a;
     }
-    if (lane < kTagRing) t.ring[static_cast<uint64_t>(s) * kTagRing + lane] = kNoStep;
+    if (t.ring && lane < kTagRing) t.ring[static_cast<uint64_t>(s) * kTagRing + lane] = kNoStep;
     if (lane == 0 && !t.svt) t.vt[s] = make_uint2(ver, kNoStep);
   }
 }

@@ -185,6 +185,8 @@ Table* table_create(const hps_table_cfg& cfg) {
     throw Error(HPS_E_CONFIG, "hps_table_create: unknown optimizer");
   if (cfg.world_size == 0 || cfg.owner_rank >= cfg.world_size)
     throw Error(HPS_E_CONFIG, "hps_table_create: owner_rank must be < world_size");
+  if (cfg.flags & ~HPS_TABLE_TAG_RING)
+    throw Error(HPS_E_CONFIG, "hps_table_create: unknown flags");
   auto t = new Table();
   try {
     t->cfg = cfg;
@@ -219,7 +221,8 @@ Table* table_create(const hps_table_cfg& cfg) {
     HPS_CUDA(cudaMalloc(&d.seen, (C / 32 + 1) * sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.multi, (C / 32 + 1) * sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.slot_id, C * sizeof(uint64_t)));
-    HPS_CUDA(cudaMalloc(&d.ring, C * kTagRing * sizeof(uint32_t)));
+    if (cfg.flags & HPS_TABLE_TAG_RING)
+      HPS_CUDA(cudaMalloc(&d.ring, C * kTagRing * sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.special, sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.hwm, sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.ctr, kCtrCount * sizeof(unsigned long long)));
@@ -637,10 +640,22 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   stg.finish(st);
 }
 
-// Step tags of tracked applies (Table::max_tag): a tag older than one already applied
-// makes the table's delay accounting leave the latest-bump-tag fast path (see note_tag
-// users). HPS_DEVICE_STEP pushes take monotone tags from the device counter.
+// Step tags of tracked applies (Table::max_tag). With the tag ring any order counts
+// exactly (the kernels walk the ring once the table saw an out-of-order tag or an
+// untracked write); without it a tracked apply the latest-bump-tag rule could miscount
+// is refused before anything mutates (HPS_TABLE_TAG_RING, hps_c.h). HPS_DEVICE_STEP
+// pushes take monotone tags from the device counter.
 static void note_tag(Table* t, uint32_t step_tag) {
+  if (!t->d.ring) {
+    if (step_tag < t->max_tag)
+      throw Error(HPS_E_CLOCK, "step tag " + std::to_string(step_tag) + " is older than " +
+                                   std::to_string(t->max_tag) +
+                                   ", which this table already applied; out-of-order step "
+                                   "tags need a table with HPS_TABLE_TAG_RING");
+    if (t->untracked_seen)
+      throw Error(HPS_E_CLOCK, "tracked apply after an untracked write: exact delays need a "
+                               "table with HPS_TABLE_TAG_RING");
+  }
   if (step_tag < t->max_tag) t->disordered = true;
   else t->max_tag = step_tag;
 }
@@ -728,21 +743,19 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     else a.fresh = 1;  // no mutation since the pull: read version == current version
   }
   if (!a.tracked) t->untracked_seen = true;
-  a.exact = t->disordered || t->untracked_seen;
+  a.exact = t->d.ring && (t->disordered || t->untracked_seen);
 
-  if (t->cfg.embedding_dim <= kHotMaxDim) {
-    // hot-row hand-off list (runs_kernel -> update_hot)
+  if (b.meta_ok) {
+    // sorted (large) plans: runs_kernel lists the rows listed more than once -- hot
+    // (>= kHotRun listings) and very hot ones in b.hot, the others in b.mlist -- for
+    // update_runs. Counters b.small[6..11] (zeroed by the register): [6] multi-list
+    // rows, [8] hot rows, [10] very hot rows (listed from the end), [9] / [11] claims.
     a.hot = b.hot;
-    // hot-row counters live in b.small[8..10]: [8] hot rows listed, [9] claimed by
-    // update_hot, [10] very hot rows (listed from the end); [6] the multi-list count
     a.n_hot = &b.small[8];
     a.hot_cap = static_cast<uint32_t>(b.N / kHotRun + 1);
-    if (b.meta_ok) {  // sorted (large) plans list their multi rows (runs_kernel)
-      a.mlist = b.mlist;
-      a.n_mlist = &b.small[6];
-      a.mlist_cap = static_cast<uint32_t>(b.N + 1);  // (sample-key plans list singles too)
-    }
-    // (the counters b.small[6..10] were zeroed by the batch's register)
+    a.mlist = b.mlist;
+    a.n_mlist = &b.small[6];
+    a.mlist_cap = static_cast<uint32_t>(b.N + 1);  // (sample-key plans list singles too)
   }
   if (!b.all_multi) {
     // Rows listed more than once (ordered chains, latency-bound, few) and rows listed
@@ -755,7 +768,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
       ProfScope p(t, "update_multi", t->aux);
       launch_runs(a, t->sm_count, t->aux);
       launch_update(pv, a, false, t->sm_count, t->aux);
-      launch_update_hot(pv, a, t->sm_count, t->aux);
+      launch_update_runs(pv, a, t->sm_count, t->aux);
     }
     {
       ProfScope p(t, "update", st);
@@ -770,7 +783,7 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     ProfScope p(t, "update_multi", st);
     launch_runs(a, t->sm_count, st);
     launch_update(pv, a, false, t->sm_count, st);
-    launch_update_hot(pv, a, t->sm_count, st);
+    launch_update_runs(pv, a, t->sm_count, st);
   }
   forget_outstanding(b);
   b.pulled = false;
@@ -895,7 +908,7 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
   a.rv64 = d_rv;
   a.tracked = d_rv ? 1 : 0;
   if (!d_rv) t->untracked_seen = true;
-  a.exact = t->disordered || t->untracked_seen;
+  a.exact = t->d.ring && (t->disordered || t->untracked_seen);
   a.out_delays = d_dl;
   a.lr = lr;
   a.step_tag = step_tag;

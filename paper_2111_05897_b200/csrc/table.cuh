@@ -374,12 +374,12 @@ struct UpdateArgs {
   // count delays from the tag ring (count_delay exactly) instead of the latest bump tag:
   // needed once step tags went out of order or untracked writes happened on the table
   int exact;
-  // Hot rows (runs of >= kHotRun listings on the sorted path): update_multi hands them to
-  // update_hot (one block per row, contributions staged in shared memory); null = off.
+  // Large (sorted) plans: rows listed more than once, as listed by runs_kernel for
+  // update_runs -- hot (>= kHotRun listings, very hot >= kVeryHotRun from the end)
   uint32_t* hot;
   uint32_t* n_hot;
   uint32_t hot_cap;
-  // large plan: rows of 2..kHotRun-1 listings (runs_kernel -> update_multi); null = scan
+  // and the other multi rows; null = update_multi scans the sorted positions
   uint32_t* mlist;
   uint32_t* n_mlist;
   uint32_t mlist_cap;
@@ -390,7 +390,6 @@ struct UpdateArgs {
 };
 constexpr uint32_t kHotRun = 64;
 constexpr uint32_t kVeryHotRun = 1024;
-constexpr uint32_t kHotMaxDim = 128;  // update_hot stages [256][D] floats in shared memory
 // Validation before mutation (embedding_ps.hpp:146-156) of a batch push: every gradient
 // finite, and the fan-out's float narrowing bounded (else the exact check of every pair
 // contribution runs in the kernel's last block). Reads a.grads [B*F][D] with a.offsets,
@@ -399,7 +398,8 @@ constexpr uint32_t kHotMaxDim = 128;  // update_hot stages [256][D] floats in sh
 // the update kernels then read as their tag.
 void launch_check_batch(const DevTable& t, const UpdateArgs& a, uint32_t B,
                         unsigned long long* step_ctr, cudaStream_t st);
-void launch_update_hot(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
+// large plan: every row listed more than once (warp per row and 32-dim chunk)
+void launch_update_runs(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
 void launch_runs(const UpdateArgs& a, int sms, cudaStream_t st);
 void launch_update(const DevTable& t, const UpdateArgs& a, bool direct, int sms, cudaStream_t st);
 void launch_update_single(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);

@@ -99,6 +99,7 @@ ADAGRAD, SGD = 0, 1
 MEAN, SUM = 0, 1
 ASYNC = 1
 DEVICE_STEP = 2
+TABLE_TAG_RING = 1  # hps_table_cfg.flags
 
 # ---- library loading -----------------------------------------------------------------
 
@@ -118,7 +119,8 @@ class TableCfg(C.Structure):
     _fields_ = [("shard_count", C.c_uint32), ("shard_salts", C.POINTER(C.c_uint64)),
                 ("capacity", C.c_uint64), ("embedding_dim", C.c_uint32),
                 ("optimizer", C.c_int32), ("device", C.c_int32), ("owner_rank", C.c_uint32),
-                ("world_size", C.c_uint32)]
+                ("world_size", C.c_uint32), ("flags", C.c_uint32), ("reserved0", C.c_uint32),
+                ("shard_capacity", C.c_uint64)]
 
 
 def lib():
@@ -349,6 +351,11 @@ def compress_indices(ids, offsets, B: int, G: int, stream=None):
 class ShardSet:
     """S logical shards (per-shard init salts) held on one device.
 
+    ``tag_ring`` (default, like PsShard): exact staleness delays for any step-tag order
+    (HPS_TABLE_TAG_RING); ``tag_ring=False`` keeps only each row's latest bump tag -- the
+    in-order pipelines' choice, one store per row cheaper -- and refuses (ClockError) the
+    tracked applies it could not count exactly.
+
     ``salts`` follows one of the reference's conventions, e.g.
     ``ShardSet(S, base_salt)`` -> ``salts[i] = mix64(base_salt + i)``
     (embedding_ps.hpp:513); pass ``salts=`` to use explicit per-shard salts.
@@ -356,12 +363,13 @@ class ShardSet:
 
     def __init__(self, shard_count: int, embedding_dim: int, capacity: int,
                  optimizer: int = ADAGRAD, base_salt: int = 0, salts=None, device: int = -1,
-                 owner_rank: int = 0, world_size: int = 1):
+                 owner_rank: int = 0, world_size: int = 1, tag_ring: bool = True):
         if salts is None:
             salts = [mix64((base_salt + i) & 0xFFFFFFFFFFFFFFFF) for i in range(shard_count)]
         self._salts = np.ascontiguousarray(salts, dtype=np.uint64)
         cfg = TableCfg(len(self._salts), self._salts.ctypes.data_as(C.POINTER(C.c_uint64)),
-                       capacity, embedding_dim, optimizer, device, owner_rank, world_size)
+                       capacity, embedding_dim, optimizer, device, owner_rank, world_size,
+                       TABLE_TAG_RING if tag_ring else 0, 0, 0)
         h = vp()
         check(lib().hps_table_create(C.byref(cfg), C.byref(h)), "ShardSet")
         self.h = h

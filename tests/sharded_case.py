@@ -97,7 +97,9 @@ def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, ag
         from paper_2111_05897_b200.sharded import ShardedEmbeddingWorker
 
         if use_device:
-            torch.cuda.set_device(rank)
+            # ranks may share a GPU (gloo control plane + the p2p transport: CUDA IPC works
+            # between processes on one device), so a 1-GPU box runs the multi-rank exchange
+            torch.cuda.set_device(rank % torch.cuda.device_count())
         dist.init_process_group(backend, init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                                 world_size=world)
         S = 8
@@ -302,13 +304,16 @@ def run_pipelined_rank(rank, world, port, D=8, B=12, F=3, steps=5, space=60, q=N
         from paper_2111_05897_b200 import hps
         from paper_2111_05897_b200.sharded import ShardedEmbeddingWorker
 
-        torch.cuda.set_device(rank)
-        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+        ndev = torch.cuda.device_count()
+        torch.cuda.set_device(rank % ndev)
+        # two ranks on one GPU: gloo control plane (NCCL refuses duplicate devices)
+        dist.init_process_group("nccl" if ndev >= world else "gloo",
+                                init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                                 world_size=world)
         S = 8
         salts = [O.mix64(7 + s) for s in range(S)]
         exp = O.Restatement(salts, D, "adagrad")
-        dev = torch.device("cuda", rank)
+        dev = torch.device("cuda", rank % ndev)
         table = hps.ShardSet(S, D, 1 << 14, hps.ADAGRAD, salts=salts)
         ews = [ShardedEmbeddingWorker(table, hps.MEAN, max_ids=world * B * F * 4)
                for _ in range(2)]

@@ -51,7 +51,7 @@ def test_library_is_sm100a(lib):
 def test_host_side_functions(lib):
     from paper_2111_05897_b200 import hps
 
-    assert hps.lib().hps_abi_version() == 1
+    assert hps.lib().hps_abi_version() == 2
     assert hps.mix64(0) == 0xE220A8397B1DCDAF
     assert hps.route_shard(0, 16) == 0xE220A8397B1DCDAF % 16
     with pytest.raises(hps.PreconditionError):

@@ -779,3 +779,209 @@ def test_pipelined_register_beside_push_large_plan(hps, graph):
     """> 4096 listings of repeated rows: the forked large sort of the next batch runs
     while this batch's update chains run on the same aux stream."""
     _pipelined_case(hps, 1024, 4, 64, 1500, steps=4, graph=graph)
+
+
+# ---------------------------------------------------------------- round 2 semantics
+
+
+def test_out_of_order_step_tags_count_like_the_reference(hps):
+    """count_delay walks the 16-deep tag ring (embedding_ps.hpp:454-480): with step tags
+    out of order (bumps 1, 5, 2, then a read-version-0 write at step 4) the reference
+    counts 2 distinct earlier tags, not the 3 bumps. Delays, versions and rows equal the
+    restatement oracle and the reference itself (oracle/_ref)."""
+    import oracle as O
+
+    D = 4
+    t = hps.ShardSet(1, D, 64, hps.ADAGRAD, salts=[5])
+    orc = O.Restatement([5], D, "adagrad")
+    ref = O.Reference([5], 64, D, "adagrad", "mean", 1)
+    rng = np.random.default_rng(3)
+    ids = np.array([7, 8, 7], np.uint64)
+    t.lookup(ids)
+    orc.lookup(ids)
+    ref.shard_lookup(0, ids)
+    seq = [(1, 0), (5, 1), (2, 2), (4, 0), (9, 1), (3, 3), (3, 0), (6, 5), (2, 0)]
+    for step, rv0 in seq:
+        g = rng.standard_normal((len(ids), D)).astype(np.float32)
+        rv = np.full(len(ids), rv0, np.uint64)
+        okg, dg = t.apply_gradients(ids, g, rv, 0.1, step)
+        oko, do = orc.apply(ids, g, rv, 0.1, step)
+        okr, dr = ref.shard_apply(0, ids, g, rv, 0.1, step, 0)
+        assert okg and oko and okr
+        assert (do == dr).all(), (step, do, dr)
+        assert (dg == do).all(), (step, dg, do)
+    w, a, v, _ = t.peek(np.array([7, 8], np.uint64))
+    wo, ao, vo, _ = orc.peek(np.array([7, 8], np.uint64))
+    assert w.tobytes() == wo.tobytes() and a.tobytes() == ao.tobytes()
+    assert (v == vo).all()
+    assert t.clock_reset_count() == orc.counters()["clock_resets"]
+
+
+def test_untracked_writes_between_tracked_ones(hps):
+    """apply_gradients_map bumps versions without a ring entry (:186); a later tracked
+    write's window then holds stale ring slots, which count_delay skips or counts exactly
+    as the reference does."""
+    import oracle as O
+
+    D = 2
+    t = hps.ShardSet(1, D, 64, hps.SGD, salts=[9])
+    orc = O.Restatement([9], D, "sgd")
+    ids = np.array([3], np.uint64)
+    t.lookup(ids)
+    orc.lookup(ids)
+    g = np.ones((1, D), np.float32)
+    for k in range(20):
+        if k % 3 == 2:
+            t.apply_gradients_map({3: g[0]}, 0.01)
+            orc.apply_map(ids, g, 0.01)
+            continue
+        rv = np.array([max(0, k - 4)], np.uint64)
+        okg, dg = t.apply_gradients(ids, g, rv, 0.01, k + 1)
+        oko, do = orc.apply(ids, g, rv, 0.01, k + 1)
+        assert (dg == do).all(), (k, dg, do)
+    w, a, v, _ = t.peek(ids)
+    wo, ao, vo, _ = orc.peek(ids)
+    assert w.tobytes() == wo.tobytes() and (v == vo).all()
+
+
+def test_async_rejection_surfaces_at_sync(hps):
+    """Two HPS_ASYNC pushes, the first with a non-finite gradient, one table.sync() at the
+    end: the sync raises DivergenceError (the rejection is sticky until reported), the
+    first push applied nothing and the second applied normally."""
+    import oracle as O
+
+    D = 8
+    salts = [O.mix64(7 + s) for s in range(2)]
+    t = hps.ShardSet(2, D, 1024, hps.ADAGRAD, salts=salts)
+    orc = O.Restatement(salts, D, "adagrad")
+    ews = [hps.EmbeddingWorker(t, hps.MEAN) for _ in range(2)]
+    rng = np.random.default_rng(1)
+    B, F = 6, 2
+    batches = []
+    for k in range(2):
+        ids = rng.integers(0, 40, B * F).astype(np.uint64)
+        offs = np.arange(B * F + 1, dtype=np.uint32)
+        g = (rng.standard_normal((B, F, D)) * 0.1).astype(np.float32)
+        batches.append((ids, offs, g))
+    batches[0][2][2, 1, 3] = np.nan
+    for k, (ids, offs, g) in enumerate(batches):
+        ews[k].register_batch(ids, offs, B, F)
+        ews[k].serve_pull()
+        assert ews[k].apply_backward(g, 0.1, k + 1, flags=hps.ASYNC)
+        orc.pull_batch(B, F, ids, offs.astype(np.uint64), "mean")
+        if k == 1:
+            orc.push_batch(B, F, ids, offs.astype(np.uint64), g, 0.1, k + 1, agg="mean")
+    with pytest.raises(hps.DivergenceError):
+        t.sync()
+    t.sync()  # reported once
+    keys = np.arange(40, dtype=np.uint64)
+    w, a, v, p = t.peek(keys)
+    wo, ao, vo, po = orc.peek(keys)
+    assert (p == po).all()
+    assert w[p].tobytes() == wo[po].tobytes() and a[p].tobytes() == ao[po].tobytes()
+    assert (v[p] == vo[po]).all()
+
+
+def test_batch_registered_before_reset_is_refused(hps):
+    """A batch registered (slots resolved) before reset_for_recovery / a checkpoint load
+    may not pull or push through its stale slots: HPS_E_STALE_SAMPLE."""
+    D = 4
+    t = hps.ShardSet(1, D, 256, hps.ADAGRAD, salts=[3])
+    ew = hps.EmbeddingWorker(t, hps.MEAN)
+    ids = np.array([1, 2, 3, 4], np.uint64)
+    offs = np.arange(5, dtype=np.uint32)
+    ew.register_batch(ids, offs, 4, 1)
+    ew.serve_pull()
+    img = t.save_checkpoint(0)
+    t.reset_for_recovery()
+    with pytest.raises(hps.StaleSampleError):
+        ew.apply_backward(np.ones((4, 1, D), np.float32), 0.1, 1)
+    ew.register_batch(ids, offs, 4, 1)
+    t.load_checkpoint([img])
+    with pytest.raises(hps.StaleSampleError):
+        ew.serve_pull()
+    ew.register_batch(ids, offs, 4, 1)  # registering again is fine
+    ew.serve_pull()
+    assert ew.apply_backward(np.ones((4, 1, D), np.float32), 0.1, 1)
+
+
+def test_batch_push_refuses_out_delays(hps):
+    import ctypes as C
+
+    t = hps.ShardSet(1, 4, 64, hps.SGD, salts=[1])
+    ew = hps.EmbeddingWorker(t, hps.SUM)
+    ew.register_batch(np.array([5], np.uint64), np.array([0, 1], np.uint32), 1, 1)
+    ew.serve_pull()
+    g = np.ones((1, 1, 4), np.float32)
+    dl = np.zeros(1, np.uint32)
+    acc = C.c_int(0)
+    rc = hps.lib().hps_batch_push(ew.h, g.ctypes.data, 0.1, 1, t.epoch(), 0, dl.ctypes.data,
+                                  C.byref(acc), 0, None)
+    with pytest.raises(hps.PreconditionError):
+        hps.check(rc, "push")
+
+
+def test_overflow_bound_exact_check_accepts_finite_large_gradients(hps):
+    """Gradients so large that the streaming bound is inconclusive (|g| * F >= 2^127) but
+    every pair contribution is finite: the last block's exact check accepts the push and
+    the update matches the oracle; a pair whose sum overflows is rejected."""
+    import oracle as O
+
+    D = 3
+    t = hps.ShardSet(1, D, 64, hps.SGD, salts=[4])
+    orc = O.Restatement([4], D, "sgd")
+    ew = hps.EmbeddingWorker(t, hps.SUM)
+    ids = np.array([1, 2, 1, 3], np.uint64)
+    offs = np.array([0, 1, 2, 3, 4], np.uint32)  # B=2, F=2, one listing per group
+    g = np.zeros((2, 2, D), np.float32)
+    g[0, 0] = [2.0e38, -1.0, 0.5]
+    g[0, 1] = [1.0, 2.0, 3.0]
+    g[1, 0] = [2.0e38, 1.0, 1.0]
+    g[1, 1] = [-2.0e38, 0.0, 0.0]
+    ew.register_batch(ids, offs, 2, 2)
+    ew.serve_pull()
+    orc.pull_batch(2, 2, ids, offs.astype(np.uint64), "sum")
+    assert ew.apply_backward(g, 1e-40, 1)
+    orc.push_batch(2, 2, ids, offs.astype(np.uint64), g, 1e-40, 1, agg="sum")
+    keys = np.array([1, 2, 3], np.uint64)
+    assert t.peek(keys)[0].tobytes() == orc.peek(keys)[0].tobytes()
+    # id 1 twice in one sample, both 2e38 -> the fp64 sum 4e38 overflows float
+    ids2 = np.array([1, 1], np.uint64)
+    offs2 = np.array([0, 1, 2], np.uint32)
+    g2 = np.full((1, 2, D), 2.0e38, np.float32)
+    ew.register_batch(ids2, offs2, 1, 2)
+    ew.serve_pull()
+    before = t.peek(keys)[0].copy()
+    with pytest.raises(hps.DivergenceError):
+        ew.apply_backward(g2, 1e-40, 2)
+    assert t.peek(keys)[0].tobytes() == before.tobytes()
+
+
+def test_table_without_tag_ring_refuses_what_it_cannot_count(hps):
+    """tag_ring=False (the in-order pipelines' tables): in-order tracked applies count
+    delays exactly; an out-of-order step tag, or a tracked apply after an untracked write,
+    is refused with ClockError before anything mutates."""
+    import oracle as O
+
+    D = 2
+    t = hps.ShardSet(1, D, 64, hps.ADAGRAD, salts=[11], tag_ring=False)
+    orc = O.Restatement([11], D, "adagrad")
+    ids = np.array([8, 9], np.uint64)
+    _, rv = t.lookup(ids)
+    orc.lookup(ids)
+    g = np.ones((2, D), np.float32)
+    for step in (1, 2, 4):
+        okg, dg = t.apply_gradients(ids, g, rv, 0.01, step)
+        _, do = orc.apply(ids, g, rv, 0.01, step)
+        assert (dg == do).all()
+    before = t.peek(ids)
+    with pytest.raises(hps.ClockError):
+        t.apply_gradients(ids, g, rv, 0.01, 3)
+    after = t.peek(ids)
+    assert before[0].tobytes() == after[0].tobytes() and (before[2] == after[2]).all()
+    t.apply_gradients_map({8: [1.0, 1.0]}, 0.01)
+    with pytest.raises(hps.ClockError):
+        t.apply_gradients(ids, g, rv, 0.01, 5)
+    t.reset_for_recovery()  # a clear forgets both conditions
+    _, rv = t.lookup(ids)
+    assert t.apply_gradients(ids, g, rv, 0.01, 1)[0]

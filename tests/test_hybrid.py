@@ -244,3 +244,32 @@ def test_hybrid_staleness_loss_curve():
         assert c[-10:].mean() < c[:5].mean(), f"tau={tau} did not learn: {c}"
     rel = abs(curves[4][-10:].mean() - curves[0][-10:].mean()) / curves[0][-10:].mean()
     assert rel < 0.03, (rel, curves)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not cuda_available(), reason="needs a GPU")
+def test_hybrid_trainer_reports_divergence():
+    """A non-finite dense input makes the loss and the dense gradient non-finite: the
+    dense update of that step is skipped and flush() raises DivergenceError (the
+    reference raises it in train_step, dense_nn.hpp:233,268, and aborts the run)."""
+    import torch
+
+    from paper_2111_05897_b200 import hps
+    from paper_2111_05897_b200.hybrid import HybridTrainer
+
+    D, F, nd, S = 8, 4, 3, 4
+    salts = [W.mix64_int(7 + s) for s in range(S)]
+    stream = _small_stream(3, F=F, D=D, nd=nd)
+    table = hps.ShardSet(S, D, 4096, hps.ADAGRAD, salts=salts, device=0)
+    tr = HybridTrainer(table, F, nd, hidden=(8,), staleness=1, init_seed=5)
+    dev = torch.device("cuda", 0)
+    for k, (ids, offs, x, y) in enumerate(stream):
+        x = x.copy()
+        if k == 1:
+            x[0, 0] = np.nan
+        tr.step(torch.from_numpy(ids.view(np.int64)).to(dev),
+                torch.from_numpy(offs.view(np.int32)).to(dev),
+                torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev))
+    with pytest.raises(hps.DivergenceError):
+        tr.flush()
+    tr.check()  # reported once

@@ -83,6 +83,43 @@ def test_sharded_device_world2_large_plan(transport):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("agg,opt", [("mean", "adagrad"), ("sum", "sgd")])
+@pytest.mark.parametrize("D", [64, 5])
+def test_sharded_p2p_two_ranks(agg, opt, D):
+    """Two ranks over the NVLink peer transport -- on two GPUs when the box has them, else
+    both processes on one GPU (CUDA IPC arenas, device barriers, gloo only for the handle
+    exchange): the multi-rank exchange, barriers and SampleId ordering run on a 1-GPU box
+    too. Bit-exact vs the global-batch oracle."""
+    res = run_world(2, "gloo", use_device=True, agg=agg, opt=opt, D=D, transport="p2p",
+                    timeout=400)
+    for r, status, n in res:
+        assert status == "ok", status
+
+
+@pytest.mark.gpu
+def test_sharded_p2p_two_ranks_large_plan_and_graph():
+    """Two ranks (one GPU if need be): the radix-sort plan of repeated ids, then a CUDA
+    graph of the p2p step replayed on new inputs."""
+    res = run_world(2, "gloo", use_device=True, B=800, F=4, D=16, space=2000, steps=2,
+                    transport="p2p", timeout=400)
+    for r, status, n in res:
+        assert status == "ok", status
+    res = run_world(2, "gloo", use_device=True, transport="p2p", graph=True, steps=4, B=16,
+                    timeout=400)
+    for r, status, n in res:
+        assert status == "ok", status
+
+
+@pytest.mark.gpu
+def test_sharded_pipelined_prefetch_two_ranks():
+    """bench.py's pipelined sharded schedule with two ranks (sharing GPU 0 on a 1-GPU box)."""
+    from sharded_case import run_pipelined_world
+
+    res = run_pipelined_world(2, D=8)
+    assert all(r[1] == "ok" for r in res), [r[1] for r in res]
+
+
+@pytest.mark.gpu
 def test_sharded_p2p_cuda_graph_replay():
     """The peer-transport step has no host round trip: captured once in a CUDA graph and
     replayed on new inputs it stays bit-exact (device barrier epochs and step tags)."""
