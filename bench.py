@@ -135,21 +135,30 @@ class ClockSampler:
 # ---------------------------------------------------------------- reference arm / cpu baseline
 
 
-def reference_run(cfg, B_sample, steps, warmup, threads, seconds_cap=None):
+def reference_run(cfg, B_sample, steps, warmup, threads, seconds_cap=None, legs=False):
     """The reference's own path (EmbeddingWorker -> LocalHub -> PsShardService ->
-    PsShard, sync order) on bounded samples of the workload. Returns samples/s."""
+    PsShard, sync order: pull on `threads` threads, ordered single-thread push) on the
+    config's batches, compiled from the unmodified headers (oracle/_ref). Like the GPU
+    arm, the timed steps cycle over a few distinct batches whose ids were created before
+    timing (no lazy inits inside the timed region); the table holds those rows.
+    Returns (samples/s, steps timed, rows held, extra legs)."""
     import oracle as O
     from paper_2111_05897_b200 import workloads as W
 
-    total = steps + warmup
-    per_shard = int(1.3 * B_sample * cfg.features * total / cfg.shards) + 1024
+    M = 2
+    batches = [W.make_batch(cfg, 10_000 + m, batch=B_sample) for m in range(M)]
+    grads = [W.make_grads(cfg, B_sample, m) for m in range(M)]
+    uniq = np.unique(np.concatenate([b.ids for b in batches]))
+    shard = (W.mix64(uniq) % np.uint64(cfg.shards)).astype(np.int64)
+    per_shard = int(np.bincount(shard, minlength=cfg.shards).max() * 1.25) + 1024
     ref = O.Reference(cfg.salts(), per_shard, cfg.dim, cfg.optimizer, cfg.aggregation,
                       cfg.features)
+    for s_ in range(cfg.shards):  # pre-warm: every id the timed steps list exists
+        ref.shard_lookup(s_, uniq[shard == s_])
     times = []
     t_start = time.perf_counter()
-    for s in range(total):
-        b = W.make_batch(cfg, 10_000 + s, batch=B_sample)
-        g = W.make_grads(cfg, b.B, s)
+    for s in range(steps + warmup):
+        b, g = batches[s % M], grads[s % M]
         off = b.offsets.astype(np.uint64)
         t0 = time.perf_counter()
         ref.step(b.B, b.ids, off, g, cfg.lr, s + 1, True, threads=threads)
@@ -158,7 +167,39 @@ def reference_run(cfg, B_sample, steps, warmup, threads, seconds_cap=None):
             times.append(dt)
         if seconds_cap and time.perf_counter() - t_start > seconds_cap and len(times) >= 1:
             break
-    return B_sample * len(times) / sum(times), len(times)
+    value = B_sample * len(times) / sum(times)
+    extra = {}
+    if legs:
+        # hybrid semantics: the same steps with the push on `threads` threads at once
+        ht = []
+        for s in range(3):
+            b, g = batches[s % M], grads[s % M]
+            off = b.offsets.astype(np.uint64)
+            t0 = time.perf_counter()
+            ref.step(b.B, b.ids, off, g, cfg.lr, 100 + s, True, threads=threads,
+                     push_threads=True)
+            ht.append(time.perf_counter() - t0)
+        extra["hybrid_push_samples_per_s"] = B_sample * len(ht) / sum(ht)
+        # raw PsShard::lookup / apply_gradients (the CPU data-structure upper bound), one
+        # thread per shard (ctypes releases the GIL), rows of one batch
+        import concurrent.futures as cf
+
+        ids0 = np.unique(batches[0].ids)
+        sh0 = (W.mix64(ids0) % np.uint64(cfg.shards)).astype(np.int64)
+        parts = [ids0[sh0 == s_] for s_ in range(cfg.shards)]
+        with cf.ThreadPoolExecutor(max_workers=min(threads, cfg.shards)) as ex:
+            t0 = time.perf_counter()
+            vers = list(ex.map(lambda s_: ref.shard_lookup(s_, parts[s_])[1], range(cfg.shards)))
+            t_look = time.perf_counter() - t0
+            gr = [np.full((len(p_), cfg.dim), 1e-3, np.float32) for p_ in parts]
+            t0 = time.perf_counter()
+            list(ex.map(lambda s_: ref.shard_apply(s_, parts[s_], gr[s_], vers[s_], cfg.lr,
+                                                   1000, 0), range(cfg.shards)))
+            t_app = time.perf_counter() - t0
+        extra["ps_lookup_rows_per_s"] = len(ids0) / t_look
+        extra["ps_apply_rows_per_s"] = len(ids0) / t_app
+        extra["ps_threads"] = min(threads, cfg.shards)
+    return value, len(times), int(len(uniq)), extra
 
 
 def run_reference_arm(args):
@@ -167,26 +208,35 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = W.CONFIGS[args.config]
-    B_sample = min(cfg.batch, 2048)
+    cfg = W.CONFIGS["c2" if args.config == "c5" else args.config]
+    B_sample = cfg.batch
     cores = nproc()
-    value, n = reference_run(cfg, B_sample, args.steps, args.warmup, cores)
+    value, n, rows, extra = reference_run(cfg, B_sample, args.steps, args.warmup, cores,
+                                          legs=True)
+    conf = workload_config(cfg, args)
+    conf["rows"] = rows
+    conf["reference_rows_note"] = (f"the reference's PsShards hold the {rows} rows the timed "
+                                   f"batches list (created before timing, as the GPU arm's "
+                                   f"pre-warm); the GPU table holds {cfg.table_capacity()}")
     line = {
         "impl": "reference", "metric": "embedding lookup+update samples/sec", "value": value,
         "unit": "samples/s", "n_gpus": args.gpus, "steps": n, "warmup": args.warmup,
         "ms_per_step": 1000.0 * B_sample / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 (fp64 pooling/fan-out)", "data": "synthetic",
-        "config": workload_config(cfg, args, ref_sample=B_sample),
+        "config": conf,
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "reference",
-                         "sample": f"{B_sample} samples/step of {cfg.name}, pull on {cores} "
-                                   f"threads + ordered push, reference headers via oracle/_ref"},
+                         "sample": f"{n} steps x {B_sample} samples of {cfg.name} (2 distinct "
+                                   f"batches, pre-warmed rows), pull on {cores} threads + "
+                                   f"ordered single-thread push, reference headers via "
+                                   f"oracle/_ref"},
+        "legs": extra,
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def workload_config(cfg, args, ref_sample=None):
+def workload_config(cfg, args):
     d = {"workload": f"{cfg.name}: batch {cfg.batch}, {cfg.features} "
                      f"{'multi-hot' if cfg.multi_hot else 'one-hot'} features, "
                      f"{cfg.rows // 1_000_000}M-row table dim {cfg.dim}, {cfg.optimizer}, "
@@ -196,8 +246,6 @@ def workload_config(cfg, args, ref_sample=None):
          "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single",
          "l2": "per-step footprint > L2 (126 MB); no flush",
          "table": "in-order step tags, latest-bump-tag delays (no HPS_TABLE_TAG_RING)"}
-    if ref_sample:
-        d["reference_sample_batch"] = ref_sample
     return d
 
 
@@ -613,6 +661,95 @@ def run_sharded(args, world, rank, local, dev):
     dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------- e2e (host buffers)
+
+
+def run_e2e_local(args, table, agg, cfg, host_batches, grads, stream, dev, B, F, D):
+    import torch
+
+    from paper_2111_05897_b200 import hps
+
+    K = 2
+    ews = [hps.EmbeddingWorker(table, agg) for _ in range(K)]
+    M = min(len(host_batches), K)
+    nmax = max(hb.N for hb in host_batches[:M])
+    h_ids = [torch.from_numpy(hb.ids.view(np.int64)).pin_memory() for hb in host_batches[:M]]
+    h_offs = [torch.from_numpy(hb.offsets.view(np.int32)).pin_memory()
+              for hb in host_batches[:M]]
+    h_grads = [grads[m].cpu().pin_memory() for m in range(M)]
+    h_pooled = [torch.empty((B, F, D), dtype=torch.float32).pin_memory() for _ in range(K)]
+    d_ids = [torch.empty(nmax, dtype=torch.int64, device=dev) for _ in range(K)]
+    d_offs = [torch.empty(B * F + 1, dtype=torch.int32, device=dev) for _ in range(K)]
+    d_grads = [torch.empty((B, F, D), dtype=torch.float32, device=dev) for _ in range(K)]
+    d_pooled = [torch.empty((B, F, D), dtype=torch.float32, device=dev) for _ in range(K)]
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    ev = lambda: torch.cuda.Event()
+    in_ready, g_ready, pooled_ready = [ev() for _ in range(K)], [ev() for _ in range(K)], \
+        [ev() for _ in range(K)]
+    push_done, out_done = [ev() for _ in range(K)], [ev() for _ in range(K)]
+    for e_ in push_done + out_done:
+        e_.record(stream)
+    ns = [0]
+
+    def stage_in(s):  # H2D of step s into slot s % K, once that slot's last user is done
+        k, m = s % K, s % M
+        with torch.cuda.stream(h2d):
+            h2d.wait_event(push_done[k])
+            n = h_ids[m].numel()
+            d_ids[k][:n].copy_(h_ids[m], non_blocking=True)
+            d_offs[k].copy_(h_offs[m], non_blocking=True)
+            in_ready[k].record(h2d)
+            d_grads[k].copy_(h_grads[m], non_blocking=True)
+            g_ready[k].record(h2d)
+
+    def step(s):
+        k, m = s % K, s % M
+        n = h_ids[m].numel()
+        stream.wait_event(in_ready[k])
+        ews[k].register_batch(d_ids[k][:n], d_offs[k], B, F, stream=stream)
+        stream.wait_event(out_done[k])  # the slot's previous pooled batch reached the host
+        ews[k].serve_pull(out_pooled=d_pooled[k], stream=stream)
+        pooled_ready[k].record(stream)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(pooled_ready[k])
+            h_pooled[k].copy_(d_pooled[k], non_blocking=True)
+            out_done[k].record(d2h)
+        stream.wait_event(g_ready[k])
+        ews[k].apply_backward(d_grads[k], cfg.lr, flags=hps.ASYNC | hps.DEVICE_STEP,
+                              stream=stream)
+        push_done[k].record(stream)
+        stage_in(s + 1)
+
+    s0 = 0
+    stage_in(s0)
+    for _ in range(3):  # warm-up
+        step(s0)
+        s0 += 1
+    torch.cuda.synchronize()
+    table.sync()
+    q0 = torch.cuda.Event(enable_timing=True)
+    q1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    q0.record(stream)
+    for _ in range(args.e2e_steps):
+        step(s0)
+        s0 += 1
+    stream.wait_stream(d2h)
+    q1.record(stream)
+    torch.cuda.synchronize()
+    _ = float(h_pooled[(s0 - 1) % K][0, 0, 0])  # the host reads the last result
+    wall_ms = (time.perf_counter() - w0) * 1000 / args.e2e_steps
+    e_ms = max(q0.elapsed_time(q1) / args.e2e_steps, wall_ms)
+    table.sync()
+    hb = host_batches[0]
+    return {"value": B * 1000.0 / e_ms, "unit": "samples/s",
+            "h2d_bytes_per_step": int(8 * hb.N + 4 * (B * F + 1) + 4 * B * F * D),
+            "d2h_bytes_per_step": int(4 * B * F * D),
+            "path": "hps_batch_register/pull/push on device buffers fed from pinned host "
+                    "memory every step (H2D of step s+1 and D2H of step s on two copy "
+                    "streams, overlapped)"}
+
+
 # ---------------------------------------------------------------- our arm
 
 
@@ -832,52 +969,31 @@ def main():
         except Exception:
             traffic = None
 
-    # -- e2e through the public API with HOST buffers (pinned), copies inside the region
+    # -- e2e through the public API, inputs from and results to pinned HOST memory: every
+    # step copies its ids, offsets and gradients in and its pooled embeddings out, inside
+    # the timed region. Two in-flight slots: the H2D copies of step s+1 (one copy
+    # stream) and the D2H copy of step s (another) overlap each other and the compute
+    # (PCIe is full duplex) -- the same double buffering a trainer feeding the table from
+    # host memory would use.
     e2e = None
     if args.e2e_steps > 0:
-        hb = host_batches[0]
-        h_ids = torch.from_numpy(hb.ids.view(np.int64)).pin_memory()
-        h_offs = torch.from_numpy(hb.offsets.view(np.int32)).pin_memory()
-        h_grads = grads[0].cpu().pin_memory()
-        h_pooled = torch.empty((B, F, D), dtype=torch.float32).pin_memory()
-        for _ in range(2):
-            ew.register_batch(h_ids, h_offs, B, F, stream=stream)
-            ew.serve_pull(out_pooled=h_pooled, stream=stream)
-            ew.apply_backward(h_grads, cfg.lr, flags=hps.DEVICE_STEP, stream=stream)
-            it += 1
-        barrier()
-        q0 = torch.cuda.Event(enable_timing=True)
-        q1 = torch.cuda.Event(enable_timing=True)
-        w0 = time.perf_counter()
-        q0.record(stream)
-        for _ in range(args.e2e_steps):
-            ew.register_batch(h_ids, h_offs, B, F, stream=stream)
-            ew.serve_pull(out_pooled=h_pooled, stream=stream)
-            ew.apply_backward(h_grads, cfg.lr, flags=hps.DEVICE_STEP, stream=stream)
-            it += 1
-        q1.record(stream)
-        torch.cuda.synchronize()
-        wall_ms = (time.perf_counter() - w0) * 1000 / args.e2e_steps
-        e_ms = max(q0.elapsed_time(q1) / args.e2e_steps, wall_ms)
+        e2e = run_e2e_local(args, table, agg, cfg, host_batches, grads, stream, dev, B, F, D)
         if world > 1:
-            t = torch.tensor([e_ms], device=dev)
+            t = torch.tensor([1000.0 * B / e2e["value"]], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
-        e2e = {"value": world * B * 1000.0 / e_ms, "unit": "samples/s",
-               "h2d_bytes_per_step": int(8 * hb.N + 4 * (B * F + 1) + 4 * B * F * D),
-               "d2h_bytes_per_step": int(4 * B * F * D),
-               "path": "hps_batch_register/pull/push with pinned host buffers"}
+            e2e["value"] = world * B * 1000.0 / float(t.item())
 
     # -- CPU baseline: the reference on this box's host cores (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cores = nproc()
-            B_s = 2048
-            v, n = reference_run(cfg, B_s, steps=100, warmup=1, threads=cores,
-                                 seconds_cap=args.cpu_seconds)
+            B_s = cfg.batch
+            v, n, rows, _ = reference_run(cfg, B_s, steps=100, warmup=1, threads=cores,
+                                          seconds_cap=args.cpu_seconds)
             cpu = {"value": v, "unit": "samples/s", "cores": cores, "kind": "reference",
-                   "sample": f"{n} steps x {B_s} samples of {cfg.name} through the reference "
+                   "sample": f"{n} steps x {B_s} samples of {cfg.name} (2 distinct batches, "
+                             f"their {rows} rows created before timing) through the reference "
                              f"EmbeddingWorker/PsShard (oracle/_ref), pull on {cores} threads + "
                              f"ordered single-thread push"}
         except Exception as e:  # report, never fake

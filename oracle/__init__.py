@@ -326,14 +326,15 @@ class Reference:
             raise OracleError(rc, f"{what}: {self.lib.ref_last_error().decode()}")
 
     def step(self, B, ids, offsets, grads=None, lr=0.0, step=0, has_step=False, threads=1,
-             pull=True, push=True):
+             pull=True, push=True, push_threads=False):
         ids = _u64(ids)
         offsets = _u64(offsets)
         grads = _f32(grads)
         pooled = np.zeros((B, self.F, self.D), np.float32) if pull else None
         rv = np.zeros(max(1, len(ids)), np.uint64) if pull else None
         sids = np.zeros(B, np.uint64) if pull else None
-        flags = (1 if pull else 0) | (2 if push else 0)
+        # push_threads: the hybrid push, apply_backward from `threads` threads at once
+        flags = (1 if pull else 0) | ((4 if push_threads else 2) if push else 0)
         rc = self.lib.ref_step(self.h, B, _p(ids, u64p), _p(offsets, u64p), _p(grads, f32p), lr,
                                step, int(has_step), threads, flags, _p(pooled, f32p),
                                _p(rv, u64p), _p(sids, u64p))

@@ -125,7 +125,8 @@ void* ref_table_create(uint32_t S, const uint64_t* salts, uint32_t capacity, uin
 void ref_table_destroy(void* h) { delete static_cast<RefTable*>(h); }
 
 // One sync step over a batch in CSR form: ids[N], offsets[B*F+1] (u64, sample-major,
-// group-minor). flags bit0 = pull, bit1 = push. Pull writes out_pooled[B*F*D] and
+// group-minor). flags bit0 = pull, bit1 = push (ordered, one thread), bit2 = push on
+// `threads` threads (hybrid). Pull writes out_pooled[B*F*D] and
 // out_read_versions[N] (per listing, the PullResult order). Push applies grads[B*F*D]
 // in ascending SampleId order for the batch registered by the last pull.
 int ref_step(void* h, uint32_t B, const uint64_t* ids, const uint64_t* offsets, const float* grads,
@@ -174,7 +175,34 @@ int ref_step(void* h, uint32_t B, const uint64_t* ids, const uint64_t* offsets, 
       if (out_sids)
         for (uint32_t i = 0; i < B; ++i) out_sids[i] = t->sids[i].raw;
     }
-    if (flags & 2) {
+    if (flags & 4) {
+      // hybrid (asynchronous) push: T threads call apply_backward concurrently, each on
+      // its own samples in ascending SampleId; no order across threads (the reference's
+      // hybrid training, orchestrator.hpp:799-830)
+      std::vector<uint32_t> order(t->sids.size());
+      for (uint32_t i = 0; i < order.size(); ++i) order[i] = i;
+      std::sort(order.begin(), order.end(),
+                [&](uint32_t a, uint32_t b) { return t->sids[a] < t->sids[b]; });
+      const int T = std::max(1, threads);
+      std::vector<std::exception_ptr> errs(T);
+      auto work = [&](int w) {
+        try {
+          std::vector<float> g((size_t)F * D);
+          for (size_t k = w; k < order.size(); k += T) {
+            const uint32_t i = order[k];
+            std::memcpy(g.data(), grads + (uint64_t)i * F * D, sizeof(float) * F * D);
+            t->ews[i % t->E]->apply_backward(t->sids[i], g, lr, step, has_step != 0);
+          }
+        } catch (...) {
+          errs[w] = std::current_exception();
+        }
+      };
+      std::vector<std::thread> th;
+      for (int w = 0; w < T; ++w) th.emplace_back(work, w);
+      for (auto& x : th) x.join();
+      for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    } else if (flags & 2) {
       std::vector<uint32_t> order(t->sids.size());
       for (uint32_t i = 0; i < order.size(); ++i) order[i] = i;
       std::sort(order.begin(), order.end(),

@@ -106,7 +106,7 @@ def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, ag
         salts = [O.mix64(7 + s) for s in range(S)]
         exp = O.Restatement(salts, D, opt)  # the whole global batch, one table
         if use_device:
-            dev = torch.device("cuda", rank)
+            dev = torch.device("cuda", rank % torch.cuda.device_count())
             table = hps.ShardSet(S, D, 1 << 14, hps.ADAGRAD if opt == "adagrad" else hps.SGD,
                                  salts=salts)
             ew = ShardedEmbeddingWorker(table, hps.MEAN if agg == "mean" else hps.SUM,

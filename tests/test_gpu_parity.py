@@ -192,6 +192,42 @@ def test_c3_multi_hot_zipf(hps):
     _sync_vs_oracle_batch(hps, cfg, b)
 
 
+def test_c3_full_size_two_steps(hps):
+    """configs[2] at full size: 16384 x 26 multi-hot (avg 50) Zipf(1.1) -- 16.9M listings,
+    3.8M rows, the hottest row listed ~16k times -- two sync steps through the large plan
+    (radix sort, runs lists, warp-per-row updates of hot and multi rows, singles), pooled
+    output, rows, accumulators and versions bit-exact vs the oracle."""
+    import oracle as O
+    from paper_2111_05897_b200 import workloads as W
+
+    cfg = W.CONFIGS["c3"]
+    b = W.make_batch(cfg, 0)
+    assert b.N > 16_000_000
+    orc = O.Restatement(cfg.salts(), cfg.dim, cfg.optimizer)
+    table = hps.ShardSet(cfg.shards, cfg.dim, 1 << 22, hps.ADAGRAD, salts=cfg.salts(),
+                         tag_ring=False)
+    ew = hps.EmbeddingWorker(table, hps.MEAN)
+    off64 = b.offsets.astype(np.uint64)
+    counts = np.bincount(np.unique(b.ids, return_inverse=True)[1])
+    assert counts.max() > 10_000  # the very-hot path is exercised
+    for step in range(2):
+        g = W.make_grads(cfg, b.B, step)
+        po, rvo = orc.pull_batch(b.B, b.F, b.ids, off64, "mean")
+        ew.register_batch(b.ids, b.offsets, b.B, b.F)
+        pg = ew.serve_pull()
+        assert pg.tobytes() == po.tobytes(), f"step {step}: pooled differs"
+        orc.push_batch(b.B, b.F, b.ids, off64, g, cfg.lr, step + 1, read_versions=rvo,
+                       agg="mean")
+        assert ew.apply_backward(g, cfg.lr, step + 1)
+    uniq = np.unique(b.ids)
+    w, a, v, p = table.peek(uniq)
+    wo, ao, vo, _ = orc.peek(uniq)
+    assert p.all()
+    assert w.tobytes() == wo.tobytes(), "rows differ"
+    assert a.tobytes() == ao.tobytes(), "accumulators differ"
+    np.testing.assert_array_equal(v, vo)
+
+
 def _sync_vs_oracle_batch(hps, cfg, b):
     import oracle as O
     from paper_2111_05897_b200 import workloads as W
