@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
     p.add_argument("--no-pipeline", action="store_true",
                    help="C2: register each batch in line instead of beside the previous push")
+    p.add_argument("--timeline", default="",
+                   help="write a CUPTI kernel timeline of a few graph replays to this file")
     p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                    help="N > 1: NVLink peer writes (p2p) or NCCL all-to-alls")
     return p.parse_args()
@@ -661,6 +663,29 @@ def run_sharded(args, world, rank, local, dev):
     dist.destroy_process_group()
 
 
+def write_timeline(path, step, it, n):
+    """Kernel start/end times (CUPTI via torch.profiler) of n replays of the timed step:
+    where the step's time goes between and beside the kernels."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for i in range(n):
+            step(it + i)
+        torch.cuda.synchronize()
+    evs = []
+    for e in prof.events():
+        if e.device_type == torch.autograd.DeviceType.CUDA and e.time_range.elapsed_us() >= 0:
+            evs.append((e.time_range.start, e.time_range.end, e.name))
+    evs.sort()
+    t0 = evs[0][0] if evs else 0
+    with open(path, "w") as f:
+        for a_, b_, nm in evs:
+            f.write(f"{a_ - t0:10.2f} {b_ - a_:8.2f}  {nm[:90]}\n")
+    print(f"timeline: {len(evs)} kernels over {n} steps -> {path}", file=sys.stderr)
+
+
 # ---------------------------------------------------------------- e2e (host buffers)
 
 
@@ -932,6 +957,10 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = world * B * 1000.0 / ms
+
+    if args.timeline:
+        write_timeline(args.timeline, step, it, 4)
+        it += 4
 
     # -- per-kernel timing pass (same steps, events around each region)
     table.profile(True)
