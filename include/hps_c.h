@@ -94,10 +94,19 @@ typedef struct hps_table_cfg {
  *   already applied, or any tracked apply after an untracked write since the last
  *   clear) is refused with HPS_E_CLOCK before anything mutates. */
 #define HPS_TABLE_TAG_RING 1u
+/* HPS_TABLE_LRU: every logical shard holds at most shard_capacity rows and evicts its
+ *   least-recently-used row when a miss finds it full (LruStore::put lru_store.hpp:86-113,
+ *   PsShard::find_or_init embedding_ps.hpp:417-434): exact LRU order over the PS surface
+ *   (hps_lookup / hps_table_gather / hps_apply, touches in array order); evictions and
+ *   clock resets counted like PsShard. A call that fits the shards' free rows runs the
+ *   parallel kernels; one that must evict runs a sequential device path (one warp walks
+ *   the call's entries in order). The embedding-worker batch surface and the exchange
+ *   refuse LRU tables (HPS_E_PRECONDITION). capacity is then shard_count * shard_capacity. */
+#define HPS_TABLE_LRU 2u
 
 typedef struct hps_counters {
   uint64_t misses;            /* PsShard::miss_count          embedding_ps.hpp:79 */
-  uint64_t evictions;         /* PsShard::eviction_count      embedding_ps.hpp:75 (always 0: no eviction) */
+  uint64_t evictions;         /* PsShard::eviction_count      embedding_ps.hpp:75 (HPS_TABLE_LRU) */
   uint64_t clock_resets;      /* PsShard::clock_reset_count   embedding_ps.hpp:83 */
   uint64_t stale_epoch_drops; /* PsShard::stale_epoch_drops   embedding_ps.hpp:87 */
   uint64_t size;              /* PsShard::size                embedding_ps.hpp:95 */

@@ -1179,6 +1179,8 @@ static void fwd_route_phase(XBatch& x, Table* t, const uint64_t* ids, uint64_t n
                             const uint32_t* offsets, uint32_t B, uint32_t F, cudaStream_t st,
                             bool fork_pairs) {
   require_connected(x, t->cfg.embedding_dim, n);
+  if (t->d.lru)
+    throw Error(HPS_E_PRECONDITION, "exchange: tables with HPS_TABLE_LRU serve the PS surface only");
   const uint64_t M = x.max_ids;
   PeerIds pid{};
   for (uint32_t d = 0; d < x.G; ++d) {

@@ -37,10 +37,23 @@ __device__ __forceinline__ uint32_t agg_inc(uint32_t* ctr) {
 // overflow counter is raised (exact LRU eviction is SURVEY.md §8f #3).
 __device__ uint32_t alloc_slot(const DevTable& t, uint64_t id, uint32_t* new_slots,
                                uint32_t* new_count) {
-  uint32_t slot = agg_inc(t.hwm);
-  if (slot >= t.capacity) {
-    atomicExch(&t.ctr[kCtrOverflow], 1ull);
-    return kInvalidSlot;
+  uint32_t slot;
+  if (t.lru) {
+    // the shard's own slot range (the host checked the call fits before taking this
+    // parallel path; otherwise lru.cu's sequential path evicts)
+    const uint32_t s = route_shard(id, t.S);
+    const uint32_t k = atomicAdd(&t.shard_hwm[s], 1u);
+    if (k >= t.shard_cap) {
+      atomicExch(&t.ctr[kCtrOverflow], 1ull);
+      return kInvalidSlot;
+    }
+    slot = s * t.shard_cap + k;
+  } else {
+    slot = agg_inc(t.hwm);
+    if (slot >= t.capacity) {
+      atomicExch(&t.ctr[kCtrOverflow], 1ull);
+      return kInvalidSlot;
+    }
   }
   t.slot_id[slot] = id;
   uint32_t q = agg_inc(new_count);

@@ -178,18 +178,23 @@ Table* table_create(const hps_table_cfg& cfg) {
   if (cfg.shard_count == 0) throw Error(HPS_E_CONFIG, "hps_table_create: shard_count must be positive");
   if (!cfg.shard_salts) throw Error(HPS_E_CONFIG, "hps_table_create: shard_salts required");
   if (cfg.embedding_dim == 0) throw Error(HPS_E_CONFIG, "hps_table_create: embedding_dim must be positive");
+  const bool lru = (cfg.flags & HPS_TABLE_LRU) != 0;
+  if (lru && (cfg.shard_capacity == 0 ||
+              cfg.shard_capacity * static_cast<uint64_t>(cfg.shard_count) >= (1ull << 31)))
+    throw Error(HPS_E_CONFIG, "hps_table_create: HPS_TABLE_LRU needs shard_capacity in [1, 2^31 / S)");
   // < 2^31 rows keeps every hash-entry index (H <= 2^32) in 32 bits.
-  if (cfg.capacity == 0 || cfg.capacity >= (1ull << 31))
+  if (!lru && (cfg.capacity == 0 || cfg.capacity >= (1ull << 31)))
     throw Error(HPS_E_CONFIG, "hps_table_create: capacity must be in [1, 2^31)");
   if (cfg.optimizer != HPS_ADAGRAD && cfg.optimizer != HPS_SGD)
     throw Error(HPS_E_CONFIG, "hps_table_create: unknown optimizer");
   if (cfg.world_size == 0 || cfg.owner_rank >= cfg.world_size)
     throw Error(HPS_E_CONFIG, "hps_table_create: owner_rank must be < world_size");
-  if (cfg.flags & ~HPS_TABLE_TAG_RING)
+  if (cfg.flags & ~(HPS_TABLE_TAG_RING | HPS_TABLE_LRU))
     throw Error(HPS_E_CONFIG, "hps_table_create: unknown flags");
   auto t = new Table();
   try {
     t->cfg = cfg;
+    if (lru) t->cfg.capacity = cfg.shard_capacity * cfg.shard_count;
     t->salts.assign(cfg.shard_salts, cfg.shard_salts + cfg.shard_count);
     t->cfg.shard_salts = t->salts.data();
     if (cfg.device >= 0) {
@@ -201,7 +206,7 @@ Table* table_create(const hps_table_cfg& cfg) {
     cudaDeviceProp prop{};
     HPS_CUDA(cudaGetDeviceProperties(&prop, t->device));
     t->sm_count = prop.multiProcessorCount;
-    const uint64_t C = cfg.capacity;
+    const uint64_t C = t->cfg.capacity;
     uint64_t H = 1024;
     int lg = 10;
     while (H < 2 * C) H <<= 1, ++lg;
@@ -223,6 +228,12 @@ Table* table_create(const hps_table_cfg& cfg) {
     HPS_CUDA(cudaMalloc(&d.slot_id, C * sizeof(uint64_t)));
     if (cfg.flags & HPS_TABLE_TAG_RING)
       HPS_CUDA(cudaMalloc(&d.ring, C * kTagRing * sizeof(uint32_t)));
+    if (lru) {
+      d.lru = 1;
+      d.shard_cap = static_cast<uint32_t>(cfg.shard_capacity);
+      HPS_CUDA(cudaMalloc(&d.shard_hwm, cfg.shard_count * sizeof(uint32_t)));
+      HPS_CUDA(cudaMalloc(&d.stamp, C * sizeof(unsigned long long)));
+    }
     HPS_CUDA(cudaMalloc(&d.special, sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.hwm, sizeof(uint32_t)));
     HPS_CUDA(cudaMalloc(&d.ctr, kCtrCount * sizeof(unsigned long long)));
@@ -254,6 +265,11 @@ void table_clear(Table* t, cudaStream_t st) {
   HPS_CUDA(cudaMemsetAsync(d.multi, 0, (d.capacity / 32 + 1) * sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.special, 0xff, sizeof(uint32_t), st));
   HPS_CUDA(cudaMemsetAsync(d.hwm, 0, sizeof(uint32_t), st));
+  if (d.lru) {
+    HPS_CUDA(cudaMemsetAsync(d.shard_hwm, 0, d.S * sizeof(uint32_t), st));
+    HPS_CUDA(cudaMemsetAsync(d.stamp, 0, d.capacity * sizeof(unsigned long long), st));
+    t->clock = 1;
+  }
   HPS_CUDA(cudaMemsetAsync(d.ctr + kCtrOverflow, 0, sizeof(unsigned long long), st));
 }
 
@@ -336,7 +352,8 @@ void table_destroy(Table* t) {
     t->stage.free_all();
     t->prof.destroy();
     DevTable& d = t->d;
-    void* ptrs[] = {d.ht,  d.rows, d.seen,     d.multi,    d.slot_id, d.ring, d.special,
+    void* ptrs[] = {d.ht, d.rows, d.seen, d.multi, d.slot_id, d.ring, d.shard_hwm, d.stamp,
+                    t->lru_scratch, t->lru_keys, t->lru_keys2, d.special,
                     d.hwm, d.ctr,  t->d_salts, t->xs.ids, t->xs.rv,  t->xs.off};
     for (void* p : ptrs)
       if (p) cudaFree(p);
@@ -368,6 +385,14 @@ void table_counters(Table* t, hps_counters* out) {
   out->clock_resets = c[kCtrClockResets];
   out->stale_epoch_drops = c[kCtrStaleDrops];
   out->size = std::min<uint64_t>(hwm, t->cfg.capacity);
+  if (t->d.lru) {
+    std::vector<uint32_t> sh(t->d.S);
+    HPS_CUDA(cudaMemcpy(sh.data(), t->d.shard_hwm, t->d.S * sizeof(uint32_t),
+                        cudaMemcpyDeviceToHost));
+    out->size = 0;
+    for (uint32_t v : sh) out->size += std::min(v, t->d.shard_cap);
+  }
+  out->evictions = c[kCtrEvictions];
   out->capacity = t->cfg.capacity;
   out->epoch = t->epoch;
   out->max_delay = static_cast<uint32_t>(c[kCtrMaxDelay]);
@@ -552,6 +577,9 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
   const uint64_t BF = static_cast<uint64_t>(B) * F;
   if (BF >= 0xffffffffull) throw Error(HPS_E_PRECONDITION, "batch too large (B*F >= 2^32)");
   if (F == 0) throw Error(HPS_E_PRECONDITION, "register: feature group count must be positive");
+  if (t->d.lru)
+    throw Error(HPS_E_PRECONDITION, "register: the batch surface needs a table without "
+                                    "HPS_TABLE_LRU (use hps_lookup / hps_apply)");
   join_sort(b, st);
   forget_outstanding(b);
   b.rv_valid = false;
@@ -816,10 +844,18 @@ void table_lookup(Table* t, const uint64_t* ids, uint64_t n, float* out_values,
   const uint64_t* d_ids = static_cast<const uint64_t*>(stg.in(ids, n * sizeof(uint64_t), st));
   float* d_out = static_cast<float*>(stg.out(out_values, n * t->cfg.embedding_dim * sizeof(float)));
   uint64_t* d_ver = static_cast<uint64_t*>(stg.out(out_versions, n * sizeof(uint64_t)));
+  if (t->d.lru && lru_needs_eviction(t, d_ids, n, st)) {
+    lru_sequential(t, 0, d_ids, n, nullptr, nullptr, 0.0f, 0, 0, d_out, d_ver, nullptr, st);
+    b.registered = false;
+    stg.finish(st);
+    if (!(flags & HPS_ASYNC)) check_flags(t, st, false);
+    return;
+  }
   HPS_CUDA(cudaMemsetAsync(b.small, 0, 8 * sizeof(uint32_t), st));
   launch_probe(t->d, d_ids, n, b.slot, nullptr, nullptr, b.new_slots, &b.small[2], false, st);
   launch_lazy_init(t->d, b.new_slots, &b.small[2], n, t->sm_count, st);
   launch_gather(t->d, b.slot, n, d_out, d_ver, st);
+  if (t->d.lru) lru_stamp(t, b.slot, n, st);
   b.registered = false;
   stg.finish(st);
   if (!(flags & HPS_ASYNC)) check_flags(t, st, false);
@@ -870,7 +906,21 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
     stg.finish(st);
     throw Error(HPS_E_DIVERGENCE, "PsShard::apply_gradients: non-finite gradient");
   }
-  if (!d_dl) {
+  if (t->d.lru) {
+    if (d_rv) note_tag(t, step_tag);
+    if (!d_rv) t->untracked_seen = true;
+    if (lru_needs_eviction(t, d_ids, n, st)) {
+      protect_reads(t, nullptr, st);
+      lru_sequential(t, d_rv ? 1 : 2, d_ids, n, d_g, d_rv, lr, step_tag,
+                     t->d.ring && (t->disordered || t->untracked_seen), nullptr, nullptr, d_dl,
+                     st);
+      if (accepted) *accepted = 1;
+      stg.finish(st);
+      if (!(flags & HPS_ASYNC)) check_flags(t, st);
+      return;
+    }
+  }
+  if (!d_dl && !t->d.lru) {
     // No per-entry delays wanted: the entries as a batch of one-listing samples (sum
     // aggregation: each contribution applied as given) through the batch plan -- rows
     // listed once skip the ordering sort; repeated ids apply in array order.
@@ -889,7 +939,7 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
     stg.finish(st);
     return;
   }
-  if (d_rv) note_tag(t, step_tag);
+  if (d_rv && !t->d.lru) note_tag(t, step_tag);
   protect_reads(t, nullptr, st);
   forget_outstanding(b);
   b.pulled = false;
@@ -913,6 +963,7 @@ void table_apply(Table* t, const uint64_t* ids, const float* grads, const uint64
   a.lr = lr;
   a.step_tag = step_tag;
   launch_update(t->d, a, true, t->sm_count, st);
+  if (t->d.lru) lru_stamp(t, b.slot, n, st);
   b.registered = false;
   if (accepted) *accepted = 1;
   stg.finish(st);

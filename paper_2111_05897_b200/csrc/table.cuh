@@ -34,6 +34,7 @@ enum CounterIdx : int {
   kCtrMaxDelay = 6,
   kCtrDelayHist = 7,   // 17 words: delays 0..15, >=16
   kCtrProtocol = 24,   // sticky until reported: malformed exchange input (exchange.cu)
+  kCtrEvictions = 25,  // LRU mode: rows evicted (PsShard::eviction_count embedding_ps.hpp:75)
   kCtrStep = 30,       // HPS_DEVICE_STEP counter (low 32 bits used)
   kCtrScratch = 31,    // per-call scratch (pair counts)
   kCtrCount = 32
@@ -100,6 +101,13 @@ struct DevTable {
   // the delay needs the exact count (UpdateArgs::exact) or an untracked write moves the
   // version onto an older ring entry.
   uint32_t* ring;
+  // LRU mode (HPS_TABLE_LRU): logical shard s owns slots [s * shard_cap, (s+1) * shard_cap)
+  // (PsShardConfig::capacity per shard, lru_store.hpp), allocated from shard_hwm[s]; each
+  // slot's last touch time is stamp[slot] (the LRU order of the shard's rows; lru.cu).
+  uint32_t lru;
+  uint32_t shard_cap;
+  uint32_t* shard_hwm;
+  unsigned long long* stamp;
   uint32_t capacity;
   uint32_t* hwm;
   unsigned long long* ctr;
@@ -249,6 +257,11 @@ struct Table {
   // older one since the last clear (out-of-order steps: hybrid stragglers).
   uint32_t max_tag = 0;
   bool disordered = false;
+  uint64_t clock = 1;  // LRU mode: touch time of the next access (stamps; 0 = never)
+  uint32_t* lru_scratch = nullptr;  // LRU mode: per-shard counts / candidate ranges
+  void* lru_keys = nullptr;         // LRU mode: candidate sort keys (ping-pong)
+  void* lru_keys2 = nullptr;
+  uint64_t lru_cap = 0;
   bool untracked_seen = false;  // some untracked write (version += 1 without a ring entry)
   cudaStream_t aux_joined = nullptr;
   Batch scratch;  // workspace for the stateless entry points

@@ -70,6 +70,13 @@ void profile_get(Table* t, const char* name, double* ms, uint64_t* count);
 void check_flags(Table* t, cudaStream_t st, bool divergence = true);
 
 void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B);
+// lru.cu (HPS_TABLE_LRU): does the call need evictions (host round trip); stamps of the
+// parallel path; the sequential path (mode 0 lookup, 1 tracked apply, 2 untracked apply)
+bool lru_needs_eviction(Table* t, const uint64_t* d_ids, uint64_t n, cudaStream_t st);
+void lru_stamp(Table* t, const uint32_t* slots, uint64_t n, cudaStream_t st);
+void lru_sequential(Table* t, int mode, const uint64_t* ids, uint64_t n, const float* grads,
+                    const uint64_t* rv, float lr, uint32_t step_tag, int exact, float* out_values,
+                    uint64_t* out_versions, uint32_t* out_delays, cudaStream_t st);
 // The table view a batch's plan kernels use: the table with the batch's own plan bitmaps.
 DevTable batch_plan_view(Batch& b);
 void batch_free(Batch& b);

@@ -100,6 +100,7 @@ MEAN, SUM = 0, 1
 ASYNC = 1
 DEVICE_STEP = 2
 TABLE_TAG_RING = 1  # hps_table_cfg.flags
+TABLE_LRU = 2
 
 # ---- library loading -----------------------------------------------------------------
 
@@ -356,6 +357,10 @@ class ShardSet:
     in-order pipelines' choice, one store per row cheaper -- and refuses (ClockError) the
     tracked applies it could not count exactly.
 
+    ``lru_shard_capacity`` > 0: every logical shard holds at most that many rows and evicts
+    its least-recently-used one on a miss (PsShardConfig::capacity + LruStore; PS surface
+    only, HPS_TABLE_LRU). ``capacity`` is then ignored.
+
     ``salts`` follows one of the reference's conventions, e.g.
     ``ShardSet(S, base_salt)`` -> ``salts[i] = mix64(base_salt + i)``
     (embedding_ps.hpp:513); pass ``salts=`` to use explicit per-shard salts.
@@ -363,13 +368,15 @@ class ShardSet:
 
     def __init__(self, shard_count: int, embedding_dim: int, capacity: int,
                  optimizer: int = ADAGRAD, base_salt: int = 0, salts=None, device: int = -1,
-                 owner_rank: int = 0, world_size: int = 1, tag_ring: bool = True):
+                 owner_rank: int = 0, world_size: int = 1, tag_ring: bool = True,
+                 lru_shard_capacity: int = 0):
         if salts is None:
             salts = [mix64((base_salt + i) & 0xFFFFFFFFFFFFFFFF) for i in range(shard_count)]
         self._salts = np.ascontiguousarray(salts, dtype=np.uint64)
         cfg = TableCfg(len(self._salts), self._salts.ctypes.data_as(C.POINTER(C.c_uint64)),
                        capacity, embedding_dim, optimizer, device, owner_rank, world_size,
-                       TABLE_TAG_RING if tag_ring else 0, 0, 0)
+                       (TABLE_TAG_RING if tag_ring else 0) |
+                       (TABLE_LRU if lru_shard_capacity else 0), 0, lru_shard_capacity)
         h = vp()
         check(lib().hps_table_create(C.byref(cfg), C.byref(h)), "ShardSet")
         self.h = h
@@ -406,6 +413,9 @@ class ShardSet:
 
     def stale_epoch_drops(self) -> int:
         return self.counters().stale_epoch_drops
+
+    def eviction_count(self) -> int:
+        return self.counters().evictions
 
     def clock_reset_count(self) -> int:
         return self.counters().clock_resets

@@ -1021,3 +1021,83 @@ def test_table_without_tag_ring_refuses_what_it_cannot_count(hps):
     t.reset_for_recovery()  # a clear forgets both conditions
     _, rv = t.lookup(ids)
     assert t.apply_gradients(ids, g, rv, 0.01, 1)[0]
+
+
+# ---------------------------------------------------------------- LRU eviction (f3)
+
+
+def _ref_split(ids, S):
+    from paper_2111_05897_b200 import workloads as W
+
+    sh = (W.mix64(np.asarray(ids, np.uint64)) % np.uint64(S)).astype(np.int64)
+    return [np.nonzero(sh == s)[0] for s in range(S)]
+
+
+@pytest.mark.parametrize("D,opt,cap", [(4, "adagrad", 16), (64, "adagrad", 40), (5, "sgd", 7)])
+def test_lru_eviction_matches_reference(hps, D, opt, cap):
+    """Capacity-bound shards over a cycling working set: every lookup's values and
+    versions, every apply's delays, and the eviction / miss / clock-reset counters equal
+    the reference's PsShards (LruStore eviction, re-init on re-miss; oracle/_ref). Calls
+    mix hits, misses that fit and misses that evict (the sequential path)."""
+    import oracle as O
+
+    S = 2
+    salts = [O.mix64(7 + s) for s in range(S)]
+    t = hps.ShardSet(S, D, 0, hps.ADAGRAD if opt == "adagrad" else hps.SGD, salts=salts,
+                     lru_shard_capacity=cap)
+    ref = O.Reference(salts, cap, D, opt, "mean", 1)
+    rng = np.random.default_rng(D + cap)
+    space = 5 * cap
+    step = 0
+    for it in range(60):
+        lo = (it * 3) % space  # a window that drifts over the id space
+        n = int(rng.integers(1, 2 * cap))
+        ids = ((lo + rng.integers(0, 2 * cap, n)) % space).astype(np.uint64)
+        parts = _ref_split(ids, S)
+        if it % 3 != 2:
+            vals, ver = t.lookup(ids)
+            for s, idx in enumerate(parts):
+                if len(idx):
+                    rv_, rver = ref.shard_lookup(s, ids[idx])
+                    assert vals[idx].tobytes() == rv_.tobytes(), (it, s)
+                    assert (ver[idx] == rver).all(), (it, s)
+        else:
+            step += 1
+            g = (rng.standard_normal((n, D)) * 0.3).astype(np.float32)
+            rv = rng.integers(0, 3, n).astype(np.uint64)
+            ok, dl = t.apply_gradients(ids, g, rv, 0.1, step)
+            assert ok
+            for s, idx in enumerate(parts):
+                if len(idx):
+                    okr, dr = ref.shard_apply(s, ids[idx], g[idx], rv[idx], 0.1, step, 0)
+                    assert (dl[idx] == dr).all(), (it, s, dl[idx], dr)
+    cs = [ref.shard_counters(s) for s in range(S)]
+    c = t.counters()
+    assert c.evictions == sum(x["evictions"] for x in cs) > 0
+    assert c.misses == sum(x["misses"] for x in cs)
+    assert c.clock_resets == sum(x["clock_resets"] for x in cs)
+    assert c.size == sum(x["size"] for x in cs)
+
+
+def test_lru_reference_eviction_cases(hps):
+    """test_embedding_ps.cpp:147-169 (EvictionReinitializesAndCounts) and :214-227
+    (EvictionResetIsNotNegative) through the C ABI."""
+    t = hps.ShardSet(1, 2, 0, hps.SGD, salts=[11], lru_shard_capacity=2)
+    fresh = t.lookup([1])[0].copy()
+    t.apply_gradients_map({1: [1.0, 1.0]}, 0.5)
+    t.lookup([2])
+    t.lookup([3])  # evicts 1
+    assert t.eviction_count() == 1
+    assert t.lookup([1])[0].tobytes() == fresh.tobytes()  # re-initialised like fresh
+    a = hps.ShardSet(1, 2, 0, hps.ADAGRAD, salts=[11], lru_shard_capacity=2)
+    g = np.ones((1, 2), np.float32)
+    a.lookup([1])
+    a.apply_gradients([1], g, [0], 0.01, 1)
+    a.apply_gradients([1], g, [1], 0.01, 2)
+    _, v = a.lookup([1])
+    assert v[0] == 2
+    a.lookup([2])
+    a.lookup([3])  # evicts id 1, its version restarts
+    ok, d = a.apply_gradients([1], g, v, 0.01, 3)
+    assert ok and d[0] == 0
+    assert a.clock_reset_count() == 1
