@@ -142,19 +142,43 @@ uint64_t table_ckpt_save(Table* t, uint32_t shard, uint32_t shard_capacity, uint
   if (shard >= S) throw Error(HPS_E_PRECONDITION, "checkpoint_save: shard out of range");
   const uint32_t D = t->cfg.embedding_dim;
   HPS_CUDA(cudaDeviceSynchronize());
-  uint32_t hwm = 0;
-  HPS_CUDA(cudaMemcpy(&hwm, t->d.hwm, sizeof(hwm), cudaMemcpyDeviceToHost));
-  hwm = std::min(hwm, t->d.capacity);
-  std::vector<uint64_t> sid(hwm);
-  if (hwm)
-    HPS_CUDA(cudaMemcpy(sid.data(), t->d.slot_id, hwm * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   std::vector<uint32_t> sel;
-  for (uint32_t s = 0; s < hwm; ++s)
-    if (route_shard(sid[s], S) == shard) sel.push_back(s);
+  std::vector<uint64_t> sid;
+  unsigned long long evictions = 0;
+  if (t->d.lru) {
+    // LRU mode: the shard's own slot range, in recency order (newest first, by stamp)
+    uint32_t hwm = 0;
+    const uint32_t base = shard * t->d.shard_cap;
+    HPS_CUDA(cudaMemcpy(&hwm, t->d.shard_hwm + shard, sizeof(hwm), cudaMemcpyDeviceToHost));
+    HPS_CUDA(cudaMemcpy(&evictions, t->d.shard_evict + shard, sizeof(evictions),
+                        cudaMemcpyDeviceToHost));
+    hwm = std::min(hwm, t->d.shard_cap);
+    sid.resize(static_cast<uint64_t>(base) + hwm);
+    std::vector<unsigned long long> stamp(hwm);
+    if (hwm) {
+      HPS_CUDA(cudaMemcpy(sid.data() + base, t->d.slot_id + base, hwm * sizeof(uint64_t),
+                          cudaMemcpyDeviceToHost));
+      HPS_CUDA(cudaMemcpy(stamp.data(), t->d.stamp + base, hwm * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost));
+    }
+    for (uint32_t k = 0; k < hwm; ++k) sel.push_back(base + k);
+    std::stable_sort(sel.begin(), sel.end(),
+                     [&](uint32_t x, uint32_t y) { return stamp[x - base] < stamp[y - base]; });
+  } else {
+    uint32_t hwm = 0;
+    HPS_CUDA(cudaMemcpy(&hwm, t->d.hwm, sizeof(hwm), cudaMemcpyDeviceToHost));
+    hwm = std::min(hwm, t->d.capacity);
+    sid.resize(hwm);
+    if (hwm)
+      HPS_CUDA(cudaMemcpy(sid.data(), t->d.slot_id, hwm * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    for (uint32_t s = 0; s < hwm; ++s)
+      if (route_shard(sid[s], S) == shard) sel.push_back(s);
+  }
   const uint64_t n = sel.size();
   const uint64_t bytes = kHdr + n * (2 * 8 + 2 * 4) + n * D * 2ull * 4;
   if (!buf || cap < bytes) return bytes;
-  const uint64_t capacity = shard_capacity ? shard_capacity : t->cfg.capacity;
+  const uint64_t capacity =
+      shard_capacity ? shard_capacity : (t->d.lru ? t->d.shard_cap : t->cfg.capacity);
   if (capacity > 0xffffffffull || n > 0xffffffffull)
     throw Error(HPS_E_CONFIG, "checkpoint_save: capacity does not fit the HPS1 header");
   // rows + versions of the shard's slots, gathered on the device
@@ -196,7 +220,7 @@ uint64_t table_ckpt_save(Table* t, uint32_t shard, uint32_t shard_capacity, uint
   wr<uint32_t>(buf + 36, kNil);                      // no free slots (nothing evicted)
   wr<uint32_t>(buf + 40, n32);
   wr<uint32_t>(buf + 44, t->epoch);
-  wr<uint64_t>(buf + 48, 0);                         // evictions: none on the device
+  wr<uint64_t>(buf + 48, evictions);                 // (LRU mode; 0 otherwise)
   uint8_t* q = buf + kHdr;
   for (uint64_t i = 0; i < n; ++i) wr<uint64_t>(q + 8 * i, sid[sel[i]]);
   q += 8 * n;
@@ -252,6 +276,10 @@ void table_ckpt_load(Table* t, const uint8_t* const* images, const uint64_t* siz
     ims.push_back(std::move(im));
   }
   if (total > t->d.capacity) throw Error(HPS_E_CONFIG, "checkpoint_load: images exceed the table capacity");
+  if (t->d.lru)
+    for (const Image& im : ims)
+      if (im.live > t->d.shard_cap)
+        throw Error(HPS_E_CONFIG, "checkpoint_load: an image holds more rows than a shard's capacity");
   // 2. pack the live rows (recency order) and adopt them on the device
   std::vector<uint64_t> ids(total), vers(total);
   std::vector<float> rows(total * 2ull * D);
@@ -298,6 +326,16 @@ void table_ckpt_load(Table* t, const uint8_t* const* images, const uint64_t* siz
     throw;
   }
   release();
+  if (t->d.lru) {  // LruStore::restore keeps the eviction count (embedding_ps.hpp:400)
+    std::vector<unsigned long long> ev(S, 0);
+    for (uint32_t k = 0; k < count; ++k) ev[shard_of[k]] = rd<uint64_t>(images[k] + 48);
+    HPS_CUDA(cudaMemcpy(t->d.shard_evict, ev.data(), S * sizeof(unsigned long long),
+                        cudaMemcpyHostToDevice));
+    unsigned long long tot = 0;
+    for (auto v : ev) tot += v;
+    HPS_CUDA(cudaMemcpy(t->d.ctr + kCtrEvictions, &tot, sizeof(tot), cudaMemcpyHostToDevice));
+    t->clock = total + 2;
+  }
   t->outstanding.clear();  // batches registered before the load refer to old slots
   t->epoch = recover ? std::max(t->epoch, max_epoch) + 1 : max_epoch;
   check_flags(t, nullptr, false);

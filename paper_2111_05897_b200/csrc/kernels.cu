@@ -436,6 +436,8 @@ __global__ void ckpt_restore_kernel(DevTable t, const uint64_t* __restrict__ ids
     }
     if (t.ring && lane < kTagRing) t.ring[static_cast<uint64_t>(s) * kTagRing + lane] = kNoStep;
     if (lane == 0 && !t.svt) t.vt[s] = make_uint2(ver, kNoStep);
+    // LRU mode: rows arrive newest first per image, so earlier rows are more recent
+    if (lane == 0 && t.lru) t.stamp[s] = 1 + n - i;
   }
 }
 

@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(32) lru_seq_kernel(DevTable t, LruSeqArgs a) {
           }
           seq_erase(t, t.slot_id[slot]);
           ++evictions;
+          ++t.shard_evict[sh];
         }
         seq_insert(t, id, slot);
         t.slot_id[slot] = id;

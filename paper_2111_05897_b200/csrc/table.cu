@@ -232,6 +232,7 @@ Table* table_create(const hps_table_cfg& cfg) {
       d.lru = 1;
       d.shard_cap = static_cast<uint32_t>(cfg.shard_capacity);
       HPS_CUDA(cudaMalloc(&d.shard_hwm, cfg.shard_count * sizeof(uint32_t)));
+      HPS_CUDA(cudaMalloc(&d.shard_evict, cfg.shard_count * sizeof(unsigned long long)));
       HPS_CUDA(cudaMalloc(&d.stamp, C * sizeof(unsigned long long)));
     }
     HPS_CUDA(cudaMalloc(&d.special, sizeof(uint32_t)));
@@ -267,6 +268,7 @@ void table_clear(Table* t, cudaStream_t st) {
   HPS_CUDA(cudaMemsetAsync(d.hwm, 0, sizeof(uint32_t), st));
   if (d.lru) {
     HPS_CUDA(cudaMemsetAsync(d.shard_hwm, 0, d.S * sizeof(uint32_t), st));
+    HPS_CUDA(cudaMemsetAsync(d.shard_evict, 0, d.S * sizeof(unsigned long long), st));
     HPS_CUDA(cudaMemsetAsync(d.stamp, 0, d.capacity * sizeof(unsigned long long), st));
     t->clock = 1;
   }
@@ -353,6 +355,7 @@ void table_destroy(Table* t) {
     t->prof.destroy();
     DevTable& d = t->d;
     void* ptrs[] = {d.ht, d.rows, d.seen, d.multi, d.slot_id, d.ring, d.shard_hwm, d.stamp,
+                    d.shard_evict,
                     t->lru_scratch, t->lru_keys, t->lru_keys2, d.special,
                     d.hwm, d.ctr,  t->d_salts, t->xs.ids, t->xs.rv,  t->xs.off};
     for (void* p : ptrs)

@@ -107,6 +107,7 @@ struct DevTable {
   uint32_t lru;
   uint32_t shard_cap;
   uint32_t* shard_hwm;
+  unsigned long long* shard_evict;  // [S] evictions per shard (HPS1 header field)
   unsigned long long* stamp;
   uint32_t capacity;
   uint32_t* hwm;

@@ -1101,3 +1101,30 @@ def test_lru_reference_eviction_cases(hps):
     ok, d = a.apply_gradients([1], g, v, 0.01, 3)
     assert ok and d[0] == 0
     assert a.clock_reset_count() == 1
+
+
+def test_lru_checkpoint_keeps_recency_and_victim(hps):
+    """test_embedding_ps.cpp:272-291 (RoundtripPreservesStateAndVictim): after save and
+    load, the next miss evicts the same row as without the round trip; the reference
+    loads the image and evicts that row too."""
+    import oracle as O
+
+    D, cap = 3, 4
+    mk = lambda: hps.ShardSet(1, D, 0, hps.SGD, salts=[11], lru_shard_capacity=cap)
+    a = mk()
+    for ids in ([1, 2, 3, 4], [2], [1, 3]):  # recency, oldest first: 4, 2, 1, 3
+        a.lookup(np.array(ids, np.uint64))
+    img = a.save_checkpoint(0)
+    b = mk()
+    b.load_checkpoint([img])
+    ref = O.Reference([11], cap, D, "sgd", "mean", 1)
+    ref.shard_import(0, img)
+    for t_ in (a, b):
+        t_.lookup(np.array([9], np.uint64))  # evicts 4
+        assert t_.eviction_count() == 1
+    ref.shard_lookup(0, np.array([9], np.uint64))
+    for t_ in (a, b):
+        _, _, _, present = t_.peek(np.array([1, 2, 3, 4, 9], np.uint64))
+        assert present.tolist() == [True, True, True, False, True]
+    assert ref.shard_counters(0)["evictions"] == 1
+    assert b.save_checkpoint(0) == a.save_checkpoint(0)
