@@ -18,3 +18,4 @@ echo ncu3=$? >> gpurun_out/rc_${TAG}.txt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"update_single|pool_warp|check_stream|probe_kernel" -s 12 -c 8 \
   -o gpurun_out/prof_${TAG} python bench.py $ARGS > gpurun_out/ncu_full_${TAG}.log 2>&1
 echo ncu2=$? >> gpurun_out/rc_${TAG}.txt
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 0 --soak-seconds 0 --timeline gpurun_out/timeline_${TAG}.txt > gpurun_out/bench_tl_${TAG}.log 2>&1; echo tl=$? >> gpurun_out/rc_${TAG}.txt
