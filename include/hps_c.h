@@ -292,6 +292,14 @@ hps_status hps_table_apply_pairs(hps_table* t, const uint64_t* recv_ids,
  *                          order (= apply_backward + flush_step + PsShard::apply_gradients)
  * A peer missing a barrier for ~4 s fails the step with HPS_E_SYNC_FAILURE instead of
  * hanging the device. */
+/* Value codec on the NVLink payloads (opt-in, lossy): with kappa > 0
+ * the owners' rows (PS pull replies, PsShardService(compress) embedding_worker.hpp:183-225)
+ * and the sources' contributions (push frames, EmbeddingWorkerConfig::compress_values
+ * :455,769) travel as kappa-scaled binary16 rows (compress_values codec.hpp:222-244, one
+ * scale per row) and are decoded (decompress_values :246-261) before pooling / applying --
+ * half the bytes on the wire. Every rank must use the same kappa; set before
+ * hps_exchange_arena; 0 = exact fp32 payloads (default). dim: a power of two in [4, 128]. */
+hps_status hps_exchange_set_codec(hps_exchange* x, float kappa);
 hps_status hps_exchange_arena(hps_exchange* x, uint64_t max_ids, uint64_t max_groups,
                               uint32_t dim, void* out_handle);
 /* hps_exchange_forward in two phases, so the next batch's routing and owner lookup can run

@@ -102,7 +102,7 @@ def reference_lib():
         lib.ref_route_shard.argtypes = [C.c_uint64, C.c_uint32]
         lib.ref_table_create.restype = C.c_void_p
         lib.ref_table_create.argtypes = [C.c_uint32, u64p, C.c_uint32, C.c_uint32, C.c_int, C.c_int,
-                                         C.c_uint32, C.c_uint32, C.c_uint64]
+                                         C.c_uint32, C.c_uint32, C.c_uint64, C.c_int]
         lib.ref_table_destroy.argtypes = [C.c_void_p]
         lib.ref_step.restype = C.c_int
         lib.ref_step.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p, f32p, C.c_float, C.c_uint64,
@@ -304,7 +304,7 @@ class Reference:
     """The reference's own path (headers compiled in oracle/_ref)."""
 
     def __init__(self, salts, capacity, dim, optimizer="adagrad", agg="mean", groups=1,
-                 workers=1, ew_buffer=0):
+                 workers=1, ew_buffer=0, compress=False):
         self.lib = reference_lib()
         self.salts = _u64(salts)
         self.S = len(self.salts)
@@ -312,7 +312,8 @@ class Reference:
         self.F = groups
         self.h = self.lib.ref_table_create(self.S, _p(self.salts, u64p), capacity, dim,
                                            0 if optimizer == "adagrad" else 1,
-                                           0 if agg == "mean" else 1, groups, workers, ew_buffer)
+                                           0 if agg == "mean" else 1, groups, workers, ew_buffer,
+                                           int(compress))
         if not self.h:
             raise OracleError(2, self.lib.ref_last_error().decode())
 

@@ -87,8 +87,10 @@ uint64_t ref_mix64(uint64_t x) { return mix64(x); }
 uint32_t ref_route_shard(uint64_t id, uint32_t s) { return s ? route_shard(id, s) : 0u; }
 
 // opt: 0 Adagrad, 1 SGD (EmbOptimizer). agg: 0 mean, 1 sum (Aggregation).
+// compress: PS pull replies and EW push frames carry compress_values blocks
+// (PsShardService(shard, true), EmbeddingWorkerConfig::compress_values).
 void* ref_table_create(uint32_t S, const uint64_t* salts, uint32_t capacity, uint32_t D, int opt,
-                       int agg, uint32_t F, uint32_t E, uint64_t ew_buffer) {
+                       int agg, uint32_t F, uint32_t E, uint64_t ew_buffer, int compress) {
   RefTable* t = nullptr;
   int rc = guarded([&] {
     auto tab = std::make_unique<RefTable>();
@@ -105,7 +107,7 @@ void* ref_table_create(uint32_t S, const uint64_t* salts, uint32_t capacity, uin
       c.rng_salt = salts[s];
       tab->shards.push_back(std::make_unique<PsShard>(c));
       std::string name = "ps" + std::to_string(s);
-      tab->hub.serve(name, PsShardService(*tab->shards[s], false));
+      tab->hub.serve(name, PsShardService(*tab->shards[s], compress != 0));
       tab->eps.push_back(tab->hub.endpoint(name));
     }
     for (uint32_t r = 0; r < tab->E; ++r) {
@@ -115,6 +117,7 @@ void* ref_table_create(uint32_t S, const uint64_t* salts, uint32_t capacity, uin
       ec.embedding_dim = D;
       ec.aggregation = tab->agg;
       ec.buffer_capacity = ew_buffer ? ew_buffer : (1u << 20);
+      ec.compress_values = compress != 0;
       tab->ews.push_back(std::make_unique<EmbeddingWorker>(ec, tab->eps));
     }
     t = tab.release();

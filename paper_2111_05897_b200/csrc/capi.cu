@@ -397,6 +397,14 @@ hps_status hps_table_apply_pairs(hps_table* t, const uint64_t* recv_ids,
   });
 }
 
+hps_status hps_exchange_set_codec(hps_exchange* x, float kappa) {
+  return guarded([&] {
+    REQUIRE(x, "hps_exchange_set_codec: null exchange");
+    std::lock_guard<std::mutex> g(x->mu);
+    hps::xbatch_set_codec(x->impl, kappa);
+  });
+}
+
 hps_status hps_exchange_arena(hps_exchange* x, uint64_t max_ids, uint64_t max_groups,
                               uint32_t dim, void* out_handle) {
   return guarded([&] {

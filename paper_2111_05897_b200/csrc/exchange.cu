@@ -18,10 +18,12 @@
 //
 // The collectives themselves (NCCL all-to-all of ids, rows, pairs) are issued by the
 // caller between these calls (paper_2111_05897_b200/sharded.py).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "common.cuh"
@@ -310,7 +312,45 @@ struct PairOut {
   // write single pairs' positions (NCCL path); the peer path's owners derive them (a
   // single pair's index is its id's index in the owner segment)
   int single_pos;
+  // value codec (kappa > 0, peer path): each contribution row travels as a kappa-scaled
+  // binary16 payload at (uint16_t*)c[d] + k * D and its f32 scale at c[d][scale_off + k]
+  float kappa;
+  uint64_t scale_off;
 };
+
+// compress_values (codec.hpp:222-244) of one row held by an L-lane group (V floats per
+// lane): scale = kappa / max|v| (1 for an all-zero row), payload = binary16(v * scale)
+// rounded to nearest (float_to_half_bits); the group's lane 0 writes the scale.
+template <int V, int L>
+__device__ __forceinline__ void put_coded(float* base, uint64_t rec, uint64_t scale_off,
+                                          uint32_t D, uint32_t d0, const float (&o)[V],
+                                          float kappa) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t mask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (lane & ~(L - 1u)));
+  float m = 0.0f;
+#pragma unroll
+  for (int v = 0; v < V; ++v) m = fmaxf(m, fabsf(o[v]));
+#pragma unroll
+  for (int off = L / 2; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(mask, m, off, L));
+  const float scale = m == 0.0f ? 1.0f : __fdiv_rn(kappa, m);
+  uint16_t h[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const float x = m == 0.0f ? 0.0f : __fmul_rn(o[v], scale);
+    h[v] = __half_as_ushort(__float2half_rn(x));
+  }
+  uint16_t* dst = reinterpret_cast<uint16_t*>(base) + rec * D + d0;
+  if constexpr (V == 4) {
+    uint2 w;
+    w.x = h[0] | (static_cast<uint32_t>(h[1]) << 16);
+    w.y = h[2] | (static_cast<uint32_t>(h[3]) << 16);
+    *reinterpret_cast<uint2*>(dst) = w;
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) dst[v] = h[v];
+  }
+  if ((lane & (L - 1u)) == 0) base[scale_off + rec] = scale;
+}
 
 template <int V>
 __device__ __forceinline__ void flag_nonfinite(const PairOut& po, uint32_t d, const float (&o)[V]) {
@@ -378,7 +418,8 @@ __global__ void __launch_bounds__(kXBlock)
 #pragma unroll
           for (int v = 0; v < V; ++v)
             o[v] = __double2float_rn(__dadd_rn(0.0, __dmul_rn(static_cast<double>(x[u][v]), scale)));
-          put_row<V, GEN>(po.c[d] + out * D + d0, o);
+          if (po.kappa > 0.0f) put_coded<V, L>(po.c[d], out, po.scale_off, D, d0, o, po.kappa);
+          else put_row<V, GEN>(po.c[d] + out * D + d0, o);
           flag_nonfinite<V>(po, d, o);
         }
       }
@@ -460,7 +501,12 @@ __global__ void __launch_bounds__(kXBlock)
       float o[V];
 #pragma unroll
       for (int v = 0; v < V; ++v) o[v] = __double2float_rn(acc[v]);
-      put_row<V, GEN>(po.c[d] + out * D + d0, o);
+      if constexpr (!GEN) {
+        if (po.kappa > 0.0f) put_coded<V, L>(po.c[d], out, po.scale_off, D, d0, o, po.kappa);
+        else put_row<V, GEN>(po.c[d] + out * D + d0, o);
+      } else {
+        put_row<V, GEN>(po.c[d] + out * D + d0, o);
+      }
       flag_nonfinite<V>(po, d, o);
     }
   }
@@ -562,6 +608,8 @@ XBatch::~XBatch() {
   if (gdirect) cudaFree(gdirect);
   if (glist) cudaFree(glist);
   if (pnew) cudaFree(pnew);
+  if (dec_rows) cudaFree(dec_rows);
+  if (dec_contrib) cudaFree(dec_contrib);
   if (side) cudaStreamDestroy(side);
   if (aux) cudaStreamDestroy(aux);
   if (ev_fork) cudaEventDestroy(ev_fork);
@@ -725,6 +773,30 @@ void xbatch_route(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_t* of
   for (uint32_t d = 0; d < x.G; ++d) out_counts[d] = h[d];
 }
 
+// decompress_values (codec.hpp:246-261) of n compressed rows (payload (uint16_t*)rec +
+// k * D, scale rec[scale_off + k]): out = (float)half / scale, one rounded division. n is
+// *n_dev when given (device-side counts), else n_host.
+__global__ void x_decode_kernel(const float* __restrict__ rec, uint64_t scale_off, uint32_t D,
+                                uint64_t n_host, const uint32_t* __restrict__ n_dev,
+                                float* __restrict__ out) {
+  pdl_entry();
+  const uint64_t n = n_dev ? min(n_host, static_cast<uint64_t>(*n_dev)) : n_host;
+  const uint16_t* pay = reinterpret_cast<const uint16_t*>(rec);
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n * D;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = e / D;
+    out[e] = __fdiv_rn(__half2float(__ushort_as_half(pay[e])), rec[scale_off + k]);
+  }
+}
+
+static void decode(const float* rec, uint64_t scale_off, uint32_t D, uint64_t n_host,
+                   const uint32_t* n_dev, float* out, int sms, cudaStream_t st) {
+  if (!n_host) return;
+  launch(x_decode_kernel, std::min<uint64_t>(ceil_div(n_host * D, 256), uint64_t(sms) * 16), 256,
+         0, st, rec, scale_off, D, n_host, n_dev, out);
+  HPS_LAUNCH_CHECK();
+}
+
 void xbatch_pool(XBatch& x, const float* rows, uint32_t D, float* out_pooled, cudaStream_t st) {
   const bool peer = !rows;
   if (peer) {  // peer path: the owners delivered into the arena
@@ -734,6 +806,10 @@ void xbatch_pool(XBatch& x, const float* rows, uint32_t D, float* out_pooled, cu
     // then hand it over (zero-copy when the caller asks for the arena buffer itself)
     const uint64_t BF = static_cast<uint64_t>(x.B) * x.F;
     float* arena_pooled = reinterpret_cast<float*>(x.arena + x.off_pooled);
+    if (x.kappa > 0.0f) {  // the delivered rows are compressed: decode, then pool
+      decode(x.arena_rows, x.max_ids * D / 2, D, x.N, x.seg + x.G, x.dec_rows, x.sms, st);
+      rows = x.dec_rows;
+    }
     if (x.direct_ok) {
       DevTable view{};
       view.rows = const_cast<float*>(rows);
@@ -1024,7 +1100,7 @@ __global__ void __launch_bounds__(256)
     x_owner_gather_kernel(DevTable t, const uint32_t* __restrict__ oslot, uint64_t stride,
                           const XHdr* __restrict__ hdr, PeerRows pr,
                           uint64_t* __restrict__ orv, PeerRows pooled,
-                          const uint32_t* __restrict__ tgt) {
+                          const uint32_t* __restrict__ tgt, float kappa, uint64_t scale_off) {
   pdl_entry();
   using Gm = Geo<V, L, kGuard>;
   const uint32_t r = blockIdx.y;
@@ -1064,6 +1140,11 @@ __global__ void __launch_bounds__(256)
         const uint64_t j = j0 + u * groups;
         // a one-listing group of the requester: its pooled value float(0.0 + (double)row),
         // i.e. row + 0.0f, goes straight into the requester's pooled output
+        if (kappa > 0.0f) {  // the row as a compressed PS pull reply (codec.hpp:222-244)
+          put_coded<V, L>(pr.p[r], seg + j, scale_off, D, ln * V, v[u], kappa);
+          if (ln == 0 && orv) orv[r * stride + j] = slot_ok(t, s[u]) ? vt_read(t, s[u]).x : 0;
+          continue;
+        }
         float* dst = g[u] != 0xffffffffu ? pooled.p[r] + static_cast<uint64_t>(g[u]) * D
                                          : dst_base + j * D;
         if (g[u] != 0xffffffffu)
@@ -1105,6 +1186,8 @@ static size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
 void xbatch_arena(XBatch& x, uint64_t max_ids, uint64_t max_groups, uint32_t D, void* out_handle) {
   if (x.arena) throw Error(HPS_E_PRECONDITION, "exchange arena already created");
   if (!max_ids || !D) throw Error(HPS_E_PRECONDITION, "exchange arena: empty");
+  if (x.kappa > 0.0f && (D % 4 != 0 || D > 128 || (D & (D - 1)) != 0))
+    throw Error(HPS_E_PRECONDITION, "exchange codec: dim must be a power of two in [4, 128]");
   const uint64_t W = x.G, M = max_ids;
   size_t o = al256(sizeof(XHdr));
   x.off_ids = o;     o += al256(W * M * 8);
@@ -1128,9 +1211,20 @@ void xbatch_arena(XBatch& x, uint64_t max_ids, uint64_t max_groups, uint32_t D, 
   HPS_CUDA(cudaMalloc(&x.dev_epoch, sizeof(unsigned long long)));
   HPS_CUDA(cudaMemset(x.dev_epoch, 0, sizeof(unsigned long long)));
   x.arena_rows = reinterpret_cast<float*>(x.arena + x.off_rows);
+  if (x.kappa > 0.0f) {
+    HPS_CUDA(cudaMalloc(&x.dec_rows, M * D * sizeof(float)));
+    HPS_CUDA(cudaMalloc(&x.dec_contrib, W * M * D * sizeof(float)));
+  }
   cudaIpcMemHandle_t h;
   HPS_CUDA(cudaIpcGetMemHandle(&h, x.arena));
   memcpy(out_handle, &h, sizeof(h));
+}
+
+void xbatch_set_codec(XBatch& x, float kappa) {
+  if (x.arena) throw Error(HPS_E_PRECONDITION, "exchange codec: set it before the arena");
+  if (!(kappa >= 0.0f) || !std::isfinite(kappa))
+    throw Error(HPS_E_PRECONDITION, "compress_values: kappa must be positive (0 = off)");
+  x.kappa = kappa;
 }
 
 void xbatch_connect(XBatch& x, uint32_t rank, const void* handles) {
@@ -1189,7 +1283,7 @@ static void fwd_route_phase(XBatch& x, Table* t, const uint64_t* ids, uint64_t n
   }
   // one-listing groups are pooled by their rows' owners when the arena's pooled buffer
   // holds the batch (every rank takes the same decision: same batch shapes)
-  x.direct_ok = static_cast<uint64_t>(B) * F <= x.max_groups;
+  x.direct_ok = static_cast<uint64_t>(B) * F <= x.max_groups && x.kappa == 0.0f;
   const PeerHdrs ph = peer_hdrs(x);
   {
     ProfScope p(t, "x_route", st);
@@ -1270,7 +1364,7 @@ static void fwd_finish_phase(XBatch& x, Table* t, cudaStream_t st) {
       // (no read versions: the owner applies in fresh mode, see xbatch_bwd)
       launch(x_owner_gather_kernel<V, L, G>, dim3(bx, x.G), 256, 0, st, 
           t->d, oslot, M, mine, pr, nullptr, x.direct_ok ? pp : PeerRows{},
-          reinterpret_cast<const uint32_t*>(x.arena + x.off_tgt));
+          reinterpret_cast<const uint32_t*>(x.arena + x.off_tgt), x.kappa, M * t->d.D / 2);
     });
     HPS_LAUNCH_CHECK();
   }
@@ -1340,6 +1434,8 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
       po.bad[d] = &ph.h[d]->bad[x.rank];
     }
     po.epoch = x.dev_epoch;
+    po.kappa = x.kappa;
+    po.scale_off = static_cast<uint64_t>(x.G) * M * D / 2;
     ProfScope p(t, "x_emit", st);
     emit_pairs(x, grads, D, spos, slist, x.xbase, po, st);
   }
@@ -1371,8 +1467,13 @@ void xbatch_bwd(XBatch& x, Table* t, const float* grads, float lr, uint32_t step
   // is the version the forward read -- without carrying it through the arena.
   b.pulled = true;
   b.rv_valid = false;
-  batch_push(b, HPS_SUM, reinterpret_cast<const float*>(x.arena + x.off_contrib), lr, step_tag,
-             epoch, 0, nullptr, accepted, flags | kPushPrechecked, st);
+  const float* contrib = reinterpret_cast<const float*>(x.arena + x.off_contrib);
+  if (x.kappa > 0.0f) {  // compressed pushes (codec.hpp:246-261), P = offsets[cap]
+    decode(contrib, cap * D / 2, D, cap, xs.off + cap, x.dec_contrib, t->sm_count, st);
+    contrib = x.dec_contrib;
+  }
+  batch_push(b, HPS_SUM, contrib, lr, step_tag, epoch, 0, nullptr, accepted,
+             flags | kPushPrechecked, st);
 }
 
 }  // namespace hps

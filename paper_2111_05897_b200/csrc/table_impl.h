@@ -163,6 +163,11 @@ struct XBatch {
   bool pairs_forked = false; // the pair plan ran on `aux` (phase 2 joins it)
   bool prefetched = false;   // phase 1 of the next forward done (hps_exchange_prefetch)
   uint32_t* pnew = nullptr;  // owner probe: [0] new-row count, then the new rows' slots
+  // value codec on the NVLink payloads (hps_exchange_set_codec): rows and contributions
+  // travel kappa-scaled binary16 (codec.hpp:222-261); decoded here before pooling / apply
+  float kappa = 0.0f;
+  float* dec_rows = nullptr;     // [max_ids][D]
+  float* dec_contrib = nullptr;  // [G * max_ids][D]
   uint64_t cap_pnew = 0;
   const uint32_t *pairs_spos = nullptr, *pairs_slist = nullptr;
   uint64_t max_ids = 0;
@@ -184,6 +189,7 @@ void xbatch_pairs(XBatch& x, const float* grads, uint32_t D, uint32_t* out_pair_
                   float* out_contrib, uint64_t* out_pair_counts, cudaStream_t st);
 void xbatch_arena(XBatch& x, uint64_t max_ids, uint64_t max_groups, uint32_t D, void* out_handle);
 void xbatch_connect(XBatch& x, uint32_t rank, const void* handles);
+void xbatch_set_codec(XBatch& x, float kappa);
 void xbatch_fwd(XBatch& x, Table* t, const uint64_t* ids, uint64_t n, const uint32_t* offsets,
                 uint32_t B, uint32_t F, cudaStream_t st);
 // the forward in two phases: route + pair plan (no barrier: may run on a stream beside

@@ -177,6 +177,7 @@ def lib():
         "hps_exchange_pool": (st, [vp, vp, u32, vp, vp]),
         "hps_exchange_pairs": (st, [vp, vp, u32, vp, vp, vp, vp]),
         "hps_exchange_arena": (st, [vp, u64, u64, u32, vp]),
+        "hps_exchange_set_codec": (st, [vp, f32]),
         "hps_exchange_pooled": (st, [vp, C.POINTER(vp)]),
         "hps_exchange_connect": (st, [vp, u32, vp]),
         "hps_exchange_forward": (st, [vp, vp, vp, sz, vp, u32, u32, vp]),

@@ -133,12 +133,15 @@ class _DeviceArray:
 class PeerExchange:
     """The NVLink peer transport (libhps.so hps_exchange_arena/connect/forward/backward)."""
 
-    def __init__(self, ops: DeviceOps, dist, group, rank: int, max_ids: int, max_groups: int):
+    def __init__(self, ops: DeviceOps, dist, group, rank: int, max_ids: int, max_groups: int,
+                 kappa: float = 0.0):
         import torch
 
         self.ops = ops
         self.max_ids = max_ids
         handle = (C.c_uint8 * 64)()
+        if kappa:
+            hps.check(hps.lib().hps_exchange_set_codec(ops.h, kappa), "exchange codec")
         hps.check(hps.lib().hps_exchange_arena(ops.h, max_ids, max_groups, ops.D, handle),
                   "exchange arena")
         ptr = hps.vp()
@@ -201,7 +204,7 @@ class ShardedEmbeddingWorker:
 
     def __init__(self, table: hps.ShardSet, aggregation: int = hps.MEAN, group=None, ops=None,
                  transport: str | None = None, max_ids: int | None = None,
-                 max_groups: int | None = None):
+                 max_groups: int | None = None, codec_kappa: float = 0.0):
         import torch.distributed as dist
 
         self.dist = dist
@@ -219,6 +222,9 @@ class ShardedEmbeddingWorker:
         self.peer = None
         self.max_ids = max_ids
         self.max_groups = max_groups
+        # kappa > 0: rows and contributions cross NVLink as kappa-scaled binary16 (the
+        # reference's compress_values codec, opt-in and lossy; p2p transport)
+        self.codec_kappa = codec_kappa
 
     # -- collectives ------------------------------------------------------------------
     def _exchange_counts(self, counts):
@@ -262,7 +268,7 @@ class ShardedEmbeddingWorker:
             if self.peer is None:
                 self.peer = PeerExchange(self.ops, self.dist, self.group, self.rank,
                                          self.max_ids or max(ids.numel(), 1),
-                                         max(self.max_groups or 0, B * F))
+                                         max(self.max_groups or 0, B * F), self.codec_kappa)
             self.peer.forward(ids, offsets, B, F)
             return
         send_ids, counts = self.ops.route(ids, offsets, B, F)
@@ -281,7 +287,7 @@ class ShardedEmbeddingWorker:
         if self.peer is None:
             self.peer = PeerExchange(self.ops, self.dist, self.group, self.rank,
                                      self.max_ids or max(ids.numel(), 1),
-                                     max(self.max_groups or 0, B * F))
+                                     max(self.max_groups or 0, B * F), self.codec_kappa)
         self._pending = (B, F, ids.numel())
         self.peer.prefetch(ids, offsets, B, F)
 

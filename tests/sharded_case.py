@@ -86,8 +86,44 @@ def _spawn_world(target, world, timeout, args_of, kw, attempts=3):
     return results
 
 
+class RefExpect:
+    """The reference itself (oracle/_ref: E = world embedding workers over S PsShards, sync
+    order) behind the Restatement calls run_rank uses; compress: PS pull replies and push
+    frames carry compress_values blocks (the exchange's codec mode)."""
+
+    def __init__(self, salts, D, opt, agg, F, world, compress):
+        import oracle as O
+
+        self.ref = O.Reference(salts, 1 << 14, D, opt, agg, F, workers=world,
+                               compress=compress)
+        self.D = D
+
+    def pull_batch(self, B, F, ids, offsets, agg):
+        pooled, rv, _ = self.ref.step(B, ids, offsets, pull=True, push=False)
+        return pooled, rv
+
+    def push_batch(self, B, F, ids, offsets, grads, lr, step, read_versions=None,
+                   sample_keys=None, agg=None):
+        self.ref.step(B, ids, offsets, grads, lr, step, True, pull=False, push=True)
+        return True, None
+
+    def peek(self, ids):
+        st = self.ref.state()
+        n = len(ids)
+        w = np.zeros((n, self.D), np.float32)
+        a = np.zeros((n, self.D), np.float32)
+        v = np.zeros(n, np.uint64)
+        p = np.zeros(n, bool)
+        for k, i in enumerate(ids):
+            if int(i) in st:
+                w[k], a[k], v[k] = st[int(i)]
+                p[k] = True
+        return w, a, v, p
+
+
 def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, agg="mean",
-             opt="adagrad", space=60, transport="p2p", graph=False, nan_step=-1, q=None):
+             opt="adagrad", space=60, transport="p2p", graph=False, nan_step=-1, codec=0.0,
+             q=None):
     try:
         import torch
         import torch.distributed as dist
@@ -104,13 +140,16 @@ def run_rank(rank, world, backend, port, use_device, D=8, B=12, F=3, steps=3, ag
                                 world_size=world)
         S = 8
         salts = [O.mix64(7 + s) for s in range(S)]
-        exp = O.Restatement(salts, D, opt)  # the whole global batch, one table
+        # the whole global batch, one table (codec: the reference itself with compression)
+        exp = RefExpect(salts, D, opt, agg, F, world, True) if codec else \
+            O.Restatement(salts, D, opt)
         if use_device:
             dev = torch.device("cuda", rank % torch.cuda.device_count())
             table = hps.ShardSet(S, D, 1 << 14, hps.ADAGRAD if opt == "adagrad" else hps.SGD,
                                  salts=salts)
             ew = ShardedEmbeddingWorker(table, hps.MEAN if agg == "mean" else hps.SUM,
-                                        transport=transport, max_ids=world * B * F * 4)
+                                        transport=transport, max_ids=world * B * F * 4,
+                                        codec_kappa=codec)
             owner_peek = table.peek
         else:
             from sharded_oracle_ops import EpochOnly, OracleOps

@@ -97,6 +97,20 @@ def test_sharded_p2p_two_ranks(agg, opt, D):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2])
+@pytest.mark.parametrize("agg,opt,D", [("mean", "adagrad", 64), ("sum", "sgd", 8)])
+def test_sharded_p2p_value_codec_matches_reference(world, agg, opt, D):
+    """Codec mode (hps_exchange_set_codec, kappa 1024): rows and contributions cross the
+    exchange as kappa-scaled binary16; pooled outputs and the owners' rows, accumulators
+    and versions equal the reference run with PsShardService(compress) and
+    EmbeddingWorkerConfig::compress_values (oracle/_ref), bit for bit."""
+    res = run_world(world, "gloo", use_device=True, agg=agg, opt=opt, D=D, transport="p2p",
+                    codec=1024.0, timeout=400)
+    for r, status, n in res:
+        assert status == "ok", status
+
+
+@pytest.mark.gpu
 def test_sharded_p2p_two_ranks_large_plan_and_graph():
     """Two ranks (one GPU if need be): the radix-sort plan of repeated ids, then a CUDA
     graph of the p2p step replayed on new inputs."""
