@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
     p.add_argument("--no-pipeline", action="store_true",
                    help="C2: register each batch in line instead of beside the previous push")
+    p.add_argument("--register-priority", type=int, default=-1,
+                   help="stream priority of the next batch's register (-1: above the step's "
+                        "own pull/push, so its latency-bound probes interleave with them)")
     p.add_argument("--timeline", default="",
                    help="write a CUPTI kernel timeline of a few graph replays to this file")
     p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
@@ -865,7 +868,7 @@ def main():
     # embedding-worker handles alternate; each batch has its own plan bitmaps.
     pipe = not args.no_pipeline and M % 2 == 0
     ews = [hps.EmbeddingWorker(table, agg) for _ in range(2)] if pipe else []
-    side = torch.cuda.Stream() if pipe else None
+    side = torch.cuda.Stream(priority=args.register_priority) if pipe else None
 
     def pipe_step(i, s):
         nxt = i + 1

@@ -278,20 +278,18 @@ void table_clear(Table* t, cudaStream_t st) {
 static void ensure_aux(Table* t) {
   if (t->aux) return;
   HPS_CUDA(cudaStreamCreateWithFlags(&t->aux, cudaStreamNonBlocking));
+  HPS_CUDA(cudaStreamCreateWithFlags(&t->aux_push, cudaStreamNonBlocking));
   HPS_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
   HPS_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
   HPS_CUDA(cudaEventCreateWithFlags(&t->ev_sort, cudaEventDisableTiming));
 }
 
-// The batch's large-plan sort (forked by batch_register) has finished before `st` goes on.
-// Nothing to wait for when a later push already joined the aux stream's work (which
-// includes this sort) into `st` -- e.g. the next batch registered beside this push.
+// The batch's large-plan sort (forked by batch_register) has finished before `st` goes on
+// (the batch's own event: another batch may be registered -- and sorted -- meanwhile).
 static void join_sort(Batch& b, cudaStream_t st) {
   if (!b.sort_pending) return;
-  Table* t = b.table;
   b.sort_pending = false;
-  if (t->aux_joined == st && t->aux_joined_seq >= b.sort_seq) return;
-  HPS_CUDA(cudaStreamWaitEvent(st, t->ev_sort, 0));
+  HPS_CUDA(cudaStreamWaitEvent(st, b.ev_sort, 0));
 }
 
 DevTable batch_plan_view(Batch& b) {
@@ -329,6 +327,7 @@ static void protect_reads(Table* t, const Batch* except, cudaStream_t st) {
 
 void batch_free(Batch& b) {
   forget_outstanding(b);
+  if (b.ev_sort) cudaEventDestroy(b.ev_sort);
   if (b.seen) cudaFree(b.seen);
   if (b.multi) cudaFree(b.multi);
   b.seen = b.multi = nullptr;
@@ -363,6 +362,7 @@ void table_destroy(Table* t) {
     if (t->h_ctr) cudaFreeHost(t->h_ctr);
     if (t->side) cudaStreamDestroy(t->side);
     if (t->aux) cudaStreamDestroy(t->aux);
+    if (t->aux_push) cudaStreamDestroy(t->aux_push);
     if (t->ev_fork) cudaEventDestroy(t->ev_fork);
     if (t->ev_join) cudaEventDestroy(t->ev_join);
     if (t->ev_sort) cudaEventDestroy(t->ev_sort);
@@ -661,9 +661,9 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     HPS_CUDA(cudaEventRecord(t->ev_fork, st));
     HPS_CUDA(cudaStreamWaitEvent(t->aux, t->ev_fork, 0));
     sort_slots(b, b.slot, true, &b.small[0], t->aux, true);
-    HPS_CUDA(cudaEventRecord(t->ev_sort, t->aux));
+    if (!b.ev_sort) HPS_CUDA(cudaEventCreateWithFlags(&b.ev_sort, cudaEventDisableTiming));
+    HPS_CUDA(cudaEventRecord(b.ev_sort, t->aux));
     b.sort_pending = true;
-    b.sort_seq = ++t->aux_seq;
   }
   b.registered = true;
   b.generation = t->generation;
@@ -792,24 +792,22 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     // Rows listed more than once (ordered chains, latency-bound, few) and rows listed
     // once are disjoint: the multi chains run on a second stream beside the single pass
     // (fork/join events; under graph capture two parallel branches).
+    // (its own stream: the next batch's register may be sorting on t->aux meanwhile)
     ensure_aux(t);
     HPS_CUDA(cudaEventRecord(t->ev_fork, st));
-    HPS_CUDA(cudaStreamWaitEvent(t->aux, t->ev_fork, 0));
+    HPS_CUDA(cudaStreamWaitEvent(t->aux_push, t->ev_fork, 0));
     {
-      ProfScope p(t, "update_multi", t->aux);
-      launch_runs(a, t->sm_count, t->aux);
-      launch_update(pv, a, false, t->sm_count, t->aux);
-      launch_update_runs(pv, a, t->sm_count, t->aux);
+      ProfScope p(t, "update_multi", t->aux_push);
+      launch_runs(a, t->sm_count, t->aux_push);
+      launch_update(pv, a, false, t->sm_count, t->aux_push);
+      launch_update_runs(pv, a, t->sm_count, t->aux_push);
     }
     {
       ProfScope p(t, "update", st);
       launch_update_single(pv, a, t->sm_count, st);
     }
-    HPS_CUDA(cudaEventRecord(t->ev_join, t->aux));
+    HPS_CUDA(cudaEventRecord(t->ev_join, t->aux_push));
     HPS_CUDA(cudaStreamWaitEvent(st, t->ev_join, 0));
-    // every aux fork so far (this push's and earlier registers' sorts) is now in `st`
-    t->aux_joined_seq = ++t->aux_seq;
-    t->aux_joined = st;
   } else {
     ProfScope p(t, "update_multi", st);
     launch_runs(a, t->sm_count, st);

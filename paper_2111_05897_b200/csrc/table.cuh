@@ -181,7 +181,7 @@ struct Batch {
   uint64_t generation = 0;        // Table::generation at register (slots valid only then)
   bool sort_pending = false;      // the plan's gated large sort runs on the table's aux
                                   // stream beside the pooling; joined before its use
-  uint64_t sort_seq = 0;          // its position in the aux stream's work (Table::aux_seq)
+  cudaEvent_t ev_sort = nullptr;  // recorded after that sort (joined by pull / push)
   // Per-batch plan bitmaps (1 bit per slot: listed / listed more than once), so the plan
   // of the next batch can be built while this batch's update runs.
   uint32_t* seen = nullptr;
@@ -246,11 +246,9 @@ struct Table {
   uint32_t sm_count = 148;
   std::mutex mu;  // one call at a time per table (PsShard's per-shard lock)
   cudaStream_t side = nullptr;  // captures the bodies of conditional graph nodes
-  cudaStream_t aux = nullptr;   // update_multi beside update_single
+  cudaStream_t aux = nullptr;       // registers' large-plan sorts beside the pooling
+  cudaStream_t aux_push = nullptr;  // a push's multi-row updates beside update_single
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sort = nullptr;
-  // aux-stream bookkeeping: forks so far, and the newest fork some push already joined
-  // back into stream `aux_joined` (later work there needs no further join)
-  uint64_t aux_seq = 0, aux_joined_seq = 0;
   // Bumped whenever the slot numbering is rebuilt (clear / reset / checkpoint load): a
   // batch registered under an older generation names slots that may now hold other rows.
   uint64_t generation = 0;
@@ -264,7 +262,6 @@ struct Table {
   void* lru_keys2 = nullptr;
   uint64_t lru_cap = 0;
   bool untracked_seen = false;  // some untracked write (version += 1 without a ring entry)
-  cudaStream_t aux_joined = nullptr;
   Batch scratch;  // workspace for the stateless entry points
   StagePool stage;
   // Batches pulled but not yet pushed. Their read versions are only materialised
