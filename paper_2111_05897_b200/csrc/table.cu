@@ -663,7 +663,13 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     sort_slots(b, b.slot, true, &b.small[0], t->aux, true);
     if (!b.ev_sort) HPS_CUDA(cudaEventCreateWithFlags(&b.ev_sort, cudaEventDisableTiming));
     HPS_CUDA(cudaEventRecord(b.ev_sort, t->aux));
-    b.sort_pending = true;
+    // Under CUDA-graph capture the fork rejoins the register's own stream (a captured
+    // branch must end inside its capture, and a later capture may not wait on it);
+    // eagerly, the pull / push of this batch joins it (join_sort).
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    HPS_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusActive) HPS_CUDA(cudaStreamWaitEvent(st, b.ev_sort, 0));
+    b.sort_pending = cs != cudaStreamCaptureStatusActive;
   }
   b.registered = true;
   b.generation = t->generation;
