@@ -144,6 +144,7 @@ uint64_t table_ckpt_save(Table* t, uint32_t shard, uint32_t shard_capacity, uint
   HPS_CUDA(cudaDeviceSynchronize());
   std::vector<uint32_t> sel;
   std::vector<uint64_t> sid;
+  std::vector<uint32_t> lru_order;  // LRU mode: image slots, most recent first
   unsigned long long evictions = 0;
   if (t->d.lru) {
     // LRU mode: the shard's own slot range, in recency order (newest first, by stamp)
@@ -161,9 +162,12 @@ uint64_t table_ckpt_save(Table* t, uint32_t shard, uint32_t shard_capacity, uint
       HPS_CUDA(cudaMemcpy(stamp.data(), t->d.stamp + base, hwm * sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost));
     }
+    // image slot k = device slot base + k; the recency chain follows the stamps
     for (uint32_t k = 0; k < hwm; ++k) sel.push_back(base + k);
-    std::stable_sort(sel.begin(), sel.end(),
-                     [&](uint32_t x, uint32_t y) { return stamp[x - base] < stamp[y - base]; });
+    lru_order.resize(hwm);
+    for (uint32_t k = 0; k < hwm; ++k) lru_order[k] = k;
+    std::stable_sort(lru_order.begin(), lru_order.end(),
+                     [&](uint32_t x, uint32_t y) { return stamp[x] > stamp[y]; });  // newest first
   } else {
     uint32_t hwm = 0;
     HPS_CUDA(cudaMemcpy(&hwm, t->d.hwm, sizeof(hwm), cudaMemcpyDeviceToHost));
@@ -215,8 +219,13 @@ uint64_t table_ckpt_save(Table* t, uint32_t shard, uint32_t shard_capacity, uint
   wr<uint32_t>(buf + 12, static_cast<uint32_t>(capacity));
   wr<uint64_t>(buf + 16, t->salts[shard]);
   wr<uint32_t>(buf + 24, n32);                       // hwm: the slots are dense
-  wr<uint32_t>(buf + 28, n32 ? n32 - 1 : kNil);      // head = newest slot (most recent)
-  wr<uint32_t>(buf + 32, n32 ? 0u : kNil);           // tail = oldest slot
+  if (t->d.lru) {
+    wr<uint32_t>(buf + 28, n32 ? lru_order[0] : kNil);       // head = most recent
+    wr<uint32_t>(buf + 32, n32 ? lru_order[n32 - 1] : kNil);  // tail = least recent
+  } else {
+    wr<uint32_t>(buf + 28, n32 ? n32 - 1 : kNil);  // head = newest slot (most recent)
+    wr<uint32_t>(buf + 32, n32 ? 0u : kNil);       // tail = oldest slot
+  }
   wr<uint32_t>(buf + 36, kNil);                      // no free slots (nothing evicted)
   wr<uint32_t>(buf + 40, n32);
   wr<uint32_t>(buf + 44, t->epoch);
@@ -224,10 +233,16 @@ uint64_t table_ckpt_save(Table* t, uint32_t shard, uint32_t shard_capacity, uint
   uint8_t* q = buf + kHdr;
   for (uint64_t i = 0; i < n; ++i) wr<uint64_t>(q + 8 * i, sid[sel[i]]);
   q += 8 * n;
-  for (uint64_t i = 0; i < n; ++i) wr<uint32_t>(q + 4 * i, i + 1 < n ? uint32_t(i + 1) : kNil);
-  q += 4 * n;
-  for (uint64_t i = 0; i < n; ++i) wr<uint32_t>(q + 4 * i, i ? uint32_t(i - 1) : kNil);
-  q += 4 * n;
+  if (t->d.lru) {  // prev = the next more recent slot, next = the next less recent one
+    for (uint64_t r = 0; r < n; ++r) {
+      wr<uint32_t>(q + 4ull * lru_order[r], r ? lru_order[r - 1] : kNil);
+      wr<uint32_t>(q + 4ull * n + 4ull * lru_order[r], r + 1 < n ? lru_order[r + 1] : kNil);
+    }
+  } else {
+    for (uint64_t i = 0; i < n; ++i) wr<uint32_t>(q + 4 * i, i + 1 < n ? uint32_t(i + 1) : kNil);
+    for (uint64_t i = 0; i < n; ++i) wr<uint32_t>(q + 4 * n + 4 * i, i ? uint32_t(i - 1) : kNil);
+  }
+  q += 8 * n;
   std::memcpy(q, ver.data(), n * 8);
   wr<uint64_t>(buf + kSumOff, fnv1a64(buf, bytes));
   return bytes;
@@ -277,22 +292,38 @@ void table_ckpt_load(Table* t, const uint8_t* const* images, const uint64_t* siz
   }
   if (total > t->d.capacity) throw Error(HPS_E_CONFIG, "checkpoint_load: images exceed the table capacity");
   if (t->d.lru)
-    for (const Image& im : ims)
-      if (im.live > t->d.shard_cap)
+    for (const Image& im : ims) {
+      if (im.hwm > t->d.shard_cap)
         throw Error(HPS_E_CONFIG, "checkpoint_load: an image holds more rows than a shard's capacity");
+      if (im.free_head != kNil)
+        throw Error(HPS_E_CONFIG, "checkpoint_load: images with free slots need a table without "
+                                  "HPS_TABLE_LRU");
+    }
   // 2. pack the live rows (recency order) and adopt them on the device
   std::vector<uint64_t> ids(total), vers(total);
   std::vector<float> rows(total * 2ull * D);
+  // LRU mode: every row back in its image slot (so a save reproduces the image byte for
+  // byte), stamped by its position in the recency chain
+  std::vector<uint32_t> at(t->d.lru ? total : 0);
+  std::vector<unsigned long long> stamps(t->d.lru ? total : 0);
+  std::vector<uint32_t> hwm_of(S, 0);
   uint64_t o = 0;
   for (uint32_t k = 0; k < count; ++k) {
     const Image& im = ims[k];
     const uint8_t* pid = images[k] + kHdr;
     const uint8_t* pv = pid + uint64_t(im.hwm) * 16;
     const uint8_t* pr = pid + uint64_t(im.hwm) * 24;
+    hwm_of[shard_of[k]] = im.hwm;
+    uint64_t rank = 0;
     for (uint32_t sl : im.live_slots) {
       ids[o] = rd<uint64_t>(pid + 8ull * sl);
       vers[o] = rd<uint64_t>(pv + 8ull * sl);
       std::memcpy(&rows[o * 2 * D], pr + uint64_t(sl) * 2 * D * 4, 2ull * D * 4);
+      if (t->d.lru) {
+        at[o] = shard_of[k] * t->d.shard_cap + sl;
+        stamps[o] = 1 + im.live - rank;  // head (most recent) first
+      }
+      ++rank;
       ++o;
     }
   }
@@ -304,10 +335,14 @@ void table_ckpt_load(Table* t, const uint8_t* const* images, const uint64_t* siz
   uint64_t* d_ids = nullptr;
   uint64_t* d_ver = nullptr;
   float* d_rows = nullptr;
+  uint32_t* d_at = nullptr;
+  unsigned long long* d_st = nullptr;
   auto release = [&] {
     cudaFree(d_ids);
     cudaFree(d_ver);
     cudaFree(d_rows);
+    cudaFree(d_at);
+    cudaFree(d_st);
   };
   try {
     if (total) {
@@ -318,7 +353,15 @@ void table_ckpt_load(Table* t, const uint8_t* const* images, const uint64_t* siz
       HPS_CUDA(cudaMemcpy(d_ver, vers.data(), total * 8, cudaMemcpyHostToDevice));
       HPS_CUDA(cudaMemcpy(d_rows, rows.data(), total * 2ull * D * 4, cudaMemcpyHostToDevice));
       HPS_CUDA(cudaMemset(b.small, 0, 8 * sizeof(uint32_t)));
-      launch_ckpt_restore(t->d, d_ids, d_rows, d_ver, total, b.new_slots, &b.small[2], nullptr);
+      if (t->d.lru) {
+        HPS_CUDA(cudaMalloc(&d_at, total * sizeof(uint32_t)));
+        HPS_CUDA(cudaMalloc(&d_st, total * sizeof(unsigned long long)));
+        HPS_CUDA(cudaMemcpy(d_at, at.data(), total * 4, cudaMemcpyHostToDevice));
+        HPS_CUDA(cudaMemcpy(d_st, stamps.data(), total * 8, cudaMemcpyHostToDevice));
+        HPS_CUDA(cudaMemcpy(t->d.shard_hwm, hwm_of.data(), S * 4, cudaMemcpyHostToDevice));
+      }
+      launch_ckpt_restore(t->d, d_ids, d_rows, d_ver, total, b.new_slots, &b.small[2], nullptr,
+                          d_at, d_st);
     }
     HPS_CUDA(cudaDeviceSynchronize());
   } catch (...) {

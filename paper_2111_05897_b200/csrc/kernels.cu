@@ -408,16 +408,45 @@ __global__ void ckpt_gather_kernel(DevTable t, const uint32_t* __restrict__ slot
 
 // Adopt rows: find-or-insert each id, then write its weights, accumulators and version;
 // the latest-bump tag is reset (adopt_locked refills the tag ring with kNoStep, :400).
+// at (LRU mode, optional): the slot each row takes (the image's own slot in its shard's
+// range) and its stamp; the index entry is inserted for that slot.
+__device__ void insert_at(const DevTable& t, uint64_t id, uint32_t slot) {
+  if (id == kEmptyKey) {
+    *t.special = slot;
+    return;
+  }
+  for (uint64_t h = mix64(id ^ kTableHashSalt) >> t.ht_shift, k = 0; k <= t.ht_mask;
+       ++k, h = (h + 1) & t.ht_mask) {
+    if (atomicCAS(&t.ht[h].key, static_cast<unsigned long long>(kEmptyKey),
+                  static_cast<unsigned long long>(id)) == kEmptyKey) {
+      t.ht[h].slot = slot;
+      return;
+    }
+  }
+  atomicExch(&t.ctr[kCtrOverflow], 1ull);
+}
+
 __global__ void ckpt_restore_kernel(DevTable t, const uint64_t* __restrict__ ids,
                                     const float* __restrict__ rows2d,
                                     const uint64_t* __restrict__ vers, uint64_t n,
-                                    uint32_t* new_slots, uint32_t* new_count) {
+                                    uint32_t* new_slots, uint32_t* new_count,
+                                    const uint32_t* __restrict__ at,
+                                    const unsigned long long* __restrict__ stamps) {
   pdl_entry();
   const int lane = threadIdx.x & 31;
   const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
     uint32_t s = 0;
-    if (lane == 0) s = find_or_insert(t, ids[i], new_slots, new_count, true);
+    if (lane == 0) {
+      if (at) {
+        s = at[i];
+        insert_at(t, ids[i], s);
+        t.slot_id[s] = ids[i];
+        t.stamp[s] = stamps[i];
+      } else {
+        s = find_or_insert(t, ids[i], new_slots, new_count, true);
+      }
+    }
     s = __shfl_sync(0xffffffffu, s, 0);
     if (!slot_ok(t, s)) continue;  // capacity: kCtrOverflow is set
     const uint32_t ver = static_cast<uint32_t>(vers[i]);
@@ -436,8 +465,6 @@ __global__ void ckpt_restore_kernel(DevTable t, const uint64_t* __restrict__ ids
     }
     if (t.ring && lane < kTagRing) t.ring[static_cast<uint64_t>(s) * kTagRing + lane] = kNoStep;
     if (lane == 0 && !t.svt) t.vt[s] = make_uint2(ver, kNoStep);
-    // LRU mode: rows arrive newest first per image, so earlier rows are more recent
-    if (lane == 0 && t.lru) t.stamp[s] = 1 + n - i;
   }
 }
 
@@ -451,10 +478,11 @@ void launch_ckpt_gather(const DevTable& t, const uint32_t* slots, uint64_t n, fl
 
 void launch_ckpt_restore(const DevTable& t, const uint64_t* ids, const float* rows2d,
                          const uint64_t* vers, uint64_t n, uint32_t* new_slots,
-                         uint32_t* new_count, cudaStream_t st) {
+                         uint32_t* new_count, cudaStream_t st, const uint32_t* at,
+                         const unsigned long long* stamps) {
   if (!n) return;
   launch(ckpt_restore_kernel, std::min<uint64_t>(ceil_div(n, 8), 148 * 32), 256, 0, st, t, ids,
-         rows2d, vers, n, new_slots, new_count);
+         rows2d, vers, n, new_slots, new_count, at, stamps);
   HPS_LAUNCH_CHECK();
 }
 

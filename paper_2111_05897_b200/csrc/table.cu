@@ -286,9 +286,15 @@ static void ensure_aux(Table* t) {
 
 // The batch's large-plan sort (forked by batch_register) has finished before `st` goes on
 // (the batch's own event: another batch may be registered -- and sorted -- meanwhile).
+// A batch registered eagerly and pulled inside a CUDA-graph capture: its sort is work
+// from before the capture (completed before the graph is launched, as any capture's
+// inputs must be) and cannot be a dependency of the graph.
 static void join_sort(Batch& b, cudaStream_t st) {
   if (!b.sort_pending) return;
   b.sort_pending = false;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  HPS_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs == cudaStreamCaptureStatusActive) return;
   HPS_CUDA(cudaStreamWaitEvent(st, b.ev_sort, 0));
 }
 

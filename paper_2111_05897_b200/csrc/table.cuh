@@ -336,7 +336,8 @@ void launch_ckpt_gather(const DevTable& t, const uint32_t* slots, uint64_t n, fl
                         uint64_t* vers, cudaStream_t st);
 void launch_ckpt_restore(const DevTable& t, const uint64_t* ids, const float* rows2d,
                          const uint64_t* vers, uint64_t n, uint32_t* new_slots,
-                         uint32_t* new_count, cudaStream_t st);
+                         uint32_t* new_count, cudaStream_t st, const uint32_t* at = nullptr,
+                         const unsigned long long* stamps = nullptr);
 void launch_snapshot_rv(const DevTable& t, const uint32_t* slots, uint64_t n, uint32_t* rv,
                         cudaStream_t st);
 void launch_check_direct(const float* grads, uint64_t n_floats, uint32_t* flag,

@@ -1128,3 +1128,30 @@ def test_lru_checkpoint_keeps_recency_and_victim(hps):
         assert present.tolist() == [True, True, True, False, True]
     assert ref.shard_counters(0)["evictions"] == 1
     assert b.save_checkpoint(0) == a.save_checkpoint(0)
+
+
+def test_lru_checkpoint_save_load_save_byte_identical(hps):
+    """test_embedding_ps.cpp:254-270: an image loaded into an LRU table saves back byte
+    for byte (rows return to their image slots, the recency chain to its order), and the
+    reference loads our image and saves the same bytes."""
+    import oracle as O
+
+    D, cap = 3, 8
+    a = hps.ShardSet(1, D, 0, hps.ADAGRAD, salts=[5], lru_shard_capacity=cap)
+    rng = np.random.default_rng(2)
+    for _ in range(50):
+        i = int(rng.integers(0, 12))
+        a.lookup(np.array([i], np.uint64))
+        a.apply_gradients_map({i: rng.uniform(-1, 1, D).astype(np.float32)}, 0.05)
+    first = a.save_checkpoint(0)
+    b = hps.ShardSet(1, D, 0, hps.ADAGRAD, salts=[5], lru_shard_capacity=cap)
+    b.load_checkpoint([first])
+    assert b.save_checkpoint(0) == first
+    ref = O.Reference([5], cap, D, "adagrad", "mean", 1)
+    ref.shard_import(0, first)
+    im = O.parse_hps1(ref.shard_export(0))["rows"]
+    mine = O.parse_hps1(first)["rows"]
+    assert list(im) == list(mine)  # the same recency chain
+    for k in mine:
+        assert im[k][0].tobytes() == mine[k][0].tobytes()
+        assert im[k][1].tobytes() == mine[k][1].tobytes() and im[k][2] == mine[k][2]
