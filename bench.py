@@ -53,6 +53,9 @@ def parse():
     p.add_argument("--register-priority", type=int, default=-1,
                    help="stream priority of the next batch's register (-1: above the step's "
                         "own pull/push, so its latency-bound probes interleave with them)")
+    p.add_argument("--register-after", default="push", choices=["push", "pull"],
+                   help="the next batch's register starts after the previous push (beside "
+                        "this step's pull and push) or after this step's pull (beside its push)")
     p.add_argument("--timeline", default="",
                    help="write a CUPTI kernel timeline of a few graph replays to this file")
     p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
@@ -872,11 +875,14 @@ def main():
 
     def pipe_step(i, s):
         nxt = i + 1
-        side.wait_stream(s)
-        ids1, offs1, _ = batches[nxt % M]
-        ews[nxt % 2].register_batch(ids1, offs1, B, F, stream=side)
         w = ews[i % 2]
-        w.serve_pull(out_pooled=pooled, stream=s)
+        ids1, offs1, _ = batches[nxt % M]
+        if args.register_after == "pull":
+            w.serve_pull(out_pooled=pooled, stream=s)
+        side.wait_stream(s)
+        ews[nxt % 2].register_batch(ids1, offs1, B, F, stream=side)
+        if args.register_after == "push":
+            w.serve_pull(out_pooled=pooled, stream=s)
         w.apply_backward(grads[i % M], cfg.lr, flags=hps.ASYNC | hps.DEVICE_STEP, stream=s)
         s.wait_stream(side)
 

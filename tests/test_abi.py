@@ -95,3 +95,22 @@ def test_compat_header_runs_reference_cases(lib, tmp_path):
     r = subprocess.run([out], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "compat_smoke OK" in r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_ps_tests_pass_on_the_device_table():
+    """The reference's own test_embedding_ps.cpp (28 TESTs: lazy init, SGD / Adagrad
+    arithmetic, atomic rejection, misses, LRU eviction, staleness delays incl. out-of-order
+    steps, HPS1 checkpoints incl. byte-identical save-load-save, corruption detection and
+    recovery, ShardSet routing and isolation), compiled unmodified against
+    tests/cpp/ref_shim -- the reference's PsShard / ShardSet API over the C ABI -- and run
+    on the GPU."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "_bin", "ref_test_embedding_ps")
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " 0 failed" in r.stdout
