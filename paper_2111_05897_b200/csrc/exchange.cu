@@ -1020,7 +1020,13 @@ struct PeerRows {
   float* p[kMaxWorld];
 };
 
-constexpr long long kBarrierTimeoutCycles = 8'000'000'000ll;  // ~4 s: never hang the GPU
+constexpr unsigned long long kBarrierTimeoutNs = 4'000'000'000ull;  // 4 s: never hang the GPU
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // All ranks: arrive (release, system scope) at every peer, then wait (acquire) for
 // every peer's arrival at this rank. A peer that never arrives trips the timeout, which
@@ -1042,12 +1048,12 @@ __global__ void x_barrier_kernel(PeerHdrs ph, uint32_t W, uint32_t rank,
   }
   if (t < W) {
     const unsigned long long* f = &ph.h[rank]->bar[t];
-    const long long t0 = clock64();
+    const unsigned long long t0 = global_ns();  // wall-clock, not SM-clock, timeout
     while (true) {
       unsigned long long v;
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
       if (v >= epoch) break;
-      if (clock64() - t0 > kBarrierTimeoutCycles) {
+      if (global_ns() - t0 > kBarrierTimeoutNs) {
         atomicExch(&ph.h[rank]->err, 1u);
         atomicOr(fail, 1ull);
         break;

@@ -277,12 +277,10 @@ void table_clear(Table* t, cudaStream_t st) {
 
 static void ensure_aux(Table* t) {
   if (t->aux) return;
-  // highest priority: the gated sort no-ops and the (few, latency-bound) multi-row
-  // chains get SM slots ahead of the long single-row pass instead of after it
-  int lo = 0, hi = 0;
-  HPS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  HPS_CUDA(cudaStreamCreateWithPriority(&t->aux, cudaStreamNonBlocking, hi));
-  HPS_CUDA(cudaStreamCreateWithPriority(&t->aux_push, cudaStreamNonBlocking, hi));
+  // (default priorities: measured faster than giving these streams the highest one,
+  // profiles/r2_sched_ab.txt)
+  HPS_CUDA(cudaStreamCreateWithFlags(&t->aux, cudaStreamNonBlocking));
+  HPS_CUDA(cudaStreamCreateWithFlags(&t->aux_push, cudaStreamNonBlocking));
   HPS_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
   HPS_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
   HPS_CUDA(cudaEventCreateWithFlags(&t->ev_sort, cudaEventDisableTiming));
