@@ -206,6 +206,20 @@ Table* table_create(const hps_table_cfg& cfg) {
     cudaDeviceProp prop{};
     HPS_CUDA(cudaGetDeviceProperties(&prop, t->device));
     t->sm_count = prop.multiProcessorCount;
+    // L2 set-aside for the batch-plan bitmaps (two batches in flight, seen + multi each):
+    // grown to what this table needs, never shrunk, within the device's maximum
+    {
+      const size_t want = 4 * (cfg.capacity / 32 + 1) * sizeof(uint32_t);
+      size_t cur = 0;
+      HPS_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+      const size_t lim = std::min<size_t>(want, prop.persistingL2CacheMaxSize);
+      if (lim > cur) HPS_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim));
+      HPS_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+      t->d.plan_l2_hit = want ? std::min(1.0f, static_cast<float>(cur) / static_cast<float>(want)) : 0.0f;
+#ifdef HPS_NO_PLAN_L2  // (A/B builds only)
+      t->d.plan_l2_hit = 0.0f;
+#endif
+    }
     const uint64_t C = t->cfg.capacity;
     uint64_t H = 1024;
     int lg = 10;
@@ -304,10 +318,9 @@ DevTable batch_plan_view(Batch& b) {
   Table* t = b.table;
   if (!b.seen) {
     const size_t words = t->d.capacity / 32 + 1;
-    HPS_CUDA(cudaMalloc(&b.seen, words * sizeof(uint32_t)));
-    HPS_CUDA(cudaMalloc(&b.multi, words * sizeof(uint32_t)));
-    HPS_CUDA(cudaMemset(b.seen, 0, words * sizeof(uint32_t)));
-    HPS_CUDA(cudaMemset(b.multi, 0, words * sizeof(uint32_t)));
+    HPS_CUDA(cudaMalloc(&b.seen, 2 * words * sizeof(uint32_t)));
+    b.multi = b.seen + words;
+    HPS_CUDA(cudaMemset(b.seen, 0, 2 * words * sizeof(uint32_t)));
   }
   DevTable d = t->d;
   d.seen = b.seen;
@@ -336,8 +349,7 @@ static void protect_reads(Table* t, const Batch* except, cudaStream_t st) {
 void batch_free(Batch& b) {
   forget_outstanding(b);
   if (b.ev_sort) cudaEventDestroy(b.ev_sort);
-  if (b.seen) cudaFree(b.seen);
-  if (b.multi) cudaFree(b.multi);
+  if (b.seen) cudaFree(b.seen);  // (multi shares the allocation)
   b.seen = b.multi = nullptr;
   void* ptrs[] = {b.offsets, b.lgrp,  b.slot,   b.keys_a,  b.vals_a,
                   b.keys_b,  b.vals_b, b.rv,  b.new_slots, b.kind,  b.hist,
