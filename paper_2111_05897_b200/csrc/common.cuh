@@ -84,32 +84,6 @@ inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
   HPS_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
-// launch() plus an L2 access-policy window: accesses to [base, base + bytes) are kept
-// in L2's persisting set-aside (the batch-plan bitmaps: small, hammered by random atomics,
-// and otherwise evicted by the step's streaming row traffic).
-template <typename... KArgs, typename... Args>
-inline void launch_persist(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                           cudaStream_t st, const void* base, size_t bytes, float hit_ratio,
-                           Args&&... args) {
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
-  attr[1].val.accessPolicyWindow.base_ptr = const_cast<void*>(base);
-  attr[1].val.accessPolicyWindow.num_bytes = bytes;
-  attr[1].val.accessPolicyWindow.hitRatio = hit_ratio;
-  attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cfg.attrs = attr;
-  cfg.numAttrs = (base && bytes && hit_ratio > 0.0f) ? 2 : 1;
-  HPS_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
-}
-
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x += kGamma;
   x ^= x >> 30;

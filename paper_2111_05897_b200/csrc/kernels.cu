@@ -211,11 +211,8 @@ void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* 
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
                   uint32_t* new_count, bool plan, cudaStream_t st, const uint32_t* n_dev) {
   if (!n) return;
-  // plan: the batch's bitmaps (seen, then multi: one allocation) persist in L2
-  launch_persist(probe_kernel, ceil_div(n, 256 * 2), 256, 0, st, plan ? t.seen : nullptr,
-                 2 * (t.capacity / 32 + 1) * sizeof(uint32_t), t.plan_l2_hit, t, ids, n, slots,
-                 sort_keys, sort_vals,
-                                                     new_slots, new_count, plan, n_dev);
+  launch(probe_kernel, ceil_div(n, 256 * 2), 256, 0, st, t, ids, n, slots, sort_keys, sort_vals,
+         new_slots, new_count, plan, n_dev);
   HPS_LAUNCH_CHECK();
 }
 

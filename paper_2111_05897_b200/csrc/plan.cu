@@ -104,10 +104,8 @@ void launch_classify(const DevTable& t, const uint32_t* slots, uint64_t n, int l
   if (!n) return;
   const uint32_t blocks =
       std::min<uint64_t>(ceil_div(n, kPlanBlock * kPlanItems), static_cast<uint64_t>(sms) * 8);
-  launch_persist(classify_kernel, blocks, kPlanBlock, 0, st, t.seen,
-                 2 * (t.capacity / 32 + 1) * sizeof(uint32_t), t.plan_l2_hit, t, slots, n,
-                 lbits, kind, mkeys, n_multi,
-                                                  n_live);
+  launch(classify_kernel, blocks, kPlanBlock, 0, st, t, slots, n, lbits, kind, mkeys, n_multi,
+         n_live);
   HPS_LAUNCH_CHECK();
 }
 

@@ -206,20 +206,7 @@ Table* table_create(const hps_table_cfg& cfg) {
     cudaDeviceProp prop{};
     HPS_CUDA(cudaGetDeviceProperties(&prop, t->device));
     t->sm_count = prop.multiProcessorCount;
-    // L2 set-aside for the batch-plan bitmaps (two batches in flight, seen + multi each):
-    // grown to what this table needs, never shrunk, within the device's maximum
-    {
-      const size_t want = 4 * (cfg.capacity / 32 + 1) * sizeof(uint32_t);
-      size_t cur = 0;
-      HPS_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-      const size_t lim = std::min<size_t>(want, prop.persistingL2CacheMaxSize);
-      if (lim > cur) HPS_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim));
-      HPS_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-      t->d.plan_l2_hit = want ? std::min(1.0f, static_cast<float>(cur) / static_cast<float>(want)) : 0.0f;
-#ifdef HPS_NO_PLAN_L2  // (A/B builds only)
-      t->d.plan_l2_hit = 0.0f;
-#endif
-    }
+
     const uint64_t C = t->cfg.capacity;
     uint64_t H = 1024;
     int lg = 10;

@@ -95,7 +95,6 @@ struct DevTable {
   // = listed by the batch being planned, `multi` = listed more than once (plan.cu).
   uint32_t* seen;
   uint32_t* multi;  // (a batch's two bitmaps are one allocation: seen, then multi)
-  float plan_l2_hit;  // hit ratio of their L2 persisting window (0: none)
   uint64_t* slot_id;
   // [C][kTagRing] step tags of each row's latest version bumps (PsShard::tag_ring_
   // embedding_ps.hpp:493-494): written at every bump (one 4-byte store), read only when
