@@ -8,3 +8,4 @@ ARGS="--config c3 --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --soak-se
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"update_runs|update_single" -c 2 \
   -o gpurun_out/prof_${TAG} python bench.py $ARGS > gpurun_out/ncu_${TAG}.log 2>&1
 echo ncu=$? >> gpurun_out/rc_${TAG}.txt
+timeout 600 python bench.py --config c3 --batches 2 --steps 6 --warmup 2 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_c3_${TAG}.log 2>&1; echo c3=$? >> gpurun_out/rc_${TAG}.txt
