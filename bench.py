@@ -58,6 +58,9 @@ def parse():
                         "this step's pull and push) or after this step's pull (beside its push)")
     p.add_argument("--timeline", default="",
                    help="write a CUPTI kernel timeline of a few graph replays to this file")
+    p.add_argument("--codec-kappa", type=float, default=0.0,
+                   help="N > 1, p2p: kappa-scaled binary16 payloads on NVLink (the reference's "
+                        "compress_values; lossy, opt-in); 0 = exact fp32 (default)")
     p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                    help="N > 1: NVLink peer writes (p2p) or NCCL all-to-alls")
     return p.parse_args()
@@ -465,7 +468,8 @@ def run_sharded(args, world, rank, local, dev):
              for _ in range(M)]
     pooled = torch.empty((B, F, D), dtype=torch.float32, device=dev)
     max_n = max(b[2] for b in batches)
-    ew = ShardedEmbeddingWorker(table, hps.MEAN, transport=args.transport, max_ids=max_n)
+    ew = ShardedEmbeddingWorker(table, hps.MEAN, transport=args.transport, max_ids=max_n,
+                                codec_kappa=args.codec_kappa)
     tag = [0]
 
     p2p = args.transport == "p2p"
@@ -491,7 +495,8 @@ def run_sharded(args, world, rank, local, dev):
     # a second stream beside this batch's owner lookup, pull and backward.
     pipe = p2p and not args.no_pipeline and M % 2 == 0
     ews = [ew, ShardedEmbeddingWorker(table, hps.MEAN, transport=args.transport,
-                                      max_ids=max_n)] if pipe else []
+                                      max_ids=max_n, codec_kappa=args.codec_kappa)] \
+        if pipe else []
     side = torch.cuda.Stream() if pipe else None
 
     def pipe_step(i):
@@ -589,7 +594,8 @@ def run_sharded(args, world, rank, local, dev):
         P_avg = float(x_pairs) / args.steps
     else:  # one-hot over >= 125M rows per GPU: ~every listing distinct, uniform owners
         U_avg = P_avg = N_avg * (world - 1) / world
-    nvl_bytes = 8 * U_avg + 4 * D * U_avg + (4 + 4 * D) * P_avg
+    row_b = (2 * D + 4) if args.codec_kappa else 4 * D  # binary16 payload + f32 scale
+    nvl_bytes = 8 * U_avg + row_b * U_avg + (4 + row_b) * P_avg
     O_ = D
     uniq = float(N_avg)  # one-hot over 125M rows per GPU: ~all listings distinct
     bytes_step = (8 * N_avg + 8 * N_avg + 12 * uniq + 4 * D * uniq + 4 * B * F * D +
@@ -647,7 +653,9 @@ def run_sharded(args, world, rank, local, dev):
                                    f"{rows // 1_000_000}M-row table dim {D} hash-sharded over "
                                    f"{world} GPUs ({S} logical shards), adagrad, mean pooling, "
                                    f"staleness 0, " + ("NVLink peer-write exchange" if
-                                   args.transport == "p2p" else "NCCL all-to-all exchange"),
+                                   args.transport == "p2p" else "NCCL all-to-all exchange") +
+                                   (f", binary16 payload codec (kappa {args.codec_kappa:g}, "
+                                    f"lossy)" if args.codec_kappa else ", exact fp32 payloads"),
                        "global_batch": B * world, "rows": rows, "dim": D, "features": F,
                        "logical_shards": S, "parallelism": f"sharded{world}",
                        "l2": "per-step footprint > L2 (126 MB); no flush"},
