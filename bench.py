@@ -319,7 +319,9 @@ def run_hybrid(args, world, rank, local, dev):
                        device_step=use_graph)
     torch.backends.cuda.matmul.allow_tf32 = False  # fp32 dense tower, as the reference
     it = 0
-    for _ in range(args.warmup):
+    # (at least one eager step per in-flight batch: every worker's exchange arena and
+    # buffers exist before the steps are captured)
+    for _ in range(max(args.warmup, tau + 1)):
         tr.step(*data[it % M])
         it += 1
     tr.sync()
