@@ -32,6 +32,22 @@ __device__ __forceinline__ uint32_t agg_inc(uint32_t* ctr) {
   return g.shfl(base, 0) + g.thread_rank();
 }
 
+// find_or_init's initialisation (embedding_ps.hpp:424-432) of one row by one thread:
+// weights from the id's random stream, accumulators 0, version 0, no step tag.
+__device__ void init_row(const DevTable& t, uint64_t id, uint32_t slot) {
+  const uint64_t seed = mix64(id ^ mix64(t.salts[route_shard(id, t.S)]));
+  const double limit = 1.0 / sqrt(static_cast<double>(t.D));
+  const double lo = -limit, span = __dsub_rn(limit, lo);
+  float* row = t.rows + static_cast<uint64_t>(slot) * t.stride;
+  for (uint32_t d = 0; d < t.D; ++d) {
+    row[d] = init_value(seed, d, lo, span);
+    row[t.D + d] = (t.svt && d < 64 && (d & 3) >= 2) ? -0.0f : 0.0f;
+  }
+  if (t.ring)
+    for (uint32_t k = 0; k < kTagRing; ++k) t.ring[static_cast<uint64_t>(slot) * kTagRing + k] = kNoStep;
+  if (!t.svt) t.vt[slot] = make_uint2(0u, kNoStep);
+}
+
 // Claim a fresh row for id (lru_store.hpp:95-101: next slot below the high-water
 // mark). No eviction on device: past capacity the insert fails and the sticky
 // overflow counter is raised (exact LRU eviction is SURVEY.md §8f #3).
@@ -56,6 +72,12 @@ __device__ uint32_t alloc_slot(const DevTable& t, uint64_t id, uint32_t* new_slo
     }
   }
   t.slot_id[slot] = id;
+  if (!new_slots) {  // initialise the row here instead of queueing it for lazy_init_kernel
+    init_row(t, id, slot);
+    cg::coalesced_group g = cg::coalesced_threads();
+    if (g.thread_rank() == 0) atomicAdd(&t.ctr[kCtrMisses], static_cast<unsigned long long>(g.size()));
+    return slot;
+  }
   uint32_t q = agg_inc(new_count);
   new_slots[q] = slot;
   return slot;
@@ -134,12 +156,22 @@ void launch_route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cu
 
 // kind (optional): bit 2 marks a listing that is alone in its group (its contribution
 // scale is 1 under mean pooling too), for the plan (plan.cu) and update_single.
+// copy (optional): also keep a copy of the offsets; zero[0 .. nzero): scalars to clear
+// (the batch's counters and flags) -- one launch instead of a copy and a memset node.
 __global__ void expand_groups_kernel(const uint32_t* __restrict__ offsets, uint32_t BF,
-                                     uint32_t* __restrict__ lgrp, uint8_t* __restrict__ kind) {
+                                     uint32_t* __restrict__ lgrp, uint8_t* __restrict__ kind,
+                                     uint32_t* __restrict__ copy, uint32_t* __restrict__ zero,
+                                     uint32_t nzero) {
   pdl_entry();
+  if (blockIdx.x == 0)
+    for (uint32_t k = threadIdx.x; k < nzero; k += blockDim.x) zero[k] = 0;
   for (uint32_t sg = blockIdx.x * blockDim.x + threadIdx.x; sg < BF;
        sg += gridDim.x * blockDim.x) {
     uint32_t a = offsets[sg], e = offsets[sg + 1];
+    if (copy) {
+      copy[sg] = a;
+      if (sg == BF - 1) copy[BF] = e;
+    }
     for (uint32_t i = a; i < e; ++i) {
       lgrp[i] = sg;
       if (kind) kind[i] = e - a == 1 ? kKindAlone : 0;
@@ -148,10 +180,10 @@ __global__ void expand_groups_kernel(const uint32_t* __restrict__ offsets, uint3
 }
 
 void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st,
-                          uint8_t* kind) {
-  if (!BF) return;
-  launch(expand_groups_kernel, std::min<uint64_t>(ceil_div(BF, 256), 148 * 16), 256, 0, st, 
-      offsets, BF, lgrp, kind);
+                          uint8_t* kind, uint32_t* copy, uint32_t* zero, uint32_t nzero) {
+  if (!BF && !nzero) return;
+  launch(expand_groups_kernel, std::max<uint32_t>(1, std::min<uint64_t>(ceil_div(BF, 256), 148 * 16)),
+         256, 0, st, offsets, BF, lgrp, kind, copy, zero, nzero);
   HPS_LAUNCH_CHECK();
 }
 

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kPlanBlock)
 void launch_classify(const DevTable& t, const uint32_t* slots, uint64_t n, int lbits,
                      uint8_t* kind, unsigned long long* mkeys, uint32_t* n_multi, int sms,
                      cudaStream_t st, const uint32_t* n_live) {
-  HPS_CUDA(cudaMemsetAsync(n_multi, 0, sizeof(uint32_t), st));
+  // (n_multi is zeroed by the batch's register, with its other scalars)
   if (!n) return;
   const uint32_t blocks =
       std::min<uint64_t>(ceil_div(n, kPlanBlock * kPlanItems), static_cast<uint64_t>(sms) * 8);

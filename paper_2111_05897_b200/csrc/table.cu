@@ -616,19 +616,17 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
       static_cast<const uint32_t*>(stg.in(offsets, (BF + 1) * sizeof(uint32_t), st));
   const uint64_t* d_sk =
       static_cast<const uint64_t*>(stg.in(sample_keys, B * sizeof(uint64_t), st));
-  // Keep our own copy of the offsets so later pull/push calls do not depend on caller
-  // buffers (ids are consumed here: everything after register works on slots).
-  HPS_CUDA(cudaMemcpyAsync(b.offsets, d_off, (BF + 1) * sizeof(uint32_t),
-                           cudaMemcpyDeviceToDevice, st));
   b.B = B;
   b.F = F;
   b.N = N;
   b.n_live = dynamic ? b.offsets + BF : nullptr;
-  // the batch's device scalars (plan counts, hot-row lists, the push's call flags); an
-  // exchange owner's assembly (slots_ready) has already written the call flags
-  HPS_CUDA(cudaMemsetAsync(b.small, 0, (slots_ready ? kSmallFlags : kSmallWords) * sizeof(uint32_t),
-                           st));
-  launch_expand_groups(b.offsets, static_cast<uint32_t>(BF), b.lgrp, st, b.kind);
+  // Keep our own copy of the offsets so later pull/push calls do not depend on caller
+  // buffers (ids are consumed here: everything after register works on slots), and clear
+  // the batch's device scalars (plan counts, hot-row lists, the push's call flags; an
+  // exchange owner's assembly (slots_ready) has already written the call flags) -- all
+  // in the launch that expands the groups.
+  launch_expand_groups(d_off, static_cast<uint32_t>(BF), b.lgrp, st, b.kind, b.offsets, b.small,
+                       slots_ready ? kSmallFlags : kSmallWords);
   // Sample keys that reorder the batch: every listing takes the sorted (multi) path.
   const bool permute = d_sk && B > 1;
   b.all_multi = permute;
@@ -636,10 +634,10 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     {
       ProfScope p(t, "probe", st);
       // dynamic: N is only a bound; the live listing count is offsets[B*F] on the device
-      launch_probe(pv, d_ids, N, b.slot, nullptr, nullptr, b.new_slots, &b.small[2],
-                   !permute, st, dynamic ? b.offsets + BF : nullptr);
+      // (new rows are initialised by the probe itself: no lazy-init launch per batch)
+      launch_probe(pv, d_ids, N, b.slot, nullptr, nullptr, nullptr, &b.small[2], !permute, st,
+                   dynamic ? b.offsets + BF : nullptr);
     }
-    launch_lazy_init(t->d, b.new_slots, &b.small[2], N, t->sm_count, st);
   }
   if (permute) {
     // Apply order = ascending sample key: enumerate listings sample by sample in key

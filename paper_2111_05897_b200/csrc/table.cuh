@@ -306,7 +306,8 @@ void launch_route(const uint64_t* ids, uint64_t n, uint32_t S, uint32_t* out, cu
 // 0 = no row; kKindAlone = the listing is alone in its (sample, group).
 constexpr uint8_t kKindAlone = 4;
 void launch_expand_groups(const uint32_t* offsets, uint32_t BF, uint32_t* lgrp, cudaStream_t st,
-                          uint8_t* kind = nullptr);
+                          uint8_t* kind = nullptr, uint32_t* copy = nullptr,
+                          uint32_t* zero = nullptr, uint32_t nzero = 0);
 // slots[i] = find_or_insert(ids[i]); when sort_keys/sort_vals are given also writes the
 // (slot, i) pairs the apply-order sort consumes.
 // plan: also mark the rows in the batch-plan bitmaps (plan.cu).

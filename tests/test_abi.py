@@ -97,20 +97,30 @@ def test_compat_header_runs_reference_cases(lib, tmp_path):
     assert "compat_smoke OK" in r.stdout
 
 
+REF_SUITES = ["embedding_ps", "embedding_worker", "nn_worker", "orchestrator"]
+
+
 @pytest.mark.gpu
-def test_reference_ps_tests_pass_on_the_device_table():
-    """The reference's own test_embedding_ps.cpp (28 TESTs: lazy init, SGD / Adagrad
-    arithmetic, atomic rejection, misses, LRU eviction, staleness delays incl. out-of-order
-    steps, HPS1 checkpoints incl. byte-identical save-load-save, corruption detection and
-    recovery, ShardSet routing and isolation), compiled unmodified against
-    tests/cpp/ref_shim -- the reference's PsShard / ShardSet API over the C ABI -- and run
-    on the GPU."""
+@pytest.mark.parametrize("suite", REF_SUITES)
+def test_reference_suites_pass_on_the_device_table(suite):
+    """The reference's own test files, compiled unmodified against tests/cpp/ref_shim --
+    hybridps::PsShard / ShardSet restated over the C ABI, so every PsShard is a device
+    table (LRU capacity, tag ring) -- and run on the GPU:
+      embedding_ps      28 TESTs: lazy init, SGD / Adagrad arithmetic, atomic rejection,
+                        misses, LRU eviction, staleness delays incl. out-of-order steps,
+                        HPS1 checkpoints (byte-identical save-load-save, corruption,
+                        recovery), ShardSet routing and isolation;
+      embedding_worker  the reference's EmbeddingWorker and its PsShardService frame
+                        handler (unmodified) serving the device shards over LocalHub:
+                        pooling, fan-out, ordering, staleness, gated flush, codec frames;
+      nn_worker / orchestrator  the reference's NN workers and whole training loops
+                        (sync / hybrid, checkpoint + recovery) on device shards."""
     import os
     import subprocess
 
-    exe = os.path.join(os.path.dirname(__file__), "cpp", "_bin", "ref_test_embedding_ps")
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "_bin", f"ref_test_{suite}")
     if not os.path.exists(exe):
         pytest.skip("tests/cpp not built (needs /root/reference at build time)")
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " 0 failed" in r.stdout
