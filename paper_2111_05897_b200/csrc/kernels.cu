@@ -197,9 +197,10 @@ __global__ void __launch_bounds__(256)
   pdl_entry();
   // n_dev: the live listing count is device-side (<= n); listings past it get no row.
   const uint64_t n_live = n_dev ? min(n, static_cast<uint64_t>(*n_dev)) : n;
-  // kProbeILP listings per thread: their first probes are issued back to back (the
-  // common case -- key found in its home entry -- then costs one round trip for all).
-  constexpr int kProbeILP = 2;
+  // One listing per thread (two back to back measured slower beside the pooling: the
+  // register runs on the side, and fewer, longer-lived warps cost the critical path
+  // more, profiles/r2_check_probe_ab.txt).
+  constexpr int kProbeILP = 1;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x * kProbeILP + threadIdx.x;
   uint64_t id[kProbeILP];
   ulonglong2 kv[kProbeILP];
@@ -243,7 +244,7 @@ void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* 
                   uint32_t* sort_keys, uint32_t* sort_vals, uint32_t* new_slots,
                   uint32_t* new_count, bool plan, cudaStream_t st, const uint32_t* n_dev) {
   if (!n) return;
-  launch(probe_kernel, ceil_div(n, 256 * 2), 256, 0, st, t, ids, n, slots, sort_keys, sort_vals,
+  launch(probe_kernel, ceil_div(n, 256), 256, 0, st, t, ids, n, slots, sort_keys, sort_vals,
          new_slots, new_count, plan, n_dev);
   HPS_LAUNCH_CHECK();
 }
