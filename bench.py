@@ -50,9 +50,10 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
     p.add_argument("--no-pipeline", action="store_true",
                    help="C2: register each batch in line instead of beside the previous push")
-    p.add_argument("--register-priority", type=int, default=-1,
-                   help="stream priority of the next batch's register (-1: above the step's "
-                        "own pull/push, so its latency-bound probes interleave with them)")
+    p.add_argument("--register-priority", type=int, default=0,
+                   help="stream priority of the next batch's register (0: the step's own; "
+                        "-1 = above it measured slower once the check streams, "
+                        "profiles/r2_check_probe_ab.txt)")
     p.add_argument("--register-after", default="push", choices=["push", "pull"],
                    help="the next batch's register starts after the previous push (beside "
                         "this step's pull and push) or after this step's pull (beside its push)")
@@ -905,13 +906,13 @@ def main():
         torch.cuda.synchronize()
         table.sync()
 
-    # One CUDA graph per input batch: the whole step (~20 kernels) replays without host
-    # launch overhead.
+    # CUDA graphs: one per PAIR of input batches (pipelined: the two steps that share the
+    # two worker handles, ~40 kernels replayed without host launch overhead and without a
+    # graph boundary between them), plus one per batch for odd step counts.
     graphs, graph_launches = [], []
+    pairs, pair_launches = [], []
     it_g = it
     if not args.no_graph:
-        # equal stream priorities for the step's own work (pull + push) and the next
-        # batch's register measured fastest (profiles/r1_prio_ab.txt)
         cap = torch.cuda.Stream()
         for m in range(M):
             g = torch.cuda.CUDAGraph()
@@ -923,6 +924,15 @@ def main():
                     eager_step(m, torch.cuda.current_stream())
             graph_launches.append(hps.launch_count() - l0)
             graphs.append(g)
+        if pipe:
+            for m in range(0, M, 2):
+                g = torch.cuda.CUDAGraph()
+                l0 = hps.launch_count()
+                with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
+                    pipe_step(it_g + m, torch.cuda.current_stream())
+                    pipe_step(it_g + m + 1, torch.cuda.current_stream())
+                pair_launches.append(hps.launch_count() - l0)
+                pairs.append(g)
         torch.cuda.synchronize()
 
     def step(i):
@@ -932,6 +942,21 @@ def main():
             pipe_step(i, stream)
         else:
             eager_step(i)
+
+    def run_steps(i, n):
+        """Steps i .. i+n-1 (pair graphs where a pair starts); returns launches issued."""
+        launches = 0
+        while n > 0:
+            k = (i - it_g) % M
+            if pairs and k % 2 == 0 and n >= 2:
+                pairs[k // 2].replay()
+                launches += pair_launches[k // 2]
+                i, n = i + 2, n - 2
+            else:
+                step(i)
+                launches += graph_launches[k if pipe else i % M] if graphs else 0
+                i, n = i + 1, n - 1
+        return launches
 
     for _ in range(2):
         step(it)
@@ -952,15 +977,13 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        step(it)
-        it += 1
+    g_launches = run_steps(it, args.steps)
+    it += args.steps
     e1.record(stream)
     barrier()
     launches = hps.launch_count() - l0
     if graphs:  # replays do not pass through the host launch counter
-        launches = sum(graph_launches[((i - it_g) if pipe else i) % M]
-                       for i in range(it - args.steps, it))
+        launches = g_launches
     ms = e0.elapsed_time(e1) / args.steps
     # soak: keep the same step running so the clock sampler sees >= soak-seconds under load
     t_soak = time.perf_counter()
