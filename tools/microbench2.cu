@@ -9,6 +9,7 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <algorithm>
 #include <vector>
 
 template <int kVariant, int kRows>
@@ -104,6 +105,15 @@ int main() {
     printf("bpsm=%2d v1 rmw %.1f us | v2 +grad %.1f | v3 +vt %.1f | v4 +adagrad %.1f | v5 2rows %.1f\n",
            bpsm, time(upd<1, 1>, bpsm), time(upd<2, 1>, bpsm), time(upd<3, 1>, bpsm),
            time(upd<4, 1>, bpsm), time(upd<4, 2>, bpsm));
+  }
+  // the same rows visited in ascending slot order (each batch's index list sorted): DRAM
+  // page / TLB locality of a slot-ordered update
+  for (int b = 0; b < 8; ++b) std::sort(h.begin() + b * N, h.begin() + (b + 1) * N);
+  cudaMemcpy(idx, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
+  for (int bpsm : {8, 16}) {
+    printf("sorted bpsm=%2d v1 rmw %.1f us | v2 +grad %.1f | v4 +adagrad %.1f | v5 2rows %.1f\n",
+           bpsm, time(upd<1, 1>, bpsm), time(upd<2, 1>, bpsm), time(upd<4, 1>, bpsm),
+           time(upd<4, 2>, bpsm));
   }
   return 0;
 }
