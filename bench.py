@@ -906,11 +906,12 @@ def main():
         torch.cuda.synchronize()
         table.sync()
 
-    # CUDA graphs: one per PAIR of input batches (pipelined: the two steps that share the
-    # two worker handles, ~40 kernels replayed without host launch overhead and without a
-    # graph boundary between them), plus one per batch for odd step counts.
+    # CUDA graphs: one of the whole cycle of M input batches (M pipelined steps replayed
+    # without host launch overhead and without graph boundaries between them), one per
+    # PAIR of batches and one per batch for step counts that do not fill a cycle.
     graphs, graph_launches = [], []
     pairs, pair_launches = [], []
+    cycle = []
     it_g = it
     if not args.no_graph:
         cap = torch.cuda.Stream()
@@ -933,6 +934,13 @@ def main():
                     pipe_step(it_g + m + 1, torch.cuda.current_stream())
                 pair_launches.append(hps.launch_count() - l0)
                 pairs.append(g)
+            if M > 2:  # and one graph of all M batches' steps
+                g = torch.cuda.CUDAGraph()
+                l0 = hps.launch_count()
+                with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
+                    for m in range(M):
+                        pipe_step(it_g + m, torch.cuda.current_stream())
+                cycle.append((g, hps.launch_count() - l0))
         torch.cuda.synchronize()
 
     def step(i):
@@ -948,7 +956,11 @@ def main():
         launches = 0
         while n > 0:
             k = (i - it_g) % M
-            if pairs and k % 2 == 0 and n >= 2:
+            if cycle and k == 0 and n >= M:
+                cycle[0][0].replay()
+                launches += cycle[0][1]
+                i, n = i + M, n - M
+            elif pairs and k % 2 == 0 and n >= 2:
                 pairs[k // 2].replay()
                 launches += pair_launches[k // 2]
                 i, n = i + 2, n - 2
