@@ -291,6 +291,7 @@ static void ensure_aux(Table* t) {
   HPS_CUDA(cudaStreamCreateWithFlags(&t->aux_push, cudaStreamNonBlocking));
   HPS_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
   HPS_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
+  HPS_CUDA(cudaEventCreateWithFlags(&t->ev_runs, cudaEventDisableTiming));
   HPS_CUDA(cudaEventCreateWithFlags(&t->ev_sort, cudaEventDisableTiming));
 }
 
@@ -379,6 +380,7 @@ void table_destroy(Table* t) {
     if (t->aux_push) cudaStreamDestroy(t->aux_push);
     if (t->ev_fork) cudaEventDestroy(t->ev_fork);
     if (t->ev_join) cudaEventDestroy(t->ev_join);
+    if (t->ev_runs) cudaEventDestroy(t->ev_runs);
     if (t->ev_sort) cudaEventDestroy(t->ev_sort);
   }
   delete t;
@@ -806,6 +808,12 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     a.n_mlist = &b.small[6];
     a.mlist_cap = static_cast<uint32_t>(b.N + 1);  // (sample-key plans list singles too)
   }
+  // Multi-hot batches (more listings than groups): the short runs of the multi list go to
+  // update_short, on the main stream after the single pass, beside update_runs' hot rows.
+  // (A host-side shape test: a one-hot batch's plan is small, its multi list empty.)
+  const bool use_short = !b.all_multi && b.meta_ok && b.N > 2ull * b.B * b.F &&
+                         update_short_fits(t->d, a);
+  a.short_multi = use_short ? 1 : 0;
   if (!b.all_multi) {
     // Rows listed more than once (ordered chains, latency-bound, few) and rows listed
     // once are disjoint: the multi chains run on a second stream beside the single pass
@@ -817,12 +825,17 @@ void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_t
     {
       ProfScope p(t, "update_multi", t->aux_push);
       launch_runs(a, t->sm_count, t->aux_push);
+      if (use_short) HPS_CUDA(cudaEventRecord(t->ev_runs, t->aux_push));
       launch_update(pv, a, false, t->sm_count, t->aux_push);
       launch_update_runs(pv, a, t->sm_count, t->aux_push);
     }
     {
       ProfScope p(t, "update", st);
       launch_update_single(pv, a, t->sm_count, st);
+      if (use_short) {
+        HPS_CUDA(cudaStreamWaitEvent(st, t->ev_runs, 0));  // the multi list is listed
+        launch_update_short(pv, a, t->sm_count, st);
+      }
     }
     HPS_CUDA(cudaEventRecord(t->ev_join, t->aux_push));
     HPS_CUDA(cudaStreamWaitEvent(st, t->ev_join, 0));

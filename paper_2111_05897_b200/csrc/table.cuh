@@ -248,7 +248,7 @@ struct Table {
   cudaStream_t side = nullptr;  // captures the bodies of conditional graph nodes
   cudaStream_t aux = nullptr;       // registers' large-plan sorts beside the pooling
   cudaStream_t aux_push = nullptr;  // a push's multi-row updates beside update_single
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sort = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sort = nullptr, ev_runs = nullptr;
   // Bumped whenever the slot numbering is rebuilt (clear / reset / checkpoint load): a
   // batch registered under an older generation names slots that may now hold other rows.
   uint64_t generation = 0;
@@ -400,6 +400,8 @@ struct UpdateArgs {
   const uint64_t* meta;
   // dynamic batches: live listings (= live groups) on the device; null = a.n
   const uint32_t* n_live;
+  // the multi list (rows of 2..kHotRun-1 listings) goes to update_short, not update_runs
+  int short_multi;
 };
 constexpr uint32_t kHotRun = 64;
 constexpr uint32_t kVeryHotRun = 1024;
@@ -416,6 +418,8 @@ void launch_update_runs(const DevTable& t, const UpdateArgs& a, int sms, cudaStr
 void launch_runs(const UpdateArgs& a, int sms, cudaStream_t st);
 void launch_update(const DevTable& t, const UpdateArgs& a, bool direct, int sms, cudaStream_t st);
 void launch_update_single(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
+void launch_update_short(const DevTable& t, const UpdateArgs& a, int sms, cudaStream_t st);
+bool update_short_fits(const DevTable& t, const UpdateArgs& a);
 void launch_count_pairs(const UpdateArgs& a, unsigned long long* ctr, cudaStream_t st);
 
 void launch_sample_order(const uint64_t* sample_keys, uint32_t B, uint64_t* keys_out,
