@@ -50,6 +50,10 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
     p.add_argument("--no-pipeline", action="store_true",
                    help="C2: register each batch in line instead of beside the previous push")
+    p.add_argument("--prefetch-priority", type=int, default=0,
+                   help="sharded: stream priority of the next batch's prefetch (0 = lowest)")
+    p.add_argument("--step-priority", type=int, default=0,
+                   help="sharded: stream priority of the captured step (-1 = above the prefetch)")
     p.add_argument("--register-priority", type=int, default=0,
                    help="stream priority of the next batch's register (0: the step's own; "
                         "-1 = above it measured slower once the check streams, "
@@ -500,7 +504,7 @@ def run_sharded(args, world, rank, local, dev):
     ews = [ew, ShardedEmbeddingWorker(table, hps.MEAN, transport=args.transport,
                                       max_ids=max_n, codec_kappa=args.codec_kappa)] \
         if pipe else []
-    side = torch.cuda.Stream() if pipe else None
+    side = torch.cuda.Stream(priority=args.prefetch_priority) if pipe else None
 
     def pipe_step(i):
         cur = torch.cuda.current_stream()
@@ -525,10 +529,10 @@ def run_sharded(args, world, rank, local, dev):
         table.sync()
     # p2p: the whole sharded step (route, peer writes, device barriers, owner apply) is
     # stream-ordered without host round trips -> one CUDA graph per input batch.
-    graphs, graph_launches = [], []
+    graphs, graph_launches, cycle = [], [], []
     it_g = it
     if p2p and not args.no_graph:
-        cs = torch.cuda.Stream()
+        cs = torch.cuda.Stream(priority=args.step_priority)
         for m in range(M):
             g = torch.cuda.CUDAGraph()
             l0 = hps.launch_count()
@@ -539,6 +543,13 @@ def run_sharded(args, world, rank, local, dev):
                     eager_step(m)
             graph_launches.append(hps.launch_count() - l0)
             graphs.append(g)
+        if pipe:  # and one graph of the whole cycle of M steps (no graph boundaries)
+            g = torch.cuda.CUDAGraph()
+            l0 = hps.launch_count()
+            with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+                for m in range(M):
+                    pipe_step(it_g + m)
+            cycle.append((g, hps.launch_count() - l0))
         torch.cuda.synchronize()
         dist.barrier()
 
@@ -549,6 +560,21 @@ def run_sharded(args, world, rank, local, dev):
             pipe_step(i)
         else:
             eager_step(i)
+
+    def run_steps(i, n):
+        """Steps i .. i+n-1 (the cycle graph where a cycle starts); returns launches."""
+        launches = 0
+        while n > 0:
+            k = (i - it_g) % M
+            if cycle and k == 0 and n >= M:
+                cycle[0][0].replay()
+                launches += cycle[0][1]
+                i, n = i + M, n - M
+            else:
+                step(i)
+                launches += graph_launches[k if pipe else i % M] if graphs else 0
+                i, n = i + 1, n - 1
+        return launches
 
     for _ in range(2):
         step(it)
@@ -564,19 +590,23 @@ def run_sharded(args, world, rank, local, dev):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     x_ids = x_pairs = 0
-    for _ in range(args.steps):
-        step(it)
-        it += 1
-        if args.transport == "nccl":
-            x_ids += sum(c for d, c in enumerate(ew.send_counts) if d != rank)
-            x_pairs += sum(c for d, c in enumerate(ew.pair_counts) if d != rank)
+    g_launches = 0
+    if graphs:
+        g_launches = run_steps(it, args.steps)
+        it += args.steps
+    else:
+        for _ in range(args.steps):
+            step(it)
+            it += 1
+            if args.transport == "nccl":
+                x_ids += sum(c for d, c in enumerate(ew.send_counts) if d != rank)
+                x_pairs += sum(c for d, c in enumerate(ew.pair_counts) if d != rank)
     e1.record(stream)
     dist.barrier()
     torch.cuda.synchronize()
     launches = hps.launch_count() - l0
-    if graphs:
-        launches = sum(graph_launches[((i - it_g) if pipe else i) % M]
-                       for i in range(it - args.steps, it))
+    if graphs:  # replays do not pass through the host launch counter
+        launches = g_launches
     ms = e0.elapsed_time(e1) / args.steps
     t_soak = time.perf_counter()
     while time.perf_counter() - t_soak < args.soak_seconds:
@@ -585,6 +615,10 @@ def run_sharded(args, world, rank, local, dev):
         torch.cuda.synchronize()
     clk = clocks.stop()
     table.sync()
+    if args.timeline:  # every rank replays (the steps are collective); one file per rank
+        write_timeline(f"{args.timeline}.r{rank}", step, it, 4)
+        it += 4
+        table.sync()
     t = torch.tensor([ms], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
