@@ -948,7 +948,7 @@ def main():
     cycle = []
     it_g = it
     if not args.no_graph:
-        cap = torch.cuda.Stream()
+        cap = torch.cuda.Stream(priority=args.step_priority)
         for m in range(M):
             g = torch.cuda.CUDAGraph()
             l0 = hps.launch_count()

@@ -276,9 +276,6 @@ void table_clear(Table* t, cudaStream_t st) {
   HPS_CUDA(cudaMemsetAsync(d.ctr + kCtrOverflow, 0, sizeof(unsigned long long), st));
 }
 
-#ifndef HPS_AUX_PRIORITY
-#define HPS_AUX_PRIORITY hi
-#endif
 static void ensure_aux(Table* t) {
   if (t->aux) return;
   // The registers' sorts (gated: a few no-op launches for one-hot batches) at the highest
@@ -287,7 +284,7 @@ static void ensure_aux(Table* t) {
   // profiles/r2_sched_ab.txt).
   int lo = 0, hi = 0;
   HPS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  HPS_CUDA(cudaStreamCreateWithPriority(&t->aux, cudaStreamNonBlocking, HPS_AUX_PRIORITY));
+  HPS_CUDA(cudaStreamCreateWithPriority(&t->aux, cudaStreamNonBlocking, hi));
   HPS_CUDA(cudaStreamCreateWithFlags(&t->aux_push, cudaStreamNonBlocking));
   HPS_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
   HPS_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
