@@ -6,7 +6,7 @@ R="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 
 for V in "$@"; do
   touch paper_2111_05897_b200/csrc/*.cu
   make -C paper_2111_05897_b200/csrc -s -j8 EXTRA="$V" > gpurun_out/ab_build.log 2>&1 || { echo "build $V failed" >> gpurun_out/ab_${TAG}.txt; continue; }
-  for F in "" "--step-priority -1"; do
+  for F in "" "--prefetch-priority -1"; do
     timeout 600 $R bench.py --gpus $N --steps 32 --warmup 5 --no-cpu-baseline --e2e-steps 0 $F > gpurun_out/ab.log 2>&1
     python3 -c "
 import json
