@@ -111,6 +111,20 @@ def test_sharded_p2p_value_codec_matches_reference(world, agg, opt, D):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("world", [4, 8])
+def test_sharded_p2p_wide_world(world):
+    """World 4 and 8 over the peer transport, ranks sharing the visible GPUs round-robin
+    (8 processes on one GPU on a 1-GPU box): the wide exchange -- 8 id regions and pair
+    segments per owner, 8-way device barriers, SampleId order across 8 sources -- bit-exact
+    vs the global-batch oracle."""
+    res = run_world(world, "gloo", use_device=True, transport="p2p", B=8, steps=2,
+                    timeout=600)
+    assert sorted(r for r, _, _ in res) == list(range(world))
+    for r, status, n in res:
+        assert status == "ok", status
+
+
+@pytest.mark.gpu
 def test_sharded_p2p_two_ranks_large_plan_and_graph():
     """Two ranks (one GPU if need be): the radix-sort plan of repeated ids, then a CUDA
     graph of the p2p step replayed on new inputs."""
