@@ -130,9 +130,9 @@ def test_sync_two_workers_sample_keys(hps):
                                        (5, "adagrad", "sum"), (128, "adagrad", "mean"),
                                        (200, "sgd", "mean")])
 def test_hot_rows_long_chains(hps, D, opt, agg):
-    # every row hit by thousands of listings per step: hot rows (update_hot: contributions
-    # staged in shared memory, one thread per dimension for the ordered recurrence);
-    # D = 200 exceeds the staging limit and stays on the inline multi path
+    # every row hit by thousands of listings per step: hot rows (update_runs: 32-position
+    # batches of contributions staged in shared memory by cp.async, a warp per 32
+    # dimensions running the ordered recurrence), odd and > 128 dims included
     _sync_vs_oracle(hps, B=2048, F=2, D=D, S=1, opt=opt, agg=agg, steps=2, seed=5,
                     id_space=4, max_per_group=5)
 
