@@ -54,6 +54,8 @@ def parse():
                    help="sharded: stream priority of the next batch's prefetch (0 = lowest)")
     p.add_argument("--step-priority", type=int, default=0,
                    help="sharded: stream priority of the captured step (-1 = above the prefetch)")
+    p.add_argument("--e2e-slots", type=int, default=2,
+                   help="e2e leg: batches in flight (pinned staging / device buffer sets)")
     p.add_argument("--register-priority", type=int, default=0,
                    help="stream priority of the next batch's register (0: the step's own; "
                         "-1 = above it measured slower once the check streams, "
@@ -745,7 +747,7 @@ def run_e2e_local(args, table, agg, cfg, host_batches, grads, stream, dev, B, F,
 
     from paper_2111_05897_b200 import hps
 
-    K = 2
+    K = args.e2e_slots
     ews = [hps.EmbeddingWorker(table, agg) for _ in range(K)]
     M = min(len(host_batches), K)
     nmax = max(hb.N for hb in host_batches[:M])
