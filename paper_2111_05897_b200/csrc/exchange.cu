@@ -608,7 +608,6 @@ XBatch::~XBatch() {
   if (gdirect) cudaFree(gdirect);
   if (glist) cudaFree(glist);
   if (pnew) cudaFree(pnew);
-  if (dec_rows) cudaFree(dec_rows);
   if (dec_contrib) cudaFree(dec_contrib);
   if (side) cudaStreamDestroy(side);
   if (aux) cudaStreamDestroy(aux);
@@ -776,25 +775,80 @@ void xbatch_route(XBatch& x, const uint64_t* ids, uint64_t n, const uint32_t* of
 // decompress_values (codec.hpp:246-261) of n compressed rows (payload (uint16_t*)rec +
 // k * D, scale rec[scale_off + k]): out = (float)half / scale, one rounded division. n is
 // *n_dev when given (device-side counts), else n_host.
-__global__ void x_decode_kernel(const float* __restrict__ rec, uint64_t scale_off, uint32_t D,
+// decompress_values (codec.hpp:246-261): v = (float)h / scale, one rounded divide per
+// element. D is a power of two >= 4 (xbatch_arena checks it): four elements per thread,
+// an 8-byte load and a 16-byte store, the record index by shift.
+__global__ void x_decode_kernel(const float* __restrict__ rec, uint64_t scale_off, uint32_t log2d,
                                 uint64_t n_host, const uint32_t* __restrict__ n_dev,
                                 float* __restrict__ out) {
   pdl_entry();
   const uint64_t n = n_dev ? min(n_host, static_cast<uint64_t>(*n_dev)) : n_host;
-  const uint16_t* pay = reinterpret_cast<const uint16_t*>(rec);
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n * D;
+  const uint2* __restrict__ pay = reinterpret_cast<const uint2*>(rec);
+  const uint64_t quads = (n << log2d) >> 2;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < quads;
        e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = e / D;
-    out[e] = __fdiv_rn(__half2float(__ushort_as_half(pay[e])), rec[scale_off + k]);
+    const float s = __ldg(rec + scale_off + ((e << 2) >> log2d));
+    const uint2 w = __ldcs(pay + e);
+    float4 v;
+    v.x = __fdiv_rn(__half2float(__ushort_as_half(static_cast<unsigned short>(w.x & 0xffffu))), s);
+    v.y = __fdiv_rn(__half2float(__ushort_as_half(static_cast<unsigned short>(w.x >> 16))), s);
+    v.z = __fdiv_rn(__half2float(__ushort_as_half(static_cast<unsigned short>(w.y & 0xffffu))), s);
+    v.w = __fdiv_rn(__half2float(__ushort_as_half(static_cast<unsigned short>(w.y >> 16))), s);
+    reinterpret_cast<float4*>(out)[e] = v;
   }
 }
 
 static void decode(const float* rec, uint64_t scale_off, uint32_t D, uint64_t n_host,
                    const uint32_t* n_dev, float* out, int sms, cudaStream_t st) {
   if (!n_host) return;
-  launch(x_decode_kernel, std::min<uint64_t>(ceil_div(n_host * D, 256), uint64_t(sms) * 16), 256,
-         0, st, rec, scale_off, D, n_host, n_dev, out);
+  uint32_t log2d = 0;
+  while ((1u << log2d) < D) ++log2d;
+  launch(x_decode_kernel,
+         std::max<uint64_t>(1, std::min<uint64_t>(ceil_div((n_host * D) / 4, 256), uint64_t(sms) * 8)),
+         256, 0, st, rec, scale_off, log2d, n_host, n_dev, out);
   HPS_LAUNCH_CHECK();
+}
+
+// serve_pull over compressed rows (codec mode): the requester pools straight from the
+// delivered binary16 records -- each element decoded as decompress_values does it
+// (one rounded divide by the record's scale, codec.hpp:246-261), then pooled exactly as
+// pool_kernel pools (fp64 sum in listing order, (float)(acc * scale), empty -> 0) --
+// without materialising the decoded rows. L = D / 4 lanes per group, 4 dims per lane.
+template <int L>
+__global__ void __launch_bounds__(256)
+    x_pool_coded_kernel(const float* __restrict__ rec, uint64_t scale_off,
+                        const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ sendpos,
+                        uint64_t BF, int mean, float* __restrict__ out) {
+  pdl_entry();
+  constexpr uint32_t D = 4 * L;
+  const uint2* __restrict__ pay = reinterpret_cast<const uint2*>(rec);
+  const uint32_t ln = threadIdx.x % L;
+  const uint64_t groups = static_cast<uint64_t>(gridDim.x) * blockDim.x / L;
+  for (uint64_t g = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L; g < BF;
+       g += groups) {
+    const uint32_t a = offsets[g], e = offsets[g + 1];
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (uint32_t l = a; l < e; ++l) {
+      const uint32_t r = sendpos[l];
+      const float sc = __ldg(rec + scale_off + r);
+      const uint2 w = pay[static_cast<uint64_t>(r) * L + ln];
+      const uint32_t hs[4] = {w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float x = __fdiv_rn(__half2float(__ushort_as_half(static_cast<unsigned short>(hs[k]))), sc);
+        acc[k] = __dadd_rn(acc[k], static_cast<double>(x));
+      }
+    }
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e > a) {
+      const double scale = mean ? __drcp_rn(static_cast<double>(e - a)) : 1.0;
+      v.x = __double2float_rn(__dmul_rn(acc[0], scale));
+      v.y = __double2float_rn(__dmul_rn(acc[1], scale));
+      v.z = __double2float_rn(__dmul_rn(acc[2], scale));
+      v.w = __double2float_rn(__dmul_rn(acc[3], scale));
+    }
+    reinterpret_cast<float4*>(out + g * D)[ln] = v;
+  }
 }
 
 void xbatch_pool(XBatch& x, const float* rows, uint32_t D, float* out_pooled, cudaStream_t st) {
@@ -806,9 +860,21 @@ void xbatch_pool(XBatch& x, const float* rows, uint32_t D, float* out_pooled, cu
     // then hand it over (zero-copy when the caller asks for the arena buffer itself)
     const uint64_t BF = static_cast<uint64_t>(x.B) * x.F;
     float* arena_pooled = reinterpret_cast<float*>(x.arena + x.off_pooled);
-    if (x.kappa > 0.0f) {  // the delivered rows are compressed: decode, then pool
-      decode(x.arena_rows, x.max_ids * D / 2, D, x.N, x.seg + x.G, x.dec_rows, x.sms, st);
-      rows = x.dec_rows;
+    if (x.kappa > 0.0f) {  // the delivered rows are compressed: pool them as they are
+      float* dst = out_pooled ? out_pooled : arena_pooled;
+      require_device(dst, "hps_exchange_pool out");
+      const uint64_t blocks = std::max<uint64_t>(
+          1, std::min<uint64_t>(ceil_div(BF * (D / 4), 256), uint64_t(x.sms) * 8));
+      switch (D) {
+        case 4: launch(x_pool_coded_kernel<1>, blocks, 256, 0, st, x.arena_rows, x.max_ids * D / 2, x.offsets, x.sendpos, BF, x.agg == HPS_MEAN ? 1 : 0, dst); break;
+        case 8: launch(x_pool_coded_kernel<2>, blocks, 256, 0, st, x.arena_rows, x.max_ids * D / 2, x.offsets, x.sendpos, BF, x.agg == HPS_MEAN ? 1 : 0, dst); break;
+        case 16: launch(x_pool_coded_kernel<4>, blocks, 256, 0, st, x.arena_rows, x.max_ids * D / 2, x.offsets, x.sendpos, BF, x.agg == HPS_MEAN ? 1 : 0, dst); break;
+        case 32: launch(x_pool_coded_kernel<8>, blocks, 256, 0, st, x.arena_rows, x.max_ids * D / 2, x.offsets, x.sendpos, BF, x.agg == HPS_MEAN ? 1 : 0, dst); break;
+        case 64: launch(x_pool_coded_kernel<16>, blocks, 256, 0, st, x.arena_rows, x.max_ids * D / 2, x.offsets, x.sendpos, BF, x.agg == HPS_MEAN ? 1 : 0, dst); break;
+        default: launch(x_pool_coded_kernel<32>, blocks, 256, 0, st, x.arena_rows, x.max_ids * D / 2, x.offsets, x.sendpos, BF, x.agg == HPS_MEAN ? 1 : 0, dst); break;
+      }
+      HPS_LAUNCH_CHECK();
+      return;
     }
     if (x.direct_ok) {
       DevTable view{};
@@ -1218,7 +1284,6 @@ void xbatch_arena(XBatch& x, uint64_t max_ids, uint64_t max_groups, uint32_t D, 
   HPS_CUDA(cudaMemset(x.dev_epoch, 0, sizeof(unsigned long long)));
   x.arena_rows = reinterpret_cast<float*>(x.arena + x.off_rows);
   if (x.kappa > 0.0f) {
-    HPS_CUDA(cudaMalloc(&x.dec_rows, M * D * sizeof(float)));
     HPS_CUDA(cudaMalloc(&x.dec_contrib, W * M * D * sizeof(float)));
   }
   cudaIpcMemHandle_t h;

@@ -166,7 +166,6 @@ struct XBatch {
   // value codec on the NVLink payloads (hps_exchange_set_codec): rows and contributions
   // travel kappa-scaled binary16 (codec.hpp:222-261); decoded here before pooling / apply
   float kappa = 0.0f;
-  float* dec_rows = nullptr;     // [max_ids][D]
   float* dec_contrib = nullptr;  // [G * max_ids][D]
   uint64_t cap_pnew = 0;
   const uint32_t *pairs_spos = nullptr, *pairs_slist = nullptr;
