@@ -334,6 +334,53 @@ def run_hybrid(args, world, rank, local, dev):
     tr.sync()
     torch.cuda.synchronize()
     table.sync()
+    # e2e (before the graphs are captured: eager steps, the trainer's pipeline state
+    # carries on into the captured cycle): the same steps through the trainer's API with HOST inputs -- every step's ids,
+    # offsets, dense features and labels copied in from pinned memory (K buffer sets, a
+    # set reused only after the step that read it has finished) and the step's loss read
+    # back to the host
+    e2e = None
+    if args.e2e_steps > 0:
+        K = tau + 2
+        hsets = []
+        for m in range(M):
+            hb = W.make_batch(cfg, 1000 * rank + m)
+            x_, y_ = W.make_dense_inputs(cfg, hb)
+            hsets.append([torch.from_numpy(a).pin_memory() for a in
+                          (hb.ids.view(np.int64), hb.offsets.view(np.int32), x_, y_)])
+        dsets = [[torch.empty_like(h, device=dev) for h in hsets[0]] for _ in range(K)]
+        done = [torch.cuda.Event() for _ in range(K)]
+        h_loss = torch.empty(args.e2e_steps, dtype=torch.float32).pin_memory()
+        nbytes = sum(h.numel() * h.element_size() for h in hsets[0])
+        for e_ in done:
+            e_.record(stream)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for j in range(args.e2e_steps):
+            k = j % K
+            stream.wait_event(done[k])
+            for dbuf, hbuf in zip(dsets[k], hsets[(it + j) % M]):
+                n_ = hbuf.numel()
+                dbuf[:n_].copy_(hbuf, non_blocking=True)
+            loss = tr.step(*dsets[k])
+            tr.sync()  # (the step's streams joined: set k is free again after this point)
+            done[k].record(stream)
+            h_loss[j:j + 1].copy_(loss.reshape(1), non_blocking=True)
+        torch.cuda.synchronize()
+        _ = float(h_loss[-1])
+        e_ms = (time.perf_counter() - w0) * 1000.0 / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        it += args.e2e_steps
+        table.sync()
+        e2e = {"value": world * B * 1000.0 / e_ms, "unit": "samples/s",
+               "h2d_bytes_per_step": int(nbytes), "d2h_bytes_per_step": 4,
+               "path": "HybridTrainer.step on device buffers fed from pinned host memory "
+                       "every step (eager launches, one trainer sync per step)"}
     # One CUDA graph per step of the cycle (lcm of the batch count and tau + 1: the step
     # index picks the batch and the in-flight slot): register + pull(s) and push(s-tau) on
     # the embedding stream, the dense step on the dense stream, forked and joined inside
@@ -418,7 +465,7 @@ def run_hybrid(args, world, rank, local, dev):
                        else "single", "staleness": tau},
             "loss_first_last": [loss_vals[0], loss_vals[-1]],
             "gpu_launches": launches, "clocks": clk, "prewarm_s": prewarm_s,
-            "cpu_baseline": None, "e2e": None,
+            "cpu_baseline": None, "e2e": e2e,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
