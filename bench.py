@@ -270,6 +270,45 @@ def workload_config(cfg, args):
 # ---------------------------------------------------------------- C5: the hybrid step
 
 
+def hybrid_cpu_baseline(cfg, B_s, steps=3):
+    """C5 on the reference's own CPU code (oracle/_ref: EmbeddingWorker -> PsShardService
+    -> PsShard pull on all threads, the reference's DenseNet batch_forward_backward and
+    sgd_step, the ordered push), on a bounded sample: B_s samples of the C5 shape per step,
+    the rows they list created first. Returns (samples/s, cores, sample description)."""
+    import oracle as O
+    from paper_2111_05897_b200 import workloads as W
+
+    hb = W.make_batch(cfg, 20_000, batch=B_s)
+    x, y = W.make_dense_inputs(cfg, hb)
+    D, F = cfg.dim, cfg.features
+    uniq = np.unique(hb.ids)
+    shard = (W.mix64(uniq) % np.uint64(cfg.shards)).astype(np.int64)
+    per_shard = int(np.bincount(shard, minlength=cfg.shards).max() * 1.25) + 1024
+    ref = O.Reference(cfg.salts(), per_shard, D, cfg.optimizer, cfg.aggregation, F)
+    for s_ in range(cfg.shards):
+        ref.shard_lookup(s_, uniq[shard == s_])
+    dims = [F * D + W.C5_NON_ID, *W.C5_HIDDEN]
+    params = O.ref_dense_init(dims, 0)
+    cores = nproc()
+    off = hb.offsets.astype(np.uint64)
+    times = []
+    for s in range(steps + 1):
+        t0 = time.perf_counter()
+        pooled, _, _ = ref.step(B_s, hb.ids, off, None, 0.0, s + 1, True, threads=cores,
+                                pull=True, push=False)
+        inputs = np.concatenate([pooled.reshape(B_s, F * D), x], axis=1)
+        _, _, dg, ig = O.ref_dense_fwd_bwd(dims, params, inputs, y)
+        params = O.ref_sgd_step(params, dg, cfg.lr)
+        g = np.ascontiguousarray(ig[:, :F * D].reshape(B_s, F, D))
+        ref.step(B_s, hb.ids, off, g, cfg.lr, s + 1, True, threads=cores, pull=False,
+                 push=True)
+        if s > 0:
+            times.append(time.perf_counter() - t0)
+    return (B_s * len(times) / sum(times), cores,
+            f"{len(times)} steps x {B_s} samples of the C5 shape (pre-warmed rows): pull on "
+            f"{cores} threads, DenseNet {dims}+1 fwd/bwd + SGD, ordered push (oracle/_ref)")
+
+
 def run_hybrid(args, world, rank, local, dev):
     """C5: embedding lookup + dense tower (1677 -> 64 -> 32 -> 1, fp32 cuBLAS) + the
     reference's canonical dense all-reduce + embedding update (HybridTrainer), bounded
@@ -448,6 +487,11 @@ def run_hybrid(args, world, rank, local, dev):
     table.sync()
     loss_vals = [float(v) for v in losses]
     value = world * B * 1000.0 / ms
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v_, c_, smp = hybrid_cpu_baseline(cfg, 1024)
+        cpu_base = {"value": v_, "unit": "samples/s", "cores": c_, "kind": "reference",
+                    "sample": smp}
     if rank == 0:
         params = tr.tower.param_count
         line = {
@@ -465,7 +509,7 @@ def run_hybrid(args, world, rank, local, dev):
                        else "single", "staleness": tau},
             "loss_first_last": [loss_vals[0], loss_vals[-1]],
             "gpu_launches": launches, "clocks": clk, "prewarm_s": prewarm_s,
-            "cpu_baseline": None, "e2e": e2e,
+            "cpu_baseline": cpu_base, "e2e": e2e,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
