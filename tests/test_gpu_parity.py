@@ -192,6 +192,57 @@ def test_c3_multi_hot_zipf(hps):
     _sync_vs_oracle_batch(hps, cfg, b)
 
 
+@pytest.mark.parametrize("opt,agg", [("sgd", "sum"), ("adagrad", "sum"), ("sgd", "mean")])
+def test_multi_hot_large_plan_short_runs(hps, opt, agg):
+    """A multi-hot batch (listings >> groups) with > 4096 repeated listings: the large plan
+    with per-position metadata, so runs of 2..63 listings take update_short (a warp per row
+    from registers) and longer ones update_runs -- for SGD and sum pooling too."""
+    from paper_2111_05897_b200 import workloads as W
+
+    rng = np.random.default_rng(41)
+    batches = [W.random_csr(rng, 1500, 4, 24, 4000) for _ in range(2)]
+    assert int(batches[0][1][-1]) > 2 * 1500 * 4
+    _sync_vs_oracle(hps, B=1500, F=4, D=64, S=4, opt=opt, agg=agg, steps=2, batches=batches)
+
+
+def test_multi_hot_large_plan_stale_reads(hps):
+    """Two multi-hot batches pulled before either is pushed: the second push's read
+    versions predate the first push (snapshot path), through the large plan's update_short /
+    update_runs version accounting -- rows, accumulators, versions and clock resets vs the
+    oracle."""
+    import oracle as O
+    from paper_2111_05897_b200 import workloads as W
+
+    rng = np.random.default_rng(43)
+    S, D, B, F = 4, 64, 1200, 4
+    salts = [W.mix64_int(100 + s) for s in range(S)]
+    orc = O.Restatement(salts, D, "adagrad")
+    table = hps.ShardSet(S, D, 1 << 16, hps.ADAGRAD, salts=salts)
+    ews = [hps.EmbeddingWorker(table, hps.MEAN) for _ in range(2)]
+    bs = [W.random_csr(rng, B, F, 24, 3000) for _ in range(2)]
+    gs = [(rng.standard_normal((B, F, D)) * 0.3).astype(np.float32) for _ in range(2)]
+    rvos = []
+    for k in range(2):
+        ids, offs = bs[k]
+        po, rvo = orc.pull_batch(B, F, ids, offs.astype(np.uint64), "mean")
+        rvos.append(rvo)
+        ews[k].register_batch(ids, offs, B, F)
+        pg = ews[k].serve_pull()
+        assert pg.tobytes() == po.tobytes()
+    for k in range(2):
+        ids, offs = bs[k]
+        orc.push_batch(B, F, ids, offs.astype(np.uint64), gs[k], 0.05, k + 1,
+                       read_versions=rvos[k], agg="mean")
+        assert ews[k].apply_backward(gs[k], 0.05, k + 1)
+    st_ids = _touched(orc)
+    w, a, v, p = table.peek(st_ids)
+    wo, ao, vo, po_ = orc.peek(st_ids)
+    assert w.tobytes() == wo.tobytes()
+    assert a.tobytes() == ao.tobytes()
+    assert (v == vo).all()
+    assert table.counters().clock_resets == orc.counters()["clock_resets"]
+
+
 def test_c3_full_size_two_steps(hps):
     """configs[2] at full size: 16384 x 26 multi-hot (avg 50) Zipf(1.1) -- 16.9M listings,
     3.8M rows, the hottest row listed ~16k times -- two sync steps through the large plan
