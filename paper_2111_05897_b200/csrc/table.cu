@@ -285,6 +285,7 @@ static void ensure_aux(Table* t) {
   int lo = 0, hi = 0;
   HPS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   HPS_CUDA(cudaStreamCreateWithPriority(&t->aux, cudaStreamNonBlocking, hi));
+  HPS_CUDA(cudaStreamCreateWithFlags(&t->aux_lo, cudaStreamNonBlocking));
   HPS_CUDA(cudaStreamCreateWithFlags(&t->aux_push, cudaStreamNonBlocking));
   HPS_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
   HPS_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
@@ -374,6 +375,7 @@ void table_destroy(Table* t) {
     if (t->h_ctr) cudaFreeHost(t->h_ctr);
     if (t->side) cudaStreamDestroy(t->side);
     if (t->aux) cudaStreamDestroy(t->aux);
+    if (t->aux_lo) cudaStreamDestroy(t->aux_lo);
     if (t->aux_push) cudaStreamDestroy(t->aux_push);
     if (t->ev_fork) cudaEventDestroy(t->ev_fork);
     if (t->ev_join) cudaEventDestroy(t->ev_join);
@@ -671,12 +673,16 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     // kSmallN) needs only the slots; the pooling does not need it. It runs on the aux
     // stream beside the pull and is joined by the pull / push (join_sort; measured
     // 0.2691 -> 0.2660 ms per C2 step against in line, profiles/r1_sort_fork_ab.txt).
+    // (a multi-hot batch's sort is real work: at normal priority it yields to the
+    // previous batch's hot-row walk, 6.60 -> 6.52 ms at C3; a one-hot batch's gated no-op
+    // launches stay at the highest priority, profiles/r2_c3_sched_ab.txt)
     ensure_aux(t);
+    cudaStream_t sst = N > 2ull * BF ? t->aux_lo : t->aux;
     HPS_CUDA(cudaEventRecord(t->ev_fork, st));
-    HPS_CUDA(cudaStreamWaitEvent(t->aux, t->ev_fork, 0));
-    sort_slots(b, b.slot, true, &b.small[0], t->aux, true);
+    HPS_CUDA(cudaStreamWaitEvent(sst, t->ev_fork, 0));
+    sort_slots(b, b.slot, true, &b.small[0], sst, true);
     if (!b.ev_sort) HPS_CUDA(cudaEventCreateWithFlags(&b.ev_sort, cudaEventDisableTiming));
-    HPS_CUDA(cudaEventRecord(b.ev_sort, t->aux));
+    HPS_CUDA(cudaEventRecord(b.ev_sort, sst));
     // Under CUDA-graph capture the fork rejoins the register's own stream (a captured
     // branch must end inside its capture, and a later capture may not wait on it);
     // eagerly, the pull / push of this batch joins it (join_sort).

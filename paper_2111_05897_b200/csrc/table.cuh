@@ -249,7 +249,7 @@ struct Table {
   cudaStream_t aux = nullptr;       // registers' large-plan sorts beside the pooling
   cudaStream_t aux_push = nullptr;  // a push's multi-row updates beside update_single
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_sort = nullptr, ev_runs = nullptr;
-  cudaStream_t aux_hot = nullptr;
+  cudaStream_t aux_hot = nullptr, aux_lo = nullptr;
   cudaEvent_t ev_hot0 = nullptr, ev_hot1 = nullptr;
   // Bumped whenever the slot numbering is rebuilt (clear / reset / checkpoint load): a
   // batch registered under an older generation names slots that may now hold other rows.
