@@ -346,7 +346,7 @@ void batch_free(Batch& b) {
   b.seen = b.multi = nullptr;
   void* ptrs[] = {b.offsets, b.lgrp,  b.slot,   b.keys_a,  b.vals_a,
                   b.keys_b,  b.vals_b, b.rv,  b.new_slots, b.kind,  b.hist,
-                  b.mkeys,   b.hot, b.mlist, b.meta, b.small_slot, b.small_listing,
+                  b.mkeys,   b.slist, b.hot, b.mlist, b.meta, b.small_slot, b.small_listing,
                   b.small,   b.skeys_a, b.skeys_b, b.sperm_a, b.sperm_b, b.sstart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -478,6 +478,8 @@ void batch_reserve(Batch& b, uint64_t N, uint64_t BF, uint64_t B) {
     c = 0;
     ensure(b.mkeys, c, n);
     c = 0;
+    ensure(b.slist, c, n);
+    c = 0;
     ensure(b.hot, c, n / kHotRun + 1);
     c = 0;
     ensure(b.mlist, c, n + 1);
@@ -538,6 +540,10 @@ static UpdateArgs plan_args(const Batch& b) {
   a.n_dev = b.all_multi ? nullptr : &b.small[0];
   a.kind = b.kind;
   a.slots = b.slot;
+  // (classify's single-listing list: multi-hot plan batches only)
+  const bool listed = !b.all_multi && b.N > 2ull * b.B * b.F;
+  a.slist = listed ? b.slist : nullptr;
+  a.n_single = listed ? &b.small[12] : nullptr;
   a.lgrp = b.lgrp;
   a.offsets = b.offsets;
   a.F = b.F;
@@ -661,7 +667,10 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     const int lbits = std::max(1, bits_for(N ? N - 1 : 0));
     {
       ProfScope p(t, "plan", st);
-      launch_classify(pv, b.slot, N, lbits, b.kind, b.mkeys, &b.small[0], t->sm_count, st,
+      // (multi-hot batches also list their single listings for update_single)
+      const bool list_singles = N > 2ull * BF;
+      launch_classify(pv, b.slot, N, lbits, b.kind, b.mkeys, &b.small[0],
+                      list_singles ? b.slist : nullptr, &b.small[12], t->sm_count, st,
                       b.n_live);
     }
     {

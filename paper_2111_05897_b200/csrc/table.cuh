@@ -154,6 +154,8 @@ struct Batch {
   uint32_t* new_slots = nullptr;  // [N] rows inserted by register (lazy-init queue)
   uint8_t* kind = nullptr;        // [N] plan: 1 = row listed once, 2 = multi (sorted path)
   unsigned long long* mkeys = nullptr;  // [N] multi listings as (slot << lbits | listing)
+  uint32_t* slist = nullptr;      // [N] multi-hot batches: listings of rows listed once
+                                  //   (classify; count small[12])
   uint32_t* hot = nullptr;        // [N / kHotRun + 1] sorted-list starts of hot rows
   uint32_t* mlist = nullptr;      // [N + 1] sorted-list starts of the other listed rows
   uint64_t* meta = nullptr;       // [N] large path: per sorted position, group | size << 32
@@ -319,7 +321,8 @@ void launch_probe(const DevTable& t, const uint64_t* ids, uint64_t n, uint32_t* 
                   const uint32_t* n_dev = nullptr);
 // plan.cu
 void launch_classify(const DevTable& t, const uint32_t* slots, uint64_t n, int lbits,
-                     uint8_t* kind, unsigned long long* mkeys, uint32_t* n_multi, int sms,
+                     uint8_t* kind, unsigned long long* mkeys, uint32_t* n_multi,
+                     uint32_t* slist, uint32_t* n_single, int sms,
                      cudaStream_t st, const uint32_t* n_live = nullptr);
 void launch_ht_clear(const DevTable& t, cudaStream_t st);
 void launch_lazy_init(const DevTable& t, const uint32_t* new_slots, const uint32_t* new_count,
@@ -366,6 +369,10 @@ struct UpdateArgs {
   uint64_t n;            // listings of the batch (entries of the direct apply)
   const uint32_t* n_dev; // multi listings of the plan (device), or null
   const uint8_t* kind;   // single kernel: plan kinds per listing
+  // single kernel, large plans of multi-hot batches: the listings of rows listed once
+  // (count *n_single) -- most of such a batch's listings belong to multi-listed rows
+  const uint32_t* slist;
+  const uint32_t* n_single;
   const uint32_t* slots; // single kernel: slot per listing
   // batch mode
   const uint32_t* lgrp;
