@@ -56,6 +56,8 @@ def parse():
                    help="sharded: stream priority of the captured step (-1 = above the prefetch)")
     p.add_argument("--e2e-slots", type=int, default=2,
                    help="e2e leg: batches in flight (pinned staging / device buffer sets)")
+    p.add_argument("--no-defer-plan-join", action="store_true",
+                   help="pipelined steps: join the next batch's plan at its register (A/B)")
     p.add_argument("--register-priority", type=int, default=0,
                    help="stream priority of the next batch's register (0: the step's own; "
                         "-1 = above it measured slower once the check streams, "
@@ -1010,6 +1012,16 @@ def main():
     pipe = not args.no_pipeline and M % 2 == 0
     ews = [hps.EmbeddingWorker(table, agg) for _ in range(2)] if pipe else []
     side = torch.cuda.Stream(priority=args.register_priority) if pipe else None
+    # the next batch's plan (its sort) is joined by its push, not by its register: the
+    # next pooling does not wait for it (hps_batch_defer_plan_join); a graph capture that
+    # ends before the push joins it itself (join_pending below)
+    defer = pipe and not args.no_defer_plan_join
+    for w_ in ews:
+        w_.defer_plan_join(defer)
+
+    def join_pending(i_last):
+        if defer:  # the batch the capture's last step registered
+            ews[(i_last + 1) % 2].join_plan(stream=torch.cuda.current_stream())
 
     def pipe_step(i, s):
         nxt = i + 1
@@ -1048,6 +1060,7 @@ def main():
             with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
                 if pipe:
                     pipe_step(it_g + m, torch.cuda.current_stream())
+                    join_pending(it_g + m)
                 else:
                     eager_step(m, torch.cuda.current_stream())
             graph_launches.append(hps.launch_count() - l0)
@@ -1059,6 +1072,7 @@ def main():
                 with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
                     pipe_step(it_g + m, torch.cuda.current_stream())
                     pipe_step(it_g + m + 1, torch.cuda.current_stream())
+                    join_pending(it_g + m + 1)
                 pair_launches.append(hps.launch_count() - l0)
                 pairs.append(g)
             if M > 2:  # and one graph of all M batches' steps
@@ -1067,6 +1081,7 @@ def main():
                 with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
                     for m in range(M):
                         pipe_step(it_g + m, torch.cuda.current_stream())
+                    join_pending(it_g + M - 1)
                 cycle.append((g, hps.launch_count() - l0))
         torch.cuda.synchronize()
 

@@ -214,6 +214,14 @@ hps_status hps_batch_destroy(hps_batch* b);
 hps_status hps_batch_register(hps_batch* b, const uint64_t* ids, size_t n_ids,
                               const uint32_t* offsets, uint32_t B, uint32_t F,
                               const uint64_t* sample_keys, hps_stream stream);
+/* Pipelines that register the next batch beside the current step: with on != 0 the
+ * batch's plan (its sort, running on an internal stream beside the register) is joined by
+ * the batch's push -- not by the register or the pull, which do not need it -- so the
+ * next pooling does not wait for it. Inside a CUDA-graph capture the caller then owns the
+ * join: the push in the same capture joins it, and a capture that ends before the push
+ * must call hps_batch_join_plan(b, s) on one of its streams first. */
+hps_status hps_batch_defer_plan_join(hps_batch* b, int on);
+hps_status hps_batch_join_plan(hps_batch* b, hps_stream stream);
 hps_status hps_batch_pull(hps_batch* b, float* out_pooled, uint64_t* out_read_versions,
                           hps_stream stream);
 hps_status hps_batch_push(hps_batch* b, const float* grads, float lr, uint32_t step_tag,

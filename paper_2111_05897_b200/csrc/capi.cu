@@ -245,6 +245,23 @@ hps_status hps_batch_register(hps_batch* b, const uint64_t* ids, size_t n_ids,
   });
 }
 
+hps_status hps_batch_defer_plan_join(hps_batch* b, int on) {
+  return guarded([&] {
+    REQUIRE(b, "hps_batch_defer_plan_join: null batch");
+    b->impl.defer_join = on != 0;
+  });
+}
+
+hps_status hps_batch_join_plan(hps_batch* b, hps_stream stream) {
+  return guarded([&] {
+    REQUIRE(b, "hps_batch_join_plan: null batch");
+    hps::Table* t = b->impl.table;
+    std::lock_guard<std::mutex> g(t->mu);
+    hps::DeviceGuard dg(t->device);
+    hps::batch_join_plan(b->impl, S(stream));
+  });
+}
+
 hps_status hps_batch_pull(hps_batch* b, float* out_pooled, uint64_t* out_read_versions,
                           hps_stream stream) {
   return guarded([&] {

@@ -303,9 +303,13 @@ static void join_sort(Batch& b, cudaStream_t st) {
   b.sort_pending = false;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   HPS_CUDA(cudaStreamIsCapturing(st, &cs));
-  if (cs == cudaStreamCaptureStatusActive) return;
+  // (a captured register rejoined its fork itself -- unless its batch defers the join)
+  if (cs == cudaStreamCaptureStatusActive && !b.sort_in_capture) return;
+  b.sort_in_capture = false;
   HPS_CUDA(cudaStreamWaitEvent(st, b.ev_sort, 0));
 }
+
+void batch_join_plan(Batch& b, cudaStream_t st) { join_sort(b, st); }
 
 DevTable batch_plan_view(Batch& b) {
   Table* t = b.table;
@@ -697,8 +701,10 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
     // eagerly, the pull / push of this batch joins it (join_sort).
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     HPS_CUDA(cudaStreamIsCapturing(st, &cs));
-    if (cs == cudaStreamCaptureStatusActive) HPS_CUDA(cudaStreamWaitEvent(st, b.ev_sort, 0));
-    b.sort_pending = cs != cudaStreamCaptureStatusActive;
+    const bool capturing = cs == cudaStreamCaptureStatusActive;
+    if (capturing && !b.defer_join) HPS_CUDA(cudaStreamWaitEvent(st, b.ev_sort, 0));
+    b.sort_pending = !capturing || b.defer_join;
+    b.sort_in_capture = capturing && b.defer_join;
   }
   b.registered = true;
   b.generation = t->generation;
@@ -754,7 +760,9 @@ void batch_pull(Batch& b, int agg, float* out_pooled, uint64_t* out_rv, cudaStre
   b.rv_valid = d_rv != nullptr;
   if (!b.pulled) t->outstanding.push_back(&b);
   b.pulled = true;
-  join_sort(b, st);  // the forward is self-contained (capturable on its own)
+  // the forward is self-contained (capturable on its own) -- unless the batch defers the
+  // plan's join to its push: the pooling does not need the sort
+  if (!b.defer_join) join_sort(b, st);
   stg.finish(st);
 }
 

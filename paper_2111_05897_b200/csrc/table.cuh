@@ -184,6 +184,11 @@ struct Batch {
   bool sort_pending = false;      // the plan's gated large sort runs on the table's aux
                                   // stream beside the pooling; joined before its use
   cudaEvent_t ev_sort = nullptr;  // recorded after that sort (joined by pull / push)
+  // hps_batch_defer_plan_join: the plan's sort is joined by the push (or an explicit
+  // hps_batch_join_plan), not by the register / pull -- also inside a graph capture, where
+  // the caller then owns the join (the push in the same capture, or join_plan)
+  bool defer_join = false;
+  bool sort_in_capture = false;
   // Per-batch plan bitmaps (1 bit per slot: listed / listed more than once), so the plan
   // of the next batch can be built while this batch's update runs.
   uint32_t* seen = nullptr;

@@ -88,6 +88,7 @@ void batch_register(Batch& b, const uint64_t* ids, uint64_t N, const uint32_t* o
                     uint32_t F, const uint64_t* sample_keys, cudaStream_t st,
                     bool dynamic = false, bool slots_ready = false);
 void batch_pull(Batch& b, int agg, float* out_pooled, uint64_t* out_rv, cudaStream_t st);
+void batch_join_plan(Batch& b, cudaStream_t st);
 // internal push flag (above the public HPS_* bits): contributions already validated
 constexpr uint32_t kPushPrechecked = 1u << 16;
 void batch_push(Batch& b, int agg, const float* grads, float lr, uint32_t step_tag,

@@ -161,6 +161,8 @@ def lib():
         "hps_batch_destroy": (st, [vp]),
         "hps_batch_register": (st, [vp, vp, sz, vp, u32, u32, vp, vp]),
         "hps_batch_pull": (st, [vp, vp, vp, vp]),
+        "hps_batch_defer_plan_join": (st, [vp, C.c_int]),
+        "hps_batch_join_plan": (st, [vp, vp]),
         "hps_batch_push": (st, [vp, vp, f32, u32, u32, C.c_int, vp, C.POINTER(C.c_int), u32, vp]),
         "hps_batch_pairs": (st, [vp, C.POINTER(u64)]),
         "hps_pull_batch": (st, [vp, vp, sz, vp, u32, u32, i32, vp, vp, vp]),
@@ -567,6 +569,16 @@ class EmbeddingWorker:
         self._keep = (ids, offsets, sk)
         check(lib().hps_batch_register(self.h, _ptr(ids), len(ids), _ptr(offsets), B, F, _ptr(sk),
                                        _stream_ptr(stream)), "register_batch")
+
+    def defer_plan_join(self, on: bool = True):
+        """Join this batch's plan (its sort) at the push instead of the register / pull
+        (hps_batch_defer_plan_join): for pipelines that register the next batch beside
+        the current step. Under graph capture, a capture that ends before the push must
+        call join_plan on one of its streams."""
+        check(lib().hps_batch_defer_plan_join(self.h, int(on)), "defer_plan_join")
+
+    def join_plan(self, stream=None):
+        check(lib().hps_batch_join_plan(self.h, _stream_ptr(stream)), "join_plan")
 
     def serve_pull(self, out_pooled=None, out_read_versions=None, stream=None, like=None):
         D = self.table.embedding_dim

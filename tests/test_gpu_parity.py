@@ -786,7 +786,7 @@ def test_stale_multi_bits_from_unapplied_batch(hps):
     np.testing.assert_array_equal(v, vo)
 
 
-def _pipelined_case(hps, B, F, D, space, steps, graph, seed=41):
+def _pipelined_case(hps, B, F, D, space, steps, graph, seed=41, defer=False):
     """bench.py's pipelined sync schedule: batch s+1 is registered on a second stream
     beside batch s's pull + push (two worker handles alternating, each with its own plan
     bitmaps), and pull(s+1) follows push(s) on the main stream. Pooled outputs and the
@@ -801,6 +801,8 @@ def _pipelined_case(hps, B, F, D, space, steps, graph, seed=41):
     orc = O.Restatement(salts, D, "adagrad")
     t = hps.ShardSet(4, D, 1 << 16, hps.ADAGRAD, salts=salts)
     ews = [hps.EmbeddingWorker(t, hps.MEAN) for _ in range(2)]
+    for w_ in ews:  # defer: the next batch's plan is joined by its push, not its register
+        w_.defer_plan_join(defer)
     dev = torch.device("cuda:0")
     main = torch.cuda.Stream()
     side = torch.cuda.Stream()
@@ -833,6 +835,8 @@ def _pipelined_case(hps, B, F, D, space, steps, graph, seed=41):
                 g_ = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g_, stream=main, capture_error_mode="thread_local"):
                     pipe_step(i, main)
+                    if defer and i + 1 < len(data):  # the capture ends before that push
+                        ews[(i + 1) % 2].join_plan(stream=main)
                 g_.replay()
                 main.synchronize()
             else:
@@ -866,6 +870,15 @@ def test_pipelined_register_beside_push_large_plan(hps, graph):
     """> 4096 listings of repeated rows: the forked large sort of the next batch runs
     while this batch's update chains run on the same aux stream."""
     _pipelined_case(hps, 1024, 4, 64, 1500, steps=4, graph=graph)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+@pytest.mark.parametrize("B,space", [(64, 300), (1024, 1500)])
+def test_pipelined_deferred_plan_join(hps, graph, B, space):
+    """hps_batch_defer_plan_join: the next batch's plan (sort) is joined by its push, not
+    by its register or pull (bench.py's pipeline); under capture the graph that registers
+    a batch joins its plan before it ends (hps_batch_join_plan). Bit-exact either way."""
+    _pipelined_case(hps, B, 4, 64 if B > 64 else 16, space, steps=4, graph=graph, defer=True)
 
 
 # ---------------------------------------------------------------- round 2 semantics
